@@ -1,0 +1,42 @@
+# Builds the product library (CUDA sm_100a + C-ABI), the input generators and
+# the CPU checkers (oracle/).  `make` is what __graft_entry__.build() runs.
+NVCC ?= /usr/local/cuda/bin/nvcc
+CXX ?= g++
+ARCH := -gencode arch=compute_100a,code=sm_100a
+PKG := paper_2207_13848_b200
+SRC := $(PKG)/csrc
+OUT := $(PKG)/_lib
+BUILD := build
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xptxas -warn-spills \
+           -Xcompiler -fPIC,-ffp-contract=off,-Wall -Iinclude -I$(SRC)
+
+CU_SRCS := $(SRC)/flop.cu $(SRC)/sample_predict.cu $(SRC)/symbolic.cu
+CPP_SRCS := $(SRC)/capi.cpp
+OBJS := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(BUILD)/%.o,$(CPP_SRCS))
+HDRS := $(SRC)/kernels.h $(SRC)/device_common.cuh include/spnnz_gpu/capi.h
+
+all: $(OUT)/libspnnz_gpu.so $(OUT)/libspnnz_gen.so oracle
+
+$(BUILD)/%.o: $(SRC)/%.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(BUILD)/%.o: $(SRC)/%.cpp $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(OUT)/libspnnz_gpu.so: $(OBJS) | $(OUT)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl
+
+$(OUT)/libspnnz_gen.so: $(SRC)/gen/generators.cpp | $(OUT)
+	$(CXX) -std=c++20 -O3 -fPIC -shared -pthread -Wall -o $@ $<
+
+oracle:
+	$(MAKE) --no-print-directory -C oracle
+
+$(BUILD) $(OUT):
+	mkdir -p $@
+
+clean:
+	rm -rf $(BUILD) $(OUT)/*.so
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

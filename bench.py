@@ -1,0 +1,397 @@
+#!/usr/bin/env python3
+"""Benchmark: SpGEMM output-structure predictor throughput (A-nnz/s) on B200.
+
+One step = one full predictor pass over the workload (spnnz::run_prediction,
+predict.hpp:220-226, + the integer per-row view): per-row FLOP, seeded row
+sample, sampled symbolic NNZ, CR / Z1* / Z2*, predicted per-row NNZ.
+Default workload: BASELINE.json config 5 (R-MAT 2^24, 402.6 M nonzeros,
+sample rate 0.1 % uncapped), the strong-scaling configuration.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5]
+  torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU)
+  python bench.py --impl reference ...   (reference CPU path on host cores)
+
+Prints ONE JSON line (rank 0).  `value` = nnz(A) / (max over ranks of the
+device time per step), inputs resident in HBM; `e2e` = the same metric through
+the host-buffer API (H2D of the CSR, D2H of the per-row prediction inside the
+timed region).  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "predictor A-nnz/s"
+UNIT = "A-nnz/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--cap", type=int, default=-1, help="sample cap (<0: none, the primary mode)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-accuracy", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=0,
+                    help="run only N untimed steps (for ncu launch lists)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_name(cfg, info, cap):
+    return f"{info['name']}: {info['desc']}; sample rate {info['fraction']}, " + \
+        ("uncapped" if cap < 0 else f"cap {cap}") + f", seed {info['seed']}"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------- CPU side
+def cpu_reference_pipeline(a, b, info, cap, threads=0):
+    """Times the reference's CPU path: oracle/_ref (the reference headers
+    compiled in place) when present, else the C restatement.  Returns
+    (callable step, kind, cores, cleanup)."""
+    from oracle.pyoracle import Oracle, Reference
+    cores = os.cpu_count() or 1
+    if Reference.available():
+        R = Reference(threads=threads)
+        ha = R.matrix(a)
+        hb = ha if b is a else R.matrix(b)
+
+        def step():
+            rep, _ = R.run_pipeline(ha, hb, info["seed"], info["fraction"], cap, a.rows)
+            return rep
+
+        def cleanup():
+            R.free_matrix(ha)
+            if hb != ha:
+                R.free_matrix(hb)
+        return step, "reference", cores, cleanup
+    O = Oracle(threads=threads)
+
+    def step():
+        rep, *_ = O.run_prediction(a, b, info["seed"], info["fraction"], cap)
+        return rep
+    return step, "port", cores, lambda: None
+
+
+def run_reference_arm(args, rank, world):
+    from paper_2207_13848_b200 import gen
+    if rank != 0:
+        return
+    info = gen.CONFIGS[args.config]
+    a, b = gen.make_config(args.config)
+    step, kind, cores, cleanup = cpu_reference_pipeline(a, b, info, args.cap)
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    cleanup()
+    t = float(np.mean(times))
+    value = a.nnz() / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "config": {"workload": workload_name(args.config, info, args.cap),
+                                         "parallelism": f"cpu threads={cores}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": "full workload per step: compute_flop + make_sample_plan + "
+                                   "run_prediction_with_plan + predict_row_structure_ceil"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- GPU side
+def flop_pass_bytes(m_local, nnz_local, k_rows):
+    """Algorithmic bytes of one FLOP pass: A.rpt + A.col +
+    B.rpt once + flop written."""
+    return 8 * (m_local + 1) + 4 * nnz_local + 8 * (k_rows + 1) + 8 * m_local
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic():
+    """dram bytes per FLOP-pass launch from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "flop_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d
+    except Exception:
+        return None, None
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_2207_13848_b200 import gen
+    from paper_2207_13848_b200.spnnz import Predictor, SamplePolicy
+    from paper_2207_13848_b200.capi import DEVICE, HOST
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    info = gen.CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    a, b = gen.make_config(args.config, threads=max(1, cores // max(world, 1)))
+    nccl_id = None
+    if world > 1:
+        obj = [Predictor.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    P = Predictor(local, rank, world, nccl_id)
+    P.load(a, None if b is a else b)
+    policy = SamplePolicy(info["fraction"], args.cap)
+    m_local = P.local_rows
+    nnz_local = int(a.rpt[P.row_hi] - a.rpt[P.row_lo])
+    stream = torch.cuda.ExternalStream(P.stream_handle())
+    dev_ceil = torch.empty(max(m_local, 1), dtype=torch.int64, device="cuda")
+
+    def step():
+        return P.run_prediction(info["seed"], policy, ceil_out=dev_ceil, residency=DEVICE,
+                                want_real=False, want_samples=False)
+
+    if args.profile_steps:
+        for _ in range(args.profile_steps):
+            step()
+        torch.cuda.synchronize()
+        return
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    args.warmup = max(args.warmup, 3)  # timing rule: at least 3 warm-up steps
+    for _ in range(args.warmup):
+        step()
+    # inputs (CSR of A and B) exceed L2 for the default config; smaller
+    # configs get an explicit flush between timed steps
+    l2_bytes = torch.cuda.get_device_properties(local).L2_cache_size
+    input_bytes = a.rpt.nbytes + a.col.nbytes + (0 if b is a else b.rpt.nbytes + b.col.nbytes)
+    flush = None if input_bytes > 2 * l2_bytes else torch.empty(256 << 20, dtype=torch.uint8,
+                                                                 device="cuda")
+    P.set_profiling(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    phase = {"flop": 0.0, "sample": 0.0, "symbolic": 0.0, "allreduce": 0.0, "predict": 0.0}
+    launches = 0
+    rep = None
+    barrier()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+                torch.cuda.synchronize()
+            ev[i][0].record(stream)
+            rep = step()
+            ev[i][1].record(stream)
+            t, n = P.last_timings()
+            for k in phase:
+                phase[k] += t[k]
+            launches += n
+        barrier()
+    P.set_profiling(False)
+    ms = float(sum(s.elapsed_time(e) for s, e in ev)) / args.steps
+    for k in phase:
+        phase[k] /= args.steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = a.nnz() / (ms_max * 1e-3)
+
+    # roofline of the dominant kernel (FLOP pass)
+    peak, peak_kind = load_peaks()
+    fbytes = flop_pass_bytes(m_local, nnz_local, (b.rows if b is not a else a.rows))
+    achieved = fbytes / (phase["flop"] * 1e-3) / 1e9 if phase["flop"] > 0 else 0.0
+    traffic, _ = load_traffic()
+
+    # end to end through the host-buffer API: H2D of the CSR + D2H of the
+    # per-row prediction, every step
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda x: torch.from_numpy(x).pin_memory().numpy()  # noqa: E731
+        ha = type(a)(a.rows, a.cols, pin(a.rpt), pin(a.col))
+        hb = ha if b is a else type(b)(b.rows, b.cols, pin(b.rpt), pin(b.col))
+        host_ceil = torch.empty(max(m_local, 1), dtype=torch.int64).pin_memory().numpy()
+        h2d = (ha.rpt.nbytes + ha.col.nbytes) if b is a else \
+            (8 * (m_local + 1) + 4 * nnz_local + hb.rpt.nbytes + hb.col.nbytes)
+        d2h = 8 * m_local + 8 * 8
+
+        def e2e_step():
+            P.load(ha, None if hb is ha else hb, residency=HOST)
+            return P.run_prediction(info["seed"], policy, ceil_out=host_ceil, residency=HOST,
+                                    want_real=False, want_samples=False)
+        e2e_step()
+        barrier()
+        ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for i in range(args.steps):
+            ee[i][0].record(stream)
+            e2e_step()
+            ee[i][1].record(stream)
+        barrier()
+        ems = float(sum(s.elapsed_time(e) for s, e in ee)) / args.steps
+        et = torch.tensor([ems], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": a.nnz() / (float(et.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": float(et.item()),
+               "path": "spnnz_gpu_load(host CSR, pinned) + spnnz_gpu_run_prediction(host ceil view)"}
+        P.load(a, None if b is a else b)
+
+    # accuracy (untimed): exact Z from the GPU exact pass
+    accuracy = None
+    if not args.no_accuracy:
+        from paper_2207_13848_b200 import spnnz
+        P.compute_flop(out=torch.empty(max(m_local, 1), dtype=torch.int64, device="cuda"))
+        t0 = time.perf_counter()
+        ex = P.exact_symbolic(per_row=False)
+        t_exact = time.perf_counter() - t0
+        er = spnnz.error_report(rep.z1_star, rep.z2_star, rep.stats.sampled_flop, ex.total_nnz,
+                                rep.total_flop, rep.plan.p)
+        accuracy = {"Z_exact": ex.total_nnz, "Z2_star": rep.z2_star, "Z1_star": rep.z1_star,
+                    "abs_rel_err_z2": abs(er.eps2), "abs_rel_err_z1": abs(er.eps1),
+                    "cr": rep.predicted_cr, "exact_pass_s": t_exact}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cstep, kind, cores, cleanup = cpu_reference_pipeline(a, b, info, args.cap)
+        t0 = time.perf_counter()
+        cstep()
+        tc = time.perf_counter() - t0
+        cleanup()
+        cpu = {"value": a.nnz() / tc, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": f"one full pass of the workload ({tc:.1f} s): compute_flop + "
+                         "make_sample_plan + run_prediction_with_plan + predict_row_structure_ceil"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (seeded generator, BASELINE.json config shapes)",
+            "config": {"workload": workload_name(args.config, info, args.cap),
+                       "nnz_A": a.nnz(), "rows": a.rows, "sample_num": rep.plan.sample_num,
+                       "parallelism": f"A row-sharded x{world} (nnz-balanced), B replicated, "
+                                      "1 NCCL all-reduce per step",
+                       "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps"},
+            "roofline": {"bound": "hbm", "kernel": "FLOP pass (merge-path k_flop + fixup)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes": fbytes, "avg_ms": phase["flop"],
+                         "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json)"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "phases_ms": phase,
+            "report": {"F": rep.total_flop, "f_star": rep.stats.sampled_flop,
+                       "z_star": rep.stats.sampled_nnz, "cr": rep.predicted_cr,
+                       "z1_star": rep.z1_star, "z2_star": rep.z2_star},
+            "accuracy": accuracy,
+        }
+        print(json.dumps(line), flush=True)
+    P.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,915 @@
+// C-ABI layer: device context, residency, validation, orchestration and the
+// single NCCL all-reduce.  See include/spnnz_gpu/capi.h for the contract and
+// the reference functions each entry point replaces.
+//
+// Built with -ffp-contract=off: the host-side estimator tail evaluates the
+// reference's double expressions (predict.hpp:86-123, :163-188) in the same
+// order, so device CR, host CR and the reference CR are the same IEEE value.
+#include "spnnz_gpu/capi.h"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+using namespace spnnz_gpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CU(call)                                                                         \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return set_err(e_ == cudaErrorMemoryAllocation ? SPNNZ_ENOMEM : SPNNZ_ECUDA, \
+                           "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,    \
+                           __LINE__);                                                    \
+    } while (0)
+
+#define RC(call)                   \
+    do {                           \
+        int r_ = (call);           \
+        if (r_ != SPNNZ_OK) return r_; \
+    } while (0)
+
+// ------------------------------------------------------------ NCCL (dlopen)
+struct Nccl {
+    bool loaded = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+Nccl& nccl() {
+    static Nccl n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            n.why = dlerror();
+            return;
+        }
+        n.GetUniqueId = reinterpret_cast<decltype(n.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+        n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+        n.AllReduce = reinterpret_cast<decltype(n.AllReduce)>(dlsym(h, "ncclAllReduce"));
+        n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(dlsym(h, "ncclGroupStart"));
+        n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+        n.GetErrorString =
+            reinterpret_cast<decltype(n.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        n.loaded = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.AllReduce &&
+                   n.GroupStart && n.GroupEnd && n.GetErrorString;
+        if (!n.loaded) n.why = "libnccl lacks required symbols";
+    });
+    return n;
+}
+
+#define NC(call)                                                                          \
+    do {                                                                                  \
+        ncclResult_t r_ = (call);                                                         \
+        if (r_ != ncclSuccess)                                                            \
+            return set_err(SPNNZ_ENCCL, "NCCL %s: %s", #call, nccl().GetErrorString(r_)); \
+    } while (0)
+
+// ---------------------------------------------------------- device buffer
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    int64_t n = 0;
+    int ensure(int64_t want) {
+        if (want <= n && p) return SPNNZ_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        const size_t bytes = sizeof(T) * static_cast<size_t>(std::max<int64_t>(want, 1));
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            return set_err(SPNNZ_ENOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+        }
+        n = want;
+        return SPNNZ_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+}  // namespace
+
+struct spnnz_gpu_ctx {
+    int device = 0, rank = 0, world = 1, num_sms = 148;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+
+    // matrices
+    bool loaded = false;
+    bool same_b = false;
+    int32_t a_rows = 0, a_cols = 0, b_rows = 0, b_cols = 0;
+    int32_t row_lo = 0, row_hi = 0;
+    DBuf<int64_t> b_rpt;
+    DBuf<int32_t> b_col;
+    DBuf<int64_t> a_rpt;  // shard rpt (only when A != B)
+    DBuf<int32_t> a_col;
+    DevCsr a;             // this rank's A shard view
+
+    // profile
+    DBuf<int64_t> flop;
+    bool profile_valid = false;
+    int64_t profile_total = 0, profile_max = 0;
+
+    // scratch
+    DBuf<int32_t> tile_x;
+    DBuf<long long> tile_carry, tile_total, tile_max;
+    DBuf<long long> totals;
+    long long* h_totals = nullptr;  // pinned mirror
+    int32_t* h_counts = nullptr;    // pinned mirror of bin counts
+    DBuf<int32_t> counts;
+    DBuf<int32_t> lists;
+    int64_t list_cap = 0;
+    DBuf<int64_t> heavy_unit_off, heavy_table_off;
+    DBuf<int32_t> heavy_mode;
+    DBuf<uint32_t> pool;
+    int64_t pool_slots = 0, pool_words = 0;
+    DBuf<long long> heavy_meta;
+    DBuf<int32_t> samples;
+    DBuf<int32_t> rows_in;
+    DBuf<int64_t> out64;
+    DBuf<double> outf;
+    DBuf<int32_t> bad;
+
+    // instrumentation
+    bool profiling = false;
+    cudaEvent_t ev[6] = {};
+    double last_ms[5] = {};
+    int64_t last_launches = 0;
+};
+
+namespace {
+
+int ensure_dev(spnnz_gpu_ctx* c) {
+    CU(cudaSetDevice(c->device));
+    return SPNNZ_OK;
+}
+
+int check_ctx(spnnz_gpu_ctx* c, bool need_loaded = true) {
+    if (!c) return set_err(SPNNZ_EINVAL, "null context");
+    RC(ensure_dev(c));
+    if (need_loaded && !c->loaded) return set_err(SPNNZ_ESTATE, "no matrices loaded");
+    return SPNNZ_OK;
+}
+
+int dims_ok(spnnz_gpu_ctx* c, const char* who) {
+    if (c->a_cols != c->b_rows)
+        return set_err(SPNNZ_EINVAL, "%s: A.cols %d != B.rows %d", who, c->a_cols, c->b_rows);
+    return SPNNZ_OK;
+}
+
+int local_rows(spnnz_gpu_ctx* c) { return c->row_hi - c->row_lo; }
+
+// Copy a caller buffer to the device (or pass device pointers through).
+template <typename T>
+int stage_in(spnnz_gpu_ctx* c, const T* src, int64_t n, int residency, DBuf<T>& buf,
+             const T** dev) {
+    if (residency == SPNNZ_DEVICE || n == 0) {
+        *dev = src;
+        return SPNNZ_OK;
+    }
+    RC(buf.ensure(n));
+    CU(cudaMemcpyAsync(buf.p, src, sizeof(T) * n, cudaMemcpyHostToDevice, c->stream));
+    *dev = buf.p;
+    return SPNNZ_OK;
+}
+
+int sym_scratch(spnnz_gpu_ctx* c, int64_t items, SymScratch* s) {
+    if (items > c->list_cap) {
+        RC(c->lists.ensure(items * kNumBins));
+        RC(c->heavy_unit_off.ensure(items + 1));
+        RC(c->heavy_table_off.ensure(items + 1));
+        RC(c->heavy_mode.ensure(items));
+        c->list_cap = items;
+    }
+    RC(c->counts.ensure(16));
+    RC(c->heavy_meta.ensure(4));
+    s->lists = c->lists.p;
+    s->capacity = c->list_cap;
+    s->counts = c->counts.p;
+    s->heavy_unit_off = c->heavy_unit_off.p;
+    s->heavy_table_off = c->heavy_table_off.p;
+    s->heavy_mode = c->heavy_mode.p;
+    s->heavy_meta = c->heavy_meta.p;
+    s->pool = c->pool.p;
+    s->pool_words = c->pool_words;
+    return SPNNZ_OK;
+}
+
+// Pool of zeroed bitmaps (one per heavy row in flight); kept clean by the
+// heavy kernel's cleaning pass, so it is zeroed only when (re)allocated.
+int ensure_pool(spnnz_gpu_ctx* c, int64_t want_slots, SymScratch* s) {
+    const int64_t words = heavy_table_words(0, c->b_cols);
+    if (c->pool_words != words) {
+        c->pool.release();
+        c->pool_slots = 0;
+        c->pool_words = words;
+    }
+    if (const char* cap = getenv("SPNNZ_HEAVY_POOL_SLOTS")) {  // test knob: force batching
+        const int64_t k = atoll(cap);
+        if (k > 0 && want_slots > k) want_slots = k;
+    }
+    if (want_slots > c->pool_slots) {
+        size_t free_b = 0, total_b = 0;
+        CU(cudaMemGetInfo(&free_b, &total_b));
+        const int64_t budget = std::min<int64_t>(int64_t(free_b) / 4, int64_t(8) << 30);
+        int64_t slots = std::min<int64_t>(want_slots, std::max<int64_t>(1, budget / (words * 4)));
+        if (slots > c->pool_slots) {
+            c->pool.release();
+            RC(c->pool.ensure(slots * words));
+            CU(cudaMemsetAsync(c->pool.p, 0, sizeof(uint32_t) * slots * words, c->stream));
+            c->pool_slots = slots;
+        }
+    }
+    s->pool = c->pool.p;
+    s->pool_words = c->pool_words;
+    return SPNNZ_OK;
+}
+
+// Symbolic pass over items (sampled rows or all local rows).  Adds the
+// total into totals[slot] (device); per-item results to out (device, nullable).
+int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64_t* d_out,
+                 int slot, bool sampled_flop, int64_t* launches) {
+    SymScratch s;
+    RC(sym_scratch(c, n_items, &s));
+    SymArgs g;
+    g.a = c->a;
+    g.brpt = c->b_rpt.p;
+    g.bcol = c->b_col.p;
+    g.bcols = c->b_cols;
+    g.row_lo = c->row_lo;
+    g.flop = c->flop.p;
+    g.rows = d_rows;
+    g.n_items = n_items;
+    g.out = d_out;
+    g.totals = c->totals.p;
+    g.total_slot = slot;
+    g.sampled_flop = sampled_flop;
+    CU(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * 16, c->stream));
+    if (n_items == 0) return SPNNZ_OK;
+    CU(launch_sym_bin(g, s, c->stream));
+    CU(launch_sym_tiers(g, s, c->num_sms, c->stream));
+    *launches += 5;
+    // Heavy rows: the host learns their number, then runs pool-sized batches.
+    CU(cudaMemcpyAsync(c->h_counts, c->counts.p, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost,
+                       c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    const int64_t heavy = c->h_counts[5];
+    if (heavy > 0) {
+        RC(ensure_pool(c, heavy, &s));
+        for (int64_t first = 0; first < heavy; first += c->pool_slots) {
+            const int64_t cnt = std::min<int64_t>(c->pool_slots, heavy - first);
+            CU(launch_sym_heavy(g, s, first, cnt, c->num_sms, c->stream));
+            *launches += 3;
+        }
+    }
+    return SPNNZ_OK;
+}
+
+int flop_pass(spnnz_gpu_ctx* c, int64_t* launches) {
+    const DevCsr& a = c->a;
+    const int64_t tiles = flop_tiles(a);
+    RC(c->flop.ensure(std::max<int64_t>(a.rows, 1)));
+    RC(c->tile_x.ensure(tiles + 1));
+    RC(c->tile_carry.ensure(tiles + 1));
+    RC(c->tile_total.ensure(tiles + 1));
+    RC(c->tile_max.ensure(tiles + 1));
+    FlopScratch s{c->tile_x.p, c->tile_carry.p, c->tile_total.p, c->tile_max.p};
+    CU(launch_flop_partition(a, s, c->stream));
+    CU(launch_flop(a, c->b_rpt.p, s, c->flop.p, c->totals.p, c->stream));
+    *launches += a.rows ? 3 : 0;
+    return SPNNZ_OK;
+}
+
+// Sum-all-reduce of totals[0..3] and max of totals[kMax] across ranks.
+int allreduce_totals(spnnz_gpu_ctx* c) {
+    if (c->world == 1 || !c->comm) return SPNNZ_OK;
+    Nccl& n = nccl();
+    NC(n.GroupStart());
+    NC(n.AllReduce(c->totals.p, c->totals.p, 4, ncclInt64, ncclSum, c->comm, c->stream));
+    NC(n.AllReduce(c->totals.p + kMax, c->totals.p + kMax, 1, ncclInt64, ncclMax, c->comm,
+                   c->stream));
+    NC(n.GroupEnd());
+    return SPNNZ_OK;
+}
+
+int read_totals(spnnz_gpu_ctx* c) {
+    CU(cudaMemcpyAsync(c->h_totals, c->totals.p, sizeof(long long) * kTotals,
+                       cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return SPNNZ_OK;
+}
+
+int sample_count(int32_t num_rows, double fraction, int64_t cap, int64_t* n, double* p) {
+    if (num_rows < 1) return set_err(SPNNZ_EINVAL, "make_sample_plan: M must be >= 1");
+    if (cap < 0) cap = INT64_MAX;
+    // predict.hpp:39-45
+    int64_t k = static_cast<int64_t>(std::ceil(fraction * num_rows));
+    k = std::min(k, cap);
+    k = std::max<int64_t>(k, 1);
+    *n = k;
+    *p = static_cast<double>(k) / static_cast<double>(num_rows);
+    return SPNNZ_OK;
+}
+
+void fill_report(spnnz_report* r, const long long* t, int64_t n, double p, uint64_t seed) {
+    r->total_flop = t[kF];
+    r->max_flop_row = t[kMax];
+    r->sample_num = n;
+    r->p = p;
+    r->seed = seed;
+    r->sampled_flop = t[kFStar];
+    r->sampled_nnz = t[kZStar];
+    r->sampled_cr = spnnz_sampled_cr(t[kFStar], t[kZStar]);
+    r->z1_star = static_cast<double>(t[kZStar]) / p;  // predict.hpp:98 (p > 0 by construction)
+    spnnz_predict_proposed(t[kFStar], t[kZStar], t[kF], &r->z2_star, &r->predicted_cr);
+}
+
+void ev_record(spnnz_gpu_ctx* c, int i) {
+    if (c->profiling) cudaEventRecord(c->ev[i], c->stream);
+}
+
+void ev_collect(spnnz_gpu_ctx* c) {
+    if (!c->profiling) return;
+    cudaEventSynchronize(c->ev[5]);
+    for (int i = 0; i < 5; ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]);
+        c->last_ms[i] = ms;
+    }
+}
+
+// Pipeline body shared by run_prediction and run_prediction_with_plan.
+int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint64_t seed,
+             int64_t* d_ceil, double* d_real) {
+    int64_t launches = 0;
+    CU(cudaMemsetAsync(c->totals.p, 0, sizeof(long long) * kTotals, c->stream));
+    ev_record(c, 0);
+    RC(flop_pass(c, &launches));
+    ev_record(c, 1);
+    if (draw) {
+        CU(launch_sample(seed, c->a_rows, n, c->samples.p, c->stream));
+        ++launches;
+    }
+    ev_record(c, 2);
+    RC(run_symbolic(c, d_rows, n, nullptr, kZStar, true, &launches));
+    ev_record(c, 3);
+    RC(allreduce_totals(c));
+    ev_record(c, 4);
+    if (d_ceil || d_real) {
+        CU(launch_predict(c->flop.p, local_rows(c), c->totals.p, 0.0, d_ceil, d_real, c->num_sms,
+                          c->stream));
+        ++launches;
+    }
+    ev_record(c, 5);
+    c->profile_valid = true;
+    c->last_launches = launches;
+    return SPNNZ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spnnz_gpu_abi_version(void) { return SPNNZ_GPU_ABI_VERSION; }
+
+const char* spnnz_gpu_last_error(void) { return g_err.c_str(); }
+
+int spnnz_gpu_nccl_unique_id(void* id128) {
+    Nccl& n = nccl();
+    if (!n.loaded) return set_err(SPNNZ_ENCCL, "NCCL unavailable: %s", n.why.c_str());
+    ncclUniqueId id;
+    NC(n.GetUniqueId(&id));
+    std::memcpy(id128, &id, sizeof id);
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz_gpu_ctx** out) {
+    if (!out) return set_err(SPNNZ_EINVAL, "null out");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world)
+        return set_err(SPNNZ_EINVAL, "bad rank %d / world %d", rank, world);
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return set_err(SPNNZ_ECUDA, "no CUDA device: %s", cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return set_err(SPNNZ_EINVAL, "bad device %d", device);
+    CU(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return set_err(SPNNZ_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device,
+                       prop.major, prop.minor);
+    auto* c = new spnnz_gpu_ctx;
+    c->device = device;
+    c->rank = rank;
+    c->world = world;
+    c->num_sms = prop.multiProcessorCount;
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_totals, sizeof(long long) * kTotals);
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_counts, sizeof(int32_t) * 16);
+    for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+    int rc = SPNNZ_OK;
+    if (e != cudaSuccess) rc = set_err(SPNNZ_ECUDA, "create: %s", cudaGetErrorString(e));
+    if (rc == SPNNZ_OK) rc = c->totals.ensure(kTotals);
+    if (rc == SPNNZ_OK && world > 1 && nccl_id) {
+        Nccl& n = nccl();
+        if (!n.loaded) {
+            rc = set_err(SPNNZ_ENCCL, "NCCL unavailable: %s", n.why.c_str());
+        } else if (!nccl_id) {
+            // detached shard: no communicator, totals stay rank-local and the
+            // caller combines them (used to check sharding on one GPU)
+        } else {
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof id);
+            ncclResult_t r = n.CommInitRank(&c->comm, world, id, rank);
+            if (r != ncclSuccess)
+                rc = set_err(SPNNZ_ENCCL, "ncclCommInitRank: %s", n.GetErrorString(r));
+        }
+    }
+    if (rc != SPNNZ_OK) {
+        spnnz_gpu_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
+    if (!c) return SPNNZ_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm) nccl().CommDestroy(c->comm);
+    for (auto* b : {&c->b_rpt, &c->a_rpt, &c->flop, &c->out64, &c->heavy_unit_off,
+                    &c->heavy_table_off})
+        b->release();
+    for (auto* b : {&c->b_col, &c->a_col, &c->tile_x, &c->counts, &c->lists, &c->heavy_mode,
+                    &c->samples, &c->rows_in, &c->bad})
+        b->release();
+    for (auto* b : {&c->tile_carry, &c->tile_total, &c->tile_max, &c->totals, &c->heavy_meta})
+        b->release();
+    c->pool.release();
+    c->outf.release();
+    if (c->h_totals) cudaFreeHost(c->h_totals);
+    if (c->h_counts) cudaFreeHost(c->h_counts);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_synchronize(spnnz_gpu_ctx* c) {
+    RC(check_ctx(c, false));
+    CU(cudaStreamSynchronize(c->stream));
+    return SPNNZ_OK;
+}
+
+void* spnnz_gpu_stream(spnnz_gpu_ctx* c) { return c ? c->stream : nullptr; }
+
+int spnnz_gpu_host_alloc(size_t bytes, void** out) {
+    cudaError_t e = cudaMallocHost(out, std::max<size_t>(bytes, 1));
+    if (e != cudaSuccess) return set_err(SPNNZ_ENOMEM, "cudaMallocHost: %s", cudaGetErrorString(e));
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_partition_rows(const int64_t* rpt, int32_t rows, int world, int32_t* bounds) {
+    if (!rpt || !bounds || world < 1 || rows < 0)
+        return set_err(SPNNZ_EINVAL, "partition_rows: bad arguments");
+    const int64_t nnz = rpt[rows] - rpt[0];
+    bounds[0] = 0;
+    for (int r = 1; r < world; ++r) {
+        const int64_t target = rpt[0] + nnz * r / world;
+        const int64_t* it = std::lower_bound(rpt, rpt + rows + 1, target);
+        int32_t b = static_cast<int32_t>(it - rpt);
+        b = std::max(b, bounds[r - 1]);
+        bounds[r] = std::min(b, rows);
+    }
+    bounds[world] = rows;
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_view* b,
+                   int residency) {
+    RC(check_ctx(c, false));
+    if (!a || a->rows < 0 || a->cols < 0) return set_err(SPNNZ_EINVAL, "load: bad A");
+    const bool same = (b == nullptr || b == a ||
+                       (b->rpt == a->rpt && b->col == a->col && b->rows == a->rows &&
+                        b->cols == a->cols));
+    const spnnz_csr_view* bv = same ? a : b;
+    if (bv->rows < 0 || bv->cols < 0) return set_err(SPNNZ_EINVAL, "load: bad B");
+    if (!a->rpt || !bv->rpt) return set_err(SPNNZ_EINVAL, "load: null rpt");
+    c->loaded = false;
+    c->profile_valid = false;
+    c->same_b = same;
+    c->a_rows = a->rows;
+    c->a_cols = a->cols;
+    c->b_rows = bv->rows;
+    c->b_cols = bv->cols;
+
+    // Shard bounds need A.rpt on the host.
+    std::vector<int64_t> host_arpt;
+    const int64_t* arpt_h = a->rpt;
+    if (residency == SPNNZ_DEVICE) {
+        host_arpt.resize(static_cast<size_t>(a->rows) + 1);
+        CU(cudaMemcpy(host_arpt.data(), a->rpt, 8 * host_arpt.size(), cudaMemcpyDeviceToHost));
+        arpt_h = host_arpt.data();
+    }
+    std::vector<int32_t> bounds(static_cast<size_t>(c->world) + 1);
+    RC(spnnz_gpu_partition_rows(arpt_h, a->rows, c->world, bounds.data()));
+    c->row_lo = bounds[c->rank];
+    c->row_hi = bounds[c->rank + 1];
+    const auto kind = residency == SPNNZ_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+
+    // B replicated (it is also A's storage when C = A*A).
+    int64_t b_nnz = 0;
+    if (residency == SPNNZ_DEVICE) {
+        CU(cudaMemcpy(&b_nnz, bv->rpt + bv->rows, 8, cudaMemcpyDeviceToHost));
+    } else {
+        b_nnz = bv->rpt[bv->rows];
+    }
+    RC(c->b_rpt.ensure(int64_t(bv->rows) + 1));
+    RC(c->b_col.ensure(std::max<int64_t>(b_nnz, 1)));
+    CU(cudaMemcpyAsync(c->b_rpt.p, bv->rpt, 8 * (size_t(bv->rows) + 1), kind, c->stream));
+    if (b_nnz) CU(cudaMemcpyAsync(c->b_col.p, bv->col, 4 * size_t(b_nnz), kind, c->stream));
+
+    DevCsr v;
+    v.rows = c->row_hi - c->row_lo;
+    v.cols = a->cols;
+    const int64_t a_lo = arpt_h[c->row_lo], a_hi = arpt_h[c->row_hi];
+    v.nnz = a_hi - a_lo;
+    if (same) {
+        v.rpt = c->b_rpt.p + c->row_lo;
+        v.col = c->b_col.p;
+    } else {
+        RC(c->a_rpt.ensure(int64_t(v.rows) + 1));
+        RC(c->a_col.ensure(std::max<int64_t>(v.nnz, 1)));
+        CU(cudaMemcpyAsync(c->a_rpt.p, a->rpt + c->row_lo, 8 * (size_t(v.rows) + 1), kind,
+                           c->stream));
+        if (v.nnz)
+            CU(cudaMemcpyAsync(c->a_col.p, a->col + a_lo, 4 * size_t(v.nnz), kind, c->stream));
+        v.rpt = c->a_rpt.p;
+        v.col = c->a_col.p - a_lo;  // indexed with absolute offsets
+    }
+    c->a = v;
+    c->loaded = true;
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_shard(spnnz_gpu_ctx* c, int32_t* lo, int32_t* hi, int32_t* rows) {
+    RC(check_ctx(c));
+    if (lo) *lo = c->row_lo;
+    if (hi) *hi = c->row_hi;
+    if (rows) *rows = c->a_rows;
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_compute_flop(spnnz_gpu_ctx* c, int64_t* flop_out, int residency, int64_t* total,
+                           int64_t* max) {
+    RC(check_ctx(c));
+    RC(dims_ok(c, "compute_flop"));
+    int64_t launches = 0;
+    CU(cudaMemsetAsync(c->totals.p, 0, sizeof(long long) * kTotals, c->stream));
+    RC(flop_pass(c, &launches));
+    RC(allreduce_totals(c));
+    const int m = local_rows(c);
+    if (flop_out && m) {
+        CU(cudaMemcpyAsync(flop_out, c->flop.p, 8 * size_t(m),
+                           residency == SPNNZ_DEVICE ? cudaMemcpyDeviceToDevice
+                                                     : cudaMemcpyDeviceToHost,
+                           c->stream));
+    }
+    RC(read_totals(c));
+    c->profile_valid = true;
+    c->profile_total = c->h_totals[kF];
+    c->profile_max = c->h_totals[kMax];
+    if (total) *total = c->profile_total;
+    if (max) *max = c->profile_max;
+    c->last_launches = launches;
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_set_profile(spnnz_gpu_ctx* c, const int64_t* flop_in, int64_t rows, int residency,
+                          int64_t total, int64_t max) {
+    RC(check_ctx(c, false));
+    if (!c->loaded) {
+        // profile-only mode (sampled_flop / predict_row_structure need no matrices)
+        if (rows < 0 || rows > INT32_MAX) return set_err(SPNNZ_EINVAL, "bad profile length");
+        c->a_rows = static_cast<int32_t>(rows);
+        c->row_lo = 0;
+        c->row_hi = static_cast<int32_t>(rows);
+    }
+    if (rows != local_rows(c))
+        return set_err(SPNNZ_EINVAL, "symbolic: profile does not match A");
+    RC(c->flop.ensure(std::max<int64_t>(rows, 1)));
+    if (rows)
+        CU(cudaMemcpyAsync(c->flop.p, flop_in, 8 * size_t(rows),
+                           residency == SPNNZ_DEVICE ? cudaMemcpyDeviceToDevice
+                                                     : cudaMemcpyHostToDevice,
+                           c->stream));
+    c->profile_valid = true;
+    c->profile_total = total;
+    c->profile_max = max;
+    return SPNNZ_OK;
+}
+
+namespace {
+int check_rows(spnnz_gpu_ctx* c, const int32_t* rows, int64_t n, int residency, const char* who,
+               const int32_t** d_rows) {
+    if (n < 0) return set_err(SPNNZ_EINVAL, "%s: negative count", who);
+    if (n > 0 && !rows) return set_err(SPNNZ_EINVAL, "%s: null rows", who);
+    if (residency == SPNNZ_HOST) {
+        for (int64_t i = 0; i < n; ++i)
+            if (rows[i] < 0 || rows[i] >= c->a_rows)
+                return set_err(SPNNZ_EINVAL, "%s: row %d out of range", who, rows[i]);
+    } else if (n > 0) {
+        RC(c->bad.ensure(1));
+        CU(cudaMemsetAsync(c->bad.p, 0, 4, c->stream));
+        CU(launch_check_rows(rows, n, c->a_rows, c->bad.p, c->stream));
+        int32_t bad = 0;
+        CU(cudaMemcpyAsync(&bad, c->bad.p, 4, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        if (bad) return set_err(SPNNZ_EINVAL, "%s: %d rows out of range", who, bad);
+    }
+    return stage_in(c, rows, n, residency, c->rows_in, d_rows);
+}
+}  // namespace
+
+int spnnz_gpu_sampled_flop(spnnz_gpu_ctx* c, const int32_t* rows, int64_t n, int residency,
+                           int64_t* out) {
+    RC(check_ctx(c, false));
+    if (!c->profile_valid) return set_err(SPNNZ_ESTATE, "sampled_flop: no resident profile");
+    const int32_t* d_rows = nullptr;
+    RC(check_rows(c, rows, n, residency, "sampled_flop", &d_rows));
+    CU(cudaMemsetAsync(c->totals.p, 0, sizeof(long long) * kTotals, c->stream));
+    CU(launch_sampled_flop(c->flop.p, c->row_lo, local_rows(c), d_rows, n, c->totals.p, c->stream));
+    RC(allreduce_totals(c));
+    RC(read_totals(c));
+    *out = c->h_totals[kFStar];
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_make_sample_plan(spnnz_gpu_ctx* c, int32_t num_rows, uint64_t seed, double fraction,
+                               int64_t cap, int32_t* rows, int residency, int64_t* n, double* p) {
+    RC(sample_count(num_rows, fraction, cap, n, p));
+    if (!rows) return SPNNZ_OK;
+    RC(check_ctx(c, false));
+    int32_t* dst = rows;
+    if (residency == SPNNZ_HOST) {
+        RC(c->samples.ensure(*n));
+        dst = c->samples.p;
+    }
+    CU(launch_sample(seed, num_rows, *n, dst, c->stream));
+    if (residency == SPNNZ_HOST)
+        CU(cudaMemcpyAsync(rows, dst, 4 * size_t(*n), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_sampled_symbolic(spnnz_gpu_ctx* c, const int32_t* rows, int64_t n, int residency,
+                               int64_t* per_sample, int64_t* total) {
+    RC(check_ctx(c));
+    if (c->a_cols != c->b_rows) return set_err(SPNNZ_EINVAL, "symbolic: A.cols != B.rows");
+    if (!c->profile_valid) return set_err(SPNNZ_ESTATE, "sampled_symbolic: no resident profile");
+    const int32_t* d_rows = nullptr;
+    RC(check_rows(c, rows, n, residency, "sampled_symbolic", &d_rows));
+    int64_t* d_out = nullptr;
+    if (per_sample) {
+        if (residency == SPNNZ_DEVICE) {
+            d_out = per_sample;
+        } else {
+            RC(c->out64.ensure(n));
+            d_out = c->out64.p;
+        }
+    }
+    int64_t launches = 0;
+    CU(cudaMemsetAsync(c->totals.p, 0, sizeof(long long) * kTotals, c->stream));
+    RC(run_symbolic(c, d_rows, n, d_out, kZStar, false, &launches));
+    RC(allreduce_totals(c));
+    if (per_sample && residency == SPNNZ_HOST && n)
+        CU(cudaMemcpyAsync(per_sample, d_out, 8 * size_t(n), cudaMemcpyDeviceToHost, c->stream));
+    RC(read_totals(c));
+    *total = c->h_totals[kZStar];
+    c->last_launches = launches;
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_exact_symbolic(spnnz_gpu_ctx* c, int64_t* per_row, int residency, int64_t* total) {
+    RC(check_ctx(c));
+    if (c->a_cols != c->b_rows) return set_err(SPNNZ_EINVAL, "symbolic: A.cols != B.rows");
+    if (!c->profile_valid) return set_err(SPNNZ_ESTATE, "exact_symbolic: no resident profile");
+    const int m = local_rows(c);
+    int64_t* d_out = nullptr;
+    if (per_row) {
+        if (residency == SPNNZ_DEVICE) {
+            d_out = per_row;
+        } else {
+            RC(c->out64.ensure(m));
+            d_out = c->out64.p;
+        }
+    }
+    int64_t launches = 0;
+    CU(cudaMemsetAsync(c->totals.p, 0, sizeof(long long) * kTotals, c->stream));
+    RC(run_symbolic(c, nullptr, m, d_out, kZ, false, &launches));
+    RC(allreduce_totals(c));
+    if (per_row && residency == SPNNZ_HOST && m)
+        CU(cudaMemcpyAsync(per_row, d_out, 8 * size_t(m), cudaMemcpyDeviceToHost, c->stream));
+    RC(read_totals(c));
+    *total = c->h_totals[kZ];
+    c->last_launches = launches;
+    return SPNNZ_OK;
+}
+
+namespace {
+int predict_view(spnnz_gpu_ctx* c, double cr, int64_t* out_ceil, double* out_real, int residency,
+                 const char* who) {
+    RC(check_ctx(c, false));
+    if (!(cr > 0.0)) return set_err(SPNNZ_EINVAL, "%s: predicted_cr must be positive", who);
+    if (!c->profile_valid) return set_err(SPNNZ_ESTATE, "%s: no resident profile", who);
+    const int m = local_rows(c);
+    if ((!out_ceil && !out_real) || m == 0) return SPNNZ_OK;
+    int64_t* d_ceil = out_ceil;
+    double* d_real = out_real;
+    if (residency == SPNNZ_HOST) {
+        if (out_ceil) {
+            RC(c->out64.ensure(m));
+            d_ceil = c->out64.p;
+        } else {
+            RC(c->outf.ensure(m));
+            d_real = c->outf.p;
+        }
+    }
+    CU(launch_predict(c->flop.p, m, nullptr, cr, d_ceil, d_real, c->num_sms, c->stream));
+    if (residency == SPNNZ_HOST)
+        CU(cudaMemcpyAsync(out_ceil ? static_cast<void*>(out_ceil) : static_cast<void*>(out_real),
+                           out_ceil ? static_cast<void*>(d_ceil) : static_cast<void*>(d_real),
+                           8 * size_t(m), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return SPNNZ_OK;
+}
+}  // namespace
+
+int spnnz_gpu_predict_row_structure(spnnz_gpu_ctx* c, double cr, double* out, int residency) {
+    return predict_view(c, cr, nullptr, out, residency, "predict_row_structure");
+}
+
+int spnnz_gpu_predict_row_structure_ceil(spnnz_gpu_ctx* c, double cr, int64_t* out,
+                                         int residency) {
+    return predict_view(c, cr, out, nullptr, residency, "predict_row_structure_ceil");
+}
+
+namespace {
+int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, bool draw,
+               uint64_t seed, spnnz_report* rep, int64_t* row_ceil, double* row_real,
+               int residency) {
+    const int m = local_rows(c);
+    int64_t* d_ceil = row_ceil;
+    double* d_real = row_real;
+    if (residency == SPNNZ_HOST) {
+        if (row_ceil) {
+            RC(c->out64.ensure(m));
+            d_ceil = c->out64.p;
+        }
+        if (row_real) {
+            RC(c->outf.ensure(m));
+            d_real = c->outf.p;
+        }
+    }
+    RC(pipeline(c, d_rows, n, draw, seed, m ? d_ceil : nullptr, m ? d_real : nullptr));
+    if (residency == SPNNZ_HOST && m) {
+        if (row_ceil)
+            CU(cudaMemcpyAsync(row_ceil, d_ceil, 8 * size_t(m), cudaMemcpyDeviceToHost, c->stream));
+        if (row_real)
+            CU(cudaMemcpyAsync(row_real, d_real, 8 * size_t(m), cudaMemcpyDeviceToHost, c->stream));
+    }
+    RC(read_totals(c));
+    ev_collect(c);
+    c->profile_total = c->h_totals[kF];
+    c->profile_max = c->h_totals[kMax];
+    if (rep) fill_report(rep, c->h_totals, n, p, seed);
+    return SPNNZ_OK;
+}
+}  // namespace
+
+int spnnz_gpu_run_prediction(spnnz_gpu_ctx* c, uint64_t seed, double fraction, int64_t cap,
+                             spnnz_report* rep, int64_t* row_ceil, double* row_real,
+                             int32_t* sample_rows, int residency) {
+    RC(check_ctx(c));
+    RC(dims_ok(c, "compute_flop"));
+    int64_t n = 0;
+    double p = 0;
+    RC(sample_count(c->a_rows, fraction, cap, &n, &p));
+    RC(c->samples.ensure(n));
+    RC(run_common(c, c->samples.p, n, p, true, seed, rep, row_ceil, row_real, residency));
+    if (sample_rows)
+        CU(cudaMemcpy(sample_rows, c->samples.p, 4 * size_t(n),
+                      residency == SPNNZ_DEVICE ? cudaMemcpyDeviceToDevice
+                                                : cudaMemcpyDeviceToHost));
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_run_prediction_with_plan(spnnz_gpu_ctx* c, const int32_t* rows, int64_t n, double p,
+                                       int rows_residency, spnnz_report* rep, int64_t* row_ceil,
+                                       double* row_real, int out_residency) {
+    RC(check_ctx(c));
+    RC(dims_ok(c, "compute_flop"));
+    const int32_t* d_rows = nullptr;
+    RC(check_rows(c, rows, n, rows_residency, "sampled_symbolic", &d_rows));
+    if (!(p > 0.0)) return set_err(SPNNZ_EINVAL, "predict_reference: p must be positive");
+    return run_common(c, d_rows, n, p, false, 0, rep, row_ceil, row_real, out_residency);
+}
+
+// ------------------------------------------------------------ estimators
+double spnnz_sampled_cr(int64_t f, int64_t z) {
+    return (f > 0 && z > 0) ? static_cast<double>(f) / static_cast<double>(z) : 1.0;
+}
+
+int spnnz_predict_reference(int64_t z, double p, double* z1) {
+    if (!(p > 0.0)) return set_err(SPNNZ_EINVAL, "predict_reference: p must be positive");
+    *z1 = static_cast<double>(z) / p;
+    return SPNNZ_OK;
+}
+
+int spnnz_predict_proposed(int64_t f, int64_t z, int64_t total_flop, double* z2, double* cr) {
+    if (f <= 0 || z <= 0) {
+        *cr = 1.0;
+        *z2 = static_cast<double>(total_flop);
+        return SPNNZ_OK;
+    }
+    *cr = static_cast<double>(f) / static_cast<double>(z);
+    *z2 = static_cast<double>(total_flop) * static_cast<double>(z) / static_cast<double>(f);
+    return SPNNZ_OK;
+}
+
+int spnnz_error_report(double z1, double z2, int64_t f_star, int64_t exact_nnz, int64_t total_flop,
+                       double p, double* out4) {
+    if (exact_nnz <= 0 || total_flop <= 0)
+        return set_err(SPNNZ_EINVAL, "error_report: relative error undefined for Z = 0 or F = 0");
+    if (!(p > 0.0)) return set_err(SPNNZ_EINVAL, "error_report: p must be positive");
+    const double z = static_cast<double>(exact_nnz), f = static_cast<double>(total_flop);
+    const double fs = static_cast<double>(f_star) / p;
+    out4[0] = (z1 - z) / z;
+    out4[1] = (fs - f) / f;
+    out4[2] = (z2 - z) / z;
+    out4[3] = f_star > 0 ? std::fabs(out4[2] - (out4[0] - out4[1]) / (1.0 + out4[1])) : 0.0;
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_set_profiling(spnnz_gpu_ctx* c, int enabled) {
+    if (!c) return set_err(SPNNZ_EINVAL, "null context");
+    c->profiling = enabled != 0;
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_last_timings(spnnz_gpu_ctx* c, double* ms5, int64_t* launches) {
+    if (!c) return set_err(SPNNZ_EINVAL, "null context");
+    if (ms5)
+        for (int i = 0; i < 5; ++i) ms5[i] = c->last_ms[i];
+    if (launches) *launches = c->last_launches;
+    return SPNNZ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+// Device-side helpers shared by the predictor kernels (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace spnnz_gpu {
+
+constexpr int kWarp = 32;
+
+// SplitMix64 output number r (0-based) of a generator seeded with `seed`:
+// the reference advances state += gamma before mixing (rng.hpp:14-19), so
+// draw r mixes seed + (r + 1) * gamma.  Counter-based => one thread per draw.
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t r) {
+    uint64_t z = seed + (r + 1) * 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// 32-bit mixer for hash-table slots (any injective-enough mix works: the
+// distinct count does not depend on the hash, symbolic.hpp:13-16 and
+// proj/tests/test_symbolic.cpp:94-109).
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352dU;
+    x ^= x >> 15;
+    x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+}
+
+template <typename T>
+__device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
+
+// Streaming 16-byte load that does not allocate in L1 (read-once data).
+__device__ __forceinline__ longlong2 ld_stream_ll2(const longlong2* p) {
+    longlong2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.s64 {%0, %1}, [%2];"
+                 : "=l"(r.x), "=l"(r.y) : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st_stream_ll2(longlong2* p, longlong2 v) {
+    asm volatile("st.global.cs.v2.s64 [%0], {%1, %2};" :: "l"(p), "l"(v.x), "l"(v.y) : "memory");
+}
+
+__device__ __forceinline__ void st_stream_d2(double2* p, double2 v) {
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ long long warp_max_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+
+// Block-wide int64 sum/max of per-thread values (all threads get the result).
+template <int BLOCK>
+__device__ __forceinline__ long long block_sum_ll(long long v, long long* scratch /* BLOCK/32 */) {
+    v = warp_sum_ll(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) scratch[w] = v;
+    __syncthreads();
+    long long t = 0;
+#pragma unroll
+    for (int i = 0; i < BLOCK / 32; ++i) t += scratch[i];
+    return t;
+}
+
+template <int BLOCK>
+__device__ __forceinline__ long long block_max_ll(long long v, long long* scratch) {
+    v = warp_max_ll(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) scratch[w] = v;
+    __syncthreads();
+    long long t = 0;
+#pragma unroll
+    for (int i = 0; i < BLOCK / 32; ++i) t = scratch[i] > t ? scratch[i] : t;
+    return t;
+}
+
+// Predicted CR from the combined totals, exactly collect_sample_stats /
+// predict_proposed (predict.hpp:86-89, :111-117): f*/z* in IEEE double, or 1.
+__device__ __forceinline__ double predicted_cr(long long f_star, long long z_star) {
+    return (f_star > 0 && z_star > 0) ? __ddiv_rn((double)f_star, (double)z_star) : 1.0;
+}
+
+}  // namespace spnnz_gpu

@@ -1,0 +1,127 @@
+// Host-side declarations of the predictor's kernel launchers (sm_100a).
+// Every launcher enqueues on `stream` and returns cudaGetLastError().
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace spnnz_gpu {
+
+// Device view of a CSR row range.  `rpt` points at the first row's offset
+// (rows + 1 entries, ABSOLUTE offsets into `col`); `col` is indexed with those
+// absolute offsets.  For a shard of A that shares B's arrays (C = A*A), rpt is
+// a view into B's rpt and col is B's col.
+struct DevCsr {
+    int32_t rows = 0;
+    int32_t cols = 0;
+    const int64_t* rpt = nullptr;
+    const int32_t* col = nullptr;
+    int64_t nnz = 0;   // rpt[rows] - rpt[0]
+};
+
+// Slots of the per-call device totals array (long long[kTotals]).
+enum TotalSlot : int {
+    kF = 0,       // total FLOP of the (local) rows
+    kFStar = 1,   // sampled FLOP f*
+    kZStar = 2,   // sampled NNZ z*
+    kZ = 3,       // exact NNZ Z (scoring)
+    kMax = 4,     // max FLOP of a row
+    kTotals = 8
+};
+
+// ---------------------------------------------------------------- FLOP
+// Merge-path tiles over the (row-end, nonzero) sequence of A (Merrill &
+// Garland's merge-based decomposition): every tile holds exactly
+// kFlopTile items, so hub rows and empty rows cost the same per item.
+constexpr int kFlopBlock = 256;
+constexpr int kFlopIpt = 8;
+constexpr int kFlopTile = kFlopBlock * kFlopIpt;
+
+inline int64_t flop_tiles(const DevCsr& a) {
+    const int64_t items = int64_t(a.rows) + a.nnz;
+    return (items + kFlopTile - 1) / kFlopTile;
+}
+
+struct FlopScratch {
+    int32_t* tile_x = nullptr;       // tiles + 1 merge-path row coordinates
+    long long* tile_carry = nullptr; // tiles: partial sum of the row open at tile end
+    long long* tile_total = nullptr; // tiles
+    long long* tile_max = nullptr;   // tiles
+};
+
+cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStream_t stream);
+cudaError_t launch_flop(const DevCsr& a, const int64_t* brpt, const FlopScratch& s, int64_t* flop,
+                        long long* totals, cudaStream_t stream);
+
+// -------------------------------------------------------------- sampler
+cudaError_t launch_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* rows,
+                          cudaStream_t stream);
+
+// ------------------------------------------------------------- symbolic
+// Items are either an explicit list of GLOBAL row ids (sampled mode) or all
+// local rows (exact mode, rows == nullptr).  Items whose row is outside the
+// shard [row_lo, row_lo + a.rows) get 0.  Rows are binned by FLOP:
+constexpr int kNumBins = 6;
+constexpr int64_t kBin1Max = 32;     // warp, __match_any_sync dedup
+constexpr int64_t kBin2Max = 512;    // warp, 1024-slot smem hash per warp
+constexpr int64_t kBin3Max = 4096;   // 256-thread block, 8192-slot smem hash
+constexpr int64_t kBin4Max = 16384;  // 1024-thread block, 32768-slot smem hash
+// bin 5: heavy rows, global-memory bitmap/hash tables, many blocks per row.
+
+struct SymScratch {
+    int32_t* lists = nullptr;        // kNumBins * capacity item ids
+    int64_t capacity = 0;
+    int32_t* counts = nullptr;       // kNumBins (+ spare) counters
+    // heavy-row work decomposition
+    int64_t* heavy_unit_off = nullptr;   // capacity + 1
+    int64_t* heavy_table_off = nullptr;  // capacity + 1 (words)
+    int32_t* heavy_mode = nullptr;       // capacity: 0 hash, 1 bitmap
+    uint32_t* pool = nullptr;            // global tables, kept clean between calls
+    int64_t pool_words = 0;
+    long long* heavy_meta = nullptr;     // [0] units, [1] words used, [2] work counter
+};
+
+struct SymArgs {
+    DevCsr a;
+    const int64_t* brpt = nullptr;
+    const int32_t* bcol = nullptr;
+    int32_t bcols = 0;          // N (columns of B)
+    int32_t row_lo = 0;         // global id of local row 0
+    const int64_t* flop = nullptr;  // local profile
+    const int32_t* rows = nullptr;  // global row ids, or nullptr = all local rows
+    int64_t n_items = 0;
+    int64_t* out = nullptr;         // per item NNZ (nullable)
+    long long* totals = nullptr;
+    int total_slot = kZStar;        // kZStar (sampled) or kZ (exact)
+    bool sampled_flop = false;      // also accumulate f* into totals[kFStar]
+};
+
+// Classifies items into bins (writes out[] = 0 for empty / foreign rows).
+cudaError_t launch_sym_bin(const SymArgs& args, const SymScratch& s, cudaStream_t stream);
+// Runs the smem tiers (bins 1-4) over the binned lists; grids are persistent
+// and read the counts on the device.
+cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_sms,
+                             cudaStream_t stream);
+// Heavy tier for bin entries [first, first + count) of list 5 (host knows
+// count after a sync).  Tables come from s.pool and are cleaned afterwards.
+cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, int64_t first,
+                             int64_t count, int num_sms, cudaStream_t stream);
+// Per heavy row table words needed (host-side sizing helper for the pool).
+int64_t heavy_table_words(int64_t flop_row, int32_t bcols);
+
+// -------------------------------------------------------------- predict
+// ceil view min(flop, ceil(flop / cr)) and/or real view flop / cr.  If
+// totals != nullptr the CR is derived on the device from totals[kFStar],
+// totals[kZStar] (predict.hpp:111-117); else cr is used as given.
+cudaError_t launch_predict(const int64_t* flop, int64_t m, const long long* totals, double cr,
+                           int64_t* ceil_out, double* real_out, int num_sms, cudaStream_t stream);
+
+// sampled_flop over global rows (flop.hpp:64-74); atomics into totals[kFStar].
+cudaError_t launch_sampled_flop(const int64_t* flop, int32_t row_lo, int32_t local_rows,
+                                const int32_t* rows, int64_t n, long long* totals,
+                                cudaStream_t stream);
+
+// Validation: counts rows outside [0, num_rows) into *bad.
+cudaError_t launch_check_rows(const int32_t* rows, int64_t n, int32_t num_rows, int32_t* bad,
+                              cudaStream_t stream);
+
+}  // namespace spnnz_gpu

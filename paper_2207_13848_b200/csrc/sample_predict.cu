@@ -1,0 +1,106 @@
+// Seeded row sampler and the fused predict kernel.
+//
+// k_sample restates spnnz::make_sample_plan's draw loop
+// (proj/include/spnnz/predict.hpp:48-54 over rng.hpp:14-24) one thread per
+// draw: SplitMix64 is counter based (state_r = seed + (r+1)*gamma), so draw r
+// needs no predecessor.  u = (z >> 11) * 2^-53 is exact; M * u is one IEEE
+// multiply (round-to-nearest, __dmul_rn keeps the compiler from contracting)
+// and the int32 cast truncates toward zero (__double2int_rz), with the
+// reference's rid >= M guard.  Indices are therefore bit-identical.
+//
+// k_predict restates predict_row_structure / _ceil (predict.hpp:126-151):
+// out = min(flop, (int64)ceil(flop / cr)) with an IEEE division (__ddiv_rn,
+// never a reciprocal multiply), optional real view flop / cr.  When fed the
+// device totals it first derives cr = f*/z* (or 1) exactly like
+// collect_sample_stats / predict_proposed (predict.hpp:86-89, :111-117), so
+// the whole pipeline runs without a host round trip.  Streaming: 16-byte
+// loads of the profile, 16-byte evict-first stores.  8 B read + 8 B written
+// per row (+8 B for the real view).
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace spnnz_gpu {
+namespace {
+
+__global__ void k_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* __restrict__ rows) {
+    const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (r >= n) return;
+    const uint64_t z = splitmix_at(seed, static_cast<uint64_t>(r));
+    const double u = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
+    int32_t rid = __double2int_rz(__dmul_rn(static_cast<double>(num_rows), u));
+    if (rid >= num_rows) rid = num_rows - 1;
+    rows[r] = rid;
+}
+
+__device__ __forceinline__ long long ceil_view(long long f, double cr, double* q_out) {
+    const double q = __ddiv_rn(static_cast<double>(f), cr);
+    *q_out = q;
+    const long long c = static_cast<long long>(ceil(q));
+    return f < c ? f : c;
+}
+
+template <bool CEIL, bool REAL>
+__global__ void __launch_bounds__(256)
+k_predict(const int64_t* __restrict__ flop, int64_t m, const long long* __restrict__ totals,
+          double cr_in, int64_t* __restrict__ ceil_out, double* __restrict__ real_out) {
+    const double cr = totals ? predicted_cr(totals[kFStar], totals[kZStar]) : cr_in;
+    const int64_t pairs = m >> 1;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(flop) |
+                          (CEIL ? reinterpret_cast<uintptr_t>(ceil_out) : 0) |
+                          (REAL ? reinterpret_cast<uintptr_t>(real_out) : 0)) & 15) == 0;
+    if (vec_ok) {
+        const longlong2* f2 = reinterpret_cast<const longlong2*>(flop);
+        for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < pairs; i += stride) {
+            const longlong2 f = ld_stream_ll2(&f2[i]);
+            double q0, q1;
+            const long long c0 = ceil_view(f.x, cr, &q0);
+            const long long c1 = ceil_view(f.y, cr, &q1);
+            if (CEIL) st_stream_ll2(reinterpret_cast<longlong2*>(ceil_out) + i, make_longlong2(c0, c1));
+            if (REAL) st_stream_d2(reinterpret_cast<double2*>(real_out) + i, make_double2(q0, q1));
+        }
+        if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+            double q;
+            const long long c = ceil_view(flop[m - 1], cr, &q);
+            if (CEIL) ceil_out[m - 1] = c;
+            if (REAL) real_out[m - 1] = q;
+        }
+    } else {
+        for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += stride) {
+            double q;
+            const long long c = ceil_view(flop[i], cr, &q);
+            if (CEIL) ceil_out[i] = c;
+            if (REAL) real_out[i] = q;
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* rows,
+                          cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    k_sample<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(seed, num_rows, n, rows);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_predict(const int64_t* flop, int64_t m, const long long* totals, double cr,
+                           int64_t* ceil_out, double* real_out, int num_sms, cudaStream_t stream) {
+    if (m == 0 || (!ceil_out && !real_out)) return cudaSuccess;
+    // Enough resident warps to cover HBM latency: 8 blocks of 256 per SM,
+    // grid-stride over 16-byte pairs.
+    int64_t grid = ((m >> 1) + 255) / 256;
+    const int64_t cap = int64_t(num_sms) * 8;
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    const unsigned g = static_cast<unsigned>(grid);
+    if (ceil_out && real_out)
+        k_predict<true, true><<<g, 256, 0, stream>>>(flop, m, totals, cr, ceil_out, real_out);
+    else if (ceil_out)
+        k_predict<true, false><<<g, 256, 0, stream>>>(flop, m, totals, cr, ceil_out, real_out);
+    else
+        k_predict<false, true><<<g, 256, 0, stream>>>(flop, m, totals, cr, ceil_out, real_out);
+    return cudaGetLastError();
+}
+
+}  // namespace spnnz_gpu

@@ -1,0 +1,439 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and
+the reference's golden fixtures, bit-exact for every integer output and for
+the IEEE-double CR / Z1* / Z2* (north_star allows 1e-12 relative; we assert
+equality).  Restates the reference's hot-path tests (proj/tests/test_flop.cpp,
+test_symbolic.cpp, test_predict.cpp, acceptance.cpp) on the device.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2207_13848_b200 import gen, spnnz
+from paper_2207_13848_b200.spnnz import Predictor, SamplePlan, SamplePolicy
+from tests.util import csr, dense_bool_multiply_row_nnz, dense_flop_count, digest, identity, upper_2x2
+
+pytestmark = pytest.mark.gpu
+UNCAPPED = -1
+CR_RTOL = 1e-12  # north_star tolerance for the compression ratio (we also check ==)
+
+
+@pytest.fixture(scope="module")
+def P():
+    p = Predictor(0)
+    yield p
+    p.close()
+
+
+def gpu_exact(P, a, b):
+    P.load(a, b)
+    prof = P.compute_flop()
+    ex = P.exact_symbolic()
+    return prof, ex
+
+
+# ------------------------------------------------------------------ flop
+def test_flop_known_answers(P):
+    eye = identity(4)
+    P.load(eye, eye)
+    pr = P.compute_flop()
+    assert pr.flop_per_row.tolist() == [1, 1, 1, 1] and pr.total_flop == 4 and pr.max_flop_row == 1
+    u = upper_2x2()
+    P.load(u, u)
+    pr = P.compute_flop()
+    assert pr.flop_per_row.tolist() == [3, 1] and pr.total_flop == 4 and pr.max_flop_row == 3
+
+
+def test_flop_errors_and_empty(P):
+    P.load(identity(3), identity(4))
+    with pytest.raises(ValueError):  # test_flop.cpp:42-44
+        P.compute_flop()
+    e = csr(0, 0, [])
+    P.load(e, e)
+    pr = P.compute_flop()
+    assert len(pr.flop_per_row) == 0 and pr.total_flop == 0 and pr.max_flop_row == 0
+
+
+def test_flop_trials_vs_reference(P, golden):
+    # test_flop.cpp:56-68 (200 trials, seed 2024) against the reference's digests
+    rng = gen.SplitMix64(2024)
+    for rec in golden["trials"]["flop_dense_oracle"]["trials"]:
+        m, k, n = 1 + rng.next_below(60), 1 + rng.next_below(60), 1 + rng.next_below(60)
+        d = 0.02 + 0.3 * rng.next_double()
+        a = gen.random_pattern(m, k, d, rng)
+        b = gen.random_pattern(k, n, d, rng)
+        P.load(a, b)
+        pr = P.compute_flop()
+        assert pr.total_flop == rec["F"] == dense_flop_count(a, b)
+        assert pr.max_flop_row == rec["max"] and digest(pr.flop_per_row) == rec["flop"]
+
+
+def test_flop_long_rows_and_empty_rows(P, oracle):
+    """Rows spanning many merge-path tiles (carry chains) and long runs of
+    empty rows (tiles with no nonzeros)."""
+    rows = [list(range(0, 20000, 2)), [], [], list(range(5)), [7] * 0, list(range(30000))]
+    rows += [[] for _ in range(5000)] + [[1, 2, 3]] + [list(range(i % 97)) for i in range(3000)]
+    a = csr(len(rows), 30000, rows)
+    b = gen.uniform_len(30000, 4000, 0, 40, 11)
+    P.load(a, b)
+    pr = P.compute_flop()
+    f, F, mx = oracle.compute_flop(a, b)
+    assert (pr.flop_per_row == f).all() and pr.total_flop == F and pr.max_flop_row == mx
+
+
+# -------------------------------------------------------------- sampler
+def test_sampler_matches_reference(P, golden):
+    for rec in golden["refkat"]["plans"]:
+        plan = spnnz.make_sample_plan(rec["m"], rec["seed"], SamplePolicy(rec["fraction"], rec["cap"]))
+        assert plan.sample_num == rec["n"] and plan.p == rec["p"]
+        assert plan.sample_rows[:8].tolist() == rec["head"] and int(plan.sample_rows[-1]) == rec["last"]
+        assert digest(plan.sample_rows) == rec["digest"]
+    with pytest.raises(ValueError):
+        spnnz.make_sample_plan(0, 1)
+
+
+def test_sampler_large_vs_oracle(P, oracle):
+    for m, seed, frac in [(2**31 - 1, 5, 1e-4), (12345678, 2**63 + 11, 0.01), (3, 0, 1.0)]:
+        plan = spnnz.make_sample_plan(m, seed, SamplePolicy(frac, UNCAPPED))
+        rows, n, p = oracle.make_sample_plan(m, seed, frac, UNCAPPED)
+        assert plan.sample_num == n and plan.p == p and (plan.sample_rows == rows).all()
+
+
+# -------------------------------------------------------------- symbolic
+def test_symbolic_known_answers(P):
+    u = upper_2x2()
+    prof, ex = gpu_exact(P, u, u)
+    assert ex.nnz_per_row.tolist() == [2, 1] and ex.total_nnz == 3  # test_symbolic.cpp:55-61
+    a, b = csr(1, 2, [[0, 1]]), csr(2, 2, [[0, 1], [1]])
+    assert gpu_exact(P, a, b)[1].nnz_per_row.tolist() == [2]  # :37-43
+    a0 = csr(1, 2, [[]])
+    assert gpu_exact(P, a0, identity(2))[1].nnz_per_row.tolist() == [0]  # :45-53
+    P.load(u, u)
+    P.compute_flop()
+    assert P.sampled_symbolic([]).total_nnz == 0  # :135-149
+    assert P.sampled_symbolic([0]).total_nnz == 2
+    r = P.sampled_symbolic([0, 0, 1])
+    assert r.total_nnz == 5 and r.nnz_per_row.tolist() == [2, 2, 1]
+    with pytest.raises(ValueError):
+        P.sampled_symbolic([2])
+    with pytest.raises(ValueError):
+        P.sampled_symbolic([-1])
+
+
+def test_symbolic_profile_mismatch_rejected():
+    # test_symbolic.cpp:157-163
+    eye3, eye4 = identity(3), identity(4)
+    prof3 = spnnz.compute_flop(eye3, eye3)
+    with pytest.raises(ValueError):
+        spnnz.exact_symbolic(eye4, eye4, prof3)
+    with pytest.raises(ValueError):
+        spnnz.exact_symbolic(eye3, eye4, prof3)
+
+
+def test_symbolic_trials_vs_reference(P, golden):
+    # test_symbolic.cpp:63-77 (100 trials, seed 31337)
+    rng = gen.SplitMix64(31337)
+    for rec in golden["trials"]["symbolic_dense_oracle"]["trials"]:
+        m, k, n = 1 + rng.next_below(80), 1 + rng.next_below(80), 1 + rng.next_below(80)
+        d = 0.01 + 0.25 * rng.next_double()
+        a = gen.random_pattern(m, k, d, rng)
+        b = gen.random_pattern(k, n, d, rng)
+        prof, ex = gpu_exact(P, a, b)
+        assert (ex.nnz_per_row == dense_bool_multiply_row_nnz(a, b)).all()
+        assert ex.total_nnz == rec["Z"] and digest(ex.nnz_per_row) == rec["nnz"]
+
+
+def test_acceptance_oracle_trials(P, golden):
+    # acceptance.cpp:147-169: 1000 trials up to 200x200x200, zero mismatches
+    rng = gen.SplitMix64(42424242)
+    mism = 0
+    for rec in golden["trials"]["acceptance_oracle"]["trials"]:
+        m, k, n = 1 + rng.next_below(200), 1 + rng.next_below(200), 1 + rng.next_below(200)
+        da, db = 0.002 + 0.25 * rng.next_double(), 0.002 + 0.25 * rng.next_double()
+        a = gen.random_pattern(m, k, da, rng)
+        b = gen.random_pattern(k, n, db, rng)
+        prof, ex = gpu_exact(P, a, b)
+        mism += (digest(ex.nnz_per_row) != rec["nnz"] or ex.total_nnz != rec["Z"]
+                 or digest(prof.flop_per_row) != rec["flop"])
+    assert mism == 0
+
+
+def tier_matrix(n_rows, n_cols, lens, b_lens, seed):
+    """A with the given row lengths, B with the given lengths, uniform cols."""
+    rng = np.random.default_rng(seed)
+    rows_a = [np.sort(rng.choice(n_cols, size=min(L, n_cols), replace=False)).tolist() for L in lens]
+    a = csr(n_rows, n_cols, rows_a)
+    rows_b = [np.sort(rng.choice(n_cols, size=min(L, n_cols), replace=False)).tolist() for L in b_lens]
+    b = csr(n_cols, n_cols, rows_b)
+    return a, b
+
+
+@pytest.mark.parametrize("ncols", [3000, 1 << 20])
+def test_every_bin_vs_oracle(P, oracle, ncols):
+    """Rows whose FLOP lands in every bin (<=32, <=512, <=4096, <=32768,
+    heavy) including duplicates-heavy rows, for small and large B.cols."""
+    rng = np.random.default_rng(ncols)
+    lens = [0, 1, 2, 5, 10, 40, 100, 300, 700, 1500, 2500] + list(rng.integers(0, 200, 200))
+    b_lens = list(rng.integers(0, 60, 3000)) + [2000, 2999]
+    nc = 3000
+    a, b = tier_matrix(len(lens), nc, lens, b_lens, 1)
+    # widen B's column space so the bitmap tier sees ncols bits
+    b = csr(b.rows, ncols, [list((np.array(b.col[b.rpt[i]:b.rpt[i + 1]]) * (ncols // nc)).tolist())
+                           for i in range(b.rows)])
+    a = csr(a.rows, b.rows, [a.col[a.rpt[i]:a.rpt[i + 1]].tolist() for i in range(a.rows)])
+    prof, ex = gpu_exact(P, a, b)
+    f, F, mx = oracle.compute_flop(a, b)
+    nnz, Z = oracle.exact_symbolic(a, b, f, mx)
+    assert (prof.flop_per_row == f).all()
+    bins = np.digitize(f, [1, 33, 513, 4097, 32769])
+    assert set(bins.tolist()) >= {0, 1, 2, 3, 4, 5}, "matrix must exercise every bin"
+    assert (ex.nnz_per_row == nnz).all() and ex.total_nnz == Z
+    rows = np.arange(a.rows, dtype=np.int32)[::-1].copy()
+    s = P.sampled_symbolic(rows)
+    assert (s.nnz_per_row == nnz[rows]).all() and s.total_nnz == Z
+
+
+def test_heavy_pool_batching(P, oracle, monkeypatch):
+    """More heavy rows than pool slots: the batch loop and the cleaning pass
+    must leave the pool zeroed for the next batch."""
+    monkeypatch.setenv("SPNNZ_HEAVY_POOL_SLOTS", "2")
+    q = Predictor(0)
+    rng = np.random.default_rng(3)
+    lens = [3000, 2500, 2800, 2900, 2700, 10, 3000]
+    a, b = tier_matrix(len(lens), 4000, lens, list(rng.integers(5, 40, 4000)), 5)
+    q.load(a, b)
+    q.compute_flop()
+    ex = q.exact_symbolic()
+    f, F, mx = oracle.compute_flop(a, b)
+    nnz, Z = oracle.exact_symbolic(a, b, f, mx)
+    assert (f[[0, 1, 2, 3, 4, 6]] > 32768).all()
+    assert (ex.nnz_per_row == nnz).all()
+    ex2 = q.exact_symbolic()  # pool must be clean again
+    assert (ex2.nnz_per_row == nnz).all()
+    q.close()
+
+
+# ------------------------------------------------------------ predictor
+def test_predict_views(P):
+    prof = spnnz.FlopProfile(np.array([3, 1, 0], np.int64), 4, 3)  # test_predict.cpp:90-112
+    assert spnnz.predict_row_structure(prof, 1.0).tolist() == [3.0, 1.0, 0.0]
+    r = spnnz.predict_row_structure(prof, 4.0 / 3.0)
+    assert r[0] == 3 / (4.0 / 3.0) and r[1] == 1 / (4.0 / 3.0) and r[2] == 0.0
+    assert spnnz.predict_row_structure_ceil(prof, 4.0 / 3.0).tolist() == [3, 1, 0]
+    with pytest.raises(ValueError):
+        spnnz.predict_row_structure(prof, 0.0)
+    with pytest.raises(ValueError):
+        spnnz.predict_row_structure_ceil(prof, -1.0)
+
+
+def test_predict_views_bitwise_vs_oracle(oracle):
+    rng = np.random.default_rng(1)
+    f = np.concatenate([rng.integers(0, 2**40, 5001), [0, 1, 2**53 + 1, 2**62]]).astype(np.int64)
+    prof = spnnz.FlopProfile(f, int(f.sum() % 2**62), int(f.max()))
+    for cr in (1.0, 1.0000000001, 4.0 / 3.0, 2.15, 5.844, 1e-3, 1e9):
+        assert (spnnz.predict_row_structure_ceil(prof, cr) == oracle.predict_row_structure_ceil(f, cr)).all()
+        assert (spnnz.predict_row_structure(prof, cr) == oracle.predict_row_structure(f, cr)).all()
+
+
+def test_identity_predicts_exactly():
+    # test_predict.cpp:146-157
+    for n in (10, 100, 1000):
+        for seed in (1, 7, 99):
+            eye = identity(n)
+            rep = spnnz.run_prediction(eye, eye, seed)
+            assert rep.predicted_cr == 1.0 and rep.z2_star == float(n)
+            assert abs(rep.z1_star - n) <= 1e-9 * n
+
+
+def test_pipeline_vs_reference_runs(golden):
+    # test_predict.cpp:184-217 against the reference's own pipeline
+    rng = gen.SplitMix64(123)
+    for rec in golden["trials"]["predict_pipeline"]["trials"]:
+        n = 20 + rng.next_below(150)
+        a = gen.random_pattern(n, n, 0.1, rng)
+        b = gen.random_pattern(n, n, 0.1, rng)
+        seed = rng.next_u64()
+        rep = spnnz.run_prediction(a, b, seed)
+        ref = rec["report"]
+        assert rep.total_flop == ref["total_flop"] and rep.stats.sampled_flop == ref["sampled_flop"]
+        assert rep.stats.sampled_nnz == ref["sampled_nnz"] and rep.plan.sample_num == ref["sample_num"]
+        assert rep.plan.p == ref["p"] and rep.z1_star == ref["z1_star"] and rep.z2_star == ref["z2_star"]
+        assert rep.predicted_cr == ref["predicted_cr"] and rep.stats.sampled_cr == ref["sampled_cr"]
+        assert digest(rep.predicted_row_nnz_ceil) == rec["ceil"]
+        assert rep.plan.sample_rows.tolist() == rec["rows"]
+
+
+def test_exhaustive_plan_is_exact():
+    # test_predict.cpp:159-182, acceptance.cpp:201-231
+    rng = gen.SplitMix64(77)
+    for _ in range(10):
+        n = 5 + rng.next_below(60)
+        a = gen.random_pattern(n, n, 0.15, rng)
+        b = gen.random_pattern(n, n, 0.15, rng)
+        prof = spnnz.compute_flop(a, b)
+        ex = spnnz.exact_symbolic(a, b, prof)
+        if ex.total_nnz == 0:
+            continue
+        rep = spnnz.run_prediction_with_plan(a, b, prof, spnnz.exhaustive_plan(n))
+        assert rep.z1_star == ex.total_nnz and rep.z2_star == ex.total_nnz
+        e = spnnz.error_report(rep.z1_star, rep.z2_star, rep.stats.sampled_flop, ex.total_nnz,
+                               prof.total_flop, rep.plan.p)
+        assert (e.eps1, e.eps_f, e.eps2) == (0.0, 0.0, 0.0)
+
+
+def test_free_function_composition(oracle):
+    """collect_sample_stats / estimators over GPU pieces equal run_prediction."""
+    rng = gen.SplitMix64(55)
+    a = gen.random_pattern(400, 400, 0.05, rng)
+    b = gen.random_pattern(400, 400, 0.05, rng)
+    prof = spnnz.compute_flop(a, b)
+    plan = spnnz.make_sample_plan(a.rows, 42)
+    sampled = spnnz.sampled_symbolic(a, b, prof, plan.sample_rows)
+    stats = spnnz.collect_sample_stats(prof, plan, sampled)
+    pp = spnnz.predict_proposed(stats, prof.total_flop)
+    rep = spnnz.run_prediction(a, b, 42)
+    assert stats.sampled_flop == rep.stats.sampled_flop and stats.sampled_nnz == rep.stats.sampled_nnz
+    assert pp.z2_star == rep.z2_star and pp.predicted_cr == rep.predicted_cr
+    assert spnnz.predict_reference(stats, plan) == rep.z1_star
+    assert spnnz.sampled_flop(prof, [0, 0]) == 2 * prof.flop_per_row[0]
+    ora = oracle.run_prediction(a, b, 42, 0.003, 300)[0]
+    assert ora.z2_star == rep.z2_star and ora.sampled_nnz == rep.stats.sampled_nnz
+
+
+# ---------------------------------------------------------- configs 1-5
+def test_config1_full_arrays(P, golden):
+    a, b = gen.make_config(1)
+    arr, rec = golden["cfg1"], golden["configs"]["1"]
+    P.load(a, b)
+    prof = P.compute_flop()
+    assert (prof.flop_per_row == arr["flop"]).all() and prof.total_flop == rec["F"]
+    ex = P.exact_symbolic()
+    assert (ex.nnz_per_row == arr["exact_nnz"]).all() and ex.total_nnz == rec["Z"]
+    for label, cap in (("uncapped", UNCAPPED), ("cap300", 300)):
+        rep = P.run_prediction(1, SamplePolicy(0.01, cap))
+        ref = rec["modes"][label]["report"]
+        for k in ("total_flop", "sampled_flop", "sampled_nnz", "p", "z1_star", "z2_star", "predicted_cr"):
+            got = getattr(rep, k) if hasattr(rep, k) else getattr(rep.stats, k, None)
+            if got is None:
+                got = getattr(rep.plan, k)
+            assert got == ref[k], k
+        assert (rep.predicted_row_nnz_ceil == arr[f"ceil_{label}"]).all()
+        assert (rep.predicted_row_nnz == arr[f"real_{label}"]).all()
+        assert (rep.plan.sample_rows == arr[f"rows_{label}"]).all()
+        s = P.sampled_symbolic(rep.plan.sample_rows)
+        assert (s.nnz_per_row == arr[f"per_sample_{label}"]).all()
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_config_vs_reference_digests(P, golden, cfg):
+    if str(cfg) not in golden["configs"]:
+        pytest.skip("configs.json lacks this config (make_golden.py --big)")
+    rec = golden["configs"][str(cfg)]
+    info = gen.CONFIGS[cfg]
+    a, b = gen.make_config(cfg)
+    assert digest(a.rpt) == rec["input"]["a_rpt"] and digest(a.col) == rec["input"]["a_col"]
+    P.load(a, b)
+    prof = P.compute_flop()
+    assert prof.total_flop == rec["F"] and prof.max_flop_row == rec["max"]
+    assert digest(prof.flop_per_row) == rec["flop"]
+    for label, cap in (("uncapped", UNCAPPED), ("cap300", 300)):
+        m = rec["modes"][label]
+        rep = P.run_prediction(info["seed"], SamplePolicy(info["fraction"], cap))
+        ref = m["report"]
+        assert rep.total_flop == ref["total_flop"]
+        assert rep.stats.sampled_flop == ref["sampled_flop"] and rep.stats.sampled_nnz == ref["sampled_nnz"]
+        assert rep.plan.sample_num == ref["sample_num"] and rep.plan.p == ref["p"]
+        assert rep.predicted_cr == ref["predicted_cr"]
+        assert abs(rep.predicted_cr - ref["predicted_cr"]) <= CR_RTOL * ref["predicted_cr"]
+        assert rep.z1_star == ref["z1_star"] and rep.z2_star == ref["z2_star"]
+        assert digest(rep.plan.sample_rows) == m["rows"]
+        assert digest(rep.predicted_row_nnz_ceil) == m["ceil"]
+        assert digest(rep.predicted_row_nnz) == m["real"]
+        s = P.sampled_symbolic(rep.plan.sample_rows)
+        assert s.total_nnz == m["z_star"] and digest(s.nnz_per_row) == m["per_sample"]
+    if "Z" in rec:
+        ex = P.exact_symbolic()
+        assert ex.total_nnz == rec["Z"] and digest(ex.nnz_per_row) == rec["exact_nnz"]
+        if cfg == 3:
+            assert ex.total_nnz == 634 ** 3 and prof.total_flop == 1142 ** 3
+
+
+def test_config5_exact_properties(P):
+    """Config 5 has no CPU exact pass (hours); check size-independent
+    properties of the GPU exact pass: nnz <= flop, nnz >= 1 where flop >= 1,
+    the sampled pass equals the exact pass at the sampled rows, and the
+    sampled CR is >= 1."""
+    a, b = gen.make_config(5)
+    P.load(a, b)
+    prof = P.compute_flop()
+    ex = P.exact_symbolic()
+    f, z = prof.flop_per_row, ex.nnz_per_row
+    assert (z <= f).all() and ((f == 0) | (z >= 1)).all()
+    assert ex.total_nnz == int(z.sum())
+    rep = P.run_prediction(5, SamplePolicy(0.001, UNCAPPED))
+    rows = rep.plan.sample_rows
+    assert rep.stats.sampled_nnz == int(z[rows].sum())
+    assert rep.stats.sampled_flop == int(f[rows].sum())
+    assert rep.predicted_cr >= 1.0
+    e = spnnz.error_report(rep.z1_star, rep.z2_star, rep.stats.sampled_flop, ex.total_nnz,
+                           prof.total_flop, rep.plan.p)
+    assert e.identity_residual <= 1e-9 * max(1.0, abs(e.eps2))
+    print(f"cfg5: Z={ex.total_nnz} eps1={e.eps1:+.4%} eps2={e.eps2:+.4%}")
+
+
+def test_detached_shards_combine_to_single_gpu(oracle):
+    """world > 1 without NCCL on one GPU: every rank's local pass, combined on
+    the host, equals the 1-GPU result (bit-exact), for 2, 3 and 8 shards."""
+    a, b = gen.make_config(2)
+    single = Predictor(0)
+    single.load(a, b)
+    ref = single.run_prediction(2, SamplePolicy(0.003, UNCAPPED))
+    single.close()
+    for world in (2, 3, 8):
+        F = fs = zs = 0
+        flops, shards = [], []
+        for r in range(world):
+            q = Predictor(0, r, world)
+            q.load(a, b)
+            pr = q.compute_flop()
+            flops.append(pr.flop_per_row)
+            F += pr.total_flop
+            mine = ref.plan.sample_rows[(ref.plan.sample_rows >= q.row_lo) & (ref.plan.sample_rows < q.row_hi)]
+            fs += q.sampled_flop(mine)
+            zs += q.sampled_symbolic(mine).total_nnz
+            shards.append(q)
+        assert F == ref.total_flop and fs == ref.stats.sampled_flop and zs == ref.stats.sampled_nnz
+        assert (np.concatenate(flops) == oracle.compute_flop(a, b)[0]).all()
+        cr = spnnz.predict_proposed(spnnz.SampleStats(fs, zs), F).predicted_cr
+        assert cr == ref.predicted_cr
+        ceil = np.concatenate([q.predict_row_structure_ceil(cr) for q in shards])
+        assert (ceil == ref.predicted_row_nnz_ceil).all()
+        for q in shards:
+            q.close()
+
+
+def test_repeat_runs_deterministic(P):
+    a, b = gen.make_config(4)
+    P.load(a, b)
+    r1 = P.run_prediction(4, SamplePolicy(0.005, UNCAPPED))
+    r2 = P.run_prediction(4, SamplePolicy(0.005, UNCAPPED))
+    assert r1.stats.sampled_nnz == r2.stats.sampled_nnz and r1.z2_star == r2.z2_star
+    assert (r1.predicted_row_nnz_ceil == r2.predicted_row_nnz_ceil).all()
+
+
+def test_device_residency_matches_host(P):
+    import torch
+    a, b = gen.make_config(3)
+    P.load(a, b)
+    host = P.run_prediction(3, SamplePolicy(0.001, UNCAPPED))
+    dev = torch.empty(a.rows, dtype=torch.int64, device="cuda")
+    rep = P.run_prediction(3, SamplePolicy(0.001, UNCAPPED), ceil_out=dev, want_real=False,
+                           want_samples=False)
+    assert rep.z2_star == host.z2_star
+    assert (dev.cpu().numpy() == host.predicted_row_nnz_ceil).all()
+    # device-resident inputs
+    ta = type("M", (), dict(rows=a.rows, cols=a.cols, rpt=torch.from_numpy(a.rpt).cuda(),
+                            col=torch.from_numpy(a.col).cuda()))()
+    P.load(ta, None)
+    rep2 = P.run_prediction(3, SamplePolicy(0.001, UNCAPPED))
+    assert rep2.z2_star == host.z2_star and (rep2.predicted_row_nnz_ceil == host.predicted_row_nnz_ceil).all()
