@@ -158,8 +158,8 @@ struct spnnz_gpu_ctx {
     DBuf<int32_t> counts;
     DBuf<int32_t> lists;
     int64_t list_cap = 0;
-    DBuf<int64_t> heavy_unit_off, heavy_table_off;
-    DBuf<int32_t> heavy_mode;
+    DBuf<int64_t> heavy_unit_off, heavy_eoff, heavy_epre, heavy_eb0;
+    long long* h_meta = nullptr;    // pinned mirror of heavy_meta
     DBuf<uint32_t> pool;
     int64_t pool_slots = 0, pool_words = 0;
     DBuf<long long> heavy_meta;
@@ -216,8 +216,7 @@ int sym_scratch(spnnz_gpu_ctx* c, int64_t items, SymScratch* s) {
     if (items > c->list_cap) {
         RC(c->lists.ensure(items * kNumBins));
         RC(c->heavy_unit_off.ensure(items + 1));
-        RC(c->heavy_table_off.ensure(items + 1));
-        RC(c->heavy_mode.ensure(items));
+        RC(c->heavy_eoff.ensure(items + 1));
         c->list_cap = items;
     }
     RC(c->counts.ensure(16));
@@ -226,8 +225,10 @@ int sym_scratch(spnnz_gpu_ctx* c, int64_t items, SymScratch* s) {
     s->capacity = c->list_cap;
     s->counts = c->counts.p;
     s->heavy_unit_off = c->heavy_unit_off.p;
-    s->heavy_table_off = c->heavy_table_off.p;
-    s->heavy_mode = c->heavy_mode.p;
+    s->heavy_eoff = c->heavy_eoff.p;
+    s->heavy_epre = c->heavy_epre.p;
+    s->heavy_eb0 = c->heavy_eb0.p;
+    s->heavy_ecap = c->heavy_epre.n;
     s->heavy_meta = c->heavy_meta.p;
     s->pool = c->pool.p;
     s->pool_words = c->pool_words;
@@ -284,6 +285,7 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     g.total_slot = slot;
     g.sampled_flop = sampled_flop;
     CU(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * 16, c->stream));
+    CU(cudaMemsetAsync(c->heavy_meta.p, 0, sizeof(long long) * 4, c->stream));
     if (n_items == 0) return SPNNZ_OK;
     CU(launch_sym_bin(g, s, c->stream));
     CU(launch_sym_tiers(g, s, c->num_sms, c->stream));
@@ -291,14 +293,25 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     // Heavy rows: the host learns their number, then runs pool-sized batches.
     CU(cudaMemcpyAsync(c->h_counts, c->counts.p, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost,
                        c->stream));
+    CU(cudaMemcpyAsync(c->h_meta, c->heavy_meta.p, sizeof(long long) * 4, cudaMemcpyDeviceToHost,
+                       c->stream));
     CU(cudaStreamSynchronize(c->stream));
     const int64_t heavy = c->h_counts[5];
     if (heavy > 0) {
+        // per-entry prefix arrays for the heavy rows (sum of lengths + 1 each)
+        const int64_t ents = c->h_meta[1];
+        if (ents > c->heavy_epre.n) {
+            RC(c->heavy_epre.ensure(ents));
+            RC(c->heavy_eb0.ensure(ents));
+        }
+        s.heavy_epre = c->heavy_epre.p;
+        s.heavy_eb0 = c->heavy_eb0.p;
+        s.heavy_ecap = c->heavy_epre.n;
         RC(ensure_pool(c, heavy, &s));
         for (int64_t first = 0; first < heavy; first += c->pool_slots) {
             const int64_t cnt = std::min<int64_t>(c->pool_slots, heavy - first);
             CU(launch_sym_heavy(g, s, first, cnt, c->num_sms, c->stream));
-            *launches += 3;
+            *launches += 4;
         }
     }
     return SPNNZ_OK;
@@ -446,6 +459,7 @@ int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz
     e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_totals, sizeof(long long) * kTotals);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_counts, sizeof(int32_t) * 16);
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_meta, sizeof(long long) * 4);
     for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     int rc = SPNNZ_OK;
     if (e != cudaSuccess) rc = set_err(SPNNZ_ECUDA, "create: %s", cudaGetErrorString(e));
@@ -479,9 +493,9 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm) nccl().CommDestroy(c->comm);
     for (auto* b : {&c->b_rpt, &c->a_rpt, &c->flop, &c->out64, &c->heavy_unit_off,
-                    &c->heavy_table_off})
+                    &c->heavy_eoff, &c->heavy_epre, &c->heavy_eb0})
         b->release();
-    for (auto* b : {&c->b_col, &c->a_col, &c->tile_x, &c->counts, &c->lists, &c->heavy_mode,
+    for (auto* b : {&c->b_col, &c->a_col, &c->tile_x, &c->counts, &c->lists,
                     &c->samples, &c->rows_in, &c->bad})
         b->release();
     for (auto* b : {&c->tile_carry, &c->tile_total, &c->tile_max, &c->totals, &c->heavy_meta})
@@ -490,6 +504,7 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     c->outf.release();
     if (c->h_totals) cudaFreeHost(c->h_totals);
     if (c->h_counts) cudaFreeHost(c->h_counts);
+    if (c->h_meta) cudaFreeHost(c->h_meta);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);

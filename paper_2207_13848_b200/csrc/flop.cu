@@ -159,7 +159,7 @@ k_flop_fixup(const int32_t* __restrict__ tile_x, int64_t tiles, int32_t m,
         sum = tile_total[t];
         mx = tile_max[t];
         const int32_t r = tile_x[t + 1];
-        const bool first = (r < m) && !(tile_x[t] == r);
+        const bool first = (r < m) && (t == 0 || tile_x[t] != r);
         if (first) {
             long long carry = 0;
             for (int64_t u = t; u < tiles && tile_x[u + 1] == r; ++u) carry += tile_carry[u];

@@ -64,20 +64,24 @@ constexpr int kNumBins = 6;
 constexpr int64_t kBin1Max = 32;     // warp, __match_any_sync dedup
 constexpr int64_t kBin2Max = 512;    // warp, 1024-slot smem hash per warp
 constexpr int64_t kBin3Max = 4096;   // 256-thread block, 8192-slot smem hash
-constexpr int64_t kBin4Max = 16384;  // 1024-thread block, 32768-slot smem hash
-// bin 5: heavy rows, global-memory bitmap/hash tables, many blocks per row.
+constexpr int64_t kBin4Max = 32768;  // 512-thread block, 53248-slot smem hash
+// bin 5: heavy rows, split into units of kHeavyUnitProducts products, many
+//        blocks per row over a global-memory bitmap of B.cols bits.
+constexpr int64_t kHeavyUnitProducts = 16384;
 
 struct SymScratch {
     int32_t* lists = nullptr;        // kNumBins * capacity item ids
     int64_t capacity = 0;
     int32_t* counts = nullptr;       // kNumBins (+ spare) counters
-    // heavy-row work decomposition
-    int64_t* heavy_unit_off = nullptr;   // capacity + 1
-    int64_t* heavy_table_off = nullptr;  // capacity + 1 (words)
-    int32_t* heavy_mode = nullptr;       // capacity: 0 hash, 1 bitmap
-    uint32_t* pool = nullptr;            // global tables, kept clean between calls
+    // heavy-row work decomposition (per batch of heavy items)
+    int64_t* heavy_unit_off = nullptr;   // capacity + 1: product-unit prefix per item
+    int64_t* heavy_eoff = nullptr;       // capacity + 1: entry-array offset per item
+    int64_t* heavy_epre = nullptr;       // per entry: exclusive product prefix (L_i + 1 per item)
+    int64_t* heavy_eb0 = nullptr;        // per entry: start of its B row
+    int64_t heavy_ecap = 0;
+    uint32_t* pool = nullptr;            // bitmaps of B.cols bits, kept clean between calls
     int64_t pool_words = 0;
-    long long* heavy_meta = nullptr;     // [0] units, [1] words used, [2] work counter
+    long long* heavy_meta = nullptr;     // [0] units in batch, [1] sum of heavy row lengths
 };
 
 struct SymArgs {

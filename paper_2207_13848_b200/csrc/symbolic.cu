@@ -93,6 +93,18 @@ __global__ void __launch_bounds__(BLOCK) k_sym_bin(SymArgs g, SymScratch sc) {
             }
             if (g.out && (bin == 0 || bin == 5 || bin == 6)) g.out[s] = 0;
         }
+        // total entries of heavy rows (sizes the per-entry prefix arrays)
+        long long hl = 0;
+        if (bin == 5) {
+            const int32_t r = (g.rows ? g.rows[s] : g.row_lo + static_cast<int32_t>(s)) - g.row_lo;
+            hl = g.a.rpt[r + 1] - g.a.rpt[r] + 1;
+        }
+        if (__any_sync(kFull, hl != 0)) {
+            hl = warp_sum_ll(hl);
+            if (lane == 0)
+                atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[1]),
+                          static_cast<unsigned long long>(hl));
+        }
         // warp-aggregated append to the bin lists
         const unsigned peers = __match_any_sync(kFull, bin);
         if (bin >= 1 && bin <= 5) {
@@ -279,78 +291,163 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
 }
 
 // ------------------------------------------------ bin 5: heavy rows
+// A heavy row's products are split into units of kHeavyUnitProducts; one
+// block per unit (grid-stride), so hub rows whose entries point at hub B rows
+// spread over the whole GPU.  Sets are global bitmaps of B.cols bits from the
+// pool (one per row of the batch); insertion = test, then atomicOr, counting
+// bits this thread turned on.  A second pass over the same products stores 0
+// to every touched word, which returns the pool to all-zero without a memset.
 constexpr int kHeavyBlock = 256;
-constexpr int kHeavyUnit = 1024;  // A-row entries per work unit
 
-// One block: unit prefix over the batch's heavy items.
-__global__ void k_heavy_prep(SymArgs g, SymScratch sc, int64_t first, int64_t count) {
-    __shared__ long long s_carry;
-    if (threadIdx.x == 0) s_carry = 0;
+// One block: per-item entry offsets and unit counts for the batch.
+__global__ void __launch_bounds__(256) k_heavy_prep(SymArgs g, SymScratch sc, int64_t first,
+                                                    int64_t count) {
+    using Scan = cub::BlockScan<long long, 256>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ long long s_carry_u, s_carry_e;
+    if (threadIdx.x == 0) s_carry_u = s_carry_e = 0;
     __syncthreads();
     const int32_t* list = sc.lists + 5 * sc.capacity + first;
-    using Scan = cub::BlockScan<long long, 1024>;
-    __shared__ typename Scan::TempStorage tmp;
-    for (int64_t b = 0; b < count; b += 1024) {
+    for (int64_t b = 0; b < count; b += 256) {
         const int64_t i = b + threadIdx.x;
-        long long units = 0;
+        long long units = 0, ents = 0;
         if (i < count) {
-            const ItemRow it = item_row(g, list[i]);
-            units = (it.a1 - it.a0 + kHeavyUnit - 1) / kHeavyUnit;
+            const int32_t s = list[i];
+            const int32_t rid = g.rows ? g.rows[s] : g.row_lo + s;
+            const ItemRow it = item_row(g, s);
+            const long long f = g.flop[rid - g.row_lo];
+            units = (f + kHeavyUnitProducts - 1) / kHeavyUnitProducts;
+            ents = it.a1 - it.a0 + 1;
         }
-        long long excl, total;
-        Scan(tmp).ExclusiveSum(units, excl, total);
-        if (i < count) sc.heavy_unit_off[i] = s_carry + excl;
+        long long ue, ee, ut, et;
+        Scan(tmp).ExclusiveSum(units, ue, ut);
         __syncthreads();
-        if (threadIdx.x == 0) s_carry += total;
+        Scan(tmp).ExclusiveSum(ents, ee, et);
+        if (i < count) {
+            sc.heavy_unit_off[i] = s_carry_u + ue;
+            sc.heavy_eoff[i] = s_carry_e + ee;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_carry_u += ut;
+            s_carry_e += et;
+        }
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        sc.heavy_unit_off[count] = s_carry;
-        sc.heavy_meta[0] = s_carry;
+        sc.heavy_unit_off[count] = s_carry_u;
+        sc.heavy_eoff[count] = s_carry_e;
+        sc.heavy_meta[0] = s_carry_u;
     }
+}
+
+// One block per heavy item: exclusive product prefix over its entries and
+// the start of each entry's B row.
+__global__ void __launch_bounds__(256) k_heavy_entries(SymArgs g, SymScratch sc, int64_t first) {
+    using Scan = cub::BlockScan<long long, 256>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ long long s_carry;
+    const int64_t i = blockIdx.x;
+    const ItemRow it = item_row(g, sc.lists[5 * sc.capacity + first + i]);
+    int64_t* ep = sc.heavy_epre + sc.heavy_eoff[i];
+    int64_t* eb = sc.heavy_eb0 + sc.heavy_eoff[i];
+    const int64_t L = it.a1 - it.a0;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < L; c0 += 256) {
+        const int64_t e = c0 + threadIdx.x;
+        long long d = 0;
+        int64_t b0 = 0;
+        if (e < L) {
+            const int c = __ldg(&g.a.col[it.a0 + e]);
+            b0 = __ldg(&g.brpt[c]);
+            d = __ldg(&g.brpt[c + 1]) - b0;
+        }
+        long long ex, tot;
+        Scan(tmp).ExclusiveSum(d, ex, tot);
+        if (e < L) {
+            ep[e] = s_carry + ex;
+            eb[e] = b0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ep[L] = s_carry;
 }
 
 template <bool CLEAN>
 __global__ void __launch_bounds__(kHeavyBlock) k_heavy(SymArgs g, SymScratch sc, int64_t first,
                                                        int64_t count, int64_t words) {
-    __shared__ int s_off[kHeavyBlock + 1];
+    __shared__ long long s_off[kHeavyBlock];
     __shared__ int64_t s_b0[kHeavyBlock];
+    __shared__ long long s_end;
     __shared__ long long s_red[kHeavyBlock / 32];
     const int32_t* list = sc.lists + 5 * sc.capacity + first;
     const long long units = sc.heavy_meta[0];
     long long acc = 0;
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-        // item owning unit u: largest i with unit_off[i] <= u
-        int64_t lo = 0, hi = count - 1;
+        int64_t lo = 0, hi = count - 1;  // item owning unit u
         while (lo < hi) {
             const int64_t mid = (lo + hi + 1) >> 1;
             if (sc.heavy_unit_off[mid] <= u) lo = mid; else hi = mid - 1;
         }
-        const ItemRow it = item_row(g, list[lo]);
-        const int64_t e0 = it.a0 + (u - sc.heavy_unit_off[lo]) * kHeavyUnit;
-        const int64_t e1 = e0 + kHeavyUnit < it.a1 ? e0 + kHeavyUnit : it.a1;
+        const int32_t s = list[lo];
+        const ItemRow it = item_row(g, s);
+        const int64_t L = it.a1 - it.a0;
+        const int64_t* ep = sc.heavy_epre + sc.heavy_eoff[lo];
+        const int64_t* eb = sc.heavy_eb0 + sc.heavy_eoff[lo];
+        const long long p0 = (u - sc.heavy_unit_off[lo]) * kHeavyUnitProducts;
+        const long long ftot = ep[L];
+        const long long p1 = p0 + kHeavyUnitProducts < ftot ? p0 + kHeavyUnitProducts : ftot;
+        int64_t e0 = 0, e1 = L - 1;  // largest entry with ep[e] <= p0
+        while (e0 < e1) {
+            const int64_t mid = (e0 + e1 + 1) >> 1;
+            if (ep[mid] <= p0) e0 = mid; else e1 = mid - 1;
+        }
         uint32_t* bm = sc.pool + lo * words;
         int cnt = 0;
-        block_products<kHeavyBlock>(g, e0, e1, s_off, s_b0, [&](int key) {
-            uint32_t* w = bm + (static_cast<uint32_t>(key) >> 5);
-            if (CLEAN) {
-                *w = 0u;
-            } else {
-                const uint32_t bit = 1u << (key & 31);
-                if (!(*reinterpret_cast<volatile uint32_t*>(w) & bit))
-                    cnt += (atomicOr(w, bit) & bit) ? 0 : 1;
+        for (int64_t e = e0;;) {
+            const int n = static_cast<int>(L - e < kHeavyBlock ? L - e : kHeavyBlock);
+            if (threadIdx.x < n) {
+                s_off[threadIdx.x] = ep[e + threadIdx.x];
+                s_b0[threadIdx.x] = eb[e + threadIdx.x];
             }
-        });
+            if (threadIdx.x == 0) s_end = ep[e + n];
+            __syncthreads();
+            const long long q0 = p0 > s_off[0] ? p0 : s_off[0];
+            const long long q1 = p1 < s_end ? p1 : s_end;
+            for (long long p = q0 + threadIdx.x; p < q1; p += kHeavyBlock) {
+                int jl = 0, jh = n - 1;
+                while (jl < jh) {
+                    const int mid = (jl + jh + 1) >> 1;
+                    if (s_off[mid] <= p) jl = mid; else jh = mid - 1;
+                }
+                const int key = __ldg(&g.bcol[s_b0[jl] + (p - s_off[jl])]);
+                uint32_t* w = bm + (static_cast<uint32_t>(key) >> 5);
+                if (CLEAN) {
+                    *w = 0u;
+                } else {
+                    const uint32_t bit = 1u << (key & 31);
+                    if (!(*reinterpret_cast<volatile uint32_t*>(w) & bit))
+                        cnt += (atomicOr(w, bit) & bit) ? 0 : 1;
+                }
+            }
+            const bool done = s_end >= p1 || e + n >= L;
+            __syncthreads();
+            if (done) break;
+            e += n;
+        }
         if (!CLEAN) {
             const long long tot = block_sum_ll<kHeavyBlock>(cnt, s_red);
             if (threadIdx.x == 0 && tot) {
                 if (g.out)
-                    atomicAdd(reinterpret_cast<unsigned long long*>(&g.out[it.s]),
+                    atomicAdd(reinterpret_cast<unsigned long long*>(&g.out[s]),
                               static_cast<unsigned long long>(tot));
                 acc += tot;
             }
-            __syncthreads();
         }
+        __syncthreads();
     }
     if (!CLEAN && threadIdx.x == 0 && acc)
         atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[g.total_slot]),
@@ -399,7 +496,8 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, int64_t f
                              int64_t count, int num_sms, cudaStream_t stream) {
     if (count == 0) return cudaSuccess;
     const int64_t words = heavy_table_words(0, args.bcols);
-    k_heavy_prep<<<1, 1024, 0, stream>>>(args, s, first, count);
+    k_heavy_prep<<<1, 256, 0, stream>>>(args, s, first, count);
+    k_heavy_entries<<<static_cast<unsigned>(count), 256, 0, stream>>>(args, s, first);
     const unsigned g = static_cast<unsigned>(num_sms) * 8;
     k_heavy<false><<<g, kHeavyBlock, 0, stream>>>(args, s, first, count, words);
     k_heavy<true><<<g, kHeavyBlock, 0, stream>>>(args, s, first, count, words);
