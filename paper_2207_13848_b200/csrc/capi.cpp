@@ -131,6 +131,8 @@ struct DBuf {
 struct spnnz_gpu_ctx {
     int device = 0, rank = 0, world = 1, num_sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t side[3] = {};            // symbolic tiers run concurrently
+    cudaEvent_t fork = nullptr, join[3] = {};
     ncclComm_t comm = nullptr;
 
     // matrices
@@ -151,6 +153,7 @@ struct spnnz_gpu_ctx {
 
     // scratch
     DBuf<int32_t> tile_x;
+    DBuf<int32_t> deg;  // int32 row lengths of B (rebuilt every FLOP pass)
     DBuf<long long> tile_carry, tile_total, tile_max;
     DBuf<long long> totals;
     long long* h_totals = nullptr;  // pinned mirror
@@ -288,15 +291,23 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     CU(cudaMemsetAsync(c->heavy_meta.p, 0, sizeof(long long) * 4, c->stream));
     if (n_items == 0) return SPNNZ_OK;
     CU(launch_sym_bin(g, s, c->stream));
-    CU(launch_sym_tiers(g, s, c->num_sms, c->stream));
-    *launches += 5;
+    // fork the tier kernels onto side streams, join before the heavy tier
+    CU(cudaEventRecord(c->fork, c->stream));
+    for (int i = 0; i < 3; ++i) CU(cudaStreamWaitEvent(c->side[i], c->fork, 0));
+    const cudaStream_t tier_streams[4] = {c->stream, c->side[0], c->side[1], c->side[2]};
+    CU(launch_sym_tiers(g, s, c->num_sms, tier_streams));
+    for (int i = 0; i < 3; ++i) {
+        CU(cudaEventRecord(c->join[i], c->side[i]));
+        CU(cudaStreamWaitEvent(c->stream, c->join[i], 0));
+    }
+    *launches += 6;
     // Heavy rows: the host learns their number, then runs pool-sized batches.
-    CU(cudaMemcpyAsync(c->h_counts, c->counts.p, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost,
+    CU(cudaMemcpyAsync(c->h_counts, c->counts.p, sizeof(int32_t) * 16, cudaMemcpyDeviceToHost,
                        c->stream));
     CU(cudaMemcpyAsync(c->h_meta, c->heavy_meta.p, sizeof(long long) * 4, cudaMemcpyDeviceToHost,
                        c->stream));
     CU(cudaStreamSynchronize(c->stream));
-    const int64_t heavy = c->h_counts[5];
+    const int64_t heavy = c->h_counts[kHeavyBin];
     if (heavy > 0) {
         // per-entry prefix arrays for the heavy rows (sum of lengths + 1 each)
         const int64_t ents = c->h_meta[1];
@@ -325,10 +336,12 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches) {
     RC(c->tile_carry.ensure(tiles + 1));
     RC(c->tile_total.ensure(tiles + 1));
     RC(c->tile_max.ensure(tiles + 1));
+    RC(c->deg.ensure(std::max<int64_t>(c->b_rows, 1)));
     FlopScratch s{c->tile_x.p, c->tile_carry.p, c->tile_total.p, c->tile_max.p};
+    CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, c->stream));
     CU(launch_flop_partition(a, s, c->stream));
-    CU(launch_flop(a, c->b_rpt.p, s, c->flop.p, c->totals.p, c->stream));
-    *launches += a.rows ? 3 : 0;
+    CU(launch_flop(a, c->deg.p, s, c->flop.p, c->totals.p, c->stream));
+    *launches += a.rows ? 4 : 0;
     return SPNNZ_OK;
 }
 
@@ -461,6 +474,11 @@ int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_counts, sizeof(int32_t) * 16);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_meta, sizeof(long long) * 4);
     for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+    for (int i = 0; i < 3 && e == cudaSuccess; ++i)
+        e = cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+    for (int i = 0; i < 3 && e == cudaSuccess; ++i)
+        e = cudaEventCreateWithFlags(&c->join[i], cudaEventDisableTiming);
     int rc = SPNNZ_OK;
     if (e != cudaSuccess) rc = set_err(SPNNZ_ECUDA, "create: %s", cudaGetErrorString(e));
     if (rc == SPNNZ_OK) rc = c->totals.ensure(kTotals);
@@ -495,7 +513,7 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     for (auto* b : {&c->b_rpt, &c->a_rpt, &c->flop, &c->out64, &c->heavy_unit_off,
                     &c->heavy_eoff, &c->heavy_epre, &c->heavy_eb0})
         b->release();
-    for (auto* b : {&c->b_col, &c->a_col, &c->tile_x, &c->counts, &c->lists,
+    for (auto* b : {&c->b_col, &c->a_col, &c->tile_x, &c->deg, &c->counts, &c->lists,
                     &c->samples, &c->rows_in, &c->bad})
         b->release();
     for (auto* b : {&c->tile_carry, &c->tile_total, &c->tile_max, &c->totals, &c->heavy_meta})
@@ -507,6 +525,11 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     if (c->h_meta) cudaFreeHost(c->h_meta);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    for (int i = 0; i < 3; ++i) {
+        if (c->side[i]) cudaStreamDestroy(c->side[i]);
+        if (c->join[i]) cudaEventDestroy(c->join[i]);
+    }
+    if (c->fork) cudaEventDestroy(c->fork);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return SPNNZ_OK;

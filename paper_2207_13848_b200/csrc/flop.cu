@@ -6,16 +6,20 @@
 // nonzeros (Merrill & Garland, merge-based SpMV).  Each 256-thread block owns
 // a tile of exactly 2048 items, so R-MAT hub rows (40 K nonzeros) and runs of
 // empty rows balance perfectly.  Per tile:
-//   1. coalesced loads of A.col for the tile's nonzeros, and for each one the
-//      gather B.rpt[k+1] - B.rpt[k] (all 8 per thread issued back to back),
-//      staged in shared memory;
+//   0. (once per call) k_degree turns B.rpt into an int32 row-length array
+//      (4 B per B row: 67 MB at config 5, L2-resident under an evict_last
+//      policy, where the int64 pair B.rpt[k], B.rpt[k+1] (134 MB) is not);
+//   1. coalesced, evict_first loads of A.col for the tile's nonzeros, and
+//      for each one the gather deg[A.col[j]] (all 8 per thread issued back to
+//      back), staged in shared memory;
 //   2. every thread walks its 8 merge-path items out of shared memory;
 //      per-row partials meet in a shared int64 accumulator;
 //   3. rows that end in the tile are written once (coalesced); the partial
 //      sum of the row still open at the tile's end is carried out and added by
 //      k_flop_fixup, which also reduces F and the row maximum.
 // Algorithmic bytes per launch: 8(M+1) A.rpt + 4 nnz A.col + 8(K+1) B.rpt
-// (gathered, L2-resident) + 8M flop written.  Integer-only: bit-exact.
+// + 8M flop written (the degree array's 4K write + re-reads are extra
+// traffic, counted against us).  Integer-only: bit-exact.
 #include "device_common.cuh"
 #include "kernels.h"
 
@@ -39,6 +43,16 @@ __device__ __forceinline__ int64_t merge_search(int64_t d, int64_t a_len, int64_
     return lo;
 }
 
+__global__ void k_degree(const int64_t* __restrict__ brpt, int64_t k_rows, int32_t* __restrict__ deg) {
+    const uint64_t first = policy_evict_first(), last = policy_evict_last();
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < k_rows;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        const long long lo = ld_stream_i64(reinterpret_cast<const long long*>(brpt) + k, first);
+        const long long hi = ld_stream_i64(reinterpret_cast<const long long*>(brpt) + k + 1, first);
+        st_keep_i32(deg + k, static_cast<int32_t>(hi - lo), last);
+    }
+}
+
 __global__ void k_flop_partition(const int64_t* __restrict__ arpt, int32_t m, int64_t nnz,
                                  int64_t tiles, int32_t* __restrict__ tile_x) {
     const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -50,19 +64,25 @@ __global__ void k_flop_partition(const int64_t* __restrict__ arpt, int32_t m, in
         merge_search(d, m, nnz, [&](int64_t i) { return __ldg(&arpt[i + 1]) - base; }));
 }
 
+// Shared-memory index with one pad word per 32: the merge-path walk reads
+// item 8t+k in thread t, which would otherwise be an 8-way bank conflict.
+__device__ __forceinline__ int pad(int i) { return i + (i >> 5); }
+
 template <int BLOCK, int IPT>
 __global__ void __launch_bounds__(BLOCK)
 k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
-       const int64_t* __restrict__ brpt, int32_t m, int64_t nnz,
+       const int32_t* __restrict__ bdeg, int32_t m, int64_t nnz,
        const int32_t* __restrict__ tile_x, int64_t* __restrict__ flop,
        long long* __restrict__ tile_carry, long long* __restrict__ tile_total,
        long long* __restrict__ tile_max) {
     constexpr int TILE = BLOCK * IPT;
-    __shared__ int32_t s_end[TILE];
-    __shared__ int32_t s_deg[TILE];
+    constexpr int PADDED = TILE + TILE / 32 + 1;
+    __shared__ int32_t s_end[PADDED];
+    __shared__ int32_t s_deg[PADDED];
     __shared__ unsigned long long s_acc[TILE + 1];
     __shared__ long long s_red[BLOCK / 32];
 
+    const uint64_t first = policy_evict_first(), last = policy_evict_last();
     const int64_t t = blockIdx.x;
     const int64_t base = __ldg(&arpt[0]);
     const int64_t total_items = int64_t(m) + nnz;
@@ -75,32 +95,28 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
     const int tid = threadIdx.x;
 
     for (int i = tid; i < nrows; i += BLOCK)
-        s_end[i] = static_cast<int32_t>(__ldg(&arpt[x0 + i + 1]) - base - y0);
+        s_end[pad(i)] = static_cast<int32_t>(
+            ld_stream_i64(reinterpret_cast<const long long*>(arpt) + x0 + i + 1, first) - base - y0);
     for (int i = tid; i <= nrows; i += BLOCK) s_acc[i] = 0;
 
-    // Column loads (coalesced) then all degree gathers in flight at once.
+    // Column loads (coalesced, evict_first) then all degree gathers in flight.
     const int32_t* tcol = acol + base + y0;
     int32_t c[IPT];
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
         const int i = tid + k * BLOCK;
-        c[k] = i < nz ? __ldg(&tcol[i]) : 0;
+        c[k] = i < nz ? ld_stream_i32(tcol + i, first) : 0;
     }
-    long long lo[IPT], hi[IPT];
+    int32_t dg[IPT];
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
         const int i = tid + k * BLOCK;
-        if (i < nz) {
-            lo[k] = __ldg(&brpt[c[k]]);
-            hi[k] = __ldg(&brpt[c[k] + 1]);
-        } else {
-            lo[k] = hi[k] = 0;
-        }
+        dg[k] = i < nz ? ld_keep_i32(bdeg + c[k], last) : 0;
     }
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
         const int i = tid + k * BLOCK;
-        if (i < nz) s_deg[i] = static_cast<int32_t>(hi[k] - lo[k]);
+        if (i < nz) s_deg[pad(i)] = dg[k];
     }
     __syncthreads();
 
@@ -108,16 +124,17 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
     const int items = nrows + nz;
     const int td = tid * IPT < items ? tid * IPT : items;
     const int tend = td + IPT < items ? td + IPT : items;
-    int x = static_cast<int>(merge_search(td, nrows, nz, [&](int64_t i) { return (int64_t)s_end[i]; }));
+    int x = static_cast<int>(
+        merge_search(td, nrows, nz, [&](int64_t i) { return (int64_t)s_end[pad(static_cast<int>(i))]; }));
     int y = td - x;
     long long acc = 0, tsum = 0;
     for (int k = td; k < tend; ++k) {
-        if (x < nrows && s_end[x] <= y) {
+        if (x < nrows && s_end[pad(x)] <= y) {
             if (acc) atomicAdd(&s_acc[x], static_cast<unsigned long long>(acc));
             acc = 0;
             ++x;
         } else {
-            const long long dv = s_deg[y];
+            const long long dv = s_deg[pad(y)];
             acc += dv;
             tsum += dv;
             ++y;
@@ -213,12 +230,21 @@ cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStr
     return cudaGetLastError();
 }
 
-cudaError_t launch_flop(const DevCsr& a, const int64_t* brpt, const FlopScratch& s, int64_t* flop,
+cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, int32_t* deg, int num_sms,
+                          cudaStream_t stream) {
+    if (k_rows == 0) return cudaSuccess;
+    int64_t grid = (k_rows + 255) / 256;
+    if (grid > int64_t(num_sms) * 16) grid = int64_t(num_sms) * 16;
+    k_degree<<<static_cast<unsigned>(grid), 256, 0, stream>>>(brpt, k_rows, deg);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flop(const DevCsr& a, const int32_t* bdeg, const FlopScratch& s, int64_t* flop,
                         long long* totals, cudaStream_t stream) {
     const int64_t tiles = flop_tiles(a);
     if (tiles == 0) return cudaSuccess;
     k_flop<kFlopBlock, kFlopIpt><<<static_cast<unsigned>(tiles), kFlopBlock, 0, stream>>>(
-        a.rpt, a.col, brpt, a.rows, a.nnz, s.tile_x, flop, s.tile_carry, s.tile_total, s.tile_max);
+        a.rpt, a.col, bdeg, a.rows, a.nnz, s.tile_x, flop, s.tile_carry, s.tile_total, s.tile_max);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     constexpr int FB = 256;

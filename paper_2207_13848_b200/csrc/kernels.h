@@ -49,7 +49,11 @@ struct FlopScratch {
 };
 
 cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStream_t stream);
-cudaError_t launch_flop(const DevCsr& a, const int64_t* brpt, const FlopScratch& s, int64_t* flop,
+// deg[k] = B.rpt[k+1] - B.rpt[k] as int32 (a B row has at most B.cols < 2^31
+// entries), written with an L2 evict_last policy for the gathers.
+cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, int32_t* deg, int num_sms,
+                          cudaStream_t stream);
+cudaError_t launch_flop(const DevCsr& a, const int32_t* bdeg, const FlopScratch& s, int64_t* flop,
                         long long* totals, cudaStream_t stream);
 
 // -------------------------------------------------------------- sampler
@@ -60,13 +64,16 @@ cudaError_t launch_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* r
 // Items are either an explicit list of GLOBAL row ids (sampled mode) or all
 // local rows (exact mode, rows == nullptr).  Items whose row is outside the
 // shard [row_lo, row_lo + a.rows) get 0.  Rows are binned by FLOP:
-constexpr int kNumBins = 6;
+constexpr int kNumBins = 7;
 constexpr int64_t kBin1Max = 32;     // warp, __match_any_sync dedup
 constexpr int64_t kBin2Max = 512;    // warp, 1024-slot smem hash per warp
-constexpr int64_t kBin3Max = 4096;   // 256-thread block, 8192-slot smem hash
-constexpr int64_t kBin4Max = 32768;  // 512-thread block, 53248-slot smem hash
-// bin 5: heavy rows, split into units of kHeavyUnitProducts products, many
-//        blocks per row over a global-memory bitmap of B.cols bits.
+constexpr int64_t kBin3Max = 2048;   // 256-thread block, 4096-slot smem hash
+constexpr int64_t kBin4Max = 8192;   // 512-thread block, 16384-slot smem hash
+constexpr int64_t kBin5Max = 32768;  // 512-thread block, 53248-slot smem hash
+constexpr int kHeavyBin = 6;         // heavier: units of kHeavyUnitProducts
+constexpr int kForeignBin = 7;       // row owned by another rank
+constexpr int kNoBin = 8;            // padding lane
+//        products, many blocks per row over a global bitmap of B.cols bits.
 constexpr int64_t kHeavyUnitProducts = 16384;
 
 struct SymScratch {
@@ -101,10 +108,11 @@ struct SymArgs {
 
 // Classifies items into bins (writes out[] = 0 for empty / foreign rows).
 cudaError_t launch_sym_bin(const SymArgs& args, const SymScratch& s, cudaStream_t stream);
-// Runs the smem tiers (bins 1-4) over the binned lists; grids are persistent
-// and read the counts on the device.
+// Runs the smem tiers (bins 1-5) over the binned lists; grids are persistent
+// and read the counts on the device.  streams[0..3] run concurrently (the
+// caller forks them from its stream and joins them afterwards).
 cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_sms,
-                             cudaStream_t stream);
+                             const cudaStream_t* streams);
 // Heavy tier for bin entries [first, first + count) of list 5 (host knows
 // count after a sync).  Tables come from s.pool and are cleaned afterwards.
 cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, int64_t first,

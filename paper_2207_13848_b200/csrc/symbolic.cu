@@ -6,18 +6,21 @@
 // a set cardinality, independent of the hash (proj/tests/test_symbolic.cpp:
 // 94-109), so every tier below is free to pick its own set representation.
 //
-// Rows are binned by their FLOP (the table size the reference uses):
+// Rows are binned by their FLOP f (the reference's table size):
 //   bin 1  f <= 32      one warp per row: products staged in registers,
 //                       duplicates found with __match_any_sync
 //   bin 2  f <= 512     one warp per row, 1024-slot shared-memory hash
-//   bin 3  f <= 4096    256-thread block, 8192-slot shared-memory hash
-//   bin 4  f <= 32768   512-thread block, 53248-slot shared-memory hash
-//   bin 5  heavier      many blocks per row over a global-memory bitmap of
-//                       B.cols bits, cleaned after use by re-walking products
-// Products of a row chunk are enumerated flat: a block scan of the chunk's B
-// row lengths gives offsets, each thread takes product p and finds its entry
-// by binary search in shared memory, so consecutive threads read consecutive
-// B.col addresses (coalesced) whatever the B row lengths are.
+//   bin 3  f <= 2048    256-thread block, 4096-slot shared-memory hash
+//   bin 4  f <= 8192    512-thread block, 16384-slot shared-memory hash
+//   bin 5  f <= 32768   512-thread block, 53248-slot shared-memory hash
+//   bin 6  heavier      products split into 16 K-product units over the whole
+//                       GPU, global-memory bitmap of B.cols bits per row,
+//                       cleaned after use by re-walking the products
+// Products are enumerated per chunk of entries: a scan of the chunk's B row
+// lengths gives product offsets; each warp takes a contiguous slice of the
+// chunk's products and its lanes walk them 32 apart with a monotone entry
+// cursor, so a warp's loads of B.col are consecutive (coalesced) whatever the
+// B row lengths, and each product costs ~1 shared-memory probe to locate.
 #include <cub/block/block_scan.cuh>
 
 #include "device_common.cuh"
@@ -70,6 +73,34 @@ __device__ __forceinline__ ItemRow item_row(const SymArgs& g, int32_t s) {
     return it;
 }
 
+// Walks products [q0, q1) of a chunk of n entries with exclusive offsets
+// off[0..n] (off[n] = chunk end) and B-row starts b0[0..n).  WARPS warps
+// share the range; fn(key) runs once per product.
+template <int WARPS, typename OffT, typename Fn>
+__device__ __forceinline__ void chunk_products(const OffT* off, const int64_t* b0, int n,
+                                               long long q0, long long q1,
+                                               const int32_t* __restrict__ bcol, Fn&& fn) {
+    const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) % WARPS;
+    const long long span = q1 - q0;
+    if (span <= 0 || n <= 0) return;
+    long long per = (span + WARPS - 1) / WARPS;
+    per = (per + 31) & ~31LL;
+    const long long ws = q0 + w * per;
+    const long long we = ws + per < q1 ? ws + per : q1;
+    long long p = ws + lane;
+    if (p >= we) return;
+    int lo = 0, hi = n - 1;  // largest e with off[e] <= p
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (static_cast<long long>(off[mid]) <= p) lo = mid; else hi = mid - 1;
+    }
+    int e = lo;
+    for (; p < we; p += 32) {
+        while (static_cast<long long>(off[e + 1]) <= p) ++e;
+        fn(__ldg(&bcol[b0[e] + (p - static_cast<long long>(off[e]))]));
+    }
+}
+
 // ------------------------------------------------------------- binning
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_sym_bin(SymArgs g, SymScratch sc) {
@@ -79,7 +110,8 @@ __global__ void __launch_bounds__(BLOCK) k_sym_bin(SymArgs g, SymScratch sc) {
     const int64_t stride = int64_t(gridDim.x) * BLOCK;
     for (int64_t base = int64_t(blockIdx.x) * BLOCK; base < g.n_items; base += stride) {
         const int64_t s = base + threadIdx.x;
-        int bin = 7;  // 7: not an item of this thread
+        int bin = kNoBin;
+        long long hl = 0;
         if (s < g.n_items) {
             const int32_t rid = g.rows ? g.rows[s] : g.row_lo + static_cast<int32_t>(s);
             const int32_t r = rid - g.row_lo;
@@ -87,33 +119,29 @@ __global__ void __launch_bounds__(BLOCK) k_sym_bin(SymArgs g, SymScratch sc) {
                 const int64_t f = g.flop[r];
                 fsum += f;
                 bin = f == 0 ? 0 : f <= kBin1Max ? 1 : f <= kBin2Max ? 2 : f <= kBin3Max ? 3
-                                 : f <= kBin4Max ? 4 : 5;
+                                 : f <= kBin4Max ? 4 : f <= kBin5Max ? 5 : kHeavyBin;
+                if (bin == kHeavyBin) hl = g.a.rpt[r + 1] - g.a.rpt[r] + 1;
             } else {
-                bin = 6;  // foreign row (another rank's shard)
+                bin = kForeignBin;  // another rank's shard
             }
-            if (g.out && (bin == 0 || bin == 5 || bin == 6)) g.out[s] = 0;
-        }
-        // total entries of heavy rows (sizes the per-entry prefix arrays)
-        long long hl = 0;
-        if (bin == 5) {
-            const int32_t r = (g.rows ? g.rows[s] : g.row_lo + static_cast<int32_t>(s)) - g.row_lo;
-            hl = g.a.rpt[r + 1] - g.a.rpt[r] + 1;
-        }
-        if (__any_sync(kFull, hl != 0)) {
-            hl = warp_sum_ll(hl);
-            if (lane == 0)
-                atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[1]),
-                          static_cast<unsigned long long>(hl));
+            if (g.out && (bin == 0 || bin == kHeavyBin || bin == kForeignBin)) g.out[s] = 0;
         }
         // warp-aggregated append to the bin lists
         const unsigned peers = __match_any_sync(kFull, bin);
-        if (bin >= 1 && bin <= 5) {
+        if (bin >= 1 && bin <= kHeavyBin) {
             const int leader = __ffs(peers) - 1;
             int pos = 0;
             if (lane == leader) pos = atomicAdd(&sc.counts[bin], __popc(peers));
             pos = __shfl_sync(peers, pos, leader);
             pos += __popc(peers & ((1u << lane) - 1));
             sc.lists[int64_t(bin) * sc.capacity + pos] = static_cast<int32_t>(s);
+        }
+        // total entries (+1 each) of heavy rows: sizes the per-entry arrays
+        if (__any_sync(kFull, hl != 0)) {
+            hl = warp_sum_ll(hl);
+            if (lane == 0)
+                atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[1]),
+                          static_cast<unsigned long long>(hl));
         }
     }
     if (g.sampled_flop) {
@@ -195,20 +223,13 @@ __global__ void __launch_bounds__(BLOCK) k_sym_warp_hash(SymArgs g, SymScratch s
                 d = static_cast<int>(__ldg(&g.brpt[c + 1]) - b0);
             }
             const int incl = warp_incl_scan(d);
+            const int nent = static_cast<int>(it.a1 - e0 < 32 ? it.a1 - e0 : 32);
             off[lane] = incl - d;
             b0s[lane] = b0;
-            if (lane == 31) off[32] = incl;
+            if (lane == nent - 1) off[nent] = incl;
             __syncwarp();
-            const int P = off[32];
-            for (int p = lane; p < P; p += 32) {
-                int lo = 0, hi = 31;  // largest j with off[j] <= p
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (off[mid] <= p) lo = mid; else hi = mid - 1;
-                }
-                const int key = __ldg(&g.bcol[b0s[lo] + (p - off[lo])]);
-                cnt += hash_insert(table, kSlots, key);
-            }
+            chunk_products<1>(off, b0s, nent, 0, off[nent], g.bcol,
+                              [&](int key) { cnt += hash_insert(table, kSlots, key); });
             __syncwarp();
         }
         cnt = static_cast<int>(warp_sum_ll(cnt));
@@ -223,48 +244,13 @@ __global__ void __launch_bounds__(BLOCK) k_sym_warp_hash(SymArgs g, SymScratch s
                   static_cast<unsigned long long>(acc));
 }
 
-// Block-cooperative enumeration of the products of entries [e_begin, e_end)
-// of one A row, in chunks of BLOCK entries; fn(key) is called once per
-// product by some thread.  Requires all threads of the block.
-template <int BLOCK, typename Fn>
-__device__ __forceinline__ void block_products(const SymArgs& g, int64_t e_begin, int64_t e_end,
-                                               int* s_off /*BLOCK+1*/, int64_t* s_b0 /*BLOCK*/,
-                                               Fn&& fn) {
-    using Scan = cub::BlockScan<int, BLOCK>;
-    __shared__ typename Scan::TempStorage scan_tmp;
-    for (int64_t c0 = e_begin; c0 < e_end; c0 += BLOCK) {
-        const int64_t e = c0 + threadIdx.x;
-        int d = 0;
-        int64_t b0 = 0;
-        if (e < e_end) {
-            const int c = __ldg(&g.a.col[e]);
-            b0 = __ldg(&g.brpt[c]);
-            d = static_cast<int>(__ldg(&g.brpt[c + 1]) - b0);
-        }
-        int excl, total;
-        Scan(scan_tmp).ExclusiveSum(d, excl, total);
-        s_off[threadIdx.x] = excl;
-        s_b0[threadIdx.x] = b0;
-        if (threadIdx.x == 0) s_off[BLOCK] = total;
-        __syncthreads();
-        const int nent = static_cast<int>(e_end - c0 < BLOCK ? e_end - c0 : BLOCK);
-        for (int p = threadIdx.x; p < total; p += BLOCK) {
-            int lo = 0, hi = nent - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (s_off[mid] <= p) lo = mid; else hi = mid - 1;
-            }
-            fn(__ldg(&g.bcol[s_b0[lo] + (p - s_off[lo])]));
-        }
-        __syncthreads();
-    }
-}
-
-// ------------------------------ bins 3, 4: block + shared-memory hash
+// ------------------------------ bins 3-5: block + shared-memory hash
 template <int BLOCK, int SLOTS, int BIN>
 __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch sc) {
     extern __shared__ int4 s_dyn[];
     int* table = reinterpret_cast<int*>(s_dyn);
+    using Scan = cub::BlockScan<int, BLOCK>;
+    __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ int s_off[BLOCK + 1];
     __shared__ int64_t s_b0[BLOCK];
     __shared__ long long s_red[BLOCK / 32];
@@ -274,10 +260,27 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
         const ItemRow it = item_row(g, list[i]);
         for (int k = threadIdx.x; k < SLOTS; k += BLOCK) table[k] = kEmpty;
-        __syncthreads();
         int cnt = 0;
-        block_products<BLOCK>(g, it.a0, it.a1, s_off, s_b0,
-                              [&](int key) { cnt += hash_insert(table, SLOTS, key); });
+        for (int64_t c0 = it.a0; c0 < it.a1; c0 += BLOCK) {
+            const int64_t e = c0 + threadIdx.x;
+            int d = 0;
+            int64_t b0 = 0;
+            if (e < it.a1) {
+                const int c = __ldg(&g.a.col[e]);
+                b0 = __ldg(&g.brpt[c]);
+                d = static_cast<int>(__ldg(&g.brpt[c + 1]) - b0);
+            }
+            int excl, total;
+            Scan(scan_tmp).ExclusiveSum(d, excl, total);
+            const int nent = static_cast<int>(it.a1 - c0 < BLOCK ? it.a1 - c0 : BLOCK);
+            s_off[threadIdx.x] = excl;
+            s_b0[threadIdx.x] = b0;
+            if (threadIdx.x == 0) s_off[nent] = total;
+            __syncthreads();  // also orders the table fill before the inserts
+            chunk_products<BLOCK / 32>(s_off, s_b0, nent, 0, total, g.bcol,
+                                       [&](int key) { cnt += hash_insert(table, SLOTS, key); });
+            __syncthreads();
+        }
         const long long tot = block_sum_ll<BLOCK>(cnt, s_red);
         if (threadIdx.x == 0) {
             if (g.out) g.out[it.s] = tot;
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
                   static_cast<unsigned long long>(acc));
 }
 
-// ------------------------------------------------ bin 5: heavy rows
+// ------------------------------------------------ bin 6: heavy rows
 // A heavy row's products are split into units of kHeavyUnitProducts; one
 // block per unit (grid-stride), so hub rows whose entries point at hub B rows
 // spread over the whole GPU.  Sets are global bitmaps of B.cols bits from the
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(256) k_heavy_prep(SymArgs g, SymScratch sc, in
     __shared__ long long s_carry_u, s_carry_e;
     if (threadIdx.x == 0) s_carry_u = s_carry_e = 0;
     __syncthreads();
-    const int32_t* list = sc.lists + 5 * sc.capacity + first;
+    const int32_t* list = sc.lists + int64_t(kHeavyBin) * sc.capacity + first;
     for (int64_t b = 0; b < count; b += 256) {
         const int64_t i = b + threadIdx.x;
         long long units = 0, ents = 0;
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(256) k_heavy_entries(SymArgs g, SymScratch sc,
     __shared__ typename Scan::TempStorage tmp;
     __shared__ long long s_carry;
     const int64_t i = blockIdx.x;
-    const ItemRow it = item_row(g, sc.lists[5 * sc.capacity + first + i]);
+    const ItemRow it = item_row(g, sc.lists[int64_t(kHeavyBin) * sc.capacity + first + i]);
     int64_t* ep = sc.heavy_epre + sc.heavy_eoff[i];
     int64_t* eb = sc.heavy_eb0 + sc.heavy_eoff[i];
     const int64_t L = it.a1 - it.a0;
@@ -379,11 +382,10 @@ __global__ void __launch_bounds__(256) k_heavy_entries(SymArgs g, SymScratch sc,
 template <bool CLEAN>
 __global__ void __launch_bounds__(kHeavyBlock) k_heavy(SymArgs g, SymScratch sc, int64_t first,
                                                        int64_t count, int64_t words) {
-    __shared__ long long s_off[kHeavyBlock];
+    __shared__ long long s_off[kHeavyBlock + 1];
     __shared__ int64_t s_b0[kHeavyBlock];
-    __shared__ long long s_end;
     __shared__ long long s_red[kHeavyBlock / 32];
-    const int32_t* list = sc.lists + 5 * sc.capacity + first;
+    const int32_t* list = sc.lists + int64_t(kHeavyBin) * sc.capacity + first;
     const long long units = sc.heavy_meta[0];
     long long acc = 0;
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
@@ -413,17 +415,11 @@ __global__ void __launch_bounds__(kHeavyBlock) k_heavy(SymArgs g, SymScratch sc,
                 s_off[threadIdx.x] = ep[e + threadIdx.x];
                 s_b0[threadIdx.x] = eb[e + threadIdx.x];
             }
-            if (threadIdx.x == 0) s_end = ep[e + n];
+            if (threadIdx.x == 0) s_off[n] = ep[e + n];
             __syncthreads();
             const long long q0 = p0 > s_off[0] ? p0 : s_off[0];
-            const long long q1 = p1 < s_end ? p1 : s_end;
-            for (long long p = q0 + threadIdx.x; p < q1; p += kHeavyBlock) {
-                int jl = 0, jh = n - 1;
-                while (jl < jh) {
-                    const int mid = (jl + jh + 1) >> 1;
-                    if (s_off[mid] <= p) jl = mid; else jh = mid - 1;
-                }
-                const int key = __ldg(&g.bcol[s_b0[jl] + (p - s_off[jl])]);
+            const long long q1 = p1 < s_off[n] ? p1 : s_off[n];
+            chunk_products<kHeavyBlock / 32>(s_off, s_b0, n, q0, q1, g.bcol, [&](int key) {
                 uint32_t* w = bm + (static_cast<uint32_t>(key) >> 5);
                 if (CLEAN) {
                     *w = 0u;
@@ -432,8 +428,8 @@ __global__ void __launch_bounds__(kHeavyBlock) k_heavy(SymArgs g, SymScratch sc,
                     if (!(*reinterpret_cast<volatile uint32_t*>(w) & bit))
                         cnt += (atomicOr(w, bit) & bit) ? 0 : 1;
                 }
-            }
-            const bool done = s_end >= p1 || e + n >= L;
+            });
+            const bool done = s_off[n] >= p1 || e + n >= L;
             __syncthreads();
             if (done) break;
             e += n;
@@ -454,8 +450,15 @@ __global__ void __launch_bounds__(kHeavyBlock) k_heavy(SymArgs g, SymScratch sc,
                   static_cast<unsigned long long>(acc));
 }
 
-constexpr int kT3Block = 256, kT3Slots = 8192;
-constexpr int kT4Block = 512, kT4Slots = 53248;
+constexpr int kT3Block = 256, kT3Slots = 4096;
+constexpr int kT4Block = 512, kT4Slots = 16384;
+constexpr int kT5Block = 512, kT5Slots = 53248;
+
+template <int BLOCK, int SLOTS, int BIN>
+void set_smem_attr() {
+    cudaFuncSetAttribute(k_sym_block_hash<BLOCK, SLOTS, BIN>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, SLOTS * 4);
+}
 
 }  // namespace
 
@@ -471,24 +474,23 @@ cudaError_t launch_sym_bin(const SymArgs& args, const SymScratch& s, cudaStream_
 }
 
 cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_sms,
-                             cudaStream_t stream) {
+                             const cudaStream_t* streams) {
     if (args.n_items == 0) return cudaSuccess;
     static unsigned attr_done = 0;  // one bit per device
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_done & (1u << (dev & 31)))) {
-        cudaFuncSetAttribute(k_sym_block_hash<kT3Block, kT3Slots, 3>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, kT3Slots * 4);
-        cudaFuncSetAttribute(k_sym_block_hash<kT4Block, kT4Slots, 4>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, kT4Slots * 4);
+        set_smem_attr<kT3Block, kT3Slots, 3>();
+        set_smem_attr<kT4Block, kT4Slots, 4>();
+        set_smem_attr<kT5Block, kT5Slots, 5>();
         attr_done |= 1u << (dev & 31);
     }
-    const unsigned g = static_cast<unsigned>(num_sms) * 4;
-    k_sym_tiny<256><<<g, 256, 0, stream>>>(args, s);
-    k_sym_warp_hash<256><<<g, 256, 0, stream>>>(args, s);
-    k_sym_block_hash<kT3Block, kT3Slots, 3><<<g, kT3Block, kT3Slots * 4, stream>>>(args, s);
-    k_sym_block_hash<kT4Block, kT4Slots, 4><<<static_cast<unsigned>(num_sms), kT4Block,
-                                              kT4Slots * 4, stream>>>(args, s);
+    const unsigned sms = static_cast<unsigned>(num_sms);
+    k_sym_tiny<256><<<sms * 4, 256, 0, streams[0]>>>(args, s);
+    k_sym_warp_hash<256><<<sms * 4, 256, 0, streams[1]>>>(args, s);
+    k_sym_block_hash<kT3Block, kT3Slots, 3><<<sms * 8, kT3Block, kT3Slots * 4, streams[2]>>>(args, s);
+    k_sym_block_hash<kT4Block, kT4Slots, 4><<<sms * 3, kT4Block, kT4Slots * 4, streams[3]>>>(args, s);
+    k_sym_block_hash<kT5Block, kT5Slots, 5><<<sms, kT5Block, kT5Slots * 4, streams[0]>>>(args, s);
     return cudaGetLastError();
 }
 

@@ -170,13 +170,16 @@ def tier_matrix(n_rows, n_cols, lens, b_lens, seed):
 
 @pytest.mark.parametrize("ncols", [3000, 1 << 20])
 def test_every_bin_vs_oracle(P, oracle, ncols):
-    """Rows whose FLOP lands in every bin (<=32, <=512, <=4096, <=32768,
-    heavy) including duplicates-heavy rows, for small and large B.cols."""
+    """Rows whose FLOP lands in every bin (<=32, <=512, <=2048, <=8192,
+    <=32768, heavy) including duplicates-heavy rows, for small and large B.cols."""
     rng = np.random.default_rng(ncols)
-    lens = [0, 1, 2, 5, 10, 40, 100, 300, 700, 1500, 2500] + list(rng.integers(0, 200, 200))
-    b_lens = list(rng.integers(0, 60, 2998)) + [2000, 2999]
+    lens = [0, 1, 2, 5, 10, 40, 100, 200, 300, 700, 1500, 2500] + list(rng.integers(0, 200, 200))
+    b_lens = [1, 2, 3, 1, 2, 3, 1, 2, 3, 4] + list(rng.integers(0, 60, 2988)) + [2000, 2999]
     nc = 3000
     a, b = tier_matrix(len(lens), nc, lens, b_lens, 1)
+    # rows whose products stay <= 32 (bin 1): entries pointing at B rows 0-9
+    extra = [[0], [1, 2], [3, 4, 5], list(range(10))]
+    a = csr(a.rows + len(extra), nc, [a.col[a.rpt[i]:a.rpt[i + 1]].tolist() for i in range(a.rows)] + extra)
     # widen B's column space so the bitmap tier sees ncols bits
     b = csr(b.rows, ncols, [list((np.array(b.col[b.rpt[i]:b.rpt[i + 1]]) * (ncols // nc)).tolist())
                            for i in range(b.rows)])
@@ -185,8 +188,8 @@ def test_every_bin_vs_oracle(P, oracle, ncols):
     f, F, mx = oracle.compute_flop(a, b)
     nnz, Z = oracle.exact_symbolic(a, b, f, mx)
     assert (prof.flop_per_row == f).all()
-    bins = np.digitize(f, [1, 33, 513, 4097, 32769])
-    assert set(bins.tolist()) >= {0, 1, 2, 3, 4, 5}, "matrix must exercise every bin"
+    bins = np.digitize(f, [1, 33, 513, 2049, 8193, 32769])
+    assert set(bins.tolist()) >= {0, 1, 2, 3, 4, 5, 6}, "matrix must exercise every bin"
     assert (ex.nnz_per_row == nnz).all() and ex.total_nnz == Z
     rows = np.arange(a.rows, dtype=np.int32)[::-1].copy()
     s = P.sampled_symbolic(rows)
