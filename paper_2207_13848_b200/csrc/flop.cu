@@ -12,14 +12,18 @@
 //   1. coalesced, evict_first loads of A.col for the tile's nonzeros, and
 //      for each one the gather deg[A.col[j]] (all 8 per thread issued back to
 //      back), staged in shared memory;
-//   2. every thread walks its 8 merge-path items out of shared memory;
-//      per-row partials meet in a shared int64 accumulator;
+//   2. every thread walks its 8 merge-path items out of shared memory; a
+//      block-wide segmented scan over (row, partial) pairs joins rows that
+//      cross thread boundaries (no shared-memory atomics: 64-bit ATOMS is a
+//      CAS loop on sm_100 and serialises on hub rows);
 //   3. rows that end in the tile are written once (coalesced); the partial
 //      sum of the row still open at the tile's end is carried out and added by
 //      k_flop_fixup, which also reduces F and the row maximum.
 // Algorithmic bytes per launch: 8(M+1) A.rpt + 4 nnz A.col + 8(K+1) B.rpt
 // + 8M flop written (the degree array's 4K write + re-reads are extra
 // traffic, counted against us).  Integer-only: bit-exact.
+#include <cub/block/block_scan.cuh>
+
 #include "device_common.cuh"
 #include "kernels.h"
 
@@ -64,6 +68,17 @@ __global__ void k_flop_partition(const int64_t* __restrict__ arpt, int32_t m, in
         merge_search(d, m, nnz, [&](int64_t i) { return __ldg(&arpt[i + 1]) - base; }));
 }
 
+// (row, partial sum) pairs for the block-wide reduce-by-row of carries.
+struct RowCarry {
+    int row;
+    long long val;
+};
+struct RowCarryOp {
+    __device__ __forceinline__ RowCarry operator()(const RowCarry& a, const RowCarry& b) const {
+        return RowCarry{b.row, a.row == b.row ? a.val + b.val : b.val};
+    }
+};
+
 // Shared-memory index with one pad word per 32: the merge-path walk reads
 // item 8t+k in thread t, which would otherwise be an 8-way bank conflict.
 __device__ __forceinline__ int pad(int i) { return i + (i >> 5); }
@@ -81,6 +96,8 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
     __shared__ int32_t s_deg[PADDED];
     __shared__ unsigned long long s_acc[TILE + 1];
     __shared__ long long s_red[BLOCK / 32];
+    using BlockCarryScan = cub::BlockScan<RowCarry, BLOCK>;
+    __shared__ typename BlockCarryScan::TempStorage s_scan;
 
     const uint64_t first = policy_evict_first(), last = policy_evict_last();
     const int64_t t = blockIdx.x;
@@ -97,7 +114,6 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
     for (int i = tid; i < nrows; i += BLOCK)
         s_end[pad(i)] = static_cast<int32_t>(
             ld_stream_i64(reinterpret_cast<const long long*>(arpt) + x0 + i + 1, first) - base - y0);
-    for (int i = tid; i <= nrows; i += BLOCK) s_acc[i] = 0;
 
     // Column loads (coalesced, evict_first) then all degree gathers in flight.
     const int32_t* tcol = acol + base + y0;
@@ -120,17 +136,27 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
     }
     __syncthreads();
 
-    // Walk this thread's IPT merge-path items.
+    // Walk this thread's IPT merge-path items.  Rows ending inside the
+    // thread's range after its first row-end are complete; the first one may
+    // owe a carry from preceding threads, and the row still open at the end
+    // is this thread's carry-out.  A block-wide segmented scan of the
+    // (row, carry) pairs resolves both without shared-memory atomics.
     const int items = nrows + nz;
     const int td = tid * IPT < items ? tid * IPT : items;
     const int tend = td + IPT < items ? td + IPT : items;
     int x = static_cast<int>(
         merge_search(td, nrows, nz, [&](int64_t i) { return (int64_t)s_end[pad(static_cast<int>(i))]; }));
     int y = td - x;
-    long long acc = 0, tsum = 0;
+    long long acc = 0, tsum = 0, first_val = 0;
+    int first_row = -1;
     for (int k = td; k < tend; ++k) {
         if (x < nrows && s_end[pad(x)] <= y) {
-            if (acc) atomicAdd(&s_acc[x], static_cast<unsigned long long>(acc));
+            if (first_row < 0) {
+                first_row = x;
+                first_val = acc;
+            } else {
+                s_acc[x] = static_cast<unsigned long long>(acc);
+            }
             acc = 0;
             ++x;
         } else {
@@ -140,7 +166,16 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
             ++y;
         }
     }
-    if (acc) atomicAdd(&s_acc[x], static_cast<unsigned long long>(acc));
+    RowCarry mine{x, acc}, before;
+    BlockCarryScan(s_scan).ExclusiveScan(mine, before, RowCarry{-1, 0}, RowCarryOp());
+    if (first_row >= 0)
+        s_acc[first_row] = static_cast<unsigned long long>(
+            first_val + (before.row == first_row ? before.val : 0));
+    if (tid == BLOCK - 1) {
+        // carry-out of the tile: the open row's partial over the whole tile
+        const RowCarry tot = RowCarryOp()(before, mine);
+        s_acc[nrows] = static_cast<unsigned long long>(tot.row == nrows ? tot.val : 0);
+    }
     __syncthreads();
 
     // Rows x0 .. x1-1 end in this tile.  Row x0 may have started in an

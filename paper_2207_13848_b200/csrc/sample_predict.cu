@@ -32,10 +32,15 @@ __global__ void k_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* __
     rows[r] = rid;
 }
 
+// (int64)ceil(q) exactly as the reference's x86-64 build evaluates it: a
+// quotient >= 2^63 (only for cr < 1 and huge rows) converts to the "integer
+// indefinite" value INT64_MIN (cvttsd2si), where the GPU's cvt would saturate.
 __device__ __forceinline__ long long ceil_view(long long f, double cr, double* q_out) {
     const double q = __ddiv_rn(static_cast<double>(f), cr);
     *q_out = q;
-    const long long c = static_cast<long long>(ceil(q));
+    const double cq = ceil(q);
+    const long long c = cq >= 9223372036854775808.0 ? static_cast<long long>(0x8000000000000000ULL)
+                                                    : static_cast<long long>(cq);
     return f < c ? f : c;
 }
 
