@@ -153,7 +153,7 @@ struct spnnz_gpu_ctx {
 
     // scratch
     DBuf<int32_t> tile_x;
-    DBuf<int32_t> deg;  // int32 row lengths of B (rebuilt every FLOP pass)
+    DBuf<uint16_t> deg;  // uint16 row lengths of B (rebuilt every FLOP pass)
     DBuf<long long> tile_carry, tile_total, tile_max;
     DBuf<long long> totals;
     long long* h_totals = nullptr;  // pinned mirror
@@ -340,7 +340,7 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches) {
     FlopScratch s{c->tile_x.p, c->tile_carry.p, c->tile_total.p, c->tile_max.p};
     CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, c->stream));
     CU(launch_flop_partition(a, s, c->stream));
-    CU(launch_flop(a, c->deg.p, s, c->flop.p, c->totals.p, c->stream));
+    CU(launch_flop(a, c->deg.p, c->b_rpt.p, s, c->flop.p, c->totals.p, c->stream));
     *launches += a.rows ? 4 : 0;
     return SPNNZ_OK;
 }
@@ -513,7 +513,8 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     for (auto* b : {&c->b_rpt, &c->a_rpt, &c->flop, &c->out64, &c->heavy_unit_off,
                     &c->heavy_eoff, &c->heavy_epre, &c->heavy_eb0})
         b->release();
-    for (auto* b : {&c->b_col, &c->a_col, &c->tile_x, &c->deg, &c->counts, &c->lists,
+    c->deg.release();
+    for (auto* b : {&c->b_col, &c->a_col, &c->tile_x, &c->counts, &c->lists,
                     &c->samples, &c->rows_in, &c->bad})
         b->release();
     for (auto* b : {&c->tile_carry, &c->tile_total, &c->tile_max, &c->totals, &c->heavy_meta})
@@ -619,6 +620,7 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
     v.cols = a->cols;
     const int64_t a_lo = arpt_h[c->row_lo], a_hi = arpt_h[c->row_hi];
     v.nnz = a_hi - a_lo;
+    v.base = a_lo;
     if (same) {
         v.rpt = c->b_rpt.p + c->row_lo;
         v.col = c->b_col.p;

@@ -68,6 +68,14 @@ __device__ __forceinline__ int ld_keep_i32(const int* p, uint64_t pol) {
     asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
 }
+__device__ __forceinline__ uint16_t ld_keep_u16(const uint16_t* p, uint64_t pol) {
+    unsigned short v;
+    asm volatile("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_keep_u16(uint16_t* p, uint16_t v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.u16 [%0], %1, %2;" :: "l"(p), "h"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void st_keep_i32(int* p, int v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" :: "l"(p), "r"(v), "l"(pol) : "memory");
 }

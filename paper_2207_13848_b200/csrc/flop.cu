@@ -1,207 +1,207 @@
 // Per-row FLOP profile (Algorithm 1): flop_i = sum_{j in A_i} |B_{A.col[j]}|.
 // GPU restatement of spnnz::compute_flop (proj/include/spnnz/flop.hpp:25-60,
-// hot loop :41-50), plus sampled_flop (:64-74).
+// hot loop :41-50), plus sampled_flop (:64-74).  A pattern SpMV y = A * deg(B).
 //
-// Decomposition: merge path over the sequence of M row-ends and nnz(A)
-// nonzeros (Merrill & Garland, merge-based SpMV).  Each 256-thread block owns
-// a tile of exactly 2048 items, so R-MAT hub rows (40 K nonzeros) and runs of
-// empty rows balance perfectly.  Per tile:
-//   0. (once per call) k_degree turns B.rpt into an int32 row-length array
-//      (4 B per B row: 67 MB at config 5, L2-resident under an evict_last
-//      policy, where the int64 pair B.rpt[k], B.rpt[k+1] (134 MB) is not);
-//   1. coalesced, evict_first loads of A.col for the tile's nonzeros, and
-//      for each one the gather deg[A.col[j]] (all 8 per thread issued back to
-//      back), staged in shared memory;
-//   2. every thread walks its 8 merge-path items out of shared memory; a
-//      block-wide segmented scan over (row, partial) pairs joins rows that
-//      cross thread boundaries (no shared-memory atomics: 64-bit ATOMS is a
-//      CAS loop on sm_100 and serialises on hub rows);
-//   3. rows that end in the tile are written once (coalesced); the partial
-//      sum of the row still open at the tile's end is carried out and added by
-//      k_flop_fixup, which also reduces F and the row maximum.
-// Algorithmic bytes per launch: 8(M+1) A.rpt + 4 nnz A.col + 8(K+1) B.rpt
-// + 8M flop written (the degree array's 4K write + re-reads are extra
-// traffic, counted against us).  Integer-only: bit-exact.
-#include <cub/block/block_scan.cuh>
-
+// Decomposition ("nnz tiles"): A's nonzeros are cut into fixed tiles of
+// kFlopTile = 4096 entries aligned to absolute multiples of 4096, one
+// 256-thread block per tile, so hub rows and runs of empty rows cost the
+// same per entry.  A tile OWNS the rows that start inside it.  Per call:
+//   0. k_degree turns B.rpt into a uint16 row-length array with an escape
+//      value for rows of >= 65535 entries (2 B per B row: 34 MB at config 5,
+//      L2-resident under an evict_last policy -- the int64 pair
+//      B.rpt[k], B.rpt[k+1] is 134 MB and is not);
+//   1. k_flop_partition: first owned row of every tile (lower_bound in rpt);
+//   2. k_flop, per tile: 16-byte evict_first loads of the tile's A.col,
+//      then the deg[] gathers (16 per thread in flight), staged in shared
+//      memory; each thread then sums one owned row's slice of the staged
+//      degrees (rows longer than 64 in the tile go to a warp each), writes
+//      flop[row] and the tile's partials: F, max, and the leading segment
+//      that belongs to a row owned by an earlier tile;
+//   3. k_flop_fixup adds the leading segments to the long rows they continue
+//      and reduces F and max over tiles.
+// Per entry ~10 thread instructions (a merge-path walk cost ~90).
+// Algorithmic bytes: 8(M+1) A.rpt + 4 nnz A.col + 8(K+1) B.rpt + 8M flop
+// (the 2K-byte degree array's write and re-reads are extra traffic).
+// Integer-only: bit-exact.
 #include "device_common.cuh"
 #include "kernels.h"
 
 namespace spnnz_gpu {
 namespace {
 
-// Merge-path search over a[0..a_len) (row ends) vs the counting sequence
-// [0, b_len): returns the number of row-ends consumed at diagonal d.
-template <typename LoadEnd>
-__device__ __forceinline__ int64_t merge_search(int64_t d, int64_t a_len, int64_t b_len,
-                                                LoadEnd end_at) {
-    int64_t lo = d - b_len > 0 ? d - b_len : 0;
-    int64_t hi = d < a_len ? d : a_len;
-    while (lo < hi) {
-        const int64_t pivot = (lo + hi) >> 1;
-        if (end_at(pivot) <= d - pivot - 1)
-            lo = pivot + 1;
-        else
-            hi = pivot;
-    }
-    return lo;
-}
+constexpr int kLongRow = 64;  // in-tile row slices longer than this go to a warp
 
-__global__ void k_degree(const int64_t* __restrict__ brpt, int64_t k_rows, int32_t* __restrict__ deg) {
+// deg16[k] = min(B.rpt[k+1] - B.rpt[k], 0xFFFF); 0xFFFF means "look the
+// exact length up in B.rpt" (rows with >= 65535 entries are rare).
+__global__ void k_degree(const int64_t* __restrict__ brpt, int64_t k_rows,
+                         uint16_t* __restrict__ deg) {
     const uint64_t first = policy_evict_first(), last = policy_evict_last();
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < k_rows;
          k += int64_t(gridDim.x) * blockDim.x) {
         const long long lo = ld_stream_i64(reinterpret_cast<const long long*>(brpt) + k, first);
         const long long hi = ld_stream_i64(reinterpret_cast<const long long*>(brpt) + k + 1, first);
-        st_keep_i32(deg + k, static_cast<int32_t>(hi - lo), last);
+        const long long d = hi - lo;
+        st_keep_u16(deg + k, static_cast<uint16_t>(d < 0xFFFF ? d : 0xFFFF), last);
     }
 }
 
-__global__ void k_flop_partition(const int64_t* __restrict__ arpt, int32_t m, int64_t nnz,
-                                 int64_t tiles, int32_t* __restrict__ tile_x) {
+__device__ __forceinline__ int64_t tile_start(int64_t base, int64_t nnz, int64_t t) {
+    const int64_t s = (base / kFlopTile + t) * kFlopTile;
+    return s > base ? (s < base + nnz ? s : base + nnz) : base;
+}
+
+// tile_row[t] = first row whose start offset is >= tile_start(t); the last
+// tile also owns the trailing empty rows (tile_row[tiles] = m).
+__global__ void k_flop_partition(const int64_t* __restrict__ arpt, int32_t m, int64_t base,
+                                 int64_t nnz, int64_t tiles, int32_t* __restrict__ tile_row) {
     const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (t > tiles) return;
-    const int64_t total = int64_t(m) + nnz;
-    const int64_t d = t * kFlopTile < total ? t * kFlopTile : total;
-    const int64_t base = arpt[0];
-    tile_x[t] = static_cast<int32_t>(
-        merge_search(d, m, nnz, [&](int64_t i) { return __ldg(&arpt[i + 1]) - base; }));
+    if (t == tiles) {
+        tile_row[t] = m;
+        return;
+    }
+    const int64_t target = tile_start(base, nnz, t);
+    int64_t lo = 0, hi = m;  // lower_bound over rpt[0..m]
+    if (t == 0) hi = 0;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(&arpt[mid]) < target) lo = mid + 1; else hi = mid;
+    }
+    tile_row[t] = static_cast<int32_t>(lo);
 }
 
-// (row, partial sum) pairs for the block-wide reduce-by-row of carries.
-struct RowCarry {
-    int row;
-    long long val;
-};
-struct RowCarryOp {
-    __device__ __forceinline__ RowCarry operator()(const RowCarry& a, const RowCarry& b) const {
-        return RowCarry{b.row, a.row == b.row ? a.val + b.val : b.val};
-    }
-};
-
-// Shared-memory index with one pad word per 32: the merge-path walk reads
-// item 8t+k in thread t, which would otherwise be an 8-way bank conflict.
-__device__ __forceinline__ int pad(int i) { return i + (i >> 5); }
-
-template <int BLOCK, int IPT>
+template <int BLOCK, int V>
 __global__ void __launch_bounds__(BLOCK)
 k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
-       const int32_t* __restrict__ bdeg, int32_t m, int64_t nnz,
-       const int32_t* __restrict__ tile_x, int64_t* __restrict__ flop,
-       long long* __restrict__ tile_carry, long long* __restrict__ tile_total,
-       long long* __restrict__ tile_max) {
-    constexpr int TILE = BLOCK * IPT;
-    constexpr int PADDED = TILE + TILE / 32 + 1;
-    __shared__ int32_t s_end[PADDED];
-    __shared__ int32_t s_deg[PADDED];
-    __shared__ unsigned long long s_acc[TILE + 1];
+       const uint16_t* __restrict__ bdeg, const int64_t* __restrict__ brpt, int32_t m,
+       int64_t base, int64_t nnz, const int32_t* __restrict__ tile_row,
+       int64_t* __restrict__ flop, long long* __restrict__ tile_lead,
+       long long* __restrict__ tile_total, long long* __restrict__ tile_max) {
+    constexpr int TILE = BLOCK * V;
+    static_assert(TILE == kFlopTile, "tile size");
+    __shared__ int32_t s_deg[TILE];
+    __shared__ int32_t s_long_row[TILE / kLongRow + 2];
+    __shared__ int32_t s_long_lo[TILE / kLongRow + 2];
+    __shared__ int32_t s_long_hi[TILE / kLongRow + 2];
+    __shared__ int s_nlong;
     __shared__ long long s_red[BLOCK / 32];
-    using BlockCarryScan = cub::BlockScan<RowCarry, BLOCK>;
-    __shared__ typename BlockCarryScan::TempStorage s_scan;
 
     const uint64_t first = policy_evict_first(), last = policy_evict_last();
     const int64_t t = blockIdx.x;
-    const int64_t base = __ldg(&arpt[0]);
-    const int64_t total_items = int64_t(m) + nnz;
-    const int64_t d0 = t * TILE;
-    const int64_t d1 = d0 + TILE < total_items ? d0 + TILE : total_items;
-    const int32_t x0 = tile_x[t], x1 = tile_x[t + 1];
-    const int64_t y0 = d0 - x0, y1 = d1 - x1;
-    const int nrows = x1 - x0;
-    const int nz = static_cast<int>(y1 - y0);
+    const int64_t ts = tile_start(base, nnz, t), te = tile_start(base, nnz, t + 1);
+    const int n = static_cast<int>(te - ts);
     const int tid = threadIdx.x;
+    if (tid == 0) s_nlong = 0;
 
-    for (int i = tid; i < nrows; i += BLOCK)
-        s_end[pad(i)] = static_cast<int32_t>(
-            ld_stream_i64(reinterpret_cast<const long long*>(arpt) + x0 + i + 1, first) - base - y0);
-
-    // Column loads (coalesced, evict_first) then all degree gathers in flight.
-    const int32_t* tcol = acol + base + y0;
-    int32_t c[IPT];
+    // 1. stage the tile's degrees: 16-byte loads of A.col (the tile start is
+    //    a multiple of 4096 entries, so only the shard's first and last tiles
+    //    can be partial), then all gathers in flight.  Entry i of the tile is
+    //    k & 3 of vector (tid + (k >> 2) * BLOCK).
+    int32_t c[V];
+    const bool vec = n == TILE && (reinterpret_cast<uintptr_t>(acol + ts) & 15) == 0;
+    if (vec) {
+        const int4* src = reinterpret_cast<const int4*>(acol + ts);
 #pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-        const int i = tid + k * BLOCK;
-        c[k] = i < nz ? ld_stream_i32(tcol + i, first) : 0;
-    }
-    int32_t dg[IPT];
+        for (int k = 0; k < V / 4; ++k) {
+            const int4 q = ld_stream_v4(src + tid + k * BLOCK, first);
+            c[4 * k] = q.x;
+            c[4 * k + 1] = q.y;
+            c[4 * k + 2] = q.z;
+            c[4 * k + 3] = q.w;
+        }
+    } else {
 #pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-        const int i = tid + k * BLOCK;
-        dg[k] = i < nz ? ld_keep_i32(bdeg + c[k], last) : 0;
-    }
+        for (int k = 0; k < V / 4; ++k)
 #pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-        const int i = tid + k * BLOCK;
-        if (i < nz) s_deg[pad(i)] = dg[k];
-    }
-    __syncthreads();
-
-    // Walk this thread's IPT merge-path items.  Rows ending inside the
-    // thread's range after its first row-end are complete; the first one may
-    // owe a carry from preceding threads, and the row still open at the end
-    // is this thread's carry-out.  A block-wide segmented scan of the
-    // (row, carry) pairs resolves both without shared-memory atomics.
-    const int items = nrows + nz;
-    const int td = tid * IPT < items ? tid * IPT : items;
-    const int tend = td + IPT < items ? td + IPT : items;
-    int x = static_cast<int>(
-        merge_search(td, nrows, nz, [&](int64_t i) { return (int64_t)s_end[pad(static_cast<int>(i))]; }));
-    int y = td - x;
-    long long acc = 0, tsum = 0, first_val = 0;
-    int first_row = -1;
-    for (int k = td; k < tend; ++k) {
-        if (x < nrows && s_end[pad(x)] <= y) {
-            if (first_row < 0) {
-                first_row = x;
-                first_val = acc;
-            } else {
-                s_acc[x] = static_cast<unsigned long long>(acc);
+            for (int j = 0; j < 4; ++j) {
+                const int i = 4 * (tid + k * BLOCK) + j;
+                c[4 * k + j] = i < n ? ld_stream_i32(acol + ts + i, first) : 0;
             }
-            acc = 0;
-            ++x;
-        } else {
-            const long long dv = s_deg[pad(y)];
-            acc += dv;
-            tsum += dv;
-            ++y;
+    }
+    int32_t dg[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        const int i = 4 * (tid + (k >> 2) * BLOCK) + (k & 3);
+        dg[k] = i < n ? static_cast<int32_t>(ld_keep_u16(bdeg + c[k], last)) : 0;
+    }
+    long long tsum = 0;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        const int i = 4 * (tid + (k >> 2) * BLOCK) + (k & 3);
+        if (i < n) {
+            int32_t d = dg[k];
+            if (d == 0xFFFF) d = static_cast<int32_t>(__ldg(&brpt[c[k] + 1]) - __ldg(&brpt[c[k]]));
+            s_deg[i] = d;
+            tsum += d;
         }
     }
-    RowCarry mine{x, acc}, before;
-    BlockCarryScan(s_scan).ExclusiveScan(mine, before, RowCarry{-1, 0}, RowCarryOp());
-    if (first_row >= 0)
-        s_acc[first_row] = static_cast<unsigned long long>(
-            first_val + (before.row == first_row ? before.val : 0));
-    if (tid == BLOCK - 1) {
-        // carry-out of the tile: the open row's partial over the whole tile
-        const RowCarry tot = RowCarryOp()(before, mine);
-        s_acc[nrows] = static_cast<unsigned long long>(tot.row == nrows ? tot.val : 0);
+    __syncthreads();
+
+    // 2. owned rows [r0, r1): one thread per row, long slices deferred.
+    const int32_t r0 = tile_row[t], r1 = tile_row[t + 1];
+    long long tmax = 0;
+    for (int32_t r = r0 + tid; r < r1; r += BLOCK) {
+        const int64_t a = __ldg(&arpt[r]), b = __ldg(&arpt[r + 1]);
+        const int lo = static_cast<int>(a - ts);
+        const int hi = static_cast<int>((b < te ? b : te) - ts);
+        if (hi - lo > kLongRow) {
+            const int slot = atomicAdd(&s_nlong, 1);
+            s_long_row[slot] = r;
+            s_long_lo[slot] = lo;
+            s_long_hi[slot] = hi;
+        } else {
+            long long sum = 0;
+            for (int i = lo; i < hi; ++i) sum += s_deg[i];
+            flop[r] = sum;
+            if (b <= te) tmax = sum > tmax ? sum : tmax;  // complete within the tile
+        }
+    }
+    // the leading slice [0, lead) continues row r0 - 1 from an earlier tile
+    if (tid == 0) {
+        const int64_t first_start = r0 < m ? __ldg(&arpt[r0]) : te;
+        const int lead = static_cast<int>((first_start < te ? first_start : te) - ts);
+        if (lead > 0) {
+            const int slot = atomicAdd(&s_nlong, 1);
+            s_long_row[slot] = -1;
+            s_long_lo[slot] = 0;
+            s_long_hi[slot] = lead;
+        } else {
+            tile_lead[t] = 0;
+        }
     }
     __syncthreads();
 
-    // Rows x0 .. x1-1 end in this tile.  Row x0 may have started in an
-    // earlier tile (carry-in): its final value is known only after the fixup.
-    const bool carry_in = nrows > 0 && (__ldg(&arpt[x0]) - base) < y0;
-    long long tmax = 0;
-    for (int i = tid; i < nrows; i += BLOCK) {
-        const long long v = static_cast<long long>(s_acc[i]);
-        flop[x0 + i] = v;
-        if (!(i == 0 && carry_in)) tmax = v > tmax ? v : tmax;
+    // 3. long slices: one warp each
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int j = warp; j < s_nlong; j += BLOCK / 32) {
+        long long sum = 0;
+        for (int i = s_long_lo[j] + lane; i < s_long_hi[j]; i += 32) sum += s_deg[i];
+        sum = warp_sum_ll(sum);
+        if (lane == 0) {
+            const int32_t r = s_long_row[j];
+            if (r < 0) {
+                tile_lead[t] = sum;
+            } else {
+                flop[r] = sum;
+                if (__ldg(&arpt[r + 1]) <= te) tmax = sum > tmax ? sum : tmax;
+            }
+        }
     }
     const long long bsum = block_sum_ll<BLOCK>(tsum, s_red);
     const long long bmax = block_max_ll<BLOCK>(tmax, s_red);
     if (tid == 0) {
         tile_total[t] = bsum;
         tile_max[t] = bmax;
-        tile_carry[t] = static_cast<long long>(s_acc[nrows]);
     }
 }
 
-// Adds carried partial sums to the rows that span tiles (one thread per first
-// carrying tile of a row) and reduces F and max over all tiles.
+// Adds each tile's leading slice to the row it continues (one thread per
+// first continuing tile of a row, summing the run of tiles that continue the
+// same row) and reduces F and max over all tiles.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK)
-k_flop_fixup(const int32_t* __restrict__ tile_x, int64_t tiles, int32_t m,
-             const long long* __restrict__ tile_carry, const long long* __restrict__ tile_total,
+k_flop_fixup(const int32_t* __restrict__ tile_row, int64_t tiles,
+             const long long* __restrict__ tile_lead, const long long* __restrict__ tile_total,
              const long long* __restrict__ tile_max, int64_t* __restrict__ flop,
              long long* __restrict__ totals) {
     __shared__ long long s_red[BLOCK / 32];
@@ -210,11 +210,14 @@ k_flop_fixup(const int32_t* __restrict__ tile_x, int64_t tiles, int32_t m,
     if (t < tiles) {
         sum = tile_total[t];
         mx = tile_max[t];
-        const int32_t r = tile_x[t + 1];
-        const bool first = (r < m) && (t == 0 || tile_x[t] != r);
+        // tile t continues row r = tile_row[t] - 1 when its leading slice is
+        // non-empty; tile t is the first such tile unless tile t-1 owned no
+        // row either (tile_row[t-1] == tile_row[t]).
+        const int32_t r = tile_row[t] - 1;
+        const bool first = t > 0 && r >= 0 && tile_row[t - 1] != tile_row[t];
         if (first) {
             long long carry = 0;
-            for (int64_t u = t; u < tiles && tile_x[u + 1] == r; ++u) carry += tile_carry[u];
+            for (int64_t u = t; u < tiles && tile_row[u] == r + 1; ++u) carry += tile_lead[u];
             const long long v = flop[r] + carry;
             flop[r] = v;
             mx = v > mx ? v : mx;
@@ -255,17 +258,14 @@ __global__ void k_check_rows(const int32_t* __restrict__ rows, int64_t n, int32_
 
 }  // namespace
 
-cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStream_t stream) {
-    const int64_t tiles = flop_tiles(a);
-    if (a.rows == 0) return cudaSuccess;
-    const int block = 256;
-    const int64_t grid = (tiles + 1 + block - 1) / block;
-    k_flop_partition<<<static_cast<unsigned>(grid), block, 0, stream>>>(a.rpt, a.rows, a.nnz, tiles,
-                                                                      s.tile_x);
-    return cudaGetLastError();
+int64_t flop_tiles(const DevCsr& a) {
+    if (a.rows == 0) return 0;
+    if (a.nnz == 0) return 1;
+    const int64_t end = a.base + a.nnz;
+    return (end + kFlopTile - 1) / kFlopTile - a.base / kFlopTile;
 }
 
-cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, int32_t* deg, int num_sms,
+cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, uint16_t* deg, int num_sms,
                           cudaStream_t stream) {
     if (k_rows == 0) return cudaSuccess;
     int64_t grid = (k_rows + 255) / 256;
@@ -274,17 +274,29 @@ cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, int32_t* deg, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_flop(const DevCsr& a, const int32_t* bdeg, const FlopScratch& s, int64_t* flop,
-                        long long* totals, cudaStream_t stream) {
+cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStream_t stream) {
+    const int64_t tiles = flop_tiles(a);
+    if (tiles == 0) return cudaSuccess;
+    const int block = 256;
+    const int64_t grid = (tiles + 1 + block - 1) / block;
+    k_flop_partition<<<static_cast<unsigned>(grid), block, 0, stream>>>(a.rpt, a.rows, a.base,
+                                                                      a.nnz, tiles, s.tile_x);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flop(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt,
+                        const FlopScratch& s, int64_t* flop, long long* totals,
+                        cudaStream_t stream) {
     const int64_t tiles = flop_tiles(a);
     if (tiles == 0) return cudaSuccess;
     k_flop<kFlopBlock, kFlopIpt><<<static_cast<unsigned>(tiles), kFlopBlock, 0, stream>>>(
-        a.rpt, a.col, bdeg, a.rows, a.nnz, s.tile_x, flop, s.tile_carry, s.tile_total, s.tile_max);
+        a.rpt, a.col, bdeg, brpt, a.rows, a.base, a.nnz, s.tile_x, flop, s.tile_carry,
+        s.tile_total, s.tile_max);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     constexpr int FB = 256;
     k_flop_fixup<FB><<<static_cast<unsigned>((tiles + FB - 1) / FB), FB, 0, stream>>>(
-        s.tile_x, tiles, a.rows, s.tile_carry, s.tile_total, s.tile_max, flop, totals);
+        s.tile_x, tiles, s.tile_carry, s.tile_total, s.tile_max, flop, totals);
     return cudaGetLastError();
 }
 

@@ -16,6 +16,7 @@ struct DevCsr {
     const int64_t* rpt = nullptr;
     const int32_t* col = nullptr;
     int64_t nnz = 0;   // rpt[rows] - rpt[0]
+    int64_t base = 0;  // rpt[0] (absolute offset of the first entry), known on the host
 };
 
 // Slots of the per-call device totals array (long long[kTotals]).
@@ -29,32 +30,29 @@ enum TotalSlot : int {
 };
 
 // ---------------------------------------------------------------- FLOP
-// Merge-path tiles over the (row-end, nonzero) sequence of A (Merrill &
-// Garland's merge-based decomposition): every tile holds exactly
-// kFlopTile items, so hub rows and empty rows cost the same per item.
+// Fixed tiles of kFlopTile nonzeros (aligned to absolute multiples of the
+// tile size), one block each; a tile owns the rows that start inside it.
 constexpr int kFlopBlock = 256;
-constexpr int kFlopIpt = 8;
+constexpr int kFlopIpt = 16;
 constexpr int kFlopTile = kFlopBlock * kFlopIpt;
 
-inline int64_t flop_tiles(const DevCsr& a) {
-    const int64_t items = int64_t(a.rows) + a.nnz;
-    return (items + kFlopTile - 1) / kFlopTile;
-}
+int64_t flop_tiles(const DevCsr& a);
 
 struct FlopScratch {
-    int32_t* tile_x = nullptr;       // tiles + 1 merge-path row coordinates
-    long long* tile_carry = nullptr; // tiles: partial sum of the row open at tile end
+    int32_t* tile_x = nullptr;       // tiles + 1: first owned row of each tile
+    long long* tile_carry = nullptr; // tiles: sum of the leading slice (row owned earlier)
     long long* tile_total = nullptr; // tiles
     long long* tile_max = nullptr;   // tiles
 };
 
 cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStream_t stream);
-// deg[k] = B.rpt[k+1] - B.rpt[k] as int32 (a B row has at most B.cols < 2^31
-// entries), written with an L2 evict_last policy for the gathers.
-cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, int32_t* deg, int num_sms,
+// deg[k] = min(B.rpt[k+1] - B.rpt[k], 0xFFFF) as uint16; 0xFFFF escapes to
+// B.rpt for the exact length.  Gathered under an L2 evict_last policy.
+cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, uint16_t* deg, int num_sms,
                           cudaStream_t stream);
-cudaError_t launch_flop(const DevCsr& a, const int32_t* bdeg, const FlopScratch& s, int64_t* flop,
-                        long long* totals, cudaStream_t stream);
+cudaError_t launch_flop(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt,
+                        const FlopScratch& s, int64_t* flop, long long* totals,
+                        cudaStream_t stream);
 
 // -------------------------------------------------------------- sampler
 cudaError_t launch_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* rows,

@@ -75,7 +75,12 @@ __device__ __forceinline__ ItemRow item_row(const SymArgs& g, int32_t s) {
 
 // Walks products [q0, q1) of a chunk of n entries with exclusive offsets
 // off[0..n] (off[n] = chunk end) and B-row starts b0[0..n).  WARPS warps
-// share the range; fn(key) runs once per product.
+// share the range.  Each lane gathers kUnroll keys (32 apart) back to back
+// and hands them to fn(keys, valid) together, so the loads -- and whatever
+// memory operations fn issues per key -- overlap instead of forming one
+// dependent chain per product.
+constexpr int kUnroll = 4;
+
 template <int WARPS, typename OffT, typename Fn>
 __device__ __forceinline__ void chunk_products(const OffT* off, const int64_t* b0, int n,
                                                long long q0, long long q1,
@@ -95,11 +100,35 @@ __device__ __forceinline__ void chunk_products(const OffT* off, const int64_t* b
         if (static_cast<long long>(off[mid]) <= p) lo = mid; else hi = mid - 1;
     }
     int e = lo;
-    for (; p < we; p += 32) {
-        while (static_cast<long long>(off[e + 1]) <= p) ++e;
-        fn(__ldg(&bcol[b0[e] + (p - static_cast<long long>(off[e]))]));
+    for (; p < we; p += 32 * kUnroll) {
+        int keys[kUnroll];
+        bool valid[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const long long q = p + 32 * u;
+            valid[u] = q < we;
+            keys[u] = 0;
+            if (valid[u]) {
+                while (static_cast<long long>(off[e + 1]) <= q) ++e;
+                keys[u] = __ldg(&bcol[b0[e] + (q - static_cast<long long>(off[e]))]);
+            }
+        }
+        fn(keys, valid);
     }
 }
+
+// fn adaptor: insert each valid key into a shared-memory hash table.
+struct HashSink {
+    int* table;
+    uint32_t size;
+    int* cnt;
+    __device__ __forceinline__ void operator()(const int (&keys)[kUnroll],
+                                               const bool (&valid)[kUnroll]) const {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            if (valid[u]) *cnt += hash_insert(table, size, keys[u]);
+    }
+};
 
 // ------------------------------------------------------------- binning
 template <int BLOCK>
@@ -228,8 +257,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_warp_hash(SymArgs g, SymScratch s
             b0s[lane] = b0;
             if (lane == nent - 1) off[nent] = incl;
             __syncwarp();
-            chunk_products<1>(off, b0s, nent, 0, off[nent], g.bcol,
-                              [&](int key) { cnt += hash_insert(table, kSlots, key); });
+            chunk_products<1>(off, b0s, nent, 0, off[nent], g.bcol, HashSink{table, kSlots, &cnt});
             __syncwarp();
         }
         cnt = static_cast<int>(warp_sum_ll(cnt));
@@ -278,7 +306,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
             if (threadIdx.x == 0) s_off[nent] = total;
             __syncthreads();  // also orders the table fill before the inserts
             chunk_products<BLOCK / 32>(s_off, s_b0, nent, 0, total, g.bcol,
-                                       [&](int key) { cnt += hash_insert(table, SLOTS, key); });
+                                       HashSink{table, SLOTS, &cnt});
             __syncthreads();
         }
         const long long tot = block_sum_ll<BLOCK>(cnt, s_red);
@@ -419,16 +447,31 @@ __global__ void __launch_bounds__(kHeavyBlock) k_heavy(SymArgs g, SymScratch sc,
             __syncthreads();
             const long long q0 = p0 > s_off[0] ? p0 : s_off[0];
             const long long q1 = p1 < s_off[n] ? p1 : s_off[n];
-            chunk_products<kHeavyBlock / 32>(s_off, s_b0, n, q0, q1, g.bcol, [&](int key) {
-                uint32_t* w = bm + (static_cast<uint32_t>(key) >> 5);
-                if (CLEAN) {
-                    *w = 0u;
-                } else {
-                    const uint32_t bit = 1u << (key & 31);
-                    if (!(*reinterpret_cast<volatile uint32_t*>(w) & bit))
-                        cnt += (atomicOr(w, bit) & bit) ? 0 : 1;
-                }
-            });
+            chunk_products<kHeavyBlock / 32>(
+                s_off, s_b0, n, q0, q1, g.bcol,
+                [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll]) {
+                    if (CLEAN) {
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u)
+                            if (valid[u]) bm[static_cast<uint32_t>(keys[u]) >> 5] = 0u;
+                    } else {
+                        // test all words first (independent loads), then
+                        // atomically set the bits still missing
+                        uint32_t cur[kUnroll];
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u)
+                            cur[u] = valid[u] ? *reinterpret_cast<volatile uint32_t*>(
+                                                    bm + (static_cast<uint32_t>(keys[u]) >> 5))
+                                              : ~0u;
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u) {
+                            const uint32_t bit = 1u << (keys[u] & 31);
+                            if (!(cur[u] & bit))
+                                cnt += (atomicOr(bm + (static_cast<uint32_t>(keys[u]) >> 5), bit) &
+                                        bit) ? 0 : 1;
+                        }
+                    }
+                });
             const bool done = s_off[n] >= p1 || e + n >= L;
             __syncthreads();
             if (done) break;
