@@ -11,9 +11,9 @@
 //      L2-resident under an evict_last policy -- the int64 pair
 //      B.rpt[k], B.rpt[k+1] is 134 MB and is not);
 //   1. k_flop_partition: first owned row of every tile (lower_bound in rpt);
-//   2. k_flop, per tile: 16-byte evict_first loads of the tile's A.col,
-//      then the deg[] gathers (16 per thread in flight), staged in shared
-//      memory; each thread then sums one owned row's slice of the staged
+//   2. k_flop, per tile: 16-byte evict_first loads of the tile's A.col into
+//      shared memory, then the deg[] gathers (8 per thread in flight, lanes
+//      on consecutive entries), staged in shared memory; each thread then sums one owned row's slice of the staged
 //      degrees (rows longer than 64 in the tile go to a warp each), writes
 //      flop[row] and the tile's partials: F, max, and the leading segment
 //      that belongs to a row owned by an earlier tile;
@@ -71,7 +71,7 @@ __global__ void k_flop_partition(const int64_t* __restrict__ arpt, int32_t m, in
 }
 
 template <int BLOCK, int V>
-__global__ void __launch_bounds__(BLOCK)
+__global__ void __launch_bounds__(BLOCK, 5)
 k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
        const uint16_t* __restrict__ bdeg, const int64_t* __restrict__ brpt, int32_t m,
        int64_t base, int64_t nnz, const int32_t* __restrict__ tile_row,
@@ -93,46 +93,47 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
     const int tid = threadIdx.x;
     if (tid == 0) s_nlong = 0;
 
-    // 1. stage the tile's degrees: 16-byte loads of A.col (the tile start is
-    //    a multiple of 4096 entries, so only the shard's first and last tiles
-    //    can be partial), then all gathers in flight.  Entry i of the tile is
-    //    k & 3 of vector (tid + (k >> 2) * BLOCK).
-    int32_t c[V];
-    const bool vec = n == TILE && (reinterpret_cast<uintptr_t>(acol + ts) & 15) == 0;
-    if (vec) {
+    // 1. stage the tile's degrees.  16-byte evict_first loads of A.col into
+    //    shared memory (the tile start is a multiple of 4096 entries, so only
+    //    a shard's first and last tiles are partial), then each thread reads
+    //    entries tid, tid + 256, ... back (stride 1 across a warp, so the
+    //    gathers of neighbouring entries share sectors when the columns are
+    //    close, as in banded matrices), issues all its gathers, and stores
+    //    the degrees in place.
+    int32_t* s_col = s_deg;
+    if (n == TILE && (reinterpret_cast<uintptr_t>(acol + ts) & 15) == 0) {
         const int4* src = reinterpret_cast<const int4*>(acol + ts);
+        int4* dst = reinterpret_cast<int4*>(s_col);
 #pragma unroll
-        for (int k = 0; k < V / 4; ++k) {
-            const int4 q = ld_stream_v4(src + tid + k * BLOCK, first);
-            c[4 * k] = q.x;
-            c[4 * k + 1] = q.y;
-            c[4 * k + 2] = q.z;
-            c[4 * k + 3] = q.w;
-        }
+        for (int k = 0; k < V / 4; ++k) dst[tid + k * BLOCK] = ld_stream_v4(src + tid + k * BLOCK, first);
     } else {
-#pragma unroll
-        for (int k = 0; k < V / 4; ++k)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int i = 4 * (tid + k * BLOCK) + j;
-                c[4 * k + j] = i < n ? ld_stream_i32(acol + ts + i, first) : 0;
-            }
+        for (int i = tid; i < n; i += BLOCK) s_col[i] = ld_stream_i32(acol + ts + i, first);
     }
-    int32_t dg[V];
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-        const int i = 4 * (tid + (k >> 2) * BLOCK) + (k & 3);
-        dg[k] = i < n ? static_cast<int32_t>(ld_keep_u16(bdeg + c[k], last)) : 0;
-    }
+    __syncthreads();
     long long tsum = 0;
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-        const int i = 4 * (tid + (k >> 2) * BLOCK) + (k & 3);
-        if (i < n) {
-            int32_t d = dg[k];
-            if (d == 0xFFFF) d = static_cast<int32_t>(__ldg(&brpt[c[k] + 1]) - __ldg(&brpt[c[k]]));
-            s_deg[i] = d;
-            tsum += d;
+    for (int h = 0; h < V; h += V / 2) {
+        int32_t c[V / 2], dg[V / 2];
+#pragma unroll
+        for (int k = 0; k < V / 2; ++k) {
+            const int i = tid + (h + k) * BLOCK;
+            c[k] = i < n ? s_col[i] : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < V / 2; ++k) {
+            const int i = tid + (h + k) * BLOCK;
+            dg[k] = i < n ? static_cast<int32_t>(ld_keep_u16(bdeg + c[k], last)) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < V / 2; ++k) {
+            const int i = tid + (h + k) * BLOCK;
+            if (i < n) {
+                int32_t d = dg[k];
+                if (d == 0xFFFF)
+                    d = static_cast<int32_t>(__ldg(&brpt[c[k] + 1]) - __ldg(&brpt[c[k]]));
+                s_deg[i] = d;
+                tsum += d;
+            }
         }
     }
     __syncthreads();
