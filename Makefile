@@ -10,10 +10,10 @@ BUILD := build
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xptxas -warn-spills \
            -Xcompiler -fPIC,-ffp-contract=off,-Wall -Iinclude -I$(SRC)
 
-CU_SRCS := $(SRC)/flop.cu $(SRC)/sample_predict.cu $(SRC)/symbolic.cu
+CU_SRCS := $(SRC)/flop.cu $(SRC)/sample_predict.cu $(SRC)/symbolic.cu $(SRC)/heavy.cu
 CPP_SRCS := $(SRC)/capi.cpp
 OBJS := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(BUILD)/%.o,$(CPP_SRCS))
-HDRS := $(SRC)/kernels.h $(SRC)/device_common.cuh include/spnnz_gpu/capi.h
+HDRS := $(SRC)/kernels.h $(SRC)/device_common.cuh $(SRC)/symbolic_common.cuh include/spnnz_gpu/capi.h
 
 all: $(OUT)/libspnnz_gpu.so $(OUT)/libspnnz_gen.so oracle
 

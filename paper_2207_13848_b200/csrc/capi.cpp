@@ -161,7 +161,10 @@ struct spnnz_gpu_ctx {
     DBuf<int32_t> counts;
     DBuf<int32_t> lists;
     int64_t list_cap = 0;
-    DBuf<int64_t> heavy_unit_off, heavy_eoff, heavy_epre, heavy_eb0;
+    DBuf<int64_t> heavy_unit_off, heavy_eoff, heavy_foff, heavy_epre, heavy_eb0, heavy_flops;
+    DBuf<long long> heavy_rc, heavy_cur;
+    DBuf<int32_t> heavy_pbuf;
+    DBuf<int4> heavy_tasks;  // HeavyTask = 32 bytes = 2 x int4
     long long* h_meta = nullptr;    // pinned mirror of heavy_meta
     DBuf<uint32_t> pool;
     int64_t pool_slots = 0, pool_words = 0;
@@ -220,51 +223,57 @@ int sym_scratch(spnnz_gpu_ctx* c, int64_t items, SymScratch* s) {
         RC(c->lists.ensure(items * kNumBins));
         RC(c->heavy_unit_off.ensure(items + 1));
         RC(c->heavy_eoff.ensure(items + 1));
+        RC(c->heavy_foff.ensure(items + 1));
         c->list_cap = items;
     }
     RC(c->counts.ensure(16));
-    RC(c->heavy_meta.ensure(4));
+    RC(c->heavy_meta.ensure(8));
     s->lists = c->lists.p;
     s->capacity = c->list_cap;
     s->counts = c->counts.p;
     s->heavy_unit_off = c->heavy_unit_off.p;
     s->heavy_eoff = c->heavy_eoff.p;
+    s->heavy_foff = c->heavy_foff.p;
     s->heavy_epre = c->heavy_epre.p;
     s->heavy_eb0 = c->heavy_eb0.p;
-    s->heavy_ecap = c->heavy_epre.n;
     s->heavy_meta = c->heavy_meta.p;
     s->pool = c->pool.p;
-    s->pool_words = c->pool_words;
+
     return SPNNZ_OK;
 }
 
-// Pool of zeroed bitmaps (one per heavy row in flight); kept clean by the
-// heavy kernel's cleaning pass, so it is zeroed only when (re)allocated.
-int ensure_pool(spnnz_gpu_ctx* c, int64_t want_slots, SymScratch* s) {
-    const int64_t words = heavy_table_words(0, c->b_cols);
-    if (c->pool_words != words) {
+// Buffers of one heavy batch (see heavy.cu); the merge-bitmap pool is zeroed
+// when (re)allocated and returned to zero by the heavy path after each use.
+int heavy_buffers(spnnz_gpu_ctx* c, int64_t count, int64_t ents, int64_t products,
+                  SymScratch* s) {
+    const HeavyGeometry geo = heavy_geometry(c->b_cols);
+    RC(c->heavy_epre.ensure(ents));
+    RC(c->heavy_eb0.ensure(ents));
+    if (geo.ranges > 1) {
+        RC(c->heavy_rc.ensure(count * geo.ranges));
+        RC(c->heavy_cur.ensure(count * geo.ranges));
+        RC(c->heavy_pbuf.ensure(products));
+    }
+    const int64_t tasks = heavy_task_bound(count, products, geo.ranges);
+    RC(c->heavy_tasks.ensure(2 * tasks));
+    const int64_t words = int64_t(geo.wwords);
+    const int64_t slots = heavy_slot_bound(count, products);
+    if (c->pool_words != words || slots > c->pool_slots) {
         c->pool.release();
-        c->pool_slots = 0;
+        RC(c->pool.ensure(slots * words));
+        CU(cudaMemsetAsync(c->pool.p, 0, sizeof(uint32_t) * slots * words, c->stream));
+        c->pool_slots = slots;
         c->pool_words = words;
     }
-    if (const char* cap = getenv("SPNNZ_HEAVY_POOL_SLOTS")) {  // test knob: force batching
-        const int64_t k = atoll(cap);
-        if (k > 0 && want_slots > k) want_slots = k;
-    }
-    if (want_slots > c->pool_slots) {
-        size_t free_b = 0, total_b = 0;
-        CU(cudaMemGetInfo(&free_b, &total_b));
-        const int64_t budget = std::min<int64_t>(int64_t(free_b) / 4, int64_t(8) << 30);
-        int64_t slots = std::min<int64_t>(want_slots, std::max<int64_t>(1, budget / (words * 4)));
-        if (slots > c->pool_slots) {
-            c->pool.release();
-            RC(c->pool.ensure(slots * words));
-            CU(cudaMemsetAsync(c->pool.p, 0, sizeof(uint32_t) * slots * words, c->stream));
-            c->pool_slots = slots;
-        }
-    }
+    s->heavy_epre = c->heavy_epre.p;
+    s->heavy_eb0 = c->heavy_eb0.p;
+    s->heavy_rc = c->heavy_rc.p;
+    s->heavy_cur = c->heavy_cur.p;
+    s->heavy_pbuf = c->heavy_pbuf.p;
+    s->heavy_tasks = c->heavy_tasks.p;
+    s->heavy_task_cap = tasks;
     s->pool = c->pool.p;
-    s->pool_words = c->pool_words;
+
     return SPNNZ_OK;
 }
 
@@ -288,7 +297,7 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     g.total_slot = slot;
     g.sampled_flop = sampled_flop;
     CU(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * 16, c->stream));
-    CU(cudaMemsetAsync(c->heavy_meta.p, 0, sizeof(long long) * 4, c->stream));
+    CU(cudaMemsetAsync(c->heavy_meta.p, 0, sizeof(long long) * 8, c->stream));
     if (n_items == 0) return SPNNZ_OK;
     CU(launch_sym_bin(g, s, c->stream));
     // fork the tier kernels onto side streams, join before the heavy tier
@@ -304,25 +313,51 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     // Heavy rows: the host learns their number, then runs pool-sized batches.
     CU(cudaMemcpyAsync(c->h_counts, c->counts.p, sizeof(int32_t) * 16, cudaMemcpyDeviceToHost,
                        c->stream));
-    CU(cudaMemcpyAsync(c->h_meta, c->heavy_meta.p, sizeof(long long) * 4, cudaMemcpyDeviceToHost,
+    CU(cudaMemcpyAsync(c->h_meta, c->heavy_meta.p, sizeof(long long) * 8, cudaMemcpyDeviceToHost,
                        c->stream));
     CU(cudaStreamSynchronize(c->stream));
     const int64_t heavy = c->h_counts[kHeavyBin];
     if (heavy > 0) {
-        // per-entry prefix arrays for the heavy rows (sum of lengths + 1 each)
-        const int64_t ents = c->h_meta[1];
-        if (ents > c->heavy_epre.n) {
-            RC(c->heavy_epre.ensure(ents));
-            RC(c->heavy_eb0.ensure(ents));
+        // One batch when the heavy rows' products fit the batch budget
+        // (always for sampled passes); exact passes over every row split the
+        // heavy list greedily by FLOP.
+        int64_t kBudget = int64_t(1) << 28;  // products per batch (1 GB buffer)
+        if (const char* env = getenv("SPNNZ_HEAVY_BATCH_PRODUCTS"))  // test knob
+            if (atoll(env) > 0) kBudget = atoll(env);
+        const int64_t ents_total = c->h_meta[1], prod_total = c->h_meta[2];
+        std::vector<int64_t> cuts{0, heavy};
+        if (prod_total > kBudget) {
+            RC(c->heavy_flops.ensure(heavy));
+            CU(launch_heavy_flops(g, s, heavy, c->heavy_flops.p, c->stream));
+            std::vector<int64_t> f(static_cast<size_t>(heavy));
+            CU(cudaMemcpyAsync(f.data(), c->heavy_flops.p, 8 * size_t(heavy), cudaMemcpyDeviceToHost,
+                               c->stream));
+            CU(cudaStreamSynchronize(c->stream));
+            cuts = {0};
+            int64_t acc = 0;
+            for (int64_t i = 0; i < heavy; ++i) {
+                if (acc > 0 && acc + f[i] > kBudget) {
+                    cuts.push_back(i);
+                    acc = 0;
+                }
+                acc += f[i];
+            }
+            cuts.push_back(heavy);
         }
-        s.heavy_epre = c->heavy_epre.p;
-        s.heavy_eb0 = c->heavy_eb0.p;
-        s.heavy_ecap = c->heavy_epre.n;
-        RC(ensure_pool(c, heavy, &s));
-        for (int64_t first = 0; first < heavy; first += c->pool_slots) {
-            const int64_t cnt = std::min<int64_t>(c->pool_slots, heavy - first);
+        const int64_t prod_cap = std::min(prod_total, std::max<int64_t>(kBudget, 1));
+        for (size_t b = 0; b + 1 < cuts.size(); ++b) {
+            const int64_t first = cuts[b], cnt = cuts[b + 1] - cuts[b];
+            // products of a batch <= max(budget, its single largest row)
+            int64_t prod = prod_cap;
+            if (cnt == 1 || prod_total <= kBudget) prod = std::max(prod_cap, prod_total);
+            if (cuts.size() > 2 && cnt == 1) {
+                long long one = 0;
+                CU(cudaMemcpy(&one, c->heavy_flops.p + first, 8, cudaMemcpyDeviceToHost));
+                prod = std::max<int64_t>(prod, one);
+            }
+            RC(heavy_buffers(c, cnt, ents_total, prod, &s));
             CU(launch_sym_heavy(g, s, first, cnt, c->num_sms, c->stream));
-            *launches += 4;
+            *launches += 8;
         }
     }
     return SPNNZ_OK;
@@ -472,7 +507,7 @@ int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz
     e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_totals, sizeof(long long) * kTotals);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_counts, sizeof(int32_t) * 16);
-    if (e == cudaSuccess) e = cudaMallocHost(&c->h_meta, sizeof(long long) * 4);
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_meta, sizeof(long long) * 8);
     for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     for (int i = 0; i < 3 && e == cudaSuccess; ++i)
         e = cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking);
@@ -511,7 +546,7 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm) nccl().CommDestroy(c->comm);
     for (auto* b : {&c->b_rpt, &c->a_rpt, &c->flop, &c->out64, &c->heavy_unit_off,
-                    &c->heavy_eoff, &c->heavy_epre, &c->heavy_eb0})
+                    &c->heavy_eoff, &c->heavy_foff, &c->heavy_epre, &c->heavy_eb0, &c->heavy_flops})
         b->release();
     c->deg.release();
     for (auto* b : {&c->b_col, &c->a_col, &c->tile_x, &c->counts, &c->lists,
@@ -521,6 +556,10 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
         b->release();
     c->pool.release();
     c->outf.release();
+    c->heavy_rc.release();
+    c->heavy_cur.release();
+    c->heavy_pbuf.release();
+    c->heavy_tasks.release();
     if (c->h_totals) cudaFreeHost(c->h_totals);
     if (c->h_counts) cudaFreeHost(c->h_counts);
     if (c->h_meta) cudaFreeHost(c->h_meta);

@@ -78,16 +78,32 @@ struct SymScratch {
     int32_t* lists = nullptr;        // kNumBins * capacity item ids
     int64_t capacity = 0;
     int32_t* counts = nullptr;       // kNumBins (+ spare) counters
-    // heavy-row work decomposition (per batch of heavy items)
+    // heavy-row work decomposition (per batch of heavy items, see heavy.cu)
     int64_t* heavy_unit_off = nullptr;   // capacity + 1: product-unit prefix per item
     int64_t* heavy_eoff = nullptr;       // capacity + 1: entry-array offset per item
+    int64_t* heavy_foff = nullptr;       // capacity + 1: product prefix per item
     int64_t* heavy_epre = nullptr;       // per entry: exclusive product prefix (L_i + 1 per item)
     int64_t* heavy_eb0 = nullptr;        // per entry: start of its B row
-    int64_t heavy_ecap = 0;
-    uint32_t* pool = nullptr;            // bitmaps of B.cols bits, kept clean between calls
-    int64_t pool_words = 0;
-    long long* heavy_meta = nullptr;     // [0] units in batch, [1] sum of heavy row lengths
+    long long* heavy_rc = nullptr;       // count * R: range histogram, then bucket starts
+    long long* heavy_cur = nullptr;      // count * R: scatter cursors
+    int32_t* heavy_pbuf = nullptr;       // products grouped by (item, range)
+    void* heavy_tasks = nullptr;         // HeavyTask[heavy_task_cap]
+    int64_t heavy_task_cap = 0;
+    uint32_t* pool = nullptr;            // merge bitmaps (W bits each), zero between calls
+    long long* heavy_meta = nullptr;     // [0] units [1] sum(len+1) [2] sum(flop) of heavy
+                                         // rows [3] tasks [4] merge slots used
 };
+
+// Column-range geometry of the heavy path: ranges of 2^wshift bits (at most
+// 2^20, a 128 KB shared bitmap), `ranges` of them cover B.cols.
+struct HeavyGeometry {
+    int wshift = 20;
+    int ranges = 1;
+    int32_t wwords = 1 << 15;
+};
+HeavyGeometry heavy_geometry(int32_t bcols);
+int64_t heavy_task_bound(int64_t count, int64_t products, int ranges);
+int64_t heavy_slot_bound(int64_t count, int64_t products);
 
 struct SymArgs {
     DevCsr a;
@@ -111,12 +127,14 @@ cudaError_t launch_sym_bin(const SymArgs& args, const SymScratch& s, cudaStream_
 // caller forks them from its stream and joins them afterwards).
 cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_sms,
                              const cudaStream_t* streams);
-// Heavy tier for bin entries [first, first + count) of list 5 (host knows
-// count after a sync).  Tables come from s.pool and are cleaned afterwards.
+// Heavy tier for entries [first, first + count) of the heavy list (the host
+// learns the count after a sync and sizes the batch's buffers).
 cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, int64_t first,
                              int64_t count, int num_sms, cudaStream_t stream);
-// Per heavy row table words needed (host-side sizing helper for the pool).
-int64_t heavy_table_words(int64_t flop_row, int32_t bcols);
+// FLOP of each heavy item in list order (batch planning when the heavy rows'
+// products exceed one batch's buffers).
+cudaError_t launch_heavy_flops(const SymArgs& args, const SymScratch& s, int64_t count,
+                               int64_t* out, cudaStream_t stream);
 
 // -------------------------------------------------------------- predict
 // ceil view min(flop, ceil(flop / cr)) and/or real view flop / cr.  If

@@ -1,0 +1,135 @@
+// Device helpers shared by the symbolic tiers (symbolic.cu) and the heavy-row
+// path (heavy.cu): item decoding, shared-memory hash insert and the
+// coalesced product enumeration of a chunk of A-row entries.
+#pragma once
+#include <cub/block/block_scan.cuh>
+
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace spnnz_gpu {
+namespace sym {
+
+constexpr int kEmpty = -1;
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(kFull, v, o);
+        if (lane >= o) v += n;
+    }
+    return v;
+}
+
+// Open-addressing insert; returns 1 if key was new.  `size` slots, hash by
+// multiply-high range reduction so any table size works.
+__device__ __forceinline__ int hash_insert(int* table, uint32_t size, int key) {
+    uint32_t h = __umulhi(mix32(static_cast<uint32_t>(key)), size);
+    for (;;) {
+        const int cur = table[h];
+        if (cur == key) return 0;
+        if (cur == kEmpty) {
+            const int prev = atomicCAS(&table[h], kEmpty, key);
+            if (prev == kEmpty) return 1;
+            if (prev == key) return 0;
+        }
+        h = (h + 1 == size) ? 0 : h + 1;
+    }
+}
+
+struct ItemRow {
+    int64_t a0, a1;  // absolute nonzero range of the A row
+    int32_t s;       // item index
+};
+
+__device__ __forceinline__ ItemRow item_row(const SymArgs& g, int32_t s) {
+    const int32_t rid = g.rows ? g.rows[s] : g.row_lo + s;
+    const int32_t r = rid - g.row_lo;
+    ItemRow it;
+    it.s = s;
+    it.a0 = g.a.rpt[r];
+    it.a1 = g.a.rpt[r + 1];
+    return it;
+}
+
+// Walks products [q0, q1) of a chunk of n entries with exclusive offsets
+// off[0..n] (off[n] = chunk end) and B-row starts b0[0..n).  WARPS warps
+// share the range.  Each lane gathers kUnroll keys (32 apart) back to back
+// and hands them to fn(keys, valid, p) together (keys[u] is product p+32u),
+// so the loads -- and whatever
+// memory operations fn issues per key -- overlap instead of forming one
+// dependent chain per product.
+constexpr int kUnroll = 4;
+
+template <int WARPS, typename OffT, typename Fn>
+__device__ __forceinline__ void chunk_products(const OffT* off, const int64_t* b0, int n,
+                                               long long q0, long long q1,
+                                               const int32_t* __restrict__ bcol, Fn&& fn) {
+    const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) % WARPS;
+    const long long span = q1 - q0;
+    if (span <= 0 || n <= 0) return;
+    long long per = (span + WARPS - 1) / WARPS;
+    per = (per + 31) & ~31LL;
+    const long long ws = q0 + w * per;
+    const long long we = ws + per < q1 ? ws + per : q1;
+    // warp-uniform loop (fn may use warp collectives); lanes past the end of
+    // the warp's slice run with valid = false
+    int e = 0;
+    if (ws + lane < we) {
+        const long long p = ws + lane;
+        int lo = 0, hi = n - 1;  // largest e with off[e] <= p
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (static_cast<long long>(off[mid]) <= p) lo = mid; else hi = mid - 1;
+        }
+        e = lo;
+    }
+    for (long long base = ws; base < we; base += 32 * kUnroll) {
+        const long long p = base + lane;
+        int keys[kUnroll];
+        bool valid[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const long long q = p + 32 * u;
+            valid[u] = q < we;
+            keys[u] = 0;
+            if (valid[u]) {
+                while (static_cast<long long>(off[e + 1]) <= q) ++e;
+                keys[u] = __ldg(&bcol[b0[e] + (q - static_cast<long long>(off[e]))]);
+            }
+        }
+        fn(keys, valid, p);  // keys[u] is product p + 32 u
+    }
+}
+
+// Warp-aggregated shared-memory add: lanes with the same bucket combine, the
+// lowest of them adds; returns the lane's rank among its bucket peers plus
+// the value the bucket had before (so it doubles as a cursor).  Must be
+// called by all 32 lanes; bucket < 0 means "not participating".
+__device__ __forceinline__ int warp_bucket_add(int* counters, int bucket) {
+    const unsigned peers = __match_any_sync(0xffffffffu, bucket);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (bucket >= 0 && lane == leader) base = atomicAdd(&counters[bucket], __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    return base + __popc(peers & ((1u << lane) - 1));
+}
+
+// fn adaptor: insert each valid key into a shared-memory hash table.
+struct HashSink {
+    int* table;
+    uint32_t size;
+    int* cnt;
+    __device__ __forceinline__ void operator()(const int (&keys)[kUnroll],
+                                               const bool (&valid)[kUnroll], long long) const {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            if (valid[u]) *cnt += hash_insert(table, size, keys[u]);
+    }
+};
+
+}  // namespace sym
+}  // namespace spnnz_gpu

@@ -196,10 +196,11 @@ def test_every_bin_vs_oracle(P, oracle, ncols):
     assert (s.nnz_per_row == nnz[rows]).all() and s.total_nnz == Z
 
 
-def test_heavy_pool_batching(P, oracle, monkeypatch):
-    """More heavy rows than pool slots: the batch loop and the cleaning pass
-    must leave the pool zeroed for the next batch."""
-    monkeypatch.setenv("SPNNZ_HEAVY_POOL_SLOTS", "2")
+def test_heavy_batching(P, oracle, monkeypatch):
+    """Heavy rows split over several batches (budget forced down to 100 K
+    products): the batch loop, and the merge-bitmap pool returning to zero
+    after each use, must keep the counts exact."""
+    monkeypatch.setenv("SPNNZ_HEAVY_BATCH_PRODUCTS", "100000")
     q = Predictor(0)
     rng = np.random.default_rng(3)
     lens = [3000, 2500, 2800, 2900, 2700, 10, 3000]
