@@ -15,7 +15,7 @@
 //               reserve each range's slice with one global atomic, and write
 //               the products out grouped by range;
 //   4. tasks    per row, consecutive ranges are packed into tasks of at most
-//               kHashTaskProducts products (shared hash of 53248 slots); a
+//               kHashTaskProducts products (shared hash of 49152 slots); a
 //               range with more products becomes bitmap tasks of at most
 //               kBitmapTaskProducts products each (shared bitmap of W bits);
 //   5. run      one block per task; a bitmap task that shares its range with
@@ -32,9 +32,9 @@ namespace {
 using namespace sym;
 
 constexpr int kHB = 256;                       // block of the unit passes
-constexpr int kRunBlock = 512;                 // block of the task runner
-constexpr int kHashSlots = 53248;              // 208 KB hash table
-constexpr int64_t kHashTaskProducts = 32768;   // load <= 0.62
+constexpr int kRunBlock = 1024;                // block of the task runners
+constexpr int kHashSlots = 49152;              // 192 KB hash table
+constexpr int64_t kHashTaskProducts = kBin5Max;  // load <= 0.5
 constexpr int64_t kBitmapTaskProducts = 131072;
 constexpr int kMaxRanges = 2048;               // B.cols < 2^31, W = 2^20
 
@@ -234,10 +234,11 @@ __global__ void __launch_bounds__(kHB) k_heavy_scatter(SymArgs g, SymScratch sc,
                                                        int64_t count, int R, int wshift) {
     __shared__ long long s_off[kHB + 1];
     __shared__ int64_t s_b0[kHB];
-    __shared__ int s_hist[kMaxRanges];
-    __shared__ long long s_base[kMaxRanges];
     extern __shared__ int4 s_dyn_keys[];
-    int32_t* s_keys = reinterpret_cast<int32_t*>(s_dyn_keys);  // kHeavyUnitProducts
+    // dynamic: keys[kHeavyUnitProducts] | base[R] (int64) | hist[R]
+    int32_t* s_keys = reinterpret_cast<int32_t*>(s_dyn_keys);
+    long long* s_base = reinterpret_cast<long long*>(s_keys + kHeavyUnitProducts);
+    int* s_hist = reinterpret_cast<int*>(s_base + R);
     const long long units = sc.heavy_meta[0];
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit un = find_unit(sc, count, u);
@@ -338,7 +339,10 @@ __global__ void k_heavy_tasks(SymScratch sc, int64_t count, int R, int64_t task_
     build_tasks(sc, i, R, reinterpret_cast<HeavyTask*>(sc.heavy_tasks) + base);
 }
 
-// ---- 5. run the tasks: one block per task, sets in shared memory
+// ---- 5. run the tasks: one block per task, sets in shared memory.  Hash
+// tasks (192 KB table) and bitmap tasks (W-bit bitmap, <= 128 KB) run in two
+// kernels so each gets 1024 threads per SM.
+template <bool HASH>
 __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch sc, int64_t first,
                                                          int32_t wwords, int wshift) {
     extern __shared__ int4 s_dyn[];
@@ -352,8 +356,9 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
     long long acc = 0;
     for (long long ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
         const HeavyTask t = tasks[ti];
+        if ((t.mode == 0) != HASH) continue;  // the other kernel's task
         int cnt = 0;
-        if (t.mode == 0) {
+        if (HASH) {
             int* table = reinterpret_cast<int*>(s_set);
             for (int k = threadIdx.x; k < kHashSlots; k += kRunBlock) table[k] = kEmpty;
             __syncthreads();
@@ -477,10 +482,12 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, int64_t f
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_done & (1u << (dev & 31)))) {
-        cudaFuncSetAttribute(k_heavy_run, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_heavy_run<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kHashSlots * 4);
+        cudaFuncSetAttribute(k_heavy_run<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (1 << 20) / 8);
         cudaFuncSetAttribute(k_heavy_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kHeavyUnitProducts * 4));
+                             int(kHeavyUnitProducts * 4 + kMaxRanges * 12));
         attr_done |= 1u << (dev & 31);
     }
     const HeavyGeometry geo = heavy_geometry(args.bcols);
@@ -492,12 +499,16 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, int64_t f
         k_heavy_count<<<grid, kHB, 0, stream>>>(args, s, first, count, geo.ranges, geo.wshift);
         k_heavy_offsets<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(
             s, count, geo.ranges);
-        k_heavy_scatter<<<static_cast<unsigned>(num_sms) * 2, kHB, kHeavyUnitProducts * 4, stream>>>(
+        const int scatter_smem = int(kHeavyUnitProducts * 4 + geo.ranges * 12);
+        k_heavy_scatter<<<static_cast<unsigned>(num_sms) * 6, kHB, scatter_smem, stream>>>(
             args, s, first, count, geo.ranges, geo.wshift);
     }
     k_heavy_tasks<<<static_cast<unsigned>((count + 127) / 128), 128, 0, stream>>>(
         s, count, geo.ranges, s.heavy_task_cap);
-    k_heavy_run<<<static_cast<unsigned>(num_sms), kRunBlock, kHashSlots * 4, stream>>>(
+    if (geo.ranges > 1)
+        k_heavy_run<true><<<static_cast<unsigned>(num_sms), kRunBlock, kHashSlots * 4, stream>>>(
+            args, s, first, geo.wwords, geo.wshift);
+    k_heavy_run<false><<<static_cast<unsigned>(num_sms), kRunBlock, geo.wwords * 4, stream>>>(
         args, s, first, geo.wwords, geo.wshift);
     k_heavy_clean<<<static_cast<unsigned>(num_sms) * 4, 256, 0, stream>>>(s, geo.wwords);
     return cudaGetLastError();

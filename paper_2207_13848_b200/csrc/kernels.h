@@ -67,12 +67,12 @@ constexpr int64_t kBin1Max = 32;     // warp, __match_any_sync dedup
 constexpr int64_t kBin2Max = 512;    // warp, 1024-slot smem hash per warp
 constexpr int64_t kBin3Max = 2048;   // 256-thread block, 4096-slot smem hash
 constexpr int64_t kBin4Max = 8192;   // 512-thread block, 16384-slot smem hash
-constexpr int64_t kBin5Max = 32768;  // 512-thread block, 53248-slot smem hash
+constexpr int64_t kBin5Max = 24576;  // 1024-thread block, 49152-slot smem hash
 constexpr int kHeavyBin = 6;         // heavier: units of kHeavyUnitProducts
 constexpr int kForeignBin = 7;       // row owned by another rank
 constexpr int kNoBin = 8;            // padding lane
 //        products, many blocks per row over a global bitmap of B.cols bits.
-constexpr int64_t kHeavyUnitProducts = 16384;
+constexpr int64_t kHeavyUnitProducts = 8192;
 
 struct SymScratch {
     int32_t* lists = nullptr;        // kNumBins * capacity item ids

@@ -12,7 +12,7 @@
 //   bin 2  f <= 512     one warp per row, 1024-slot shared-memory hash
 //   bin 3  f <= 2048    256-thread block, 4096-slot shared-memory hash
 //   bin 4  f <= 8192    512-thread block, 16384-slot shared-memory hash
-//   bin 5  f <= 32768   512-thread block, 53248-slot shared-memory hash
+//   bin 5  f <= 24576   1024-thread block, 49152-slot shared-memory hash
 //   bin 6  heavier      heavy.cu: products bucketed by column range, every
 //                       set operation in shared memory, many blocks per row
 // Products are enumerated per chunk of entries: a scan of the chunk's B row
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
 
 constexpr int kT3Block = 256, kT3Slots = 4096;
 constexpr int kT4Block = 512, kT4Slots = 16384;
-constexpr int kT5Block = 512, kT5Slots = 53248;
+constexpr int kT5Block = 1024, kT5Slots = 49152;
 
 template <int BLOCK, int SLOTS, int BIN>
 void set_smem_attr() {
