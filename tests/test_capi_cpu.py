@@ -129,3 +129,25 @@ def test_exhaustive_plan():
     assert p.sample_rows.tolist() == [0, 1, 2, 3, 4] and p.p == 1.0
     with pytest.raises(ValueError):
         spnnz.exhaustive_plan(0)
+
+
+def test_cpp_header_accepts_reference_csr(tmp_path):
+    """The C++ mirror compiles against the reference's own spnnz::CsrMatrix
+    (drop-in: callers keep their matrix type).  Needs /root/reference."""
+    import subprocess
+    ref_inc = "/root/reference/proj/include"
+    if not os.path.isdir(ref_inc):
+        pytest.skip("reference headers not present")
+    src = tmp_path / "dropin_ref.cpp"
+    src.write_text(
+        '#include "spnnz/csr.hpp"\n#include "spnnz_gpu/spnnz_gpu.hpp"\n'
+        "int main() { spnnz::CsrMatrix a; a.rows = a.cols = 1; a.rpt = {0, 1}; a.col = {0};\n"
+        "  auto p = spnnz::gpu::compute_flop(a, a);\n"
+        "  auto r = spnnz::gpu::run_prediction(a, a, 1, {0.5, 10});\n"
+        "  auto e = spnnz::gpu::exact_symbolic(a, a, p);\n"
+        "  return int(p.total_flop + r.total_flop + e.total_nnz) == 0; }\n")
+    out = tmp_path / "dropin_ref"
+    r = subprocess.run(["g++", "-std=c++20", "-I", ref_inc, "-I", os.path.join(ROOT, "include"),
+                        str(src), "-o", str(out), "-L", os.path.dirname(capi.LIB_PATH),
+                        "-lspnnz_gpu"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

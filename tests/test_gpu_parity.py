@@ -441,3 +441,15 @@ def test_device_residency_matches_host(P):
     P.load(ta, None)
     rep2 = P.run_prediction(3, SamplePolicy(0.001, UNCAPPED))
     assert rep2.z2_star == host.z2_star and (rep2.predicted_row_nnz_ceil == host.predicted_row_nnz_ceil).all()
+
+
+def test_cpp_dropin_header():
+    """include/spnnz_gpu/spnnz_gpu.hpp: the reference's known answers through
+    the C++ mirror (tests/cpp/test_dropin.cpp)."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "build", "test_dropin")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", root, "build/test_dropin"], check=True, capture_output=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
