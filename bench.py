@@ -366,11 +366,19 @@ def run_ours(args, rank, world, local):
                        "parallelism": f"A row-sharded x{world} (nnz-balanced), B replicated, "
                                       "1 NCCL all-reduce per step",
                        "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps"},
-            "roofline": {"bound": "hbm", "kernel": "FLOP pass (merge-path k_flop + fixup)",
+            "roofline": {"bound": "hbm",
+                         "kernel": "FLOP pass (k_degree + k_flop_partition + k_flop + k_flop_fixup)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes": fbytes, "avg_ms": phase["flop"],
-                         "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json)"},
+                         "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json)",
+                         # the FLOP pass gathers one B-row length per A nonzero; random
+                         # 2-4 B gathers are capped by the L1 sector rate (measured
+                         # 287 G/s chip-wide, profiles/r01_microbench.md), not by HBM
+                         "gathers_per_s": nnz_local / (phase["flop"] * 1e-3) if phase["flop"] else 0.0,
+                         "gather_peak_per_s": 287.6e9,
+                         "gather_frac": (nnz_local / (phase["flop"] * 1e-3) / 287.6e9)
+                         if phase["flop"] else 0.0},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "phases_ms": phase,
             "report": {"F": rep.total_flop, "f_star": rep.stats.sampled_flop,

@@ -1,0 +1,76 @@
+"""Writes the judged profile summaries into profiles/ from ncu artefacts that a
+gpurun call brought back into gpurun_out/:
+
+  python tools/profile_round.py --round r01 \
+      --launches gpurun_out/launches_cfg5.csv [--launches ...] \
+      --full gpurun_out/prof_flop5.ncu-rep [--full ...]
+
+For every launch list: profiles/<round>_launches_<name>.md (per-kernel count,
+mean, total, share).  For every full capture: profiles/<round>_ncu_<name>.md
+(key counters per kernel).  The k_flop capture also writes
+profiles/flop_traffic.json, which bench.py reports as roofline.traffic.
+"""
+import argparse
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, HERE)
+
+import launches as L  # noqa: E402
+import ncu_summary as N  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--round", required=True)
+    ap.add_argument("--launches", action="append", default=[])
+    ap.add_argument("--full", action="append", default=[])
+    ap.add_argument("--note", default="")
+    args = ap.parse_args()
+    out = os.path.join(ROOT, "profiles")
+    os.makedirs(out, exist_ok=True)
+    for p in args.launches:
+        name = os.path.splitext(os.path.basename(p))[0]
+        with open(os.path.join(out, f"{args.round}_{name}.md"), "w") as f:
+            f.write(f"# {args.round} launch list: {name}\n\n")
+            f.write("`ncu --metrics gpu__time_duration.sum --clock-control none` over "
+                    "`bench.py --profile-steps 2` (two predictor passes, cold-cache, serialised: "
+                    "compare shares, not absolutes).\n\n```\n")
+            f.write(L.summarize(p) + "\n```\n")
+            if args.note:
+                f.write("\n" + args.note + "\n")
+    for p in args.full:
+        name = os.path.splitext(os.path.basename(p))[0]
+        data, units = N.rows(p)
+        with open(os.path.join(out, f"{args.round}_{name}.md"), "w") as f:
+            f.write(f"# {args.round} ncu --set full: {name}\n\n")
+            for d in data:
+                f.write(f"## {d.get('Kernel Name', '?')[:120]}\n\n| counter | value |\n|---|---|\n")
+                for w in N.WANT[1:]:
+                    if w in d:
+                        f.write(f"| {w} | {d[w]} {units.get(w, '')} |\n")
+                f.write("\n")
+                if "k_flop<" in d.get("Kernel Name", ""):
+                    def num(k):
+                        v = float(d[k].replace(",", ""))
+                        u = units.get(k, "")
+                        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+                        return v * scale
+                    traffic = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
+                    with open(os.path.join(out, "flop_traffic.json"), "w") as g:
+                        json.dump({"kernel": "k_flop", "source": f"profiles/{args.round}_{name}.md",
+                                   "dram_bytes_per_launch": traffic,
+                                   "dram_read": num("dram__bytes_read.sum"),
+                                   "dram_write": num("dram__bytes_write.sum"),
+                                   "duration_ms": float(d["gpu__time_duration.sum"].replace(",", "")) *
+                                   {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0,
+                                    "msecond": 1.0, "nsecond": 1e-6}.get(
+                                       units.get("gpu__time_duration.sum", "ms"), 1.0)}, g,
+                                  indent=1)
+
+
+if __name__ == "__main__":
+    main()
