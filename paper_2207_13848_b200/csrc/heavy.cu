@@ -2,49 +2,52 @@
 // counts with every set operation in shared memory.
 //
 // A heavy row of C = A*B can have millions of products (config 5: 8.5 M) and
-// its distinct set does not fit one SM.  Instead of a per-row global bitmap
-// (B.cols bits: 2 MB at config 5, ~1000 rows in flight => gigabytes of
-// random read-modify-write traffic that thrashes L2), the row's products are
-// bucketed by column range and every bucket is counted on chip:
-//   1. count    per unit of kHeavyUnitProducts products (one block), a
-//               shared histogram over the R column ranges of width W
-//               (W = min(B.cols, 2^20) bits, R = ceil(B.cols / W));
-//   2. offsets  per row, bucket starts in a product buffer (prefix of the
-//               histogram, per-row spans laid out by an item prefix of FLOP);
-//   3. scatter  per unit again: stage the unit's products in shared memory,
-//               reserve each range's slice with one global atomic, and write
-//               the products out grouped by range;
-//   4. tasks    per row, consecutive ranges are packed into tasks of at most
-//               kHashTaskProducts products (shared hash of 49152 slots); a
-//               range with more products becomes bitmap tasks of at most
-//               kBitmapTaskProducts products each (shared bitmap of W bits);
-//   5. run      one block per task; a bitmap task that shares its range with
-//               other tasks ORs its non-zero words into a global W-bit merge
-//               bitmap and counts popc(word & ~old): the bits it added first.
-// When R == 1 (B.cols <= 2^20: configs 2 and 4) steps 1-3 are skipped and
-// bitmap tasks enumerate their product range straight from the B rows.
-// Every count is a set cardinality, so the result is exact and independent
-// of bucketing, task boundaries and scheduling.
+// its distinct set does not fit one SM.  A per-row global bitmap (2 MB at
+// config 5, ~850 rows in flight) thrashes L2 into gigabytes of DRAM
+// read-modify-write, so instead the row's products are bucketed by column
+// range and every bucket is counted on chip in a shared-memory bitmap:
+//   0. prep/entries  per batch: unit, entry and product offsets of every
+//                    heavy row; per row, the product prefix over its entries;
+//   1. count    per unit of kHeavyUnitProducts products (one block): per-warp
+//               shared histograms over the R column ranges of width W;
+//   2. offsets  per row, bucket starts in the product buffer;
+//   3. scatter  per unit again: stage the products in shared memory, count
+//               them per warp and range, reserve each range's slice with one
+//               global atomic, and write them out grouped by range;
+//   4. tasks    per row, consecutive ranges are packed into tasks spanning at
+//               most 2^20 columns (a 128 KB shared bitmap) and at most
+//               kTaskProducts products; a range with more products is split
+//               into several tasks that share a merge slot;
+//   5. run      one 1024-thread block per task: clear the span's bitmap,
+//               atomicOr each product's bit and count the bits it set first.
+//               Tasks that share a range then OR their non-zero words into a
+//               global W-bit merge bitmap and count popc(word & ~old) instead.
+// B.cols <= 2^20 (configs 2 and 4): one range covers all columns, steps 1-3
+// are skipped and tasks read their product slice straight from the B rows.
+// W = max(2^17, 2^ceil(log2 B.cols) / 256) keeps R <= 256 (per-warp
+// histograms) up to B.cols = 2^28; beyond that W = 2^20 and the histograms
+// are shared.  Every count is a set cardinality: exact and independent of
+// bucketing, task boundaries and scheduling.
 #include "symbolic_common.cuh"
 
 namespace spnnz_gpu {
 namespace {
 using namespace sym;
 
-constexpr int kHB = 256;                       // block of the unit passes
-constexpr int kRunBlock = 1024;                // block of the task runners
-constexpr int kHashSlots = 49152;              // 192 KB hash table
-constexpr int64_t kHashTaskProducts = kBin5Max;  // load <= 0.5
-constexpr int64_t kBitmapTaskProducts = 131072;
-constexpr int kMaxRanges = 2048;               // B.cols < 2^31, W = 2^20
+constexpr int kHB = 256;                  // block of the unit passes
+constexpr int kHW = kHB / 32;             // warps per unit block
+constexpr int kRunBlock = 1024;           // block of the task runner
+constexpr int kSpanShift = 20;            // task column span <= 2^20 (128 KB)
+constexpr int kPrivRanges = 256;          // per-warp histograms up to this R
+constexpr int kMaxRanges = 2048;          // B.cols < 2^31 with W = 2^20
+constexpr int64_t kTaskProducts = 131072;
 
 struct HeavyTask {
-    int32_t item;   // index in the batch
-    int32_t slot;   // merge bitmap slot, or -1
-    int32_t mode;   // 0: hash over a pbuf span, 1: bitmap over a pbuf span,
-                    // 2: bitmap over the item's own product range (R == 1)
-    int32_t range;  // column range of a bitmap task
-    int64_t p0, p1;
+    int32_t item;      // index in the batch
+    int32_t slot;      // merge bitmap slot, or -1
+    int32_t col_base;  // first column of the task's span
+    int32_t words;     // span / 32 (bitmap words to clear)
+    int64_t p0, p1;    // R > 1: product-buffer span; R == 1: the item's product range
 };
 static_assert(sizeof(HeavyTask) == 32, "task layout");
 
@@ -52,7 +55,7 @@ __device__ __forceinline__ const int32_t* heavy_list(const SymScratch& sc, int64
     return sc.lists + int64_t(kHeavyBin) * sc.capacity + first;
 }
 
-// ---- batch bookkeeping: units, entry offsets, product offsets (1 block)
+// ---- 0a. batch bookkeeping: units, entry offsets, product offsets (1 block)
 __global__ void __launch_bounds__(256) k_heavy_prep(SymArgs g, SymScratch sc, int64_t first,
                                                     int64_t count) {
     using Scan = cub::BlockScan<long long, 256>;
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(256) k_heavy_prep(SymArgs g, SymScratch sc, in
     }
 }
 
-// ---- one block per item: product prefix over its entries, B-row starts
+// ---- 0b. one block per item: product prefix over its entries, B-row starts
 __global__ void __launch_bounds__(256) k_heavy_entries(SymArgs g, SymScratch sc, int64_t first) {
     using Scan = cub::BlockScan<long long, 256>;
     __shared__ typename Scan::TempStorage tmp;
@@ -135,10 +138,9 @@ __global__ void __launch_bounds__(256) k_heavy_entries(SymArgs g, SymScratch sc,
     if (threadIdx.x == 0) ep[L] = s_carry;
 }
 
-// Locates unit u: item index, and the item's product window [p0, p1).
 struct Unit {
     int64_t item;
-    long long p0, p1;
+    long long p0, p1;  // product window of the item
 };
 
 __device__ __forceinline__ Unit find_unit(const SymScratch& sc, int64_t count, long long u) {
@@ -155,17 +157,20 @@ __device__ __forceinline__ Unit find_unit(const SymScratch& sc, int64_t count, l
     return r;
 }
 
-// Block-wide walk over products [p0, p1) of heavy item `item`, via its entry
-// prefix (chunks of BLOCK entries staged in shared memory).  fn(keys, valid).
+// Block-wide walk over products [p0, p1) of heavy item `item` (p1 - p0 <
+// 2^31): chunks of BLOCK entries are staged in shared memory with offsets
+// relative to p0 (clamped to [0, p1 - p0], B-row starts shifted to match) so
+// the per-product cursor works in 32-bit.  fn(keys, valid, q) with keys[u]
+// = product p0 + q + 32 u.
 template <int BLOCK, typename Fn>
 __device__ __forceinline__ void item_products(const SymArgs& g, const SymScratch& sc,
                                               int64_t first, int64_t item, long long p0,
-                                              long long p1, long long* s_off, int64_t* s_b0,
-                                              Fn&& fn) {
+                                              long long p1, int* s_off, int64_t* s_b0, Fn&& fn) {
     const ItemRow it = item_row(g, heavy_list(sc, first)[item]);
     const int64_t L = it.a1 - it.a0;
     const int64_t* ep = sc.heavy_epre + sc.heavy_eoff[item];
     const int64_t* eb = sc.heavy_eb0 + sc.heavy_eoff[item];
+    const long long span = p1 - p0;
     int64_t e0 = 0, e1 = L - 1;  // largest entry with ep[e] <= p0
     while (e0 < e1) {
         const int64_t mid = (e0 + e1 + 1) >> 1;
@@ -174,16 +179,15 @@ __device__ __forceinline__ void item_products(const SymArgs& g, const SymScratch
     for (int64_t e = e0;;) {
         const int n = static_cast<int>(L - e < BLOCK ? L - e : BLOCK);
         __syncthreads();  // previous chunk fully consumed
-        if (threadIdx.x < n) {
-            s_off[threadIdx.x] = ep[e + threadIdx.x];
-            s_b0[threadIdx.x] = eb[e + threadIdx.x];
+        for (int i = threadIdx.x; i <= n; i += BLOCK) {
+            const long long rel = ep[e + i] - p0;
+            const long long cl = rel < 0 ? 0 : (rel > span ? span : rel);
+            s_off[i] = static_cast<int>(cl);
+            if (i < n) s_b0[i] = eb[e + i] + (cl - rel);
         }
-        if (threadIdx.x == 0) s_off[n] = ep[e + n];
         __syncthreads();
-        const long long q0 = p0 > s_off[0] ? p0 : s_off[0];
-        const long long q1 = p1 < s_off[n] ? p1 : s_off[n];
-        chunk_products<BLOCK / 32>(s_off, s_b0, n, q0, q1, g.bcol, fn);
-        const bool done = s_off[n] >= p1 || e + n >= L;
+        chunk_products<BLOCK / 32>(s_off, s_b0, n, s_off[0], s_off[n], g.bcol, fn);
+        const bool done = s_off[n] >= span || e + n >= L;
         if (done) break;
         e += n;
     }
@@ -191,26 +195,33 @@ __device__ __forceinline__ void item_products(const SymArgs& g, const SymScratch
 }
 
 // ---- 1. per-unit histogram over column ranges
+template <bool PRIV>
 __global__ void __launch_bounds__(kHB) k_heavy_count(SymArgs g, SymScratch sc, int64_t first,
                                                      int64_t count, int R, int wshift) {
-    __shared__ long long s_off[kHB + 1];
+    constexpr int NW = PRIV ? kHW : 1, RM = PRIV ? kPrivRanges : kMaxRanges;
+    __shared__ int s_off[kHB + 1];
     __shared__ int64_t s_b0[kHB];
-    __shared__ int s_hist[kMaxRanges];
+    __shared__ int s_hist[NW][RM];
+    const int w = PRIV ? threadIdx.x >> 5 : 0;
     const long long units = sc.heavy_meta[0];
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit un = find_unit(sc, count, u);
-        for (int r = threadIdx.x; r < R; r += kHB) s_hist[r] = 0;
+        for (int k = threadIdx.x; k < NW * R; k += kHB) s_hist[k / R][k % R] = 0;
         item_products<kHB>(g, sc, first, un.item, un.p0, un.p1, s_off, s_b0,
                            [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll], long long) {
 #pragma unroll
                                for (int k = 0; k < kUnroll; ++k)
-                                   warp_bucket_add(s_hist, valid[k] ? (keys[k] >> wshift) : -1);
+                                   if (valid[k]) atomicAdd(&s_hist[w][keys[k] >> wshift], 1);
                            });
         long long* rc = sc.heavy_rc + un.item * R;
-        for (int r = threadIdx.x; r < R; r += kHB)
-            if (s_hist[r])
+        for (int r = threadIdx.x; r < R; r += kHB) {
+            int c = 0;
+#pragma unroll
+            for (int v = 0; v < NW; ++v) c += s_hist[v][r];
+            if (c)
                 atomicAdd(reinterpret_cast<unsigned long long*>(&rc[r]),
-                          static_cast<unsigned long long>(s_hist[r]));
+                          static_cast<unsigned long long>(c));
+        }
     }
 }
 
@@ -230,83 +241,93 @@ __global__ void k_heavy_offsets(SymScratch sc, int64_t count, int R) {
 }
 
 // ---- 3. scatter products into their range buckets
+template <bool PRIV>
 __global__ void __launch_bounds__(kHB) k_heavy_scatter(SymArgs g, SymScratch sc, int64_t first,
                                                        int64_t count, int R, int wshift) {
-    __shared__ long long s_off[kHB + 1];
+    constexpr int NW = PRIV ? kHW : 1, RM = PRIV ? kPrivRanges : kMaxRanges;
+    __shared__ int s_off[kHB + 1];
     __shared__ int64_t s_b0[kHB];
+    __shared__ int s_hist[NW][RM];      // counts, then per-warp cursors
+    __shared__ long long s_base[RM];    // global start of the unit's slice per range
     extern __shared__ int4 s_dyn_keys[];
-    // dynamic: keys[kHeavyUnitProducts] | base[R] (int64) | hist[R]
-    int32_t* s_keys = reinterpret_cast<int32_t*>(s_dyn_keys);
-    long long* s_base = reinterpret_cast<long long*>(s_keys + kHeavyUnitProducts);
-    int* s_hist = reinterpret_cast<int*>(s_base + R);
+    int32_t* s_keys = reinterpret_cast<int32_t*>(s_dyn_keys);  // kHeavyUnitProducts
+    const int w = PRIV ? threadIdx.x >> 5 : 0;
     const long long units = sc.heavy_meta[0];
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit un = find_unit(sc, count, u);
-        for (int r = threadIdx.x; r < R; r += kHB) s_hist[r] = 0;
-        // stage the unit's products (product p -> slot p - p0) and count ranges
+        for (int k = threadIdx.x; k < NW * R; k += kHB) s_hist[k / R][k % R] = 0;
         item_products<kHB>(g, sc, first, un.item, un.p0, un.p1, s_off, s_b0,
                            [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll],
-                               long long p) {
+                               long long q) {
 #pragma unroll
-                               for (int k = 0; k < kUnroll; ++k) {
-                                   if (valid[k]) s_keys[p + 32 * k - un.p0] = keys[k];
-                                   warp_bucket_add(s_hist, valid[k] ? (keys[k] >> wshift) : -1);
-                               }
+                               for (int k = 0; k < kUnroll; ++k)
+                                   if (valid[k]) s_keys[q + 32 * k] = keys[k];
                            });
-        // reserve each range's slice of the bucket, then reuse s_hist as the
-        // per-range cursor inside it
+        const int n = static_cast<int>(un.p1 - un.p0);
+        for (int i = threadIdx.x; i < n; i += kHB) atomicAdd(&s_hist[w][s_keys[i] >> wshift], 1);
+        __syncthreads();
+        // per range: reserve the unit's slice, turn the counts into per-warp offsets
         long long* cur = sc.heavy_cur + un.item * R;
         for (int r = threadIdx.x; r < R; r += kHB) {
-            const int c = s_hist[r];
-            s_base[r] = c ? static_cast<long long>(atomicAdd(
-                                reinterpret_cast<unsigned long long*>(&cur[r]),
-                                static_cast<unsigned long long>(c)))
-                          : 0;
-            s_hist[r] = 0;
+            int tot = 0;
+#pragma unroll
+            for (int v = 0; v < NW; ++v) {
+                const int c = s_hist[v][r];
+                s_hist[v][r] = tot;
+                tot += c;
+            }
+            s_base[r] = tot ? static_cast<long long>(atomicAdd(
+                                  reinterpret_cast<unsigned long long*>(&cur[r]),
+                                  static_cast<unsigned long long>(tot)))
+                            : 0;
         }
         __syncthreads();
-        const int n = static_cast<int>(un.p1 - un.p0);
-        for (int i0 = 0; i0 < n; i0 += kHB) {
-            const int i = i0 + threadIdx.x;
-            const int key = i < n ? s_keys[i] : 0;
-            const int r = i < n ? (key >> wshift) : -1;
-            const int rank = warp_bucket_add(s_hist, r);
-            if (i < n) sc.heavy_pbuf[s_base[r] + rank] = key;
+        for (int i = threadIdx.x; i < n; i += kHB) {  // same thread <-> item mapping
+            const int key = s_keys[i];
+            const int r = key >> wshift;
+            sc.heavy_pbuf[s_base[r] + atomicAdd(&s_hist[w][r], 1)] = key;
         }
         __syncthreads();
     }
 }
 
 // ---- 4. tasks per item (one thread per item; appends with one atomic)
-// Builds item i's task list; with out == nullptr it only counts.  Bitmap
-// tasks of a range that needs more than one task share a merge slot.
-__device__ int build_tasks(const SymScratch& sc, int64_t i, int R, HeavyTask* out) {
+// Builds item i's task list; with out == nullptr it only counts.
+__device__ int build_tasks(const SymScratch& sc, int64_t i, int R, int wshift, int32_t bcols,
+                           HeavyTask* out) {
     const int32_t item = static_cast<int32_t>(i);
     int k = 0;
-    auto bitmap = [&](int32_t range, long long p0, long long p1, int mode) {
-        const long long parts = (p1 - p0 + kBitmapTaskProducts - 1) / kBitmapTaskProducts;
+    // [p0, p1) products of one span starting at column `base`, `words` wide
+    auto emit = [&](int32_t base, int32_t words, long long p0, long long p1) {
+        const long long parts = (p1 - p0 + kTaskProducts - 1) / kTaskProducts;
         int32_t slot = -1;
         if (out && parts > 1)
             slot = static_cast<int32_t>(
                 atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[4]), 1ULL));
         for (long long q = 0; q < parts; ++q, ++k) {
             if (!out) continue;
-            const long long a = p0 + q * kBitmapTaskProducts;
-            const long long b = a + kBitmapTaskProducts < p1 ? a + kBitmapTaskProducts : p1;
-            out[k] = HeavyTask{item, slot, mode, range, a, b};
+            const long long a = p0 + q * kTaskProducts;
+            const long long b = a + kTaskProducts < p1 ? a + kTaskProducts : p1;
+            out[k] = HeavyTask{item, slot, base, words, a, b};
         }
     };
-    if (R == 1) {  // whole row in one range, read from the B rows
-        bitmap(0, 0, sc.heavy_foff[i + 1] - sc.heavy_foff[i], 2);
+    if (R == 1) {  // whole row in one span, read from the B rows
+        emit(0, static_cast<int32_t>((int64_t(bcols) + 31) / 32), 0,
+             sc.heavy_foff[i + 1] - sc.heavy_foff[i]);
         return k;
     }
+    const int per_span = 1 << (kSpanShift - wshift);  // ranges per 2^20-column span
+    const int32_t wwords = static_cast<int32_t>((int64_t(1) << wshift) / 32);
     const long long* rc = sc.heavy_rc + i * R;
     const long long end = sc.heavy_foff[i + 1];
-    long long g0 = -1, g1 = -1;  // open hash group [g0, g1) of the product buffer
+    int g0 = -1, g1 = -1;  // open group of ranges [g0, g1)
     auto flush = [&]() {
-        if (g0 >= 0 && g1 > g0) {
-            if (out) out[k] = HeavyTask{item, -1, 0, 0, g0, g1};
-            ++k;
+        if (g0 >= 0) {
+            const long long a = rc[g0], b = g1 < R ? rc[g1] : end;
+            if (b > a) {
+                if (out) out[k] = HeavyTask{item, -1, g0 << wshift, (g1 - g0) * wwords, a, b};
+                ++k;
+            }
         }
         g0 = g1 = -1;
     };
@@ -314,102 +335,82 @@ __device__ int build_tasks(const SymScratch& sc, int64_t i, int R, HeavyTask* ou
         const long long b0 = rc[r];
         const long long b1 = r + 1 < R ? rc[r + 1] : end;
         if (b1 == b0) continue;
-        if (b1 - b0 > kHashTaskProducts) {
+        if (b1 - b0 > kTaskProducts) {  // one range, several tasks, merged
             flush();
-            bitmap(r, b0, b1, 1);
-        } else if (g0 >= 0 && b1 - g0 <= kHashTaskProducts) {
-            g1 = b1;
+            emit(r << wshift, wwords, b0, b1);
+        } else if (g0 >= 0 && r + 1 - g0 <= per_span && b1 - rc[g0] <= kTaskProducts) {
+            g1 = r + 1;
         } else {
             flush();
-            g0 = b0;
-            g1 = b1;
+            g0 = r;
+            g1 = r + 1;
         }
     }
     flush();
     return k;
 }
 
-__global__ void k_heavy_tasks(SymScratch sc, int64_t count, int R, int64_t task_cap) {
+__global__ void k_heavy_tasks(SymScratch sc, int64_t count, int R, int wshift, int32_t bcols,
+                              int64_t task_cap) {
     const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (i >= count) return;
-    const int n = build_tasks(sc, i, R, nullptr);
+    const int n = build_tasks(sc, i, R, wshift, bcols, nullptr);
     const long long base = static_cast<long long>(atomicAdd(
         reinterpret_cast<unsigned long long*>(&sc.heavy_meta[3]), static_cast<unsigned long long>(n)));
     if (base + n > task_cap) __trap();  // host sizes task_cap to heavy_task_bound()
-    build_tasks(sc, i, R, reinterpret_cast<HeavyTask*>(sc.heavy_tasks) + base);
+    build_tasks(sc, i, R, wshift, bcols, reinterpret_cast<HeavyTask*>(sc.heavy_tasks) + base);
 }
 
-// ---- 5. run the tasks: one block per task, sets in shared memory.  Hash
-// tasks (192 KB table) and bitmap tasks (W-bit bitmap, <= 128 KB) run in two
-// kernels so each gets 1024 threads per SM.
-template <bool HASH>
+// ---- 5. run the tasks: one block per task, a <= 2^20-bit shared bitmap
 __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch sc, int64_t first,
-                                                         int32_t wwords, int wshift) {
+                                                         int R, int wshift) {
     extern __shared__ int4 s_dyn[];
     uint32_t* s_set = reinterpret_cast<uint32_t*>(s_dyn);
-    __shared__ long long s_off[kRunBlock + 1];
+    __shared__ int s_off[kRunBlock + 1];
     __shared__ int64_t s_b0[kRunBlock];
     __shared__ long long s_red[kRunBlock / 32];
     const HeavyTask* tasks = reinterpret_cast<const HeavyTask*>(sc.heavy_tasks);
     const long long ntask = sc.heavy_meta[3];
     const int32_t* list = heavy_list(sc, first);
+    const int32_t wwords = static_cast<int32_t>((int64_t(1) << wshift) / 32);
     long long acc = 0;
     for (long long ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
         const HeavyTask t = tasks[ti];
-        if ((t.mode == 0) != HASH) continue;  // the other kernel's task
+        for (int k = threadIdx.x; k < t.words; k += kRunBlock) s_set[k] = 0u;
+        __syncthreads();
         int cnt = 0;
-        if (HASH) {
-            int* table = reinterpret_cast<int*>(s_set);
-            for (int k = threadIdx.x; k < kHashSlots; k += kRunBlock) table[k] = kEmpty;
-            __syncthreads();
+        auto insert = [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll], long long) {
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+                if (valid[u]) {
+                    const uint32_t off = static_cast<uint32_t>(keys[u] - t.col_base);
+                    const uint32_t bit = 1u << (off & 31);
+                    cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
+                }
+        };
+        if (R > 1) {
             for (long long p = t.p0 + threadIdx.x; p < t.p1; p += kRunBlock * kUnroll) {
                 int keys[kUnroll];
+                bool valid[kUnroll];
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u) {
                     const long long q = p + u * kRunBlock;
-                    keys[u] = q < t.p1 ? __ldg(&sc.heavy_pbuf[q]) : kEmpty;
+                    valid[u] = q < t.p1;
+                    keys[u] = valid[u] ? __ldg(&sc.heavy_pbuf[q]) : 0;
                 }
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u)
-                    if (keys[u] != kEmpty) cnt += hash_insert(table, kHashSlots, keys[u]);
+                insert(keys, valid, 0);
             }
         } else {
-            for (int k = threadIdx.x; k < wwords; k += kRunBlock) s_set[k] = 0u;
+            item_products<kRunBlock>(g, sc, first, t.item, t.p0, t.p1, s_off, s_b0, insert);
+        }
+        if (t.slot >= 0) {
+            // range shared by several tasks: the bits this task adds first
             __syncthreads();
-            const uint32_t lo_mask = (1u << wshift) - 1u;  // column offset inside the range
-            auto insert = [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll], long long) {
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u)
-                    if (valid[u]) {
-                        const uint32_t off = static_cast<uint32_t>(keys[u]) & lo_mask;
-                        const uint32_t bit = 1u << (off & 31);
-                        cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
-                    }
-            };
-            if (t.mode == 1) {
-                for (long long p = t.p0 + threadIdx.x; p < t.p1; p += kRunBlock * kUnroll) {
-                    int keys[kUnroll];
-                    bool valid[kUnroll];
-#pragma unroll
-                    for (int u = 0; u < kUnroll; ++u) {
-                        const long long q = p + u * kRunBlock;
-                        valid[u] = q < t.p1;
-                        keys[u] = valid[u] ? __ldg(&sc.heavy_pbuf[q]) : 0;
-                    }
-                    insert(keys, valid, 0);
-                }
-            } else {
-                item_products<kRunBlock>(g, sc, first, t.item, t.p0, t.p1, s_off, s_b0, insert);
-            }
-            if (t.slot >= 0) {
-                // shared range: the bits this task adds first are what counts
-                __syncthreads();
-                cnt = 0;
-                uint32_t* gbm = sc.pool + int64_t(t.slot) * wwords;
-                for (int k = threadIdx.x; k < wwords; k += kRunBlock) {
-                    const uint32_t w = s_set[k];
-                    if (w) cnt += __popc(w & ~atomicOr(&gbm[k], w));
-                }
+            cnt = 0;
+            uint32_t* gbm = sc.pool + int64_t(t.slot) * wwords;
+            for (int k = threadIdx.x; k < t.words; k += kRunBlock) {
+                const uint32_t w = s_set[k];
+                if (w) cnt += __popc(w & ~atomicOr(&gbm[k], w));
             }
         }
         const long long tot = block_sum_ll<kRunBlock>(cnt, s_red);
@@ -436,8 +437,8 @@ __global__ void k_heavy_flops(SymArgs g, SymScratch sc, int64_t count, int64_t* 
 }
 
 // ---- 6. return the used merge bitmaps to zero
-__global__ void k_heavy_clean(SymScratch sc, int32_t wwords) {
-    const long long used = sc.heavy_meta[4] * wwords;
+__global__ void k_heavy_clean(SymScratch sc, int64_t slot_words) {
+    const long long used = sc.heavy_meta[4] * slot_words;
     for (long long i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < used;
          i += int64_t(gridDim.x) * blockDim.x)
         sc.pool[i] = 0u;
@@ -447,25 +448,30 @@ __global__ void k_heavy_clean(SymScratch sc, int32_t wwords) {
 
 HeavyGeometry heavy_geometry(int32_t bcols) {
     HeavyGeometry h;
-    int shift = 5;
-    while ((int64_t(1) << shift) < bcols && shift < 20) ++shift;
-    h.wshift = shift;  // range width 2^shift bits (>= 32, <= 2^20)
-    h.ranges = static_cast<int>((int64_t(bcols) + (int64_t(1) << shift) - 1) >> shift);
-    if (h.ranges < 1) h.ranges = 1;
-    h.wwords = static_cast<int32_t>((int64_t(1) << shift) / 32);
+    int lg = 5;
+    while ((int64_t(1) << lg) < bcols) ++lg;  // 2^lg >= B.cols
+    if (lg <= kSpanShift) {
+        h.wshift = lg;
+        h.ranges = 1;
+    } else {
+        int ws = lg - 8;  // R <= 256
+        if (ws < 17) ws = 17;
+        if (ws > kSpanShift) ws = kSpanShift;
+        h.wshift = ws;
+        h.ranges = static_cast<int>((int64_t(bcols) + (int64_t(1) << ws) - 1) >> ws);
+    }
+    h.wwords = static_cast<int32_t>(((int64_t(1) << h.wshift) + 31) / 32);
     return h;
 }
 
 int64_t heavy_task_bound(int64_t count, int64_t products, int ranges) {
-    // hash groups: at most 2 per kHashTaskProducts of products plus one per
-    // item; bitmap parts: one per kBitmapTaskProducts plus one per range
-    return count * (ranges + 2) + 2 * (products / kHashTaskProducts + 1) +
-           products / kBitmapTaskProducts + 1;
+    // groups: at most one per non-empty range, plus split parts
+    return count * (int64_t(ranges) + 1) + 2 * (products / kTaskProducts + 1);
 }
 
 int64_t heavy_slot_bound(int64_t, int64_t products) {
-    // a merge slot serves one range that needs >= 2 bitmap tasks
-    return products / kBitmapTaskProducts + 1;
+    // a merge slot serves one range (or row) that needs >= 2 tasks
+    return products / kTaskProducts + 1;
 }
 
 cudaError_t launch_heavy_flops(const SymArgs& args, const SymScratch& s, int64_t count,
@@ -482,35 +488,38 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, int64_t f
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_done & (1u << (dev & 31)))) {
-        cudaFuncSetAttribute(k_heavy_run<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kHashSlots * 4);
-        cudaFuncSetAttribute(k_heavy_run<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (1 << 20) / 8);
-        cudaFuncSetAttribute(k_heavy_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kHeavyUnitProducts * 4 + kMaxRanges * 12));
+        cudaFuncSetAttribute(k_heavy_run, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (1 << kSpanShift) / 8);
+        cudaFuncSetAttribute(k_heavy_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kHeavyUnitProducts * 4));
+        cudaFuncSetAttribute(k_heavy_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kHeavyUnitProducts * 4));
         attr_done |= 1u << (dev & 31);
     }
     const HeavyGeometry geo = heavy_geometry(args.bcols);
+    const int R = geo.ranges;
     k_heavy_prep<<<1, 256, 0, stream>>>(args, s, first, count);
     k_heavy_entries<<<static_cast<unsigned>(count), 256, 0, stream>>>(args, s, first);
-    const unsigned grid = static_cast<unsigned>(num_sms) * 8;
-    if (geo.ranges > 1) {
-        cudaMemsetAsync(s.heavy_rc, 0, sizeof(long long) * count * geo.ranges, stream);
-        k_heavy_count<<<grid, kHB, 0, stream>>>(args, s, first, count, geo.ranges, geo.wshift);
-        k_heavy_offsets<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(
-            s, count, geo.ranges);
-        const int scatter_smem = int(kHeavyUnitProducts * 4 + geo.ranges * 12);
-        k_heavy_scatter<<<static_cast<unsigned>(num_sms) * 6, kHB, scatter_smem, stream>>>(
-            args, s, first, count, geo.ranges, geo.wshift);
+    const unsigned sms = static_cast<unsigned>(num_sms);
+    if (R > 1) {
+        cudaMemsetAsync(s.heavy_rc, 0, sizeof(long long) * count * R, stream);
+        const int keys_smem = int(kHeavyUnitProducts * 4);
+        if (R <= kPrivRanges) {
+            k_heavy_count<true><<<sms * 8, kHB, 0, stream>>>(args, s, first, count, R, geo.wshift);
+            k_heavy_offsets<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(s, count, R);
+            k_heavy_scatter<true><<<sms * 4, kHB, keys_smem, stream>>>(args, s, first, count, R,
+                                                                       geo.wshift);
+        } else {
+            k_heavy_count<false><<<sms * 8, kHB, 0, stream>>>(args, s, first, count, R, geo.wshift);
+            k_heavy_offsets<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(s, count, R);
+            k_heavy_scatter<false><<<sms * 2, kHB, keys_smem, stream>>>(args, s, first, count, R,
+                                                                        geo.wshift);
+        }
     }
     k_heavy_tasks<<<static_cast<unsigned>((count + 127) / 128), 128, 0, stream>>>(
-        s, count, geo.ranges, s.heavy_task_cap);
-    if (geo.ranges > 1)
-        k_heavy_run<true><<<static_cast<unsigned>(num_sms), kRunBlock, kHashSlots * 4, stream>>>(
-            args, s, first, geo.wwords, geo.wshift);
-    k_heavy_run<false><<<static_cast<unsigned>(num_sms), kRunBlock, geo.wwords * 4, stream>>>(
-        args, s, first, geo.wwords, geo.wshift);
-    k_heavy_clean<<<static_cast<unsigned>(num_sms) * 4, 256, 0, stream>>>(s, geo.wwords);
+        s, count, R, geo.wshift, args.bcols, s.heavy_task_cap);
+    k_heavy_run<<<sms, kRunBlock, (1 << kSpanShift) / 8, stream>>>(args, s, first, R, geo.wshift);
+    k_heavy_clean<<<sms * 4, 256, 0, stream>>>(s, int64_t(geo.wwords));
     return cudaGetLastError();
 }
 
