@@ -111,7 +111,9 @@ __device__ __forceinline__ long long warp_max_ll(long long v) {
     return v;
 }
 
-// Block-wide int64 sum/max of per-thread values (all threads get the result).
+// Block-wide int64 sum/max of per-thread values.  The result is valid in
+// warp 0 (callers use it from thread 0); the scratch may be reused by the
+// next call (leading barrier).
 template <int BLOCK>
 __device__ __forceinline__ long long block_sum_ll(long long v, long long* scratch /* BLOCK/32 */) {
     v = warp_sum_ll(v);
@@ -120,8 +122,10 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long* scratc
     if (l == 0) scratch[w] = v;
     __syncthreads();
     long long t = 0;
-#pragma unroll
-    for (int i = 0; i < BLOCK / 32; ++i) t += scratch[i];
+    if (w == 0) {
+        t = l < BLOCK / 32 ? scratch[l] : 0;
+        t = warp_sum_ll(t);
+    }
     return t;
 }
 
@@ -133,8 +137,10 @@ __device__ __forceinline__ long long block_max_ll(long long v, long long* scratc
     if (l == 0) scratch[w] = v;
     __syncthreads();
     long long t = 0;
-#pragma unroll
-    for (int i = 0; i < BLOCK / 32; ++i) t = scratch[i] > t ? scratch[i] : t;
+    if (w == 0) {
+        t = l < BLOCK / 32 ? scratch[l] : 0;
+        t = warp_max_ll(t);
+    }
     return t;
 }
 

@@ -5,28 +5,31 @@
 // its distinct set does not fit one SM.  A per-row global bitmap (2 MB at
 // config 5, ~850 rows in flight) thrashes L2 into gigabytes of DRAM
 // read-modify-write, so instead the row's products are bucketed by column
-// range and every bucket is counted on chip in a shared-memory bitmap:
+// range (ranges of W = 2^wshift columns) and every bucket is counted on chip:
 //   0. prep/entries  per batch: unit, entry and product offsets of every
 //                    heavy row; per row, the product prefix over its entries;
 //   1. count    per unit of kHeavyUnitProducts products (one block): per-warp
-//               shared histograms over the R column ranges of width W;
+//               shared histograms over the R ranges, added into the row's
+//               bucket counts;
 //   2. offsets  per row, bucket starts in the product buffer;
-//   3. scatter  per unit again: stage the products in shared memory, count
-//               them per warp and range, reserve each range's slice with one
-//               global atomic, and write them out grouped by range;
-//   4. tasks    per row, consecutive ranges are packed into tasks spanning at
-//               most 2^20 columns (a 128 KB shared bitmap) and at most
-//               kTaskProducts products; a range with more products is split
-//               into several tasks that share a merge slot;
-//   5. run      one 1024-thread block per task: clear the span's bitmap,
-//               atomicOr each product's bit and count the bits it set first.
-//               Tasks that share a range then OR their non-zero words into a
-//               global W-bit merge bitmap and count popc(word & ~old) instead.
-// B.cols <= 2^20 (configs 2 and 4): one range covers all columns, steps 1-3
-// are skipped and tasks read their product slice straight from the B rows.
+//   3. place    per unit again: stage the products in shared memory, counting-
+//               sort them by range, reserve each range's slice of its bucket
+//               with one atomic and write the sorted runs out (coalesced);
+//   4. tasks    per row, its buckets are cut into aligned spans of 2^19
+//               columns (a 64 KB shared bitmap); a span is one task, or, above
+//               kTaskProducts products, several tasks that share a merge slot;
+//   5. run      one 512-thread block per task (3 per SM) reads its span's
+//               contiguous products, atomicOr's each bit into the bitmap and
+//               counts the bits it set first; tasks sharing a span OR their
+//               non-zero words into a global merge bitmap and count
+//               popc(word & ~old) instead.  The bitmap is returned to zero by
+//               re-walking the keys (sparse spans) or clearing it.
+// B.cols <= 2^20 (configs 2 and 4): one range covers all columns; tasks are
+// slices of the row's product range read straight from the B rows (1024
+// threads, 128 KB bitmap).
 // W = max(2^17, 2^ceil(log2 B.cols) / 256) keeps R <= 256 (per-warp
-// histograms) up to B.cols = 2^28; beyond that W = 2^20 and the histograms
-// are shared.  Every count is a set cardinality: exact and independent of
+// histograms) up to B.cols = 2^27; beyond that W = 2^19 with shared
+// histograms.  Every count is a set cardinality: exact and independent of
 // bucketing, task boundaries and scheduling.
 #include "symbolic_common.cuh"
 
@@ -36,18 +39,17 @@ using namespace sym;
 
 constexpr int kHB = 256;                  // block of the unit passes
 constexpr int kHW = kHB / 32;             // warps per unit block
-constexpr int kRunBlock = 1024;           // block of the task runner
-constexpr int kSpanShift = 20;            // task column span <= 2^20 (128 KB)
+constexpr int kSpanShift = 20;            // R == 1: one span of <= 2^20 columns (128 KB)
+constexpr int kTaskSpanShift = 19;        // R > 1: task spans of <= 2^19 columns (64 KB)
 constexpr int kPrivRanges = 256;          // per-warp histograms up to this R
-constexpr int kMaxRanges = 2048;          // B.cols < 2^31 with W = 2^20
+constexpr int kMaxRanges = 4096;          // B.cols < 2^31 with W = 2^19
 constexpr int64_t kTaskProducts = 131072;
 
 struct HeavyTask {
-    int32_t item;      // index in the batch
-    int32_t slot;      // merge bitmap slot, or -1
-    int32_t col_base;  // first column of the task's span
-    int32_t words;     // span / 32 (bitmap words to clear)
-    int64_t p0, p1;    // R > 1: product-buffer span; R == 1: the item's product range
+    int32_t item;    // index in the batch
+    int32_t slot;    // merge bitmap slot, or -1
+    int32_t r0, r1;  // column ranges [r0, r1) (R > 1)
+    int64_t a, b;    // R > 1: product-buffer span; R == 1: the item's product range
 };
 static_assert(sizeof(HeavyTask) == 32, "task layout");
 
@@ -157,6 +159,15 @@ __device__ __forceinline__ Unit find_unit(const SymScratch& sc, int64_t count, l
     return r;
 }
 
+// Thread 0 locates unit u, every thread gets it (block-uniform call).
+__device__ __forceinline__ Unit find_unit_block(const SymScratch& sc, int64_t count, long long u) {
+    __shared__ Unit s_unit;
+    __syncthreads();
+    if (threadIdx.x == 0) s_unit = find_unit(sc, count, u);
+    __syncthreads();
+    return s_unit;
+}
+
 // Block-wide walk over products [p0, p1) of heavy item `item` (p1 - p0 <
 // 2^31): chunks of BLOCK entries are staged in shared memory with offsets
 // relative to p0 (clamped to [0, p1 - p0], B-row starts shifted to match) so
@@ -171,12 +182,18 @@ __device__ __forceinline__ void item_products(const SymArgs& g, const SymScratch
     const int64_t* ep = sc.heavy_epre + sc.heavy_eoff[item];
     const int64_t* eb = sc.heavy_eb0 + sc.heavy_eoff[item];
     const long long span = p1 - p0;
-    int64_t e0 = 0, e1 = L - 1;  // largest entry with ep[e] <= p0
-    while (e0 < e1) {
-        const int64_t mid = (e0 + e1 + 1) >> 1;
-        if (ep[mid] <= p0) e0 = mid; else e1 = mid - 1;
+    __shared__ int64_t s_e0;
+    __syncthreads();  // s_e0 of a previous call is consumed
+    if (threadIdx.x == 0) {
+        int64_t e0 = 0, e1 = L - 1;  // largest entry with ep[e] <= p0
+        while (e0 < e1) {
+            const int64_t mid = (e0 + e1 + 1) >> 1;
+            if (ep[mid] <= p0) e0 = mid; else e1 = mid - 1;
+        }
+        s_e0 = e0;
     }
-    for (int64_t e = e0;;) {
+    __syncthreads();
+    for (int64_t e = s_e0;;) {
         const int n = static_cast<int>(L - e < BLOCK ? L - e : BLOCK);
         __syncthreads();  // previous chunk fully consumed
         for (int i = threadIdx.x; i <= n; i += BLOCK) {
@@ -194,7 +211,7 @@ __device__ __forceinline__ void item_products(const SymArgs& g, const SymScratch
     __syncthreads();
 }
 
-// ---- 1. per-unit histogram over column ranges
+// ---- 1. per-unit histogram over column ranges, added to the bucket counts
 template <bool PRIV>
 __global__ void __launch_bounds__(kHB) k_heavy_count(SymArgs g, SymScratch sc, int64_t first,
                                                      int64_t count, int R, int wshift) {
@@ -205,7 +222,7 @@ __global__ void __launch_bounds__(kHB) k_heavy_count(SymArgs g, SymScratch sc, i
     const int w = PRIV ? threadIdx.x >> 5 : 0;
     const long long units = sc.heavy_meta[0];
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit un = find_unit(sc, count, u);
+        const Unit un = find_unit_block(sc, count, u);
         for (int k = threadIdx.x; k < NW * R; k += kHB) s_hist[k / R][k % R] = 0;
         item_products<kHB>(g, sc, first, un.item, un.p0, un.p1, s_off, s_b0,
                            [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll], long long) {
@@ -225,48 +242,65 @@ __global__ void __launch_bounds__(kHB) k_heavy_count(SymArgs g, SymScratch sc, i
     }
 }
 
-// ---- 2. bucket offsets (exclusive prefix per item, placed at foff[item])
+// ---- 2. bucket starts (exclusive prefix per item, placed at foff[item])
 __global__ void k_heavy_offsets(SymScratch sc, int64_t count, int R) {
-    const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (i >= count) return;
-    long long acc = sc.heavy_foff[i];
+    const int64_t i = blockIdx.x;
+    using Scan = cub::BlockScan<long long, 256>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ long long s_carry;
+    if (threadIdx.x == 0) s_carry = sc.heavy_foff[i];
+    __syncthreads();
     long long* rc = sc.heavy_rc + i * R;
     long long* cur = sc.heavy_cur + i * R;
-    for (int r = 0; r < R; ++r) {
-        const long long c = rc[r];
-        rc[r] = acc;
-        cur[r] = acc;
-        acc += c;
+    for (int r0 = 0; r0 < R; r0 += 256) {
+        const int r = r0 + threadIdx.x;
+        const long long c = r < R ? rc[r] : 0;
+        long long ex, tot;
+        Scan(tmp).ExclusiveSum(c, ex, tot);
+        if (r < R) {
+            rc[r] = s_carry + ex;
+            cur[r] = s_carry + ex;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += tot;
+        __syncthreads();
     }
 }
 
-// ---- 3. scatter products into their range buckets
+// ---- 3. place: counting-sort each unit by range in shared memory, write the
+// sorted runs to their bucket slices (coalesced)
 template <bool PRIV>
-__global__ void __launch_bounds__(kHB) k_heavy_scatter(SymArgs g, SymScratch sc, int64_t first,
-                                                       int64_t count, int R, int wshift) {
+__global__ void __launch_bounds__(kHB) k_heavy_place(SymArgs g, SymScratch sc, int64_t first,
+                                                     int64_t count, int R, int wshift) {
     constexpr int NW = PRIV ? kHW : 1, RM = PRIV ? kPrivRanges : kMaxRanges;
     __shared__ int s_off[kHB + 1];
     __shared__ int64_t s_b0[kHB];
-    __shared__ int s_hist[NW][RM];      // counts, then per-warp cursors
-    __shared__ long long s_base[RM];    // global start of the unit's slice per range
-    extern __shared__ int4 s_dyn_keys[];
-    int32_t* s_keys = reinterpret_cast<int32_t*>(s_dyn_keys);  // kHeavyUnitProducts
+    // dynamic: dst_base[RM] (int64: bucket position of the unit's first key of
+    //          range r, minus its sorted position) | keys_in[U] | keys_out[U] |
+    //          hist[NW][RM] | offs[RM + 1]
+    extern __shared__ int4 s_dyn_place[];
+    long long* s_dst = reinterpret_cast<long long*>(s_dyn_place);
+    int32_t* s_in = reinterpret_cast<int32_t*>(s_dst + RM);
+    int32_t* s_out = s_in + kHeavyUnitProducts;
+    int (*s_hist)[RM] = reinterpret_cast<int (*)[RM]>(s_out + kHeavyUnitProducts);
+    int* s_offs = reinterpret_cast<int*>(s_hist + NW);
     const int w = PRIV ? threadIdx.x >> 5 : 0;
+    const int lane = threadIdx.x & 31;
     const long long units = sc.heavy_meta[0];
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit un = find_unit(sc, count, u);
+        const Unit un = find_unit_block(sc, count, u);
         for (int k = threadIdx.x; k < NW * R; k += kHB) s_hist[k / R][k % R] = 0;
         item_products<kHB>(g, sc, first, un.item, un.p0, un.p1, s_off, s_b0,
                            [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll],
                                long long q) {
 #pragma unroll
                                for (int k = 0; k < kUnroll; ++k)
-                                   if (valid[k]) s_keys[q + 32 * k] = keys[k];
+                                   if (valid[k]) s_in[q + 32 * k] = keys[k];
                            });
         const int n = static_cast<int>(un.p1 - un.p0);
-        for (int i = threadIdx.x; i < n; i += kHB) atomicAdd(&s_hist[w][s_keys[i] >> wshift], 1);
+        for (int i = threadIdx.x; i < n; i += kHB) atomicAdd(&s_hist[w][s_in[i] >> wshift], 1);
         __syncthreads();
-        // per range: reserve the unit's slice, turn the counts into per-warp offsets
+        // per range: totals, per-warp offsets inside the range, bucket reservation
         long long* cur = sc.heavy_cur + un.item * R;
         for (int r = threadIdx.x; r < R; r += kHB) {
             int tot = 0;
@@ -276,153 +310,196 @@ __global__ void __launch_bounds__(kHB) k_heavy_scatter(SymArgs g, SymScratch sc,
                 s_hist[v][r] = tot;
                 tot += c;
             }
-            s_base[r] = tot ? static_cast<long long>(atomicAdd(
-                                  reinterpret_cast<unsigned long long*>(&cur[r]),
-                                  static_cast<unsigned long long>(tot)))
-                            : 0;
+            s_offs[r] = tot;
+            s_dst[r] = tot ? static_cast<long long>(atomicAdd(
+                                 reinterpret_cast<unsigned long long*>(&cur[r]),
+                                 static_cast<unsigned long long>(tot)))
+                           : 0;
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // exclusive scan of the R totals by warp 0
+            const int per = (R + 31) / 32;
+            const int r0 = lane * per, r1 = r0 + per < R ? r0 + per : R;
+            int sum = 0;
+            for (int r = r0; r < r1; ++r) sum += s_offs[r];
+            int incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int run = incl - sum;
+            for (int r = r0; r < r1; ++r) {
+                const int c = s_offs[r];
+                s_offs[r] = run;
+                s_dst[r] -= run;  // position i of range r goes to s_dst[r] + i
+                run += c;
+            }
+            if (lane == 31) s_offs[R] = incl;
         }
         __syncthreads();
         for (int i = threadIdx.x; i < n; i += kHB) {  // same thread <-> item mapping
-            const int key = s_keys[i];
+            const int key = s_in[i];
             const int r = key >> wshift;
-            sc.heavy_pbuf[s_base[r] + atomicAdd(&s_hist[w][r], 1)] = key;
+            s_out[s_offs[r] + atomicAdd(&s_hist[w][r], 1)] = key;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += kHB) {
+            const int key = s_out[i];
+            sc.heavy_pbuf[s_dst[key >> wshift] + i] = key;
         }
         __syncthreads();
     }
 }
 
-// ---- 4. tasks per item (one thread per item; appends with one atomic)
-// Builds item i's task list; with out == nullptr it only counts.
-__device__ int build_tasks(const SymScratch& sc, int64_t i, int R, int wshift, int32_t bcols,
-                           HeavyTask* out) {
-    const int32_t item = static_cast<int32_t>(i);
-    int k = 0;
-    // [p0, p1) products of one span starting at column `base`, `words` wide
-    auto emit = [&](int32_t base, int32_t words, long long p0, long long p1) {
-        const long long parts = (p1 - p0 + kTaskProducts - 1) / kTaskProducts;
-        int32_t slot = -1;
-        if (out && parts > 1)
-            slot = static_cast<int32_t>(
-                atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[4]), 1ULL));
-        for (long long q = 0; q < parts; ++q, ++k) {
-            if (!out) continue;
-            const long long a = p0 + q * kTaskProducts;
-            const long long b = a + kTaskProducts < p1 ? a + kTaskProducts : p1;
-            out[k] = HeavyTask{item, slot, base, words, a, b};
-        }
-    };
-    if (R == 1) {  // whole row in one span, read from the B rows
-        emit(0, static_cast<int32_t>((int64_t(bcols) + 31) / 32), 0,
-             sc.heavy_foff[i + 1] - sc.heavy_foff[i]);
-        return k;
-    }
-    const int per_span = 1 << (kSpanShift - wshift);  // ranges per 2^20-column span
-    const int32_t wwords = static_cast<int32_t>((int64_t(1) << wshift) / 32);
+// ---- 4. tasks
+// R > 1: one block per item, one thread per aligned span.
+__global__ void __launch_bounds__(128) k_heavy_plan(SymScratch sc, int64_t count, int R,
+                                                    int wshift, int64_t task_cap) {
+    using Scan = cub::BlockScan<int, 128>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ long long s_base;
+    const int64_t i = blockIdx.x;
+    const int per_span = 1 << (kTaskSpanShift - wshift);
+    const int S = (R + per_span - 1) / per_span;
     const long long* rc = sc.heavy_rc + i * R;
     const long long end = sc.heavy_foff[i + 1];
-    int g0 = -1, g1 = -1;  // open group of ranges [g0, g1)
-    auto flush = [&]() {
-        if (g0 >= 0) {
-            const long long a = rc[g0], b = g1 < R ? rc[g1] : end;
-            if (b > a) {
-                if (out) out[k] = HeavyTask{item, -1, g0 << wshift, (g1 - g0) * wwords, a, b};
-                ++k;
+    HeavyTask* tasks = reinterpret_cast<HeavyTask*>(sc.heavy_tasks);
+    for (int s0 = 0; s0 < S; s0 += 128) {
+        const int sp = s0 + threadIdx.x;
+        const int r0 = sp * per_span, r1 = r0 + per_span < R ? r0 + per_span : R;
+        long long a = 0, b = 0;
+        int parts = 0;
+        if (sp < S) {
+            a = rc[r0];
+            b = r1 < R ? rc[r1] : end;
+            parts = static_cast<int>((b - a + kTaskProducts - 1) / kTaskProducts);
+        }
+        int excl, total;
+        Scan(tmp).ExclusiveSum(parts, excl, total);
+        if (threadIdx.x == 0)
+            s_base = static_cast<long long>(atomicAdd(
+                reinterpret_cast<unsigned long long*>(&sc.heavy_meta[3]),
+                static_cast<unsigned long long>(total)));
+        __syncthreads();
+        if (s_base + total > task_cap) __trap();  // host sizes task_cap to heavy_task_bound()
+        if (parts > 0) {
+            const int32_t slot = parts > 1 ? static_cast<int32_t>(atomicAdd(
+                                                 reinterpret_cast<unsigned long long*>(&sc.heavy_meta[4]), 1ULL))
+                                           : -1;
+            HeavyTask* out = tasks + s_base + excl;
+            for (int q = 0; q < parts; ++q) {
+                const long long p = a + q * kTaskProducts;
+                out[q] = HeavyTask{static_cast<int32_t>(i), slot, r0, r1, p,
+                                   p + kTaskProducts < b ? p + kTaskProducts : b};
             }
         }
-        g0 = g1 = -1;
-    };
-    for (int r = 0; r < R; ++r) {
-        const long long b0 = rc[r];
-        const long long b1 = r + 1 < R ? rc[r + 1] : end;
-        if (b1 == b0) continue;
-        if (b1 - b0 > kTaskProducts) {  // one range, several tasks, merged
-            flush();
-            emit(r << wshift, wwords, b0, b1);
-        } else if (g0 >= 0 && r + 1 - g0 <= per_span && b1 - rc[g0] <= kTaskProducts) {
-            g1 = r + 1;
-        } else {
-            flush();
-            g0 = r;
-            g1 = r + 1;
-        }
+        __syncthreads();
     }
-    flush();
-    return k;
 }
 
-__global__ void k_heavy_tasks(SymScratch sc, int64_t count, int R, int wshift, int32_t bcols,
-                              int64_t task_cap) {
+// R == 1: one thread per item, parts of its product range.
+__global__ void k_heavy_tasks_r1(SymScratch sc, int64_t count, int64_t task_cap) {
     const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (i >= count) return;
-    const int n = build_tasks(sc, i, R, wshift, bcols, nullptr);
+    const long long f = sc.heavy_foff[i + 1] - sc.heavy_foff[i];
+    const long long parts = (f + kTaskProducts - 1) / kTaskProducts;
+    if (parts == 0) return;
     const long long base = static_cast<long long>(atomicAdd(
-        reinterpret_cast<unsigned long long*>(&sc.heavy_meta[3]), static_cast<unsigned long long>(n)));
-    if (base + n > task_cap) __trap();  // host sizes task_cap to heavy_task_bound()
-    build_tasks(sc, i, R, wshift, bcols, reinterpret_cast<HeavyTask*>(sc.heavy_tasks) + base);
+        reinterpret_cast<unsigned long long*>(&sc.heavy_meta[3]), static_cast<unsigned long long>(parts)));
+    if (base + parts > task_cap) __trap();
+    const int32_t slot = parts > 1 ? static_cast<int32_t>(atomicAdd(
+                                         reinterpret_cast<unsigned long long*>(&sc.heavy_meta[4]), 1ULL))
+                                   : -1;
+    HeavyTask* out = reinterpret_cast<HeavyTask*>(sc.heavy_tasks) + base;
+    for (long long q = 0; q < parts; ++q) {
+        const long long a = q * kTaskProducts;
+        out[q] = HeavyTask{static_cast<int32_t>(i), slot, 0, 1, a, a + kTaskProducts < f ? a + kTaskProducts : f};
+    }
 }
 
-// ---- 5. run the tasks: one block per task, a <= 2^20-bit shared bitmap
+// ---- 5. run the tasks: one block per task, a shared bitmap over the span,
+// kept all-zero between tasks.
+template <int kRunBlock>
 __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch sc, int64_t first,
-                                                         int R, int wshift) {
+                                                         int R, int wshift, int32_t slot_words) {
     extern __shared__ int4 s_dyn[];
     uint32_t* s_set = reinterpret_cast<uint32_t*>(s_dyn);
     __shared__ int s_off[kRunBlock + 1];
     __shared__ int64_t s_b0[kRunBlock];
-    __shared__ long long s_red[kRunBlock / 32];
+    __shared__ HeavyTask s_task;
     const HeavyTask* tasks = reinterpret_cast<const HeavyTask*>(sc.heavy_tasks);
     const long long ntask = sc.heavy_meta[3];
     const int32_t* list = heavy_list(sc, first);
-    const int32_t wwords = static_cast<int32_t>((int64_t(1) << wshift) / 32);
+    const int lane = threadIdx.x & 31;
+    const int32_t max_words = R > 1 ? (1 << (kTaskSpanShift - 5))
+                                    : static_cast<int32_t>((int64_t(g.bcols) + 31) / 32);
+    for (int k = threadIdx.x; k < max_words; k += kRunBlock) s_set[k] = 0u;
     long long acc = 0;
     for (long long ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
-        const HeavyTask t = tasks[ti];
-        for (int k = threadIdx.x; k < t.words; k += kRunBlock) s_set[k] = 0u;
+        __syncthreads();  // previous task's clear is complete
+        if (threadIdx.x == 0) s_task = tasks[ti];
         __syncthreads();
+        const HeavyTask t = s_task;
+        const int32_t col_base = R > 1 ? (t.r0 << wshift) : 0;
+        const int32_t words = R > 1 ? ((t.r1 - t.r0) << (wshift - 5)) : max_words;
         int cnt = 0;
         auto insert = [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll], long long) {
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
                 if (valid[u]) {
-                    const uint32_t off = static_cast<uint32_t>(keys[u] - t.col_base);
+                    const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
                     const uint32_t bit = 1u << (off & 31);
                     cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
                 }
         };
-        if (R > 1) {
-            for (long long p = t.p0 + threadIdx.x; p < t.p1; p += kRunBlock * kUnroll) {
+        auto contiguous = [&](auto&& fn) {
+            for (long long p = t.a + threadIdx.x; p < t.b; p += kRunBlock * kUnroll) {
                 int keys[kUnroll];
                 bool valid[kUnroll];
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u) {
                     const long long q = p + u * kRunBlock;
-                    valid[u] = q < t.p1;
+                    valid[u] = q < t.b;
                     keys[u] = valid[u] ? __ldg(&sc.heavy_pbuf[q]) : 0;
                 }
-                insert(keys, valid, 0);
+                fn(keys, valid, 0);
             }
-        } else {
-            item_products<kRunBlock>(g, sc, first, t.item, t.p0, t.p1, s_off, s_b0, insert);
-        }
+        };
+        if (R > 1)
+            contiguous(insert);
+        else
+            item_products<kRunBlock>(g, sc, first, t.item, t.a, t.b, s_off, s_b0, insert);
+        __syncthreads();  // every insert is done
         if (t.slot >= 0) {
-            // range shared by several tasks: the bits this task adds first
-            __syncthreads();
+            // span shared by several tasks: the bits this task adds first
             cnt = 0;
-            uint32_t* gbm = sc.pool + int64_t(t.slot) * wwords;
-            for (int k = threadIdx.x; k < t.words; k += kRunBlock) {
+            uint32_t* gbm = sc.pool + int64_t(t.slot) * slot_words;
+            for (int k = threadIdx.x; k < words; k += kRunBlock) {
                 const uint32_t w = s_set[k];
                 if (w) cnt += __popc(w & ~atomicOr(&gbm[k], w));
             }
+            __syncthreads();  // the merge scan has read the bitmap
         }
-        const long long tot = block_sum_ll<kRunBlock>(cnt, s_red);
-        if (threadIdx.x == 0 && tot) {
+        cnt = static_cast<int>(warp_sum_ll(cnt));
+        if (lane == 0 && cnt) {
             if (g.out)
                 atomicAdd(reinterpret_cast<unsigned long long*>(&g.out[list[t.item]]),
-                          static_cast<unsigned long long>(tot));
-            acc += tot;
+                          static_cast<unsigned long long>(cnt));
+            acc += cnt;
         }
-        __syncthreads();
+        // back to all-zero: re-walk the keys of a sparse span, else clear
+        if (R > 1 && (t.b - t.a) * 8 < words) {
+            contiguous([&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll], long long) {
+#pragma unroll
+                for (int v = 0; v < kUnroll; ++v)
+                    if (valid[v]) s_set[static_cast<uint32_t>(keys[v] - col_base) >> 5] = 0u;
+            });
+        } else {
+            for (int k = threadIdx.x; k < words; k += kRunBlock) s_set[k] = 0u;
+        }
     }
-    if (threadIdx.x == 0 && acc)
+    if (lane == 0 && acc)
         atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[g.total_slot]),
                   static_cast<unsigned long long>(acc));
 }
@@ -444,6 +521,11 @@ __global__ void k_heavy_clean(SymScratch sc, int64_t slot_words) {
         sc.pool[i] = 0u;
 }
 
+int place_smem(bool priv) {
+    const int nw = priv ? kHW : 1, rm = priv ? kPrivRanges : kMaxRanges;
+    return int(rm * 8 + 2 * kHeavyUnitProducts * 4 + nw * rm * 4 + (rm + 1) * 4);
+}
+
 }  // namespace
 
 HeavyGeometry heavy_geometry(int32_t bcols) {
@@ -456,21 +538,23 @@ HeavyGeometry heavy_geometry(int32_t bcols) {
     } else {
         int ws = lg - 8;  // R <= 256
         if (ws < 17) ws = 17;
-        if (ws > kSpanShift) ws = kSpanShift;
+        if (ws > kTaskSpanShift) ws = kTaskSpanShift;
         h.wshift = ws;
         h.ranges = static_cast<int>((int64_t(bcols) + (int64_t(1) << ws) - 1) >> ws);
     }
-    h.wwords = static_cast<int32_t>(((int64_t(1) << h.wshift) + 31) / 32);
+    // words of a merge slot: a task span (R > 1) or the whole row (R == 1)
+    h.wwords = h.ranges > 1 ? (1 << kTaskSpanShift) / 32
+                            : static_cast<int32_t>(((int64_t(1) << h.wshift) + 31) / 32);
     return h;
 }
 
 int64_t heavy_task_bound(int64_t count, int64_t products, int ranges) {
-    // groups: at most one per non-empty range, plus split parts
+    // one task per span of every item, plus the extra parts of split spans
     return count * (int64_t(ranges) + 1) + 2 * (products / kTaskProducts + 1);
 }
 
 int64_t heavy_slot_bound(int64_t, int64_t products) {
-    // a merge slot serves one range (or row) that needs >= 2 tasks
+    // a merge slot serves one span (or row) that needs >= 2 tasks
     return products / kTaskProducts + 1;
 }
 
@@ -488,37 +572,44 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, int64_t f
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_done & (1u << (dev & 31)))) {
-        cudaFuncSetAttribute(k_heavy_run, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_heavy_run<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (1 << kSpanShift) / 8);
-        cudaFuncSetAttribute(k_heavy_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kHeavyUnitProducts * 4));
-        cudaFuncSetAttribute(k_heavy_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kHeavyUnitProducts * 4));
+        cudaFuncSetAttribute(k_heavy_run<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (1 << kTaskSpanShift) / 8);
+        cudaFuncSetAttribute(k_heavy_place<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             place_smem(true));
+        cudaFuncSetAttribute(k_heavy_place<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             place_smem(false));
         attr_done |= 1u << (dev & 31);
     }
     const HeavyGeometry geo = heavy_geometry(args.bcols);
     const int R = geo.ranges;
+    const unsigned sms = static_cast<unsigned>(num_sms);
     k_heavy_prep<<<1, 256, 0, stream>>>(args, s, first, count);
     k_heavy_entries<<<static_cast<unsigned>(count), 256, 0, stream>>>(args, s, first);
-    const unsigned sms = static_cast<unsigned>(num_sms);
     if (R > 1) {
         cudaMemsetAsync(s.heavy_rc, 0, sizeof(long long) * count * R, stream);
-        const int keys_smem = int(kHeavyUnitProducts * 4);
         if (R <= kPrivRanges) {
             k_heavy_count<true><<<sms * 8, kHB, 0, stream>>>(args, s, first, count, R, geo.wshift);
-            k_heavy_offsets<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(s, count, R);
-            k_heavy_scatter<true><<<sms * 4, kHB, keys_smem, stream>>>(args, s, first, count, R,
-                                                                       geo.wshift);
+            k_heavy_offsets<<<static_cast<unsigned>(count), 256, 0, stream>>>(s, count, R);
+            k_heavy_place<true><<<sms * 4, kHB, place_smem(true), stream>>>(args, s, first, count,
+                                                                           R, geo.wshift);
         } else {
             k_heavy_count<false><<<sms * 8, kHB, 0, stream>>>(args, s, first, count, R, geo.wshift);
-            k_heavy_offsets<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(s, count, R);
-            k_heavy_scatter<false><<<sms * 2, kHB, keys_smem, stream>>>(args, s, first, count, R,
-                                                                        geo.wshift);
+            k_heavy_offsets<<<static_cast<unsigned>(count), 256, 0, stream>>>(s, count, R);
+            k_heavy_place<false><<<sms * 2, kHB, place_smem(false), stream>>>(args, s, first,
+                                                                             count, R, geo.wshift);
         }
+        k_heavy_plan<<<static_cast<unsigned>(count), 128, 0, stream>>>(s, count, R, geo.wshift,
+                                                                     s.heavy_task_cap);
+        k_heavy_run<512><<<sms * 3, 512, (1 << kTaskSpanShift) / 8, stream>>>(
+            args, s, first, R, geo.wshift, geo.wwords);
+    } else {
+        k_heavy_tasks_r1<<<static_cast<unsigned>((count + 127) / 128), 128, 0, stream>>>(
+            s, count, s.heavy_task_cap);
+        k_heavy_run<1024><<<sms, 1024, (1 << kSpanShift) / 8, stream>>>(args, s, first, R,
+                                                                       geo.wshift, geo.wwords);
     }
-    k_heavy_tasks<<<static_cast<unsigned>((count + 127) / 128), 128, 0, stream>>>(
-        s, count, R, geo.wshift, args.bcols, s.heavy_task_cap);
-    k_heavy_run<<<sms, kRunBlock, (1 << kSpanShift) / 8, stream>>>(args, s, first, R, geo.wshift);
     k_heavy_clean<<<sms * 4, 256, 0, stream>>>(s, int64_t(geo.wwords));
     return cudaGetLastError();
 }

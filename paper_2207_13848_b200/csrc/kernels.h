@@ -72,7 +72,7 @@ constexpr int kHeavyBin = 6;         // heavier: units of kHeavyUnitProducts
 constexpr int kForeignBin = 7;       // row owned by another rank
 constexpr int kNoBin = 8;            // padding lane
 //        products, many blocks per row over a global bitmap of B.cols bits.
-constexpr int64_t kHeavyUnitProducts = 8192;
+constexpr int64_t kHeavyUnitProducts = 4096;
 
 struct SymScratch {
     int32_t* lists = nullptr;        // kNumBins * capacity item ids
@@ -84,8 +84,8 @@ struct SymScratch {
     int64_t* heavy_foff = nullptr;       // capacity + 1: product prefix per item
     int64_t* heavy_epre = nullptr;       // per entry: exclusive product prefix (L_i + 1 per item)
     int64_t* heavy_eb0 = nullptr;        // per entry: start of its B row
-    long long* heavy_rc = nullptr;       // count * R: range histogram, then bucket starts
-    long long* heavy_cur = nullptr;      // count * R: scatter cursors
+    long long* heavy_rc = nullptr;       // count * R: bucket counts, then bucket starts
+    long long* heavy_cur = nullptr;      // count * R: placement cursors
     int32_t* heavy_pbuf = nullptr;       // products grouped by (item, range)
     void* heavy_tasks = nullptr;         // HeavyTask[heavy_task_cap]
     int64_t heavy_task_cap = 0;

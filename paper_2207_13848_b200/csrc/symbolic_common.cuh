@@ -64,43 +64,42 @@ __device__ __forceinline__ ItemRow item_row(const SymArgs& g, int32_t s) {
 constexpr int kUnroll = 4;
 
 template <int WARPS, typename OffT, typename Fn>
-__device__ __forceinline__ void chunk_products(const OffT* off, const int64_t* b0, int n,
-                                               long long q0, long long q1,
-                                               const int32_t* __restrict__ bcol, Fn&& fn) {
+__device__ __forceinline__ void chunk_products(const OffT* off, const int64_t* b0, int n, OffT q0,
+                                               OffT q1, const int32_t* __restrict__ bcol, Fn&& fn) {
     const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) % WARPS;
-    const long long span = q1 - q0;
+    const OffT span = q1 - q0;
     if (span <= 0 || n <= 0) return;
-    long long per = (span + WARPS - 1) / WARPS;
-    per = (per + 31) & ~31LL;
-    const long long ws = q0 + w * per;
-    const long long we = ws + per < q1 ? ws + per : q1;
+    OffT per = (span + WARPS - 1) / WARPS;
+    per = (per + 31) & ~OffT(31);
+    const OffT ws = q0 + w * per;
+    const OffT we = ws + per < q1 ? ws + per : q1;
     // warp-uniform loop (fn may use warp collectives); lanes past the end of
     // the warp's slice run with valid = false
     int e = 0;
     if (ws + lane < we) {
-        const long long p = ws + lane;
+        const OffT p = ws + lane;
         int lo = 0, hi = n - 1;  // largest e with off[e] <= p
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if (static_cast<long long>(off[mid]) <= p) lo = mid; else hi = mid - 1;
+            if (off[mid] <= p) lo = mid; else hi = mid - 1;
         }
         e = lo;
     }
-    for (long long base = ws; base < we; base += 32 * kUnroll) {
-        const long long p = base + lane;
+    for (OffT base = ws; base < we; base += 32 * kUnroll) {
+        const OffT p = base + lane;
         int keys[kUnroll];
         bool valid[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            const long long q = p + 32 * u;
+            const OffT q = p + 32 * u;
             valid[u] = q < we;
             keys[u] = 0;
             if (valid[u]) {
-                while (static_cast<long long>(off[e + 1]) <= q) ++e;
-                keys[u] = __ldg(&bcol[b0[e] + (q - static_cast<long long>(off[e]))]);
+                while (off[e + 1] <= q) ++e;
+                keys[u] = __ldg(&bcol[b0[e] + (q - off[e])]);
             }
         }
-        fn(keys, valid, p);  // keys[u] is product p + 32 u
+        fn(keys, valid, static_cast<long long>(p));  // keys[u] is product p + 32 u
     }
 }
 
