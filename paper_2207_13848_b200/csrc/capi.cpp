@@ -138,6 +138,8 @@ struct spnnz_gpu_ctx {
     // matrices
     bool loaded = false;
     bool same_b = false;
+    bool b_sorted = false;     // B rows non-decreasing (enables the interval heavy path)
+    bool b_intervals = false;  // interval heavy path selected (SPNNZ_HEAVY_INTERVALS=1)
     int32_t a_rows = 0, a_cols = 0, b_rows = 0, b_cols = 0;
     int32_t row_lo = 0, row_hi = 0;
     DBuf<int64_t> b_rpt;
@@ -163,12 +165,15 @@ struct spnnz_gpu_ctx {
     int64_t list_cap = 0;
     DBuf<int64_t> heavy_unit_off, heavy_eoff, heavy_foff, heavy_epre, heavy_eb0, heavy_flops;
     DBuf<long long> heavy_rc, heavy_cur;
-    DBuf<int32_t> heavy_pbuf;
+    DBuf<int32_t> heavy_pbuf, heavy_utab;
+    DBuf<int64_t> heavy_boff;                  // interval path (sorted B)
+    DBuf<int32_t> heavy_bnd, heavy_unit_item, heavy_unit_e0;
     DBuf<int4> heavy_tasks;  // HeavyTask = 32 bytes = 2 x int4
     long long* h_meta = nullptr;    // pinned mirror of heavy_meta
     DBuf<uint32_t> pool;
     int64_t pool_slots = 0, pool_words = 0;
     DBuf<long long> heavy_meta;
+    DBuf<long long> sorted_cnt;
     DBuf<int32_t> samples;
     DBuf<int32_t> rows_in;
     DBuf<int64_t> out64;
@@ -242,17 +247,46 @@ int sym_scratch(spnnz_gpu_ctx* c, int64_t items, SymScratch* s) {
     return SPNNZ_OK;
 }
 
+// The interval heavy path needs B's rows sorted and at most kMaxIntervals
+// column intervals (B.cols <= 2^27).
+bool interval_path(const spnnz_gpu_ctx* c) {
+    return c->b_intervals && c->b_sorted && interval_geometry(c->b_cols).count <= kMaxIntervals;
+}
+
 // Buffers of one heavy batch (see heavy.cu); the merge-bitmap pool is zeroed
 // when (re)allocated and returned to zero by the heavy path after each use.
 int heavy_buffers(spnnz_gpu_ctx* c, int64_t count, int64_t ents, int64_t products,
-                  SymScratch* s) {
+                  int64_t cells, SymScratch* s) {
     const HeavyGeometry geo = heavy_geometry(c->b_cols);
     RC(c->heavy_epre.ensure(ents));
     RC(c->heavy_eb0.ensure(ents));
+    s->heavy_epre = c->heavy_epre.p;
+    s->heavy_eb0 = c->heavy_eb0.p;
+    if (interval_path(c)) {
+        const int64_t units = products / kHeavyUnitProducts + count;
+        const int64_t tasks = count * int64_t(interval_geometry(c->b_cols).count);
+        RC(c->heavy_boff.ensure(count + 1));
+        RC(c->heavy_bnd.ensure(std::max<int64_t>(cells, 1)));
+        RC(c->heavy_unit_item.ensure(units));
+        RC(c->heavy_unit_e0.ensure(units));
+        RC(c->heavy_tasks.ensure(2 * std::max<int64_t>(tasks, 1)));
+        s->heavy_boff = c->heavy_boff.p;
+        s->heavy_bnd = c->heavy_bnd.p;
+        s->heavy_bnd_cap = cells;
+        s->heavy_unit_item = c->heavy_unit_item.p;
+        s->heavy_unit_e0 = c->heavy_unit_e0.p;
+        s->heavy_tasks = c->heavy_tasks.p;
+        s->heavy_task_cap = tasks;
+        return SPNNZ_OK;
+    }
+    s->heavy_boff = nullptr;
+    s->heavy_unit_item = nullptr;
     if (geo.ranges > 1) {
         RC(c->heavy_rc.ensure(count * geo.ranges));
         RC(c->heavy_cur.ensure(count * geo.ranges));
         RC(c->heavy_pbuf.ensure(products));
+        if (geo.unit_sorted)
+            RC(c->heavy_utab.ensure((products / kHeavyUnitProducts + count) * (geo.ranges + 1)));
     }
     const int64_t tasks = heavy_task_bound(count, products, geo.ranges);
     RC(c->heavy_tasks.ensure(2 * tasks));
@@ -265,11 +299,10 @@ int heavy_buffers(spnnz_gpu_ctx* c, int64_t count, int64_t ents, int64_t product
         c->pool_slots = slots;
         c->pool_words = words;
     }
-    s->heavy_epre = c->heavy_epre.p;
-    s->heavy_eb0 = c->heavy_eb0.p;
     s->heavy_rc = c->heavy_rc.p;
     s->heavy_cur = c->heavy_cur.p;
     s->heavy_pbuf = c->heavy_pbuf.p;
+    s->heavy_utab = c->heavy_utab.p;
     s->heavy_tasks = c->heavy_tasks.p;
     s->heavy_task_cap = tasks;
     s->pool = c->pool.p;
@@ -318,45 +351,43 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     CU(cudaStreamSynchronize(c->stream));
     const int64_t heavy = c->h_counts[kHeavyBin];
     if (heavy > 0) {
-        // One batch when the heavy rows' products fit the batch budget
-        // (always for sampled passes); exact passes over every row split the
-        // heavy list greedily by FLOP.
+        // One batch when the heavy rows fit the batch budgets (always for
+        // sampled passes); exact passes over every row split the heavy list
+        // greedily.  Budgets: products (bucket paths' product buffer) and
+        // boundary-table cells (interval path).
         int64_t kBudget = int64_t(1) << 28;  // products per batch (1 GB buffer)
         if (const char* env = getenv("SPNNZ_HEAVY_BATCH_PRODUCTS"))  // test knob
             if (atoll(env) > 0) kBudget = atoll(env);
-        const int64_t ents_total = c->h_meta[1], prod_total = c->h_meta[2];
-        std::vector<int64_t> cuts{0, heavy};
-        if (prod_total > kBudget) {
-            RC(c->heavy_flops.ensure(heavy));
+        const int64_t kCellBudget = kBudget;
+        const bool iv = interval_path(c);
+        struct Batch {
+            int64_t first, count, ents, products, cells;
+        };
+        std::vector<Batch> batches{{0, heavy, c->h_meta[1], c->h_meta[2], iv ? c->h_meta[5] : 0}};
+        if (batches[0].products > kBudget || batches[0].cells > kCellBudget) {
+            RC(c->heavy_flops.ensure(3 * heavy));
             CU(launch_heavy_flops(g, s, heavy, c->heavy_flops.p, c->stream));
-            std::vector<int64_t> f(static_cast<size_t>(heavy));
-            CU(cudaMemcpyAsync(f.data(), c->heavy_flops.p, 8 * size_t(heavy), cudaMemcpyDeviceToHost,
-                               c->stream));
+            std::vector<int64_t> h(static_cast<size_t>(3 * heavy));
+            CU(cudaMemcpyAsync(h.data(), c->heavy_flops.p, 8 * h.size(), cudaMemcpyDeviceToHost, c->stream));
             CU(cudaStreamSynchronize(c->stream));
-            cuts = {0};
-            int64_t acc = 0;
+            batches.clear();
+            Batch b{0, 0, 0, 0, 0};
             for (int64_t i = 0; i < heavy; ++i) {
-                if (acc > 0 && acc + f[i] > kBudget) {
-                    cuts.push_back(i);
-                    acc = 0;
+                const int64_t f = h[i], L = h[heavy + i], cl = iv ? h[2 * heavy + i] : 0;
+                if (b.count > 0 && (b.products + f > kBudget || b.cells + cl > kCellBudget)) {
+                    batches.push_back(b);
+                    b = Batch{i, 0, 0, 0, 0};
                 }
-                acc += f[i];
+                ++b.count;
+                b.ents += L + 1;
+                b.products += f;
+                b.cells += cl;
             }
-            cuts.push_back(heavy);
+            batches.push_back(b);
         }
-        const int64_t prod_cap = std::min(prod_total, std::max<int64_t>(kBudget, 1));
-        for (size_t b = 0; b + 1 < cuts.size(); ++b) {
-            const int64_t first = cuts[b], cnt = cuts[b + 1] - cuts[b];
-            // products of a batch <= max(budget, its single largest row)
-            int64_t prod = prod_cap;
-            if (cnt == 1 || prod_total <= kBudget) prod = std::max(prod_cap, prod_total);
-            if (cuts.size() > 2 && cnt == 1) {
-                long long one = 0;
-                CU(cudaMemcpy(&one, c->heavy_flops.p + first, 8, cudaMemcpyDeviceToHost));
-                prod = std::max<int64_t>(prod, one);
-            }
-            RC(heavy_buffers(c, cnt, ents_total, prod, &s));
-            CU(launch_sym_heavy(g, s, first, cnt, c->num_sms, c->stream));
+        for (const Batch& b : batches) {
+            RC(heavy_buffers(c, b.count, b.ents, b.products, b.cells, &s));
+            CU(launch_sym_heavy(g, s, iv, b.first, b.count, c->num_sms, c->stream));
             *launches += 8;
         }
     }
@@ -552,13 +583,16 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     for (auto* b : {&c->b_col, &c->a_col, &c->tile_x, &c->counts, &c->lists,
                     &c->samples, &c->rows_in, &c->bad})
         b->release();
-    for (auto* b : {&c->tile_carry, &c->tile_total, &c->tile_max, &c->totals, &c->heavy_meta})
+    for (auto* b : {&c->tile_carry, &c->tile_total, &c->tile_max, &c->totals, &c->heavy_meta, &c->sorted_cnt})
         b->release();
     c->pool.release();
     c->outf.release();
     c->heavy_rc.release();
     c->heavy_cur.release();
     c->heavy_pbuf.release();
+    c->heavy_utab.release();
+    c->heavy_boff.release();
+    for (auto* b : {&c->heavy_bnd, &c->heavy_unit_item, &c->heavy_unit_e0}) b->release();
     c->heavy_tasks.release();
     if (c->h_totals) cudaFreeHost(c->h_totals);
     if (c->h_counts) cudaFreeHost(c->h_counts);
@@ -674,6 +708,19 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
         v.col = c->a_col.p - a_lo;  // indexed with absolute offsets
     }
     c->a = v;
+    // B's rows sorted (the reference's CsrMatrix invariant)?  Decides the
+    // heavy-row algorithm; both give identical counts.
+    RC(c->sorted_cnt.ensure(2));
+    CU(launch_check_sorted(c->b_rpt.p, c->b_col.p, c->b_rows, b_nnz,
+                           reinterpret_cast<unsigned long long*>(c->sorted_cnt.p), c->num_sms, c->stream));
+    long long cnt[2] = {0, 0};
+    CU(cudaMemcpyAsync(cnt, c->sorted_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    c->b_sorted = cnt[0] == cnt[1];
+    if (const char* env = getenv("SPNNZ_HEAVY_UNSORTED"))  // test knob: force the sort-agnostic path
+        if (atoi(env) > 0) c->b_sorted = false;
+    const char* ivenv = getenv("SPNNZ_HEAVY_INTERVALS");
+    c->b_intervals = ivenv && atoi(ivenv) > 0;
     c->loaded = true;
     return SPNNZ_OK;
 }

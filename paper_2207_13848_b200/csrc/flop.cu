@@ -257,7 +257,41 @@ __global__ void k_check_rows(const int32_t* __restrict__ rows, int64_t n, int32_
     if (i < n && (rows[i] < 0 || rows[i] >= num_rows)) atomicAdd(bad, 1);
 }
 
+// Row-sortedness of B (the CsrMatrix invariant, csr.hpp:16-18), checked once
+// at load: every descent col[j] < col[j-1] must sit at the start of a
+// non-empty row.  cnt[0] += descents over all j, cnt[1] += descents at row
+// starts; B is sorted iff they are equal.
+__global__ void k_descents(const int32_t* __restrict__ col, int64_t nnz, unsigned long long* cnt) {
+    unsigned long long d = 0;
+    for (int64_t j = 1 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < nnz;
+         j += int64_t(gridDim.x) * blockDim.x)
+        d += __ldg(&col[j]) < __ldg(&col[j - 1]);
+    d = warp_sum_ll(static_cast<long long>(d));
+    if ((threadIdx.x & 31) == 0 && d) atomicAdd(&cnt[0], d);
+}
+
+__global__ void k_start_descents(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col,
+                                 int32_t rows, unsigned long long* cnt) {
+    unsigned long long d = 0;
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < rows;
+         r += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t j = rpt[r];
+        if (j >= 1 && j < rpt[r + 1]) d += __ldg(&col[j]) < __ldg(&col[j - 1]);
+    }
+    d = warp_sum_ll(static_cast<long long>(d));
+    if ((threadIdx.x & 31) == 0 && d) atomicAdd(&cnt[1], d);
+}
+
 }  // namespace
+
+cudaError_t launch_check_sorted(const int64_t* rpt, const int32_t* col, int32_t rows, int64_t nnz,
+                                unsigned long long* cnt, int num_sms, cudaStream_t stream) {
+    cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), stream);
+    const unsigned grid = static_cast<unsigned>(num_sms) * 8;
+    if (nnz > 1) k_descents<<<grid, 256, 0, stream>>>(col, nnz, cnt);
+    if (rows > 0) k_start_descents<<<grid, 256, 0, stream>>>(rpt, col, rows, cnt);
+    return cudaGetLastError();
+}
 
 int64_t flop_tiles(const DevCsr& a) {
     if (a.rows == 0) return 0;

@@ -57,52 +57,58 @@ __device__ __forceinline__ const int32_t* heavy_list(const SymScratch& sc, int64
     return sc.lists + int64_t(kHeavyBin) * sc.capacity + first;
 }
 
-// ---- 0a. batch bookkeeping: units, entry offsets, product offsets (1 block)
-__global__ void __launch_bounds__(256) k_heavy_prep(SymArgs g, SymScratch sc, int64_t first,
-                                                    int64_t count) {
-    using Scan = cub::BlockScan<long long, 256>;
+// ---- 0a. batch bookkeeping: per item its units, entries, products,
+// interval tasks and boundary-table cells, as exclusive prefixes (1 block)
+constexpr int kPrepBlock = 512;
+
+__global__ void __launch_bounds__(kPrepBlock) k_heavy_prep(SymArgs g, SymScratch sc, int64_t first,
+                                                           int64_t count) {
+    using Scan = cub::BlockScan<long long, kPrepBlock>;
     __shared__ typename Scan::TempStorage tmp;
-    __shared__ long long s_u, s_e, s_f;
-    if (threadIdx.x == 0) s_u = s_e = s_f = 0;
+    __shared__ long long s_carry[4];
+    if (threadIdx.x < 4) s_carry[threadIdx.x] = 0;
     __syncthreads();
     const int32_t* list = heavy_list(sc, first);
-    for (int64_t b = 0; b < count; b += 256) {
+    for (int64_t b = 0; b < count; b += kPrepBlock) {
         const int64_t i = b + threadIdx.x;
-        long long units = 0, ents = 0, f = 0;
+        long long x[4] = {0, 0, 0, 0};
         if (i < count) {
             const int32_t s = list[i];
             const int32_t rid = g.rows ? g.rows[s] : g.row_lo + s;
             const ItemRow it = item_row(g, s);
-            f = g.flop[rid - g.row_lo];
-            units = (f + kHeavyUnitProducts - 1) / kHeavyUnitProducts;
-            ents = it.a1 - it.a0 + 1;
+            const long long f = g.flop[rid - g.row_lo];
+            const long long L = it.a1 - it.a0;
+            x[0] = (f + kHeavyUnitProducts - 1) / kHeavyUnitProducts;  // units
+            x[1] = L + 1;                                               // entries (+ end)
+            x[2] = f;                                                   // products
+            x[3] = (interval_geometry(g.bcols).count - 1) * L;          // boundary cells
         }
-        long long ue, ee, fe, ut, et, ft;
-        Scan(tmp).ExclusiveSum(units, ue, ut);
-        __syncthreads();
-        Scan(tmp).ExclusiveSum(ents, ee, et);
-        __syncthreads();
-        Scan(tmp).ExclusiveSum(f, fe, ft);
+        long long ex[4], tot[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            Scan(tmp).ExclusiveSum(x[k], ex[k], tot[k]);
+            __syncthreads();
+        }
         if (i < count) {
-            sc.heavy_unit_off[i] = s_u + ue;
-            sc.heavy_eoff[i] = s_e + ee;
-            sc.heavy_foff[i] = s_f + fe;
+            sc.heavy_unit_off[i] = s_carry[0] + ex[0];
+            sc.heavy_eoff[i] = s_carry[1] + ex[1];
+            sc.heavy_foff[i] = s_carry[2] + ex[2];
+            if (sc.heavy_boff) sc.heavy_boff[i] = s_carry[3] + ex[3];
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            s_u += ut;
-            s_e += et;
-            s_f += ft;
-        }
+        if (threadIdx.x == 0)
+            for (int k = 0; k < 4; ++k) s_carry[k] += tot[k];
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        sc.heavy_unit_off[count] = s_u;
-        sc.heavy_eoff[count] = s_e;
-        sc.heavy_foff[count] = s_f;
-        sc.heavy_meta[0] = s_u;
+        sc.heavy_unit_off[count] = s_carry[0];
+        sc.heavy_eoff[count] = s_carry[1];
+        sc.heavy_foff[count] = s_carry[2];
+        if (sc.heavy_boff) sc.heavy_boff[count] = s_carry[3];
+        sc.heavy_meta[0] = s_carry[0];
         sc.heavy_meta[3] = 0;  // tasks
         sc.heavy_meta[4] = 0;  // merge slots
+        sc.heavy_meta[7] = 0;  // interval-task cursor
     }
 }
 
@@ -130,8 +136,17 @@ __global__ void __launch_bounds__(256) k_heavy_entries(SymArgs g, SymScratch sc,
         long long ex, tot;
         Scan(tmp).ExclusiveSum(d, ex, tot);
         if (e < L) {
-            ep[e] = s_carry + ex;
+            const long long p = s_carry + ex;
+            ep[e] = p;
             eb[e] = b0;
+            if (sc.heavy_unit_item) {  // units whose first product is in this entry
+                const int64_t ubase = sc.heavy_unit_off[i];
+                for (long long u = (p + kHeavyUnitProducts - 1) / kHeavyUnitProducts;
+                     u * kHeavyUnitProducts < p + d; ++u) {
+                    sc.heavy_unit_item[ubase + u] = static_cast<int32_t>(i);
+                    sc.heavy_unit_e0[ubase + u] = static_cast<int32_t>(e);
+                }
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) s_carry += tot;
@@ -352,6 +367,111 @@ __global__ void __launch_bounds__(kHB) k_heavy_place(SymArgs g, SymScratch sc, i
     }
 }
 
+// ---- 3u. (1 < R <= kPrivRanges) sort each unit in place instead of count +
+// place: the unit's products are counting-sorted by range in shared memory
+// and written back to the unit's own window of the product buffer, with its
+// R + 1 range starts in heavy_utab; the per-(item, range) totals go to
+// heavy_rc for the planner.  A task then reads range r as one slice per unit.
+__global__ void __launch_bounds__(kHB) k_heavy_sort_units(SymArgs g, SymScratch sc, int64_t first,
+                                                          int64_t count, int R, int wshift) {
+    constexpr int RM = kPrivRanges;
+    __shared__ int s_off[kHB + 1];
+    __shared__ int64_t s_b0[kHB];
+    // dynamic: keys_in[U] | keys_out[U] | hist[kHW][RM] | offs[RM + 1]
+    extern __shared__ int4 s_dyn_sort[];
+    int32_t* s_in = reinterpret_cast<int32_t*>(s_dyn_sort);
+    int32_t* s_out = s_in + kHeavyUnitProducts;
+    int* s_hist = s_out + kHeavyUnitProducts;  // [w * RM + r]
+    int* s_offs = s_hist + kHW * RM;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long units = sc.heavy_meta[0];
+    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit un = find_unit_block(sc, count, u);
+        for (int k = threadIdx.x; k < kHW * RM; k += kHB) s_hist[k] = 0;
+        item_products<kHB>(g, sc, first, un.item, un.p0, un.p1, s_off, s_b0,
+                           [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll],
+                               long long q) {
+#pragma unroll
+                               for (int k = 0; k < kUnroll; ++k)
+                                   if (valid[k]) s_in[q + 32 * k] = keys[k];
+                           });
+        const int n = static_cast<int>(un.p1 - un.p0);
+        for (int i = threadIdx.x; i < n; i += kHB) atomicAdd(&s_hist[w * RM + (s_in[i] >> wshift)], 1);
+        __syncthreads();
+        // per range: warp offsets inside the range, the range total
+        long long* rc = sc.heavy_rc + un.item * R;
+        for (int r = threadIdx.x; r < R; r += kHB) {
+            int tot = 0;
+#pragma unroll
+            for (int v = 0; v < kHW; ++v) {
+                const int c = s_hist[v * RM + r];
+                s_hist[v * RM + r] = tot;
+                tot += c;
+            }
+            s_offs[r] = tot;
+            if (tot)
+                atomicAdd(reinterpret_cast<unsigned long long*>(&rc[r]), static_cast<unsigned long long>(tot));
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // exclusive scan of the R totals by warp 0
+            const int per = (R + 31) / 32;
+            const int r0 = lane * per, r1 = r0 + per < R ? r0 + per : R;
+            int sum = 0;
+            for (int r = r0; r < r1; ++r) sum += s_offs[r];
+            const int incl = warp_incl_scan(sum);
+            int run = incl - sum;
+            for (int r = r0; r < r1; ++r) {
+                const int c = s_offs[r];
+                s_offs[r] = run;
+                run += c;
+            }
+            if (lane == 31) s_offs[R] = incl;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += kHB) {  // same thread <-> key mapping as the histogram
+            const int key = s_in[i];
+            const int r = key >> wshift;
+            s_out[s_offs[r] + atomicAdd(&s_hist[w * RM + r], 1)] = key;
+        }
+        __syncthreads();
+        int32_t* dst = sc.heavy_pbuf + sc.heavy_foff[un.item] + un.p0;
+        for (int i = threadIdx.x; i < n; i += kHB) dst[i] = s_out[i];
+        int32_t* tab = sc.heavy_utab + u * (R + 1);
+        for (int r = threadIdx.x; r <= R; r += kHB) tab[r] = s_offs[r];
+    }
+}
+
+// Unit-sorted tasks: one block per item, one thread per range; a range above
+// kTaskProducts products is split into groups of the item's units that share
+// a merge slot.
+__global__ void __launch_bounds__(kPrivRanges) k_heavy_plan_units(SymScratch sc, int64_t count, int R,
+                                                                  int64_t task_cap) {
+    using Scan = cub::BlockScan<int, kPrivRanges>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ long long s_base;
+    const int64_t i = blockIdx.x;
+    const int r = threadIdx.x;
+    const long long nu = sc.heavy_unit_off[i + 1] - sc.heavy_unit_off[i];
+    const long long cnt = r < R ? sc.heavy_rc[i * R + r] : 0;
+    long long p = (cnt + kTaskProducts - 1) / kTaskProducts;
+    const int parts = static_cast<int>(p < nu ? p : nu);
+    int excl, total;
+    Scan(tmp).ExclusiveSum(parts, excl, total);
+    if (threadIdx.x == 0)
+        s_base = static_cast<long long>(atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[3]),
+                                                  static_cast<unsigned long long>(total)));
+    __syncthreads();
+    if (s_base + total > task_cap) __trap();  // host sizes task_cap to heavy_task_bound()
+    if (parts > 0) {
+        const int32_t slot = parts > 1 ? static_cast<int32_t>(atomicAdd(
+                                             reinterpret_cast<unsigned long long*>(&sc.heavy_meta[4]), 1ULL))
+                                       : -1;
+        HeavyTask* out = reinterpret_cast<HeavyTask*>(sc.heavy_tasks) + s_base + excl;
+        for (int q = 0; q < parts; ++q)
+            out[q] = HeavyTask{static_cast<int32_t>(i), slot, r, r + 1, nu * q / parts, nu * (q + 1) / parts};
+    }
+}
+
 // ---- 4. tasks
 // R > 1: one block per item, one thread per aligned span.
 __global__ void __launch_bounds__(128) k_heavy_plan(SymScratch sc, int64_t count, int R,
@@ -420,7 +540,12 @@ __global__ void k_heavy_tasks_r1(SymScratch sc, int64_t count, int64_t task_cap)
 
 // ---- 5. run the tasks: one block per task, a shared bitmap over the span,
 // kept all-zero between tasks.
-template <int kRunBlock>
+// MODE: kRunItem (R == 1) products straight from the B rows; kRunBuckets the
+// task's contiguous bucket span; kRunUnits one slice per unit of the task's
+// unit group.
+constexpr int kRunItem = 0, kRunBuckets = 1, kRunUnits = 2;
+
+template <int kRunBlock, int MODE>
 __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch sc, int64_t first,
                                                          int R, int wshift, int32_t slot_words) {
     extern __shared__ int4 s_dyn[];
@@ -453,23 +578,66 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
                     cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
                 }
         };
+        // the span's keys: 16-byte vectors over the aligned body, two vectors
+        // per thread in flight; the unaligned head and tail (< 4 keys each)
+        // go to the first threads
         auto contiguous = [&](auto&& fn) {
-            for (long long p = t.a + threadIdx.x; p < t.b; p += kRunBlock * kUnroll) {
-                int keys[kUnroll];
-                bool valid[kUnroll];
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
-                    const long long q = p + u * kRunBlock;
-                    valid[u] = q < t.b;
-                    keys[u] = valid[u] ? __ldg(&sc.heavy_pbuf[q]) : 0;
-                }
+            long long a4 = (t.a + 3) & ~3LL;
+            if (a4 > t.b) a4 = t.b;
+            const long long n4 = (t.b - a4) >> 2, b4 = a4 + 4 * n4;
+            const int head = static_cast<int>(a4 - t.a), tail = static_cast<int>(t.b - b4);
+            if (threadIdx.x < head + tail) {
+                const long long q = threadIdx.x < head ? t.a + threadIdx.x : b4 + (threadIdx.x - head);
+                const int keys[kUnroll] = {__ldg(&sc.heavy_pbuf[q]), 0, 0, 0};
+                const bool valid[kUnroll] = {true, false, false, false};
                 fn(keys, valid, 0);
             }
+            const int4* v = reinterpret_cast<const int4*>(sc.heavy_pbuf + a4);
+            for (long long i = threadIdx.x; i < n4; i += 2 * kRunBlock) {
+                const bool two = i + kRunBlock < n4;
+                const int4 x = __ldg(v + i);
+                const int4 y = two ? __ldg(v + i + kRunBlock) : make_int4(0, 0, 0, 0);
+                const bool all[kUnroll] = {true, true, true, true};
+                const int kx[kUnroll] = {x.x, x.y, x.z, x.w};
+                fn(kx, all, 0);
+                if (two) {
+                    const int ky[kUnroll] = {y.x, y.y, y.z, y.w};
+                    fn(ky, all, 0);
+                }
+            }
         };
-        if (R > 1)
+        if constexpr (MODE == kRunBuckets) {
             contiguous(insert);
-        else
+        } else if constexpr (MODE == kRunItem) {
             item_products<kRunBlock>(g, sc, first, t.item, t.a, t.b, s_off, s_b0, insert);
+        } else {
+            using Scan = cub::BlockScan<int, kRunBlock>;
+            __shared__ typename Scan::TempStorage s_scan;
+            const long long ubase = sc.heavy_unit_off[t.item];
+            const long long pbase = sc.heavy_foff[t.item];
+            for (long long u0 = t.a; u0 < t.b; u0 += kRunBlock) {
+                const int n = static_cast<int>(t.b - u0 < kRunBlock ? t.b - u0 : kRunBlock);
+                int len = 0;
+                int64_t start = 0;
+                if (threadIdx.x < n) {
+                    const long long u = u0 + threadIdx.x;
+                    const int32_t* tab = sc.heavy_utab + (ubase + u) * (R + 1);
+                    const int lo = tab[t.r0], hi = tab[t.r1];
+                    len = hi - lo;
+                    start = pbase + u * kHeavyUnitProducts + lo;
+                }
+                int ex, tot;
+                __syncthreads();  // the previous round's slices are consumed
+                Scan(s_scan).ExclusiveSum(len, ex, tot);
+                if (threadIdx.x < n) {
+                    s_off[threadIdx.x] = ex;
+                    s_b0[threadIdx.x] = start;
+                }
+                if (threadIdx.x == 0) s_off[n] = tot;
+                __syncthreads();
+                chunk_products<kRunBlock / 32>(s_off, s_b0, n, 0, tot, sc.heavy_pbuf, insert);
+            }
+        }
         __syncthreads();  // every insert is done
         if (t.slot >= 0) {
             // span shared by several tasks: the bits this task adds first
@@ -489,14 +657,16 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
             acc += cnt;
         }
         // back to all-zero: re-walk the keys of a sparse span, else clear
-        if (R > 1 && (t.b - t.a) * 8 < words) {
+        if (MODE == kRunBuckets && (t.b - t.a) * 8 < words) {
             contiguous([&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll], long long) {
 #pragma unroll
                 for (int v = 0; v < kUnroll; ++v)
                     if (valid[v]) s_set[static_cast<uint32_t>(keys[v] - col_base) >> 5] = 0u;
             });
         } else {
-            for (int k = threadIdx.x; k < words; k += kRunBlock) s_set[k] = 0u;
+            uint4* s4 = reinterpret_cast<uint4*>(s_set);
+            for (int k = threadIdx.x; k < (words >> 2); k += kRunBlock) s4[k] = make_uint4(0u, 0u, 0u, 0u);
+            for (int k = (words & ~3) + threadIdx.x; k < words; k += kRunBlock) s_set[k] = 0u;
         }
     }
     if (lane == 0 && acc)
@@ -504,13 +674,291 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
                   static_cast<unsigned long long>(acc));
 }
 
-// FLOP of every heavy item (for the host's batch planning in exact mode).
+// ======================================================= interval path
+// B rows sorted (non-decreasing, the CsrMatrix invariant): the part of B row
+// k inside a column interval is one contiguous run, so the columns are cut
+// into P intervals of 2^shift <= 2^19 columns (interval_geometry) and a heavy
+// row is counted interval by interval in a 64 KB shared bitmap, its products
+// read straight from B -- no product buffer, no sort, no merge.  Per item and
+// entry e the boundary table holds, for p = 1..P-1, the number of elements of
+// e's B row below column p * 2^shift (row-relative).
+//   bounds  per unit of products: 32 entries per warp step, one per lane;
+//           slices longer than 32 elements are read by the whole warp
+//           (coalesced) -- each element writes the boundaries it crosses;
+//   plan    per item: exact product count of every interval (a pass over the
+//           table), then tasks = runs of consecutive non-empty intervals with
+//           at most kIntervalTarget products (one interval may exceed it);
+//   run     two 512-thread blocks per SM take tasks off a counter; per
+//           interval: clear the bitmap, stage the entries' runs (<= 2048 per
+//           round), walk the products and count the bits set first.
+struct IntervalTask {
+    int32_t item;
+    int32_t p0, p1;  // intervals [p0, p1)
+    int32_t pad;
+    int64_t products;
+    int64_t pad2;
+};
+static_assert(sizeof(IntervalTask) == 32, "interval task layout");
+
+constexpr int kIvBlock = 512;
+constexpr int kIvItems = 4;                     // staged entries per thread
+constexpr int kIvStage = kIvBlock * kIvItems;   // entries per staging round
+constexpr int kIvSmem = (1 << kIvShift) / 8;    // the bitmap
+
+struct MappedUnit {
+    int64_t item;
+    long long p0, p1;
+    int64_t e0;
+};
+
+__device__ __forceinline__ MappedUnit mapped_unit(const SymScratch& sc, long long u) {
+    MappedUnit m;
+    m.item = sc.heavy_unit_item[u];
+    m.e0 = sc.heavy_unit_e0[u];
+    const long long f = sc.heavy_foff[m.item + 1] - sc.heavy_foff[m.item];
+    m.p0 = (u - sc.heavy_unit_off[m.item]) * kHeavyUnitProducts;
+    m.p1 = m.p0 + kHeavyUnitProducts < f ? m.p0 + kHeavyUnitProducts : f;
+    return m;
+}
+
+__device__ __forceinline__ void set_bounds(int32_t* bnd, int64_t L, int64_t e, int from, int to, int32_t v) {
+    for (int p = from; p <= to; ++p) bnd[static_cast<int64_t>(p - 1) * L + e] = v;
+}
+
+__global__ void __launch_bounds__(kHB) k_heavy_bounds(SymArgs g, SymScratch sc) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Intervals iv = interval_geometry(g.bcols);
+    const int ks = iv.shift, P = iv.count;
+    const long long units = sc.heavy_meta[0];
+    // one warp per unit
+    for (long long u = (blockIdx.x * int64_t(kHW) + w); u < units; u += int64_t(gridDim.x) * kHW) {
+        const MappedUnit un = mapped_unit(sc, u);
+        const int64_t i = un.item;
+        const int64_t L = sc.heavy_eoff[i + 1] - sc.heavy_eoff[i] - 1;
+        const int64_t* ep = sc.heavy_epre + sc.heavy_eoff[i];
+        const int64_t* eb = sc.heavy_eb0 + sc.heavy_eoff[i];
+        int32_t* bnd = sc.heavy_bnd + sc.heavy_boff[i];
+        for (int64_t base = un.e0;; base += 32) {
+            const int64_t e = base + lane;
+            int64_t pe = 0, pn = 0, sb = 0, te = 0, b0 = 0;
+            const bool in = e < L && (pe = ep[e]) < un.p1;
+            if (in) {
+                pn = ep[e + 1];
+                sb = un.p0 > pe ? un.p0 - pe : 0;
+                te = (pn < un.p1 ? pn : un.p1) - pe;
+                b0 = eb[e];
+            }
+            if (!__any_sync(kFull, in)) break;  // past the unit's window
+            const bool live = in && sb < te;
+            const bool longs = live && te - sb > 32;
+            if (live && !longs) {
+                const int32_t* row = g.bcol + b0;
+                int q[32];
+                const int n = static_cast<int>(te - sb);
+#pragma unroll
+                for (int k = 0; k < 32; ++k) q[k] = k < n ? (__ldg(&row[sb + k]) >> ks) : 0;
+                int prev = sb > 0 ? (__ldg(&row[sb - 1]) >> ks) : q[0];
+#pragma unroll
+                for (int k = 0; k < 32; ++k)
+                    if (k < n) {
+                        set_bounds(bnd, L, e, prev + 1, q[k] < P - 1 ? q[k] : P - 1, static_cast<int32_t>(sb + k));
+                        prev = q[k];
+                    }
+                if (te == pn - pe) set_bounds(bnd, L, e, prev + 1, P - 1, static_cast<int32_t>(pn - pe));
+            }
+            for (unsigned m = __ballot_sync(kFull, longs); m; m &= m - 1) {
+                const int src = __ffs(m) - 1;
+                const int64_t ew = base + src;
+                const int64_t s0 = __shfl_sync(kFull, sb, src), t0 = __shfl_sync(kFull, te, src);
+                const int64_t len = __shfl_sync(kFull, pn - pe, src);
+                const int32_t* row = g.bcol + __shfl_sync(kFull, b0, src);
+                int qlast = 0;
+                for (int64_t c = s0; c < t0; c += 32 * 4) {
+                    int q[4], pv[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int64_t j = c + 32 * k + lane;
+                        q[k] = j < t0 ? (__ldg(&row[j]) >> ks) : 0;
+                        // the element before j (row start: no boundaries below it)
+                        pv[k] = (lane == 0 && j < t0) ? (j > 0 ? (__ldg(&row[j - 1]) >> ks) : q[k]) : 0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int64_t j = c + 32 * k + lane;
+                        int prev = __shfl_up_sync(kFull, q[k], 1);
+                        if (lane == 0) prev = pv[k];
+                        if (j < t0) set_bounds(bnd, L, ew, prev + 1, q[k] < P - 1 ? q[k] : P - 1, static_cast<int32_t>(j));
+                        const int64_t left = t0 - (c + 32 * k);
+                        if (left > 0) qlast = __shfl_sync(kFull, q[k], left < 32 ? static_cast<int>(left - 1) : 31);
+                    }
+                }
+                if (t0 == len)
+                    for (int p = qlast + 1 + lane; p <= P - 1; p += 32)
+                        bnd[static_cast<int64_t>(p - 1) * L + ew] = static_cast<int32_t>(len);
+            }
+        }
+    }
+}
+
+// One block per item: product count of every interval, then the tasks.
+__global__ void __launch_bounds__(kHB) k_heavy_iplan(SymArgs g, SymScratch sc) {
+    __shared__ long long s_cnt[kMaxIntervals];
+    __shared__ int32_t s_t0[kMaxIntervals], s_t1[kMaxIntervals];
+    __shared__ long long s_tp[kMaxIntervals];
+    __shared__ int s_nt;
+    __shared__ long long s_base;
+    const int64_t i = blockIdx.x;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Intervals iv = interval_geometry(g.bcols);
+    const int P = iv.count;
+    const int64_t L = sc.heavy_eoff[i + 1] - sc.heavy_eoff[i] - 1;
+    const int64_t* ep = sc.heavy_epre + sc.heavy_eoff[i];
+    const int32_t* bnd = sc.heavy_bnd + sc.heavy_boff[i];
+    for (int p = w; p < P; p += kHW) {
+        long long c = 0;
+        for (int64_t e = lane; e < L; e += 32) {
+            const long long lo = p == 0 ? 0 : bnd[static_cast<int64_t>(p - 1) * L + e];
+            const long long hi = p == P - 1 ? ep[e + 1] - ep[e] : bnd[static_cast<int64_t>(p) * L + e];
+            c += hi - lo;
+        }
+        c = warp_sum_ll(c);
+        if (lane == 0) s_cnt[p] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int nt = 0;
+        long long acc = 0;
+        for (int p = 0; p < P; ++p) {
+            const long long c = s_cnt[p];
+            if (c == 0) {  // an empty interval ends the run
+                acc = 0;
+                continue;
+            }
+            if (acc == 0 || acc + c > kIntervalTarget) {
+                s_t0[nt] = p;
+                s_tp[nt] = 0;
+                ++nt;
+                acc = 0;
+            }
+            acc += c;
+            s_t1[nt - 1] = p + 1;
+            s_tp[nt - 1] += c;
+        }
+        s_nt = nt;
+        s_base = static_cast<long long>(atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[3]),
+                                                  static_cast<unsigned long long>(nt)));
+    }
+    __syncthreads();
+    IntervalTask* out = reinterpret_cast<IntervalTask*>(sc.heavy_tasks) + s_base;
+    for (int k = threadIdx.x; k < s_nt; k += kHB)
+        out[k] = IntervalTask{static_cast<int32_t>(i), s_t0[k], s_t1[k], 0, s_tp[k], 0};
+}
+
+__global__ void __launch_bounds__(kIvBlock, 2) k_heavy_intervals(SymArgs g, SymScratch sc, int64_t first) {
+    extern __shared__ int4 s_dyn_iv[];
+    uint32_t* s_set = reinterpret_cast<uint32_t*>(s_dyn_iv);
+    using Scan = cub::BlockScan<long long, kIvBlock>;
+    __shared__ typename Scan::TempStorage s_scan;
+    __shared__ int s_off[kIvStage + 1];
+    __shared__ int64_t s_b0[kIvStage];
+    __shared__ IntervalTask s_task;
+    const IntervalTask* tasks = reinterpret_cast<const IntervalTask*>(sc.heavy_tasks);
+    const int32_t* list = heavy_list(sc, first);
+    const Intervals iv = interval_geometry(g.bcols);
+    const int ks = iv.shift, P = iv.count;
+    const int lane = threadIdx.x & 31;
+    long long acc = 0;
+    for (;;) {
+        __syncthreads();  // the previous task is finished with the shared state
+        if (threadIdx.x == 0) {
+            const long long t = static_cast<long long>(
+                atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[7]), 1ULL));
+            s_task = t < sc.heavy_meta[3] ? tasks[t] : IntervalTask{-1, 0, 0, 0, 0, 0};
+        }
+        __syncthreads();
+        const IntervalTask t = s_task;
+        if (t.item < 0) break;
+        const int64_t i = t.item;
+        const int64_t L = sc.heavy_eoff[i + 1] - sc.heavy_eoff[i] - 1;
+        const int64_t* ep = sc.heavy_epre + sc.heavy_eoff[i];
+        const int64_t* eb = sc.heavy_eb0 + sc.heavy_eoff[i];
+        const int32_t* bnd = sc.heavy_bnd + sc.heavy_boff[i];
+        int cnt = 0;
+        for (int p = t.p0; p < t.p1; ++p) {
+            const int c0 = p << ks;
+            const int64_t width = (int64_t(p) + 1 << ks) < g.bcols ? (int64_t(1) << ks) : g.bcols - (int64_t(p) << ks);
+            const int words = static_cast<int>((width + 31) >> 5);
+            __syncthreads();  // the previous interval's inserts are done
+            uint4* s4 = reinterpret_cast<uint4*>(s_set);
+            for (int k = threadIdx.x; k < (words >> 2); k += kIvBlock) s4[k] = make_uint4(0u, 0u, 0u, 0u);
+            for (int k = (words & ~3) + threadIdx.x; k < words; k += kIvBlock) s_set[k] = 0u;
+            for (int64_t e0 = 0; e0 < L; e0 += kIvStage) {
+                const int n = static_cast<int>(L - e0 < kIvStage ? L - e0 : kIvStage);
+                long long len[kIvItems];
+                int64_t start[kIvItems];
+#pragma unroll
+                for (int k = 0; k < kIvItems; ++k) {
+                    const int j = threadIdx.x * kIvItems + k;
+                    len[k] = 0;
+                    start[k] = 0;
+                    if (j < n) {
+                        const int64_t e = e0 + j;
+                        const int64_t lo = p == 0 ? 0 : bnd[static_cast<int64_t>(p - 1) * L + e];
+                        const int64_t hi = p == P - 1 ? ep[e + 1] - ep[e] : bnd[static_cast<int64_t>(p) * L + e];
+                        len[k] = hi - lo;
+                        start[k] = eb[e] + lo;
+                    }
+                }
+                long long ex[kIvItems], tot;
+                __syncthreads();  // the clear is done / the previous round's walk is done
+                Scan(s_scan).ExclusiveSum(len, ex, tot);
+#pragma unroll
+                for (int k = 0; k < kIvItems; ++k) {
+                    const int j = threadIdx.x * kIvItems + k;
+                    if (j < n) {
+                        s_off[j] = static_cast<int>(ex[k]);
+                        s_b0[j] = start[k];
+                    }
+                }
+                if (threadIdx.x == 0) s_off[n] = static_cast<int>(tot);
+                __syncthreads();
+                chunk_products<kIvBlock / 32>(s_off, s_b0, n, 0, static_cast<int>(tot), g.bcol,
+                                              [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll], long long) {
+#pragma unroll
+                                                  for (int v = 0; v < kUnroll; ++v)
+                                                      if (valid[v]) {
+                                                          const uint32_t off = static_cast<uint32_t>(keys[v] - c0);
+                                                          const uint32_t bit = 1u << (off & 31);
+                                                          cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
+                                                      }
+                                              });
+            }
+        }
+        cnt = static_cast<int>(warp_sum_ll(cnt));
+        if (lane == 0 && cnt) {
+            if (g.out)
+                atomicAdd(reinterpret_cast<unsigned long long*>(&g.out[list[i]]),
+                          static_cast<unsigned long long>(cnt));
+            acc += cnt;
+        }
+    }
+    if (lane == 0 && acc)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[g.total_slot]),
+                  static_cast<unsigned long long>(acc));
+}
+
+// FLOP, A-row length and boundary cells of every heavy item (host batch
+// planning in exact mode).
 __global__ void k_heavy_flops(SymArgs g, SymScratch sc, int64_t count, int64_t* out) {
     const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (i >= count) return;
     const int32_t s = heavy_list(sc, 0)[i];
     const int32_t rid = g.rows ? g.rows[s] : g.row_lo + s;
-    out[i] = g.flop[rid - g.row_lo];
+    const int32_t r = rid - g.row_lo;
+    const int64_t L = g.a.rpt[r + 1] - g.a.rpt[r];
+    out[i] = g.flop[r];
+    out[count + i] = L;
+    out[2 * count + i] = (interval_geometry(g.bcols).count - 1) * L;
 }
 
 // ---- 6. return the used merge bitmaps to zero
@@ -520,6 +968,8 @@ __global__ void k_heavy_clean(SymScratch sc, int64_t slot_words) {
          i += int64_t(gridDim.x) * blockDim.x)
         sc.pool[i] = 0u;
 }
+
+int sort_smem() { return int(2 * kHeavyUnitProducts * 4 + (kHW + 1) * kPrivRanges * 4 + 4); }
 
 int place_smem(bool priv) {
     const int nw = priv ? kHW : 1, rm = priv ? kPrivRanges : kMaxRanges;
@@ -536,11 +986,10 @@ HeavyGeometry heavy_geometry(int32_t bcols) {
         h.wshift = lg;
         h.ranges = 1;
     } else {
-        int ws = lg - 8;  // R <= 256
-        if (ws < 17) ws = 17;
-        if (ws > kTaskSpanShift) ws = kTaskSpanShift;
+        const int ws = kTaskSpanShift;  // one range per task span
         h.wshift = ws;
         h.ranges = static_cast<int>((int64_t(bcols) + (int64_t(1) << ws) - 1) >> ws);
+        h.unit_sorted = h.ranges <= kPrivRanges;
     }
     // words of a merge slot: a task span (R > 1) or the whole row (R == 1)
     h.wwords = h.ranges > 1 ? (1 << kTaskSpanShift) / 32
@@ -565,50 +1014,60 @@ cudaError_t launch_heavy_flops(const SymArgs& args, const SymScratch& s, int64_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, int64_t first,
+cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sorted, int64_t first,
                              int64_t count, int num_sms, cudaStream_t stream) {
     if (count == 0) return cudaSuccess;
     static unsigned attr_done = 0;
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_done & (1u << (dev & 31)))) {
-        cudaFuncSetAttribute(k_heavy_run<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_heavy_run<1024, kRunItem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (1 << kSpanShift) / 8);
-        cudaFuncSetAttribute(k_heavy_run<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_heavy_run<512, kRunBuckets>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (1 << kTaskSpanShift) / 8);
-        cudaFuncSetAttribute(k_heavy_place<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             place_smem(true));
+        cudaFuncSetAttribute(k_heavy_run<512, kRunUnits>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (1 << kTaskSpanShift) / 8);
         cudaFuncSetAttribute(k_heavy_place<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              place_smem(false));
+        cudaFuncSetAttribute(k_heavy_sort_units, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             sort_smem());
+        cudaFuncSetAttribute(k_heavy_intervals, cudaFuncAttributeMaxDynamicSharedMemorySize, kIvSmem);
         attr_done |= 1u << (dev & 31);
     }
     const HeavyGeometry geo = heavy_geometry(args.bcols);
     const int R = geo.ranges;
     const unsigned sms = static_cast<unsigned>(num_sms);
-    k_heavy_prep<<<1, 256, 0, stream>>>(args, s, first, count);
-    k_heavy_entries<<<static_cast<unsigned>(count), 256, 0, stream>>>(args, s, first);
+    const unsigned items = static_cast<unsigned>(count);
+    k_heavy_prep<<<1, kPrepBlock, 0, stream>>>(args, s, first, count);
+    k_heavy_entries<<<items, 256, 0, stream>>>(args, s, first);
+    if (sorted) {
+        cudaMemsetAsync(s.heavy_bnd, 0, sizeof(int32_t) * s.heavy_bnd_cap, stream);
+        k_heavy_bounds<<<sms * 8, kHB, 0, stream>>>(args, s);
+        k_heavy_iplan<<<items, kHB, 0, stream>>>(args, s);
+        k_heavy_intervals<<<sms * 2, kIvBlock, kIvSmem, stream>>>(args, s, first);
+        return cudaGetLastError();
+    }
     if (R > 1) {
         cudaMemsetAsync(s.heavy_rc, 0, sizeof(long long) * count * R, stream);
-        if (R <= kPrivRanges) {
-            k_heavy_count<true><<<sms * 8, kHB, 0, stream>>>(args, s, first, count, R, geo.wshift);
-            k_heavy_offsets<<<static_cast<unsigned>(count), 256, 0, stream>>>(s, count, R);
-            k_heavy_place<true><<<sms * 4, kHB, place_smem(true), stream>>>(args, s, first, count,
-                                                                           R, geo.wshift);
+        if (geo.unit_sorted) {
+            k_heavy_sort_units<<<sms * 4, kHB, sort_smem(), stream>>>(args, s, first, count, R, geo.wshift);
+            k_heavy_plan_units<<<items, kPrivRanges, 0, stream>>>(s, count, R, s.heavy_task_cap);
+            k_heavy_run<512, kRunUnits><<<sms * 3, 512, (1 << kTaskSpanShift) / 8, stream>>>(
+                args, s, first, R, geo.wshift, geo.wwords);
         } else {
             k_heavy_count<false><<<sms * 8, kHB, 0, stream>>>(args, s, first, count, R, geo.wshift);
-            k_heavy_offsets<<<static_cast<unsigned>(count), 256, 0, stream>>>(s, count, R);
+            k_heavy_offsets<<<items, 256, 0, stream>>>(s, count, R);
             k_heavy_place<false><<<sms * 2, kHB, place_smem(false), stream>>>(args, s, first,
                                                                              count, R, geo.wshift);
+            k_heavy_plan<<<items, 128, 0, stream>>>(s, count, R, geo.wshift, s.heavy_task_cap);
+            k_heavy_run<512, kRunBuckets><<<sms * 3, 512, (1 << kTaskSpanShift) / 8, stream>>>(
+                args, s, first, R, geo.wshift, geo.wwords);
         }
-        k_heavy_plan<<<static_cast<unsigned>(count), 128, 0, stream>>>(s, count, R, geo.wshift,
-                                                                     s.heavy_task_cap);
-        k_heavy_run<512><<<sms * 3, 512, (1 << kTaskSpanShift) / 8, stream>>>(
-            args, s, first, R, geo.wshift, geo.wwords);
     } else {
         k_heavy_tasks_r1<<<static_cast<unsigned>((count + 127) / 128), 128, 0, stream>>>(
             s, count, s.heavy_task_cap);
-        k_heavy_run<1024><<<sms, 1024, (1 << kSpanShift) / 8, stream>>>(args, s, first, R,
-                                                                       geo.wshift, geo.wwords);
+        k_heavy_run<1024, kRunItem><<<sms, 1024, (1 << kSpanShift) / 8, stream>>>(
+            args, s, first, R, geo.wshift, geo.wwords);
     }
     k_heavy_clean<<<sms * 4, 256, 0, stream>>>(s, int64_t(geo.wwords));
     return cudaGetLastError();

@@ -73,6 +73,31 @@ constexpr int kForeignBin = 7;       // row owned by another rank
 constexpr int kNoBin = 8;            // padding lane
 //        products, many blocks per row over a global bitmap of B.cols bits.
 constexpr int64_t kHeavyUnitProducts = 4096;
+// Sorted B (the interval path, heavy.cu): B's columns are cut into
+// P = ceil(B.cols / 2^shift) intervals of 2^shift <= 2^kIvShift columns (one
+// 64 KB shared bitmap each); a heavy row's task is a run of consecutive
+// non-empty intervals with at most ~kIntervalTarget products.
+constexpr int kIvShift = 19;
+constexpr int kMaxIntervals = 256;  // B.cols <= 2^27; wider B takes the bucket path
+constexpr int64_t kIntervalTarget = 32768;
+#ifdef __CUDACC__
+#define SPNNZ_HD __host__ __device__
+#else
+#define SPNNZ_HD
+#endif
+struct Intervals {
+    int shift;
+    int32_t count;
+};
+SPNNZ_HD inline Intervals interval_geometry(int32_t bcols) {
+    int lg = 5;
+    while ((int64_t(1) << lg) < bcols) ++lg;  // 2^lg >= B.cols
+    Intervals iv;
+    iv.shift = lg < kIvShift ? lg : kIvShift;
+    iv.count = static_cast<int32_t>((int64_t(bcols) + (int64_t(1) << iv.shift) - 1) >> iv.shift);
+    if (iv.count < 1) iv.count = 1;
+    return iv;
+}
 
 struct SymScratch {
     int32_t* lists = nullptr;        // kNumBins * capacity item ids
@@ -86,12 +111,21 @@ struct SymScratch {
     int64_t* heavy_eb0 = nullptr;        // per entry: start of its B row
     long long* heavy_rc = nullptr;       // count * R: bucket counts, then bucket starts
     long long* heavy_cur = nullptr;      // count * R: placement cursors
-    int32_t* heavy_pbuf = nullptr;       // products grouped by (item, range)
+    int32_t* heavy_pbuf = nullptr;       // products grouped by (item, range) or (unit, range)
+    int32_t* heavy_utab = nullptr;       // units * (R + 1): range starts inside each sorted unit
     void* heavy_tasks = nullptr;         // HeavyTask[heavy_task_cap]
     int64_t heavy_task_cap = 0;
     uint32_t* pool = nullptr;            // merge bitmaps (W bits each), zero between calls
     long long* heavy_meta = nullptr;     // [0] units [1] sum(len+1) [2] sum(flop) of heavy
                                          // rows [3] tasks [4] merge slots used
+                                         // [5] sum((P-1) len) [6] sum(P) of heavy rows (interval path)
+                                         // [7] interval-task cursor
+    // interval path (sorted B)
+    int64_t* heavy_boff = nullptr;       // capacity + 1: boundary-table offset per item
+    int32_t* heavy_bnd = nullptr;        // per item (P-1) x len: interval starts inside each B row
+    int64_t heavy_bnd_cap = 0;
+    int32_t* heavy_unit_item = nullptr;  // per unit: its item
+    int32_t* heavy_unit_e0 = nullptr;    // per unit: the entry holding its first product
 };
 
 // Column-range geometry of the heavy path: ranges of 2^wshift bits (at most
@@ -100,6 +134,7 @@ struct HeavyGeometry {
     int wshift = 20;
     int ranges = 1;
     int32_t wwords = 1 << 15;
+    bool unit_sorted = false;  // 1 < ranges <= 256: units sorted in place (no count pass)
 };
 HeavyGeometry heavy_geometry(int32_t bcols);
 int64_t heavy_task_bound(int64_t count, int64_t products, int ranges);
@@ -129,9 +164,11 @@ cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_s
                              const cudaStream_t* streams);
 // Heavy tier for entries [first, first + count) of the heavy list (the host
 // learns the count after a sync and sizes the batch's buffers).
-cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, int64_t first,
+// sorted: B rows non-decreasing -> the interval path (no product buffer).
+cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sorted, int64_t first,
                              int64_t count, int num_sms, cudaStream_t stream);
-// FLOP of each heavy item in list order (batch planning when the heavy rows'
+// Per heavy item in list order: out[i] = FLOP, out[count + i] = A-row length,
+// out[2 count + i] = boundary-table cells (batch planning when the heavy rows'
 // products exceed one batch's buffers).
 cudaError_t launch_heavy_flops(const SymArgs& args, const SymScratch& s, int64_t count,
                                int64_t* out, cudaStream_t stream);
@@ -149,6 +186,9 @@ cudaError_t launch_sampled_flop(const int64_t* flop, int32_t row_lo, int32_t loc
                                 cudaStream_t stream);
 
 // Validation: counts rows outside [0, num_rows) into *bad.
+// B rows non-decreasing? cnt[0] == cnt[1] afterwards (device counters).
+cudaError_t launch_check_sorted(const int64_t* rpt, const int32_t* col, int32_t rows, int64_t nnz,
+                                unsigned long long* cnt, int num_sms, cudaStream_t stream);
 cudaError_t launch_check_rows(const int32_t* rows, int64_t n, int32_t num_rows, int32_t* bad,
                               cudaStream_t stream);
 

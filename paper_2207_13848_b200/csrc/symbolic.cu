@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_bin(SymArgs g, SymScratch sc) {
     for (int64_t base = int64_t(blockIdx.x) * BLOCK; base < g.n_items; base += stride) {
         const int64_t s = base + threadIdx.x;
         int bin = kNoBin;
-        long long hl = 0, hf = 0;
+        long long hl = 0, hf = 0, hb = 0, hp = 0;
         if (s < g.n_items) {
             const int32_t rid = g.rows ? g.rows[s] : g.row_lo + static_cast<int32_t>(s);
             const int32_t r = rid - g.row_lo;
@@ -48,6 +48,8 @@ __global__ void __launch_bounds__(BLOCK) k_sym_bin(SymArgs g, SymScratch sc) {
                 if (bin == kHeavyBin) {
                     hl = g.a.rpt[r + 1] - g.a.rpt[r] + 1;
                     hf = f;
+                    hp = interval_geometry(g.bcols).count;
+                    hb = (hp - 1) * (hl - 1);
                 }
             } else {
                 bin = kForeignBin;  // another rank's shard
@@ -68,11 +70,14 @@ __global__ void __launch_bounds__(BLOCK) k_sym_bin(SymArgs g, SymScratch sc) {
         if (__any_sync(kFull, hl != 0)) {
             hl = warp_sum_ll(hl);
             hf = warp_sum_ll(hf);
+            hb = warp_sum_ll(hb);
+            hp = warp_sum_ll(hp);
             if (lane == 0) {
-                atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[1]),
-                          static_cast<unsigned long long>(hl));
-                atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[2]),
-                          static_cast<unsigned long long>(hf));
+                auto* m = reinterpret_cast<unsigned long long*>(sc.heavy_meta);
+                atomicAdd(&m[1], static_cast<unsigned long long>(hl));
+                atomicAdd(&m[2], static_cast<unsigned long long>(hf));
+                atomicAdd(&m[5], static_cast<unsigned long long>(hb));
+                atomicAdd(&m[6], static_cast<unsigned long long>(hp));
             }
         }
     }

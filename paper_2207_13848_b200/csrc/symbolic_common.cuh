@@ -85,6 +85,10 @@ __device__ __forceinline__ void chunk_products(const OffT* off, const int64_t* b
         }
         e = lo;
     }
+    // the lane's current entry lives in registers: its end offset and the
+    // B.col index of product 0 (key of product q = bcol[kb + q])
+    OffT nxt = off[e + 1];
+    long long kb = static_cast<long long>(b0[e]) - static_cast<long long>(off[e]);
     for (OffT base = ws; base < we; base += 32 * kUnroll) {
         const OffT p = base + lane;
         int keys[kUnroll];
@@ -95,8 +99,14 @@ __device__ __forceinline__ void chunk_products(const OffT* off, const int64_t* b
             valid[u] = q < we;
             keys[u] = 0;
             if (valid[u]) {
-                while (off[e + 1] <= q) ++e;
-                keys[u] = __ldg(&bcol[b0[e] + (q - off[e])]);
+                if (nxt <= q) {
+                    do {
+                        ++e;
+                        nxt = off[e + 1];
+                    } while (nxt <= q);
+                    kb = static_cast<long long>(b0[e]) - static_cast<long long>(off[e]);
+                }
+                keys[u] = __ldg(&bcol[kb + q]);
             }
         }
         fn(keys, valid, static_cast<long long>(p));  // keys[u] is product p + 32 u

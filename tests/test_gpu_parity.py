@@ -168,10 +168,24 @@ def tier_matrix(n_rows, n_cols, lens, b_lens, seed):
     return a, b
 
 
-@pytest.mark.parametrize("ncols", [3000, 1 << 20])
-def test_every_bin_vs_oracle(P, oracle, ncols):
+HEAVY_PATHS = ["default", "intervals", "unsorted"]  # heavy-row algorithms (heavy.cu)
+
+
+def heavy_path(monkeypatch, path):
+    if path == "intervals":
+        monkeypatch.setenv("SPNNZ_HEAVY_INTERVALS", "1")
+    if path == "unsorted":
+        monkeypatch.setenv("SPNNZ_HEAVY_UNSORTED", "1")
+
+
+@pytest.mark.parametrize("path", HEAVY_PATHS)
+@pytest.mark.parametrize("ncols", [3000, 1 << 20, 1 << 24, 1 << 28])
+def test_every_bin_vs_oracle(oracle, ncols, path, monkeypatch):
     """Rows whose FLOP lands in every bin (<=32, <=512, <=2048, <=8192,
-    <=32768, heavy) including duplicates-heavy rows, for small and large B.cols."""
+    <=32768, heavy) including duplicates-heavy rows, for small and large B.cols
+    (one range, unit-sorted ranges, > 256 ranges), on both heavy paths."""
+    heavy_path(monkeypatch, path)
+    P = Predictor(0)
     rng = np.random.default_rng(ncols)
     lens = [0, 1, 2, 5, 10, 40, 100, 200, 300, 700, 1500, 2500] + list(rng.integers(0, 200, 200))
     b_lens = [1, 2, 3, 1, 2, 3, 1, 2, 3, 4] + list(rng.integers(0, 60, 2988)) + [2000, 2999]
@@ -194,13 +208,63 @@ def test_every_bin_vs_oracle(P, oracle, ncols):
     rows = np.arange(a.rows, dtype=np.int32)[::-1].copy()
     s = P.sampled_symbolic(rows)
     assert (s.nnz_per_row == nnz[rows]).all() and s.total_nnz == Z
+    P.close()
 
 
-def test_heavy_batching(P, oracle, monkeypatch):
+@pytest.mark.parametrize("path", HEAVY_PATHS)
+@pytest.mark.parametrize("ncols", [1 << 20, 1 << 28])
+def test_heavy_skewed_intervals(oracle, ncols, path, monkeypatch):
+    """Heavy rows whose products all fall in the first column interval: on a
+    2^28-column B the interval is wider than the bitmap, so the hash runs in
+    several key-hash passes; on 2^20 columns one bitmap interval takes all."""
+    rng = np.random.default_rng(7)
+    nb = 5000
+    b_rows = [np.sort(rng.choice(ncols >> 7, size=int(rng.integers(10, 60)), replace=False)).tolist()
+              for _ in range(nb)]
+    b = csr(nb, ncols, b_rows)
+    a_rows = [np.sort(rng.choice(nb, size=L, replace=False)).tolist() for L in (3000, 4000, 2500, 50)]
+    a = csr(len(a_rows), nb, a_rows)
+    heavy_path(monkeypatch, path)
+    q = Predictor(0)
+    q.load(a, b)
+    prof = q.compute_flop()
+    ex = q.exact_symbolic()
+    f, F, mx = oracle.compute_flop(a, b)
+    nnz, Z = oracle.exact_symbolic(a, b, f, mx)
+    assert (prof.flop_per_row == f).all() and f[:3].min() > 3 * 24576
+    assert (ex.nnz_per_row == nnz).all() and ex.total_nnz == Z
+    q.close()
+
+
+def test_unsorted_b_rows(oracle):
+    """B rows in arbitrary order (the sortedness check at load must route the
+    heavy rows to the sort-agnostic path): counts still exact."""
+    rng = np.random.default_rng(11)
+    lens = [3000, 2000, 100, 5, 2500]
+    a, b = tier_matrix(len(lens), 4000, lens, list(rng.integers(5, 40, 4000)), 9)
+    cols = [np.array(b.col[b.rpt[i]:b.rpt[i + 1]]) for i in range(b.rows)]
+    for c in cols:
+        rng.shuffle(c)
+    wide = 1 << 24
+    b = csr(b.rows, wide, [(c * (wide // 4000)).tolist() for c in cols])
+    q = Predictor(0)
+    q.load(a, b)
+    q.compute_flop()
+    ex = q.exact_symbolic()
+    f, F, mx = oracle.compute_flop(a, b)
+    nnz, Z = oracle.exact_symbolic(a, b, f, mx)
+    assert f.max() > 32768
+    assert (ex.nnz_per_row == nnz).all() and ex.total_nnz == Z
+    q.close()
+
+
+@pytest.mark.parametrize("path", HEAVY_PATHS)
+def test_heavy_batching(oracle, monkeypatch, path):
     """Heavy rows split over several batches (budget forced down to 100 K
     products): the batch loop, and the merge-bitmap pool returning to zero
     after each use, must keep the counts exact."""
     monkeypatch.setenv("SPNNZ_HEAVY_BATCH_PRODUCTS", "100000")
+    heavy_path(monkeypatch, path)
     q = Predictor(0)
     rng = np.random.default_rng(3)
     lens = [3000, 2500, 2800, 2900, 2700, 10, 3000]
@@ -326,6 +390,23 @@ def test_config1_full_arrays(P, golden):
         assert (rep.plan.sample_rows == arr[f"rows_{label}"]).all()
         s = P.sampled_symbolic(rep.plan.sample_rows)
         assert (s.nnz_per_row == arr[f"per_sample_{label}"]).all()
+
+
+@pytest.mark.parametrize("path", ["intervals", "unsorted"])
+@pytest.mark.parametrize("cfg", [2, 5])
+def test_config_heavy_paths_sampled(golden, cfg, path, monkeypatch):
+    """The non-default heavy-row algorithms reproduce the reference's sampled
+    NNZ on the skewed configs (the default path is checked below)."""
+    rec = golden["configs"][str(cfg)]
+    info = gen.CONFIGS[cfg]
+    a, b = gen.make_config(cfg)
+    heavy_path(monkeypatch, path)
+    q = Predictor(0)
+    q.load(a, b)
+    q.compute_flop()
+    rep = q.run_prediction(info["seed"], SamplePolicy(info["fraction"], UNCAPPED))
+    assert rep.stats.sampled_nnz == rec["modes"]["uncapped"]["report"]["sampled_nnz"]
+    q.close()
 
 
 @pytest.mark.parametrize("cfg", [2, 3, 4, 5])
