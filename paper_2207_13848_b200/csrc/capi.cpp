@@ -131,8 +131,9 @@ struct DBuf {
 struct spnnz_gpu_ctx {
     int device = 0, rank = 0, world = 1, num_sms = 148;
     cudaStream_t stream = nullptr;
-    cudaStream_t side[3] = {};            // symbolic tiers run concurrently
-    cudaEvent_t fork = nullptr, join[3] = {};
+    static constexpr int kSide = 4;
+    cudaStream_t side[kSide] = {};        // symbolic tiers, concurrent with the heavy rows
+    cudaEvent_t fork = nullptr, join[kSide] = {};
     ncclComm_t comm = nullptr;
 
     // matrices
@@ -333,22 +334,19 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     CU(cudaMemsetAsync(c->heavy_meta.p, 0, sizeof(long long) * 8, c->stream));
     if (n_items == 0) return SPNNZ_OK;
     CU(launch_sym_bin(g, s, c->stream));
-    // fork the tier kernels onto side streams, join before the heavy tier
+    // The host learns the heavy rows' number (bin counts) while the tier
+    // kernels run on side streams; the heavy batches then run on the main
+    // stream concurrently with the tiers, joined at the end.
     CU(cudaEventRecord(c->fork, c->stream));
-    for (int i = 0; i < 3; ++i) CU(cudaStreamWaitEvent(c->side[i], c->fork, 0));
-    const cudaStream_t tier_streams[4] = {c->stream, c->side[0], c->side[1], c->side[2]};
-    CU(launch_sym_tiers(g, s, c->num_sms, tier_streams));
-    for (int i = 0; i < 3; ++i) {
-        CU(cudaEventRecord(c->join[i], c->side[i]));
-        CU(cudaStreamWaitEvent(c->stream, c->join[i], 0));
-    }
-    *launches += 6;
-    // Heavy rows: the host learns their number, then runs pool-sized batches.
     CU(cudaMemcpyAsync(c->h_counts, c->counts.p, sizeof(int32_t) * 16, cudaMemcpyDeviceToHost,
                        c->stream));
     CU(cudaMemcpyAsync(c->h_meta, c->heavy_meta.p, sizeof(long long) * 8, cudaMemcpyDeviceToHost,
                        c->stream));
-    CU(cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaStreamWaitEvent(c->side[i], c->fork, 0));
+    CU(launch_sym_tiers(g, s, c->num_sms, c->side));
+    for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaEventRecord(c->join[i], c->side[i]));
+    *launches += 6;
+    CU(cudaStreamSynchronize(c->stream));  // bin + the two small copies
     const int64_t heavy = c->h_counts[kHeavyBin];
     if (heavy > 0) {
         // One batch when the heavy rows fit the batch budgets (always for
@@ -391,6 +389,7 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
             *launches += 8;
         }
     }
+    for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaStreamWaitEvent(c->stream, c->join[i], 0));
     return SPNNZ_OK;
 }
 
@@ -540,10 +539,10 @@ int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_counts, sizeof(int32_t) * 16);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_meta, sizeof(long long) * 8);
     for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
-    for (int i = 0; i < 3 && e == cudaSuccess; ++i)
+    for (int i = 0; i < spnnz_gpu_ctx::kSide && e == cudaSuccess; ++i)
         e = cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
-    for (int i = 0; i < 3 && e == cudaSuccess; ++i)
+    for (int i = 0; i < spnnz_gpu_ctx::kSide && e == cudaSuccess; ++i)
         e = cudaEventCreateWithFlags(&c->join[i], cudaEventDisableTiming);
     int rc = SPNNZ_OK;
     if (e != cudaSuccess) rc = set_err(SPNNZ_ECUDA, "create: %s", cudaGetErrorString(e));
@@ -599,7 +598,7 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     if (c->h_meta) cudaFreeHost(c->h_meta);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) {
         if (c->side[i]) cudaStreamDestroy(c->side[i]);
         if (c->join[i]) cudaEventDestroy(c->join[i]);
     }

@@ -264,10 +264,10 @@ cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_s
     }
     const unsigned sms = static_cast<unsigned>(num_sms);
     k_sym_tiny<256><<<sms * 4, 256, 0, streams[0]>>>(args, s);
-    k_sym_warp_hash<256><<<sms * 4, 256, 0, streams[1]>>>(args, s);
-    k_sym_block_hash<kT3Block, kT3Slots, 3><<<sms * 8, kT3Block, kT3Slots * 4, streams[2]>>>(args, s);
-    k_sym_block_hash<kT4Block, kT4Slots, 4><<<sms * 3, kT4Block, kT4Slots * 4, streams[3]>>>(args, s);
-    k_sym_block_hash<kT5Block, kT5Slots, 5><<<sms, kT5Block, kT5Slots * 4, streams[0]>>>(args, s);
+    k_sym_warp_hash<256><<<sms * 4, 256, 0, streams[0]>>>(args, s);
+    k_sym_block_hash<kT3Block, kT3Slots, 3><<<sms * 8, kT3Block, kT3Slots * 4, streams[1]>>>(args, s);
+    k_sym_block_hash<kT4Block, kT4Slots, 4><<<sms * 3, kT4Block, kT4Slots * 4, streams[2]>>>(args, s);
+    k_sym_block_hash<kT5Block, kT5Slots, 5><<<sms, kT5Block, kT5Slots * 4, streams[3]>>>(args, s);
     return cudaGetLastError();
 }
 
