@@ -139,8 +139,8 @@ struct spnnz_gpu_ctx {
     // matrices
     bool loaded = false;
     bool same_b = false;
-    bool b_sorted = false;     // B rows non-decreasing (enables the interval heavy path)
-    bool b_intervals = false;  // interval heavy path selected (SPNNZ_HEAVY_INTERVALS=1)
+    bool b_intervals = false;  // interval heavy path requested (SPNNZ_HEAVY_INTERVALS=1)
+    bool b_sorted = false;     // ... and B's rows checked non-decreasing at load
     int32_t a_rows = 0, a_cols = 0, b_rows = 0, b_cols = 0;
     int32_t row_lo = 0, row_hi = 0;
     DBuf<int64_t> b_rpt;
@@ -707,19 +707,21 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
         v.col = c->a_col.p - a_lo;  // indexed with absolute offsets
     }
     c->a = v;
-    // B's rows sorted (the reference's CsrMatrix invariant)?  Decides the
-    // heavy-row algorithm; both give identical counts.
-    RC(c->sorted_cnt.ensure(2));
-    CU(launch_check_sorted(c->b_rpt.p, c->b_col.p, c->b_rows, b_nnz,
-                           reinterpret_cast<unsigned long long*>(c->sorted_cnt.p), c->num_sms, c->stream));
-    long long cnt[2] = {0, 0};
-    CU(cudaMemcpyAsync(cnt, c->sorted_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
-    c->b_sorted = cnt[0] == cnt[1];
-    if (const char* env = getenv("SPNNZ_HEAVY_UNSORTED"))  // test knob: force the sort-agnostic path
-        if (atoi(env) > 0) c->b_sorted = false;
+    // The interval heavy path (opt-in, SPNNZ_HEAVY_INTERVALS=1) needs B's rows
+    // sorted -- the reference's CsrMatrix invariant, checked here once.
     const char* ivenv = getenv("SPNNZ_HEAVY_INTERVALS");
     c->b_intervals = ivenv && atoi(ivenv) > 0;
+    c->b_sorted = false;
+    if (c->b_intervals) {
+        RC(c->sorted_cnt.ensure(2));
+        CU(launch_check_sorted(c->b_rpt.p, c->b_col.p, c->b_rows, b_nnz,
+                               reinterpret_cast<unsigned long long*>(c->sorted_cnt.p), c->num_sms,
+                               c->stream));
+        long long cnt[2] = {0, 0};
+        CU(cudaMemcpyAsync(cnt, c->sorted_cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        c->b_sorted = cnt[0] == cnt[1];
+    }
     c->loaded = true;
     return SPNNZ_OK;
 }

@@ -11,15 +11,18 @@
 //      L2-resident under an evict_last policy -- the int64 pair
 //      B.rpt[k], B.rpt[k+1] is 134 MB and is not);
 //   1. k_flop_partition: first owned row of every tile (lower_bound in rpt);
-//   2. k_flop, per tile: 16-byte evict_first loads of the tile's A.col into
-//      shared memory, then the deg[] gathers (8 per thread in flight, lanes
-//      on consecutive entries), staged in shared memory; each thread then sums one owned row's slice of the staged
-//      degrees (rows longer than 64 in the tile go to a warp each), writes
-//      flop[row] and the tile's partials: F, max, and the leading segment
+//   2. k_flop, per tile: each thread loads V = 16 consecutive A.col entries
+//      (16-byte evict_first loads) and issues their 16 degree gathers at once
+//      (evict_last); the tile's owned rows mark their starts in a 4096-bit
+//      shared bitmap; each thread sums its entries segment by segment in
+//      registers (rows inside the thread are written directly) and a
+//      block-wide segmented scan of (flag, partial, row) carries finishes the
+//      rows that span threads.  Partials out: F, max, and the leading segment
 //      that belongs to a row owned by an earlier tile;
 //   3. k_flop_fixup adds the leading segments to the long rows they continue
 //      and reduces F and max over tiles.
-// Per entry ~10 thread instructions (a merge-path walk cost ~90).
+// No shared-memory round trip per entry: the L1/shared pipe is left to the
+// gathers, which bound the pass (~1 L2 request per entry).
 // Algorithmic bytes: 8(M+1) A.rpt + 4 nnz A.col + 8(K+1) B.rpt + 8M flop
 // (the 2K-byte degree array's write and re-reads are extra traffic).
 // Integer-only: bit-exact.
@@ -28,8 +31,6 @@
 
 namespace spnnz_gpu {
 namespace {
-
-constexpr int kLongRow = 64;  // in-tile row slices longer than this go to a warp
 
 // deg16[k] = min(B.rpt[k+1] - B.rpt[k], 0xFFFF); 0xFFFF means "look the
 // exact length up in B.rpt" (rows with >= 65535 entries are rare).
@@ -70,6 +71,29 @@ __global__ void k_flop_partition(const int64_t* __restrict__ arpt, int32_t m, in
     tile_row[t] = static_cast<int32_t>(lo);
 }
 
+// Segmented-sum carry across threads: (has a row start, carried value, row).
+struct Carry {
+    int flag;
+    long long v;
+    int32_t row;
+};
+
+__device__ __forceinline__ Carry carry_op(const Carry& a, const Carry& b) {
+    Carry r;
+    r.flag = a.flag | b.flag;
+    r.v = b.flag ? b.v : a.v + b.v;
+    r.row = b.flag ? b.row : a.row;
+    return r;
+}
+
+__device__ __forceinline__ Carry shfl_up_carry(const Carry& c, int d) {
+    Carry r;
+    r.flag = __shfl_up_sync(0xffffffffu, c.flag, d);
+    r.v = __shfl_up_sync(0xffffffffu, c.v, d);
+    r.row = __shfl_up_sync(0xffffffffu, c.row, d);
+    return r;
+}
+
 template <int BLOCK, int V>
 __global__ void __launch_bounds__(BLOCK, 5)
 k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
@@ -77,115 +101,122 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
        int64_t base, int64_t nnz, const int32_t* __restrict__ tile_row,
        int64_t* __restrict__ flop, long long* __restrict__ tile_lead,
        long long* __restrict__ tile_total, long long* __restrict__ tile_max) {
-    constexpr int TILE = BLOCK * V;
-    static_assert(TILE == kFlopTile, "tile size");
-    __shared__ int32_t s_deg[TILE];
-    __shared__ int32_t s_long_row[TILE / kLongRow + 2];
-    __shared__ int32_t s_long_lo[TILE / kLongRow + 2];
-    __shared__ int32_t s_long_hi[TILE / kLongRow + 2];
-    __shared__ int s_nlong;
-    __shared__ long long s_red[BLOCK / 32];
+    constexpr int TILE = BLOCK * V, NW = BLOCK / 32;
+    static_assert(TILE == kFlopTile && V == 16, "tile size");
+    __shared__ uint32_t s_start[TILE / 32];  // bit i: an owned non-empty row starts at entry i
+    __shared__ int32_t s_rowat[TILE];        // ... and its id (read only where the bit is set)
+    __shared__ Carry s_wc[NW];
+    __shared__ long long s_red[NW];
 
     const uint64_t first = policy_evict_first(), last = policy_evict_last();
     const int64_t t = blockIdx.x;
     const int64_t ts = tile_start(base, nnz, t), te = tile_start(base, nnz, t + 1);
     const int n = static_cast<int>(te - ts);
-    const int tid = threadIdx.x;
-    if (tid == 0) s_nlong = 0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int k = tid; k < TILE / 32; k += BLOCK) s_start[k] = 0u;
 
-    // 1. stage the tile's degrees.  16-byte evict_first loads of A.col into
-    //    shared memory (the tile start is a multiple of 4096 entries, so only
-    //    a shard's first and last tiles are partial), then each thread reads
-    //    entries tid, tid + 256, ... back (stride 1 across a warp, so the
-    //    gathers of neighbouring entries share sectors when the columns are
-    //    close, as in banded matrices), issues all its gathers, and stores
-    //    the degrees in place.
-    int32_t* s_col = s_deg;
-    if (n == TILE && (reinterpret_cast<uintptr_t>(acol + ts) & 15) == 0) {
-        const int4* src = reinterpret_cast<const int4*>(acol + ts);
-        int4* dst = reinterpret_cast<int4*>(s_col);
+    // 1. this thread's V consecutive entries: columns (16-byte evict_first
+    //    loads when the tile is whole), then all V degree gathers in flight
+    const int i0 = tid * V;
+    int32_t d[V];
+    {
+        int32_t c[V];
+        if (n == TILE && (reinterpret_cast<uintptr_t>(acol + ts) & 15) == 0) {
+            const int4* src = reinterpret_cast<const int4*>(acol + ts + i0);
 #pragma unroll
-        for (int k = 0; k < V / 4; ++k) dst[tid + k * BLOCK] = ld_stream_v4(src + tid + k * BLOCK, first);
-    } else {
-        for (int i = tid; i < n; i += BLOCK) s_col[i] = ld_stream_i32(acol + ts + i, first);
+            for (int k = 0; k < V / 4; ++k) {
+                const int4 x = ld_stream_v4(src + k, first);
+                c[4 * k] = x.x;
+                c[4 * k + 1] = x.y;
+                c[4 * k + 2] = x.z;
+                c[4 * k + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < V; ++k) c[k] = i0 + k < n ? ld_stream_i32(acol + ts + i0 + k, first) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k) d[k] = c[k] >= 0 ? static_cast<int32_t>(ld_keep_u16(bdeg + c[k], last)) : 0;
+#pragma unroll
+        for (int k = 0; k < V; ++k)
+            if (d[k] == 0xFFFF) d[k] = static_cast<int32_t>(__ldg(&brpt[c[k] + 1]) - __ldg(&brpt[c[k]]));
     }
-    __syncthreads();
     long long tsum = 0;
 #pragma unroll
-    for (int h = 0; h < V; h += V / 2) {
-        int32_t c[V / 2], dg[V / 2];
-#pragma unroll
-        for (int k = 0; k < V / 2; ++k) {
-            const int i = tid + (h + k) * BLOCK;
-            c[k] = i < n ? s_col[i] : 0;
-        }
-#pragma unroll
-        for (int k = 0; k < V / 2; ++k) {
-            const int i = tid + (h + k) * BLOCK;
-            dg[k] = i < n ? static_cast<int32_t>(ld_keep_u16(bdeg + c[k], last)) : 0;
-        }
-#pragma unroll
-        for (int k = 0; k < V / 2; ++k) {
-            const int i = tid + (h + k) * BLOCK;
-            if (i < n) {
-                int32_t d = dg[k];
-                if (d == 0xFFFF)
-                    d = static_cast<int32_t>(__ldg(&brpt[c[k] + 1]) - __ldg(&brpt[c[k]]));
-                s_deg[i] = d;
-                tsum += d;
-            }
-        }
-    }
-    __syncthreads();
+    for (int k = 0; k < V; ++k) tsum += d[k];
+    __syncthreads();  // the start bitmap is clear
 
-    // 2. owned rows [r0, r1): one thread per row, long slices deferred.
+    // 2. owned rows [r0, r1): mark where the non-empty ones start; empty ones are 0
     const int32_t r0 = tile_row[t], r1 = tile_row[t + 1];
-    long long tmax = 0;
     for (int32_t r = r0 + tid; r < r1; r += BLOCK) {
         const int64_t a = __ldg(&arpt[r]), b = __ldg(&arpt[r + 1]);
-        const int lo = static_cast<int>(a - ts);
-        const int hi = static_cast<int>((b < te ? b : te) - ts);
-        if (hi - lo > kLongRow) {
-            const int slot = atomicAdd(&s_nlong, 1);
-            s_long_row[slot] = r;
-            s_long_lo[slot] = lo;
-            s_long_hi[slot] = hi;
+        if (b > a) {
+            const int pos = static_cast<int>(a - ts);
+            atomicOr(&s_start[pos >> 5], 1u << (pos & 31));
+            s_rowat[pos] = r;
         } else {
-            long long sum = 0;
-            for (int i = lo; i < hi; ++i) sum += s_deg[i];
-            flop[r] = sum;
-            if (b <= te) tmax = sum > tmax ? sum : tmax;  // complete within the tile
-        }
-    }
-    // the leading slice [0, lead) continues row r0 - 1 from an earlier tile
-    if (tid == 0) {
-        const int64_t first_start = r0 < m ? __ldg(&arpt[r0]) : te;
-        const int lead = static_cast<int>((first_start < te ? first_start : te) - ts);
-        if (lead > 0) {
-            const int slot = atomicAdd(&s_nlong, 1);
-            s_long_row[slot] = -1;
-            s_long_lo[slot] = 0;
-            s_long_hi[slot] = lead;
-        } else {
-            tile_lead[t] = 0;
+            flop[r] = 0;
         }
     }
     __syncthreads();
 
-    // 3. long slices: one warp each
-    const int lane = tid & 31, warp = tid >> 5;
-    for (int j = warp; j < s_nlong; j += BLOCK / 32) {
-        long long sum = 0;
-        for (int i = s_long_lo[j] + lane; i < s_long_hi[j]; i += 32) sum += s_deg[i];
-        sum = warp_sum_ll(sum);
-        if (lane == 0) {
-            const int32_t r = s_long_row[j];
-            if (r < 0) {
-                tile_lead[t] = sum;
+    // 3. segmented sum over the thread's entries: rows that start and end
+    //    inside are written here; the head (before the first start) and the
+    //    tail (from the last start) are combined across threads below
+    const uint32_t bits = (s_start[i0 >> 5] >> (i0 & 31)) & 0xFFFFu;
+    long long cur = 0, head = 0, tmax = 0;
+    int32_t row = -1;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        if ((bits >> k) & 1u) {
+            if (row >= 0) {
+                flop[row] = cur;  // complete inside the thread
+                tmax = cur > tmax ? cur : tmax;
             } else {
-                flop[r] = sum;
-                if (__ldg(&arpt[r + 1]) <= te) tmax = sum > tmax ? sum : tmax;
+                head = cur;
             }
+            row = s_rowat[i0 + k];
+            cur = 0;
+        }
+        cur += d[k];
+    }
+    Carry mine;
+    mine.flag = bits != 0u;
+    mine.v = mine.flag ? cur : cur;  // tail value, or the whole thread when no row starts here
+    mine.row = row;
+    if (!mine.flag) head = cur;
+
+    // 4. block-wide exclusive segmented scan of the carries
+    Carry inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const Carry u = shfl_up_carry(inc, o);
+        if (lane >= o) inc = carry_op(u, inc);
+    }
+    if (lane == 31) s_wc[warp] = inc;
+    __syncthreads();
+    Carry pre{0, 0, -1};  // carry entering this warp
+    for (int w = 0; w < warp; ++w) pre = carry_op(pre, s_wc[w]);
+    Carry excl = shfl_up_carry(inc, 1);
+    if (lane == 0) excl = Carry{0, 0, -1};
+    const Carry cin = carry_op(pre, excl);  // carry entering this thread
+    if (mine.flag) {
+        // the carried row ends right before this thread's first start
+        const long long v = cin.v + head;
+        if (cin.flag) {
+            flop[cin.row] = v;
+            tmax = v > tmax ? v : tmax;
+        } else {
+            tile_lead[t] = v;  // continues a row owned by an earlier tile
+        }
+    }
+    if (tid == BLOCK - 1) {
+        const Carry all = carry_op(cin, mine);
+        if (all.flag) {
+            flop[all.row] = all.v;  // the fixup adds the following tiles' leading slices
+            if (__ldg(&arpt[all.row + 1]) <= te) tmax = all.v > tmax ? all.v : tmax;
+        } else {
+            tile_lead[t] = all.v;  // no row starts in this tile
         }
     }
     const long long bsum = block_sum_ll<BLOCK>(tsum, s_red);

@@ -168,14 +168,14 @@ def tier_matrix(n_rows, n_cols, lens, b_lens, seed):
     return a, b
 
 
-HEAVY_PATHS = ["default", "intervals", "unsorted"]  # heavy-row algorithms (heavy.cu)
+# heavy-row algorithms (heavy.cu): the default sort-agnostic bucket paths and
+# the opt-in sorted-B interval path
+HEAVY_PATHS = ["default", "intervals"]
 
 
 def heavy_path(monkeypatch, path):
     if path == "intervals":
         monkeypatch.setenv("SPNNZ_HEAVY_INTERVALS", "1")
-    if path == "unsorted":
-        monkeypatch.setenv("SPNNZ_HEAVY_UNSORTED", "1")
 
 
 @pytest.mark.parametrize("path", HEAVY_PATHS)
@@ -236,9 +236,12 @@ def test_heavy_skewed_intervals(oracle, ncols, path, monkeypatch):
     q.close()
 
 
-def test_unsorted_b_rows(oracle):
-    """B rows in arbitrary order (the sortedness check at load must route the
-    heavy rows to the sort-agnostic path): counts still exact."""
+@pytest.mark.parametrize("path", HEAVY_PATHS)
+def test_unsorted_b_rows(oracle, path, monkeypatch):
+    """B rows in arbitrary order (with the interval path requested, the
+    sortedness check at load must route the heavy rows to the sort-agnostic
+    path): counts still exact."""
+    heavy_path(monkeypatch, path)
     rng = np.random.default_rng(11)
     lens = [3000, 2000, 100, 5, 2500]
     a, b = tier_matrix(len(lens), 4000, lens, list(rng.integers(5, 40, 4000)), 9)
@@ -392,11 +395,11 @@ def test_config1_full_arrays(P, golden):
         assert (s.nnz_per_row == arr[f"per_sample_{label}"]).all()
 
 
-@pytest.mark.parametrize("path", ["intervals", "unsorted"])
 @pytest.mark.parametrize("cfg", [2, 5])
-def test_config_heavy_paths_sampled(golden, cfg, path, monkeypatch):
-    """The non-default heavy-row algorithms reproduce the reference's sampled
-    NNZ on the skewed configs (the default path is checked below)."""
+def test_config_interval_path_sampled(golden, cfg, monkeypatch):
+    """The interval heavy-row path reproduces the reference's sampled NNZ on
+    the skewed configs (the default path is checked below)."""
+    path = "intervals"
     rec = golden["configs"][str(cfg)]
     info = gen.CONFIGS[cfg]
     a, b = gen.make_config(cfg)

@@ -37,8 +37,9 @@ def main():
         with open(os.path.join(out, f"{args.round}_{name}.md"), "w") as f:
             f.write(f"# {args.round} launch list: {name}\n\n")
             f.write("`ncu --metrics gpu__time_duration.sum --clock-control none` over "
-                    "`bench.py --profile-steps 2` (two predictor passes, cold-cache, serialised: "
-                    "compare shares, not absolutes).\n\n```\n")
+                    "`bench.py --config <c> --profile-steps 1` (tools/qprof.sh: load + one "
+                    "predictor pass; per-launch times are cold-cache and serialised: compare "
+                    "shares, not absolutes).\n\n```\n")
             f.write(L.summarize(p) + "\n```\n")
             if args.note:
                 f.write("\n" + args.note + "\n")
