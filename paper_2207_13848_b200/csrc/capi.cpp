@@ -263,25 +263,25 @@ int heavy_buffers(spnnz_gpu_ctx* c, int64_t count, int64_t ents, int64_t product
     RC(c->heavy_eb0.ensure(ents));
     s->heavy_epre = c->heavy_epre.p;
     s->heavy_eb0 = c->heavy_eb0.p;
+    // unit -> (item, first entry) map, written by k_heavy_entries
+    const int64_t units = products / kHeavyUnitProducts + count;
+    RC(c->heavy_unit_item.ensure(units));
+    RC(c->heavy_unit_e0.ensure(units));
+    s->heavy_unit_item = c->heavy_unit_item.p;
+    s->heavy_unit_e0 = c->heavy_unit_e0.p;
     if (interval_path(c)) {
-        const int64_t units = products / kHeavyUnitProducts + count;
         const int64_t tasks = count * int64_t(interval_geometry(c->b_cols).count);
         RC(c->heavy_boff.ensure(count + 1));
         RC(c->heavy_bnd.ensure(std::max<int64_t>(cells, 1)));
-        RC(c->heavy_unit_item.ensure(units));
-        RC(c->heavy_unit_e0.ensure(units));
         RC(c->heavy_tasks.ensure(2 * std::max<int64_t>(tasks, 1)));
         s->heavy_boff = c->heavy_boff.p;
         s->heavy_bnd = c->heavy_bnd.p;
         s->heavy_bnd_cap = cells;
-        s->heavy_unit_item = c->heavy_unit_item.p;
-        s->heavy_unit_e0 = c->heavy_unit_e0.p;
         s->heavy_tasks = c->heavy_tasks.p;
         s->heavy_task_cap = tasks;
         return SPNNZ_OK;
     }
     s->heavy_boff = nullptr;
-    s->heavy_unit_item = nullptr;
     if (geo.ranges > 1) {
         RC(c->heavy_rc.ensure(count * geo.ranges));
         RC(c->heavy_cur.ensure(count * geo.ranges));

@@ -158,26 +158,35 @@ __global__ void __launch_bounds__(256) k_heavy_entries(SymArgs g, SymScratch sc,
 struct Unit {
     int64_t item;
     long long p0, p1;  // product window of the item
+    int64_t e0;        // entry holding product p0, or -1 (unknown)
 };
 
 __device__ __forceinline__ Unit find_unit(const SymScratch& sc, int64_t count, long long u) {
-    int64_t lo = 0, hi = count - 1;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (sc.heavy_unit_off[mid] <= u) lo = mid; else hi = mid - 1;
-    }
     Unit r;
-    r.item = lo;
-    const long long ftot = sc.heavy_foff[lo + 1] - sc.heavy_foff[lo];
-    r.p0 = (u - sc.heavy_unit_off[lo]) * kHeavyUnitProducts;
+    if (sc.heavy_unit_item) {  // the unit map written by k_heavy_entries
+        r.item = sc.heavy_unit_item[u];
+        r.e0 = sc.heavy_unit_e0[u];
+    } else {
+        int64_t lo = 0, hi = count - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (sc.heavy_unit_off[mid] <= u) lo = mid; else hi = mid - 1;
+        }
+        r.item = lo;
+        r.e0 = -1;
+    }
+    const long long ftot = sc.heavy_foff[r.item + 1] - sc.heavy_foff[r.item];
+    r.p0 = (u - sc.heavy_unit_off[r.item]) * kHeavyUnitProducts;
     r.p1 = r.p0 + kHeavyUnitProducts < ftot ? r.p0 + kHeavyUnitProducts : ftot;
     return r;
 }
 
-// Thread 0 locates unit u, every thread gets it (block-uniform call).
+// Every thread gets unit u (block-uniform call; the barrier also separates
+// consecutive units' use of shared memory).
 __device__ __forceinline__ Unit find_unit_block(const SymScratch& sc, int64_t count, long long u) {
     __shared__ Unit s_unit;
     __syncthreads();
+    if (sc.heavy_unit_item) return find_unit(sc, count, u);
     if (threadIdx.x == 0) s_unit = find_unit(sc, count, u);
     __syncthreads();
     return s_unit;
@@ -187,28 +196,32 @@ __device__ __forceinline__ Unit find_unit_block(const SymScratch& sc, int64_t co
 // 2^31): chunks of BLOCK entries are staged in shared memory with offsets
 // relative to p0 (clamped to [0, p1 - p0], B-row starts shifted to match) so
 // the per-product cursor works in 32-bit.  fn(keys, valid, q) with keys[u]
-// = product p0 + q + 32 u.
+// = product p0 + q + 32 u.  e0: the entry holding product p0, or -1.
 template <int BLOCK, typename Fn>
 __device__ __forceinline__ void item_products(const SymArgs& g, const SymScratch& sc,
                                               int64_t first, int64_t item, long long p0,
-                                              long long p1, int* s_off, int64_t* s_b0, Fn&& fn) {
+                                              long long p1, int* s_off, int64_t* s_b0, Fn&& fn,
+                                              int64_t e0 = -1) {
     const ItemRow it = item_row(g, heavy_list(sc, first)[item]);
     const int64_t L = it.a1 - it.a0;
     const int64_t* ep = sc.heavy_epre + sc.heavy_eoff[item];
     const int64_t* eb = sc.heavy_eb0 + sc.heavy_eoff[item];
     const long long span = p1 - p0;
     __shared__ int64_t s_e0;
-    __syncthreads();  // s_e0 of a previous call is consumed
-    if (threadIdx.x == 0) {
-        int64_t e0 = 0, e1 = L - 1;  // largest entry with ep[e] <= p0
-        while (e0 < e1) {
-            const int64_t mid = (e0 + e1 + 1) >> 1;
-            if (ep[mid] <= p0) e0 = mid; else e1 = mid - 1;
+    if (e0 < 0) {
+        __syncthreads();  // s_e0 of a previous call is consumed
+        if (threadIdx.x == 0) {
+            int64_t lo = 0, hi = L - 1;  // largest entry with ep[e] <= p0
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (ep[mid] <= p0) lo = mid; else hi = mid - 1;
+            }
+            s_e0 = lo;
         }
-        s_e0 = e0;
+        __syncthreads();
+        e0 = s_e0;
     }
-    __syncthreads();
-    for (int64_t e = s_e0;;) {
+    for (int64_t e = e0;;) {
         const int n = static_cast<int>(L - e < BLOCK ? L - e : BLOCK);
         __syncthreads();  // previous chunk fully consumed
         for (int i = threadIdx.x; i <= n; i += BLOCK) {
@@ -244,7 +257,7 @@ __global__ void __launch_bounds__(kHB) k_heavy_count(SymArgs g, SymScratch sc, i
 #pragma unroll
                                for (int k = 0; k < kUnroll; ++k)
                                    if (valid[k]) atomicAdd(&s_hist[w][keys[k] >> wshift], 1);
-                           });
+                           }, un.e0);
         long long* rc = sc.heavy_rc + un.item * R;
         for (int r = threadIdx.x; r < R; r += kHB) {
             int c = 0;
@@ -311,7 +324,7 @@ __global__ void __launch_bounds__(kHB) k_heavy_place(SymArgs g, SymScratch sc, i
 #pragma unroll
                                for (int k = 0; k < kUnroll; ++k)
                                    if (valid[k]) s_in[q + 32 * k] = keys[k];
-                           });
+                           }, un.e0);
         const int n = static_cast<int>(un.p1 - un.p0);
         for (int i = threadIdx.x; i < n; i += kHB) atomicAdd(&s_hist[w][s_in[i] >> wshift], 1);
         __syncthreads();
@@ -374,29 +387,28 @@ __global__ void __launch_bounds__(kHB) k_heavy_place(SymArgs g, SymScratch sc, i
 // heavy_rc for the planner.  A task then reads range r as one slice per unit.
 __global__ void __launch_bounds__(kHB) k_heavy_sort_units(SymArgs g, SymScratch sc, int64_t first,
                                                           int64_t count, int R, int wshift) {
-    constexpr int RM = kPrivRanges;
     __shared__ int s_off[kHB + 1];
     __shared__ int64_t s_b0[kHB];
-    // dynamic: keys_in[U] | keys_out[U] | hist[kHW][RM] | offs[RM + 1]
+    // dynamic: keys_in[U] | keys_out[U] | hist[kHW][R] | offs[R + 1]
     extern __shared__ int4 s_dyn_sort[];
     int32_t* s_in = reinterpret_cast<int32_t*>(s_dyn_sort);
     int32_t* s_out = s_in + kHeavyUnitProducts;
-    int* s_hist = s_out + kHeavyUnitProducts;  // [w * RM + r]
-    int* s_offs = s_hist + kHW * RM;
+    int* s_hist = s_out + kHeavyUnitProducts;  // [w * R + r]
+    int* s_offs = s_hist + kHW * R;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long units = sc.heavy_meta[0];
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit un = find_unit_block(sc, count, u);
-        for (int k = threadIdx.x; k < kHW * RM; k += kHB) s_hist[k] = 0;
+        for (int k = threadIdx.x; k < kHW * R; k += kHB) s_hist[k] = 0;
         item_products<kHB>(g, sc, first, un.item, un.p0, un.p1, s_off, s_b0,
                            [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll],
                                long long q) {
 #pragma unroll
                                for (int k = 0; k < kUnroll; ++k)
                                    if (valid[k]) s_in[q + 32 * k] = keys[k];
-                           });
+                           }, un.e0);
         const int n = static_cast<int>(un.p1 - un.p0);
-        for (int i = threadIdx.x; i < n; i += kHB) atomicAdd(&s_hist[w * RM + (s_in[i] >> wshift)], 1);
+        for (int i = threadIdx.x; i < n; i += kHB) atomicAdd(&s_hist[w * R + (s_in[i] >> wshift)], 1);
         __syncthreads();
         // per range: warp offsets inside the range, the range total
         long long* rc = sc.heavy_rc + un.item * R;
@@ -404,8 +416,8 @@ __global__ void __launch_bounds__(kHB) k_heavy_sort_units(SymArgs g, SymScratch 
             int tot = 0;
 #pragma unroll
             for (int v = 0; v < kHW; ++v) {
-                const int c = s_hist[v * RM + r];
-                s_hist[v * RM + r] = tot;
+                const int c = s_hist[v * R + r];
+                s_hist[v * R + r] = tot;
                 tot += c;
             }
             s_offs[r] = tot;
@@ -431,7 +443,7 @@ __global__ void __launch_bounds__(kHB) k_heavy_sort_units(SymArgs g, SymScratch 
         for (int i = threadIdx.x; i < n; i += kHB) {  // same thread <-> key mapping as the histogram
             const int key = s_in[i];
             const int r = key >> wshift;
-            s_out[s_offs[r] + atomicAdd(&s_hist[w * RM + r], 1)] = key;
+            s_out[s_offs[r] + atomicAdd(&s_hist[w * R + r], 1)] = key;
         }
         __syncthreads();
         int32_t* dst = sc.heavy_pbuf + sc.heavy_foff[un.item] + un.p0;
@@ -674,6 +686,109 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
                   static_cast<unsigned long long>(acc));
 }
 
+// ---- 5u. run for unit-sorted buckets, software-pipelined across tasks:
+// while task i's products are walked, the descriptor and the unit-table
+// entries of the block's next task are already in flight, so a task costs
+// one global round trip less.  Tasks with more than kRunBlock units stage
+// their slices in rounds (no prefetch).
+template <int kRunBlock>
+__global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, SymScratch sc, int64_t first,
+                                                               int R, int wshift, int32_t slot_words) {
+    extern __shared__ int4 s_dyn_ru[];
+    uint32_t* s_set = reinterpret_cast<uint32_t*>(s_dyn_ru);
+    using Scan = cub::BlockScan<int, kRunBlock>;
+    __shared__ typename Scan::TempStorage s_scan;
+    __shared__ int s_off[kRunBlock + 1];
+    __shared__ int64_t s_b0[kRunBlock];
+    const HeavyTask* tasks = reinterpret_cast<const HeavyTask*>(sc.heavy_tasks);
+    const long long ntask = sc.heavy_meta[3];
+    const int32_t* list = heavy_list(sc, first);
+    const int lane = threadIdx.x & 31;
+    constexpr int32_t kWords = 1 << (kTaskSpanShift - 5);
+    for (int k = threadIdx.x; k < kWords; k += kRunBlock) s_set[k] = 0u;
+    // unit-table entries of task t for this thread's unit (first round only)
+    auto fetch = [&](const HeavyTask& t, int& lo, int& hi) {
+        lo = hi = 0;
+        if (threadIdx.x < t.b - t.a) {
+            const int32_t* tab = sc.heavy_utab + (sc.heavy_unit_off[t.item] + t.a + threadIdx.x) * (R + 1);
+            lo = tab[t.r0];
+            hi = tab[t.r1];
+        }
+    };
+    long long acc = 0;
+    long long ti = blockIdx.x;
+    HeavyTask tn{};
+    int nlo = 0, nhi = 0;
+    if (ti < ntask) {
+        tn = tasks[ti];
+        fetch(tn, nlo, nhi);
+    }
+    for (; ti < ntask; ti += gridDim.x) {
+        const HeavyTask t = tn;
+        int lo = nlo, hi = nhi;
+        const long long tj = ti + gridDim.x;
+        if (tj < ntask) tn = tasks[tj];  // in flight during this task
+        const int32_t col_base = t.r0 << wshift;
+        const int32_t words = (t.r1 - t.r0) << (wshift - 5);
+        const long long pbase = sc.heavy_foff[t.item];
+        int cnt = 0;
+        auto insert = [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll], long long) {
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+                if (valid[u]) {
+                    const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
+                    const uint32_t bit = 1u << (off & 31);
+                    cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
+                }
+        };
+        for (long long u0 = t.a; u0 < t.b; u0 += kRunBlock) {
+            const int n = static_cast<int>(t.b - u0 < kRunBlock ? t.b - u0 : kRunBlock);
+            if (u0 != t.a) {  // later rounds of a task with many units
+                lo = hi = 0;
+                if (threadIdx.x < n) {
+                    const int32_t* tab = sc.heavy_utab + (sc.heavy_unit_off[t.item] + u0 + threadIdx.x) * (R + 1);
+                    lo = tab[t.r0];
+                    hi = tab[t.r1];
+                }
+            }
+            int ex, tot;
+            __syncthreads();  // the previous round / task is done with s_off, s_b0, s_set
+            Scan(s_scan).ExclusiveSum(hi - lo, ex, tot);
+            if (threadIdx.x < n) {
+                s_off[threadIdx.x] = ex;
+                s_b0[threadIdx.x] = pbase + (u0 + threadIdx.x) * kHeavyUnitProducts + lo;
+            }
+            if (threadIdx.x == 0) s_off[n] = tot;
+            __syncthreads();
+            if (u0 + kRunBlock >= t.b && tj < ntask) fetch(tn, nlo, nhi);  // next task's table, in flight
+            chunk_products<kRunBlock / 32>(s_off, s_b0, n, 0, tot, sc.heavy_pbuf, insert);
+        }
+        __syncthreads();  // every insert is done
+        if (t.slot >= 0) {
+            // span shared by several tasks: the bits this task adds first
+            cnt = 0;
+            uint32_t* gbm = sc.pool + int64_t(t.slot) * slot_words;
+            for (int k = threadIdx.x; k < words; k += kRunBlock) {
+                const uint32_t w = s_set[k];
+                if (w) cnt += __popc(w & ~atomicOr(&gbm[k], w));
+            }
+            __syncthreads();  // the merge scan has read the bitmap
+        }
+        cnt = static_cast<int>(warp_sum_ll(cnt));
+        if (lane == 0 && cnt) {
+            if (g.out)
+                atomicAdd(reinterpret_cast<unsigned long long*>(&g.out[list[t.item]]),
+                          static_cast<unsigned long long>(cnt));
+            acc += cnt;
+        }
+        uint4* s4 = reinterpret_cast<uint4*>(s_set);
+        for (int k = threadIdx.x; k < (words >> 2); k += kRunBlock) s4[k] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    if (lane == 0 && acc)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[g.total_slot]),
+                  static_cast<unsigned long long>(acc));
+}
+
 // ======================================================= interval path
 // B rows sorted (non-decreasing, the CsrMatrix invariant): the part of B row
 // k inside a column interval is one contiguous run, so the columns are cut
@@ -705,22 +820,6 @@ constexpr int kIvItems = 4;                     // staged entries per thread
 constexpr int kIvStage = kIvBlock * kIvItems;   // entries per staging round
 constexpr int kIvSmem = (1 << kIvShift) / 8;    // the bitmap
 
-struct MappedUnit {
-    int64_t item;
-    long long p0, p1;
-    int64_t e0;
-};
-
-__device__ __forceinline__ MappedUnit mapped_unit(const SymScratch& sc, long long u) {
-    MappedUnit m;
-    m.item = sc.heavy_unit_item[u];
-    m.e0 = sc.heavy_unit_e0[u];
-    const long long f = sc.heavy_foff[m.item + 1] - sc.heavy_foff[m.item];
-    m.p0 = (u - sc.heavy_unit_off[m.item]) * kHeavyUnitProducts;
-    m.p1 = m.p0 + kHeavyUnitProducts < f ? m.p0 + kHeavyUnitProducts : f;
-    return m;
-}
-
 __device__ __forceinline__ void set_bounds(int32_t* bnd, int64_t L, int64_t e, int from, int to, int32_t v) {
     for (int p = from; p <= to; ++p) bnd[static_cast<int64_t>(p - 1) * L + e] = v;
 }
@@ -732,7 +831,7 @@ __global__ void __launch_bounds__(kHB) k_heavy_bounds(SymArgs g, SymScratch sc) 
     const long long units = sc.heavy_meta[0];
     // one warp per unit
     for (long long u = (blockIdx.x * int64_t(kHW) + w); u < units; u += int64_t(gridDim.x) * kHW) {
-        const MappedUnit un = mapped_unit(sc, u);
+        const Unit un = find_unit(sc, 0, u);
         const int64_t i = un.item;
         const int64_t L = sc.heavy_eoff[i + 1] - sc.heavy_eoff[i] - 1;
         const int64_t* ep = sc.heavy_epre + sc.heavy_eoff[i];
@@ -969,7 +1068,7 @@ __global__ void k_heavy_clean(SymScratch sc, int64_t slot_words) {
         sc.pool[i] = 0u;
 }
 
-int sort_smem() { return int(2 * kHeavyUnitProducts * 4 + (kHW + 1) * kPrivRanges * 4 + 4); }
+int sort_smem(int R) { return int(2 * kHeavyUnitProducts * 4 + ((kHW + 1) * R + 1) * 4); }
 
 int place_smem(bool priv) {
     const int nw = priv ? kHW : 1, rm = priv ? kPrivRanges : kMaxRanges;
@@ -1025,12 +1124,12 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
                              (1 << kSpanShift) / 8);
         cudaFuncSetAttribute(k_heavy_run<512, kRunBuckets>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (1 << kTaskSpanShift) / 8);
-        cudaFuncSetAttribute(k_heavy_run<512, kRunUnits>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_heavy_run_units<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (1 << kTaskSpanShift) / 8);
         cudaFuncSetAttribute(k_heavy_place<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              place_smem(false));
         cudaFuncSetAttribute(k_heavy_sort_units, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             sort_smem());
+                             sort_smem(kPrivRanges));
         cudaFuncSetAttribute(k_heavy_intervals, cudaFuncAttributeMaxDynamicSharedMemorySize, kIvSmem);
         attr_done |= 1u << (dev & 31);
     }
@@ -1050,9 +1149,9 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
     if (R > 1) {
         cudaMemsetAsync(s.heavy_rc, 0, sizeof(long long) * count * R, stream);
         if (geo.unit_sorted) {
-            k_heavy_sort_units<<<sms * 4, kHB, sort_smem(), stream>>>(args, s, first, count, R, geo.wshift);
+            k_heavy_sort_units<<<sms * 6, kHB, sort_smem(R), stream>>>(args, s, first, count, R, geo.wshift);
             k_heavy_plan_units<<<items, kPrivRanges, 0, stream>>>(s, count, R, s.heavy_task_cap);
-            k_heavy_run<512, kRunUnits><<<sms * 3, 512, (1 << kTaskSpanShift) / 8, stream>>>(
+            k_heavy_run_units<512><<<sms * 3, 512, (1 << kTaskSpanShift) / 8, stream>>>(
                 args, s, first, R, geo.wshift, geo.wwords);
         } else {
             k_heavy_count<false><<<sms * 8, kHB, 0, stream>>>(args, s, first, count, R, geo.wshift);
