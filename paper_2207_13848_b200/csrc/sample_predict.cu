@@ -55,14 +55,27 @@ k_predict(const int64_t* __restrict__ flop, int64_t m, const long long* __restri
                           (CEIL ? reinterpret_cast<uintptr_t>(ceil_out) : 0) |
                           (REAL ? reinterpret_cast<uintptr_t>(real_out) : 0)) & 15) == 0;
     if (vec_ok) {
+        // kU pairs per thread per step, their loads issued back to back
+        constexpr int kU = 4;
         const longlong2* f2 = reinterpret_cast<const longlong2*>(flop);
-        for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < pairs; i += stride) {
-            const longlong2 f = ld_stream_ll2(&f2[i]);
-            double q0, q1;
-            const long long c0 = ceil_view(f.x, cr, &q0);
-            const long long c1 = ceil_view(f.y, cr, &q1);
-            if (CEIL) st_stream_ll2(reinterpret_cast<longlong2*>(ceil_out) + i, make_longlong2(c0, c1));
-            if (REAL) st_stream_d2(reinterpret_cast<double2*>(real_out) + i, make_double2(q0, q1));
+        for (int64_t i0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i0 < pairs; i0 += kU * stride) {
+            longlong2 f[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int64_t i = i0 + u * stride;
+                f[u] = i < pairs ? ld_stream_ll2(&f2[i]) : make_longlong2(0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int64_t i = i0 + u * stride;
+                if (i < pairs) {
+                    double q0, q1;
+                    const long long c0 = ceil_view(f[u].x, cr, &q0);
+                    const long long c1 = ceil_view(f[u].y, cr, &q1);
+                    if (CEIL) st_stream_ll2(reinterpret_cast<longlong2*>(ceil_out) + i, make_longlong2(c0, c1));
+                    if (REAL) st_stream_d2(reinterpret_cast<double2*>(real_out) + i, make_double2(q0, q1));
+                }
+            }
         }
         if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
             double q;
