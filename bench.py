@@ -294,6 +294,7 @@ def run_ours(args, rank, world, local):
     fbytes = flop_pass_bytes(m_local, nnz_local, (b.rows if b is not a else a.rows))
     achieved = fbytes / (phase["flop"] * 1e-3) / 1e9 if phase["flop"] > 0 else 0.0
     traffic, _ = load_traffic()
+    pbytes = 16 * m_local
 
     # end to end through the host-buffer API: H2D of the CSR + D2H of the
     # per-row prediction, every step
@@ -373,12 +374,22 @@ def run_ours(args, rank, world, local):
                          "algorithmic_bytes": fbytes, "avg_ms": phase["flop"],
                          "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json)",
                          # the FLOP pass gathers one B-row length per A nonzero; random
-                         # 2-4 B gathers are capped by the L1 sector rate (measured
-                         # 287 G/s chip-wide, profiles/r01_microbench.md), not by HBM
+                         # 2-4 B gathers are capped by the L2->SM request rate (measured
+                         # 287 G/s chip-wide for LDG, TMA and both together,
+                         # profiles/r01_microbench.md), not by HBM
                          "gathers_per_s": nnz_local / (phase["flop"] * 1e-3) if phase["flop"] else 0.0,
                          "gather_peak_per_s": 287.6e9,
                          "gather_frac": (nnz_local / (phase["flop"] * 1e-3) / 287.6e9)
                          if phase["flop"] else 0.0},
+            # the other HBM-streaming kernel the north star names: the predict
+            # pass reads flop and writes the ceil view, 16 B per local row
+            "roofline_predict": {"bound": "hbm", "kernel": "k_predict (ceil view)",
+                                 "achieved": pbytes / (phase["predict"] * 1e-3) / 1e9
+                                 if phase["predict"] else 0.0,
+                                 "peak": peak, "unit": "GB/s",
+                                 "frac": (pbytes / (phase["predict"] * 1e-3) / 1e9 / peak)
+                                 if phase["predict"] else 0.0,
+                                 "algorithmic_bytes": pbytes, "avg_ms": phase["predict"]},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "phases_ms": phase,
             "report": {"F": rep.total_flop, "f_star": rep.stats.sampled_flop,

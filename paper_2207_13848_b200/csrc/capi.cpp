@@ -143,6 +143,7 @@ struct spnnz_gpu_ctx {
     bool b_sorted = false;     // ... and B's rows checked non-decreasing at load
     int32_t a_rows = 0, a_cols = 0, b_rows = 0, b_cols = 0;
     int32_t row_lo = 0, row_hi = 0;
+    int64_t b_nnz = 0;
     DBuf<int64_t> b_rpt;
     DBuf<int32_t> b_col;
     DBuf<int64_t> a_rpt;  // shard rpt (only when A != B)
@@ -175,6 +176,7 @@ struct spnnz_gpu_ctx {
     int64_t pool_slots = 0, pool_words = 0;
     DBuf<long long> heavy_meta;
     DBuf<long long> sorted_cnt;
+    DBuf<int64_t> item_flop;  // FLOP of this rank's sampled rows (balanced multi-GPU pass)
     DBuf<int32_t> samples;
     DBuf<int32_t> rows_in;
     DBuf<int64_t> out64;
@@ -314,16 +316,18 @@ int heavy_buffers(spnnz_gpu_ctx* c, int64_t count, int64_t ents, int64_t product
 // Symbolic pass over items (sampled rows or all local rows).  Adds the
 // total into totals[slot] (device); per-item results to out (device, nullable).
 int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64_t* d_out,
-                 int slot, bool sampled_flop, int64_t* launches) {
+                 int slot, bool sampled_flop, int64_t* launches, const int64_t* item_flop = nullptr,
+                 const DevCsr* a_view = nullptr) {
     SymScratch s;
     RC(sym_scratch(c, n_items, &s));
     SymArgs g;
-    g.a = c->a;
+    g.a = a_view ? *a_view : c->a;
     g.brpt = c->b_rpt.p;
     g.bcol = c->b_col.p;
     g.bcols = c->b_cols;
-    g.row_lo = c->row_lo;
+    g.row_lo = a_view ? 0 : c->row_lo;
     g.flop = c->flop.p;
+    g.item_flop = item_flop;
     g.rows = d_rows;
     g.n_items = n_items;
     g.out = d_out;
@@ -481,7 +485,28 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
         ++launches;
     }
     ev_record(c, 2);
-    RC(run_symbolic(c, d_rows, n, nullptr, kZStar, true, &launches));
+    if (c->world > 1 && c->same_b) {
+        // Multi-GPU, C = A*A: every rank holds all of A (it is the replicated
+        // B), so the sampled rows are split by position in the sample list --
+        // a random order, hence an even share of the heavy rows per rank --
+        // instead of by row ownership (R-MAT's hub rows all sit in rank 0's
+        // shard).  Each rank derives its rows' FLOP directly.
+        const int64_t lo = n * c->rank / c->world, hi = n * (c->rank + 1) / c->world;
+        DevCsr full;
+        full.rows = c->b_rows;
+        full.cols = c->b_cols;
+        full.rpt = c->b_rpt.p;
+        full.col = c->b_col.p;
+        full.base = 0;
+        full.nnz = c->b_nnz;
+        RC(c->item_flop.ensure(std::max<int64_t>(hi - lo, 1)));
+        CU(launch_item_flop(full, c->b_rpt.p, 0, d_rows + lo, hi - lo, c->item_flop.p, c->num_sms,
+                            c->stream));
+        ++launches;
+        RC(run_symbolic(c, d_rows + lo, hi - lo, nullptr, kZStar, true, &launches, c->item_flop.p, &full));
+    } else {
+        RC(run_symbolic(c, d_rows, n, nullptr, kZStar, true, &launches));
+    }
     ev_record(c, 3);
     RC(allreduce_totals(c));
     ev_record(c, 4);
@@ -590,6 +615,7 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     c->heavy_cur.release();
     c->heavy_pbuf.release();
     c->heavy_utab.release();
+    c->item_flop.release();
     c->heavy_boff.release();
     for (auto* b : {&c->heavy_bnd, &c->heavy_unit_item, &c->heavy_unit_e0}) b->release();
     c->heavy_tasks.release();
@@ -682,6 +708,7 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
     } else {
         b_nnz = bv->rpt[bv->rows];
     }
+    c->b_nnz = b_nnz;
     RC(c->b_rpt.ensure(int64_t(bv->rows) + 1));
     RC(c->b_col.ensure(std::max<int64_t>(b_nnz, 1)));
     CU(cudaMemcpyAsync(c->b_rpt.p, bv->rpt, 8 * (size_t(bv->rows) + 1), kind, c->stream));

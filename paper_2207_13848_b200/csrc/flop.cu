@@ -288,6 +288,32 @@ __global__ void k_check_rows(const int32_t* __restrict__ rows, int64_t n, int32_
     if (i < n && (rows[i] < 0 || rows[i] >= num_rows)) atomicAdd(bad, 1);
 }
 
+// One warp per listed row: flop = sum of B row lengths over its entries
+// (compute_flop's sum, flop.hpp:41-50, for that row).
+__global__ void __launch_bounds__(256) k_item_flop(DevCsr a, const int64_t* __restrict__ brpt,
+                                                  int32_t row_lo, const int32_t* __restrict__ rows,
+                                                  int64_t n, int64_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t s = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; s < n;
+         s += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+        const int32_t r = rows[s] - row_lo;
+        long long f = 0;
+        if (r >= 0 && r < a.rows) {
+            const int64_t e1 = a.rpt[r + 1];
+            for (int64_t e = a.rpt[r] + lane; e < e1; e += 32 * 4) {
+                int c[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) c[k] = e + 32 * k < e1 ? __ldg(&a.col[e + 32 * k]) : -1;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (c[k] >= 0) f += __ldg(&brpt[c[k] + 1]) - __ldg(&brpt[c[k]]);
+            }
+        }
+        f = warp_sum_ll(f);
+        if (lane == 0) out[s] = f;
+    }
+}
+
 // Row-sortedness of B (the CsrMatrix invariant, csr.hpp:16-18), checked once
 // at load: every descent col[j] < col[j-1] must sit at the start of a
 // non-empty row.  cnt[0] += descents over all j, cnt[1] += descents at row
@@ -314,6 +340,16 @@ __global__ void k_start_descents(const int64_t* __restrict__ rpt, const int32_t*
 }
 
 }  // namespace
+
+cudaError_t launch_item_flop(const DevCsr& a, const int64_t* brpt, int32_t row_lo,
+                             const int32_t* rows, int64_t n, int64_t* out, int num_sms,
+                             cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    int64_t grid = (n + 7) / 8;
+    if (grid > int64_t(num_sms) * 8) grid = int64_t(num_sms) * 8;
+    k_item_flop<<<static_cast<unsigned>(grid), 256, 0, stream>>>(a, brpt, row_lo, rows, n, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_check_sorted(const int64_t* rpt, const int32_t* col, int32_t rows, int64_t nnz,
                                 unsigned long long* cnt, int num_sms, cudaStream_t stream) {

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kPrepBlock) k_heavy_prep(SymArgs g, SymScratch
             const int32_t s = list[i];
             const int32_t rid = g.rows ? g.rows[s] : g.row_lo + s;
             const ItemRow it = item_row(g, s);
-            const long long f = g.flop[rid - g.row_lo];
+            const long long f = g.item_flop ? g.item_flop[s] : g.flop[rid - g.row_lo];
             const long long L = it.a1 - it.a0;
             x[0] = (f + kHeavyUnitProducts - 1) / kHeavyUnitProducts;  // units
             x[1] = L + 1;                                               // entries (+ end)
@@ -1055,7 +1055,7 @@ __global__ void k_heavy_flops(SymArgs g, SymScratch sc, int64_t count, int64_t* 
     const int32_t rid = g.rows ? g.rows[s] : g.row_lo + s;
     const int32_t r = rid - g.row_lo;
     const int64_t L = g.a.rpt[r + 1] - g.a.rpt[r];
-    out[i] = g.flop[r];
+    out[i] = g.item_flop ? g.item_flop[s] : g.flop[r];
     out[count + i] = L;
     out[2 * count + i] = (interval_geometry(g.bcols).count - 1) * L;
 }

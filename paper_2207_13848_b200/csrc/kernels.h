@@ -147,6 +147,7 @@ struct SymArgs {
     int32_t bcols = 0;          // N (columns of B)
     int32_t row_lo = 0;         // global id of local row 0
     const int64_t* flop = nullptr;  // local profile
+    const int64_t* item_flop = nullptr;  // per item FLOP (balanced multi-GPU pass), else flop[row]
     const int32_t* rows = nullptr;  // global row ids, or nullptr = all local rows
     int64_t n_items = 0;
     int64_t* out = nullptr;         // per item NNZ (nullable)
@@ -186,6 +187,11 @@ cudaError_t launch_sampled_flop(const int64_t* flop, int32_t row_lo, int32_t loc
                                 cudaStream_t stream);
 
 // Validation: counts rows outside [0, num_rows) into *bad.
+// FLOP of each listed row (global ids; 0 outside [row_lo, row_lo + a.rows)),
+// straight from A and B.rpt.
+cudaError_t launch_item_flop(const DevCsr& a, const int64_t* brpt, int32_t row_lo,
+                             const int32_t* rows, int64_t n, int64_t* out, int num_sms,
+                             cudaStream_t stream);
 // B rows non-decreasing? cnt[0] == cnt[1] afterwards (device counters).
 cudaError_t launch_check_sorted(const int64_t* rpt, const int32_t* col, int32_t rows, int64_t nnz,
                                 unsigned long long* cnt, int num_sms, cudaStream_t stream);

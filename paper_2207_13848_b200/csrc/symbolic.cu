@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_bin(SymArgs g, SymScratch sc) {
             const int32_t rid = g.rows ? g.rows[s] : g.row_lo + static_cast<int32_t>(s);
             const int32_t r = rid - g.row_lo;
             if (r >= 0 && r < g.a.rows) {
-                const int64_t f = g.flop[r];
+                const int64_t f = g.item_flop ? g.item_flop[s] : g.flop[r];
                 fsum += f;
                 bin = f == 0 ? 0 : f <= kBin1Max ? 1 : f <= kBin2Max ? 2 : f <= kBin3Max ? 3
                                  : f <= kBin4Max ? 4 : f <= kBin5Max ? 5 : kHeavyBin;

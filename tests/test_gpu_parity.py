@@ -500,6 +500,28 @@ def test_detached_shards_combine_to_single_gpu(oracle):
             q.close()
 
 
+def test_detached_pipeline_shards_sum_to_single_gpu():
+    """run_prediction on detached shards (world > 1, no NCCL): for C = A*A the
+    sampled rows are split by list position (balanced heavy rows), and the
+    per-rank F, f*, z* still add up to the single-GPU totals."""
+    a, b = gen.make_config(2)
+    single = Predictor(0)
+    single.load(a, b)
+    ref = single.run_prediction(2, SamplePolicy(0.003, UNCAPPED))
+    single.close()
+    for world in (2, 4):
+        F = fs = zs = 0
+        for r in range(world):
+            q = Predictor(0, r, world)
+            q.load(a, b)
+            rep = q.run_prediction(2, SamplePolicy(0.003, UNCAPPED))
+            F += rep.total_flop
+            fs += rep.stats.sampled_flop
+            zs += rep.stats.sampled_nnz
+            q.close()
+        assert (F, fs, zs) == (ref.total_flop, ref.stats.sampled_flop, ref.stats.sampled_nnz)
+
+
 def test_repeat_runs_deterministic(P):
     a, b = gen.make_config(4)
     P.load(a, b)
