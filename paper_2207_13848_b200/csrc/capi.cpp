@@ -235,7 +235,7 @@ int sym_scratch(spnnz_gpu_ctx* c, int64_t items, SymScratch* s) {
         c->list_cap = items;
     }
     RC(c->counts.ensure(16));
-    RC(c->heavy_meta.ensure(8));
+    RC(c->heavy_meta.ensure(kHeavyMeta));
     s->lists = c->lists.p;
     s->capacity = c->list_cap;
     s->counts = c->counts.p;
@@ -335,7 +335,7 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     g.total_slot = slot;
     g.sampled_flop = sampled_flop;
     CU(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * 16, c->stream));
-    CU(cudaMemsetAsync(c->heavy_meta.p, 0, sizeof(long long) * 8, c->stream));
+    CU(cudaMemsetAsync(c->heavy_meta.p, 0, sizeof(long long) * kHeavyMeta, c->stream));
     if (n_items == 0) return SPNNZ_OK;
     CU(launch_sym_bin(g, s, c->stream));
     // The host learns the heavy rows' number (bin counts) while the tier
@@ -344,7 +344,7 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     CU(cudaEventRecord(c->fork, c->stream));
     CU(cudaMemcpyAsync(c->h_counts, c->counts.p, sizeof(int32_t) * 16, cudaMemcpyDeviceToHost,
                        c->stream));
-    CU(cudaMemcpyAsync(c->h_meta, c->heavy_meta.p, sizeof(long long) * 8, cudaMemcpyDeviceToHost,
+    CU(cudaMemcpyAsync(c->h_meta, c->heavy_meta.p, sizeof(long long) * kHeavyMeta, cudaMemcpyDeviceToHost,
                        c->stream));
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaStreamWaitEvent(c->side[i], c->fork, 0));
     CU(launch_sym_tiers(g, s, c->num_sms, c->side));
@@ -562,7 +562,7 @@ int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz
     e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_totals, sizeof(long long) * kTotals);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_counts, sizeof(int32_t) * 16);
-    if (e == cudaSuccess) e = cudaMallocHost(&c->h_meta, sizeof(long long) * 8);
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_meta, sizeof(long long) * kHeavyMeta);
     for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     for (int i = 0; i < spnnz_gpu_ctx::kSide && e == cudaSuccess; ++i)
         e = cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking);

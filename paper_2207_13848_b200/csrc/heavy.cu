@@ -44,6 +44,7 @@ constexpr int kTaskSpanShift = 19;        // R > 1: task spans of <= 2^19 column
 constexpr int kPrivRanges = 256;          // per-warp histograms up to this R
 constexpr int kMaxRanges = 4096;          // B.cols < 2^31 with W = 2^19
 constexpr int64_t kTaskProducts = 131072;
+constexpr int64_t kSmallTaskProducts = 2048;  // ranges this small go to k_heavy_run_small
 
 struct HeavyTask {
     int32_t item;    // index in the batch
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(kPrepBlock) k_heavy_prep(SymArgs g, SymScratch
         sc.heavy_meta[3] = 0;  // tasks
         sc.heavy_meta[4] = 0;  // merge slots
         sc.heavy_meta[7] = 0;  // interval-task cursor
+        sc.heavy_meta[8] = 0;  // small tasks
     }
 }
 
@@ -465,15 +467,23 @@ __global__ void __launch_bounds__(kPrivRanges) k_heavy_plan_units(SymScratch sc,
     const int r = threadIdx.x;
     const long long nu = sc.heavy_unit_off[i + 1] - sc.heavy_unit_off[i];
     const long long cnt = r < R ? sc.heavy_rc[i * R + r] : 0;
+    const bool small = cnt > 0 && cnt <= kSmallTaskProducts;
     long long p = (cnt + kTaskProducts - 1) / kTaskProducts;
-    const int parts = static_cast<int>(p < nu ? p : nu);
+    const int parts = small ? 0 : static_cast<int>(p < nu ? p : nu);
     int excl, total;
     Scan(tmp).ExclusiveSum(parts, excl, total);
     if (threadIdx.x == 0)
         s_base = static_cast<long long>(atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[3]),
                                                   static_cast<unsigned long long>(total)));
     __syncthreads();
-    if (s_base + total > task_cap) __trap();  // host sizes task_cap to heavy_task_bound()
+    if (small) {  // small ranges: a list of their own, filled from the end of the array
+        const long long k = static_cast<long long>(
+            atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[8]), 1ULL));
+        reinterpret_cast<HeavyTask*>(sc.heavy_tasks)[task_cap - 1 - k] =
+            HeavyTask{static_cast<int32_t>(i), -1, r, r + 1, 0, nu};
+    }
+    __syncthreads();
+    if (s_base + total + sc.heavy_meta[8] > task_cap) __trap();  // host sizes task_cap to heavy_task_bound()
     if (parts > 0) {
         const int32_t slot = parts > 1 ? static_cast<int32_t>(atomicAdd(
                                              reinterpret_cast<unsigned long long*>(&sc.heavy_meta[4]), 1ULL))
@@ -783,6 +793,79 @@ __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, Sym
         }
         uint4* s4 = reinterpret_cast<uint4*>(s_set);
         for (int k = threadIdx.x; k < (words >> 2); k += kRunBlock) s4[k] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    if (lane == 0 && acc)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[g.total_slot]),
+                  static_cast<unsigned long long>(acc));
+}
+
+// ---- 5s. small unit-sorted ranges (<= kSmallTaskProducts products): a
+// 512-thread block is four independent 128-thread groups, each with a
+// 4096-slot shared hash and its own named barrier, so an SM keeps twelve
+// small tasks in flight instead of three bitmap tasks.
+constexpr int kSG = 128, kSGroups = 4, kSSlots = 4096;
+
+__device__ __forceinline__ void group_sync(int grp) {
+    asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(kSG) : "memory");
+}
+
+__global__ void __launch_bounds__(kSG * kSGroups, 3) k_heavy_run_small(SymArgs g, SymScratch sc, int64_t first,
+                                                                       int R) {
+    extern __shared__ int4 s_dyn_rs[];
+    const int grp = threadIdx.x / kSG, gt = threadIdx.x % kSG, gw = gt >> 5, lane = threadIdx.x & 31;
+    int* table = reinterpret_cast<int*>(s_dyn_rs) + grp * kSSlots;
+    __shared__ int s_off[kSGroups][kSG + 1];
+    __shared__ int64_t s_b0[kSGroups][kSG];
+    __shared__ int s_wt[kSGroups][kSG / 32];
+    const HeavyTask* tasks = reinterpret_cast<const HeavyTask*>(sc.heavy_tasks) + sc.heavy_task_cap - 1;
+    const long long ntask = sc.heavy_meta[8];
+    const int32_t* list = heavy_list(sc, first);
+    long long acc = 0;
+    for (long long ti = blockIdx.x * int64_t(kSGroups) + grp; ti < ntask; ti += int64_t(gridDim.x) * kSGroups) {
+        const HeavyTask t = *(tasks - ti);
+        for (int k = gt; k < kSSlots; k += kSG) table[k] = kEmpty;
+        const long long ubase = sc.heavy_unit_off[t.item];
+        const long long pbase = sc.heavy_foff[t.item];
+        int cnt = 0;
+        for (long long u0 = t.a; u0 < t.b; u0 += kSG) {
+            const int n = static_cast<int>(t.b - u0 < kSG ? t.b - u0 : kSG);
+            int len = 0;
+            int64_t start = 0;
+            if (gt < n) {
+                const long long u = u0 + gt;
+                const int32_t* tab = sc.heavy_utab + (ubase + u) * (R + 1);
+                const int lo = tab[t.r0];
+                len = tab[t.r1] - lo;
+                start = pbase + u * kHeavyUnitProducts + lo;
+            }
+            const int incl = warp_incl_scan(len);
+            group_sync(grp);  // the previous round's walk is done with s_off / s_b0
+            if (lane == 31) s_wt[grp][gw] = incl;
+            group_sync(grp);
+            int before = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < kSG / 32; ++w) {
+                const int v = s_wt[grp][w];
+                before += w < gw ? v : 0;
+                tot += v;
+            }
+            if (gt < n) {
+                s_off[grp][gt] = before + incl - len;
+                s_b0[grp][gt] = start;
+            }
+            if (gt == 0) s_off[grp][n] = tot;
+            group_sync(grp);  // also orders the table clear before the inserts
+            chunk_products<kSG / 32>(s_off[grp], s_b0[grp], n, 0, tot, sc.heavy_pbuf,
+                                     HashSink{table, kSSlots, &cnt});
+        }
+        cnt = static_cast<int>(warp_sum_ll(cnt));
+        if (lane == 0 && cnt) {
+            if (g.out)
+                atomicAdd(reinterpret_cast<unsigned long long*>(&g.out[list[t.item]]),
+                          static_cast<unsigned long long>(cnt));
+            acc += cnt;
+        }
+        group_sync(grp);  // the table is free again
     }
     if (lane == 0 && acc)
         atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[g.total_slot]),
@@ -1126,6 +1209,8 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
                              (1 << kTaskSpanShift) / 8);
         cudaFuncSetAttribute(k_heavy_run_units<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (1 << kTaskSpanShift) / 8);
+        cudaFuncSetAttribute(k_heavy_run_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSGroups * kSSlots * 4);
         cudaFuncSetAttribute(k_heavy_place<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              place_smem(false));
         cudaFuncSetAttribute(k_heavy_sort_units, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1153,6 +1238,7 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
             k_heavy_plan_units<<<items, kPrivRanges, 0, stream>>>(s, count, R, s.heavy_task_cap);
             k_heavy_run_units<512><<<sms * 3, 512, (1 << kTaskSpanShift) / 8, stream>>>(
                 args, s, first, R, geo.wshift, geo.wwords);
+            k_heavy_run_small<<<sms * 3, kSG * kSGroups, kSGroups * kSSlots * 4, stream>>>(args, s, first, R);
         } else {
             k_heavy_count<false><<<sms * 8, kHB, 0, stream>>>(args, s, first, count, R, geo.wshift);
             k_heavy_offsets<<<items, 256, 0, stream>>>(s, count, R);

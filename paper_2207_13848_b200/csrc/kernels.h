@@ -99,6 +99,8 @@ SPNNZ_HD inline Intervals interval_geometry(int32_t bcols) {
     return iv;
 }
 
+constexpr int kHeavyMeta = 16;
+
 struct SymScratch {
     int32_t* lists = nullptr;        // kNumBins * capacity item ids
     int64_t capacity = 0;
@@ -116,10 +118,11 @@ struct SymScratch {
     void* heavy_tasks = nullptr;         // HeavyTask[heavy_task_cap]
     int64_t heavy_task_cap = 0;
     uint32_t* pool = nullptr;            // merge bitmaps (W bits each), zero between calls
-    long long* heavy_meta = nullptr;     // [0] units [1] sum(len+1) [2] sum(flop) of heavy
-                                         // rows [3] tasks [4] merge slots used
-                                         // [5] sum((P-1) len) [6] sum(P) of heavy rows (interval path)
-                                         // [7] interval-task cursor
+    long long* heavy_meta = nullptr;     // kHeavyMeta slots: [0] units [1] sum(len+1)
+                                         // [2] sum(flop) of heavy rows [3] tasks [4] merge
+                                         // slots used [5] sum((P-1) len) [6] sum(P) of heavy
+                                         // rows (interval path) [7] interval-task cursor
+                                         // [8] small tasks (stored from the list's end)
     // interval path (sorted B)
     int64_t* heavy_boff = nullptr;       // capacity + 1: boundary-table offset per item
     int32_t* heavy_bnd = nullptr;        // per item (P-1) x len: interval starts inside each B row
