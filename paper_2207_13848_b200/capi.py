@@ -12,7 +12,9 @@ import os
 from ctypes import POINTER, c_double, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libspnnz_gpu.so")
+# SPNNZ_GPU_LIB: an alternative build of the same library (A/B experiments,
+# tools/variants.sh); the in-tree build otherwise.
+LIB_PATH = os.environ.get("SPNNZ_GPU_LIB") or os.path.join(_HERE, "_lib", "libspnnz_gpu.so")
 GEN_PATH = os.path.join(_HERE, "_lib", "libspnnz_gen.so")
 
 OK, EINVAL, ECUDA, ENCCL, ENOMEM, ESTATE = 0, 1, 2, 3, 4, 5

@@ -71,6 +71,46 @@ __global__ void k_flop_partition(const int64_t* __restrict__ arpt, int32_t m, in
     tile_row[t] = static_cast<int32_t>(lo);
 }
 
+#ifndef SPNNZ_FLOP_GATHER
+#define SPNNZ_FLOP_GATHER 0
+#endif
+// The degree gather (A/B-tested variants: 0 evict_last hint, 1 plain __ldg,
+// 2 evict_last without L1 allocation, 3 plain coherent load).
+__device__ __forceinline__ uint16_t gather_deg(const uint16_t* p, uint64_t last) {
+#if SPNNZ_FLOP_GATHER == 1
+    return __ldg(p);
+#elif SPNNZ_FLOP_GATHER == 2
+    unsigned short v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(last));
+    return v;
+#elif SPNNZ_FLOP_GATHER == 3
+    return *p;
+#else
+    return ld_keep_u16(p, last);
+#endif
+}
+
+#ifndef SPNNZ_FLOP_COLLOAD
+#define SPNNZ_FLOP_COLLOAD 1
+#endif
+// A.col loads: a thread's four 16-byte loads cover 64 contiguous bytes, 64 B
+// apart across lanes, so two loads share each 32-byte sector.  Allocating in
+// L1 (variant 1, the default; L2 still evict_first) lets the second load of a
+// sector merge with the first: -2.4 % FLOP-pass time at config 5 versus the
+// no-allocate load (0), as the pass is bound by L2 requests.
+__device__ __forceinline__ int4 load_cols(const int4* p, uint64_t first) {
+#if SPNNZ_FLOP_COLLOAD == 1
+    int4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(first));
+    return v;
+#elif SPNNZ_FLOP_COLLOAD == 2
+    return __ldg(p);
+#else
+    return ld_stream_v4(p, first);
+#endif
+}
+
 // Segmented-sum carry across threads: (has a row start, carried value, row).
 struct Carry {
     int flag;
@@ -125,7 +165,7 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
             const int4* src = reinterpret_cast<const int4*>(acol + ts + i0);
 #pragma unroll
             for (int k = 0; k < V / 4; ++k) {
-                const int4 x = ld_stream_v4(src + k, first);
+                const int4 x = load_cols(src + k, first);
                 c[4 * k] = x.x;
                 c[4 * k + 1] = x.y;
                 c[4 * k + 2] = x.z;
@@ -136,7 +176,7 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
             for (int k = 0; k < V; ++k) c[k] = i0 + k < n ? ld_stream_i32(acol + ts + i0 + k, first) : -1;
         }
 #pragma unroll
-        for (int k = 0; k < V; ++k) d[k] = c[k] >= 0 ? static_cast<int32_t>(ld_keep_u16(bdeg + c[k], last)) : 0;
+        for (int k = 0; k < V; ++k) d[k] = c[k] >= 0 ? static_cast<int32_t>(gather_deg(bdeg + c[k], last)) : 0;
 #pragma unroll
         for (int k = 0; k < V; ++k)
             if (d[k] == 0xFFFF) d[k] = static_cast<int32_t>(__ldg(&brpt[c[k] + 1]) - __ldg(&brpt[c[k]]));
