@@ -65,32 +65,81 @@ def workload_name(cfg, info, cap):
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock and throttle reasons sampled DURING the timed region: an NVML
+    poller thread (~1 ms period) whose samples are kept only between mark()
+    calls bracketing the region; nvidia-smi -lms as the fallback."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index = index
+    def __init__(self, index: int, pci_bus_id: str = ""):
+        self.index, self.pci = index, pci_bus_id
+        self.samples = []  # (t, sm_mhz, max_mhz, reason bits)
+        self.window = [None, None]
+        self.stop = threading.Event()
+        self.nvml = None
         self.proc = None
         self.lines = []
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            if self.pci:
+                try:
+                    h = pynvml.nvmlDeviceGetHandleByPciBusId(self.pci)
+                except Exception:
+                    h = None
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml, self.h = pynvml, h
+            self.reasons_fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.maxclk = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.nvml = None
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._read, daemon=True)
+                self.t.start()
+            except Exception:
+                self.proc = None
         return self
+
+    def mark(self, i):
+        self.window[i] = time.perf_counter()
+
+    def _poll(self):
+        n = self.nvml
+        while not self.stop.is_set():
+            try:
+                self.samples.append((time.perf_counter(),
+                                     float(n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM)),
+                                     self.maxclk, int(self.reasons_fn(self.h))))
+            except Exception:
+                pass
+            time.sleep(0.001)
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml:
+            self.t.join(1)
+            try:
+                self.nvml.nvmlShutdown()
+            except Exception:
+                pass
         if self.proc:
             time.sleep(0.25)
             self.proc.terminate()
@@ -100,6 +149,20 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        t0, t1 = self.window
+        if self.nvml is not None:
+            inside = [s for s in self.samples if t0 is None or t1 is None or t0 <= s[0] <= t1]
+            if not inside and self.samples:  # region shorter than one poll: nearest samples
+                mid = 0.5 * ((t0 or 0) + (t1 or 0))
+                inside = sorted(self.samples, key=lambda s: abs(s[0] - mid))[:2]
+            if not inside:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": "nvml"}
+            bits = 0
+            for s in inside:
+                bits |= s[3]
+            return {"sm_mhz": float(np.median([s[1] for s in inside])), "sm_max_mhz": inside[0][2],
+                    "reasons": sorted(v for k, v in self.REASONS.items() if bits & k),
+                    "samples": len(inside), "source": "nvml"}
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -117,7 +180,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi"}
 
 
 # ------------------------------------------------------------- CPU side
@@ -265,8 +328,15 @@ def run_ours(args, rank, world, local):
     phase = {"flop": 0.0, "sample": 0.0, "symbolic": 0.0, "allreduce": 0.0, "predict": 0.0}
     launches = 0
     rep = None
-    barrier()
-    with ClockSampler(local) as clk:
+    try:
+        pr = torch.cuda.get_device_properties(local)
+        pci = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+    except Exception:
+        pci = ""
+    with ClockSampler(local, pci) as clk:
+        time.sleep(0.005)  # the poller is running before the region starts
+        barrier()
+        clk.mark(0)
         for i in range(args.steps):
             if flush is not None:
                 flush.zero_()
@@ -279,6 +349,7 @@ def run_ours(args, rank, world, local):
                 phase[k] += t[k]
             launches += n
         barrier()
+        clk.mark(1)
     P.set_profiling(False)
     ms = float(sum(s.elapsed_time(e) for s, e in ev)) / args.steps
     for k in phase:
