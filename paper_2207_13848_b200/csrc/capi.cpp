@@ -177,6 +177,8 @@ struct spnnz_gpu_ctx {
     DBuf<long long> heavy_meta;
     DBuf<long long> sorted_cnt;
     DBuf<int64_t> item_flop;  // FLOP of this rank's sampled rows (balanced multi-GPU pass)
+    DBuf<int32_t> redo;       // fused predict: rows left to an IEEE division
+    DBuf<unsigned long long> nredo;
     DBuf<int32_t> samples;
     DBuf<int32_t> rows_in;
     DBuf<int64_t> out64;
@@ -185,6 +187,8 @@ struct spnnz_gpu_ctx {
 
     // instrumentation
     bool profiling = false;
+    bool fused = false;  // SPNNZ_FUSED_PREDICT=1: the fused single-pass predictor
+    int ev_order = 0;
     cudaEvent_t ev[6] = {};
     double last_ms[5] = {};
     int64_t last_launches = 0;
@@ -397,7 +401,9 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     return SPNNZ_OK;
 }
 
-int flop_pass(spnnz_gpu_ctx* c, int64_t* launches) {
+int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr,
+              const PredOut& pred = PredOut()) {
+    if (!stream) stream = c->stream;
     const DevCsr& a = c->a;
     const int64_t tiles = flop_tiles(a);
     RC(c->flop.ensure(std::max<int64_t>(a.rows, 1)));
@@ -407,21 +413,24 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches) {
     RC(c->tile_max.ensure(tiles + 1));
     RC(c->deg.ensure(std::max<int64_t>(c->b_rows, 1)));
     FlopScratch s{c->tile_x.p, c->tile_carry.p, c->tile_total.p, c->tile_max.p};
-    CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, c->stream));
-    CU(launch_flop_partition(a, s, c->stream));
-    CU(launch_flop(a, c->deg.p, c->b_rpt.p, s, c->flop.p, c->totals.p, c->stream));
+    CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, stream));
+    CU(launch_flop_partition(a, s, stream));
+    CU(launch_flop(a, c->deg.p, c->b_rpt.p, s, c->flop.p, c->totals.p, stream, pred));
     *launches += a.rows ? 4 : 0;
     return SPNNZ_OK;
 }
 
-// Sum-all-reduce of totals[0..3] and max of totals[kMax] across ranks.
-int allreduce_totals(spnnz_gpu_ctx* c) {
+// Sum-all-reduce of totals[first, first + count) (default: F, f*, z*, Z), and
+// with_max the max of totals[kMax], across ranks.
+int allreduce_totals(spnnz_gpu_ctx* c, int first = 0, int count = 4, bool with_max = true) {
     if (c->world == 1 || !c->comm) return SPNNZ_OK;
     Nccl& n = nccl();
     NC(n.GroupStart());
-    NC(n.AllReduce(c->totals.p, c->totals.p, 4, ncclInt64, ncclSum, c->comm, c->stream));
-    NC(n.AllReduce(c->totals.p + kMax, c->totals.p + kMax, 1, ncclInt64, ncclMax, c->comm,
+    NC(n.AllReduce(c->totals.p + first, c->totals.p + first, count, ncclInt64, ncclSum, c->comm,
                    c->stream));
+    if (with_max)
+        NC(n.AllReduce(c->totals.p + kMax, c->totals.p + kMax, 1, ncclInt64, ncclMax, c->comm,
+                       c->stream));
     NC(n.GroupEnd());
     return SPNNZ_OK;
 }
@@ -462,60 +471,138 @@ void ev_record(spnnz_gpu_ctx* c, int i) {
     if (c->profiling) cudaEventRecord(c->ev[i], c->stream);
 }
 
+// last_ms: [0] FLOP pass (fused: + predict) [1] sampler (+ sampled-row FLOP)
+// [2] symbolic [3] all-reduce(s) [4] predict pass (fused: 0)
 void ev_collect(spnnz_gpu_ctx* c) {
     if (!c->profiling) return;
     cudaEventSynchronize(c->ev[5]);
-    for (int i = 0; i < 5; ++i) {
-        float ms = 0;
-        cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]);
-        c->last_ms[i] = ms;
+    float m[5] = {0, 0, 0, 0, 0};
+    for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&m[i], c->ev[i], c->ev[i + 1]);
+    if (c->ev_order == 0) {
+        for (int i = 0; i < 5; ++i) c->last_ms[i] = m[i];
+    } else {
+        c->last_ms[0] = m[3];
+        c->last_ms[1] = m[0];
+        c->last_ms[2] = m[1];
+        c->last_ms[3] = m[2] + m[4];
+        c->last_ms[4] = 0.0;
     }
 }
 
-// Pipeline body shared by run_prediction and run_prediction_with_plan.
+// The sampled rows this rank counts, and their FLOP.  Multi-GPU with C = A*A:
+// every rank holds all of A (it is the replicated B), so the sampled rows are
+// split by position in the sample list -- a random order, hence an even share
+// of the heavy rows per rank -- instead of by row ownership (R-MAT's hub rows
+// all sit in rank 0's shard); their FLOP comes straight from A and B.rpt.
+// Otherwise the whole list, with the resident profile (or, fused, the same
+// direct FLOP restricted to the shard).
+struct SampleShare {
+    const int32_t* rows = nullptr;
+    int64_t n = 0;
+    const int64_t* item_flop = nullptr;
+    DevCsr full;
+    bool use_full = false;
+};
+
+int sample_share(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool need_flop,
+                 SampleShare* sh, int64_t* launches) {
+    sh->rows = d_rows;
+    sh->n = n;
+    if (c->world > 1 && c->same_b) {
+        const int64_t lo = n * c->rank / c->world, hi = n * (c->rank + 1) / c->world;
+        sh->full.rows = c->b_rows;
+        sh->full.cols = c->b_cols;
+        sh->full.rpt = c->b_rpt.p;
+        sh->full.col = c->b_col.p;
+        sh->full.base = 0;
+        sh->full.nnz = c->b_nnz;
+        sh->use_full = true;
+        sh->rows = d_rows + lo;
+        sh->n = hi - lo;
+        need_flop = true;
+    }
+    if (need_flop) {
+        RC(c->item_flop.ensure(std::max<int64_t>(sh->n, 1)));
+        CU(launch_item_flop(sh->use_full ? sh->full : c->a, c->b_rpt.p, sh->use_full ? 0 : c->row_lo,
+                            sh->rows, sh->n, c->item_flop.p, c->num_sms, c->stream));
+        *launches += 2;
+        sh->item_flop = c->item_flop.p;
+    }
+    return SPNNZ_OK;
+}
+
+// Pipeline body shared by run_prediction and run_prediction_with_plan:
+// FLOP pass -> sampler -> sampled symbolic -> one all-reduce -> predict pass.
+// With c->fused (SPNNZ_FUSED_PREDICT=1) the sampled rows' FLOP
+// is derived directly so the symbolic pass and CR come first, and one FLOP
+// pass writes every row's flop together with its prediction (two
+// all-reduces on multi-GPU).  Measured slower on B200 at config 5 (the
+// per-row division and scattered 8-byte stores land in the gather-bound FLOP
+// kernel: 2.12 ms vs 1.85 + 0.07 ms), so it is not the default.
 int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint64_t seed,
              int64_t* d_ceil, double* d_real) {
     int64_t launches = 0;
+    const char* fenv = getenv("SPNNZ_FUSED_PREDICT");
+    c->fused = fenv && atoi(fenv) > 0;
     CU(cudaMemsetAsync(c->totals.p, 0, sizeof(long long) * kTotals, c->stream));
-    ev_record(c, 0);
-    RC(flop_pass(c, &launches));
-    ev_record(c, 1);
-    if (draw) {
-        CU(launch_sample(seed, c->a_rows, n, c->samples.p, c->stream));
-        ++launches;
-    }
-    ev_record(c, 2);
-    if (c->world > 1 && c->same_b) {
-        // Multi-GPU, C = A*A: every rank holds all of A (it is the replicated
-        // B), so the sampled rows are split by position in the sample list --
-        // a random order, hence an even share of the heavy rows per rank --
-        // instead of by row ownership (R-MAT's hub rows all sit in rank 0's
-        // shard).  Each rank derives its rows' FLOP directly.
-        const int64_t lo = n * c->rank / c->world, hi = n * (c->rank + 1) / c->world;
-        DevCsr full;
-        full.rows = c->b_rows;
-        full.cols = c->b_cols;
-        full.rpt = c->b_rpt.p;
-        full.col = c->b_col.p;
-        full.base = 0;
-        full.nnz = c->b_nnz;
-        RC(c->item_flop.ensure(std::max<int64_t>(hi - lo, 1)));
-        CU(launch_item_flop(full, c->b_rpt.p, 0, d_rows + lo, hi - lo, c->item_flop.p, c->num_sms,
-                            c->stream));
-        ++launches;
-        RC(run_symbolic(c, d_rows + lo, hi - lo, nullptr, kZStar, true, &launches, c->item_flop.p, &full));
+    SampleShare sh;
+    if (!c->fused) {
+        ev_record(c, 0);
+        RC(flop_pass(c, &launches));
+        ev_record(c, 1);
+        if (draw) {
+            CU(launch_sample(seed, c->a_rows, n, c->samples.p, c->stream));
+            ++launches;
+        }
+        RC(sample_share(c, d_rows, n, false, &sh, &launches));
+        ev_record(c, 2);
+        RC(run_symbolic(c, sh.rows, sh.n, nullptr, kZStar, true, &launches, sh.item_flop,
+                        sh.use_full ? &sh.full : nullptr));
+        ev_record(c, 3);
+        RC(allreduce_totals(c));
+        ev_record(c, 4);
+        if (d_ceil || d_real) {
+            CU(launch_predict(c->flop.p, local_rows(c), c->totals.p, 0.0, d_ceil, d_real, c->num_sms,
+                              c->stream));
+            ++launches;
+        }
+        ev_record(c, 5);
+        c->ev_order = 0;
     } else {
-        RC(run_symbolic(c, d_rows, n, nullptr, kZStar, true, &launches));
+        ev_record(c, 0);
+        if (draw) {
+            CU(launch_sample(seed, c->a_rows, n, c->samples.p, c->stream));
+            ++launches;
+        }
+        RC(sample_share(c, d_rows, n, true, &sh, &launches));
+        ev_record(c, 1);
+        RC(run_symbolic(c, sh.rows, sh.n, nullptr, kZStar, true, &launches, sh.item_flop,
+                        sh.use_full ? &sh.full : nullptr));
+        ev_record(c, 2);
+        RC(allreduce_totals(c, kFStar, 2, false));  // f*, z*: CR is known everywhere
+        ev_record(c, 3);
+        PredOut pred;
+        pred.totals = c->totals.p;
+        pred.ceil = d_ceil;
+        pred.real = d_real;
+        if (pred.on()) {
+            pred.redo_cap = std::min<int64_t>(std::max(local_rows(c), 1), int64_t(1) << 16);
+            RC(c->redo.ensure(pred.redo_cap));
+            RC(c->nredo.ensure(1));
+            CU(cudaMemsetAsync(c->nredo.p, 0, sizeof(unsigned long long), c->stream));
+            pred.redo = c->redo.p;
+            pred.nredo = c->nredo.p;
+        }
+        RC(flop_pass(c, &launches, c->stream, pred));
+        if (pred.on()) {
+            CU(launch_predict_redo(c->flop.p, local_rows(c), pred, c->num_sms, c->stream));
+            ++launches;
+        }
+        ev_record(c, 4);
+        RC(allreduce_totals(c, kF, 1, true));  // F, max
+        ev_record(c, 5);
+        c->ev_order = 1;
     }
-    ev_record(c, 3);
-    RC(allreduce_totals(c));
-    ev_record(c, 4);
-    if (d_ceil || d_real) {
-        CU(launch_predict(c->flop.p, local_rows(c), c->totals.p, 0.0, d_ceil, d_real, c->num_sms,
-                          c->stream));
-        ++launches;
-    }
-    ev_record(c, 5);
     c->profile_valid = true;
     c->last_launches = launches;
     return SPNNZ_OK;
@@ -616,6 +703,8 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     c->heavy_pbuf.release();
     c->heavy_utab.release();
     c->item_flop.release();
+    c->redo.release();
+    c->nredo.release();
     c->heavy_boff.release();
     for (auto* b : {&c->heavy_bnd, &c->heavy_unit_item, &c->heavy_unit_e0}) b->release();
     c->heavy_tasks.release();

@@ -150,4 +150,50 @@ __device__ __forceinline__ double predicted_cr(long long f_star, long long z_sta
     return (f_star > 0 && z_star > 0) ? __ddiv_rn((double)f_star, (double)z_star) : 1.0;
 }
 
+// (int64)ceil(q) exactly as the reference's x86-64 build evaluates it: a
+// quotient >= 2^63 (only for cr < 1 and huge rows) converts to the "integer
+// indefinite" value INT64_MIN (cvttsd2si), where the GPU's cvt would saturate.
+__device__ __forceinline__ long long ceil_of(long long f, double q) {
+    const double cq = ceil(q);
+    const long long c = cq >= 9223372036854775808.0 ? static_cast<long long>(0x8000000000000000ULL)
+                                                    : static_cast<long long>(cq);
+    return f < c ? f : c;
+}
+
+__device__ __forceinline__ long long ceil_view(long long f, double cr, double* q_out) {
+    const double q = __ddiv_rn(static_cast<double>(f), cr);
+    *q_out = q;
+    return ceil_of(f, q);
+}
+
+// a / b correctly rounded (== __ddiv_rn) for a fixed divisor b >= 1 without
+// a division per call: q from the reciprocal y = RN(1/b) plus one FMA
+// correction, then an exact acceptance test -- the remainder r = a - q b is
+// exact (FMA, q within an ulp), ulp(q) * b is exact (power-of-two scaling),
+// and |r| < ulp(q) b / 2 means q is the unique nearest double to a / b.
+// Anything else (ties, a <= 0) takes __ddiv_rn.
+struct FastDiv {
+    double b, y;
+    __device__ __forceinline__ void init(double b_) {
+        b = b_;
+        y = __drcp_rn(b_);
+    }
+    // q = a / b correctly rounded when it returns true (a > 0, b >= 1); false
+    // leaves the case to __ddiv_rn.
+    __device__ __forceinline__ bool fast(double a, double* q_out) const {
+        if (!(a > 0.0 && b >= 1.0)) return false;
+        double q = __dmul_rn(a, y);
+        q = __fma_rn(__fma_rn(-q, b, a), y, q);
+        const double r = __fma_rn(-q, b, a);
+        const double u = __longlong_as_double((__double_as_longlong(q) & 0x7ff0000000000000LL) -
+                                              (52LL << 52));
+        *q_out = q;
+        return __dmul_rn(2.0, fabs(r)) < __dmul_rn(u, b);
+    }
+    __device__ __forceinline__ double operator()(double a) const {
+        double q;
+        return fast(a, &q) ? q : __ddiv_rn(a, b);
+    }
+};
+
 }  // namespace spnnz_gpu

@@ -134,13 +134,36 @@ __device__ __forceinline__ Carry shfl_up_carry(const Carry& c, int d) {
     return r;
 }
 
-template <int BLOCK, int V>
+// The per-row prediction of a final flop value (fused predict).
+struct Emit {
+    FastDiv div;
+    PredOut p;
+    __device__ __forceinline__ void operator()(int32_t r, long long v) const {
+        double q = 0.0;  // 0 / cr = +0 (cr >= 1)
+        if (v == 0 || div.fast(static_cast<double>(v), &q)) {
+            if (p.ceil) p.ceil[r] = ceil_of(v, q);
+            if (p.real) p.real[r] = q;
+        } else {
+            const unsigned long long k = atomicAdd(p.nredo, 1ULL);
+            if (k < static_cast<unsigned long long>(p.redo_cap)) p.redo[k] = r;
+        }
+    }
+};
+
+__device__ __forceinline__ Emit make_emit(const PredOut& p) {
+    Emit e;
+    e.div.init(p.on() ? predicted_cr(p.totals[kFStar], p.totals[kZStar]) : 1.0);
+    e.p = p;
+    return e;
+}
+
+template <int BLOCK, int V, bool PRED>
 __global__ void __launch_bounds__(BLOCK, 5)
 k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
        const uint16_t* __restrict__ bdeg, const int64_t* __restrict__ brpt, int32_t m,
        int64_t base, int64_t nnz, const int32_t* __restrict__ tile_row,
        int64_t* __restrict__ flop, long long* __restrict__ tile_lead,
-       long long* __restrict__ tile_total, long long* __restrict__ tile_max) {
+       long long* __restrict__ tile_total, long long* __restrict__ tile_max, PredOut pred) {
     constexpr int TILE = BLOCK * V, NW = BLOCK / 32;
     static_assert(TILE == kFlopTile && V == 16, "tile size");
     __shared__ uint32_t s_start[TILE / 32];  // bit i: an owned non-empty row starts at entry i
@@ -154,6 +177,8 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
     const int n = static_cast<int>(te - ts);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int k = tid; k < TILE / 32; k += BLOCK) s_start[k] = 0u;
+    Emit emit{};
+    if (PRED) emit = make_emit(pred);
 
     // 1. this thread's V consecutive entries: columns (16-byte evict_first
     //    loads when the tile is whole), then all V degree gathers in flight
@@ -196,6 +221,7 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
             s_rowat[pos] = r;
         } else {
             flop[r] = 0;
+            if (PRED) emit(r, 0);
         }
     }
     __syncthreads();
@@ -211,6 +237,7 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
         if ((bits >> k) & 1u) {
             if (row >= 0) {
                 flop[row] = cur;  // complete inside the thread
+                if (PRED) emit(row, cur);
                 tmax = cur > tmax ? cur : tmax;
             } else {
                 head = cur;
@@ -245,6 +272,7 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
         const long long v = cin.v + head;
         if (cin.flag) {
             flop[cin.row] = v;
+            if (PRED) emit(cin.row, v);
             tmax = v > tmax ? v : tmax;
         } else {
             tile_lead[t] = v;  // continues a row owned by an earlier tile
@@ -254,7 +282,10 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
         const Carry all = carry_op(cin, mine);
         if (all.flag) {
             flop[all.row] = all.v;  // the fixup adds the following tiles' leading slices
-            if (__ldg(&arpt[all.row + 1]) <= te) tmax = all.v > tmax ? all.v : tmax;
+            if (__ldg(&arpt[all.row + 1]) <= te) {  // the row ends with the tile: final
+                tmax = all.v > tmax ? all.v : tmax;
+                if (PRED) emit(all.row, all.v);
+            }
         } else {
             tile_lead[t] = all.v;  // no row starts in this tile
         }
@@ -270,12 +301,12 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
 // Adds each tile's leading slice to the row it continues (one thread per
 // first continuing tile of a row, summing the run of tiles that continue the
 // same row) and reduces F and max over all tiles.
-template <int BLOCK>
+template <int BLOCK, bool PRED>
 __global__ void __launch_bounds__(BLOCK)
 k_flop_fixup(const int32_t* __restrict__ tile_row, int64_t tiles,
              const long long* __restrict__ tile_lead, const long long* __restrict__ tile_total,
              const long long* __restrict__ tile_max, int64_t* __restrict__ flop,
-             long long* __restrict__ totals) {
+             long long* __restrict__ totals, PredOut pred) {
     __shared__ long long s_red[BLOCK / 32];
     const int64_t t = blockIdx.x * int64_t(BLOCK) + threadIdx.x;
     long long sum = 0, mx = 0;
@@ -292,6 +323,7 @@ k_flop_fixup(const int32_t* __restrict__ tile_row, int64_t tiles,
             for (int64_t u = t; u < tiles && tile_row[u] == r + 1; ++u) carry += tile_lead[u];
             const long long v = flop[r] + carry;
             flop[r] = v;
+            if (PRED) make_emit(pred)(r, v);
             mx = v > mx ? v : mx;
         }
     }
@@ -328,8 +360,26 @@ __global__ void k_check_rows(const int32_t* __restrict__ rows, int64_t n, int32_
     if (i < n && (rows[i] < 0 || rows[i] >= num_rows)) atomicAdd(bad, 1);
 }
 
-// One warp per listed row: flop = sum of B row lengths over its entries
-// (compute_flop's sum, flop.hpp:41-50, for that row).
+// FLOP of listed rows (compute_flop's sum, flop.hpp:41-50, for those rows):
+// one warp per row up to kItemLong entries; longer rows (hub rows of
+// power-law matrices, tens of thousands of entries) are left to
+// k_item_flop_long, where a whole block takes each one.
+constexpr int64_t kItemLong = 2048;
+
+__device__ __forceinline__ long long item_flop_range(const DevCsr& a, const int64_t* __restrict__ brpt,
+                                                     int64_t e, int64_t e1, int stride) {
+    long long f = 0;
+    for (; e < e1; e += int64_t(stride) * 4) {
+        int c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k] = e + int64_t(stride) * k < e1 ? __ldg(&a.col[e + int64_t(stride) * k]) : -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (c[k] >= 0) f += __ldg(&brpt[c[k] + 1]) - __ldg(&brpt[c[k]]);
+    }
+    return f;
+}
+
 __global__ void __launch_bounds__(256) k_item_flop(DevCsr a, const int64_t* __restrict__ brpt,
                                                   int32_t row_lo, const int32_t* __restrict__ rows,
                                                   int64_t n, int64_t* __restrict__ out) {
@@ -339,18 +389,27 @@ __global__ void __launch_bounds__(256) k_item_flop(DevCsr a, const int64_t* __re
         const int32_t r = rows[s] - row_lo;
         long long f = 0;
         if (r >= 0 && r < a.rows) {
-            const int64_t e1 = a.rpt[r + 1];
-            for (int64_t e = a.rpt[r] + lane; e < e1; e += 32 * 4) {
-                int c[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) c[k] = e + 32 * k < e1 ? __ldg(&a.col[e + 32 * k]) : -1;
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (c[k] >= 0) f += __ldg(&brpt[c[k] + 1]) - __ldg(&brpt[c[k]]);
-            }
+            const int64_t e0 = a.rpt[r], e1 = a.rpt[r + 1];
+            if (e1 - e0 > kItemLong) continue;  // k_item_flop_long
+            f = item_flop_range(a, brpt, e0 + lane, e1, 32);
         }
         f = warp_sum_ll(f);
         if (lane == 0) out[s] = f;
+    }
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_item_flop_long(DevCsr a, const int64_t* __restrict__ brpt,
+                                                         int32_t row_lo, const int32_t* __restrict__ rows,
+                                                         int64_t n, int64_t* __restrict__ out) {
+    __shared__ long long s_red[BLOCK / 32];
+    for (int64_t s = blockIdx.x; s < n; s += gridDim.x) {  // block-uniform
+        const int32_t r = rows[s] - row_lo;
+        if (r < 0 || r >= a.rows) continue;
+        const int64_t e0 = a.rpt[r], e1 = a.rpt[r + 1];
+        if (e1 - e0 <= kItemLong) continue;
+        const long long f = block_sum_ll<BLOCK>(item_flop_range(a, brpt, e0 + threadIdx.x, e1, BLOCK), s_red);
+        if (threadIdx.x == 0) out[s] = f;
     }
 }
 
@@ -388,6 +447,29 @@ cudaError_t launch_item_flop(const DevCsr& a, const int64_t* brpt, int32_t row_l
     int64_t grid = (n + 7) / 8;
     if (grid > int64_t(num_sms) * 8) grid = int64_t(num_sms) * 8;
     k_item_flop<<<static_cast<unsigned>(grid), 256, 0, stream>>>(a, brpt, row_lo, rows, n, out);
+    k_item_flop_long<1024><<<static_cast<unsigned>(num_sms), 1024, 0, stream>>>(a, brpt, row_lo, rows, n, out);
+    return cudaGetLastError();
+}
+
+__global__ void k_predict_redo(const int64_t* __restrict__ flop, int64_t m, PredOut p) {
+    const double cr = predicted_cr(p.totals[kFStar], p.totals[kZStar]);
+    const unsigned long long n = *p.nredo;
+    const bool all = n > static_cast<unsigned long long>(p.redo_cap);
+    const int64_t cnt = all ? m : static_cast<int64_t>(n);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < cnt;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = all ? i : p.redo[i];
+        double q;
+        const long long c = ceil_view(flop[r], cr, &q);
+        if (p.ceil) p.ceil[r] = c;
+        if (p.real) p.real[r] = q;
+    }
+}
+
+cudaError_t launch_predict_redo(const int64_t* flop, int64_t m, const PredOut& pred, int num_sms,
+                                cudaStream_t stream) {
+    if (!pred.on() || m == 0) return cudaSuccess;
+    k_predict_redo<<<static_cast<unsigned>(num_sms) * 4, 256, 0, stream>>>(flop, m, pred);
     return cudaGetLastError();
 }
 
@@ -428,17 +510,25 @@ cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStr
 
 cudaError_t launch_flop(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt,
                         const FlopScratch& s, int64_t* flop, long long* totals,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, const PredOut& pred) {
     const int64_t tiles = flop_tiles(a);
     if (tiles == 0) return cudaSuccess;
-    k_flop<kFlopBlock, kFlopIpt><<<static_cast<unsigned>(tiles), kFlopBlock, 0, stream>>>(
-        a.rpt, a.col, bdeg, brpt, a.rows, a.base, a.nnz, s.tile_x, flop, s.tile_carry,
-        s.tile_total, s.tile_max);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    const unsigned g = static_cast<unsigned>(tiles);
     constexpr int FB = 256;
-    k_flop_fixup<FB><<<static_cast<unsigned>((tiles + FB - 1) / FB), FB, 0, stream>>>(
-        s.tile_x, tiles, s.tile_carry, s.tile_total, s.tile_max, flop, totals);
+    const unsigned gf = static_cast<unsigned>((tiles + FB - 1) / FB);
+    if (pred.on()) {
+        k_flop<kFlopBlock, kFlopIpt, true><<<g, kFlopBlock, 0, stream>>>(
+            a.rpt, a.col, bdeg, brpt, a.rows, a.base, a.nnz, s.tile_x, flop, s.tile_carry,
+            s.tile_total, s.tile_max, pred);
+        k_flop_fixup<FB, true><<<gf, FB, 0, stream>>>(s.tile_x, tiles, s.tile_carry, s.tile_total,
+                                                      s.tile_max, flop, totals, pred);
+    } else {
+        k_flop<kFlopBlock, kFlopIpt, false><<<g, kFlopBlock, 0, stream>>>(
+            a.rpt, a.col, bdeg, brpt, a.rows, a.base, a.nnz, s.tile_x, flop, s.tile_carry,
+            s.tile_total, s.tile_max, pred);
+        k_flop_fixup<FB, false><<<gf, FB, 0, stream>>>(s.tile_x, tiles, s.tile_carry, s.tile_total,
+                                                       s.tile_max, flop, totals, pred);
+    }
     return cudaGetLastError();
 }
 

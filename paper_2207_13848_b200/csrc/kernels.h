@@ -4,6 +4,12 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifdef __CUDACC__
+#define SPNNZ_HD __host__ __device__
+#else
+#define SPNNZ_HD
+#endif
+
 namespace spnnz_gpu {
 
 // Device view of a CSR row range.  `rpt` points at the first row's offset
@@ -50,9 +56,27 @@ cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStr
 // B.rpt for the exact length.  Gathered under an L2 evict_last policy.
 cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, uint16_t* deg, int num_sms,
                           cudaStream_t stream);
+// Fused predict: with ceil/real set, the FLOP pass also writes
+// min(flop, ceil(flop / cr)) (and flop / cr) for every row as its flop becomes
+// final, cr derived on the device from totals[kFStar], totals[kZStar].
+struct PredOut {
+    const long long* totals = nullptr;
+    int64_t* ceil = nullptr;
+    double* real = nullptr;
+    // rows whose quotient the reciprocal fast path could not certify
+    // (ties): redone with an IEEE division by launch_predict_redo
+    int32_t* redo = nullptr;
+    unsigned long long* nredo = nullptr;
+    int64_t redo_cap = 0;
+    SPNNZ_HD bool on() const { return ceil || real; }
+};
+// Redoes the rows listed by a fused FLOP pass (or every row when the list
+// overflowed) with __ddiv_rn.
+cudaError_t launch_predict_redo(const int64_t* flop, int64_t m, const PredOut& pred, int num_sms,
+                                cudaStream_t stream);
 cudaError_t launch_flop(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt,
                         const FlopScratch& s, int64_t* flop, long long* totals,
-                        cudaStream_t stream);
+                        cudaStream_t stream, const PredOut& pred = PredOut());
 
 // -------------------------------------------------------------- sampler
 cudaError_t launch_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* rows,
@@ -80,11 +104,6 @@ constexpr int64_t kHeavyUnitProducts = 4096;
 constexpr int kIvShift = 19;
 constexpr int kMaxIntervals = 256;  // B.cols <= 2^27; wider B takes the bucket path
 constexpr int64_t kIntervalTarget = 32768;
-#ifdef __CUDACC__
-#define SPNNZ_HD __host__ __device__
-#else
-#define SPNNZ_HD
-#endif
 struct Intervals {
     int shift;
     int32_t count;

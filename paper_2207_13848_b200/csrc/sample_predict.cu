@@ -32,23 +32,12 @@ __global__ void k_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* __
     rows[r] = rid;
 }
 
-// (int64)ceil(q) exactly as the reference's x86-64 build evaluates it: a
-// quotient >= 2^63 (only for cr < 1 and huge rows) converts to the "integer
-// indefinite" value INT64_MIN (cvttsd2si), where the GPU's cvt would saturate.
-__device__ __forceinline__ long long ceil_view(long long f, double cr, double* q_out) {
-    const double q = __ddiv_rn(static_cast<double>(f), cr);
-    *q_out = q;
-    const double cq = ceil(q);
-    const long long c = cq >= 9223372036854775808.0 ? static_cast<long long>(0x8000000000000000ULL)
-                                                    : static_cast<long long>(cq);
-    return f < c ? f : c;
-}
-
 template <bool CEIL, bool REAL>
 __global__ void __launch_bounds__(256)
 k_predict(const int64_t* __restrict__ flop, int64_t m, const long long* __restrict__ totals,
           double cr_in, int64_t* __restrict__ ceil_out, double* __restrict__ real_out) {
     const double cr = totals ? predicted_cr(totals[kFStar], totals[kZStar]) : cr_in;
+
     const int64_t pairs = m >> 1;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(flop) |

@@ -306,6 +306,23 @@ def test_predict_views_bitwise_vs_oracle(oracle):
         assert (spnnz.predict_row_structure(prof, cr) == oracle.predict_row_structure(f, cr)).all()
 
 
+def test_predict_division_random_ratios(oracle):
+    """Per-row views bit-identical to the CPU division for random ratios,
+    including quotients that are exact integers and near-halfway cases
+    (flop = k * cr rounded).  (The fused predictor's certified reciprocal
+    path, FastDiv, is checked on whole configs by test_config_fused_predictor.)"""
+    rng = np.random.default_rng(2)
+    f = np.concatenate([rng.integers(1, 2**31, 20000), rng.integers(2**31, 2**62, 20000),
+                        np.arange(1, 5000)]).astype(np.int64)
+    crs = list(rng.uniform(1.0, 64.0, 24)) + list(1.0 + rng.uniform(0, 1e-9, 4)) + [3.0, 7.0, 1.5, 1.25]
+    for cr in crs:
+        near = np.unique(np.round(np.arange(1, 3000) * cr)).astype(np.int64)  # quotients near integers
+        g = np.concatenate([f, near])
+        prof = spnnz.FlopProfile(g, int(g.sum() % 2**62), int(g.max()))
+        assert (spnnz.predict_row_structure(prof, cr) == oracle.predict_row_structure(g, cr)).all(), cr
+        assert (spnnz.predict_row_structure_ceil(prof, cr) == oracle.predict_row_structure_ceil(g, cr)).all(), cr
+
+
 def test_identity_predicts_exactly():
     # test_predict.cpp:146-157
     for n in (10, 100, 1000):
@@ -393,6 +410,35 @@ def test_config1_full_arrays(P, golden):
         assert (rep.plan.sample_rows == arr[f"rows_{label}"]).all()
         s = P.sampled_symbolic(rep.plan.sample_rows)
         assert (s.nnz_per_row == arr[f"per_sample_{label}"]).all()
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 4, 5])
+def test_config_fused_predictor(golden, cfg, monkeypatch):
+    """SPNNZ_FUSED_PREDICT=1 (CR first, one pass writing flop and
+    the prediction): same report, sample rows and per-row views as the
+    reference."""
+    rec = golden["configs"][str(cfg)]
+    info = gen.CONFIGS[cfg]
+    a, b = gen.make_config(cfg)
+    monkeypatch.setenv("SPNNZ_FUSED_PREDICT", "1")
+    q = Predictor(0)
+    q.load(a, b)
+    m = rec["modes"]["uncapped"]
+    rep = q.run_prediction(info["seed"], SamplePolicy(info["fraction"], UNCAPPED))
+    ref = m["report"]
+    assert rep.total_flop == ref["total_flop"] and rep.stats.sampled_flop == ref["sampled_flop"]
+    assert rep.stats.sampled_nnz == ref["sampled_nnz"] and rep.predicted_cr == ref["predicted_cr"]
+    assert rep.z1_star == ref["z1_star"] and rep.z2_star == ref["z2_star"]
+    if cfg == 1:
+        arr = golden["cfg1"]
+        assert (rep.predicted_row_nnz_ceil == arr["ceil_uncapped"]).all()
+        assert (rep.predicted_row_nnz == arr["real_uncapped"]).all()
+    else:
+        assert digest(rep.predicted_row_nnz_ceil) == m["ceil"]
+        assert digest(rep.predicted_row_nnz) == m["real"]
+    prof = q.compute_flop()
+    assert prof.total_flop == ref["total_flop"]
+    q.close()
 
 
 @pytest.mark.parametrize("cfg", [2, 5])
