@@ -398,18 +398,34 @@ __global__ void __launch_bounds__(256) k_item_flop(DevCsr a, const int64_t* __re
     }
 }
 
+// Each block checks a contiguous group of items in parallel, collects the
+// long rows in shared memory, then sums each of them with all its threads.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_item_flop_long(DevCsr a, const int64_t* __restrict__ brpt,
                                                          int32_t row_lo, const int32_t* __restrict__ rows,
                                                          int64_t n, int64_t* __restrict__ out) {
     __shared__ long long s_red[BLOCK / 32];
-    for (int64_t s = blockIdx.x; s < n; s += gridDim.x) {  // block-uniform
-        const int32_t r = rows[s] - row_lo;
-        if (r < 0 || r >= a.rows) continue;
-        const int64_t e0 = a.rpt[r], e1 = a.rpt[r + 1];
-        if (e1 - e0 <= kItemLong) continue;
-        const long long f = block_sum_ll<BLOCK>(item_flop_range(a, brpt, e0 + threadIdx.x, e1, BLOCK), s_red);
-        if (threadIdx.x == 0) out[s] = f;
+    __shared__ int64_t s_item[BLOCK];
+    __shared__ int s_n;
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t g0 = blockIdx.x * per, g1 = g0 + per < n ? g0 + per : n;
+    for (int64_t b = g0; b < g1; b += BLOCK) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_n = 0;
+        __syncthreads();
+        const int64_t s = b + threadIdx.x;
+        if (s < g1) {
+            const int32_t r = rows[s] - row_lo;
+            if (r >= 0 && r < a.rows && a.rpt[r + 1] - a.rpt[r] > kItemLong) s_item[atomicAdd(&s_n, 1)] = s;
+        }
+        __syncthreads();
+        for (int k = 0; k < s_n; ++k) {
+            const int64_t it = s_item[k];
+            const int32_t r = rows[it] - row_lo;
+            const long long f =
+                block_sum_ll<BLOCK>(item_flop_range(a, brpt, a.rpt[r] + threadIdx.x, a.rpt[r + 1], BLOCK), s_red);
+            if (threadIdx.x == 0) out[it] = f;
+        }
     }
 }
 

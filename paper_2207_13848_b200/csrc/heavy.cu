@@ -1,36 +1,38 @@
 // Heavy rows of the symbolic engine (FLOP > kBin5Max): exact distinct-column
 // counts with every set operation in shared memory.
 //
-// A heavy row of C = A*B can have millions of products (config 5: 8.5 M) and
-// its distinct set does not fit one SM.  A per-row global bitmap (2 MB at
-// config 5, ~850 rows in flight) thrashes L2 into gigabytes of DRAM
-// read-modify-write, so instead the row's products are bucketed by column
-// range (ranges of W = 2^wshift columns) and every bucket is counted on chip:
-//   0. prep/entries  per batch: unit, entry and product offsets of every
-//                    heavy row; per row, the product prefix over its entries;
-//   1. count    per unit of kHeavyUnitProducts products (one block): per-warp
-//               shared histograms over the R ranges, added into the row's
-//               bucket counts;
-//   2. offsets  per row, bucket starts in the product buffer;
-//   3. place    per unit again: stage the products in shared memory, counting-
-//               sort them by range, reserve each range's slice of its bucket
-//               with one atomic and write the sorted runs out (coalesced);
-//   4. tasks    per row, its buckets are cut into aligned spans of 2^19
-//               columns (a 64 KB shared bitmap); a span is one task, or, above
-//               kTaskProducts products, several tasks that share a merge slot;
-//   5. run      one 512-thread block per task (3 per SM) reads its span's
-//               contiguous products, atomicOr's each bit into the bitmap and
-//               counts the bits it set first; tasks sharing a span OR their
-//               non-zero words into a global merge bitmap and count
-//               popc(word & ~old) instead.  The bitmap is returned to zero by
-//               re-walking the keys (sparse spans) or clearing it.
-// B.cols <= 2^20 (configs 2 and 4): one range covers all columns; tasks are
-// slices of the row's product range read straight from the B rows (1024
-// threads, 128 KB bitmap).
-// W = max(2^17, 2^ceil(log2 B.cols) / 256) keeps R <= 256 (per-warp
-// histograms) up to B.cols = 2^27; beyond that W = 2^19 with shared
-// histograms.  Every count is a set cardinality: exact and independent of
-// bucketing, task boundaries and scheduling.
+// A heavy row of C = A*B can have millions of products (config 5: up to
+// 1.2 M, 84 M over 1 249 sampled rows) and its distinct set does not fit one
+// SM.  A per-row global bitmap (2 MB at config 5, ~850 rows in flight)
+// thrashes L2 into gigabytes of DRAM read-modify-write, so the columns are cut
+// into ranges of W = 2^19 (a 64 KB shared bitmap) and each (row, range) is
+// counted on chip.  Per batch of heavy rows:
+//   0. prep / entries   unit (4096 products), entry and product offsets of
+//                       every row; per entry its product prefix and B-row
+//                       start; a unit -> (row, first entry) map;
+//   1 < R <= 256 ranges (B.cols <= 2^27, the default path):
+//   1. sort_units   each unit's products are enumerated, counting-sorted by
+//                   range in shared memory and written back in place with the
+//                   unit's R + 1 range starts; per-(row, range) totals;
+//   2. plan_units   a task per (row, range); ranges above kTaskProducts split
+//                   into unit groups sharing a merge slot; ranges of at most
+//                   kSmallTaskProducts go to a separate list;
+//   3. run_units    3 x 512-thread blocks per SM, one bitmap task each: the
+//                   range is read as one slice per unit, each bit atomically
+//                   OR-ed and the bits set first counted; split ranges OR
+//                   their non-zero words into a global merge bitmap and count
+//                   popc(word & ~old); the next task's descriptor and table
+//                   entries are fetched while the current one runs;
+//   4. run_small    small ranges: four 128-thread groups per block, each with
+//                   a 4096-slot shared hash and its own named barrier;
+//   R == 1 (B.cols <= 2^20): tasks are product slices read straight from the
+//                   B rows (1024 threads, 128 KB bitmap, merge slots);
+//   R > 256: count -> offsets -> place -> plan -> run over global buckets;
+//   opt-in interval path (SPNNZ_HEAVY_INTERVALS=1, B rows sorted): a
+//                   per-(entry, interval) boundary table replaces the product
+//                   buffer (exact; slower at config 5).
+// Every count is a set cardinality: exact and independent of bucketing, task
+// boundaries and scheduling.
 #include "symbolic_common.cuh"
 
 namespace spnnz_gpu {
@@ -563,9 +565,8 @@ __global__ void k_heavy_tasks_r1(SymScratch sc, int64_t count, int64_t task_cap)
 // ---- 5. run the tasks: one block per task, a shared bitmap over the span,
 // kept all-zero between tasks.
 // MODE: kRunItem (R == 1) products straight from the B rows; kRunBuckets the
-// task's contiguous bucket span; kRunUnits one slice per unit of the task's
-// unit group.
-constexpr int kRunItem = 0, kRunBuckets = 1, kRunUnits = 2;
+// task's contiguous bucket span (unit-sorted buckets: k_heavy_run_units).
+constexpr int kRunItem = 0, kRunBuckets = 1;
 
 template <int kRunBlock, int MODE>
 __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch sc, int64_t first,
@@ -630,35 +631,8 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
         };
         if constexpr (MODE == kRunBuckets) {
             contiguous(insert);
-        } else if constexpr (MODE == kRunItem) {
-            item_products<kRunBlock>(g, sc, first, t.item, t.a, t.b, s_off, s_b0, insert);
         } else {
-            using Scan = cub::BlockScan<int, kRunBlock>;
-            __shared__ typename Scan::TempStorage s_scan;
-            const long long ubase = sc.heavy_unit_off[t.item];
-            const long long pbase = sc.heavy_foff[t.item];
-            for (long long u0 = t.a; u0 < t.b; u0 += kRunBlock) {
-                const int n = static_cast<int>(t.b - u0 < kRunBlock ? t.b - u0 : kRunBlock);
-                int len = 0;
-                int64_t start = 0;
-                if (threadIdx.x < n) {
-                    const long long u = u0 + threadIdx.x;
-                    const int32_t* tab = sc.heavy_utab + (ubase + u) * (R + 1);
-                    const int lo = tab[t.r0], hi = tab[t.r1];
-                    len = hi - lo;
-                    start = pbase + u * kHeavyUnitProducts + lo;
-                }
-                int ex, tot;
-                __syncthreads();  // the previous round's slices are consumed
-                Scan(s_scan).ExclusiveSum(len, ex, tot);
-                if (threadIdx.x < n) {
-                    s_off[threadIdx.x] = ex;
-                    s_b0[threadIdx.x] = start;
-                }
-                if (threadIdx.x == 0) s_off[n] = tot;
-                __syncthreads();
-                chunk_products<kRunBlock / 32>(s_off, s_b0, n, 0, tot, sc.heavy_pbuf, insert);
-            }
+            item_products<kRunBlock>(g, sc, first, t.item, t.a, t.b, s_off, s_b0, insert);
         }
         __syncthreads();  // every insert is done
         if (t.slot >= 0) {
