@@ -26,8 +26,8 @@ $(BUILD)/%.o: $(SRC)/%.cpp $(HDRS) | $(BUILD)
 $(OUT)/libspnnz_gpu.so: $(OBJS) | $(OUT)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl
 
-$(OUT)/libspnnz_gen.so: $(SRC)/gen/generators.cpp | $(OUT)
-	$(CXX) -std=c++20 -O3 -fPIC -shared -pthread -Wall -o $@ $<
+$(OUT)/libspnnz_gen.so: $(SRC)/gen/generators.cpp $(SRC)/gen/mmio.cpp | $(OUT)
+	$(CXX) -std=c++20 -O3 -fPIC -shared -pthread -Wall -Wl,--exclude-libs,ALL -o $@ $(SRC)/gen/generators.cpp $(SRC)/gen/mmio.cpp
 
 # C++ drop-in test (runs on a GPU box: tests/test_gpu_parity.py)
 $(BUILD)/test_dropin: tests/cpp/test_dropin.cpp include/spnnz_gpu/spnnz_gpu.hpp $(OUT)/libspnnz_gpu.so | $(BUILD)

@@ -414,7 +414,10 @@ def run_ours(args, rank, world, local):
                                 rep.total_flop, rep.plan.p)
         accuracy = {"Z_exact": ex.total_nnz, "Z2_star": rep.z2_star, "Z1_star": rep.z1_star,
                     "abs_rel_err_z2": abs(er.eps2), "abs_rel_err_z1": abs(er.eps1),
-                    "cr": rep.predicted_cr, "exact_pass_s": t_exact}
+                    "cr": rep.predicted_cr, "exact_pass_s": t_exact,
+                    # the paper's overhead metric (bench.hpp:346-369): prediction
+                    # time over the precise method, here the GPU exact symbolic pass
+                    "overhead_fraction": (ms_max * 1e-3) / t_exact if t_exact > 0 else None}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

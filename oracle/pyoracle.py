@@ -181,6 +181,11 @@ class Reference:
         L.ref_run_pipeline.argtypes = [c_void_p, c_void_p, c_uint64, c_double, c_int64, c_int, POINTER(RefReport), c_void_p]
         L.ref_error_report.argtypes = [c_double, c_double, c_int64, c_int64, c_int64, c_double, c_void_p]
         L.ref_splitmix_seq.argtypes = [c_uint64, c_int64, c_void_p]
+        L.ref_matrix_export.argtypes = [c_void_p, POINTER(c_int32), POINTER(c_int32), POINTER(c_int64), c_void_p, c_void_p]
+        L.ref_generate_synthetic.argtypes = [c_int, c_int32, c_int32, c_double, c_uint64, c_int32, c_double,
+                                             POINTER(c_void_p), ctypes.c_char_p, c_int]
+        L.ref_read_matrix_market.argtypes = [ctypes.c_char_p, POINTER(c_void_p)]
+        L.ref_write_matrix_market.argtypes = [ctypes.c_char_p, c_void_p]
 
     def _chk(self, rc):
         if rc == 1:
@@ -193,6 +198,40 @@ class Reference:
 
     def free_matrix(self, h):
         self.L.ref_matrix_free(h)
+
+    def export(self, h):
+        """(rows, cols, rpt, col) of a reference matrix handle."""
+        r, c, n = c_int32(), c_int32(), c_int64()
+        self.L.ref_matrix_export(h, byref(r), byref(c), byref(n), None, None)
+        rpt = np.empty(r.value + 1, np.int64)
+        col = np.empty(max(n.value, 1), np.int32)
+        self.L.ref_matrix_export(h, byref(r), byref(c), byref(n), rpt.ctypes.data, col.ctypes.data)
+        return r.value, c.value, rpt, col[: n.value]
+
+    def generate_synthetic(self, model, rows, cols, target, seed, bandwidth=0, skew=1.0):
+        """spnnz::generate_synthetic + synthetic_name -> (rows, cols, rpt, col, name)."""
+        h = c_void_p()
+        name = ctypes.create_string_buffer(256)
+        codes = {"uniform": 0, "banded": 1, "power-law": 2}
+        self._chk(self.L.ref_generate_synthetic(codes[model], rows, cols, target, seed, bandwidth, skew,
+                                                byref(h), name, 256))
+        out = self.export(h)
+        self.free_matrix(h)
+        return (*out, name.value.decode())
+
+    def read_matrix_market(self, path):
+        h = c_void_p()
+        self._chk(self.L.ref_read_matrix_market(str(path).encode(), byref(h)))
+        out = self.export(h)
+        self.free_matrix(h)
+        return out
+
+    def write_matrix_market(self, path, m):
+        h = self.matrix(m)
+        try:
+            self._chk(self.L.ref_write_matrix_market(str(path).encode(), h))
+        finally:
+            self.free_matrix(h)
 
     def splitmix(self, seed, n):
         out = np.empty(n, np.uint64)

@@ -2,11 +2,13 @@
 // INFRASTRUCTURE ONLY.
 //
 // Compiled by oracle/Makefile directly from /root/reference/proj/include
-// (the reference's own hot-path headers: csr, flop, symbolic, predict, rng,
-// parallel, types -- nothing is copied) into oracle/_ref/libspnnz_ref.so.
+// (the reference's own headers: csr, flop, symbolic, predict, rng, parallel,
+// types, plus synthetic and matrix_market for the corpus / ingestion checks
+// -- nothing is copied) into oracle/_ref/libspnnz_ref.so.
 // Used to (1) generate the golden fixtures in tests/golden/ and (2) time the
 // reference CPU path for bench.py --impl reference / cpu_baseline.
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -15,6 +17,8 @@
 
 #include "spnnz/csr.hpp"
 #include "spnnz/flop.hpp"
+#include "spnnz/matrix_market.hpp"
+#include "spnnz/synthetic.hpp"
 #include "spnnz/predict.hpp"
 #include "spnnz/symbolic.hpp"
 
@@ -197,5 +201,60 @@ extern "C" {
 void ref_splitmix_seq(uint64_t seed, int64_t n, uint64_t* out) {
     spnnz::SplitMix64 r(seed);
     for (int64_t i = 0; i < n; ++i) out[i] = r.next_u64();
+}
+}
+
+extern "C" {
+// Sizes of a reference matrix handle, then its arrays (rpt/col may be null).
+void ref_matrix_export(void* h, int32_t* rows, int32_t* cols, int64_t* nnz, int64_t* rpt, int32_t* col) {
+    const spnnz::CsrMatrix& m = static_cast<RefMatrix*>(h)->m;
+    *rows = m.rows;
+    *cols = m.cols;
+    *nnz = m.nnz();
+    if (rpt) std::memcpy(rpt, m.rpt.data(), m.rpt.size() * 8);
+    if (col) std::memcpy(col, m.col.data(), m.col.size() * 4);
+}
+
+// spnnz::generate_synthetic (synthetic.hpp:92) and synthetic_name (:203).
+int ref_generate_synthetic(int model, int32_t rows, int32_t cols, double target, uint64_t seed,
+                           int32_t bandwidth, double skew, void** out, char* name, int name_cap) {
+    return guard([&] {
+        spnnz::SyntheticSpec spec;
+        spec.rows = rows;
+        spec.cols = cols;
+        spec.model = model == 1 ? spnnz::SyntheticModel::banded
+                     : model == 2 ? spnnz::SyntheticModel::power_law
+                                  : spnnz::SyntheticModel::uniform;
+        spec.target_nnz_per_row = target;
+        spec.seed = seed;
+        spec.bandwidth = bandwidth;
+        spec.skew = skew;
+        auto* h = new RefMatrix;
+        h->m = spnnz::generate_synthetic(spec);
+        *out = h;
+        if (name) {
+            const std::string n = spnnz::synthetic_name(spec);
+            std::snprintf(name, static_cast<size_t>(name_cap), "%s", n.c_str());
+        }
+    });
+}
+
+// spnnz::read_matrix_market (matrix_market.hpp:89); parse errors -> 3 with
+// the reference's message in ref_last_error().
+int ref_read_matrix_market(const char* path, void** out) {
+    return guard([&] {
+        auto* h = new RefMatrix;
+        try {
+            h->m = spnnz::read_matrix_market(path);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int ref_write_matrix_market(const char* path, void* h) {
+    return guard([&] { spnnz::write_matrix_market(path, static_cast<RefMatrix*>(h)->m); });
 }
 }

@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <thread>
+#include <unordered_set>
 #include <vector>
 
 namespace {
@@ -65,12 +66,23 @@ int64_t poisson(double lambda, Rng& r) {
 void distinct(int32_t range, int32_t k, Rng& r, std::vector<int32_t>& out) {
     out.clear();
     if (k > range) k = range;
-    for (int32_t j = range - k; j < range; ++j) {
-        const int32_t t = static_cast<int32_t>(r.next_below(static_cast<uint64_t>(j) + 1));
-        if (std::find(out.begin(), out.end(), t) == out.end())
-            out.push_back(t);
-        else
-            out.push_back(j);
+    if (k <= 64) {
+        for (int32_t j = range - k; j < range; ++j) {
+            const int32_t t = static_cast<int32_t>(r.next_below(static_cast<uint64_t>(j) + 1));
+            if (std::find(out.begin(), out.end(), t) == out.end())
+                out.push_back(t);
+            else
+                out.push_back(j);
+        }
+    } else {  // same draws, a hash set for the membership test
+        std::unordered_set<int32_t> seen;
+        seen.reserve(static_cast<size_t>(k) * 2);
+        for (int32_t j = range - k; j < range; ++j) {
+            const int32_t t = static_cast<int32_t>(r.next_below(static_cast<uint64_t>(j) + 1));
+            const int32_t v = seen.insert(t).second ? t : j;
+            if (v == j) seen.insert(j);
+            out.push_back(v);
+        }
     }
     std::sort(out.begin(), out.end());
 }
@@ -151,6 +163,41 @@ int build_rows(int32_t rows, int32_t cols, int threads, spnnz_gen_csr* out, RowF
 }  // namespace
 
 extern "C" {
+
+// The reference's synthetic corpus model (synthetic.hpp:92-154): model 0
+// uniform, 1 banded, 2 power-law.  Per row: its own fork(seed, row) stream, a
+// Poisson(target_i) count by chunked products of uniforms, then that many
+// distinct columns (Floyd) in the row's window -- all columns, or the band
+// around the scaled diagonal.  Power-law rows scale the target by
+// (i+1)^-skew / sum_k (k+1)^-skew * rows (the sum taken in row order, as the
+// reference does, so the doubles agree).  Rows are built in parallel.
+// Returns 3 for an infeasible spec (the reference's invalid_argument).
+int spnnz_gen_synthetic(int model, int32_t rows, int32_t cols, double target, uint64_t seed,
+                        int32_t bandwidth, double skew, int threads, spnnz_gen_csr* out) {
+    if (rows < 0 || cols < 0) return 3;
+    if (target < 0 || target > static_cast<double>(cols)) return 3;
+    const int32_t band = bandwidth > 0 ? bandwidth
+                                       : static_cast<int32_t>(std::max(16.0, 4.0 * std::ceil(target)));
+    double wsum = 0.0;
+    if (model == 2)
+        for (int32_t i = 0; i < rows; ++i) wsum += std::pow(static_cast<double>(i) + 1.0, -skew);
+    return build_rows(rows, cols, threads, out, [&](int32_t i, std::vector<int32_t>& v) {
+        Rng r = Rng::fork(seed, static_cast<uint64_t>(i));
+        double t = target;
+        if (model == 2 && wsum > 0.0)
+            t = target * static_cast<double>(rows) * std::pow(static_cast<double>(i) + 1.0, -skew) / wsum;
+        int64_t k = poisson(t, r);
+        int32_t lo = 0, range = cols;
+        if (model == 1) {
+            const int32_t center = rows > 0 ? static_cast<int32_t>((static_cast<int64_t>(i) * cols) / rows) : 0;
+            lo = std::max<int32_t>(0, center - band);
+            range = std::min<int32_t>(cols, center + band + 1) - lo;
+        }
+        if (k > range) k = range;
+        distinct(range, static_cast<int32_t>(k), r, v);
+        for (auto& c : v) c += lo;
+    });
+}
 
 // cfg 1
 int spnnz_gen_poisson_uniform(int32_t rows, int32_t cols, double mean, int32_t lo, int32_t hi,
