@@ -15,7 +15,7 @@ CPP_SRCS := $(SRC)/capi.cpp
 OBJS := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(BUILD)/%.o,$(CPP_SRCS))
 HDRS := $(SRC)/kernels.h $(SRC)/device_common.cuh $(SRC)/symbolic_common.cuh include/spnnz_gpu/capi.h
 
-all: $(OUT)/libspnnz_gpu.so $(OUT)/libspnnz_gen.so $(BUILD)/test_dropin oracle
+all: $(OUT)/libspnnz_gpu.so $(OUT)/libspnnz_gen.so $(BUILD)/test_dropin $(BUILD)/spnnz_corpus oracle
 
 $(BUILD)/%.o: $(SRC)/%.cu $(HDRS) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
@@ -28,6 +28,10 @@ $(OUT)/libspnnz_gpu.so: $(OBJS) | $(OUT)
 
 $(OUT)/libspnnz_gen.so: $(SRC)/gen/generators.cpp $(SRC)/gen/mmio.cpp | $(OUT)
 	$(CXX) -std=c++20 -O3 -fPIC -shared -pthread -Wall -Wl,--exclude-libs,ALL -o $@ $(SRC)/gen/generators.cpp $(SRC)/gen/mmio.cpp
+
+# corpus harness: include/spnnz_gpu/harness.hpp
+$(BUILD)/spnnz_corpus: tools/spnnz_corpus.cpp include/spnnz_gpu/harness.hpp include/spnnz_gpu/spnnz_gpu.hpp include/spnnz_gpu/host.h $(OUT)/libspnnz_gpu.so $(OUT)/libspnnz_gen.so | $(BUILD)
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L$(OUT) -lspnnz_gpu -lspnnz_gen -Wl,-rpath,'$$ORIGIN/../$(OUT)'
 
 # C++ drop-in test (runs on a GPU box: tests/test_gpu_parity.py)
 $(BUILD)/test_dropin: tests/cpp/test_dropin.cpp include/spnnz_gpu/spnnz_gpu.hpp $(OUT)/libspnnz_gpu.so | $(BUILD)
