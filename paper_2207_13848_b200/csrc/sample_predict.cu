@@ -45,7 +45,10 @@ k_predict(const int64_t* __restrict__ flop, int64_t m, const long long* __restri
                           (REAL ? reinterpret_cast<uintptr_t>(real_out) : 0)) & 15) == 0;
     if (vec_ok) {
         // kU pairs per thread per step, their loads issued back to back
-        constexpr int kU = 4;
+#ifndef SPNNZ_PRED_U
+#define SPNNZ_PRED_U 4
+#endif
+        constexpr int kU = SPNNZ_PRED_U;
         const longlong2* f2 = reinterpret_cast<const longlong2*>(flop);
         for (int64_t i0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i0 < pairs; i0 += kU * stride) {
             longlong2 f[kU];
@@ -94,10 +97,14 @@ cudaError_t launch_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* r
 cudaError_t launch_predict(const int64_t* flop, int64_t m, const long long* totals, double cr,
                            int64_t* ceil_out, double* real_out, int num_sms, cudaStream_t stream) {
     if (m == 0 || (!ceil_out && !real_out)) return cudaSuccess;
-    // Enough resident warps to cover HBM latency: 8 blocks of 256 per SM,
-    // grid-stride over 16-byte pairs.
+    // 32 blocks of 256 per SM (measured best of 4-32 x unroll 1-8 at
+    // config 5: 0.068 ms, 60 % of the copy bandwidth), grid-stride over
+    // 16-byte pairs.
     int64_t grid = ((m >> 1) + 255) / 256;
-    const int64_t cap = int64_t(num_sms) * 8;
+#ifndef SPNNZ_PRED_GRID
+#define SPNNZ_PRED_GRID 32
+#endif
+    const int64_t cap = int64_t(num_sms) * SPNNZ_PRED_GRID;
     if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
     const unsigned g = static_cast<unsigned>(grid);
