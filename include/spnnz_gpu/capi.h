@@ -102,7 +102,12 @@ int spnnz_gpu_partition_rows(const int64_t* rpt, int32_t rows, int world, int32_
 /* Upload A (this rank's shard) and B (replicated).  b == NULL or b == a means
  * C = A*A and B shares A's device arrays.  residency says where the view's
  * pointers live.  Throws-equivalent: EINVAL if A.cols != B.rows
- * (flop.hpp:26-29).  Re-loading replaces the previous matrices. */
+ * (flop.hpp:26-29).  Re-loading replaces the previous matrices.
+ * Host views are copied asynchronously (for C = A*A in chunks, so the next
+ * run_prediction's FLOP pass overlaps the copy): pageable memory is staged
+ * before the call returns; pinned memory (spnnz_gpu_host_alloc or
+ * cudaHostAlloc) must stay unchanged until the next call on the context
+ * returns. */
 int spnnz_gpu_load(spnnz_gpu_ctx* ctx, const spnnz_csr_view* a, const spnnz_csr_view* b,
                    int residency);
 /* This rank's global A rows [row_lo, row_hi), and the global A.rows. */

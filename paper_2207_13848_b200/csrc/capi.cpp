@@ -131,6 +131,14 @@ struct DBuf {
 struct spnnz_gpu_ctx {
     int device = 0, rank = 0, world = 1, num_sms = 148;
     cudaStream_t stream = nullptr;
+    // host-residency loads of C = A*A upload B.col in chunks on a copy stream
+    // so the next FLOP pass can start on the tiles whose entries have landed
+    cudaStream_t cstream = nullptr, fstream = nullptr;
+    static constexpr int kChunks = 8;
+    cudaEvent_t ev_rpt = nullptr, ev_chunk[kChunks] = {}, ev_fdone = nullptr;
+    int64_t chunk_tile_end[kChunks] = {};
+    int n_chunks = 0;
+    bool pending_upload = false;
     static constexpr int kSide = 4;
     cudaStream_t side[kSide] = {};        // symbolic tiers, concurrent with the heavy rows
     cudaEvent_t fork = nullptr, join[kSide] = {};
@@ -201,10 +209,21 @@ int ensure_dev(spnnz_gpu_ctx* c) {
     return SPNNZ_OK;
 }
 
-int check_ctx(spnnz_gpu_ctx* c, bool need_loaded = true) {
+// The main stream waits for a chunked upload still in flight (every entry
+// point but the prediction pipeline, which overlaps its FLOP pass with it).
+int settle_upload(spnnz_gpu_ctx* c) {
+    if (!c->pending_upload) return SPNNZ_OK;
+    CU(cudaStreamWaitEvent(c->stream, c->ev_rpt, 0));
+    for (int k = 0; k < c->n_chunks; ++k) CU(cudaStreamWaitEvent(c->stream, c->ev_chunk[k], 0));
+    c->pending_upload = false;
+    return SPNNZ_OK;
+}
+
+int check_ctx(spnnz_gpu_ctx* c, bool need_loaded = true, bool settle = true) {
     if (!c) return set_err(SPNNZ_EINVAL, "null context");
     RC(ensure_dev(c));
     if (need_loaded && !c->loaded) return set_err(SPNNZ_ESTATE, "no matrices loaded");
+    if (settle) RC(settle_upload(c));
     return SPNNZ_OK;
 }
 
@@ -413,6 +432,35 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
     RC(c->tile_max.ensure(tiles + 1));
     RC(c->deg.ensure(std::max<int64_t>(c->b_rows, 1)));
     FlopScratch s{c->tile_x.p, c->tile_carry.p, c->tile_total.p, c->tile_max.p};
+    if (c->pending_upload && stream == c->stream) {
+        // B.col still landing: degrees and the partition need only B.rpt; the
+        // tiles of each chunk run on fstream as soon as the chunk is in; the
+        // fixup and everything after wait for all of it
+        CU(cudaStreamWaitEvent(c->stream, c->ev_rpt, 0));
+        CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, stream));
+        CU(launch_flop_partition(a, s, stream));
+        CU(cudaEventRecord(c->ev_fdone, stream));
+        CU(cudaStreamWaitEvent(c->fstream, c->ev_fdone, 0));
+        int64_t t_prev = 0;
+        const int64_t first_tile = a.base / kFlopTile;
+        for (int k = 0; k < c->n_chunks; ++k) {
+            int64_t t_end = c->chunk_tile_end[k] >= a.base + a.nnz
+                                ? tiles
+                                : c->chunk_tile_end[k] / kFlopTile - first_tile;
+            t_end = std::max<int64_t>(std::min<int64_t>(t_end, tiles), t_prev);
+            if (k + 1 == c->n_chunks) t_end = tiles;
+            CU(cudaStreamWaitEvent(c->fstream, c->ev_chunk[k], 0));
+            if (t_end > t_prev)
+                CU(launch_flop_tiles(a, c->deg.p, c->b_rpt.p, s, c->flop.p, t_prev, t_end, c->fstream, pred));
+            t_prev = t_end;
+        }
+        CU(cudaEventRecord(c->ev_fdone, c->fstream));
+        CU(cudaStreamWaitEvent(c->stream, c->ev_fdone, 0));
+        RC(settle_upload(c));
+        CU(launch_flop_fixup(a, s, c->flop.p, c->totals.p, stream, pred));
+        *launches += a.rows ? 3 + c->n_chunks : 0;
+        return SPNNZ_OK;
+    }
     CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, stream));
     CU(launch_flop_partition(a, s, stream));
     CU(launch_flop(a, c->deg.p, c->b_rpt.p, s, c->flop.p, c->totals.p, stream, pred));
@@ -569,6 +617,7 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
         ev_record(c, 5);
         c->ev_order = 0;
     } else {
+        RC(settle_upload(c));  // the symbolic pass reads B first here
         ev_record(c, 0);
         if (draw) {
             CU(launch_sample(seed, c->a_rows, n, c->samples.p, c->stream));
@@ -653,6 +702,12 @@ int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz
     for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     for (int i = 0; i < spnnz_gpu_ctx::kSide && e == cudaSuccess; ++i)
         e = cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->fstream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_rpt, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fdone, cudaEventDisableTiming);
+    for (int i = 0; i < spnnz_gpu_ctx::kChunks && e == cudaSuccess; ++i)
+        e = cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
     for (int i = 0; i < spnnz_gpu_ctx::kSide && e == cudaSuccess; ++i)
         e = cudaEventCreateWithFlags(&c->join[i], cudaEventDisableTiming);
@@ -686,6 +741,8 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     if (!c) return SPNNZ_OK;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->cstream) cudaStreamSynchronize(c->cstream);
+    if (c->fstream) cudaStreamSynchronize(c->fstream);
     if (c->comm) nccl().CommDestroy(c->comm);
     for (auto* b : {&c->b_rpt, &c->a_rpt, &c->flop, &c->out64, &c->heavy_unit_off,
                     &c->heavy_eoff, &c->heavy_foff, &c->heavy_epre, &c->heavy_eb0, &c->heavy_flops})
@@ -718,6 +775,12 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
         if (c->join[i]) cudaEventDestroy(c->join[i]);
     }
     if (c->fork) cudaEventDestroy(c->fork);
+    for (auto ev : c->ev_chunk)
+        if (ev) cudaEventDestroy(ev);
+    if (c->ev_rpt) cudaEventDestroy(c->ev_rpt);
+    if (c->ev_fdone) cudaEventDestroy(c->ev_fdone);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
+    if (c->fstream) cudaStreamDestroy(c->fstream);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return SPNNZ_OK;
@@ -800,8 +863,32 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
     c->b_nnz = b_nnz;
     RC(c->b_rpt.ensure(int64_t(bv->rows) + 1));
     RC(c->b_col.ensure(std::max<int64_t>(b_nnz, 1)));
-    CU(cudaMemcpyAsync(c->b_rpt.p, bv->rpt, 8 * (size_t(bv->rows) + 1), kind, c->stream));
-    if (b_nnz) CU(cudaMemcpyAsync(c->b_col.p, bv->col, 4 * size_t(b_nnz), kind, c->stream));
+    const bool chunked = residency == SPNNZ_HOST && same && b_nnz >= (int64_t(1) << 24);
+    c->n_chunks = 0;
+    if (!chunked) {
+        CU(cudaMemcpyAsync(c->b_rpt.p, bv->rpt, 8 * (size_t(bv->rows) + 1), kind, c->stream));
+        if (b_nnz) CU(cudaMemcpyAsync(c->b_col.p, bv->col, 4 * size_t(b_nnz), kind, c->stream));
+    } else {
+        // copy stream: B.rpt, then B.col in kChunks pieces (cut at FLOP-tile
+        // multiples), one event each; the main stream waits on them lazily
+        CU(cudaEventRecord(c->ev_rpt, c->stream));  // after whatever the main stream holds
+        CU(cudaStreamWaitEvent(c->cstream, c->ev_rpt, 0));
+        CU(cudaMemcpyAsync(c->b_rpt.p, bv->rpt, 8 * (size_t(bv->rows) + 1), kind, c->cstream));
+        CU(cudaEventRecord(c->ev_rpt, c->cstream));
+        int64_t prev = 0;
+        for (int k = 0; k < spnnz_gpu_ctx::kChunks; ++k) {
+            int64_t end = b_nnz * (k + 1) / spnnz_gpu_ctx::kChunks;
+            end = k + 1 == spnnz_gpu_ctx::kChunks ? b_nnz : (end / kFlopTile) * kFlopTile;
+            if (end > prev)
+                CU(cudaMemcpyAsync(c->b_col.p + prev, bv->col + prev, 4 * size_t(end - prev), kind,
+                                   c->cstream));
+            CU(cudaEventRecord(c->ev_chunk[k], c->cstream));
+            c->chunk_tile_end[k] = end;  // absolute entry end; tiles resolved per shard below
+            prev = end;
+        }
+        c->n_chunks = spnnz_gpu_ctx::kChunks;
+        c->pending_upload = true;
+    }
 
     DevCsr v;
     v.rows = c->row_hi - c->row_lo;
@@ -843,7 +930,7 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
 }
 
 int spnnz_gpu_shard(spnnz_gpu_ctx* c, int32_t* lo, int32_t* hi, int32_t* rows) {
-    RC(check_ctx(c));
+    RC(check_ctx(c, true, false));  // host-side facts only
     if (lo) *lo = c->row_lo;
     if (hi) *hi = c->row_hi;
     if (rows) *rows = c->a_rows;
@@ -1080,7 +1167,7 @@ int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, boo
 int spnnz_gpu_run_prediction(spnnz_gpu_ctx* c, uint64_t seed, double fraction, int64_t cap,
                              spnnz_report* rep, int64_t* row_ceil, double* row_real,
                              int32_t* sample_rows, int residency) {
-    RC(check_ctx(c));
+    RC(check_ctx(c, true, false));  // the pipeline overlaps a pending upload
     RC(dims_ok(c, "compute_flop"));
     int64_t n = 0;
     double p = 0;
@@ -1097,7 +1184,7 @@ int spnnz_gpu_run_prediction(spnnz_gpu_ctx* c, uint64_t seed, double fraction, i
 int spnnz_gpu_run_prediction_with_plan(spnnz_gpu_ctx* c, const int32_t* rows, int64_t n, double p,
                                        int rows_residency, spnnz_report* rep, int64_t* row_ceil,
                                        double* row_real, int out_residency) {
-    RC(check_ctx(c));
+    RC(check_ctx(c, true, false));  // the pipeline overlaps a pending upload
     RC(dims_ok(c, "compute_flop"));
     const int32_t* d_rows = nullptr;
     RC(check_rows(c, rows, n, rows_residency, "sampled_symbolic", &d_rows));

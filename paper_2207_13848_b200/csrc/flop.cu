@@ -163,7 +163,8 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
        const uint16_t* __restrict__ bdeg, const int64_t* __restrict__ brpt, int32_t m,
        int64_t base, int64_t nnz, const int32_t* __restrict__ tile_row,
        int64_t* __restrict__ flop, long long* __restrict__ tile_lead,
-       long long* __restrict__ tile_total, long long* __restrict__ tile_max, PredOut pred) {
+       long long* __restrict__ tile_total, long long* __restrict__ tile_max, PredOut pred,
+       int64_t t0) {
     constexpr int TILE = BLOCK * V, NW = BLOCK / 32;
     static_assert(TILE == kFlopTile && V == 16, "tile size");
     __shared__ uint32_t s_start[TILE / 32];  // bit i: an owned non-empty row starts at entry i
@@ -172,7 +173,7 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
     __shared__ long long s_red[NW];
 
     const uint64_t first = policy_evict_first(), last = policy_evict_last();
-    const int64_t t = blockIdx.x;
+    const int64_t t = t0 + blockIdx.x;
     const int64_t ts = tile_start(base, nnz, t), te = tile_start(base, nnz, t + 1);
     const int n = static_cast<int>(te - ts);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -524,28 +525,43 @@ cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStr
     return cudaGetLastError();
 }
 
+cudaError_t launch_flop_tiles(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt,
+                              const FlopScratch& s, int64_t* flop, int64_t t_begin, int64_t t_end,
+                              cudaStream_t stream, const PredOut& pred) {
+    if (t_end <= t_begin) return cudaSuccess;
+    const unsigned g = static_cast<unsigned>(t_end - t_begin);
+    if (pred.on())
+        k_flop<kFlopBlock, kFlopIpt, true><<<g, kFlopBlock, 0, stream>>>(
+            a.rpt, a.col, bdeg, brpt, a.rows, a.base, a.nnz, s.tile_x, flop, s.tile_carry,
+            s.tile_total, s.tile_max, pred, t_begin);
+    else
+        k_flop<kFlopBlock, kFlopIpt, false><<<g, kFlopBlock, 0, stream>>>(
+            a.rpt, a.col, bdeg, brpt, a.rows, a.base, a.nnz, s.tile_x, flop, s.tile_carry,
+            s.tile_total, s.tile_max, pred, t_begin);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flop_fixup(const DevCsr& a, const FlopScratch& s, int64_t* flop, long long* totals,
+                              cudaStream_t stream, const PredOut& pred) {
+    const int64_t tiles = flop_tiles(a);
+    if (tiles == 0) return cudaSuccess;
+    constexpr int FB = 256;
+    const unsigned gf = static_cast<unsigned>((tiles + FB - 1) / FB);
+    if (pred.on())
+        k_flop_fixup<FB, true><<<gf, FB, 0, stream>>>(s.tile_x, tiles, s.tile_carry, s.tile_total,
+                                                      s.tile_max, flop, totals, pred);
+    else
+        k_flop_fixup<FB, false><<<gf, FB, 0, stream>>>(s.tile_x, tiles, s.tile_carry, s.tile_total,
+                                                       s.tile_max, flop, totals, pred);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_flop(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt,
                         const FlopScratch& s, int64_t* flop, long long* totals,
                         cudaStream_t stream, const PredOut& pred) {
-    const int64_t tiles = flop_tiles(a);
-    if (tiles == 0) return cudaSuccess;
-    const unsigned g = static_cast<unsigned>(tiles);
-    constexpr int FB = 256;
-    const unsigned gf = static_cast<unsigned>((tiles + FB - 1) / FB);
-    if (pred.on()) {
-        k_flop<kFlopBlock, kFlopIpt, true><<<g, kFlopBlock, 0, stream>>>(
-            a.rpt, a.col, bdeg, brpt, a.rows, a.base, a.nnz, s.tile_x, flop, s.tile_carry,
-            s.tile_total, s.tile_max, pred);
-        k_flop_fixup<FB, true><<<gf, FB, 0, stream>>>(s.tile_x, tiles, s.tile_carry, s.tile_total,
-                                                      s.tile_max, flop, totals, pred);
-    } else {
-        k_flop<kFlopBlock, kFlopIpt, false><<<g, kFlopBlock, 0, stream>>>(
-            a.rpt, a.col, bdeg, brpt, a.rows, a.base, a.nnz, s.tile_x, flop, s.tile_carry,
-            s.tile_total, s.tile_max, pred);
-        k_flop_fixup<FB, false><<<gf, FB, 0, stream>>>(s.tile_x, tiles, s.tile_carry, s.tile_total,
-                                                       s.tile_max, flop, totals, pred);
-    }
-    return cudaGetLastError();
+    const cudaError_t e = launch_flop_tiles(a, bdeg, brpt, s, flop, 0, flop_tiles(a), stream, pred);
+    if (e != cudaSuccess) return e;
+    return launch_flop_fixup(a, s, flop, totals, stream, pred);
 }
 
 cudaError_t launch_sampled_flop(const int64_t* flop, int32_t row_lo, int32_t local_rows,

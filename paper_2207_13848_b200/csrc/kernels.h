@@ -77,6 +77,13 @@ cudaError_t launch_predict_redo(const int64_t* flop, int64_t m, const PredOut& p
 cudaError_t launch_flop(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt,
                         const FlopScratch& s, int64_t* flop, long long* totals,
                         cudaStream_t stream, const PredOut& pred = PredOut());
+// The same in two steps: tiles [t_begin, t_end) (any order, any streams),
+// then the fixup once every tile is done.
+cudaError_t launch_flop_tiles(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt,
+                              const FlopScratch& s, int64_t* flop, int64_t t_begin, int64_t t_end,
+                              cudaStream_t stream, const PredOut& pred = PredOut());
+cudaError_t launch_flop_fixup(const DevCsr& a, const FlopScratch& s, int64_t* flop, long long* totals,
+                              cudaStream_t stream, const PredOut& pred = PredOut());
 
 // -------------------------------------------------------------- sampler
 cudaError_t launch_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* rows,
