@@ -244,14 +244,13 @@ __device__ __forceinline__ void item_products(const SymArgs& g, const SymScratch
 }
 
 // ---- 1. per-unit histogram over column ranges, added to the bucket counts
-template <bool PRIV>
 __global__ void __launch_bounds__(kHB) k_heavy_count(SymArgs g, SymScratch sc, int64_t first,
                                                      int64_t count, int R, int wshift) {
-    constexpr int NW = PRIV ? kHW : 1, RM = PRIV ? kPrivRanges : kMaxRanges;
+    constexpr int NW = 1, RM = kMaxRanges;  // R > kPrivRanges: one shared histogram
     __shared__ int s_off[kHB + 1];
     __shared__ int64_t s_b0[kHB];
     __shared__ int s_hist[NW][RM];
-    const int w = PRIV ? threadIdx.x >> 5 : 0;
+    constexpr int w = 0;
     const long long units = sc.heavy_meta[0];
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit un = find_unit_block(sc, count, u);
@@ -301,10 +300,9 @@ __global__ void k_heavy_offsets(SymScratch sc, int64_t count, int R) {
 
 // ---- 3. place: counting-sort each unit by range in shared memory, write the
 // sorted runs to their bucket slices (coalesced)
-template <bool PRIV>
 __global__ void __launch_bounds__(kHB) k_heavy_place(SymArgs g, SymScratch sc, int64_t first,
                                                      int64_t count, int R, int wshift) {
-    constexpr int NW = PRIV ? kHW : 1, RM = PRIV ? kPrivRanges : kMaxRanges;
+    constexpr int NW = 1, RM = kMaxRanges;  // R > kPrivRanges: one shared histogram
     __shared__ int s_off[kHB + 1];
     __shared__ int64_t s_b0[kHB];
     // dynamic: dst_base[RM] (int64: bucket position of the unit's first key of
@@ -316,7 +314,7 @@ __global__ void __launch_bounds__(kHB) k_heavy_place(SymArgs g, SymScratch sc, i
     int32_t* s_out = s_in + kHeavyUnitProducts;
     int (*s_hist)[RM] = reinterpret_cast<int (*)[RM]>(s_out + kHeavyUnitProducts);
     int* s_offs = reinterpret_cast<int*>(s_hist + NW);
-    const int w = PRIV ? threadIdx.x >> 5 : 0;
+    constexpr int w = 0;
     const int lane = threadIdx.x & 31;
     const long long units = sc.heavy_meta[0];
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
@@ -1127,10 +1125,7 @@ __global__ void k_heavy_clean(SymScratch sc, int64_t slot_words) {
 
 int sort_smem(int R) { return int(2 * kHeavyUnitProducts * 4 + ((kHW + 1) * R + 1) * 4); }
 
-int place_smem(bool priv) {
-    const int nw = priv ? kHW : 1, rm = priv ? kPrivRanges : kMaxRanges;
-    return int(rm * 8 + 2 * kHeavyUnitProducts * 4 + nw * rm * 4 + (rm + 1) * 4);
-}
+int place_smem() { return int(kMaxRanges * 8 + 2 * kHeavyUnitProducts * 4 + kMaxRanges * 4 + (kMaxRanges + 1) * 4); }
 
 }  // namespace
 
@@ -1185,8 +1180,8 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
                              (1 << kTaskSpanShift) / 8);
         cudaFuncSetAttribute(k_heavy_run_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kSGroups * kSSlots * 4);
-        cudaFuncSetAttribute(k_heavy_place<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             place_smem(false));
+        cudaFuncSetAttribute(k_heavy_place, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             place_smem());
         cudaFuncSetAttribute(k_heavy_sort_units, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              sort_smem(kPrivRanges));
         cudaFuncSetAttribute(k_heavy_intervals, cudaFuncAttributeMaxDynamicSharedMemorySize, kIvSmem);
@@ -1214,9 +1209,9 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
                 args, s, first, R, geo.wshift, geo.wwords);
             k_heavy_run_small<<<sms * 3, kSG * kSGroups, kSGroups * kSSlots * 4, stream>>>(args, s, first, R);
         } else {
-            k_heavy_count<false><<<sms * 8, kHB, 0, stream>>>(args, s, first, count, R, geo.wshift);
+            k_heavy_count<<<sms * 8, kHB, 0, stream>>>(args, s, first, count, R, geo.wshift);
             k_heavy_offsets<<<items, 256, 0, stream>>>(s, count, R);
-            k_heavy_place<false><<<sms * 2, kHB, place_smem(false), stream>>>(args, s, first,
+            k_heavy_place<<<sms * 2, kHB, place_smem(), stream>>>(args, s, first,
                                                                              count, R, geo.wshift);
             k_heavy_plan<<<items, 128, 0, stream>>>(s, count, R, geo.wshift, s.heavy_task_cap);
             k_heavy_run<512, kRunBuckets><<<sms * 3, 512, (1 << kTaskSpanShift) / 8, stream>>>(
