@@ -42,7 +42,13 @@ using namespace sym;
 constexpr int kHB = 256;                  // block of the unit passes
 constexpr int kHW = kHB / 32;             // warps per unit block
 constexpr int kSpanShift = 20;            // R == 1: one span of <= 2^20 columns (128 KB)
-constexpr int kTaskSpanShift = 19;        // R > 1: task spans of <= 2^19 columns (64 KB)
+#ifndef SPNNZ_SPAN_SHIFT
+#define SPNNZ_SPAN_SHIFT 19
+#endif
+#ifndef SPNNZ_RUN_GRID
+#define SPNNZ_RUN_GRID 3
+#endif
+constexpr int kTaskSpanShift = SPNNZ_SPAN_SHIFT;  // R > 1: task spans of <= 2^19 columns (64 KB)
 constexpr int kPrivRanges = 256;          // per-warp histograms up to this R
 constexpr int kMaxRanges = 4096;          // B.cols < 2^31 with W = 2^19
 constexpr int64_t kTaskProducts = 131072;
@@ -1205,7 +1211,7 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
         if (geo.unit_sorted) {
             k_heavy_sort_units<<<sms * 6, kHB, sort_smem(R), stream>>>(args, s, first, count, R, geo.wshift);
             k_heavy_plan_units<<<items, kPrivRanges, 0, stream>>>(s, count, R, s.heavy_task_cap);
-            k_heavy_run_units<512><<<sms * 3, 512, (1 << kTaskSpanShift) / 8, stream>>>(
+            k_heavy_run_units<512><<<sms * SPNNZ_RUN_GRID, 512, (1 << kTaskSpanShift) / 8, stream>>>(
                 args, s, first, R, geo.wshift, geo.wwords);
             k_heavy_run_small<<<sms * 3, kSG * kSGroups, kSGroups * kSSlots * 4, stream>>>(args, s, first, R);
         } else {
