@@ -605,3 +605,61 @@ def test_cpp_dropin_header():
         subprocess.run(["make", "-C", root, "build/test_dropin"], check=True, capture_output=True)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+# ------------------------------------------------------------------ fuzzing
+def _fuzz_matrix(rng, rows, cols, kind):
+    """Random CSR with sorted distinct columns: uniform, skewed (a few hub
+    rows with thousands of entries) or banded."""
+    out = []
+    for i in range(rows):
+        if kind == "skewed":
+            k = int(rng.integers(2000, 6000)) if rng.random() < 0.01 else int(rng.integers(0, 12))
+        elif kind == "banded":
+            k = int(rng.integers(1, 30))
+        else:
+            k = int(rng.integers(0, 40))
+        k = min(k, cols)
+        if kind == "banded":
+            c0 = max(0, min(cols - k, i * cols // max(rows, 1) - k // 2))
+            out.append(np.arange(c0, c0 + k))
+        else:
+            out.append(np.sort(rng.choice(cols, size=k, replace=False)))
+    return csr(rows, cols, [r.tolist() for r in out])
+
+
+@pytest.mark.parametrize("case", range(36))
+def test_fuzz_pipeline_vs_oracle(oracle, case, monkeypatch):
+    """Random shapes (square and rectangular, narrow to 2^26 columns),
+    uniform / skewed / banded rows, random heavy-path and pipeline options:
+    per-row FLOP, exact NNZ, sampled totals and the ceil view equal the
+    oracle's."""
+    rng = np.random.default_rng(1000 + case)
+    kinds = ["uniform", "skewed", "banded"]
+    m = int(rng.integers(200, 3000))
+    k = int(rng.integers(200, 3000))
+    n = int(rng.choice([64, 3000, 1 << 16, 1 << 21, 1 << 26]))
+    a = _fuzz_matrix(rng, m, k, kinds[case % 3])
+    b = _fuzz_matrix(rng, k, min(n, 1 << 16) if kinds[(case + 1) % 3] == "banded" else n, kinds[(case + 1) % 3])
+    b = csr(b.rows, n, [b.col[b.rpt[i]:b.rpt[i + 1]].tolist() for i in range(b.rows)])
+    if case % 4 == 1:
+        monkeypatch.setenv("SPNNZ_HEAVY_INTERVALS", "1")
+    if case % 4 == 2:
+        monkeypatch.setenv("SPNNZ_FUSED_PREDICT", "1")
+    if case % 4 == 3:
+        monkeypatch.setenv("SPNNZ_HEAVY_BATCH_PRODUCTS", "50000")
+    q = Predictor(0)
+    q.load(a, b)
+    prof = q.compute_flop()
+    f, F, mx = oracle.compute_flop(a, b)
+    assert (prof.flop_per_row == f).all() and prof.total_flop == F and prof.max_flop_row == mx
+    ex = q.exact_symbolic()
+    nnz, Z = oracle.exact_symbolic(a, b, f, mx)
+    assert (ex.nnz_per_row == nnz).all() and ex.total_nnz == Z
+    seed, frac = int(rng.integers(1, 1 << 40)), float(rng.choice([0.01, 0.1, 0.5]))
+    rep = q.run_prediction(seed, SamplePolicy(frac, UNCAPPED))
+    o, _, oceil, oreal = oracle.run_prediction(a, b, seed, frac, UNCAPPED)
+    assert rep.stats.sampled_flop == o.sampled_flop and rep.stats.sampled_nnz == o.sampled_nnz
+    assert rep.predicted_cr == o.predicted_cr and rep.z2_star == o.z2_star
+    assert (rep.predicted_row_nnz_ceil == oceil).all() and (rep.predicted_row_nnz == oreal).all()
+    q.close()
