@@ -396,8 +396,13 @@ def run_ours(args, rank, world, local):
         et = torch.tensor([ems], dtype=torch.float64, device="cuda")
         if dist:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        # whole-job bytes: every rank uploads B (replicated) and its A shard,
+        # and reads back its rows' view (+ the 8 totals)
+        hd = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(hd, op=dist.ReduceOp.SUM)
         e2e = {"value": a.nnz() / (float(et.item()) * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "h2d_bytes_per_step": int(hd[0].item()), "d2h_bytes_per_step": int(hd[1].item()),
                "ms_per_step": float(et.item()),
                "path": "spnnz_gpu_load(host CSR, pinned) + spnnz_gpu_run_prediction(host ceil view)"}
         P.load(a, None if b is a else b)
