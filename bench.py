@@ -292,6 +292,7 @@ def run_ours(args, rank, world, local):
         nccl_id = obj[0]
     P = Predictor(local, rank, world, nccl_id)
     P.load(a, None if b is a else b)
+    P.synchronize()  # the upload has landed: every step below runs on resident inputs
     policy = SamplePolicy(info["fraction"], args.cap)
     m_local = P.local_rows
     nnz_local = int(a.rpt[P.row_hi] - a.rpt[P.row_lo])
