@@ -245,9 +245,9 @@ def run_reference_arm(args, rank, world):
 
 # ------------------------------------------------------------- GPU side
 def flop_pass_bytes(m_local, nnz_local, k_rows):
-    """Algorithmic bytes of one fused FLOP + predict pass:
-    A.rpt + A.col + B.rpt once + flop written + the ceil view written."""
-    return 8 * (m_local + 1) + 4 * nnz_local + 8 * (k_rows + 1) + 8 * m_local + 8 * m_local
+    """Algorithmic bytes of one FLOP pass: A.rpt + A.col +
+    B.rpt once + flop written."""
+    return 8 * (m_local + 1) + 4 * nnz_local + 8 * (k_rows + 1) + 8 * m_local
 
 
 def load_peaks():
@@ -365,8 +365,16 @@ def run_ours(args, rank, world, local):
     peak, peak_kind = load_peaks()
     fbytes = flop_pass_bytes(m_local, nnz_local, (b.rows if b is not a else a.rows))
     achieved = fbytes / (phase["flop"] * 1e-3) / 1e9 if phase["flop"] > 0 else 0.0
-    traffic, _ = load_traffic()
+    traffic, tmeta = load_traffic()
+    if args.config != 5:  # the committed ncu capture is of the config-5 workload
+        traffic = None
     pbytes = 16 * m_local
+    # sampled symbolic: B_samp = sum_s 16 + 20 len(A_row) + 4 flop_row,
+    # dominated by the B.col reads; its bound is shared-memory atomics and the
+    # latency of the per-row / per-range phases, reported for transparency
+    plan = P.make_sample_plan(a.rows, info["seed"], policy)
+    lens = (a.rpt[plan.sample_rows.astype(np.int64) + 1] - a.rpt[plan.sample_rows.astype(np.int64)])
+    sbytes = 16 * plan.sample_num + 20 * int(lens.sum()) + 4 * int(rep.stats.sampled_flop)
 
     # end to end through the host-buffer API: H2D of the CSR + D2H of the
     # per-row prediction, every step
@@ -448,8 +456,7 @@ def run_ours(args, rank, world, local):
                                       "1 NCCL all-reduce per step",
                        "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps"},
             "roofline": {"bound": "hbm",
-                         "kernel": "fused FLOP + predict pass (k_degree + k_flop_partition + "
-                                   "k_flop + k_flop_fixup; writes flop and the ceil view)",
+                         "kernel": "FLOP pass (k_degree + k_flop_partition + k_flop + k_flop_fixup)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes": fbytes, "avg_ms": phase["flop"],
@@ -462,16 +469,25 @@ def run_ours(args, rank, world, local):
                          "gather_peak_per_s": 287.6e9,
                          "gather_frac": (nnz_local / (phase["flop"] * 1e-3) / 287.6e9)
                          if phase["flop"] else 0.0},
-            # the predict pass the north star names is fused into the FLOP
-            # pass: its 8 B/row ceil write is in `roofline`
-            "roofline_predict": ({"fused": "into the FLOP pass (8 B/row ceil view written "
-                                           "as each row's flop completes; no re-read)"}
+            # the other HBM-streaming kernel the north star names (fused into
+            # the FLOP pass only under SPNNZ_FUSED_PREDICT=1)
+            "roofline_predict": ({"fused": "into the FLOP pass (SPNNZ_FUSED_PREDICT=1)"}
                                  if not phase["predict"] else
                                  {"bound": "hbm", "kernel": "k_predict (ceil view)",
                                   "achieved": pbytes / (phase["predict"] * 1e-3) / 1e9,
                                   "peak": peak, "unit": "GB/s",
                                   "frac": pbytes / (phase["predict"] * 1e-3) / 1e9 / peak,
                                   "algorithmic_bytes": pbytes, "avg_ms": phase["predict"]}),
+            "roofline_symbolic": {"bound": "shared-memory atomics / phase latency (not HBM)",
+                                  "kernel": "sampled symbolic (bins 1-5 + heavy rows)",
+                                  "products": int(rep.stats.sampled_flop),
+                                  "products_per_s": rep.stats.sampled_flop / (phase["symbolic"] * 1e-3)
+                                  if phase["symbolic"] else 0.0,
+                                  "algorithmic_bytes": sbytes,
+                                  "achieved": sbytes / (phase["symbolic"] * 1e-3) / 1e9 if phase["symbolic"] else 0.0,
+                                  "peak": peak, "unit": "GB/s",
+                                  "frac": sbytes / (phase["symbolic"] * 1e-3) / 1e9 / peak if phase["symbolic"] else 0.0,
+                                  "avg_ms": phase["symbolic"]},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "phases_ms": phase,
             "report": {"F": rep.total_flop, "f_star": rep.stats.sampled_flop,
