@@ -170,7 +170,7 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
     __shared__ uint32_t s_start[TILE / 32];  // bit i: an owned non-empty row starts at entry i
     __shared__ int32_t s_rowat[TILE];        // ... and its id (read only where the bit is set)
     __shared__ Carry s_wc[NW];
-    __shared__ long long s_red[NW];
+    __shared__ long long s_red[NW], s_red2[NW];
 
     const uint64_t first = policy_evict_first(), last = policy_evict_last();
     const int64_t t = t0 + blockIdx.x;
@@ -291,11 +291,23 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
             tile_lead[t] = all.v;  // no row starts in this tile
         }
     }
-    const long long bsum = block_sum_ll<BLOCK>(tsum, s_red);
-    const long long bmax = block_max_ll<BLOCK>(tmax, s_red);
-    if (tid == 0) {
-        tile_total[t] = bsum;
-        tile_max[t] = bmax;
+    // tile F and max in one pass: warp reductions, one shared slot pair per
+    // warp, warp 0 finishes both (the scan's barrier orders s_red's reuse)
+    tsum = warp_sum_ll(tsum);
+    tmax = warp_max_ll(tmax);
+    if (lane == 0) {
+        s_red[warp] = tsum;
+        s_red2[warp] = tmax;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        long long a = lane < NW ? s_red[lane] : 0, b = lane < NW ? s_red2[lane] : 0;
+        a = warp_sum_ll(a);
+        b = warp_max_ll(b);
+        if (lane == 0) {
+            tile_total[t] = a;
+            tile_max[t] = b;
+        }
     }
 }
 
