@@ -1172,8 +1172,9 @@ cudaError_t launch_heavy_flops(const SymArgs& args, const SymScratch& s, int64_t
 }
 
 cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sorted, int64_t first,
-                             int64_t count, int num_sms, cudaStream_t stream) {
+                             int64_t count, int num_sms, cudaStream_t stream, int64_t* launches) {
     if (count == 0) return cudaSuccess;
+    int64_t n = 0;  // kernels launched (memsets not counted)
     static unsigned attr_done = 0;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1199,11 +1200,13 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
     const unsigned items = static_cast<unsigned>(count);
     k_heavy_prep<<<1, kPrepBlock, 0, stream>>>(args, s, first, count);
     k_heavy_entries<<<items, 256, 0, stream>>>(args, s, first);
+    n += 2;
     if (sorted) {
         cudaMemsetAsync(s.heavy_bnd, 0, sizeof(int32_t) * s.heavy_bnd_cap, stream);
         k_heavy_bounds<<<sms * 8, kHB, 0, stream>>>(args, s);
         k_heavy_iplan<<<items, kHB, 0, stream>>>(args, s);
         k_heavy_intervals<<<sms * 2, kIvBlock, kIvSmem, stream>>>(args, s, first);
+        if (launches) *launches += n + 3;
         return cudaGetLastError();
     }
     if (R > 1) {
@@ -1214,12 +1217,14 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
             k_heavy_run_units<512><<<sms * SPNNZ_RUN_GRID, 512, (1 << kTaskSpanShift) / 8, stream>>>(
                 args, s, first, R, geo.wshift, geo.wwords);
             k_heavy_run_small<<<sms * 3, kSG * kSGroups, kSGroups * kSSlots * 4, stream>>>(args, s, first, R);
+            n += 4;
         } else {
             k_heavy_count<<<sms * 8, kHB, 0, stream>>>(args, s, first, count, R, geo.wshift);
             k_heavy_offsets<<<items, 256, 0, stream>>>(s, count, R);
             k_heavy_place<<<sms * 2, kHB, place_smem(), stream>>>(args, s, first,
                                                                              count, R, geo.wshift);
             k_heavy_plan<<<items, 128, 0, stream>>>(s, count, R, geo.wshift, s.heavy_task_cap);
+            n += 5;
             k_heavy_run<512, kRunBuckets><<<sms * 3, 512, (1 << kTaskSpanShift) / 8, stream>>>(
                 args, s, first, R, geo.wshift, geo.wwords);
         }
@@ -1228,8 +1233,10 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
             s, count, s.heavy_task_cap);
         k_heavy_run<1024, kRunItem><<<sms, 1024, (1 << kSpanShift) / 8, stream>>>(
             args, s, first, R, geo.wshift, geo.wwords);
+        n += 2;
     }
     k_heavy_clean<<<sms * 4, 256, 0, stream>>>(s, int64_t(geo.wwords));
+    if (launches) *launches += n + 1;
     return cudaGetLastError();
 }
 

@@ -196,7 +196,7 @@ cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_s
 // learns the count after a sync and sizes the batch's buffers).
 // sorted: B rows non-decreasing -> the interval path (no product buffer).
 cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sorted, int64_t first,
-                             int64_t count, int num_sms, cudaStream_t stream);
+                             int64_t count, int num_sms, cudaStream_t stream, int64_t* launches = nullptr);
 // Per heavy item in list order: out[i] = FLOP, out[count + i] = A-row length,
 // out[2 count + i] = boundary-table cells (batch planning when the heavy rows'
 // products exceed one batch's buffers).
