@@ -81,6 +81,25 @@ def test_flop_long_rows_and_empty_rows(P, oracle):
     assert (pr.flop_per_row == f).all() and pr.total_flop == F and pr.max_flop_row == mx
 
 
+def test_flop_tiles_owning_over_65535_rows(P, oracle):
+    """Tiles owning more than 2^16 rows (long runs of empty rows between
+    short ones): the row a start position belongs to is far from the tile's
+    first row."""
+    rng = np.random.default_rng(7)
+    m = 300_000
+    rows = [[] for _ in range(m)]
+    for r in sorted(rng.choice(m, 900, replace=False)):
+        rows[int(r)] = sorted(int(c) for c in rng.choice(5000, int(rng.integers(1, 6)), replace=False))
+    rows[0] = list(range(3000))  # the first tile: rows 0.. plus the sparse run
+    rows[m - 1] = list(range(4000, 4100))
+    a = csr(m, 5000, rows)
+    b = gen.uniform_len(5000, 5000, 0, 30, 12)
+    P.load(a, b)
+    pr = P.compute_flop()
+    f, F, mx = oracle.compute_flop(a, b)
+    assert (pr.flop_per_row == f).all() and pr.total_flop == F and pr.max_flop_row == mx
+
+
 # -------------------------------------------------------------- sampler
 def test_sampler_matches_reference(P, golden):
     for rec in golden["refkat"]["plans"]:
