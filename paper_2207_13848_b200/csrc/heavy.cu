@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kHB) k_heavy_place(SymArgs g, SymScratch sc, i
 // and written back to the unit's own window of the product buffer, with its
 // R + 1 range starts in heavy_utab; the per-(item, range) totals go to
 // heavy_rc for the planner.  A task then reads range r as one slice per unit.
-__global__ void __launch_bounds__(kHB) k_heavy_sort_units(SymArgs g, SymScratch sc, int64_t first,
+__global__ void __launch_bounds__(kHB, 6) k_heavy_sort_units(SymArgs g, SymScratch sc, int64_t first,
                                                           int64_t count, int R, int wshift) {
     __shared__ int s_off[kHB + 1];
     __shared__ int64_t s_b0[kHB];
@@ -448,10 +448,12 @@ __global__ void __launch_bounds__(kHB) k_heavy_sort_units(SymArgs g, SymScratch 
             if (lane == 31) s_offs[R] = incl;
         }
         __syncthreads();
+        // warp cursors become absolute positions in the sorted unit
+        for (int k = threadIdx.x; k < kHW * R; k += kHB) s_hist[k] += s_offs[k % R];
+        __syncthreads();
         for (int i = threadIdx.x; i < n; i += kHB) {  // same thread <-> key mapping as the histogram
             const int key = s_in[i];
-            const int r = key >> wshift;
-            s_out[s_offs[r] + atomicAdd(&s_hist[w * R + r], 1)] = key;
+            s_out[atomicAdd(&s_hist[w * R + (key >> wshift)], 1)] = key;
         }
         __syncthreads();
         int32_t* dst = sc.heavy_pbuf + sc.heavy_foff[un.item] + un.p0;
