@@ -96,9 +96,18 @@ cudaError_t launch_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* r
 constexpr int kNumBins = 7;
 constexpr int64_t kBin1Max = 32;     // warp, __match_any_sync dedup
 constexpr int64_t kBin2Max = 512;    // warp, 1024-slot smem hash per warp
-constexpr int64_t kBin3Max = 2048;   // 256-thread block, 4096-slot smem hash
-constexpr int64_t kBin4Max = 8192;   // 512-thread block, 16384-slot smem hash
-constexpr int64_t kBin5Max = 24576;  // 1024-thread block, 49152-slot smem hash
+#ifndef SPNNZ_BIN3_MAX
+#define SPNNZ_BIN3_MAX 2048
+#endif
+#ifndef SPNNZ_BIN4_MAX
+#define SPNNZ_BIN4_MAX 8192
+#endif
+#ifndef SPNNZ_BIN5_MAX
+#define SPNNZ_BIN5_MAX 24576
+#endif
+constexpr int64_t kBin3Max = SPNNZ_BIN3_MAX;  // 256-thread block, 4096-slot smem hash
+constexpr int64_t kBin4Max = SPNNZ_BIN4_MAX;  // 512-thread block, 16384-slot smem hash
+constexpr int64_t kBin5Max = SPNNZ_BIN5_MAX;  // 1024-thread block, 49152-slot smem hash
 constexpr int kHeavyBin = 6;         // heavier: units of kHeavyUnitProducts
 constexpr int kForeignBin = 7;       // row owned by another rank
 constexpr int kNoBin = 8;            // padding lane
