@@ -160,7 +160,15 @@ __device__ __forceinline__ long long ceil_of(long long f, double q) {
     return f < c ? f : c;
 }
 
+// Empty rows skip the division: 0 / cr is +0 for every accepted cr (> 0, +inf
+// included; NaN is rejected at the boundary), and __ddiv_rn sends a zero
+// dividend down its slow path (config 5: ~20 % empty rows, 72 -> 55 us for
+// the pass, tools/microbench/predict_bw.cu).
 __device__ __forceinline__ long long ceil_view(long long f, double cr, double* q_out) {
+    if (f == 0) {
+        *q_out = 0.0;
+        return 0;
+    }
     const double q = __ddiv_rn(static_cast<double>(f), cr);
     *q_out = q;
     return ceil_of(f, q);
