@@ -83,7 +83,8 @@ const char* spnnz_gpu_last_error(void);
 /* Fills 128 bytes with an ncclUniqueId (rank 0 calls it and broadcasts). */
 int spnnz_gpu_nccl_unique_id(void* id128);
 
-/* One context per GPU. world == 1 needs no NCCL (nccl_id may be NULL).
+/* One context per GPU. world == 1 needs no NCCL (nccl_id may be NULL; with
+ * an id the context joins a one-rank communicator and takes the NCCL path).
  * world > 1 with nccl_id == NULL creates a DETACHED shard: same partition,
  * no communicator, totals stay rank-local and the caller combines them. */
 int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz_gpu_ctx** out);

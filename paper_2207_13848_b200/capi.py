@@ -89,6 +89,24 @@ EXPORTED = tuple(_SIGS)
 _lib = None
 
 
+def _default_nccl() -> None:
+    """Points SPNNZ_NCCL_LIB at the pip-installed NCCL (the one torch loads),
+    so a communicator created before `import torch` does not pin an older
+    system libnccl.so.2 into the process."""
+    if os.environ.get("SPNNZ_NCCL_LIB"):
+        return
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        p = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            os.environ["SPNNZ_NCCL_LIB"] = p
+            return
+
+
 def lib() -> ctypes.CDLL:
     """The loaded product library; raises if it was not built."""
     global _lib
@@ -96,6 +114,7 @@ def lib() -> ctypes.CDLL:
         if not os.path.exists(LIB_PATH):
             raise SpnnzError(ECUDA, f"{LIB_PATH} not built (run `make` or "
                                     "__graft_entry__.build()); there is no CPU fallback")
+        _default_nccl()
         L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
         for name, (res, args) in _SIGS.items():
             f = getattr(L, name)

@@ -72,8 +72,17 @@ Nccl& nccl() {
     static Nccl n;
     static std::once_flag once;
     std::call_once(once, [] {
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        // The process's NCCL when one is loaded (e.g. torch's), else
+        // SPNNZ_NCCL_LIB (the Python layer points it at the pip-installed
+        // NCCL torch itself uses), else the loader's libnccl.so.2.  Local
+        // binding: loading an older system libnccl.so.2 first would make a
+        // later `import torch` bind to it and fail on newer NCCL symbols.
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h)
+            if (const char* p = getenv("SPNNZ_NCCL_LIB"))
+                if (*p) h = dlopen(p, RTLD_NOW | RTLD_LOCAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
         if (!h) {
             n.why = dlerror();
             return;
@@ -470,7 +479,7 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
 // Sum-all-reduce of totals[first, first + count) (default: F, f*, z*, Z), and
 // with_max the max of totals[kMax], across ranks.
 int allreduce_totals(spnnz_gpu_ctx* c, int first = 0, int count = 4, bool with_max = true) {
-    if (c->world == 1 || !c->comm) return SPNNZ_OK;
+    if (!c->comm) return SPNNZ_OK;
     Nccl& n = nccl();
     NC(n.GroupStart());
     NC(n.AllReduce(c->totals.p + first, c->totals.p + first, count, ncclInt64, ncclSum, c->comm,
@@ -713,13 +722,13 @@ int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz
     int rc = SPNNZ_OK;
     if (e != cudaSuccess) rc = set_err(SPNNZ_ECUDA, "create: %s", cudaGetErrorString(e));
     if (rc == SPNNZ_OK) rc = c->totals.ensure(kTotals);
-    if (rc == SPNNZ_OK && world > 1 && nccl_id) {
+    // Without an id a shard is detached: no communicator, totals stay
+    // rank-local and the caller combines them (sharding checks on one GPU).
+    // A one-rank communicator is allowed (it exercises the NCCL path).
+    if (rc == SPNNZ_OK && nccl_id) {
         Nccl& n = nccl();
         if (!n.loaded) {
             rc = set_err(SPNNZ_ENCCL, "NCCL unavailable: %s", n.why.c_str());
-        } else if (!nccl_id) {
-            // detached shard: no communicator, totals stay rank-local and the
-            // caller combines them (used to check sharding on one GPU)
         } else {
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof id);

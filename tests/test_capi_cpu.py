@@ -151,3 +151,18 @@ def test_cpp_header_accepts_reference_csr(tmp_path):
                         str(src), "-o", str(out), "-L", os.path.dirname(capi.LIB_PATH),
                         "-lspnnz_gpu"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_nccl_id_before_torch_import_keeps_torch_importable():
+    """Creating an NCCL id loads NCCL before torch: it must be the NCCL torch
+    itself uses (or bound locally), so a later `import torch` still resolves
+    its newer NCCL symbols."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2207_13848_b200.spnnz import Predictor\n"
+            "assert len(Predictor.nccl_unique_id()) == 128\n"
+            "import torch\n"
+            "print('ok', torch.__version__)\n") % ROOT
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]

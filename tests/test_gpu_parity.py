@@ -534,6 +534,32 @@ def test_config5_exact_properties(P):
     print(f"cfg5: Z={ex.total_nnz} eps1={e.eps1:+.4%} eps2={e.eps2:+.4%}")
 
 
+def test_nccl_one_rank_communicator_matches_plain_context():
+    """The NCCL path (dlopen of libnccl, ncclCommInitRank, the grouped
+    all-reduces on the pipeline stream) with a one-rank communicator gives
+    the communicator-free context's results exactly."""
+    a, b = gen.make_config(1)
+    plain = Predictor(0)
+    comm = Predictor(0, 0, 1, Predictor.nccl_unique_id())
+    try:
+        reps = []
+        for P_ in (plain, comm):
+            P_.load(a, b)
+            rep = P_.run_prediction(1, SamplePolicy(0.05, UNCAPPED))
+            ex = P_.exact_symbolic()
+            reps.append((rep, ex))
+        (r0, e0), (r1, e1) = reps
+        assert r1.total_flop == r0.total_flop and r1.max_flop_row == r0.max_flop_row
+        assert r1.stats.sampled_flop == r0.stats.sampled_flop
+        assert r1.stats.sampled_nnz == r0.stats.sampled_nnz
+        assert r1.predicted_cr == r0.predicted_cr and r1.z2_star == r0.z2_star
+        assert np.array_equal(r1.predicted_row_nnz_ceil, r0.predicted_row_nnz_ceil)
+        assert e1.total_nnz == e0.total_nnz and np.array_equal(e1.nnz_per_row, e0.nnz_per_row)
+    finally:
+        plain.close()
+        comm.close()
+
+
 def test_detached_shards_combine_to_single_gpu(oracle):
     """world > 1 without NCCL on one GPU: every rank's local pass, combined on
     the host, equals the 1-GPU result (bit-exact), for 2, 3 and 8 shards."""
