@@ -445,8 +445,8 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
         // tiles of each chunk run on fstream as soon as the chunk is in; the
         // fixup and everything after wait for all of it
         CU(cudaStreamWaitEvent(c->stream, c->ev_rpt, 0));
-        CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, stream));
-        CU(launch_flop_partition(a, s, stream));
+        int64_t nk = 0;
+        CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, stream, &a, &s, &nk));
         CU(cudaEventRecord(c->ev_fdone, stream));
         CU(cudaStreamWaitEvent(c->fstream, c->ev_fdone, 0));
         int64_t t_prev = 0;
@@ -466,13 +466,13 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
         CU(cudaStreamWaitEvent(c->stream, c->ev_fdone, 0));
         RC(settle_upload(c));
         CU(launch_flop_fixup(a, s, c->flop.p, c->totals.p, stream, pred));
-        *launches += a.rows ? 3 + c->n_chunks : 0;
+        *launches += a.rows ? nk + 1 + c->n_chunks : 0;
         return SPNNZ_OK;
     }
-    CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, stream));
-    CU(launch_flop_partition(a, s, stream));
+    int64_t nk = 0;
+    CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, stream, &a, &s, &nk));
     CU(launch_flop(a, c->deg.p, c->b_rpt.p, s, c->flop.p, c->totals.p, stream, pred));
-    *launches += a.rows ? 4 : 0;
+    *launches += a.rows ? nk + 2 : 0;
     return SPNNZ_OK;
 }
 

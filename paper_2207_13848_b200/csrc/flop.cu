@@ -3,17 +3,20 @@
 // hot loop :41-50), plus sampled_flop (:64-74).  A pattern SpMV y = A * deg(B).
 //
 // Decomposition ("nnz tiles"): A's nonzeros are cut into fixed tiles of
-// kFlopTile = 4096 entries aligned to absolute multiples of 4096, one
-// 256-thread block per tile, so hub rows and runs of empty rows cost the
-// same per entry.  A tile OWNS the rows that start inside it.  Per call:
+// kFlopTile = 2048 entries aligned to absolute multiples of 2048, one
+// 128-thread block per tile (10 resident per SM; 128 measured 3 % faster
+// than 256- and 64-thread tiles at configs 3 and 5), so hub rows and runs of
+// empty rows cost the same per entry.  A tile OWNS the rows that start inside it.  Per call:
 //   0. k_degree turns B.rpt into a uint16 row-length array with an escape
 //      value for rows of >= 65535 entries (2 B per B row: 34 MB at config 5,
 //      L2-resident under an evict_last policy -- the int64 pair
 //      B.rpt[k], B.rpt[k+1] is 134 MB and is not);
-//   1. k_flop_partition: first owned row of every tile (lower_bound in rpt);
+//   1. the tile partition (first owned row of every tile): each A row marks
+//      the tiles whose start falls inside it -- in the same pass over B.rpt
+//      when A.rpt is a view of it (C = A*A), else k_tile_rows over A.rpt;
 //   2. k_flop, per tile: each thread loads V = 16 consecutive A.col entries
 //      (16-byte evict_first loads) and issues their 16 degree gathers at once
-//      (evict_last); the tile's owned rows mark their starts in a 4096-bit
+//      (evict_last); the tile's owned rows mark their starts in a tile-sized
 //      shared bitmap; each thread sums its entries segment by segment in
 //      registers (rows inside the thread are written directly) and a
 //      block-wide segmented scan of (flag, partial, row) carries finishes the
@@ -32,25 +35,103 @@
 namespace spnnz_gpu {
 namespace {
 
-// deg16[k] = min(B.rpt[k+1] - B.rpt[k], 0xFFFF); 0xFFFF means "look the
-// exact length up in B.rpt" (rows with >= 65535 entries are rare).
-__global__ void k_degree(const int64_t* __restrict__ brpt, int64_t k_rows,
-                         uint16_t* __restrict__ deg) {
-    const uint64_t first = policy_evict_first(), last = policy_evict_last();
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < k_rows;
-         k += int64_t(gridDim.x) * blockDim.x) {
-        const long long lo = ld_stream_i64(reinterpret_cast<const long long*>(brpt) + k, first);
-        const long long hi = ld_stream_i64(reinterpret_cast<const long long*>(brpt) + k + 1, first);
-        const long long d = hi - lo;
-        st_keep_u16(deg + k, static_cast<uint16_t>(d < 0xFFFF ? d : 0xFFFF), last);
-    }
-}
-
 __device__ __forceinline__ int64_t tile_start(int64_t base, int64_t nnz, int64_t t) {
     const int64_t s = (base / kFlopTile + t) * kFlopTile;
     return s > base ? (s < base + nnz ? s : base + nnz) : base;
 }
 
+// Tile partition by streaming (one A row per thread instead of one binary
+// search per tile): tile_row[t] = first row r with rpt[r] >= tile_start(t),
+// i.e. row r >= 1 is the answer for the tiles whose start lies in
+// (rpt[r-1], rpt[r]].  For 1 <= t < tiles, tile_start(t) = (base/T + t) T
+// exactly, so those tiles are t in [rpt[r-1]/T + 1, rpt[r]/T] - base/T.
+// tile_row[0] = 0 and tile_row[tiles] = m are written by the caller's thread 0.
+struct TileMarks {
+    int32_t* tile_row = nullptr;  // null: no marking
+    int64_t a_off = 0;            // A row r is B row a_off + r (A.rpt is a view of B.rpt)
+    int32_t m = 0;
+    int64_t base = 0, tiles = 0;
+    // rows crossing no tile boundary (most) cost one shift-compare
+    __device__ __forceinline__ void row(int32_t r, long long lo, long long hi) const {
+        constexpr int kShift = __builtin_ctz(kFlopTile);
+        const uint64_t q0 = static_cast<uint64_t>(lo) >> kShift, q1 = static_cast<uint64_t>(hi) >> kShift;
+        if (q0 == q1) return;
+        const int64_t b0 = static_cast<int64_t>(static_cast<uint64_t>(base) >> kShift);
+        int64_t t0 = static_cast<int64_t>(q0) + 1 - b0, t1 = static_cast<int64_t>(q1) - b0;
+        if (t0 < 1) t0 = 1;
+        if (t1 > tiles - 1) t1 = tiles - 1;
+        for (int64_t t = t0; t <= t1; ++t) tile_row[t] = r;
+    }
+    __device__ __forceinline__ void ends() const {
+        tile_row[0] = 0;
+        tile_row[tiles] = m;
+    }
+};
+
+// deg16[k] = min(B.rpt[k+1] - B.rpt[k], 0xFFFF); 0xFFFF means "look the
+// exact length up in B.rpt" (rows with >= 65535 entries are rare).  With
+// marks on (C = A*A: A's row pointers are a view of B's), the same pass over
+// B.rpt also writes A's tile partition.
+__device__ __forceinline__ void degree_row(const TileMarks& mk, uint16_t* deg, int64_t k, long long lo,
+                                           long long hi) {
+    const long long d = hi - lo;
+    deg[k] = static_cast<uint16_t>(d < 0xFFFF ? d : 0xFFFF);
+    if (mk.tile_row && d > 0) {
+        const int64_t r = k + 1 - mk.a_off;  // A row whose start is B.rpt[k + 1]
+        if (r >= 1 && r <= mk.m) mk.row(static_cast<int32_t>(r), lo, hi);
+    }
+}
+
+// Four rows per thread per step: B.rpt[k .. k+4] as two 16-byte loads plus
+// one 8-byte load, all issued before any store, then one 8-byte store of the
+// four degrees (the marking branch would otherwise serialise the loads).
+__global__ void k_degree(const int64_t* __restrict__ brpt, int64_t k_rows,
+                         uint16_t* __restrict__ deg, TileMarks mk) {
+    const uint64_t first = policy_evict_first(), last = policy_evict_last();
+    if (mk.tile_row && blockIdx.x == 0 && threadIdx.x == 0) mk.ends();
+    const int64_t groups = k_rows >> 2;
+    for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < groups;
+         g += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t k = g << 2;
+        const int4 v0 = ld_stream_v4(reinterpret_cast<const int4*>(brpt + k), first);
+        const int4 v1 = ld_stream_v4(reinterpret_cast<const int4*>(brpt + k + 2), first);
+        const long long r4 = ld_stream_i64(reinterpret_cast<const long long*>(brpt) + k + 4, first);
+        long long r[5];
+        r[0] = (static_cast<long long>(static_cast<unsigned>(v0.y)) << 32) | static_cast<unsigned>(v0.x);
+        r[1] = (static_cast<long long>(static_cast<unsigned>(v0.w)) << 32) | static_cast<unsigned>(v0.z);
+        r[2] = (static_cast<long long>(static_cast<unsigned>(v1.y)) << 32) | static_cast<unsigned>(v1.x);
+        r[3] = (static_cast<long long>(static_cast<unsigned>(v1.w)) << 32) | static_cast<unsigned>(v1.z);
+        r[4] = r4;
+        uint64_t packed = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const long long d = r[j + 1] - r[j];
+            packed |= static_cast<uint64_t>(d < 0xFFFF ? d : 0xFFFF) << (16 * j);
+        }
+        asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(deg + k), "l"(packed), "l"(last));
+        if (mk.tile_row) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t row = k + j + 1 - mk.a_off;
+                if (r[j + 1] > r[j] && row >= 1 && row <= mk.m) mk.row(static_cast<int32_t>(row), r[j], r[j + 1]);
+            }
+        }
+    }
+    // the k_rows % 4 tail
+    const int64_t t = (groups << 2) + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (t < k_rows) degree_row(mk, deg, t, __ldg(&brpt[t]), __ldg(&brpt[t + 1]));
+}
+
+__global__ void k_tile_rows(const int64_t* __restrict__ arpt, TileMarks mk) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) mk.ends();
+    for (int64_t r = 1 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r <= mk.m;
+         r += int64_t(gridDim.x) * blockDim.x) {
+        const long long lo = __ldg(&arpt[r - 1]), hi = __ldg(&arpt[r]);
+        if (hi > lo) mk.row(static_cast<int32_t>(r), lo, hi);
+    }
+}
+
+#ifdef SPNNZ_BINARY_PARTITION  // A/B reference: one binary search per tile
 // tile_row[t] = first row whose start offset is >= tile_start(t); the last
 // tile also owns the trailing empty rows (tile_row[tiles] = m).
 __global__ void k_flop_partition(const int64_t* __restrict__ arpt, int32_t m, int64_t base,
@@ -70,6 +151,7 @@ __global__ void k_flop_partition(const int64_t* __restrict__ arpt, int32_t m, in
     }
     tile_row[t] = static_cast<int32_t>(lo);
 }
+#endif
 
 #ifndef SPNNZ_FLOP_GATHER
 #define SPNNZ_FLOP_GATHER 0
@@ -158,7 +240,7 @@ __device__ __forceinline__ Emit make_emit(const PredOut& p) {
 }
 
 template <int BLOCK, int V, bool PRED>
-__global__ void __launch_bounds__(BLOCK, 5)
+__global__ void __launch_bounds__(BLOCK, (1280 / BLOCK < 32 ? 1280 / BLOCK : 32))
 k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
        const uint16_t* __restrict__ bdeg, const int64_t* __restrict__ brpt, int32_t m,
        int64_t base, int64_t nnz, const int32_t* __restrict__ tile_row,
@@ -518,15 +600,42 @@ int64_t flop_tiles(const DevCsr& a) {
     return (end + kFlopTile - 1) / kFlopTile - a.base / kFlopTile;
 }
 
-cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, uint16_t* deg, int num_sms,
-                          cudaStream_t stream) {
-    if (k_rows == 0) return cudaSuccess;
-    int64_t grid = (k_rows + 255) / 256;
+static TileMarks tile_marks(const DevCsr& a, const FlopScratch& s, int64_t a_off) {
+    TileMarks mk;
+    mk.tile_row = s.tile_x;
+    mk.a_off = a_off;
+    mk.m = a.rows;
+    mk.base = a.base;
+    mk.tiles = flop_tiles(a);
+    return mk;
+}
+
+static unsigned stream_grid(int64_t n, int num_sms) {
+    int64_t grid = (n + 255) / 256;
     if (grid > int64_t(num_sms) * 16) grid = int64_t(num_sms) * 16;
-    k_degree<<<static_cast<unsigned>(grid), 256, 0, stream>>>(brpt, k_rows, deg);
+    return static_cast<unsigned>(grid < 1 ? 1 : grid);
+}
+
+cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, uint16_t* deg, int num_sms,
+                          cudaStream_t stream, const DevCsr* a, const FlopScratch* s, int64_t* launches) {
+    // A's partition rides along when A.rpt is a view into B.rpt
+    const bool fuse = a && s && a->rows > 0 && a->rpt >= brpt && a->rpt + a->rows <= brpt + k_rows;
+    if (k_rows == 0 && !(a && s)) return cudaSuccess;
+    if (a && s && a->rows > 0 && !fuse) {
+        k_tile_rows<<<stream_grid(a->rows, num_sms), 256, 0, stream>>>(a->rpt, tile_marks(*a, *s, 0));
+        if (launches) ++*launches;
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (k_rows == 0) return cudaSuccess;
+    const TileMarks mk = fuse ? tile_marks(*a, *s, a->rpt - brpt) : TileMarks();
+    if (reinterpret_cast<uintptr_t>(brpt) & 15) return cudaErrorMisalignedAddress;  // cudaMalloc'd
+    k_degree<<<stream_grid((k_rows + 3) / 4, num_sms), 256, 0, stream>>>(brpt, k_rows, deg, mk);
+    if (launches) ++*launches;
     return cudaGetLastError();
 }
 
+#ifdef SPNNZ_BINARY_PARTITION
 cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStream_t stream) {
     const int64_t tiles = flop_tiles(a);
     if (tiles == 0) return cudaSuccess;
@@ -536,6 +645,7 @@ cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStr
                                                                       a.nnz, tiles, s.tile_x);
     return cudaGetLastError();
 }
+#endif
 
 cudaError_t launch_flop_tiles(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt,
                               const FlopScratch& s, int64_t* flop, int64_t t_begin, int64_t t_end,

@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(kSG * kSGroups, 3) k_heavy_run_small(SymArgs g
     long long acc = 0;
     for (long long ti = blockIdx.x * int64_t(kSGroups) + grp; ti < ntask; ti += int64_t(gridDim.x) * kSGroups) {
         const HeavyTask t = *(tasks - ti);
-        for (int k = gt; k < kSSlots; k += kSG) table[k] = kEmpty;
+        hash_clear(table, kSSlots, gt, kSG);
         const long long ubase = sc.heavy_unit_off[t.item];
         const long long pbase = sc.heavy_foff[t.item];
         int cnt = 0;

@@ -38,9 +38,13 @@ enum TotalSlot : int {
 // ---------------------------------------------------------------- FLOP
 // Fixed tiles of kFlopTile nonzeros (aligned to absolute multiples of the
 // tile size), one block each; a tile owns the rows that start inside it.
-constexpr int kFlopBlock = 256;
+#ifndef SPNNZ_FLOP_BLOCK
+#define SPNNZ_FLOP_BLOCK 128
+#endif
+constexpr int kFlopBlock = SPNNZ_FLOP_BLOCK;
 constexpr int kFlopIpt = 16;
 constexpr int kFlopTile = kFlopBlock * kFlopIpt;
+static_assert((kFlopTile & (kFlopTile - 1)) == 0, "tile size is a power of two");
 
 int64_t flop_tiles(const DevCsr& a);
 
@@ -51,11 +55,13 @@ struct FlopScratch {
     long long* tile_max = nullptr;   // tiles
 };
 
-cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStream_t stream);
 // deg[k] = min(B.rpt[k+1] - B.rpt[k], 0xFFFF) as uint16; 0xFFFF escapes to
 // B.rpt for the exact length.  Gathered under an L2 evict_last policy.
+// Degree array of B and, when a and s are given, A's tile partition (fused
+// into the same pass when A.rpt is a view of B.rpt); *launches counts kernels.
 cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, uint16_t* deg, int num_sms,
-                          cudaStream_t stream);
+                          cudaStream_t stream, const DevCsr* a = nullptr, const FlopScratch* s = nullptr,
+                          int64_t* launches = nullptr);
 // Fused predict: with ceil/real set, the FLOP pass also writes
 // min(flop, ceil(flop / cr)) (and flop / cr) for every row as its flop becomes
 // final, cr derived on the device from totals[kFStar], totals[kZStar].

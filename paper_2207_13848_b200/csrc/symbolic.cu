@@ -136,7 +136,7 @@ template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_sym_warp_hash(SymArgs g, SymScratch sc) {
     constexpr int kSlots = 1024;
     constexpr int W = BLOCK / 32;
-    __shared__ int s_table[W][kSlots];
+    __shared__ __align__(16) int s_table[W][kSlots];
     __shared__ int s_off[W][33];
     __shared__ int64_t s_b0[W][32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_warp_hash(SymArgs g, SymScratch s
     long long acc = 0;
     for (int i = blockIdx.x * W + wib; i < n; i += gridDim.x * W) {
         const ItemRow it = item_row(g, list[i]);
-        for (int k = lane; k < kSlots; k += 32) table[k] = kEmpty;
+        hash_clear(table, kSlots, lane, 32);
         int cnt = 0;
         for (int64_t e0 = it.a0; e0 < it.a1; e0 += 32) {
             const int64_t e = e0 + lane;
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_warp_hash(SymArgs g, SymScratch s
 }
 
 // ------------------------------ bins 3-5: block + shared-memory hash
-template <int BLOCK, int SLOTS, int BIN>
+template <int BLOCK, int SLOTS, int BIN, int UNROLL>
 __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch sc) {
     extern __shared__ int4 s_dyn[];
     int* table = reinterpret_cast<int*>(s_dyn);
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
     long long acc = 0;
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
         const ItemRow it = item_row(g, list[i]);
-        for (int k = threadIdx.x; k < SLOTS; k += BLOCK) table[k] = kEmpty;
+        hash_clear(table, SLOTS, threadIdx.x, BLOCK);
         int cnt = 0;
         for (int64_t c0 = it.a0; c0 < it.a1; c0 += BLOCK) {
             const int64_t e = c0 + threadIdx.x;
@@ -213,8 +213,8 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
             s_b0[threadIdx.x] = b0;
             if (threadIdx.x == 0) s_off[nent] = total;
             __syncthreads();  // also orders the table fill before the inserts
-            chunk_products<BLOCK / 32>(s_off, s_b0, nent, 0, total, g.bcol,
-                                       HashSink{table, SLOTS, &cnt});
+            chunk_products<BLOCK / 32, UNROLL>(s_off, s_b0, nent, 0, total, g.bcol,
+                                               HashSinkU<UNROLL>{table, SLOTS, &cnt});
             __syncthreads();
         }
         const long long tot = block_sum_ll<BLOCK>(cnt, s_red);
@@ -232,10 +232,20 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
 constexpr int kT3Block = 256, kT3Slots = 4096;
 constexpr int kT4Block = 512, kT4Slots = 16384;
 constexpr int kT5Block = 1024, kT5Slots = 49152;
+// keys in flight per lane (B.col loads issued together before the inserts)
+#ifndef SPNNZ_T3_UNROLL
+#define SPNNZ_T3_UNROLL 4
+#endif
+#ifndef SPNNZ_T4_UNROLL
+#define SPNNZ_T4_UNROLL 8
+#endif
+#ifndef SPNNZ_T5_UNROLL
+#define SPNNZ_T5_UNROLL 4
+#endif
 
-template <int BLOCK, int SLOTS, int BIN>
+template <int BLOCK, int SLOTS, int BIN, int UNROLL>
 void set_smem_attr() {
-    cudaFuncSetAttribute(k_sym_block_hash<BLOCK, SLOTS, BIN>,
+    cudaFuncSetAttribute(k_sym_block_hash<BLOCK, SLOTS, BIN, UNROLL>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, SLOTS * 4);
 }
 
@@ -257,17 +267,17 @@ cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_s
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_done & (1u << (dev & 31)))) {
-        set_smem_attr<kT3Block, kT3Slots, 3>();
-        set_smem_attr<kT4Block, kT4Slots, 4>();
-        set_smem_attr<kT5Block, kT5Slots, 5>();
+        set_smem_attr<kT3Block, kT3Slots, 3, SPNNZ_T3_UNROLL>();
+        set_smem_attr<kT4Block, kT4Slots, 4, SPNNZ_T4_UNROLL>();
+        set_smem_attr<kT5Block, kT5Slots, 5, SPNNZ_T5_UNROLL>();
         attr_done |= 1u << (dev & 31);
     }
     const unsigned sms = static_cast<unsigned>(num_sms);
     k_sym_tiny<256><<<sms * 4, 256, 0, streams[0]>>>(args, s);
     k_sym_warp_hash<256><<<sms * 4, 256, 0, streams[0]>>>(args, s);
-    k_sym_block_hash<kT3Block, kT3Slots, 3><<<sms * 8, kT3Block, kT3Slots * 4, streams[1]>>>(args, s);
-    k_sym_block_hash<kT4Block, kT4Slots, 4><<<sms * 3, kT4Block, kT4Slots * 4, streams[2]>>>(args, s);
-    k_sym_block_hash<kT5Block, kT5Slots, 5><<<sms, kT5Block, kT5Slots * 4, streams[3]>>>(args, s);
+    k_sym_block_hash<kT3Block, kT3Slots, 3, SPNNZ_T3_UNROLL><<<sms * 8, kT3Block, kT3Slots * 4, streams[1]>>>(args, s);
+    k_sym_block_hash<kT4Block, kT4Slots, 4, SPNNZ_T4_UNROLL><<<sms * 3, kT4Block, kT4Slots * 4, streams[2]>>>(args, s);
+    k_sym_block_hash<kT5Block, kT5Slots, 5, SPNNZ_T5_UNROLL><<<sms, kT5Block, kT5Slots * 4, streams[3]>>>(args, s);
     return cudaGetLastError();
 }
 

@@ -63,7 +63,7 @@ __device__ __forceinline__ ItemRow item_row(const SymArgs& g, int32_t s) {
 // dependent chain per product.
 constexpr int kUnroll = 4;
 
-template <int WARPS, typename OffT, typename Fn>
+template <int WARPS, int U = kUnroll, typename OffT, typename Fn>
 __device__ __forceinline__ void chunk_products(const OffT* off, const int64_t* b0, int n, OffT q0,
                                                OffT q1, const int32_t* __restrict__ bcol, Fn&& fn) {
     const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) % WARPS;
@@ -89,12 +89,12 @@ __device__ __forceinline__ void chunk_products(const OffT* off, const int64_t* b
     // B.col index of product 0 (key of product q = bcol[kb + q])
     OffT nxt = off[e + 1];
     long long kb = static_cast<long long>(b0[e]) - static_cast<long long>(off[e]);
-    for (OffT base = ws; base < we; base += 32 * kUnroll) {
+    for (OffT base = ws; base < we; base += 32 * U) {
         const OffT p = base + lane;
-        int keys[kUnroll];
-        bool valid[kUnroll];
+        int keys[U];
+        bool valid[U];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
+        for (int u = 0; u < U; ++u) {
             const OffT q = p + 32 * u;
             valid[u] = q < we;
             keys[u] = 0;
@@ -127,18 +127,58 @@ __device__ __forceinline__ int warp_bucket_add(int* counters, int bucket) {
     return base + __popc(peers & ((1u << lane) - 1));
 }
 
+#ifndef SPNNZ_HASH_BUCKET
+#define SPNNZ_HASH_BUCKET 0
+#endif
+// Bucketed open addressing: `size` slots as size/4 buckets of four (one
+// 16-byte shared-memory read per probe), linear probing over buckets.  A
+// bucket's slots fill in order and are never emptied, so a key is found
+// before the first empty slot of its probe sequence; a lost CAS re-reads the
+// same bucket.  At the tiers' load factors almost every insert is one probe,
+// which keeps the 32 lanes of a warp in step (per-slot linear probing made
+// the warp wait for its longest chain: ~2.9 probe rounds per key in bin 5).
+// The table (and size) must be 16-byte aligned (a multiple of 4).
+__device__ __forceinline__ int hash_insert_bucket(int* table, uint32_t size, int key) {
+    const uint32_t nb = size >> 2;
+    uint32_t h = __umulhi(mix32(static_cast<uint32_t>(key)), nb);
+    const int4* t4 = reinterpret_cast<const int4*>(table);
+    for (;;) {
+        const int4 v = t4[h];
+        if (v.x == key || v.y == key || v.z == key || v.w == key) return 0;
+        const int slot = v.x == kEmpty ? 0 : v.y == kEmpty ? 1 : v.z == kEmpty ? 2 : v.w == kEmpty ? 3 : 4;
+        if (slot < 4) {
+            const int prev = atomicCAS(&table[4 * h + slot], kEmpty, key);
+            if (prev == kEmpty) return 1;
+            if (prev == key) return 0;
+            continue;  // another key took the slot: re-read the bucket
+        }
+        h = (h + 1 == nb) ? 0 : h + 1;
+    }
+}
+
+// Fills a table with kEmpty using 16-byte stores (size a multiple of 4).
+__device__ __forceinline__ void hash_clear(int* table, int size, int t, int nt) {
+    int4* t4 = reinterpret_cast<int4*>(table);
+    for (int k = t; k < (size >> 2); k += nt) t4[k] = make_int4(kEmpty, kEmpty, kEmpty, kEmpty);
+}
+
 // fn adaptor: insert each valid key into a shared-memory hash table.
-struct HashSink {
+template <int U = kUnroll>
+struct HashSinkU {
     int* table;
     uint32_t size;
     int* cnt;
-    __device__ __forceinline__ void operator()(const int (&keys)[kUnroll],
-                                               const bool (&valid)[kUnroll], long long) const {
+    __device__ __forceinline__ void operator()(const int (&keys)[U], const bool (&valid)[U], long long) const {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
+        for (int u = 0; u < U; ++u)
+#if SPNNZ_HASH_BUCKET
+            if (valid[u]) *cnt += hash_insert_bucket(table, size, keys[u]);
+#else
             if (valid[u]) *cnt += hash_insert(table, size, keys[u]);
+#endif
     }
 };
+using HashSink = HashSinkU<kUnroll>;
 
 }  // namespace sym
 }  // namespace spnnz_gpu
