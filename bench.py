@@ -456,9 +456,12 @@ def run_ours(args, rank, world, local):
                                       "1 NCCL all-reduce per step",
                        "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps"},
             "roofline": {"bound": "hbm",
-                         "kernel": "FLOP pass (k_degree + k_flop_partition + k_flop + k_flop_fixup)",
+                         "kernel": "FLOP pass (k_degree with the tile partition + k_flop + k_flop_fixup)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         # L2 hit rate of the pass (the degree gathers dominate its
+                         # requests), from the same committed ncu capture
+                         "l2_hit_rate_pct": (tmeta or {}).get("l2_hit_rate_pct") if traffic else None,
                          "algorithmic_bytes": fbytes, "avg_ms": phase["flop"],
                          "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json)",
                          # the FLOP pass gathers one B-row length per A nonzero; random

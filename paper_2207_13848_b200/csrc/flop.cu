@@ -153,6 +153,10 @@ __global__ void k_flop_partition(const int64_t* __restrict__ arpt, int32_t m, in
 }
 #endif
 
+#ifndef SPNNZ_FLOP_MINB  // resident threads per SM the register budget targets
+#define SPNNZ_FLOP_MINB 1280
+#endif
+
 #ifndef SPNNZ_FLOP_GATHER
 #define SPNNZ_FLOP_GATHER 0
 #endif
@@ -240,7 +244,7 @@ __device__ __forceinline__ Emit make_emit(const PredOut& p) {
 }
 
 template <int BLOCK, int V, bool PRED>
-__global__ void __launch_bounds__(BLOCK, (1280 / BLOCK < 32 ? 1280 / BLOCK : 32))
+__global__ void __launch_bounds__(BLOCK, (SPNNZ_FLOP_MINB / BLOCK < 32 ? SPNNZ_FLOP_MINB / BLOCK : 32))
 k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
        const uint16_t* __restrict__ bdeg, const int64_t* __restrict__ brpt, int32_t m,
        int64_t base, int64_t nnz, const int32_t* __restrict__ tile_row,
@@ -248,7 +252,7 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
        long long* __restrict__ tile_total, long long* __restrict__ tile_max, PredOut pred,
        int64_t t0) {
     constexpr int TILE = BLOCK * V, NW = BLOCK / 32;
-    static_assert(TILE == kFlopTile && V == 16, "tile size");
+    static_assert(TILE == kFlopTile && (V == 8 || V == 16 || V == 32), "tile size");
     __shared__ uint32_t s_start[TILE / 32];  // bit i: an owned non-empty row starts at entry i
     __shared__ int32_t s_rowat[TILE];        // ... and its id (read only where the bit is set)
     __shared__ Carry s_wc[NW];
@@ -312,7 +316,7 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
     // 3. segmented sum over the thread's entries: rows that start and end
     //    inside are written here; the head (before the first start) and the
     //    tail (from the last start) are combined across threads below
-    const uint32_t bits = (s_start[i0 >> 5] >> (i0 & 31)) & 0xFFFFu;
+    const uint32_t bits = V == 32 ? s_start[i0 >> 5] : (s_start[i0 >> 5] >> (i0 & 31)) & ((1u << (V & 31)) - 1u);
     long long cur = 0, head = 0, tmax = 0;
     int32_t row = -1;
 #pragma unroll

@@ -42,7 +42,10 @@ enum TotalSlot : int {
 #define SPNNZ_FLOP_BLOCK 128
 #endif
 constexpr int kFlopBlock = SPNNZ_FLOP_BLOCK;
-constexpr int kFlopIpt = 16;
+#ifndef SPNNZ_FLOP_IPT
+#define SPNNZ_FLOP_IPT 16
+#endif
+constexpr int kFlopIpt = SPNNZ_FLOP_IPT;
 constexpr int kFlopTile = kFlopBlock * kFlopIpt;
 static_assert((kFlopTile & (kFlopTile - 1)) == 0, "tile size is a power of two");
 

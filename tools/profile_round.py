@@ -66,6 +66,9 @@ def main():
                                    "dram_bytes_per_launch": traffic,
                                    "dram_read": num("dram__bytes_read.sum"),
                                    "dram_write": num("dram__bytes_write.sum"),
+                                   "l2_hit_rate_pct": float(d.get("lts__t_sector_hit_rate.pct", "nan").replace(",", "")),
+                                   "l1_hit_rate_pct": float(d.get("l1tex__t_sector_hit_rate.pct", "nan").replace(",", "")),
+                                   "l2_read_requests": float(d.get("lts__t_requests_srcunit_tex_op_read.sum", "nan").replace(",", "")),
                                    "duration_ms": float(d["gpu__time_duration.sum"].replace(",", "")) *
                                    {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0,
                                     "msecond": 1.0, "nsecond": 1e-6}.get(
