@@ -194,6 +194,7 @@ struct spnnz_gpu_ctx {
     DBuf<long long> heavy_meta;
     DBuf<long long> sorted_cnt;
     DBuf<int64_t> item_flop;  // FLOP of this rank's sampled rows (balanced multi-GPU pass)
+    DBuf<int64_t> item_units; // their chunk offsets (flat item-FLOP decomposition)
     DBuf<int32_t> redo;       // fused predict: rows left to an IEEE division
     DBuf<unsigned long long> nredo;
     DBuf<int32_t> samples;
@@ -579,9 +580,10 @@ int sample_share(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool need_f
     }
     if (need_flop) {
         RC(c->item_flop.ensure(std::max<int64_t>(sh->n, 1)));
+        RC(c->item_units.ensure(sh->n + 1));
         CU(launch_item_flop(sh->use_full ? sh->full : c->a, c->b_rpt.p, sh->use_full ? 0 : c->row_lo,
-                            sh->rows, sh->n, c->item_flop.p, c->num_sms, c->stream));
-        *launches += 2;
+                            sh->rows, sh->n, c->item_flop.p, c->item_units.p, c->num_sms, c->stream));
+        *launches += 3;
         sh->item_flop = c->item_flop.p;
     }
     return SPNNZ_OK;

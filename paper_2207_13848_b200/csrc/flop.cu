@@ -29,6 +29,8 @@
 // Algorithmic bytes: 8(M+1) A.rpt + 4 nnz A.col + 8(K+1) B.rpt + 8M flop
 // (the 2K-byte degree array's write and re-reads are extra traffic).
 // Integer-only: bit-exact.
+#include <cub/block/block_scan.cuh>
+
 #include "device_common.cuh"
 #include "kernels.h"
 
@@ -459,72 +461,76 @@ __global__ void k_check_rows(const int32_t* __restrict__ rows, int64_t n, int32_
     if (i < n && (rows[i] < 0 || rows[i] >= num_rows)) atomicAdd(bad, 1);
 }
 
-// FLOP of listed rows (compute_flop's sum, flop.hpp:41-50, for those rows):
-// one warp per row up to kItemLong entries; longer rows (hub rows of
-// power-law matrices, tens of thousands of entries) are left to
-// k_item_flop_long, where a whole block takes each one.
-constexpr int64_t kItemLong = 2048;
+// FLOP of listed rows (compute_flop's sum, flop.hpp:41-50, for those rows),
+// as a flat decomposition so no warp walks a long row step after dependent
+// step: every row is cut into kItemChunk-entry chunks, a one-block scan
+// numbers them, and one warp per chunk adds its sum into the row's slot.
+// (Warps over rows of up to 2048 entries plus one block per hub row left the
+// multi-GPU sampled-FLOP step at ~40 us, latency-bound.)
+constexpr int kItemChunk = 128;  // one step of four loads per lane
 
-__device__ __forceinline__ long long item_flop_range(const DevCsr& a, const int64_t* __restrict__ brpt,
-                                                     int64_t e, int64_t e1, int stride) {
-    long long f = 0;
-    for (; e < e1; e += int64_t(stride) * 4) {
-        int c[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) c[k] = e + int64_t(stride) * k < e1 ? __ldg(&a.col[e + int64_t(stride) * k]) : -1;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (c[k] >= 0) f += __ldg(&brpt[c[k] + 1]) - __ldg(&brpt[c[k]]);
+// units[s] = chunks of item s (0 outside the shard); out[s] = 0
+__global__ void __launch_bounds__(256) k_item_chunks(DevCsr a, int32_t row_lo, const int32_t* __restrict__ rows,
+                                                    int64_t n, int64_t* __restrict__ units,
+                                                    int64_t* __restrict__ out) {
+    for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < n; s += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t r = rows[s] - row_lo;
+        int64_t u = 0;
+        if (r >= 0 && r < a.rows) u = (a.rpt[r + 1] - a.rpt[r] + kItemChunk - 1) / kItemChunk;
+        units[s] = u;
+        out[s] = 0;
     }
-    return f;
+}
+
+// In-place exclusive scan of units[0..n) by one block; units[n] = total.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_item_scan(int64_t* __restrict__ units, int64_t n) {
+    using Scan = cub::BlockScan<long long, BLOCK>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ long long s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += BLOCK) {
+        const int64_t s = base + threadIdx.x;
+        const long long v = s < n ? units[s] : 0;
+        long long excl, total;
+        Scan(tmp).ExclusiveSum(v, excl, total);
+        const long long carry = s_carry;
+        if (s < n) units[s] = carry + excl;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry = carry + total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) units[n] = s_carry;
 }
 
 __global__ void __launch_bounds__(256) k_item_flop(DevCsr a, const int64_t* __restrict__ brpt,
                                                   int32_t row_lo, const int32_t* __restrict__ rows,
-                                                  int64_t n, int64_t* __restrict__ out) {
+                                                  int64_t n, const int64_t* __restrict__ pre,
+                                                  int64_t* __restrict__ out) {
     const int lane = threadIdx.x & 31;
-    for (int64_t s = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; s < n;
-         s += (int64_t(gridDim.x) * blockDim.x) >> 5) {
-        const int32_t r = rows[s] - row_lo;
+    const long long total = pre[n];
+    for (long long u = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; u < total;
+         u += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+        int64_t lo = 0, hi = n - 1;  // largest item with pre[item] <= u
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (__ldg(&pre[mid]) <= u) lo = mid; else hi = mid - 1;
+        }
+        const int32_t r = rows[lo] - row_lo;
+        const int64_t e1 = a.rpt[r + 1];
+        const int64_t c0 = a.rpt[r] + (u - pre[lo]) * kItemChunk;
+        const int64_t c1 = c0 + kItemChunk < e1 ? c0 + kItemChunk : e1;
         long long f = 0;
-        if (r >= 0 && r < a.rows) {
-            const int64_t e0 = a.rpt[r], e1 = a.rpt[r + 1];
-            if (e1 - e0 > kItemLong) continue;  // k_item_flop_long
-            f = item_flop_range(a, brpt, e0 + lane, e1, 32);
-        }
+        int c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k] = c0 + lane + 32 * k < c1 ? __ldg(&a.col[c0 + lane + 32 * k]) : -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (c[k] >= 0) f += __ldg(&brpt[c[k] + 1]) - __ldg(&brpt[c[k]]);
         f = warp_sum_ll(f);
-        if (lane == 0) out[s] = f;
-    }
-}
-
-// Each block checks a contiguous group of items in parallel, collects the
-// long rows in shared memory, then sums each of them with all its threads.
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) k_item_flop_long(DevCsr a, const int64_t* __restrict__ brpt,
-                                                         int32_t row_lo, const int32_t* __restrict__ rows,
-                                                         int64_t n, int64_t* __restrict__ out) {
-    __shared__ long long s_red[BLOCK / 32];
-    __shared__ int64_t s_item[BLOCK];
-    __shared__ int s_n;
-    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-    const int64_t g0 = blockIdx.x * per, g1 = g0 + per < n ? g0 + per : n;
-    for (int64_t b = g0; b < g1; b += BLOCK) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_n = 0;
-        __syncthreads();
-        const int64_t s = b + threadIdx.x;
-        if (s < g1) {
-            const int32_t r = rows[s] - row_lo;
-            if (r >= 0 && r < a.rows && a.rpt[r + 1] - a.rpt[r] > kItemLong) s_item[atomicAdd(&s_n, 1)] = s;
-        }
-        __syncthreads();
-        for (int k = 0; k < s_n; ++k) {
-            const int64_t it = s_item[k];
-            const int32_t r = rows[it] - row_lo;
-            const long long f =
-                block_sum_ll<BLOCK>(item_flop_range(a, brpt, a.rpt[r] + threadIdx.x, a.rpt[r + 1], BLOCK), s_red);
-            if (threadIdx.x == 0) out[it] = f;
-        }
+        if (lane == 0 && f)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&out[lo]), static_cast<unsigned long long>(f));
     }
 }
 
@@ -556,13 +562,14 @@ __global__ void k_start_descents(const int64_t* __restrict__ rpt, const int32_t*
 }  // namespace
 
 cudaError_t launch_item_flop(const DevCsr& a, const int64_t* brpt, int32_t row_lo,
-                             const int32_t* rows, int64_t n, int64_t* out, int num_sms,
+                             const int32_t* rows, int64_t n, int64_t* out, int64_t* units, int num_sms,
                              cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
-    int64_t grid = (n + 7) / 8;
-    if (grid > int64_t(num_sms) * 8) grid = int64_t(num_sms) * 8;
-    k_item_flop<<<static_cast<unsigned>(grid), 256, 0, stream>>>(a, brpt, row_lo, rows, n, out);
-    k_item_flop_long<1024><<<static_cast<unsigned>(num_sms), 1024, 0, stream>>>(a, brpt, row_lo, rows, n, out);
+    int64_t g1 = (n + 255) / 256;
+    if (g1 > int64_t(num_sms) * 4) g1 = int64_t(num_sms) * 4;
+    k_item_chunks<<<static_cast<unsigned>(g1), 256, 0, stream>>>(a, row_lo, rows, n, units, out);
+    k_item_scan<1024><<<1, 1024, 0, stream>>>(units, n);
+    k_item_flop<<<static_cast<unsigned>(num_sms) * 8, 256, 0, stream>>>(a, brpt, row_lo, rows, n, units, out);
     return cudaGetLastError();
 }
 

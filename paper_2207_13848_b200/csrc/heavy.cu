@@ -68,7 +68,7 @@ __device__ __forceinline__ const int32_t* heavy_list(const SymScratch& sc, int64
 
 // ---- 0a. batch bookkeeping: per item its units, entries, products,
 // interval tasks and boundary-table cells, as exclusive prefixes (1 block)
-constexpr int kPrepBlock = 512;
+constexpr int kPrepBlock = 1024;
 
 __global__ void __launch_bounds__(kPrepBlock) k_heavy_prep(SymArgs g, SymScratch sc, int64_t first,
                                                            int64_t count) {
@@ -122,9 +122,14 @@ __global__ void __launch_bounds__(kPrepBlock) k_heavy_prep(SymArgs g, SymScratch
     }
 }
 
-// ---- 0b. one block per item: product prefix over its entries, B-row starts
-__global__ void __launch_bounds__(256) k_heavy_entries(SymArgs g, SymScratch sc, int64_t first) {
-    using Scan = cub::BlockScan<long long, 256>;
+// ---- 0b. one block per item: product prefix over its entries, B-row starts.
+// kEntV consecutive entries per thread, their loads issued together, so a
+// row of up to kEntB * kEntV entries costs one dependent load chain (the
+// walk of 256 entries per step made the longest heavy row the critical path:
+// ~30 us whatever the number of heavy rows).
+constexpr int kEntB = 512, kEntV = 4;
+__global__ void __launch_bounds__(kEntB) k_heavy_entries(SymArgs g, SymScratch sc, int64_t first) {
+    using Scan = cub::BlockScan<long long, kEntB>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ long long s_carry;
     const int64_t i = blockIdx.x;
@@ -132,31 +137,45 @@ __global__ void __launch_bounds__(256) k_heavy_entries(SymArgs g, SymScratch sc,
     int64_t* ep = sc.heavy_epre + sc.heavy_eoff[i];
     int64_t* eb = sc.heavy_eb0 + sc.heavy_eoff[i];
     const int64_t L = it.a1 - it.a0;
+    const int64_t ubase = sc.heavy_unit_off[i];
     if (threadIdx.x == 0) s_carry = 0;
     __syncthreads();
-    for (int64_t c0 = 0; c0 < L; c0 += 256) {
-        const int64_t e = c0 + threadIdx.x;
-        long long d = 0;
-        int64_t b0 = 0;
-        if (e < L) {
-            const int c = __ldg(&g.a.col[it.a0 + e]);
-            b0 = __ldg(&g.brpt[c]);
-            d = __ldg(&g.brpt[c + 1]) - b0;
+    for (int64_t c0 = 0; c0 < L; c0 += int64_t(kEntB) * kEntV) {
+        const int64_t e0 = c0 + int64_t(threadIdx.x) * kEntV;
+        int c[kEntV];
+        long long d[kEntV];
+        int64_t b0[kEntV];
+#pragma unroll
+        for (int k = 0; k < kEntV; ++k) c[k] = e0 + k < L ? __ldg(&g.a.col[it.a0 + e0 + k]) : -1;
+#pragma unroll
+        for (int k = 0; k < kEntV; ++k) {
+            b0[k] = c[k] >= 0 ? __ldg(&g.brpt[c[k]]) : 0;
+            d[k] = c[k] >= 0 ? __ldg(&g.brpt[c[k] + 1]) : 0;
+        }
+        long long sum = 0;
+#pragma unroll
+        for (int k = 0; k < kEntV; ++k) {
+            d[k] -= b0[k];
+            sum += d[k];
         }
         long long ex, tot;
-        Scan(tmp).ExclusiveSum(d, ex, tot);
-        if (e < L) {
-            const long long p = s_carry + ex;
-            ep[e] = p;
-            eb[e] = b0;
-            if (sc.heavy_unit_item) {  // units whose first product is in this entry
-                const int64_t ubase = sc.heavy_unit_off[i];
-                for (long long u = (p + kHeavyUnitProducts - 1) / kHeavyUnitProducts;
-                     u * kHeavyUnitProducts < p + d; ++u) {
-                    sc.heavy_unit_item[ubase + u] = static_cast<int32_t>(i);
-                    sc.heavy_unit_e0[ubase + u] = static_cast<int32_t>(e);
+        Scan(tmp).ExclusiveSum(sum, ex, tot);
+        long long p = s_carry + ex;
+#pragma unroll
+        for (int k = 0; k < kEntV; ++k) {
+            const int64_t e = e0 + k;
+            if (e < L) {
+                ep[e] = p;
+                eb[e] = b0[k];
+                if (sc.heavy_unit_item) {  // units whose first product is in this entry
+                    for (long long u = (p + kHeavyUnitProducts - 1) / kHeavyUnitProducts;
+                         u * kHeavyUnitProducts < p + d[k]; ++u) {
+                        sc.heavy_unit_item[ubase + u] = static_cast<int32_t>(i);
+                        sc.heavy_unit_e0[ubase + u] = static_cast<int32_t>(e);
+                    }
                 }
             }
+            p += d[k];
         }
         __syncthreads();
         if (threadIdx.x == 0) s_carry += tot;
@@ -1201,7 +1220,7 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
     const unsigned sms = static_cast<unsigned>(num_sms);
     const unsigned items = static_cast<unsigned>(count);
     k_heavy_prep<<<1, kPrepBlock, 0, stream>>>(args, s, first, count);
-    k_heavy_entries<<<items, 256, 0, stream>>>(args, s, first);
+    k_heavy_entries<<<items, kEntB, 0, stream>>>(args, s, first);
     n += 2;
     if (sorted) {
         cudaMemsetAsync(s.heavy_bnd, 0, sizeof(int32_t) * s.heavy_bnd_cap, stream);

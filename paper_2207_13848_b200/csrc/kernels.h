@@ -235,9 +235,9 @@ cudaError_t launch_sampled_flop(const int64_t* flop, int32_t row_lo, int32_t loc
 
 // Validation: counts rows outside [0, num_rows) into *bad.
 // FLOP of each listed row (global ids; 0 outside [row_lo, row_lo + a.rows)),
-// straight from A and B.rpt.
+// straight from A and B.rpt.  units: scratch of n + 1 entries.
 cudaError_t launch_item_flop(const DevCsr& a, const int64_t* brpt, int32_t row_lo,
-                             const int32_t* rows, int64_t n, int64_t* out, int num_sms,
+                             const int32_t* rows, int64_t n, int64_t* out, int64_t* units, int num_sms,
                              cudaStream_t stream);
 // B rows non-decreasing? cnt[0] == cnt[1] afterwards (device counters).
 cudaError_t launch_check_sorted(const int64_t* rpt, const int32_t* col, int32_t rows, int64_t nnz,
