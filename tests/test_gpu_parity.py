@@ -600,7 +600,7 @@ def test_detached_pipeline_shards_sum_to_single_gpu():
     single.load(a, b)
     ref = single.run_prediction(2, SamplePolicy(0.003, UNCAPPED))
     single.close()
-    for world in (2, 4):
+    for world in (2, 4, 8):
         F = fs = zs = 0
         for r in range(world):
             q = Predictor(0, r, world)
@@ -611,6 +611,30 @@ def test_detached_pipeline_shards_sum_to_single_gpu():
             zs += rep.stats.sampled_nnz
             q.close()
         assert (F, fs, zs) == (ref.total_flop, ref.stats.sampled_flop, ref.stats.sampled_nnz)
+
+
+def test_detached_shards_sampled_flop_chunk_edges(oracle):
+    """The balanced split derives each rank's sampled-row FLOP directly (rows
+    cut into 128-entry chunks, one warp each): row lengths on and around the
+    chunk edges, empty rows and repeated draws, summed over 3 ranks, equal the
+    oracle's sampled FLOP."""
+    rng = np.random.default_rng(77)
+    n = 6000
+    lens = np.tile([0, 1, 127, 128, 129, 255, 256, 257, 1000, 3000], n // 10)
+    rows = [np.sort(rng.choice(n, size=L, replace=False)).astype(np.int32) for L in lens]
+    a = csr(n, n, rows)
+    flop, F, _ = oracle.compute_flop(a, a)
+    for fraction in (0.05, 1.0):
+        plan = spnnz.make_sample_plan(n, 9, SamplePolicy(fraction, UNCAPPED))
+        want = int(flop[plan.sample_rows.astype(np.int64)].sum())
+        fs = 0
+        for r in range(3):
+            q = Predictor(0, r, 3)
+            q.load(a)
+            rep = q.run_prediction(9, SamplePolicy(fraction, UNCAPPED))
+            fs += rep.stats.sampled_flop
+            q.close()
+        assert fs == want
 
 
 def test_repeat_runs_deterministic(P):
