@@ -162,6 +162,30 @@ __device__ __forceinline__ void hash_clear(int* table, int size, int t, int nt) 
     for (int k = t; k < (size >> 2); k += nt) t4[k] = make_int4(kEmpty, kEmpty, kEmpty, kEmpty);
 }
 
+#ifndef SPNNZ_HASH_PTX
+#define SPNNZ_HASH_PTX 1
+#endif
+// hash_insert on a 32-bit shared-window address: the generic-pointer form
+// re-derives the shared window (S2R SR_CgaCtaId + 64-bit arithmetic) on every
+// probe of the loop.
+__device__ __forceinline__ int hash_insert_shared(uint32_t table_s, uint32_t size, int key) {
+    uint32_t h = __umulhi(mix32(static_cast<uint32_t>(key)), size);
+    for (;;) {
+        const uint32_t addr = table_s + 4u * h;
+        int cur;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(cur) : "r"(addr) : "memory");
+        if (cur == key) return 0;
+        if (cur == kEmpty) {
+            int prev;
+            asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;"
+                         : "=r"(prev) : "r"(addr), "r"(kEmpty), "r"(key) : "memory");
+            if (prev == kEmpty) return 1;
+            if (prev == key) return 0;
+        }
+        h = (h + 1 == size) ? 0 : h + 1;
+    }
+}
+
 // fn adaptor: insert each valid key into a shared-memory hash table.
 template <int U = kUnroll>
 struct HashSinkU {
@@ -169,10 +193,15 @@ struct HashSinkU {
     uint32_t size;
     int* cnt;
     __device__ __forceinline__ void operator()(const int (&keys)[U], const bool (&valid)[U], long long) const {
+#if SPNNZ_HASH_PTX && !SPNNZ_HASH_BUCKET
+        const uint32_t ts = static_cast<uint32_t>(__cvta_generic_to_shared(table));
+#endif
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #if SPNNZ_HASH_BUCKET
             if (valid[u]) *cnt += hash_insert_bucket(table, size, keys[u]);
+#elif SPNNZ_HASH_PTX
+            if (valid[u]) *cnt += hash_insert_shared(ts, size, keys[u]);
 #else
             if (valid[u]) *cnt += hash_insert(table, size, keys[u]);
 #endif
