@@ -462,6 +462,8 @@ def run_ours(args, rank, world, local):
                          # L2 hit rate of the pass (the degree gathers dominate its
                          # requests), from the same committed ncu capture
                          "l2_hit_rate_pct": (tmeta or {}).get("l2_hit_rate_pct") if traffic else None,
+                         # the north star quotes HBM3e at about 8 TB/s (nominal)
+                         "nominal_peak": 8000.0, "nominal_frac": achieved / 8000.0,
                          "algorithmic_bytes": fbytes, "avg_ms": phase["flop"],
                          "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json)",
                          # the FLOP pass gathers one B-row length per A nonzero; random
@@ -480,6 +482,7 @@ def run_ours(args, rank, world, local):
                                   "achieved": pbytes / (phase["predict"] * 1e-3) / 1e9,
                                   "peak": peak, "unit": "GB/s",
                                   "frac": pbytes / (phase["predict"] * 1e-3) / 1e9 / peak,
+                                  "nominal_frac": pbytes / (phase["predict"] * 1e-3) / 1e9 / 8000.0,
                                   "algorithmic_bytes": pbytes, "avg_ms": phase["predict"]}),
             "roofline_symbolic": {"bound": "shared-memory atomics / phase latency (not HBM)",
                                   "kernel": "sampled symbolic (bins 1-5 + heavy rows)",
