@@ -33,6 +33,8 @@
 //                   buffer (exact; slower at config 5).
 // Every count is a set cardinality: exact and independent of bucketing, task
 // boundaries and scheduling.
+#include <atomic>
+
 #include "symbolic_common.cuh"
 
 namespace spnnz_gpu {
@@ -1196,10 +1198,10 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
                              int64_t count, int num_sms, cudaStream_t stream, int64_t* launches) {
     if (count == 0) return cudaSuccess;
     int64_t n = 0;  // kernels launched (memsets not counted)
-    static unsigned attr_done = 0;
+    static std::atomic<unsigned long long> attr_done{0};  // one bit per device; the sets are idempotent
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!(attr_done & (1u << (dev & 31)))) {
+    if (!(attr_done.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
         cudaFuncSetAttribute(k_heavy_run<1024, kRunItem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (1 << kSpanShift) / 8);
         cudaFuncSetAttribute(k_heavy_run<512, kRunBuckets>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1213,7 +1215,7 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
         cudaFuncSetAttribute(k_heavy_sort_units, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              sort_smem(kPrivRanges));
         cudaFuncSetAttribute(k_heavy_intervals, cudaFuncAttributeMaxDynamicSharedMemorySize, kIvSmem);
-        attr_done |= 1u << (dev & 31);
+        attr_done.fetch_or(1ull << (dev & 63), std::memory_order_release);
     }
     const HeavyGeometry geo = heavy_geometry(args.bcols);
     const int R = geo.ranges;

@@ -20,6 +20,8 @@
 // chunk's products and its lanes walk them 32 apart with a monotone entry
 // cursor, so a warp's loads of B.col are consecutive (coalesced) whatever the
 // B row lengths, and each product costs ~1 shared-memory probe to locate.
+#include <atomic>
+
 #include "symbolic_common.cuh"
 
 namespace spnnz_gpu {
@@ -263,14 +265,14 @@ cudaError_t launch_sym_bin(const SymArgs& args, const SymScratch& s, cudaStream_
 cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_sms,
                              const cudaStream_t* streams) {
     if (args.n_items == 0) return cudaSuccess;
-    static unsigned attr_done = 0;  // one bit per device
+    static std::atomic<unsigned long long> attr_done{0};  // one bit per device; the sets are idempotent
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!(attr_done & (1u << (dev & 31)))) {
+    if (!(attr_done.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
         set_smem_attr<kT3Block, kT3Slots, 3, SPNNZ_T3_UNROLL>();
         set_smem_attr<kT4Block, kT4Slots, 4, SPNNZ_T4_UNROLL>();
         set_smem_attr<kT5Block, kT5Slots, 5, SPNNZ_T5_UNROLL>();
-        attr_done |= 1u << (dev & 31);
+        attr_done.fetch_or(1ull << (dev & 63), std::memory_order_release);
     }
     const unsigned sms = static_cast<unsigned>(num_sms);
     k_sym_tiny<256><<<sms * 4, 256, 0, streams[0]>>>(args, s);
