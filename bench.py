@@ -184,6 +184,18 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- CPU side
+def cpu_model() -> str:
+    """Host CPU model (SURVEY §8d asks for it next to the core count)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_pipeline(a, b, info, cap, threads=0):
     """Times the reference's CPU path: oracle/_ref (the reference headers
     compiled in place) when present, else the C restatement.  Returns
@@ -235,7 +247,7 @@ def run_reference_arm(args, rank, world):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic", "config": {"workload": workload_name(args.config, info, args.cap),
                                          "parallelism": f"cpu threads={cores}"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": cpu_model(),
                          "sample": "full workload per step: compute_flop + make_sample_plan + "
                                    "run_prediction_with_plan + predict_row_structure_ceil"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -440,7 +452,7 @@ def run_ours(args, rank, world, local):
         cstep()
         tc = time.perf_counter() - t0
         cleanup()
-        cpu = {"value": a.nnz() / tc, "unit": UNIT, "cores": cores, "kind": kind,
+        cpu = {"value": a.nnz() / tc, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": cpu_model(),
                "sample": f"one full pass of the workload ({tc:.1f} s): compute_flop + "
                          "make_sample_plan + run_prediction_with_plan + predict_row_structure_ceil"}
 

@@ -231,9 +231,16 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
                   static_cast<unsigned long long>(acc));
 }
 
+#ifndef SPNNZ_T4_SLOTS
+#define SPNNZ_T4_SLOTS 16384
+#endif
+#ifndef SPNNZ_T4_BLOCKS_PER_SM
+#define SPNNZ_T4_BLOCKS_PER_SM 3
+#endif
 constexpr int kT3Block = 256, kT3Slots = 4096;
-constexpr int kT4Block = 512, kT4Slots = 16384;
+constexpr int kT4Block = 512, kT4Slots = SPNNZ_T4_SLOTS;
 constexpr int kT5Block = 1024, kT5Slots = 49152;
+static_assert(kT4Slots >= 2 * kBin4Max, "bin-4 table load <= 1/2");
 // keys in flight per lane (B.col loads issued together before the inserts)
 #ifndef SPNNZ_T3_UNROLL
 #define SPNNZ_T3_UNROLL 4
@@ -278,7 +285,7 @@ cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_s
     k_sym_tiny<256><<<sms * 4, 256, 0, streams[0]>>>(args, s);
     k_sym_warp_hash<256><<<sms * 4, 256, 0, streams[0]>>>(args, s);
     k_sym_block_hash<kT3Block, kT3Slots, 3, SPNNZ_T3_UNROLL><<<sms * 8, kT3Block, kT3Slots * 4, streams[1]>>>(args, s);
-    k_sym_block_hash<kT4Block, kT4Slots, 4, SPNNZ_T4_UNROLL><<<sms * 3, kT4Block, kT4Slots * 4, streams[2]>>>(args, s);
+    k_sym_block_hash<kT4Block, kT4Slots, 4, SPNNZ_T4_UNROLL><<<sms * SPNNZ_T4_BLOCKS_PER_SM, kT4Block, kT4Slots * 4, streams[2]>>>(args, s);
     k_sym_block_hash<kT5Block, kT5Slots, 5, SPNNZ_T5_UNROLL><<<sms, kT5Block, kT5Slots * 4, streams[3]>>>(args, s);
     return cudaGetLastError();
 }
