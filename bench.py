@@ -485,7 +485,12 @@ def run_ours(args, rank, world, local):
                          "gathers_per_s": nnz_local / (phase["flop"] * 1e-3) if phase["flop"] else 0.0,
                          "gather_peak_per_s": 287.6e9,
                          "gather_frac": (nnz_local / (phase["flop"] * 1e-3) / 287.6e9)
-                         if phase["flop"] else 0.0},
+                         if phase["flop"] else 0.0,
+                         # the same loads with none of the row logic, on this very
+                         # matrix (tools/microbench/flop_ceiling.cu, r01_microbench.md)
+                         "pattern_ceiling_ms": 1.500 if args.config == 5 and world == 1 else None,
+                         "pattern_ceiling_frac": (1.500 / phase["flop"]) if args.config == 5 and world == 1
+                         and phase["flop"] else None},
             # the other HBM-streaming kernel the north star names (fused into
             # the FLOP pass only under SPNNZ_FUSED_PREDICT=1)
             "roofline_predict": ({"fused": "into the FLOP pass (SPNNZ_FUSED_PREDICT=1)"}
