@@ -179,6 +179,7 @@ class Reference:
         L.ref_predict_row_structure_ceil.argtypes = [c_void_p, c_double, c_void_p]
         L.ref_predict_row_structure.argtypes = [c_void_p, c_double, c_void_p]
         L.ref_run_pipeline.argtypes = [c_void_p, c_void_p, c_uint64, c_double, c_int64, c_int, POINTER(RefReport), c_void_p]
+        L.ref_run_pipeline_ceil.argtypes = L.ref_run_pipeline.argtypes
         L.ref_error_report.argtypes = [c_double, c_double, c_int64, c_int64, c_int64, c_double, c_void_p]
         L.ref_splitmix_seq.argtypes = [c_uint64, c_int64, c_void_p]
         L.ref_matrix_export.argtypes = [c_void_p, POINTER(c_int32), POINTER(c_int32), POINTER(c_int64), c_void_p, c_void_p]
@@ -278,11 +279,16 @@ class Reference:
         self._chk(self.L.ref_predict_row_structure(prof, cr, out.ctypes.data))
         return out
 
-    def run_pipeline(self, ha, hb, seed, fraction, cap, rows, want_ceil=True):
+    def run_pipeline(self, ha, hb, seed, fraction, cap, rows, want_ceil=True, real_view=True):
+        """compute_flop + make_sample_plan + run_prediction_with_plan (which
+        also builds the real per-row view) + predict_row_structure_ceil; with
+        real_view=False the same functions composed without the real view
+        (the outputs the GPU step produces)."""
         rep = RefReport()
         ceil = np.empty(rows, np.int64) if want_ceil else None
-        self._chk(self.L.ref_run_pipeline(ha, hb, seed, fraction, cap if cap >= 0 else 2**63 - 1,
-                                          self.threads, byref(rep), ceil.ctypes.data if want_ceil else None))
+        fn = self.L.ref_run_pipeline if real_view else self.L.ref_run_pipeline_ceil
+        self._chk(fn(ha, hb, seed, fraction, cap if cap >= 0 else 2**63 - 1,
+                     self.threads, byref(rep), ceil.ctypes.data if want_ceil else None))
         return rep, ceil
 
     def error_report(self, z1, z2, f_star, Z, F, p):

@@ -183,6 +183,40 @@ int ref_run_pipeline(void* a, void* b, uint64_t seed, double fraction, int64_t c
     });
 }
 
+// The same outputs as the GPU step (report scalars + the integer per-row
+// view, no real view), composed from the reference's public functions in the
+// order run_prediction_with_plan calls them (predict.hpp:202-216) with
+// predict_row_structure_ceil (predict.hpp:140-151) in place of the real view.
+int ref_run_pipeline_ceil(void* a, void* b, uint64_t seed, double fraction, int64_t cap, int threads,
+                          ref_report* rep, int64_t* row_ceil) {
+    return guard([&] {
+        const spnnz::CsrMatrix& ma = static_cast<RefMatrix*>(a)->m;
+        const spnnz::CsrMatrix& mb = static_cast<RefMatrix*>(b)->m;
+        spnnz::SamplePolicy pol;
+        pol.fraction = fraction;
+        pol.cap = cap;
+        const spnnz::FlopProfile profile = spnnz::compute_flop(ma, mb, threads);
+        const spnnz::SamplePlan plan = spnnz::make_sample_plan(ma.rows, seed, pol);
+        const spnnz::RowNnzResult sampled = spnnz::sampled_symbolic(ma, mb, profile, plan.sample_rows, threads);
+        const spnnz::SampleStats stats = spnnz::collect_sample_stats(profile, plan, sampled);
+        const double z1 = spnnz::predict_reference(stats, plan);
+        const spnnz::ProposedPrediction proposed = spnnz::predict_proposed(stats, profile.total_flop);
+        std::vector<spnnz::offset_t> ceil_view =
+            spnnz::predict_row_structure_ceil(profile, proposed.predicted_cr);
+        rep->total_flop = profile.total_flop;
+        rep->max_flop_row = profile.max_flop_row;
+        rep->sample_num = plan.sample_num;
+        rep->p = plan.p;
+        rep->sampled_flop = stats.sampled_flop;
+        rep->sampled_nnz = stats.sampled_nnz;
+        rep->sampled_cr = stats.sampled_cr;
+        rep->z1_star = z1;
+        rep->z2_star = proposed.z2_star;
+        rep->predicted_cr = proposed.predicted_cr;
+        if (row_ceil) std::memcpy(row_ceil, ceil_view.data(), ceil_view.size() * 8);
+    });
+}
+
 int ref_error_report(double z1, double z2, int64_t f_star, int64_t exact_nnz, int64_t total_flop,
                      double p, double* out4) {
     return guard([&] {

@@ -306,3 +306,24 @@ def test_config_digests(oracle, golden, cfg):
         for k, v in rec["modes"][label]["report"].items():
             assert getattr(rep, k) == v, k
         assert digest(ceil) == rec["modes"][label]["ceil"]
+
+
+def test_reference_ceil_pipeline_equals_full_pipeline():
+    """bench.py's CPU arm composes the reference's functions without the real
+    per-row view (the GPU step's outputs); its report and integer view equal
+    those of the reference's run_prediction_with_plan pipeline."""
+    from oracle.pyoracle import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built")
+    R = Reference(threads=2)
+    a, _ = gen.make_config(1)
+    h = R.matrix(a)
+    try:
+        for cap in (UNCAPPED, 300, 5):
+            full, c_full = R.run_pipeline(h, h, 1, 0.01, cap, a.rows)
+            lean, c_lean = R.run_pipeline(h, h, 1, 0.01, cap, a.rows, real_view=False)
+            for k, _t in full._fields_:
+                assert getattr(full, k) == getattr(lean, k), k
+            assert (c_full == c_lean).all()
+    finally:
+        R.free_matrix(h)
