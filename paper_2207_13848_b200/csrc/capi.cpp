@@ -705,13 +705,22 @@ int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz
     c->rank = rank;
     c->world = world;
     c->num_sms = prop.multiProcessorCount;
-    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    // stream priorities (A/B knob SPNNZ_STREAM_PRIO): 1 = main stream (FLOP,
+    // heavy rows) above the symbolic side streams, 2 = the reverse
+    int prio_main = 0, prio_side = 0;
+    if (const char* pe = getenv("SPNNZ_STREAM_PRIO")) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (atoi(pe) == 1) prio_main = hi, prio_side = lo;
+        if (atoi(pe) == 2) prio_main = lo, prio_side = hi;
+    }
+    e = cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_main);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_totals, sizeof(long long) * kTotals);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_counts, sizeof(int32_t) * 16);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_meta, sizeof(long long) * kHeavyMeta);
     for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     for (int i = 0; i < spnnz_gpu_ctx::kSide && e == cudaSuccess; ++i)
-        e = cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking);
+        e = cudaStreamCreateWithPriority(&c->side[i], cudaStreamNonBlocking, prio_side);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->fstream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_rpt, cudaEventDisableTiming);
