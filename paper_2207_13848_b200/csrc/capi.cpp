@@ -195,6 +195,7 @@ struct spnnz_gpu_ctx {
     DBuf<long long> sorted_cnt;
     DBuf<int64_t> item_flop;  // FLOP of this rank's sampled rows (balanced multi-GPU pass)
     DBuf<int64_t> item_units; // their chunk offsets (flat item-FLOP decomposition)
+    DBuf<int64_t> item_window;  // [lo, hi) of the sampled rows this rank counts
     DBuf<int32_t> redo;       // fused predict: rows left to an IEEE division
     DBuf<unsigned long long> nredo;
     DBuf<int32_t> samples;
@@ -350,7 +351,7 @@ int heavy_buffers(spnnz_gpu_ctx* c, int64_t count, int64_t ents, int64_t product
 // total into totals[slot] (device); per-item results to out (device, nullable).
 int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64_t* d_out,
                  int slot, bool sampled_flop, int64_t* launches, const int64_t* item_flop = nullptr,
-                 const DevCsr* a_view = nullptr) {
+                 const DevCsr* a_view = nullptr, const int64_t* window = nullptr) {
     SymScratch s;
     RC(sym_scratch(c, n_items, &s));
     SymArgs g;
@@ -367,6 +368,7 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     g.totals = c->totals.p;
     g.total_slot = slot;
     g.sampled_flop = sampled_flop;
+    g.window = window;
     CU(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * 16, c->stream));
     CU(cudaMemsetAsync(c->heavy_meta.p, 0, sizeof(long long) * kHeavyMeta, c->stream));
     if (n_items == 0) return SPNNZ_OK;
@@ -557,16 +559,20 @@ struct SampleShare {
     const int32_t* rows = nullptr;
     int64_t n = 0;
     const int64_t* item_flop = nullptr;
+    const int64_t* window = nullptr;  // device [lo, hi) of the items this rank counts
     DevCsr full;
     bool use_full = false;
 };
 
 int sample_share(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool need_flop,
-                 SampleShare* sh, int64_t* launches) {
+                 SampleShare* sh, int64_t* launches, cudaStream_t stream = nullptr) {
+    if (!stream) stream = c->stream;
     sh->rows = d_rows;
     sh->n = n;
-    if (c->world > 1 && c->same_b) {
-        const int64_t lo = n * c->rank / c->world, hi = n * (c->rank + 1) / c->world;
+    const bool split = c->world > 1 && c->same_b;
+    if (split) {
+        // every rank holds all of A (it is the replicated B): each derives the
+        // FLOP of the whole list and counts a contiguous FLOP-balanced window
         sh->full.rows = c->b_rows;
         sh->full.cols = c->b_cols;
         sh->full.rpt = c->b_rpt.p;
@@ -574,17 +580,21 @@ int sample_share(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool need_f
         sh->full.base = 0;
         sh->full.nnz = c->b_nnz;
         sh->use_full = true;
-        sh->rows = d_rows + lo;
-        sh->n = hi - lo;
         need_flop = true;
     }
     if (need_flop) {
         RC(c->item_flop.ensure(std::max<int64_t>(sh->n, 1)));
         RC(c->item_units.ensure(sh->n + 1));
         CU(launch_item_flop(sh->use_full ? sh->full : c->a, c->b_rpt.p, sh->use_full ? 0 : c->row_lo,
-                            sh->rows, sh->n, c->item_flop.p, c->item_units.p, c->num_sms, c->stream));
+                            sh->rows, sh->n, c->item_flop.p, c->item_units.p, c->num_sms, stream));
         *launches += 3;
         sh->item_flop = c->item_flop.p;
+    }
+    if (split && sh->n > 0) {
+        RC(c->item_window.ensure(2));
+        CU(launch_flop_window(c->item_flop.p, sh->n, c->rank, c->world, c->item_window.p, stream));
+        ++*launches;
+        sh->window = c->item_window.p;
     }
     return SPNNZ_OK;
 }
@@ -606,16 +616,32 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
     SampleShare sh;
     if (!c->fused) {
         ev_record(c, 0);
-        RC(flop_pass(c, &launches));
-        ev_record(c, 1);
+        // the sampler and the rank's sampled-row FLOP / window need only A,
+        // B.rpt and the seed: they run on a side stream under the FLOP pass
+        // (latency-bound small kernels, off the critical path)
+        // (not while B is still landing from the host: the sampled rows read it)
+        const bool beside = !c->pending_upload;
+        cudaStream_t ss = beside ? c->side[0] : c->stream;
+        if (beside) {
+            CU(cudaEventRecord(c->fork, c->stream));
+            CU(cudaStreamWaitEvent(ss, c->fork, 0));
+        } else {
+            RC(flop_pass(c, &launches));
+        }
         if (draw) {
-            CU(launch_sample(seed, c->a_rows, n, c->samples.p, c->stream));
+            CU(launch_sample(seed, c->a_rows, n, c->samples.p, ss));
             ++launches;
         }
-        RC(sample_share(c, d_rows, n, false, &sh, &launches));
+        RC(sample_share(c, d_rows, n, false, &sh, &launches, ss));
+        if (beside) {
+            CU(cudaEventRecord(c->join[0], ss));
+            RC(flop_pass(c, &launches));
+        }
+        ev_record(c, 1);
+        if (beside) CU(cudaStreamWaitEvent(c->stream, c->join[0], 0));
         ev_record(c, 2);
         RC(run_symbolic(c, sh.rows, sh.n, nullptr, kZStar, true, &launches, sh.item_flop,
-                        sh.use_full ? &sh.full : nullptr));
+                        sh.use_full ? &sh.full : nullptr, sh.window));
         ev_record(c, 3);
         RC(allreduce_totals(c));
         ev_record(c, 4);
@@ -636,7 +662,7 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
         RC(sample_share(c, d_rows, n, true, &sh, &launches));
         ev_record(c, 1);
         RC(run_symbolic(c, sh.rows, sh.n, nullptr, kZStar, true, &launches, sh.item_flop,
-                        sh.use_full ? &sh.full : nullptr));
+                        sh.use_full ? &sh.full : nullptr, sh.window));
         ev_record(c, 2);
         RC(allreduce_totals(c, kFStar, 2, false));  // f*, z*: CR is known everywhere
         ev_record(c, 3);

@@ -29,6 +29,8 @@
 // Algorithmic bytes: 8(M+1) A.rpt + 4 nnz A.col + 8(K+1) B.rpt + 8M flop
 // (the 2K-byte degree array's write and re-reads are extra traffic).
 // Integer-only: bit-exact.
+#include <atomic>
+
 #include <cub/block/block_scan.cuh>
 
 #include "device_common.cuh"
@@ -483,25 +485,39 @@ __global__ void __launch_bounds__(256) k_item_chunks(DevCsr a, int32_t row_lo, c
 }
 
 // In-place exclusive scan of units[0..n) by one block; units[n] = total.
+// Thread t owns the contiguous run [t c, (t + 1) c), c = ceil(n / BLOCK),
+// staged through shared memory when the list fits (coalesced loads and
+// stores, one block scan of the run sums); a scan per BLOCK items made this a
+// chain of barriers (~2 us per 1024 items).
+constexpr int kScanSmemItems = 24576;  // 192 KB of int64
+
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_item_scan(int64_t* __restrict__ units, int64_t n) {
     using Scan = cub::BlockScan<long long, BLOCK>;
     __shared__ typename Scan::TempStorage tmp;
-    __shared__ long long s_carry;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < n; base += BLOCK) {
-        const int64_t s = base + threadIdx.x;
-        const long long v = s < n ? units[s] : 0;
-        long long excl, total;
-        Scan(tmp).ExclusiveSum(v, excl, total);
-        const long long carry = s_carry;
-        if (s < n) units[s] = carry + excl;
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry = carry + total;
+    extern __shared__ long long s_items[];
+    const bool staged = n <= kScanSmemItems;
+    long long* v = staged ? s_items : reinterpret_cast<long long*>(units);
+    if (staged) {
+        for (int64_t i = threadIdx.x; i < n; i += BLOCK) s_items[i] = units[i];
         __syncthreads();
     }
-    if (threadIdx.x == 0) units[n] = s_carry;
+    const int64_t c = (n + BLOCK - 1) / BLOCK;
+    const int64_t i0 = threadIdx.x * c, i1 = i0 + c < n ? i0 + c : n;
+    long long sum = 0;
+    for (int64_t i = i0; i < i1; ++i) sum += v[i];
+    long long ex, tot;
+    Scan(tmp).ExclusiveSum(sum, ex, tot);
+    for (int64_t i = i0; i < i1; ++i) {
+        const long long x = v[i];
+        v[i] = ex;
+        ex += x;
+    }
+    if (staged) {
+        __syncthreads();
+        for (int64_t i = threadIdx.x; i < n; i += BLOCK) units[i] = s_items[i];
+    }
+    if (threadIdx.x == 0) units[n] = tot;
 }
 
 __global__ void __launch_bounds__(256) k_item_flop(DevCsr a, const int64_t* __restrict__ brpt,
@@ -534,6 +550,47 @@ __global__ void __launch_bounds__(256) k_item_flop(DevCsr a, const int64_t* __re
     }
 }
 
+// Rank r counts the items whose FLOP prefix P[i] lies in [T_r, T_{r+1}),
+// T_r = floor(total r / world) (the last rank also takes P[i] = total), so
+// the ranks split the list into contiguous, FLOP-balanced windows whatever
+// the order of heavy and light rows.  One block: the list is the sample.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_flop_window(const int64_t* __restrict__ f, int64_t n, int rank,
+                                                      int world, int64_t* __restrict__ window) {
+    using Scan = cub::BlockScan<long long, BLOCK>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ long long s_red[BLOCK / 32];
+    extern __shared__ long long s_items[];
+    const bool staged = n <= kScanSmemItems;  // coalesced loads, as k_item_scan
+    const long long* v = staged ? s_items : reinterpret_cast<const long long*>(f);
+    if (staged) {
+        for (int64_t i = threadIdx.x; i < n; i += BLOCK) s_items[i] = f[i];
+        __syncthreads();
+    }
+    const int64_t c = (n + BLOCK - 1) / BLOCK;  // thread t owns items [t c, (t + 1) c)
+    const int64_t i0 = threadIdx.x * c, i1 = i0 + c < n ? i0 + c : n;
+    long long sum = 0;
+    for (int64_t i = i0; i < i1; ++i) sum += v[i];
+    long long ex, total;
+    Scan(tmp).ExclusiveSum(sum, ex, total);  // total is broadcast to every thread
+    const auto split = [&](int r) -> long long {  // floor(total r / world) without overflow
+        return (total / world) * r + (total % world) * r / world;
+    };
+    const long long t_lo = split(rank), t_hi = split(rank + 1);
+    long long below_lo = 0, below_hi = 0;  // items with P[i] < T_r, < T_{r+1}
+    for (int64_t i = i0; i < i1; ++i) {
+        below_lo += ex < t_lo;
+        below_hi += ex < t_hi;
+        ex += v[i];
+    }
+    below_lo = block_sum_ll<BLOCK>(below_lo, s_red);  // valid in warp 0
+    below_hi = block_sum_ll<BLOCK>(below_hi, s_red);
+    if (threadIdx.x == 0) {
+        window[0] = rank == 0 ? 0 : below_lo;
+        window[1] = rank == world - 1 ? n : below_hi;
+    }
+}
+
 // Row-sortedness of B (the CsrMatrix invariant, csr.hpp:16-18), checked once
 // at load: every descent col[j] < col[j-1] must sit at the start of a
 // non-empty row.  cnt[0] += descents over all j, cnt[1] += descents at row
@@ -561,6 +618,21 @@ __global__ void k_start_descents(const int64_t* __restrict__ rpt, const int32_t*
 
 }  // namespace
 
+cudaError_t launch_flop_window(const int64_t* item_flop, int64_t n, int rank, int world, int64_t* window,
+                               cudaStream_t stream) {
+    static std::atomic<unsigned long long> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_done.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
+        cudaFuncSetAttribute(k_flop_window<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanSmemItems * 8);
+        cudaFuncSetAttribute(k_item_scan<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanSmemItems * 8);
+        attr_done.fetch_or(1ull << (dev & 63), std::memory_order_release);
+    }
+    const size_t smem = n <= kScanSmemItems ? size_t(n) * 8 : 0;
+    k_flop_window<1024><<<1, 1024, smem, stream>>>(item_flop, n, rank, world, window);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_item_flop(const DevCsr& a, const int64_t* brpt, int32_t row_lo,
                              const int32_t* rows, int64_t n, int64_t* out, int64_t* units, int num_sms,
                              cudaStream_t stream) {
@@ -568,7 +640,14 @@ cudaError_t launch_item_flop(const DevCsr& a, const int64_t* brpt, int32_t row_l
     int64_t g1 = (n + 255) / 256;
     if (g1 > int64_t(num_sms) * 4) g1 = int64_t(num_sms) * 4;
     k_item_chunks<<<static_cast<unsigned>(g1), 256, 0, stream>>>(a, row_lo, rows, n, units, out);
-    k_item_scan<1024><<<1, 1024, 0, stream>>>(units, n);
+    static std::atomic<unsigned long long> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_done.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
+        cudaFuncSetAttribute(k_item_scan<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, kScanSmemItems * 8);
+        attr_done.fetch_or(1ull << (dev & 63), std::memory_order_release);
+    }
+    k_item_scan<1024><<<1, 1024, n <= kScanSmemItems ? size_t(n) * 8 : 0, stream>>>(units, n);
     k_item_flop<<<static_cast<unsigned>(num_sms) * 8, 256, 0, stream>>>(a, brpt, row_lo, rows, n, units, out);
     return cudaGetLastError();
 }

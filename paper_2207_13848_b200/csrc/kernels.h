@@ -201,6 +201,7 @@ struct SymArgs {
     long long* totals = nullptr;
     int total_slot = kZStar;        // kZStar (sampled) or kZ (exact)
     bool sampled_flop = false;      // also accumulate f* into totals[kFStar]
+    const int64_t* window = nullptr;  // device [lo, hi): the items this rank counts (nullable = all)
 };
 
 // Classifies items into bins (writes out[] = 0 for empty / foreign rows).
@@ -239,6 +240,10 @@ cudaError_t launch_sampled_flop(const int64_t* flop, int32_t row_lo, int32_t loc
 cudaError_t launch_item_flop(const DevCsr& a, const int64_t* brpt, int32_t row_lo,
                              const int32_t* rows, int64_t n, int64_t* out, int64_t* units, int num_sms,
                              cudaStream_t stream);
+// FLOP-balanced share of a sample list: window[0..1] = [lo, hi) such that
+// rank's items carry ~1/world of the list's total FLOP (item_flop[n]).
+cudaError_t launch_flop_window(const int64_t* item_flop, int64_t n, int rank, int world, int64_t* window,
+                               cudaStream_t stream);
 // B rows non-decreasing? cnt[0] == cnt[1] afterwards (device counters).
 cudaError_t launch_check_sorted(const int64_t* rpt, const int32_t* col, int32_t rows, int64_t nnz,
                                 unsigned long long* cnt, int num_sms, cudaStream_t stream);

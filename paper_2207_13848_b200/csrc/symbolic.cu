@@ -42,7 +42,8 @@ __global__ void __launch_bounds__(BLOCK) k_sym_bin(SymArgs g, SymScratch sc) {
         if (s < g.n_items) {
             const int32_t rid = g.rows ? g.rows[s] : g.row_lo + static_cast<int32_t>(s);
             const int32_t r = rid - g.row_lo;
-            if (r >= 0 && r < g.a.rows) {
+            const bool mine = !g.window || (s >= g.window[0] && s < g.window[1]);
+            if (mine && r >= 0 && r < g.a.rows) {
                 const int64_t f = g.item_flop ? g.item_flop[s] : g.flop[r];
                 fsum += f;
                 bin = f == 0 ? 0 : f <= kBin1Max ? 1 : f <= kBin2Max ? 2 : f <= kBin3Max ? 3

@@ -94,3 +94,74 @@ def test_two_rank_prediction_equals_single(cap):
     # the shards are nnz-balanced (within one row's worth)
     nnz = [int(a.rpt[p[1]] - a.rpt[p[0]]) for p in parts]
     assert abs(nnz[0] - nnz[1]) <= int(np.diff(a.rpt).max()) + 1
+
+
+def flop_window(item_flop, rank, world):
+    """The FLOP-balanced share of a sample list that rank counts when every
+    rank holds all of A (C = A*A; csrc/flop.cu k_flop_window): items whose
+    exclusive FLOP prefix lies in [T_r, T_{r+1}), T_r = floor(total r / W),
+    the last rank taking the rest."""
+    total = int(item_flop.sum())
+    t = [(total // world) * r + (total % world) * r // world for r in range(world + 1)]
+    pre = np.concatenate([[0], np.cumsum(item_flop)[:-1]]) if len(item_flop) else np.zeros(0, np.int64)
+    lo = 0 if rank == 0 else int((pre < t[rank]).sum())
+    hi = len(item_flop) if rank == world - 1 else int((pre < t[rank + 1]).sum())
+    return lo, hi
+
+
+def _worker_window(rank, world, port, cfg, results):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.pyoracle import Oracle
+        from paper_2207_13848_b200 import capi, gen
+        O = Oracle(threads=1)
+        a = gen.rmat(*cfg[0])
+        seed, frac, cap = cfg[1:]
+        bounds = np.zeros(world + 1, np.int32)
+        capi.check(capi.lib().spnnz_gpu_partition_rows(a.rpt.ctypes.data, a.rows, world,
+                                                        bounds.ctypes.data))
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        F = int(O.compute_flop(_slice(a, lo, hi), a)[0].sum())      # local FLOP pass
+        full, _, mx = O.compute_flop(a, a)                            # every rank holds all of A
+        rows, n, p = O.make_sample_plan(a.rows, seed, frac, cap)
+        item = full[rows.astype(np.int64)]                            # sampled rows' FLOP
+        wlo, whi = flop_window(item, rank, world)
+        mine = rows[wlo:whi]
+        fs = int(item[wlo:whi].sum())
+        zs = O.sampled_symbolic(a, a, full, mx, mine)[1] if len(mine) else 0
+        t = torch.tensor([F, fs, zs], dtype=torch.int64)
+        dist.all_reduce(t)
+        parts = [None] * world
+        dist.all_gather_object(parts, (wlo, whi, int(item[wlo:whi].sum())))
+        if rank == 0:
+            results.put((tuple(int(x) for x in t), parts, int(item.sum())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_flop_balanced_sample_split_equals_single(world):
+    """C = A*A on several ranks: the sample list is split into contiguous,
+    FLOP-balanced windows; the windows tile the list and the all-reduced
+    {F, f*, z*} equal the single-process values."""
+    import torch.multiprocessing as mp
+    from oracle.pyoracle import Oracle
+    from paper_2207_13848_b200 import gen
+    cfg = ((14, 16 << 14, 0.57, 0.19, 0.19, 2), 7, 0.02, -1)
+    q = mp.get_context("spawn").SimpleQueue()
+    procs = mp.start_processes(_worker_window, args=(world, _free_port(), cfg, q), nprocs=world,
+                               join=False, start_method="spawn")
+    tot, parts, fsum = q.get()
+    while not procs.join():
+        pass
+    a = gen.rmat(*cfg[0])
+    rep = Oracle().run_prediction(a, a, cfg[1], cfg[2], cfg[3])[0]
+    assert tot == (rep.total_flop, rep.sampled_flop, rep.sampled_nnz)
+    parts.sort()
+    assert parts[0][0] == 0 and parts[-1][1] == rep.sample_num
+    assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+    # balanced: every window within one row's FLOP of its share
+    assert max(abs(f - fsum / world) for _, _, f in parts) <= rep.max_flop_row + 1
