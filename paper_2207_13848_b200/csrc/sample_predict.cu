@@ -32,6 +32,10 @@ __global__ void k_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* __
     rows[r] = rid;
 }
 
+#ifndef SPNNZ_PRED_U
+#define SPNNZ_PRED_U 4
+#endif
+
 template <bool CEIL, bool REAL>
 __global__ void __launch_bounds__(256)
 k_predict(const int64_t* __restrict__ flop, int64_t m, const long long* __restrict__ totals,
@@ -45,9 +49,6 @@ k_predict(const int64_t* __restrict__ flop, int64_t m, const long long* __restri
                           (REAL ? reinterpret_cast<uintptr_t>(real_out) : 0)) & 15) == 0;
     if (vec_ok) {
         // kU pairs per thread per step, their loads issued back to back
-#ifndef SPNNZ_PRED_U
-#define SPNNZ_PRED_U 4
-#endif
         constexpr int kU = SPNNZ_PRED_U;
         const longlong2* f2 = reinterpret_cast<const longlong2*>(flop);
         for (int64_t i0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i0 < pairs; i0 += kU * stride) {
@@ -100,7 +101,10 @@ cudaError_t launch_predict(const int64_t* flop, int64_t m, const long long* tota
     // 32 blocks of 256 per SM (measured best of 4-32 x unroll 1-8 at
     // config 5: 0.068 ms, 60 % of the copy bandwidth), grid-stride over
     // 16-byte pairs.
-    int64_t grid = ((m >> 1) + 255) / 256;
+    // one block per 256 threads x SPNNZ_PRED_U pairs, so a small shard (a
+    // rank's rows at N = 8) runs as one wave with every load in flight
+    // instead of several waves of one pair per thread (19 -> ~7 us at 2.7 M rows)
+    int64_t grid = ((m >> 1) + 256 * SPNNZ_PRED_U - 1) / (256 * SPNNZ_PRED_U);
 #ifndef SPNNZ_PRED_GRID
 #define SPNNZ_PRED_GRID 32
 #endif
