@@ -127,35 +127,6 @@ __device__ __forceinline__ int warp_bucket_add(int* counters, int bucket) {
     return base + __popc(peers & ((1u << lane) - 1));
 }
 
-#ifndef SPNNZ_HASH_BUCKET
-#define SPNNZ_HASH_BUCKET 0
-#endif
-// Bucketed open addressing: `size` slots as size/4 buckets of four (one
-// 16-byte shared-memory read per probe), linear probing over buckets.  A
-// bucket's slots fill in order and are never emptied, so a key is found
-// before the first empty slot of its probe sequence; a lost CAS re-reads the
-// same bucket.  At the tiers' load factors almost every insert is one probe,
-// which keeps the 32 lanes of a warp in step (per-slot linear probing made
-// the warp wait for its longest chain: ~2.9 probe rounds per key in bin 5).
-// The table (and size) must be 16-byte aligned (a multiple of 4).
-__device__ __forceinline__ int hash_insert_bucket(int* table, uint32_t size, int key) {
-    const uint32_t nb = size >> 2;
-    uint32_t h = __umulhi(mix32(static_cast<uint32_t>(key)), nb);
-    const int4* t4 = reinterpret_cast<const int4*>(table);
-    for (;;) {
-        const int4 v = t4[h];
-        if (v.x == key || v.y == key || v.z == key || v.w == key) return 0;
-        const int slot = v.x == kEmpty ? 0 : v.y == kEmpty ? 1 : v.z == kEmpty ? 2 : v.w == kEmpty ? 3 : 4;
-        if (slot < 4) {
-            const int prev = atomicCAS(&table[4 * h + slot], kEmpty, key);
-            if (prev == kEmpty) return 1;
-            if (prev == key) return 0;
-            continue;  // another key took the slot: re-read the bucket
-        }
-        h = (h + 1 == nb) ? 0 : h + 1;
-    }
-}
-
 // Fills a table with kEmpty using 16-byte stores (size a multiple of 4).
 __device__ __forceinline__ void hash_clear(int* table, int size, int t, int nt) {
     int4* t4 = reinterpret_cast<int4*>(table);
@@ -193,14 +164,12 @@ struct HashSinkU {
     uint32_t size;
     int* cnt;
     __device__ __forceinline__ void operator()(const int (&keys)[U], const bool (&valid)[U], long long) const {
-#if SPNNZ_HASH_PTX && !SPNNZ_HASH_BUCKET
+#if SPNNZ_HASH_PTX
         const uint32_t ts = static_cast<uint32_t>(__cvta_generic_to_shared(table));
 #endif
 #pragma unroll
         for (int u = 0; u < U; ++u)
-#if SPNNZ_HASH_BUCKET
-            if (valid[u]) *cnt += hash_insert_bucket(table, size, keys[u]);
-#elif SPNNZ_HASH_PTX
+#if SPNNZ_HASH_PTX
             if (valid[u]) *cnt += hash_insert_shared(ts, size, keys[u]);
 #else
             if (valid[u]) *cnt += hash_insert(table, size, keys[u]);
