@@ -732,3 +732,25 @@ def test_fuzz_pipeline_vs_oracle(oracle, case, monkeypatch):
     assert rep.predicted_cr == o.predicted_cr and rep.z2_star == o.z2_star
     assert (rep.predicted_row_nnz_ceil == oceil).all() and (rep.predicted_row_nnz == oreal).all()
     q.close()
+
+
+def test_detached_shards_more_ranks_than_heavy_samples(oracle):
+    """FLOP-balanced windows when the ranks outnumber the useful samples: a
+    matrix whose sampled FLOP sits in one hub row plus empty rows; 8 detached
+    ranks still sum to the single-GPU f* and z*."""
+    n = 4000
+    rows = [list(range(0, n, 3))] + [[] for _ in range(n - 2)] + [[5, 6]]
+    a = csr(n, n, rows)
+    single = Predictor(0)
+    single.load(a)
+    ref = single.run_prediction(3, SamplePolicy(0.002, UNCAPPED))
+    single.close()
+    fs = zs = 0
+    for r in range(8):
+        q = Predictor(0, r, 8)
+        q.load(a)
+        rep = q.run_prediction(3, SamplePolicy(0.002, UNCAPPED))
+        fs += rep.stats.sampled_flop
+        zs += rep.stats.sampled_nnz
+        q.close()
+    assert (fs, zs) == (ref.stats.sampled_flop, ref.stats.sampled_nnz)
