@@ -151,6 +151,7 @@ struct spnnz_gpu_ctx {
     static constexpr int kSide = 4;
     cudaStream_t side[kSide] = {};        // symbolic tiers, concurrent with the heavy rows
     cudaEvent_t fork = nullptr, join[kSide] = {};
+    cudaEvent_t ev_bin = nullptr, ev_flop = nullptr;  // early binning (run_symbolic)
     ncclComm_t comm = nullptr;
 
     // matrices
@@ -349,9 +350,17 @@ int heavy_buffers(spnnz_gpu_ctx* c, int64_t count, int64_t ents, int64_t product
 
 // Symbolic pass over items (sampled rows or all local rows).  Adds the
 // total into totals[slot] (device); per-item results to out (device, nullable).
+// early (bin_stream set): the binning runs on bin_stream while the FLOP pass
+// (already queued on c->stream, ending in c->ev_flop) is still running, so
+// the host learns the heavy count without waiting for it; the tiers wait for
+// the FLOP pass and the heavy batches queue behind it on c->stream -- no
+// host round trip between the FLOP pass and the symbolic work.
 int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64_t* d_out,
                  int slot, bool sampled_flop, int64_t* launches, const int64_t* item_flop = nullptr,
-                 const DevCsr* a_view = nullptr, const int64_t* window = nullptr) {
+                 const DevCsr* a_view = nullptr, const int64_t* window = nullptr,
+                 cudaStream_t bin_stream = nullptr) {
+    const bool early = bin_stream != nullptr;
+    cudaStream_t bs = early ? bin_stream : c->stream;
     SymScratch s;
     RC(sym_scratch(c, n_items, &s));
     SymArgs g;
@@ -369,23 +378,30 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     g.total_slot = slot;
     g.sampled_flop = sampled_flop;
     g.window = window;
-    CU(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * 16, c->stream));
-    CU(cudaMemsetAsync(c->heavy_meta.p, 0, sizeof(long long) * kHeavyMeta, c->stream));
+    CU(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * 16, bs));
+    CU(cudaMemsetAsync(c->heavy_meta.p, 0, sizeof(long long) * kHeavyMeta, bs));
     if (n_items == 0) return SPNNZ_OK;
-    CU(launch_sym_bin(g, s, c->stream));
+    CU(launch_sym_bin(g, s, bs));
     // The host learns the heavy rows' number (bin counts) while the tier
     // kernels run on side streams; the heavy batches then run on the main
     // stream concurrently with the tiers, joined at the end.
-    CU(cudaEventRecord(c->fork, c->stream));
-    CU(cudaMemcpyAsync(c->h_counts, c->counts.p, sizeof(int32_t) * 16, cudaMemcpyDeviceToHost,
-                       c->stream));
-    CU(cudaMemcpyAsync(c->h_meta, c->heavy_meta.p, sizeof(long long) * kHeavyMeta, cudaMemcpyDeviceToHost,
-                       c->stream));
-    for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaStreamWaitEvent(c->side[i], c->fork, 0));
+    CU(cudaEventRecord(c->fork, bs));
+    CU(cudaMemcpyAsync(c->h_counts, c->counts.p, sizeof(int32_t) * 16, cudaMemcpyDeviceToHost, bs));
+    CU(cudaMemcpyAsync(c->h_meta, c->heavy_meta.p, sizeof(long long) * kHeavyMeta, cudaMemcpyDeviceToHost, bs));
+    if (early) CU(cudaEventRecord(c->ev_bin, bs));
+    for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) {
+        CU(cudaStreamWaitEvent(c->side[i], c->fork, 0));
+        if (early) CU(cudaStreamWaitEvent(c->side[i], c->ev_flop, 0));
+    }
     CU(launch_sym_tiers(g, s, c->num_sms, c->side));
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaEventRecord(c->join[i], c->side[i]));
     *launches += 6;
-    CU(cudaStreamSynchronize(c->stream));  // bin + the two small copies
+    if (early) {
+        CU(cudaEventSynchronize(c->ev_bin));             // bin + the two small copies only
+        CU(cudaStreamWaitEvent(c->stream, c->fork, 0));  // heavy batches: after the bin
+    } else {
+        CU(cudaStreamSynchronize(c->stream));  // bin + the two small copies
+    }
     const int64_t heavy = c->h_counts[kHeavyBin];
     if (heavy > 0) {
         // One batch when the heavy rows fit the batch budgets (always for
@@ -632,16 +648,17 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
             CU(launch_sample(seed, c->a_rows, n, c->samples.p, ss));
             ++launches;
         }
-        RC(sample_share(c, d_rows, n, false, &sh, &launches, ss));
+        // beside the FLOP pass the sampled rows' FLOP is derived directly, so
+        // the binning need not wait for the pass either (early run_symbolic)
+        RC(sample_share(c, d_rows, n, beside, &sh, &launches, ss));
         if (beside) {
-            CU(cudaEventRecord(c->join[0], ss));
             RC(flop_pass(c, &launches));
+            CU(cudaEventRecord(c->ev_flop, c->stream));
         }
         ev_record(c, 1);
-        if (beside) CU(cudaStreamWaitEvent(c->stream, c->join[0], 0));
         ev_record(c, 2);
         RC(run_symbolic(c, sh.rows, sh.n, nullptr, kZStar, true, &launches, sh.item_flop,
-                        sh.use_full ? &sh.full : nullptr, sh.window));
+                        sh.use_full ? &sh.full : nullptr, sh.window, beside ? ss : nullptr));
         ev_record(c, 3);
         RC(allreduce_totals(c));
         ev_record(c, 4);
@@ -754,6 +771,8 @@ int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz
     for (int i = 0; i < spnnz_gpu_ctx::kChunks && e == cudaSuccess; ++i)
         e = cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_bin, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_flop, cudaEventDisableTiming);
     for (int i = 0; i < spnnz_gpu_ctx::kSide && e == cudaSuccess; ++i)
         e = cudaEventCreateWithFlags(&c->join[i], cudaEventDisableTiming);
     int rc = SPNNZ_OK;
@@ -820,6 +839,8 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
         if (c->join[i]) cudaEventDestroy(c->join[i]);
     }
     if (c->fork) cudaEventDestroy(c->fork);
+    if (c->ev_bin) cudaEventDestroy(c->ev_bin);
+    if (c->ev_flop) cudaEventDestroy(c->ev_flop);
     for (auto ev : c->ev_chunk)
         if (ev) cudaEventDestroy(ev);
     if (c->ev_rpt) cudaEventDestroy(c->ev_rpt);
