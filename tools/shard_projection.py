@@ -37,6 +37,11 @@ def main():
     from paper_2207_13848_b200.spnnz import Predictor, SamplePolicy
 
     info = gen.CONFIGS[args.config]
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        peak = 6650.0  # the profiling recipe's fallback
     a, b = gen.make_config(args.config)
     policy = SamplePolicy(info["fraction"], -1)
     out = {"config": info["name"], "nnz_A": a.nnz(), "kind": "detached shards on one GPU (projection)",
@@ -71,7 +76,14 @@ def main():
             torch.cuda.synchronize()
             P.set_profiling(False)
             ms = float(np.mean([s.elapsed_time(e) for s, e in ev]))
-            per_rank.append({"rank": rank, "rows": P.local_rows, "ms": ms,
+            # the FLOP pass of this rank against the HBM roofline (bench.py's
+            # algorithmic bytes for its shard, measured copy peak)
+            nnz_local = int(a.rpt[P.row_hi] - a.rpt[P.row_lo])
+            fbytes = 8 * (P.local_rows + 1) + 4 * nnz_local + 8 * (b.rows + 1) + 8 * P.local_rows
+            flop_ms = phase[0] / args.steps
+            per_rank.append({"rank": rank, "rows": P.local_rows, "nnz": nnz_local, "ms": ms,
+                             "flop_pass_GBps": fbytes / (flop_ms * 1e-3) / 1e9 if flop_ms else None,
+                             "flop_pass_hbm_frac": fbytes / (flop_ms * 1e-3) / 1e9 / peak if flop_ms else None,
                              "phases_ms": dict(zip(("flop", "sample", "symbolic", "allreduce", "predict"),
                                                    (phase / args.steps).round(4).tolist()))})
             P.close()
@@ -81,6 +93,8 @@ def main():
         mean = float(np.mean([r["ms"] for r in per_rank]))
         out["per_world"][str(world)] = {"max_ms": mx, "mean_ms": mean, "imbalance": mx / mean,
                                         "projected_A_nnz_per_s": a.nnz() / (mx * 1e-3),
+                                        "flop_pass_hbm_frac_mean": float(np.mean(
+                                            [r["flop_pass_hbm_frac"] or 0 for r in per_rank])),
                                         "ranks": per_rank}
     base = out["per_world"].get("1") if args.only_rank < 0 else None
     if base:
