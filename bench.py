@@ -365,7 +365,9 @@ def run_ours(args, rank, world, local):
         barrier()
         clk.mark(1)
     P.set_profiling(False)
-    ms = float(sum(s.elapsed_time(e) for s, e in ev)) / args.steps
+    step_ms = [s.elapsed_time(e) for s, e in ev]
+    ms = float(sum(step_ms)) / args.steps
+    ms_median = float(np.median(step_ms))  # SURVEY §8d asks for the median of >= 10 runs
     for k in phase:
         phase[k] /= args.steps
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -463,6 +465,7 @@ def run_ours(args, rank, world, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "ms_per_step_median_rank0": ms_median,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (seeded generator, BASELINE.json config shapes)",
             "config": {"workload": workload_name(args.config, info, args.cap),
