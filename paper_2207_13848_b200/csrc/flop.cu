@@ -114,10 +114,19 @@ __global__ void k_degree(const int64_t* __restrict__ brpt, int64_t k_rows,
         }
         asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(deg + k), "l"(packed), "l"(last));
         if (mk.tile_row) {
+            // a row marks tiles only when it crosses a tile boundary: one
+            // compare of the tile indices of its ends (equal for empty rows)
+            constexpr int kShift = __builtin_ctz(kFlopTile);
+            uint64_t q[5];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int64_t row = k + j + 1 - mk.a_off;
-                if (r[j + 1] > r[j] && row >= 1 && row <= mk.m) mk.row(static_cast<int32_t>(row), r[j], r[j + 1]);
+            for (int j = 0; j < 5; ++j) q[j] = static_cast<uint64_t>(r[j]) >> kShift;
+            if (q[0] != q[4]) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int64_t row = k + j + 1 - mk.a_off;
+                    if (q[j] != q[j + 1] && row >= 1 && row <= mk.m)
+                        mk.row(static_cast<int32_t>(row), r[j], r[j + 1]);
+                }
             }
         }
     }
