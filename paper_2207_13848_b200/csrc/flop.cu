@@ -25,7 +25,13 @@
 //   3. k_flop_fixup adds the leading segments to the long rows they continue
 //      and reduces F and max over tiles.
 // No shared-memory round trip per entry: the L1/shared pipe is left to the
-// gathers, which bound the pass (~1 L2 request per entry).
+// gathers, which bound the pass (~1 L2 request per entry; at config 5 the pass
+// runs at 86-89 % of the same loads with no row logic,
+// tools/microbench/flop_ceiling.cu).
+// Also here: the FLOP of listed rows straight from A and B.rpt (a flat
+// decomposition into 128-entry chunks: the sampled rows' FLOP the symbolic
+// binning and the multi-GPU split use) and the FLOP-balanced window of a
+// sample list a rank counts (k_flop_window).
 // Algorithmic bytes: 8(M+1) A.rpt + 4 nnz A.col + 8(K+1) B.rpt + 8M flop
 // (the 2K-byte degree array's write and re-reads are extra traffic).
 // Integer-only: bit-exact.
