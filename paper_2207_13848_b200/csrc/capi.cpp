@@ -617,6 +617,12 @@ int sample_share(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool need_f
 
 // Pipeline body shared by run_prediction and run_prediction_with_plan:
 // FLOP pass -> sampler -> sampled symbolic -> one all-reduce -> predict pass.
+// Default schedule (inputs resident): the sampler, the sampled rows' FLOP
+// (and on multi-GPU their FLOP-balanced window) and the binning run on a side
+// stream underneath the FLOP pass; the host reads the heavy count meanwhile
+// and queues the symbolic tiers and heavy batches behind the pass (see
+// run_symbolic's early mode).  While B is still landing from the host
+// (chunked upload) the FLOP pass goes first and the rest follows it.
 // With c->fused (SPNNZ_FUSED_PREDICT=1) the sampled rows' FLOP
 // is derived directly so the symbolic pass and CR come first, and one FLOP
 // pass writes every row's flop together with its prediction (two
