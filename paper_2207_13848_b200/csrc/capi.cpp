@@ -440,7 +440,8 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
         }
         for (const Batch& b : batches) {
             RC(heavy_buffers(c, b.count, b.ents, b.products, b.cells, &s));
-            CU(launch_sym_heavy(g, s, iv, b.first, b.count, c->num_sms, c->stream, launches));
+            CU(launch_sym_heavy(g, s, iv, b.first, b.count, c->num_sms, c->stream, launches,
+                                c->pending_upload ? nullptr : c->fstream, c->ev_bin, c->ev_flop));
         }
     }
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaStreamWaitEvent(c->stream, c->join[i], 0));

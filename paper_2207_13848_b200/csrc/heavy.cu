@@ -1195,7 +1195,8 @@ cudaError_t launch_heavy_flops(const SymArgs& args, const SymScratch& s, int64_t
 }
 
 cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sorted, int64_t first,
-                             int64_t count, int num_sms, cudaStream_t stream, int64_t* launches) {
+                             int64_t count, int num_sms, cudaStream_t stream, int64_t* launches,
+                             cudaStream_t aux, cudaEvent_t ev_a, cudaEvent_t ev_b) {
     if (count == 0) return cudaSuccess;
     int64_t n = 0;  // kernels launched (memsets not counted)
     static std::atomic<unsigned long long> attr_done{0};  // one bit per device; the sets are idempotent
@@ -1237,9 +1238,20 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
         if (geo.unit_sorted) {
             k_heavy_sort_units<<<sms * 6, kHB, sort_smem(R), stream>>>(args, s, first, count, R, geo.wshift);
             k_heavy_plan_units<<<items, kPrivRanges, 0, stream>>>(s, count, R, s.heavy_task_cap);
+            // the bitmap tasks and the small hash tasks are independent: on
+            // two streams (aux given) each fills the other's tail
+            if (aux) {
+                cudaEventRecord(ev_a, stream);
+                cudaStreamWaitEvent(aux, ev_a, 0);
+            }
             k_heavy_run_units<512><<<sms * SPNNZ_RUN_GRID, 512, (1 << kTaskSpanShift) / 8, stream>>>(
                 args, s, first, R, geo.wshift, geo.wwords);
-            k_heavy_run_small<<<sms * 3, kSG * kSGroups, kSGroups * kSSlots * 4, stream>>>(args, s, first, R);
+            k_heavy_run_small<<<sms * 3, kSG * kSGroups, kSGroups * kSSlots * 4, aux ? aux : stream>>>(
+                args, s, first, R);
+            if (aux) {
+                cudaEventRecord(ev_b, aux);
+                cudaStreamWaitEvent(stream, ev_b, 0);
+            }
             n += 4;
         } else {
             k_heavy_count<<<sms * 8, kHB, 0, stream>>>(args, s, first, count, R, geo.wshift);

@@ -214,8 +214,11 @@ cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_s
 // Heavy tier for entries [first, first + count) of the heavy list (the host
 // learns the count after a sync and sizes the batch's buffers).
 // sorted: B rows non-decreasing -> the interval path (no product buffer).
+// aux (nullable): a second stream for the small-range tasks, forked and
+// joined through the events ev_a, ev_b.
 cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sorted, int64_t first,
-                             int64_t count, int num_sms, cudaStream_t stream, int64_t* launches = nullptr);
+                             int64_t count, int num_sms, cudaStream_t stream, int64_t* launches = nullptr,
+                             cudaStream_t aux = nullptr, cudaEvent_t ev_a = nullptr, cudaEvent_t ev_b = nullptr);
 // Per heavy item in list order: out[i] = FLOP, out[count + i] = A-row length,
 // out[2 count + i] = boundary-table cells (batch planning when the heavy rows'
 // products exceed one batch's buffers).
