@@ -195,6 +195,12 @@ int spnnz_gpu_set_profiling(spnnz_gpu_ctx* ctx, int enabled);
 int spnnz_gpu_last_timings(spnnz_gpu_ctx* ctx, double* ms_out5, int64_t* launches);
 /* The context's CUDA stream (cudaStream_t), for callers that time on it. */
 void* spnnz_gpu_stream(spnnz_gpu_ctx* ctx);
+/* Ordering of DEVICE-residency inputs: every call that reads one first makes
+ * the context's (non-blocking) stream wait for the work queued on `stream`
+ * (a cudaStream_t) at the time of the call -- default NULL, the legacy
+ * default stream.  A caller that produces its inputs on another stream
+ * names it here (or synchronizes it before the call). */
+int spnnz_gpu_set_input_stream(spnnz_gpu_ctx* ctx, void* stream);
 
 #ifdef __cplusplus
 }

@@ -13,9 +13,13 @@
 // contiguous) members, so the reference's own spnnz::CsrMatrix works as is.
 // `threads` parameters are accepted for signature parity and ignored.
 //
-// Free functions use a thread-local Session on device 0 that keeps the last
-// matrices resident (re-uploaded when the caller passes different data);
-// Session can also be used directly (device choice, rank/world sharding).
+// Free functions use a thread-local Session on device 0 and upload their
+// matrices on every call, as the stateless reference reads them on every
+// call (a cache keyed on addresses could match a different matrix once the
+// old one is freed, and would miss in-place edits).  A Session used directly
+// keeps its matrices resident between calls (device choice, rank/world
+// sharding); Session::ensure re-uploads only when the addresses or shapes
+// change, so its caller must not reuse or edit the buffers in between.
 #pragma once
 
 #include <cstdint>
@@ -234,7 +238,7 @@ inline Session& default_session() {
 template <typename MA, typename MB>
 FlopProfile compute_flop(const MA& a, const MB& b, int /*threads*/ = 0) {  // flop.hpp:25
     auto& s = default_session();
-    s.ensure(a, b);
+    s.load(a, b);
     return s.compute_flop();
 }
 
@@ -283,7 +287,7 @@ RowNnzResult sampled_symbolic(const MA& a, const MB& b, const FlopProfile& profi
                               std::span<const index_t> rows, int /*threads*/ = 0) {  // symbolic.hpp:122
     check_symbolic_args(a, b, profile);
     auto& s = default_session();
-    s.ensure(a, b);
+    s.load(a, b);
     s.set_profile(profile);
     return s.sampled_symbolic(rows);
 }
@@ -293,7 +297,7 @@ RowNnzResult exact_symbolic(const MA& a, const MB& b, const FlopProfile& profile
                             int /*threads*/ = 0) {  // symbolic.hpp:94
     check_symbolic_args(a, b, profile);
     auto& s = default_session();
-    s.ensure(a, b);
+    s.load(a, b);
     s.set_profile(profile);
     return s.exact_symbolic();
 }
@@ -352,7 +356,7 @@ PredictionReport run_prediction_with_plan(const MA& a, const MB& b, const FlopPr
                                           SamplePlan plan, int /*threads*/ = 0) {  // :202
     check_symbolic_args(a, b, profile);
     auto& s = default_session();
-    s.ensure(a, b);
+    s.load(a, b);
     return s.run_prediction_with_plan(std::move(plan));
 }
 
@@ -360,7 +364,7 @@ template <typename MA, typename MB>
 PredictionReport run_prediction(const MA& a, const MB& b, std::uint64_t seed,
                                 SamplePolicy policy = {}, int /*threads*/ = 0) {  // :220
     auto& s = default_session();
-    s.ensure(a, b);
+    s.load(a, b);
     return s.run_prediction(seed, policy);
 }
 

@@ -82,6 +82,7 @@ _SIGS = {
     "spnnz_gpu_set_profiling": (c_int, [c_void_p, c_int]),
     "spnnz_gpu_last_timings": (c_int, [c_void_p, c_void_p, POINTER(c_int64)]),
     "spnnz_gpu_stream": (c_void_p, [c_void_p]),
+    "spnnz_gpu_set_input_stream": (c_int, [c_void_p, c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -110,10 +110,16 @@ Nccl& nccl() {
     } while (0)
 
 // ---------------------------------------------------------- device buffer
+// Owns one device allocation; freed with the context (the destructor runs
+// after spnnz_gpu_destroy has selected the context's device).
 template <typename T>
 struct DBuf {
     T* p = nullptr;
     int64_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
     int ensure(int64_t want) {
         if (want <= n && p) return SPNNZ_OK;
         if (p) cudaFree(p);
@@ -152,6 +158,11 @@ struct spnnz_gpu_ctx {
     cudaStream_t side[kSide] = {};        // symbolic tiers, concurrent with the heavy rows
     cudaEvent_t fork = nullptr, join[kSide] = {};
     cudaEvent_t ev_bin = nullptr, ev_flop = nullptr;  // early binning (run_symbolic)
+    // device-residency inputs are read after the caller's work queued on
+    // in_stream (default: the legacy default stream, where torch and most
+    // callers queue); c->stream itself is non-blocking
+    cudaStream_t in_stream = nullptr;
+    cudaEvent_t ev_in = nullptr;
     ncclComm_t comm = nullptr;
 
     // matrices
@@ -228,6 +239,14 @@ int settle_upload(spnnz_gpu_ctx* c) {
     CU(cudaStreamWaitEvent(c->stream, c->ev_rpt, 0));
     for (int k = 0; k < c->n_chunks; ++k) CU(cudaStreamWaitEvent(c->stream, c->ev_chunk[k], 0));
     c->pending_upload = false;
+    return SPNNZ_OK;
+}
+
+// The context stream waits for the caller's queued work before it reads a
+// device-residency input (e.g. a tensor an asynchronous kernel just wrote).
+int order_after_caller(spnnz_gpu_ctx* c) {
+    CU(cudaEventRecord(c->ev_in, c->in_stream));
+    CU(cudaStreamWaitEvent(c->stream, c->ev_in, 0));
     return SPNNZ_OK;
 }
 
@@ -780,6 +799,7 @@ int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_bin, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_flop, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming);
     for (int i = 0; i < spnnz_gpu_ctx::kSide && e == cudaSuccess; ++i)
         e = cudaEventCreateWithFlags(&c->join[i], cudaEventDisableTiming);
     int rc = SPNNZ_OK;
@@ -815,27 +835,8 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     if (c->cstream) cudaStreamSynchronize(c->cstream);
     if (c->fstream) cudaStreamSynchronize(c->fstream);
     if (c->comm) nccl().CommDestroy(c->comm);
-    for (auto* b : {&c->b_rpt, &c->a_rpt, &c->flop, &c->out64, &c->heavy_unit_off,
-                    &c->heavy_eoff, &c->heavy_foff, &c->heavy_epre, &c->heavy_eb0, &c->heavy_flops})
-        b->release();
-    c->deg.release();
-    for (auto* b : {&c->b_col, &c->a_col, &c->tile_x, &c->counts, &c->lists,
-                    &c->samples, &c->rows_in, &c->bad})
-        b->release();
-    for (auto* b : {&c->tile_carry, &c->tile_total, &c->tile_max, &c->totals, &c->heavy_meta, &c->sorted_cnt})
-        b->release();
-    c->pool.release();
-    c->outf.release();
-    c->heavy_rc.release();
-    c->heavy_cur.release();
-    c->heavy_pbuf.release();
-    c->heavy_utab.release();
-    c->item_flop.release();
-    c->redo.release();
-    c->nredo.release();
-    c->heavy_boff.release();
-    for (auto* b : {&c->heavy_bnd, &c->heavy_unit_item, &c->heavy_unit_e0}) b->release();
-    c->heavy_tasks.release();
+    // device buffers: the DBuf members free themselves in `delete c` below
+    // (the device is already selected)
     if (c->h_totals) cudaFreeHost(c->h_totals);
     if (c->h_counts) cudaFreeHost(c->h_counts);
     if (c->h_meta) cudaFreeHost(c->h_meta);
@@ -848,6 +849,7 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     if (c->fork) cudaEventDestroy(c->fork);
     if (c->ev_bin) cudaEventDestroy(c->ev_bin);
     if (c->ev_flop) cudaEventDestroy(c->ev_flop);
+    if (c->ev_in) cudaEventDestroy(c->ev_in);
     for (auto ev : c->ev_chunk)
         if (ev) cudaEventDestroy(ev);
     if (c->ev_rpt) cudaEventDestroy(c->ev_rpt);
@@ -866,6 +868,12 @@ int spnnz_gpu_synchronize(spnnz_gpu_ctx* c) {
 }
 
 void* spnnz_gpu_stream(spnnz_gpu_ctx* c) { return c ? c->stream : nullptr; }
+
+int spnnz_gpu_set_input_stream(spnnz_gpu_ctx* c, void* stream) {
+    if (!c) return set_err(SPNNZ_EINVAL, "null context");
+    c->in_stream = static_cast<cudaStream_t>(stream);
+    return SPNNZ_OK;
+}
 
 int spnnz_gpu_host_alloc(size_t bytes, void** out) {
     cudaError_t e = cudaMallocHost(out, std::max<size_t>(bytes, 1));
@@ -916,6 +924,7 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
     std::vector<int64_t> host_arpt;
     const int64_t* arpt_h = a->rpt;
     if (residency == SPNNZ_DEVICE) {
+        RC(order_after_caller(c));
         host_arpt.resize(static_cast<size_t>(a->rows) + 1);
         CU(cudaMemcpy(host_arpt.data(), a->rpt, 8 * host_arpt.size(), cudaMemcpyDeviceToHost));
         arpt_h = host_arpt.data();
@@ -989,6 +998,8 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
     c->b_intervals = ivenv && atoi(ivenv) > 0;
     c->b_sorted = false;
     if (c->b_intervals) {
+        // B may still be landing on the copy stream (chunked upload)
+        RC(settle_upload(c));
         RC(c->sorted_cnt.ensure(2));
         CU(launch_check_sorted(c->b_rpt.p, c->b_col.p, c->b_rows, b_nnz,
                                reinterpret_cast<unsigned long long*>(c->sorted_cnt.p), c->num_sms,
@@ -1048,6 +1059,7 @@ int spnnz_gpu_set_profile(spnnz_gpu_ctx* c, const int64_t* flop_in, int64_t rows
     if (rows != local_rows(c))
         return set_err(SPNNZ_EINVAL, "symbolic: profile does not match A");
     RC(c->flop.ensure(std::max<int64_t>(rows, 1)));
+    if (residency == SPNNZ_DEVICE) RC(order_after_caller(c));
     if (rows)
         CU(cudaMemcpyAsync(c->flop.p, flop_in, 8 * size_t(rows),
                            residency == SPNNZ_DEVICE ? cudaMemcpyDeviceToDevice
@@ -1069,6 +1081,7 @@ int check_rows(spnnz_gpu_ctx* c, const int32_t* rows, int64_t n, int residency, 
             if (rows[i] < 0 || rows[i] >= c->a_rows)
                 return set_err(SPNNZ_EINVAL, "%s: row %d out of range", who, rows[i]);
     } else if (n > 0) {
+        RC(order_after_caller(c));
         RC(c->bad.ensure(1));
         CU(cudaMemsetAsync(c->bad.p, 0, 4, c->stream));
         CU(launch_check_rows(rows, n, c->a_rows, c->bad.p, c->stream));

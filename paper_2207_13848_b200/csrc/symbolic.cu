@@ -241,7 +241,14 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
 constexpr int kT3Block = 256, kT3Slots = 4096;
 constexpr int kT4Block = 512, kT4Slots = SPNNZ_T4_SLOTS;
 constexpr int kT5Block = 1024, kT5Slots = 49152;
+// every shared hash table holds its bin's largest row at load <= 1/2, so a
+// probe always finds an empty slot (the A/B build knobs SPNNZ_BIN*_MAX
+// cannot push a row past its table: a full table would never terminate)
+static_assert(1024 >= 2 * kBin2Max, "bin-2 table load <= 1/2");
+static_assert(kT3Slots >= 2 * kBin3Max, "bin-3 table load <= 1/2");
 static_assert(kT4Slots >= 2 * kBin4Max, "bin-4 table load <= 1/2");
+static_assert(kT5Slots >= 2 * kBin5Max, "bin-5 table load <= 1/2");
+static_assert(kBin1Max <= 32, "bin 1 stages a row's products in one warp's 32 slots");
 // keys in flight per lane (B.col loads issued together before the inserts)
 #ifndef SPNNZ_T3_UNROLL
 #define SPNNZ_T3_UNROLL 4

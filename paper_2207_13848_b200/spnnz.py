@@ -160,7 +160,6 @@ class Predictor:
         idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
         check(lib().spnnz_gpu_create(device, rank, world, idbuf, ctypes.byref(self._ctx)))
         self.device, self.rank, self.world = device, rank, world
-        self._key = None
         self.row_lo = self.row_hi = self.a_rows = 0
 
     @staticmethod
@@ -184,11 +183,23 @@ class Predictor:
     def ctx(self):
         return self._ctx
 
+    def _after_torch(self, *objs):
+        """Device tensors are read after the work torch queued on its current
+        stream (spnnz_gpu_set_input_stream), so a tensor an asynchronous kernel
+        just wrote is complete when the context's stream reads it."""
+        for o in objs:
+            if _res(o) == DEVICE:
+                import torch
+                h = torch.cuda.current_stream(o.device).cuda_stream
+                check(lib().spnnz_gpu_set_input_stream(self._ctx, ctypes.c_void_p(h)))
+                return
+
     # -- matrices
     def load(self, a, b=None, residency: Optional[int] = None):
         """Upload A (this rank's shard) and B (replicated).  ``a``/``b`` are
         CsrMatrix (host) or objects with rows/cols/rpt/col device tensors."""
         res = residency if residency is not None else _res(a.rpt)
+        self._after_torch(a.rpt)
         va = CsrView(a.rows, a.cols, ctypes.cast(_ptr(a.rpt), ctypes.POINTER(ctypes.c_int64)),
                      ctypes.cast(_ptr(a.col), ctypes.POINTER(ctypes.c_int32)))
         vb = None
@@ -199,16 +210,16 @@ class Predictor:
         lo, hi, rows = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         check(lib().spnnz_gpu_shard(self._ctx, ctypes.byref(lo), ctypes.byref(hi), ctypes.byref(rows)))
         self.row_lo, self.row_hi, self.a_rows = lo.value, hi.value, rows.value
-        self._key = (id(a), id(b), _ptr(a.rpt), _ptr(a.col), a.rows, a.cols,
-                     None if b is None else (_ptr(b.rpt), _ptr(b.col), b.rows, b.cols))
         return self
 
     def ensure_loaded(self, a, b):
-        key = (id(a), id(b if b is not a else None), _ptr(a.rpt), _ptr(a.col), a.rows, a.cols,
-               None if (b is None or b is a) else (_ptr(b.rpt), _ptr(b.col), b.rows, b.cols))
-        if key != self._key:
-            self.load(a, None if b is a else b)
-            self._key = key
+        """Upload (A, B) for a stateless reference-style call.  The reference's
+        free functions read their matrices on every call, so this always
+        re-uploads: a cache keyed on object ids or buffer addresses can match a
+        different matrix once the old one is freed (CPython and the allocator
+        reuse both), and it misses in-place edits.  Callers that want the
+        matrices to stay resident use a Predictor's methods directly."""
+        self.load(a, None if b is a else b)
 
     @property
     def local_rows(self) -> int:
@@ -227,11 +238,13 @@ class Predictor:
         f = profile.flop_per_row
         if isinstance(f, np.ndarray):
             f = np.ascontiguousarray(f, dtype=np.int64)
+        self._after_torch(f)
         check(lib().spnnz_gpu_set_profile(self._ctx, _ptr(f), len(f), _res(f),
                                           int(profile.total_flop), int(profile.max_flop_row)))
 
     def sampled_flop(self, rows) -> int:
         rows = _rows_arg(rows)
+        self._after_torch(rows)
         out = ctypes.c_int64()
         check(lib().spnnz_gpu_sampled_flop(self._ctx, _ptr(rows), len(rows), _res(rows),
                                            ctypes.byref(out)))
@@ -253,6 +266,7 @@ class Predictor:
         out = np.empty(len(rows), np.int64) if per_sample else None
         tot = ctypes.c_int64()
         res = _res(rows)
+        self._after_torch(rows)
         if res == DEVICE and per_sample:
             import torch
             out = torch.empty(len(rows), dtype=torch.int64, device=rows.device)
@@ -302,6 +316,7 @@ class Predictor:
                                  want_ceil=True) -> PredictionReport:
         m = self.local_rows
         rows = _rows_arg(plan.sample_rows)
+        self._after_torch(rows)
         ceil_out = np.empty(m, np.int64) if want_ceil else None
         real_out = np.empty(m, np.float64) if want_real else None
         rep = Report()
