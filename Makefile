@@ -15,7 +15,7 @@ CPP_SRCS := $(SRC)/capi.cpp
 OBJS := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(BUILD)/%.o,$(CPP_SRCS))
 HDRS := $(SRC)/kernels.h $(SRC)/device_common.cuh $(SRC)/symbolic_common.cuh include/spnnz_gpu/capi.h
 
-all: $(OUT)/libspnnz_gpu.so $(OUT)/libspnnz_gen.so $(BUILD)/test_dropin $(BUILD)/spnnz_corpus oracle
+all: $(OUT)/libspnnz_gpu.so $(OUT)/libspnnz_gen.so $(BUILD)/test_dropin $(BUILD)/spnnz_corpus oracle dropin_ref
 
 $(BUILD)/%.o: $(SRC)/%.cu $(HDRS) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
@@ -37,6 +37,17 @@ $(BUILD)/spnnz_corpus: tools/spnnz_corpus.cpp include/spnnz_gpu/harness.hpp incl
 $(BUILD)/test_dropin: tests/cpp/test_dropin.cpp include/spnnz_gpu/spnnz_gpu.hpp $(OUT)/libspnnz_gpu.so | $(BUILD)
 	$(CXX) -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L$(OUT) -lspnnz_gpu -Wl,-rpath,'$$ORIGIN/../$(OUT)'
 
+# C++ drop-in with the reference's own types (test infrastructure: built only
+# where the reference headers exist, like oracle/_ref; run on a GPU box)
+REF_INC ?= /root/reference/proj/include
+dropin_ref:
+	@if [ -d "$(REF_INC)/spnnz" ]; then \
+	  $(MAKE) --no-print-directory $(BUILD)/test_dropin_ref; \
+	else echo "reference headers absent: skipping build/test_dropin_ref"; fi
+
+$(BUILD)/test_dropin_ref: tests/cpp/test_dropin_ref.cpp include/spnnz_gpu/spnnz_gpu.hpp $(OUT)/libspnnz_gpu.so | $(BUILD)
+	$(CXX) -std=c++20 -O2 -Wall -ffp-contract=off -I$(REF_INC) -Iinclude -o $@ $< -L$(OUT) -lspnnz_gpu -pthread -Wl,-rpath,'$$ORIGIN/../$(OUT)'
+
 oracle:
 	$(MAKE) --no-print-directory -C oracle
 
@@ -47,4 +58,4 @@ clean:
 	rm -rf $(BUILD) $(OUT)/*.so
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean dropin_ref

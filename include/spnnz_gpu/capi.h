@@ -144,7 +144,13 @@ int spnnz_gpu_make_sample_plan(spnnz_gpu_ctx* ctx, int32_t num_rows, uint64_t se
 
 /* spnnz::sampled_symbolic (symbolic.hpp:122-154): exact output-row NNZ of
  * each sampled row (duplicates recomputed), and the global total z*.
- * nnz_per_sample nullable.  EINVAL on out-of-range rows (:125-131). */
+ * nnz_per_sample nullable.  EINVAL on out-of-range rows (:125-131).
+ * With a caller-installed profile its flop_per_row is each row's table size,
+ * as in the reference: a row whose profile flop is 0 counts 0, and one above
+ * the profile's max_flop_row is EINVAL ("HashAccumulator: tsize ... exceeds
+ * capacity ...", :37-40); any other row gets its exact count (the
+ * reference's probe would not terminate on a table smaller than the row's
+ * distinct count; here the count is still exact).  Same for exact_symbolic. */
 int spnnz_gpu_sampled_symbolic(spnnz_gpu_ctx* ctx, const int32_t* rows, int64_t n, int residency,
                                int64_t* nnz_per_sample, int64_t* total_nnz);
 
@@ -170,9 +176,13 @@ int spnnz_gpu_run_prediction(spnnz_gpu_ctx* ctx, uint64_t seed, double fraction,
                              spnnz_report* report, int64_t* row_ceil, double* row_real,
                              int32_t* sample_rows, int residency);
 
-/* Same pipeline on an explicit sample list (run_prediction_with_plan,
- * predict.hpp:202-216; e.g. spnnz::exhaustive_plan, :60-70).  p is the plan's
- * p.  Recomputes the profile. */
+/* spnnz::run_prediction_with_plan (predict.hpp:202-216) on an explicit sample
+ * list (e.g. spnnz::exhaustive_plan, :60-70) and the RESIDENT profile -- the
+ * reference's `const FlopProfile&` argument: the one compute_flop left, or the
+ * caller's installed with set_profile.  No FLOP pass runs: f* and the per-row
+ * views come from the profile's flop_per_row, F from its total_flop, and a
+ * row's flop is its table size (tsize 0 counts 0; tsize above max_flop_row is
+ * EINVAL, symbolic.hpp:35-40).  p is the plan's p.  ESTATE without a profile. */
 int spnnz_gpu_run_prediction_with_plan(spnnz_gpu_ctx* ctx, const int32_t* rows, int64_t n, double p,
                                        int rows_residency, spnnz_report* report, int64_t* row_ceil,
                                        double* row_real, int out_residency);

@@ -99,6 +99,16 @@ inline void check(int rc) {
     throw std::runtime_error("spnnz_gpu: " + msg);
 }
 
+// Any profile type with the reference's fields (spnnz::FlopProfile or
+// spnnz::gpu::FlopProfile): passed to the device without a copy.
+template <typename P>
+concept ProfileLike = requires(const P& p) {
+    p.flop_per_row.data();
+    p.flop_per_row.size();
+    p.total_flop;
+    p.max_flop_row;
+};
+
 template <typename M>
 spnnz_csr_view view(const M& m) {
     return spnnz_csr_view{static_cast<int32_t>(m.rows), static_cast<int32_t>(m.cols),
@@ -143,8 +153,9 @@ public:
                                              &p.total_flop, &p.max_flop_row));
         return p;
     }
-    void set_profile(const FlopProfile& p) {
-        detail::check(spnnz_gpu_set_profile(ctx(), p.flop_per_row.data(),
+    template <detail::ProfileLike P>
+    void set_profile(const P& p) {
+        detail::check(spnnz_gpu_set_profile(ctx(), reinterpret_cast<const int64_t*>(p.flop_per_row.data()),
                                             static_cast<int64_t>(p.flop_per_row.size()),
                                             SPNNZ_HOST, p.total_flop, p.max_flop_row));
     }
@@ -178,6 +189,8 @@ public:
         fill(out, rep);
         return out;
     }
+    // run_prediction_with_plan on the resident profile (compute_flop's, or
+    // the one set_profile installed)
     PredictionReport run_prediction_with_plan(SamplePlan plan) {
         PredictionReport out;
         out.predicted_row_nnz.resize(static_cast<size_t>(local_rows_));
@@ -234,6 +247,95 @@ inline Session& default_session() {
     return s;
 }
 
+// ---- reference <-> mirror conversions ----------------------------------
+// Field-for-field copies between the reference's structs (spnnz::FlopProfile,
+// SamplePlan, RowNnzResult, SampleStats, PredictionReport, ...) and these,
+// for callers that keep the reference's types around the GPU calls:
+//   spnnz::PredictionReport r = spnnz::gpu::to_reference<spnnz::PredictionReport>(
+//       spnnz::gpu::run_prediction(a, b, seed));
+// (Profiles need no conversion: every function taking one accepts either.)
+template <typename Plan>
+SamplePlan from_reference_plan(const Plan& p) {
+    SamplePlan out;
+    out.sample_rows.assign(p.sample_rows.begin(), p.sample_rows.end());
+    out.sample_num = p.sample_num;
+    out.p = p.p;
+    out.seed = p.seed;
+    return out;
+}
+
+template <detail::ProfileLike P>
+FlopProfile from_reference_profile(const P& p) {
+    return FlopProfile{{p.flop_per_row.begin(), p.flop_per_row.end()}, p.total_flop, p.max_flop_row};
+}
+
+template <typename R>
+R to_reference(const FlopProfile& g) {
+    R r;
+    r.flop_per_row.assign(g.flop_per_row.begin(), g.flop_per_row.end());
+    r.total_flop = g.total_flop;
+    r.max_flop_row = g.max_flop_row;
+    return r;
+}
+
+template <typename R>
+R to_reference(const RowNnzResult& g) {
+    R r;
+    r.nnz_per_row.assign(g.nnz_per_row.begin(), g.nnz_per_row.end());
+    r.total_nnz = g.total_nnz;
+    return r;
+}
+
+template <typename R>
+R to_reference(const SamplePlan& g) {
+    R r;
+    r.sample_rows.assign(g.sample_rows.begin(), g.sample_rows.end());
+    r.sample_num = g.sample_num;
+    r.p = g.p;
+    r.seed = g.seed;
+    return r;
+}
+
+template <typename R>
+R to_reference(const SampleStats& g) {
+    R r;
+    r.sampled_flop = g.sampled_flop;
+    r.sampled_nnz = g.sampled_nnz;
+    r.sampled_cr = g.sampled_cr;
+    return r;
+}
+
+template <typename R>
+R to_reference(const ProposedPrediction& g) {
+    R r;
+    r.z2_star = g.z2_star;
+    r.predicted_cr = g.predicted_cr;
+    return r;
+}
+
+template <typename R>
+R to_reference(const ErrorReport& g) {
+    R r;
+    r.eps1 = g.eps1;
+    r.eps_f = g.eps_f;
+    r.eps2 = g.eps2;
+    r.identity_residual = g.identity_residual;
+    return r;
+}
+
+template <typename R>
+R to_reference(const PredictionReport& g) {  // predict.hpp:192-200 (the ceil view has no slot there)
+    R r;
+    r.z1_star = g.z1_star;
+    r.z2_star = g.z2_star;
+    r.predicted_cr = g.predicted_cr;
+    r.predicted_row_nnz.assign(g.predicted_row_nnz.begin(), g.predicted_row_nnz.end());
+    r.plan = to_reference<decltype(r.plan)>(g.plan);
+    r.stats = to_reference<decltype(r.stats)>(g.stats);
+    r.total_flop = g.total_flop;
+    return r;
+}
+
 // ---- the reference's free functions ------------------------------------
 template <typename MA, typename MB>
 FlopProfile compute_flop(const MA& a, const MB& b, int /*threads*/ = 0) {  // flop.hpp:25
@@ -242,7 +344,8 @@ FlopProfile compute_flop(const MA& a, const MB& b, int /*threads*/ = 0) {  // fl
     return s.compute_flop();
 }
 
-inline offset_t sampled_flop(const FlopProfile& profile, std::span<const index_t> rows) {  // flop.hpp:64
+template <detail::ProfileLike P>
+offset_t sampled_flop(const P& profile, std::span<const index_t> rows) {  // flop.hpp:64
     offset_t sum = 0;
     thread_local Session s(0);  // profile-only context
     s.set_profile(profile);
@@ -275,15 +378,15 @@ inline SamplePlan exhaustive_plan(index_t num_rows) {  // predict.hpp:60
     return plan;
 }
 
-template <typename MA, typename MB>
-void check_symbolic_args(const MA& a, const MB& b, const FlopProfile& profile) {  // symbolic.hpp:79-87
+template <typename MA, typename MB, detail::ProfileLike P>
+void check_symbolic_args(const MA& a, const MB& b, const P& profile) {  // symbolic.hpp:79-87
     if (a.cols != b.rows) throw std::invalid_argument("symbolic: A.cols != B.rows");
     if (profile.flop_per_row.size() != static_cast<size_t>(a.rows))
         throw std::invalid_argument("symbolic: profile does not match A");
 }
 
-template <typename MA, typename MB>
-RowNnzResult sampled_symbolic(const MA& a, const MB& b, const FlopProfile& profile,
+template <typename MA, typename MB, detail::ProfileLike P>
+RowNnzResult sampled_symbolic(const MA& a, const MB& b, const P& profile,
                               std::span<const index_t> rows, int /*threads*/ = 0) {  // symbolic.hpp:122
     check_symbolic_args(a, b, profile);
     auto& s = default_session();
@@ -292,8 +395,8 @@ RowNnzResult sampled_symbolic(const MA& a, const MB& b, const FlopProfile& profi
     return s.sampled_symbolic(rows);
 }
 
-template <typename MA, typename MB>
-RowNnzResult exact_symbolic(const MA& a, const MB& b, const FlopProfile& profile,
+template <typename MA, typename MB, detail::ProfileLike P>
+RowNnzResult exact_symbolic(const MA& a, const MB& b, const P& profile,
                             int /*threads*/ = 0) {  // symbolic.hpp:94
     check_symbolic_args(a, b, profile);
     auto& s = default_session();
@@ -302,29 +405,34 @@ RowNnzResult exact_symbolic(const MA& a, const MB& b, const FlopProfile& profile
     return s.exact_symbolic();
 }
 
-inline SampleStats collect_sample_stats(const FlopProfile& profile, const SamplePlan& plan,
-                                        const RowNnzResult& sampled) {  // predict.hpp:81
+template <detail::ProfileLike P, typename Plan, typename Nnz>
+SampleStats collect_sample_stats(const P& profile, const Plan& plan,
+                                 const Nnz& sampled) {  // predict.hpp:81
     SampleStats st;
-    st.sampled_flop = sampled_flop(profile, plan.sample_rows);
+    st.sampled_flop = sampled_flop(profile, std::span<const index_t>(plan.sample_rows.data(),
+                                                                      plan.sample_rows.size()));
     st.sampled_nnz = sampled.total_nnz;
     st.sampled_cr = spnnz_sampled_cr(st.sampled_flop, st.sampled_nnz);
     return st;
 }
 
-inline double predict_reference(const SampleStats& stats, const SamplePlan& plan) {  // predict.hpp:94
+template <typename Stats, typename Plan>
+double predict_reference(const Stats& stats, const Plan& plan) {  // predict.hpp:94
     double z1 = 0;
     detail::check(spnnz_predict_reference(stats.sampled_nnz, plan.p, &z1));
     return z1;
 }
 
-inline ProposedPrediction predict_proposed(const SampleStats& stats, offset_t total_flop) {  // :109
+template <typename Stats>
+ProposedPrediction predict_proposed(const Stats& stats, offset_t total_flop) {  // :109
     ProposedPrediction out;
     detail::check(spnnz_predict_proposed(stats.sampled_flop, stats.sampled_nnz, total_flop,
                                          &out.z2_star, &out.predicted_cr));
     return out;
 }
 
-inline std::vector<double> predict_row_structure(const FlopProfile& profile, double cr) {  // :126
+template <detail::ProfileLike P>
+std::vector<double> predict_row_structure(const P& profile, double cr) {  // :126
     if (!(cr > 0.0))
         throw std::invalid_argument("predict_row_structure: predicted_cr must be positive");
     thread_local Session s(0);
@@ -334,7 +442,8 @@ inline std::vector<double> predict_row_structure(const FlopProfile& profile, dou
     return out;
 }
 
-inline std::vector<offset_t> predict_row_structure_ceil(const FlopProfile& profile, double cr) {  // :140
+template <detail::ProfileLike P>
+std::vector<offset_t> predict_row_structure_ceil(const P& profile, double cr) {  // :140
     if (!(cr > 0.0))
         throw std::invalid_argument("predict_row_structure_ceil: predicted_cr must be positive");
     thread_local Session s(0);
@@ -351,13 +460,17 @@ inline ErrorReport error_report(double z1, double z2, offset_t f_star, offset_t 
     return ErrorReport{o[0], o[1], o[2], o[3]};
 }
 
-template <typename MA, typename MB>
-PredictionReport run_prediction_with_plan(const MA& a, const MB& b, const FlopProfile& profile,
-                                          SamplePlan plan, int /*threads*/ = 0) {  // :202
+// The caller's profile is the input, as in the reference: its flop is each
+// sampled row's table size, f* and the per-row views come from it and F is
+// its total_flop; no FLOP pass runs.
+template <typename MA, typename MB, detail::ProfileLike P, typename Plan>
+PredictionReport run_prediction_with_plan(const MA& a, const MB& b, const P& profile,
+                                          Plan plan, int /*threads*/ = 0) {  // :202
     check_symbolic_args(a, b, profile);
     auto& s = default_session();
     s.load(a, b);
-    return s.run_prediction_with_plan(std::move(plan));
+    s.set_profile(profile);
+    return s.run_prediction_with_plan(from_reference_plan(plan));
 }
 
 template <typename MA, typename MB>

@@ -180,6 +180,10 @@ class Reference:
         L.ref_predict_row_structure.argtypes = [c_void_p, c_double, c_void_p]
         L.ref_run_pipeline.argtypes = [c_void_p, c_void_p, c_uint64, c_double, c_int64, c_int, POINTER(RefReport), c_void_p]
         L.ref_run_pipeline_ceil.argtypes = L.ref_run_pipeline.argtypes
+        L.ref_profile_new.restype = c_void_p
+        L.ref_profile_new.argtypes = [c_void_p, c_int64, c_int64, c_int64]
+        L.ref_run_with_plan.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_double, c_uint64,
+                                        c_int, POINTER(RefReport), c_void_p, c_void_p]
         L.ref_error_report.argtypes = [c_double, c_double, c_int64, c_int64, c_int64, c_double, c_void_p]
         L.ref_splitmix_seq.argtypes = [c_uint64, c_int64, c_void_p]
         L.ref_matrix_export.argtypes = [c_void_p, POINTER(c_int32), POINTER(c_int32), POINTER(c_int64), c_void_p, c_void_p]
@@ -290,6 +294,22 @@ class Reference:
         self._chk(fn(ha, hb, seed, fraction, cap if cap >= 0 else 2**63 - 1,
                      self.threads, byref(rep), ceil.ctypes.data if want_ceil else None))
         return rep, ceil
+
+    def run_with_plan(self, ha, hb, flop, total, mx, rows, p, seed=0):
+        """spnnz::run_prediction_with_plan on a hand-built FlopProfile
+        {flop, total, mx}: (report, real view, ceil view)."""
+        flop = np.ascontiguousarray(flop, np.int64)
+        rows = np.ascontiguousarray(rows, np.int32)
+        prof = self.L.ref_profile_new(flop.ctypes.data, len(flop), int(total), int(mx))
+        rep = RefReport()
+        real = np.empty(len(flop), np.float64)
+        ceil = np.empty(len(flop), np.int64)
+        try:
+            self._chk(self.L.ref_run_with_plan(ha, hb, prof, rows.ctypes.data, len(rows), p, seed,
+                                               self.threads, byref(rep), real.ctypes.data, ceil.ctypes.data))
+        finally:
+            self.L.ref_profile_free(prof)
+        return rep, real, ceil
 
     def error_report(self, z1, z2, f_star, Z, F, p):
         out = (c_double * 4)()

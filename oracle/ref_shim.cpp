@@ -217,6 +217,41 @@ int ref_run_pipeline_ceil(void* a, void* b, uint64_t seed, double fraction, int6
     });
 }
 
+// spnnz::run_prediction_with_plan (predict.hpp:202-216) on a caller-provided
+// profile handle and sample list (the profile need not be compute_flop's:
+// the boundary test hands in edited ones); row_real (predicted_row_nnz) and
+// row_ceil (predict_row_structure_ceil of the same profile) nullable.
+int ref_run_with_plan(void* a, void* b, void* profile, const int32_t* rows, int64_t n, double p,
+                      uint64_t seed, int threads, ref_report* rep, double* row_real,
+                      int64_t* row_ceil) {
+    return guard([&] {
+        const spnnz::FlopProfile& prof = static_cast<RefProfile*>(profile)->p;
+        spnnz::SamplePlan plan;
+        plan.sample_rows.assign(rows, rows + n);
+        plan.sample_num = n;
+        plan.p = p;
+        plan.seed = seed;
+        spnnz::PredictionReport r = spnnz::run_prediction_with_plan(
+            static_cast<RefMatrix*>(a)->m, static_cast<RefMatrix*>(b)->m, prof, std::move(plan),
+            threads);
+        rep->total_flop = r.total_flop;
+        rep->max_flop_row = prof.max_flop_row;
+        rep->sample_num = r.plan.sample_num;
+        rep->p = r.plan.p;
+        rep->sampled_flop = r.stats.sampled_flop;
+        rep->sampled_nnz = r.stats.sampled_nnz;
+        rep->sampled_cr = r.stats.sampled_cr;
+        rep->z1_star = r.z1_star;
+        rep->z2_star = r.z2_star;
+        rep->predicted_cr = r.predicted_cr;
+        if (row_real) std::memcpy(row_real, r.predicted_row_nnz.data(), r.predicted_row_nnz.size() * 8);
+        if (row_ceil) {
+            auto v = spnnz::predict_row_structure_ceil(prof, r.predicted_cr);
+            std::memcpy(row_ceil, v.data(), v.size() * 8);
+        }
+    });
+}
+
 int ref_error_report(double z1, double z2, int64_t f_star, int64_t exact_nnz, int64_t total_flop,
                      double p, double* out4) {
     return guard([&] {

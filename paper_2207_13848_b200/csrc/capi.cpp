@@ -170,6 +170,7 @@ struct spnnz_gpu_ctx {
     bool same_b = false;
     bool b_intervals = false;  // interval heavy path requested (SPNNZ_HEAVY_INTERVALS=1)
     bool b_sorted = false;     // ... and B's rows checked non-decreasing at load
+    bool rows_mode = false;    // banded A: the FLOP pass's row-per-thread tiles (checked at load)
     int32_t a_rows = 0, a_cols = 0, b_rows = 0, b_cols = 0;
     int32_t row_lo = 0, row_hi = 0;
     int64_t b_nnz = 0;
@@ -182,6 +183,11 @@ struct spnnz_gpu_ctx {
     // profile
     DBuf<int64_t> flop;
     bool profile_valid = false;
+    // own: computed by this context's FLOP pass over the loaded matrices;
+    // else installed by the caller (set_profile) and used as the reference
+    // uses its FlopProfile argument (tsize, f*, F, the per-row views)
+    bool profile_own = false;
+    DBuf<int64_t> flop_true;  // true FLOP of every local row under a caller profile (exact pass)
     int64_t profile_total = 0, profile_max = 0;
 
     // scratch
@@ -377,7 +383,8 @@ int heavy_buffers(spnnz_gpu_ctx* c, int64_t count, int64_t ents, int64_t product
 int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64_t* d_out,
                  int slot, bool sampled_flop, int64_t* launches, const int64_t* item_flop = nullptr,
                  const DevCsr* a_view = nullptr, const int64_t* window = nullptr,
-                 cudaStream_t bin_stream = nullptr) {
+                 cudaStream_t bin_stream = nullptr, const int64_t* tsize = nullptr,
+                 long long tsize_cap = 0) {
     const bool early = bin_stream != nullptr;
     cudaStream_t bs = early ? bin_stream : c->stream;
     SymScratch s;
@@ -397,6 +404,8 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     g.total_slot = slot;
     g.sampled_flop = sampled_flop;
     g.window = window;
+    g.tsize = tsize;
+    g.tsize_cap = tsize_cap;
     CU(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * 16, bs));
     CU(cudaMemsetAsync(c->heavy_meta.p, 0, sizeof(long long) * kHeavyMeta, bs));
     if (n_items == 0) return SPNNZ_OK;
@@ -420,6 +429,11 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
         CU(cudaStreamWaitEvent(c->stream, c->fork, 0));  // heavy batches: after the bin
     } else {
         CU(cudaStreamSynchronize(c->stream));  // bin + the two small copies
+    }
+    if (tsize && c->h_meta[kMetaCapacity] > 0) {  // symbolic.hpp:37-40
+        for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaStreamWaitEvent(c->stream, c->join[i], 0));
+        return set_err(SPNNZ_EINVAL, "HashAccumulator: tsize %lld exceeds capacity %lld",
+                       static_cast<long long>(c->h_meta[kMetaCapacity]), tsize_cap);
     }
     const int64_t heavy = c->h_counts[kHeavyBin];
     if (heavy > 0) {
@@ -467,18 +481,25 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     return SPNNZ_OK;
 }
 
+// FLOP pass of the local rows into `out` (default: the resident profile).
 int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr,
-              const PredOut& pred = PredOut()) {
+              const PredOut& pred = PredOut(), DBuf<int64_t>* out = nullptr) {
     if (!stream) stream = c->stream;
+    if (!out) out = &c->flop;
     const DevCsr& a = c->a;
     const int64_t tiles = flop_tiles(a);
-    RC(c->flop.ensure(std::max<int64_t>(a.rows, 1)));
+    RC(out->ensure(std::max<int64_t>(a.rows, 1)));
     RC(c->tile_x.ensure(tiles + 1));
     RC(c->tile_carry.ensure(tiles + 1));
     RC(c->tile_total.ensure(tiles + 1));
     RC(c->tile_max.ensure(tiles + 1));
-    RC(c->deg.ensure(std::max<int64_t>(c->b_rows, 1)));
+    RC(c->deg.ensure(int64_t(c->b_rows) + 8));  // + padding: shared-memory copies read 16-byte words
     FlopScratch s{c->tile_x.p, c->tile_carry.p, c->tile_total.p, c->tile_max.p};
+    FlopMode mode;
+    mode.b_rows = c->b_rows;
+    mode.rows_mode = c->rows_mode;
+    mode.num_sms = c->num_sms;
+    if (const char* e = getenv("SPNNZ_FLOP_SMEM")) mode.no_smem = atoi(e) == 0;  // A/B knob
     if (c->pending_upload && stream == c->stream) {
         // B.col still landing: degrees and the partition need only B.rpt; the
         // tiles of each chunk run on fstream as soon as the chunk is in; the
@@ -498,19 +519,20 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
             if (k + 1 == c->n_chunks) t_end = tiles;
             CU(cudaStreamWaitEvent(c->fstream, c->ev_chunk[k], 0));
             if (t_end > t_prev)
-                CU(launch_flop_tiles(a, c->deg.p, c->b_rpt.p, s, c->flop.p, t_prev, t_end, c->fstream, pred));
+                CU(launch_flop_tiles(a, c->deg.p, c->b_rpt.p, s, out->p, t_prev, t_end, c->fstream, pred,
+                                     mode));
             t_prev = t_end;
         }
         CU(cudaEventRecord(c->ev_fdone, c->fstream));
         CU(cudaStreamWaitEvent(c->stream, c->ev_fdone, 0));
         RC(settle_upload(c));
-        CU(launch_flop_fixup(a, s, c->flop.p, c->totals.p, stream, pred));
+        CU(launch_flop_fixup(a, s, out->p, c->totals.p, stream, pred));
         *launches += a.rows ? nk + 1 + c->n_chunks : 0;
         return SPNNZ_OK;
     }
     int64_t nk = 0;
     CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, stream, &a, &s, &nk));
-    CU(launch_flop(a, c->deg.p, c->b_rpt.p, s, c->flop.p, c->totals.p, stream, pred));
+    CU(launch_flop(a, c->deg.p, c->b_rpt.p, s, out->p, c->totals.p, stream, pred, mode));
     *launches += a.rows ? nk + 2 : 0;
     return SPNNZ_OK;
 }
@@ -732,6 +754,51 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
         c->ev_order = 1;
     }
     c->profile_valid = true;
+    c->profile_own = true;
+    c->last_launches = launches;
+    return SPNNZ_OK;
+}
+
+// run_prediction_with_plan (predict.hpp:202-216) on the RESIDENT profile --
+// the reference takes the profile as an argument and runs no FLOP pass:
+// sampled symbolic (tsize = the profile's flop), f* from the profile,
+// F = profile.total_flop, one all-reduce of {f*, z*}, the per-row views of
+// the profile's flop.
+int pipeline_profile(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, int64_t* d_ceil,
+                     double* d_real) {
+    int64_t launches = 0;
+    RC(settle_upload(c));
+    c->h_totals[kF] = c->profile_total;
+    c->h_totals[kMax] = c->profile_max;
+    for (int i = 0; i < kTotals; ++i)
+        if (i != kF && i != kMax) c->h_totals[i] = 0;
+    CU(cudaMemcpyAsync(c->totals.p, c->h_totals, sizeof(long long) * kTotals, cudaMemcpyHostToDevice,
+                       c->stream));
+    const int64_t* item_flop = nullptr;
+    if (!c->profile_own && n > 0) {
+        // bin by each sampled row's true FLOP; the profile is the table size
+        RC(c->item_flop.ensure(n));
+        RC(c->item_units.ensure(n + 1));
+        CU(launch_item_flop(c->a, c->b_rpt.p, c->row_lo, d_rows, n, c->item_flop.p, c->item_units.p,
+                            c->num_sms, c->stream));
+        launches += 3;
+        item_flop = c->item_flop.p;
+    }
+    ev_record(c, 0);
+    ev_record(c, 1);
+    ev_record(c, 2);
+    RC(run_symbolic(c, d_rows, n, nullptr, kZStar, true, &launches, item_flop, nullptr, nullptr,
+                    nullptr, c->profile_own ? nullptr : c->flop.p, c->profile_max));
+    ev_record(c, 3);
+    RC(allreduce_totals(c, kFStar, 2, false));  // f*, z*; F and max are the profile's
+    ev_record(c, 4);
+    if (d_ceil || d_real) {
+        CU(launch_predict(c->flop.p, local_rows(c), c->totals.p, 0.0, d_ceil, d_real, c->num_sms,
+                          c->stream));
+        ++launches;
+    }
+    ev_record(c, 5);
+    c->ev_order = 0;
     c->last_launches = launches;
     return SPNNZ_OK;
 }
@@ -914,6 +981,7 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
     if (!a->rpt || !bv->rpt) return set_err(SPNNZ_EINVAL, "load: null rpt");
     c->loaded = false;
     c->profile_valid = false;
+    c->profile_own = false;
     c->same_b = same;
     c->a_rows = a->rows;
     c->a_cols = a->cols;
@@ -992,6 +1060,34 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
         v.col = c->a_col.p - a_lo;  // indexed with absolute offsets
     }
     c->a = v;
+    // Banded A (consecutive rows reach consecutive columns): sampled pairs of
+    // consecutive rows of the shard; on the host for host views, else by a
+    // small kernel (the device path synchronizes here anyway)
+    {
+        int st[3] = {0, 0, 0};
+        const int32_t lo = c->row_lo, hi = c->row_hi;
+        if (hi - lo >= 2) {
+            if (residency == SPNNZ_HOST) {
+                for (int i = 0; i < kLocalitySamples; ++i) {
+                    const int32_t r = lo + static_cast<int32_t>((int64_t(hi - lo - 1) * i) / kLocalitySamples);
+                    const int64_t p0 = a->rpt[r], p1 = a->rpt[r + 1], p2 = a->rpt[r + 2];
+                    if (p1 > p0 && p2 > p1) {
+                        ++st[0];
+                        const int d = a->col[p1] - a->col[p0];
+                        st[1] += d >= 0 && d <= 2;
+                        st[2] += p1 - p0 <= 64;
+                    }
+                }
+            } else {
+                RC(c->bad.ensure(3));
+                CU(launch_locality(a->rpt, a->col, lo, hi, kLocalitySamples, c->bad.p, c->stream));
+                CU(cudaMemcpyAsync(st, c->bad.p, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+                CU(cudaStreamSynchronize(c->stream));
+            }
+        }
+        c->rows_mode = banded_rows(st[0], st[1], st[2]);
+        if (const char* e = getenv("SPNNZ_FLOP_ROWS")) c->rows_mode = atoi(e) > 0;  // A/B knob
+    }
     // The interval heavy path (opt-in, SPNNZ_HEAVY_INTERVALS=1) needs B's rows
     // sorted -- the reference's CsrMatrix invariant, checked here once.
     const char* ivenv = getenv("SPNNZ_HEAVY_INTERVALS");
@@ -1038,6 +1134,7 @@ int spnnz_gpu_compute_flop(spnnz_gpu_ctx* c, int64_t* flop_out, int residency, i
     }
     RC(read_totals(c));
     c->profile_valid = true;
+    c->profile_own = true;
     c->profile_total = c->h_totals[kF];
     c->profile_max = c->h_totals[kMax];
     if (total) *total = c->profile_total;
@@ -1066,6 +1163,7 @@ int spnnz_gpu_set_profile(spnnz_gpu_ctx* c, const int64_t* flop_in, int64_t rows
                                                      : cudaMemcpyHostToDevice,
                            c->stream));
     c->profile_valid = true;
+    c->profile_own = false;
     c->profile_total = total;
     c->profile_max = max;
     return SPNNZ_OK;
@@ -1143,7 +1241,17 @@ int spnnz_gpu_sampled_symbolic(spnnz_gpu_ctx* c, const int32_t* rows, int64_t n,
     }
     int64_t launches = 0;
     CU(cudaMemsetAsync(c->totals.p, 0, sizeof(long long) * kTotals, c->stream));
-    RC(run_symbolic(c, d_rows, n, d_out, kZStar, false, &launches));
+    const int64_t* item_flop = nullptr;
+    if (!c->profile_own && n > 0) {  // caller profile: bin by true FLOP, profile = tsize
+        RC(c->item_flop.ensure(n));
+        RC(c->item_units.ensure(n + 1));
+        CU(launch_item_flop(c->a, c->b_rpt.p, c->row_lo, d_rows, n, c->item_flop.p, c->item_units.p,
+                            c->num_sms, c->stream));
+        launches += 3;
+        item_flop = c->item_flop.p;
+    }
+    RC(run_symbolic(c, d_rows, n, d_out, kZStar, false, &launches, item_flop, nullptr, nullptr,
+                    nullptr, c->profile_own ? nullptr : c->flop.p, c->profile_max));
     RC(allreduce_totals(c));
     if (per_sample && residency == SPNNZ_HOST && n)
         CU(cudaMemcpyAsync(per_sample, d_out, 8 * size_t(n), cudaMemcpyDeviceToHost, c->stream));
@@ -1169,7 +1277,13 @@ int spnnz_gpu_exact_symbolic(spnnz_gpu_ctx* c, int64_t* per_row, int residency, 
     }
     int64_t launches = 0;
     CU(cudaMemsetAsync(c->totals.p, 0, sizeof(long long) * kTotals, c->stream));
-    RC(run_symbolic(c, nullptr, m, d_out, kZ, false, &launches));
+    const int64_t* item_flop = nullptr;
+    if (!c->profile_own && m > 0) {  // caller profile: bin by true FLOP, profile = tsize
+        RC(flop_pass(c, &launches, c->stream, PredOut(), &c->flop_true));
+        item_flop = c->flop_true.p;
+    }
+    RC(run_symbolic(c, nullptr, m, d_out, kZ, false, &launches, item_flop, nullptr, nullptr,
+                    nullptr, c->profile_own ? nullptr : c->flop.p, c->profile_max));
     RC(allreduce_totals(c));
     if (per_row && residency == SPNNZ_HOST && m)
         CU(cudaMemcpyAsync(per_row, d_out, 8 * size_t(m), cudaMemcpyDeviceToHost, c->stream));
@@ -1220,7 +1334,7 @@ int spnnz_gpu_predict_row_structure_ceil(spnnz_gpu_ctx* c, double cr, int64_t* o
 namespace {
 int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, bool draw,
                uint64_t seed, spnnz_report* rep, int64_t* row_ceil, double* row_real,
-               int residency) {
+               int residency, bool with_profile = false) {
     const int m = local_rows(c);
     int64_t* d_ceil = row_ceil;
     double* d_real = row_real;
@@ -1234,7 +1348,10 @@ int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, boo
             d_real = c->outf.p;
         }
     }
-    RC(pipeline(c, d_rows, n, draw, seed, m ? d_ceil : nullptr, m ? d_real : nullptr));
+    if (with_profile)
+        RC(pipeline_profile(c, d_rows, n, m ? d_ceil : nullptr, m ? d_real : nullptr));
+    else
+        RC(pipeline(c, d_rows, n, draw, seed, m ? d_ceil : nullptr, m ? d_real : nullptr));
     if (residency == SPNNZ_HOST && m) {
         if (row_ceil)
             CU(cudaMemcpyAsync(row_ceil, d_ceil, 8 * size_t(m), cudaMemcpyDeviceToHost, c->stream));
@@ -1270,12 +1387,14 @@ int spnnz_gpu_run_prediction(spnnz_gpu_ctx* c, uint64_t seed, double fraction, i
 int spnnz_gpu_run_prediction_with_plan(spnnz_gpu_ctx* c, const int32_t* rows, int64_t n, double p,
                                        int rows_residency, spnnz_report* rep, int64_t* row_ceil,
                                        double* row_real, int out_residency) {
-    RC(check_ctx(c, true, false));  // the pipeline overlaps a pending upload
-    RC(dims_ok(c, "compute_flop"));
+    RC(check_ctx(c));
+    if (c->a_cols != c->b_rows) return set_err(SPNNZ_EINVAL, "symbolic: A.cols != B.rows");
+    if (!c->profile_valid)
+        return set_err(SPNNZ_ESTATE, "run_prediction_with_plan: no resident profile");
     const int32_t* d_rows = nullptr;
     RC(check_rows(c, rows, n, rows_residency, "sampled_symbolic", &d_rows));
     if (!(p > 0.0)) return set_err(SPNNZ_EINVAL, "predict_reference: p must be positive");
-    return run_common(c, d_rows, n, p, false, 0, rep, row_ceil, row_real, out_residency);
+    return run_common(c, d_rows, n, p, false, 0, rep, row_ceil, row_real, out_residency, true);
 }
 
 // ------------------------------------------------------------ estimators

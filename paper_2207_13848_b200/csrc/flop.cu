@@ -262,114 +262,237 @@ __device__ __forceinline__ Emit make_emit(const PredOut& p) {
     return e;
 }
 
-template <int BLOCK, int V, bool PRED>
-__global__ void __launch_bounds__(BLOCK, (SPNNZ_FLOP_MINB / BLOCK < 32 ? SPNNZ_FLOP_MINB / BLOCK : 32))
-k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
-       const uint16_t* __restrict__ bdeg, const int64_t* __restrict__ brpt, int32_t m,
-       int64_t base, int64_t nnz, const int32_t* __restrict__ tile_row,
-       int64_t* __restrict__ flop, long long* __restrict__ tile_lead,
-       long long* __restrict__ tile_total, long long* __restrict__ tile_max, PredOut pred,
-       int64_t t0) {
+// Degree sources: the uint16 degree array in global memory (L2-resident,
+// gathered under evict_last) or a copy of it in shared memory (B with few
+// rows: config 4's 65536 rows are a 128 KB table).  0xFFFF escapes to B.rpt.
+struct GlobalDeg {
+    const uint16_t* deg;
+    uint64_t last;
+    __device__ __forceinline__ int32_t operator()(int32_t c) const { return gather_deg(deg + c, last); }
+};
+struct SharedDeg {
+    const uint16_t* deg;  // shared window
+    __device__ __forceinline__ int32_t operator()(int32_t c) const { return deg[c]; }
+};
+
+// Barrier over the threads that work on one tile: the whole block, or one
+// 128-thread group of a persistent block (named barrier 1 + group).
+struct BlockBar {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+template <int THREADS>
+struct GroupBar {
+    int id;
+    __device__ __forceinline__ void operator()() const {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(THREADS) : "memory");
+    }
+};
+
+// Shared memory of one tile.
+template <int BLOCK, int V>
+struct TileSmem {
+    static constexpr int TILE = BLOCK * V, NW = BLOCK / 32;
+    uint32_t start[TILE / 32];  // bit i: an owned non-empty row starts at entry i
+    int32_t rowat[TILE];        // ... and its id (read only where the bit is set); row mode: the tile's columns
+    Carry wc[NW];
+    long long red[NW], red2[NW];
+};
+
+struct TileArgs {
+    const int64_t* __restrict__ arpt;
+    const int32_t* __restrict__ acol;
+    const int64_t* __restrict__ brpt;
+    int64_t base, nnz;
+    const int32_t* __restrict__ tile_row;
+    int64_t* __restrict__ flop;
+    long long* __restrict__ tile_lead;
+    long long* __restrict__ tile_total;
+    long long* __restrict__ tile_max;
+    int rows_mode;  // banded A (host check at load): short-row tiles go row per thread
+};
+
+// The exact degree of B row c given its uint16 entry (0xFFFF: look it up).
+__device__ __forceinline__ int32_t exact_deg(int32_t d, int32_t c, const int64_t* brpt) {
+    return d == 0xFFFF ? static_cast<int32_t>(__ldg(&brpt[c + 1]) - __ldg(&brpt[c])) : d;
+}
+
+// Tile totals: F and max in one pass (warp reductions, one shared slot pair
+// per warp, warp 0 finishes both).
+template <int BLOCK, int V, class Bar>
+__device__ __forceinline__ void tile_totals(TileSmem<BLOCK, V>& sm, const TileArgs& g, int64_t t, int tid,
+                                            long long tsum, long long tmax, Bar bar) {
+    constexpr int NW = BLOCK / 32;
+    const int lane = tid & 31, warp = tid >> 5;
+    tsum = warp_sum_ll(tsum);
+    tmax = warp_max_ll(tmax);
+    if (lane == 0) {
+        sm.red[warp] = tsum;
+        sm.red2[warp] = tmax;
+    }
+    bar();
+    if (warp == 0) {
+        long long a = lane < NW ? sm.red[lane] : 0, b = lane < NW ? sm.red2[lane] : 0;
+        a = warp_sum_ll(a);
+        b = warp_max_ll(b);
+        if (lane == 0) {
+            g.tile_total[t] = a;
+            g.tile_max[t] = b;
+        }
+    }
+}
+
+// Row mode, for banded A (27-point stencil: consecutive rows reach
+// consecutive columns): the tile's columns are staged in shared memory and
+// each thread walks whole rows, so a warp's k-th gathers hit ~32 consecutive
+// degrees (one or two L1 lines) instead of ~9 clusters per instruction.
+template <int BLOCK, int V, bool PRED, class Deg, class Bar>
+__device__ __forceinline__ void flop_tile_rows(TileSmem<BLOCK, V>& sm, const TileArgs& g, int64_t t, int tid,
+                                               int64_t ts, int n, int32_t r0, int32_t r1, const int32_t (&c)[V],
+                                               Deg deg, Bar bar, const Emit& emit) {
+    const int i0 = tid * V;
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+        if (i0 + k < n) sm.rowat[i0 + k] = c[k];
+    bar();
+    const int64_t te = ts + n;
+    long long tsum = 0, tmax = 0;
+    // the leading slice (a row owned by an earlier tile): warp 0
+    if (tid < 32) {
+        const int64_t a0 = __ldg(&g.arpt[r0]);
+        const int lead_n = static_cast<int>((a0 < te ? a0 : te) - ts);
+        long long s = 0;
+        for (int i = tid; i < lead_n; i += 32) s += exact_deg(deg(sm.rowat[i]), sm.rowat[i], g.brpt);
+        s = warp_sum_ll(s);
+        if (tid == 0) {
+            g.tile_lead[t] = s;
+            tsum += s;
+        }
+    }
+    for (int32_t r = r0 + tid; r < r1; r += BLOCK) {
+        const int64_t a = __ldg(&g.arpt[r]), b = __ldg(&g.arpt[r + 1]);
+        const int e0 = static_cast<int>(a - ts), e1 = static_cast<int>((b < te ? b : te) - ts);
+        long long s = 0;
+        int e = e0;
+        for (; e + 4 <= e1; e += 4) {  // four gathers in flight
+            int32_t d[4], cc[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cc[k] = sm.rowat[e + k];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) d[k] = deg(cc[k]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s += exact_deg(d[k], cc[k], g.brpt);
+        }
+        for (; e < e1; ++e) s += exact_deg(deg(sm.rowat[e]), sm.rowat[e], g.brpt);
+        tsum += s;
+        g.flop[r] = s;  // partial when the row runs past the tile: the fixup adds the rest
+        if (b <= te) {
+            tmax = s > tmax ? s : tmax;
+            if (PRED) emit(r, s);
+        }
+    }
+    tile_totals<BLOCK, V>(sm, g, t, tid, tsum, tmax, bar);
+}
+
+// One tile of kFlopTile entries by BLOCK threads (tid in [0, BLOCK)).
+template <int BLOCK, int V, bool PRED, class Deg, class Bar>
+__device__ __forceinline__ void flop_tile(TileSmem<BLOCK, V>& sm, const TileArgs& g, int64_t t, int tid,
+                                          Deg deg, Bar bar, const Emit& emit) {
     constexpr int TILE = BLOCK * V, NW = BLOCK / 32;
     static_assert(TILE == kFlopTile && (V == 8 || V == 16 || V == 32), "tile size");
-    __shared__ uint32_t s_start[TILE / 32];  // bit i: an owned non-empty row starts at entry i
-    __shared__ int32_t s_rowat[TILE];        // ... and its id (read only where the bit is set)
-    __shared__ Carry s_wc[NW];
-    __shared__ long long s_red[NW], s_red2[NW];
-
-    const uint64_t first = policy_evict_first(), last = policy_evict_last();
-    const int64_t t = t0 + blockIdx.x;
-    const int64_t ts = tile_start(base, nnz, t), te = tile_start(base, nnz, t + 1);
+    const uint64_t first = policy_evict_first();
+    const int64_t ts = tile_start(g.base, g.nnz, t), te = tile_start(g.base, g.nnz, t + 1);
     const int n = static_cast<int>(te - ts);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int k = tid; k < TILE / 32; k += BLOCK) s_start[k] = 0u;
-    Emit emit{};
-    if (PRED) emit = make_emit(pred);
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int k = tid; k < TILE / 32; k += BLOCK) sm.start[k] = 0u;
+    const int32_t r0 = g.tile_row[t], r1 = g.tile_row[t + 1];
 
     // 1. this thread's V consecutive entries: columns (16-byte evict_first
-    //    loads when the tile is whole), then all V degree gathers in flight
+    //    loads when the tile is whole)
     const int i0 = tid * V;
-    int32_t d[V];
-    {
-        int32_t c[V];
-        if (n == TILE && (reinterpret_cast<uintptr_t>(acol + ts) & 15) == 0) {
-            const int4* src = reinterpret_cast<const int4*>(acol + ts + i0);
+    int32_t c[V];
+    if (n == TILE && (reinterpret_cast<uintptr_t>(g.acol + ts) & 15) == 0) {
+        const int4* src = reinterpret_cast<const int4*>(g.acol + ts + i0);
 #pragma unroll
-            for (int k = 0; k < V / 4; ++k) {
-                const int4 x = load_cols(src + k, first);
-                c[4 * k] = x.x;
-                c[4 * k + 1] = x.y;
-                c[4 * k + 2] = x.z;
-                c[4 * k + 3] = x.w;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < V; ++k) c[k] = i0 + k < n ? ld_stream_i32(acol + ts + i0 + k, first) : -1;
+        for (int k = 0; k < V / 4; ++k) {
+            const int4 x = load_cols(src + k, first);
+            c[4 * k] = x.x;
+            c[4 * k + 1] = x.y;
+            c[4 * k + 2] = x.z;
+            c[4 * k + 3] = x.w;
         }
+    } else {
 #pragma unroll
-        for (int k = 0; k < V; ++k) d[k] = c[k] >= 0 ? static_cast<int32_t>(gather_deg(bdeg + c[k], last)) : 0;
-#pragma unroll
-        for (int k = 0; k < V; ++k)
-            if (d[k] == 0xFFFF) d[k] = static_cast<int32_t>(__ldg(&brpt[c[k] + 1]) - __ldg(&brpt[c[k]]));
+        for (int k = 0; k < V; ++k) c[k] = i0 + k < n ? ld_stream_i32(g.acol + ts + i0 + k, first) : -1;
     }
+    // row mode: owned rows averaging <= 48 entries in a banded matrix
+    if (g.rows_mode && r1 > r0 && n <= 48 * (r1 - r0)) {
+        flop_tile_rows<BLOCK, V, PRED>(sm, g, t, tid, ts, n, r0, r1, c, deg, bar, emit);
+        return;
+    }
+    //    ... then all V degree gathers in flight
+    int32_t d[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) d[k] = c[k] >= 0 ? deg(c[k]) : 0;
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+        if (d[k] == 0xFFFF) d[k] = static_cast<int32_t>(__ldg(&g.brpt[c[k] + 1]) - __ldg(&g.brpt[c[k]]));
     long long tsum = 0;
 #pragma unroll
     for (int k = 0; k < V; ++k) tsum += d[k];
-    __syncthreads();  // the start bitmap is clear
+    bar();  // the start bitmap is clear
 
     // 2. owned rows [r0, r1): mark where the non-empty ones start; empty ones are 0
-    const int32_t r0 = tile_row[t], r1 = tile_row[t + 1];
     for (int32_t r = r0 + tid; r < r1; r += BLOCK) {
-        const int64_t a = __ldg(&arpt[r]), b = __ldg(&arpt[r + 1]);
+        const int64_t a = __ldg(&g.arpt[r]), b = __ldg(&g.arpt[r + 1]);
         if (b > a) {
             const int pos = static_cast<int>(a - ts);
-            atomicOr(&s_start[pos >> 5], 1u << (pos & 31));
-            s_rowat[pos] = r;
+            atomicOr(&sm.start[pos >> 5], 1u << (pos & 31));
+            sm.rowat[pos] = r;
         } else {
-            flop[r] = 0;
+            g.flop[r] = 0;
             if (PRED) emit(r, 0);
         }
     }
-    __syncthreads();
+    bar();
 
     // 3. segmented sum over the thread's entries: rows that start and end
     //    inside are written here; the head (before the first start) and the
     //    tail (from the last start) are combined across threads below
-    const uint32_t bits = V == 32 ? s_start[i0 >> 5] : (s_start[i0 >> 5] >> (i0 & 31)) & ((1u << (V & 31)) - 1u);
+    const uint32_t bits = V == 32 ? sm.start[i0 >> 5] : (sm.start[i0 >> 5] >> (i0 & 31)) & ((1u << (V & 31)) - 1u);
     long long cur = 0, head = 0, tmax = 0;
     int32_t row = -1;
 #pragma unroll
     for (int k = 0; k < V; ++k) {
         if ((bits >> k) & 1u) {
             if (row >= 0) {
-                flop[row] = cur;  // complete inside the thread
+                g.flop[row] = cur;  // complete inside the thread
                 if (PRED) emit(row, cur);
                 tmax = cur > tmax ? cur : tmax;
             } else {
                 head = cur;
             }
-            row = s_rowat[i0 + k];
+            row = sm.rowat[i0 + k];
             cur = 0;
         }
         cur += d[k];
     }
     Carry mine;
     mine.flag = bits != 0u;
-    mine.v = mine.flag ? cur : cur;  // tail value, or the whole thread when no row starts here
+    mine.v = cur;  // tail value, or the whole thread when no row starts here
     mine.row = row;
     if (!mine.flag) head = cur;
 
-    // 4. block-wide exclusive segmented scan of the carries
+    // 4. tile-wide exclusive segmented scan of the carries
     Carry inc = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const Carry u = shfl_up_carry(inc, o);
         if (lane >= o) inc = carry_op(u, inc);
     }
-    if (lane == 31) s_wc[warp] = inc;
-    __syncthreads();
+    if (lane == 31) sm.wc[warp] = inc;
+    bar();
     Carry pre{0, 0, -1};  // carry entering this warp
-    for (int w = 0; w < warp; ++w) pre = carry_op(pre, s_wc[w]);
+    for (int w = 0; w < warp; ++w) pre = carry_op(pre, sm.wc[w]);
     Carry excl = shfl_up_carry(inc, 1);
     if (lane == 0) excl = Carry{0, 0, -1};
     const Carry cin = carry_op(pre, excl);  // carry entering this thread
@@ -377,43 +500,64 @@ k_flop(const int64_t* __restrict__ arpt, const int32_t* __restrict__ acol,
         // the carried row ends right before this thread's first start
         const long long v = cin.v + head;
         if (cin.flag) {
-            flop[cin.row] = v;
+            g.flop[cin.row] = v;
             if (PRED) emit(cin.row, v);
             tmax = v > tmax ? v : tmax;
         } else {
-            tile_lead[t] = v;  // continues a row owned by an earlier tile
+            g.tile_lead[t] = v;  // continues a row owned by an earlier tile
         }
     }
     if (tid == BLOCK - 1) {
         const Carry all = carry_op(cin, mine);
         if (all.flag) {
-            flop[all.row] = all.v;  // the fixup adds the following tiles' leading slices
-            if (__ldg(&arpt[all.row + 1]) <= te) {  // the row ends with the tile: final
+            g.flop[all.row] = all.v;  // the fixup adds the following tiles' leading slices
+            if (__ldg(&g.arpt[all.row + 1]) <= te) {  // the row ends with the tile: final
                 tmax = all.v > tmax ? all.v : tmax;
                 if (PRED) emit(all.row, all.v);
             }
         } else {
-            tile_lead[t] = all.v;  // no row starts in this tile
+            g.tile_lead[t] = all.v;  // no row starts in this tile
         }
     }
-    // tile F and max in one pass: warp reductions, one shared slot pair per
-    // warp, warp 0 finishes both (the scan's barrier orders s_red's reuse)
-    tsum = warp_sum_ll(tsum);
-    tmax = warp_max_ll(tmax);
-    if (lane == 0) {
-        s_red[warp] = tsum;
-        s_red2[warp] = tmax;
-    }
+    // (the scan's barrier orders the reuse of red / red2)
+    (void)NW;
+    tile_totals<BLOCK, V>(sm, g, t, tid, tsum, tmax, bar);
+}
+
+// One block per tile, degrees gathered from global memory (L2).
+template <int BLOCK, int V, bool PRED>
+__global__ void __launch_bounds__(BLOCK, (SPNNZ_FLOP_MINB / BLOCK < 32 ? SPNNZ_FLOP_MINB / BLOCK : 32))
+k_flop(TileArgs g, const uint16_t* __restrict__ bdeg, PredOut pred, int64_t t0) {
+    __shared__ TileSmem<BLOCK, V> sm;
+    Emit emit{};
+    if (PRED) emit = make_emit(pred);
+    flop_tile<BLOCK, V, PRED>(sm, g, t0 + blockIdx.x, threadIdx.x, GlobalDeg{bdeg, policy_evict_last()},
+                              BlockBar{}, emit);
+}
+
+// Persistent blocks of G tile groups (G x 128 threads, one block per SM) with
+// B's whole degree table in shared memory: loaded once per block, then every
+// gather is a shared-memory load (config 4: K = 65536, 128 KB).  Each group
+// runs the tile code on its own tiles with its own named barrier.
+constexpr int kSmemGroups = 8;
+template <int V, bool PRED>
+__global__ void __launch_bounds__(kFlopBlock * kSmemGroups, 1)
+k_flop_smem(TileArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut pred, int64_t t0,
+            int64_t t1) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    auto* tiles = reinterpret_cast<TileSmem<kFlopBlock, V>*>(s_raw);
+    uint16_t* s_deg = reinterpret_cast<uint16_t*>(s_raw + sizeof(TileSmem<kFlopBlock, V>) * kSmemGroups);
+    // the degree table, 16 bytes per thread per step (k_rows padded to 8)
+    const int words = (k_rows + 7) >> 3;
+    for (int i = threadIdx.x; i < words; i += blockDim.x)
+        reinterpret_cast<int4*>(s_deg)[i] = __ldg(reinterpret_cast<const int4*>(bdeg) + i);
     __syncthreads();
-    if (warp == 0) {
-        long long a = lane < NW ? s_red[lane] : 0, b = lane < NW ? s_red2[lane] : 0;
-        a = warp_sum_ll(a);
-        b = warp_max_ll(b);
-        if (lane == 0) {
-            tile_total[t] = a;
-            tile_max[t] = b;
-        }
-    }
+    Emit emit{};
+    if (PRED) emit = make_emit(pred);
+    const int grp = threadIdx.x / kFlopBlock, tid = threadIdx.x % kFlopBlock;
+    const GroupBar<kFlopBlock> bar{1 + grp};
+    for (int64_t t = t0 + int64_t(blockIdx.x) * kSmemGroups + grp; t < t1; t += int64_t(gridDim.x) * kSmemGroups)
+        flop_tile<kFlopBlock, V, PRED>(tiles[grp], g, t, tid, SharedDeg{s_deg}, bar, emit);
 }
 
 // Adds each tile's leading slice to the row it continues (one thread per
@@ -631,7 +775,32 @@ __global__ void k_start_descents(const int64_t* __restrict__ rpt, const int32_t*
     if ((threadIdx.x & 31) == 0 && d) atomicAdd(&cnt[1], d);
 }
 
+// Banded-A check for the FLOP pass's row mode (sampled pairs of
+// consecutive rows): out[0] pairs with both rows non-empty, out[1] of them
+// whose first columns advance by 0..2 (a stencil's rows do), out[2] of them
+// whose first row has <= 64 entries.
+__global__ void k_locality(const int64_t* __restrict__ rpt, const int32_t* __restrict__ col, int32_t lo,
+                           int32_t hi, int n, int* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || hi - lo < 2) return;
+    const int32_t r = lo + static_cast<int32_t>((int64_t(hi - lo - 1) * i) / n);
+    const int64_t a = rpt[r], b = rpt[r + 1], c = rpt[r + 2];
+    if (b > a && c > b) {
+        atomicAdd(&out[0], 1);
+        const int d = col[b] - col[a];
+        if (d >= 0 && d <= 2) atomicAdd(&out[1], 1);
+        if (b - a <= 64) atomicAdd(&out[2], 1);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_locality(const int64_t* rpt, const int32_t* col, int32_t lo, int32_t hi, int n, int* out3,
+                            cudaStream_t stream) {
+    cudaMemsetAsync(out3, 0, 3 * sizeof(int), stream);
+    k_locality<<<(n + 255) / 256, 256, 0, stream>>>(rpt, col, lo, hi, n, out3);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_flop_window(const int64_t* item_flop, int64_t n, int rank, int world, int64_t* window,
                                cudaStream_t stream) {
@@ -752,20 +921,60 @@ cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStr
 }
 #endif
 
+static size_t flop_smem_bytes(int32_t k_rows) {
+    return sizeof(TileSmem<kFlopBlock, kFlopIpt>) * kSmemGroups + ((size_t(k_rows) * 2 + 15) & ~size_t(15));
+}
+
+bool flop_smem_fits(int32_t k_rows) { return k_rows > 0 && flop_smem_bytes(k_rows) <= 227 * 1024; }
+
+static TileArgs tile_args(const DevCsr& a, const int64_t* brpt, const FlopScratch& s, int64_t* flop,
+                          const FlopMode& mode) {
+    TileArgs g;
+    g.arpt = a.rpt;
+    g.acol = a.col;
+    g.brpt = brpt;
+    g.base = a.base;
+    g.nnz = a.nnz;
+    g.tile_row = s.tile_x;
+    g.flop = flop;
+    g.tile_lead = s.tile_carry;
+    g.tile_total = s.tile_total;
+    g.tile_max = s.tile_max;
+    g.rows_mode = mode.rows_mode ? 1 : 0;
+    return g;
+}
+
+template <bool PRED>
+static cudaError_t launch_tiles(const TileArgs& g, const uint16_t* bdeg, int64_t t_begin, int64_t t_end,
+                                cudaStream_t stream, const PredOut& pred, const FlopMode& mode) {
+    if (flop_smem_fits(mode.b_rows) && !mode.no_smem) {
+        const size_t smem = flop_smem_bytes(mode.b_rows);
+        static std::atomic<unsigned long long> attr_done{0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!(attr_done.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
+            cudaFuncSetAttribute(k_flop_smem<kFlopIpt, PRED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 227 * 1024);
+            attr_done.fetch_or(1ull << (dev & 63), std::memory_order_release);
+        }
+        int64_t grid = (t_end - t_begin + kSmemGroups - 1) / kSmemGroups;
+        if (grid > mode.num_sms) grid = mode.num_sms;
+        k_flop_smem<kFlopIpt, PRED><<<static_cast<unsigned>(grid), kFlopBlock * kSmemGroups, smem, stream>>>(
+            g, bdeg, mode.b_rows, pred, t_begin, t_end);
+    } else {
+        k_flop<kFlopBlock, kFlopIpt, PRED><<<static_cast<unsigned>(t_end - t_begin), kFlopBlock, 0, stream>>>(
+            g, bdeg, pred, t_begin);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_flop_tiles(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt,
                               const FlopScratch& s, int64_t* flop, int64_t t_begin, int64_t t_end,
-                              cudaStream_t stream, const PredOut& pred) {
+                              cudaStream_t stream, const PredOut& pred, const FlopMode& mode) {
     if (t_end <= t_begin) return cudaSuccess;
-    const unsigned g = static_cast<unsigned>(t_end - t_begin);
-    if (pred.on())
-        k_flop<kFlopBlock, kFlopIpt, true><<<g, kFlopBlock, 0, stream>>>(
-            a.rpt, a.col, bdeg, brpt, a.rows, a.base, a.nnz, s.tile_x, flop, s.tile_carry,
-            s.tile_total, s.tile_max, pred, t_begin);
-    else
-        k_flop<kFlopBlock, kFlopIpt, false><<<g, kFlopBlock, 0, stream>>>(
-            a.rpt, a.col, bdeg, brpt, a.rows, a.base, a.nnz, s.tile_x, flop, s.tile_carry,
-            s.tile_total, s.tile_max, pred, t_begin);
-    return cudaGetLastError();
+    const TileArgs g = tile_args(a, brpt, s, flop, mode);
+    return pred.on() ? launch_tiles<true>(g, bdeg, t_begin, t_end, stream, pred, mode)
+                     : launch_tiles<false>(g, bdeg, t_begin, t_end, stream, pred, mode);
 }
 
 cudaError_t launch_flop_fixup(const DevCsr& a, const FlopScratch& s, int64_t* flop, long long* totals,
@@ -785,8 +994,8 @@ cudaError_t launch_flop_fixup(const DevCsr& a, const FlopScratch& s, int64_t* fl
 
 cudaError_t launch_flop(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt,
                         const FlopScratch& s, int64_t* flop, long long* totals,
-                        cudaStream_t stream, const PredOut& pred) {
-    const cudaError_t e = launch_flop_tiles(a, bdeg, brpt, s, flop, 0, flop_tiles(a), stream, pred);
+                        cudaStream_t stream, const PredOut& pred, const FlopMode& mode) {
+    const cudaError_t e = launch_flop_tiles(a, bdeg, brpt, s, flop, 0, flop_tiles(a), stream, pred, mode);
     if (e != cudaSuccess) return e;
     return launch_flop_fixup(a, s, flop, totals, stream, pred);
 }

@@ -79,18 +79,38 @@ struct PredOut {
     int64_t redo_cap = 0;
     SPNNZ_HD bool on() const { return ceil || real; }
 };
+// Kernel choice of a FLOP pass.  B with few rows: its whole uint16 degree
+// table sits in shared memory (persistent blocks of 8 tile groups, config 4's
+// 65536 rows = 128 KB); banded A (rows_mode, checked on the host at load):
+// tiles of short rows walk one row per thread over shared-staged columns.
+struct FlopMode {
+    int32_t b_rows = 0;
+    bool rows_mode = false;
+    bool no_smem = false;  // A/B knob: keep the degree table in global memory
+    int num_sms = 148;
+};
+bool flop_smem_fits(int32_t k_rows);
+// Sampled banded-A check (n pairs of consecutive rows in [lo, hi)), rpt/col
+// device arrays with absolute offsets: out3 = {pairs, advancing, short}.
+cudaError_t launch_locality(const int64_t* rpt, const int32_t* col, int32_t lo, int32_t hi, int n, int* out3,
+                            cudaStream_t stream);
+constexpr int kLocalitySamples = 4096;
+// rows_mode when most sampled consecutive rows advance like a stencil's
+inline bool banded_rows(int pairs, int advancing, int short_rows) {
+    return pairs >= 64 && advancing * 4 >= pairs * 3 && short_rows * 20 >= pairs * 19;
+}
 // Redoes the rows listed by a fused FLOP pass (or every row when the list
 // overflowed) with __ddiv_rn.
 cudaError_t launch_predict_redo(const int64_t* flop, int64_t m, const PredOut& pred, int num_sms,
                                 cudaStream_t stream);
 cudaError_t launch_flop(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt,
                         const FlopScratch& s, int64_t* flop, long long* totals,
-                        cudaStream_t stream, const PredOut& pred = PredOut());
+                        cudaStream_t stream, const PredOut& pred, const FlopMode& mode);
 // The same in two steps: tiles [t_begin, t_end) (any order, any streams),
 // then the fixup once every tile is done.
 cudaError_t launch_flop_tiles(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt,
                               const FlopScratch& s, int64_t* flop, int64_t t_begin, int64_t t_end,
-                              cudaStream_t stream, const PredOut& pred = PredOut());
+                              cudaStream_t stream, const PredOut& pred, const FlopMode& mode);
 cudaError_t launch_flop_fixup(const DevCsr& a, const FlopScratch& s, int64_t* flop, long long* totals,
                               cudaStream_t stream, const PredOut& pred = PredOut());
 
@@ -202,7 +222,17 @@ struct SymArgs {
     int total_slot = kZStar;        // kZStar (sampled) or kZ (exact)
     bool sampled_flop = false;      // also accumulate f* into totals[kFStar]
     const int64_t* window = nullptr;  // device [lo, hi): the items this rank counts (nullable = all)
+    // A caller-provided FlopProfile (set_profile): its flop_per_row is the
+    // reference's table size `tsize` (symbolic.hpp:35-40) -- a row with
+    // tsize 0 counts 0 and tsize > max_flop_row is the reference's
+    // invalid_argument (reported through heavy_meta[kMetaCapacity]); f* sums
+    // tsize.  Binning and buffer sizing always use the row's true FLOP
+    // (item_flop), so a profile that disagrees with the matrices cannot
+    // overrun a tier's table.  nullptr: the profile is this context's own.
+    const int64_t* tsize = nullptr;
+    long long tsize_cap = 0;
 };
+constexpr int kMetaCapacity = 9;  // heavy_meta slot: largest tsize above the profile's capacity
 
 // Classifies items into bins (writes out[] = 0 for empty / foreign rows).
 cudaError_t launch_sym_bin(const SymArgs& args, const SymScratch& s, cudaStream_t stream);

@@ -45,8 +45,12 @@ __global__ void __launch_bounds__(BLOCK) k_sym_bin(SymArgs g, SymScratch sc) {
             const bool mine = !g.window || (s >= g.window[0] && s < g.window[1]);
             if (mine && r >= 0 && r < g.a.rows) {
                 const int64_t f = g.item_flop ? g.item_flop[s] : g.flop[r];
-                fsum += f;
-                bin = f == 0 ? 0 : f <= kBin1Max ? 1 : f <= kBin2Max ? 2 : f <= kBin3Max ? 3
+                const int64_t ts = g.tsize ? g.tsize[r] : f;  // the reference's table size
+                fsum += ts;
+                if (g.tsize && ts > g.tsize_cap)  // HashAccumulator: tsize exceeds capacity
+                    atomicMax(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[kMetaCapacity]),
+                              static_cast<unsigned long long>(ts));
+                bin = (f == 0 || ts == 0) ? 0 : f <= kBin1Max ? 1 : f <= kBin2Max ? 2 : f <= kBin3Max ? 3
                                  : f <= kBin4Max ? 4 : f <= kBin5Max ? 5 : kHeavyBin;
                 if (bin == kHeavyBin) {
                     hl = g.a.rpt[r + 1] - g.a.rpt[r] + 1;

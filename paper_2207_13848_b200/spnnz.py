@@ -312,8 +312,17 @@ class Predictor:
                                              _ptr(samples_out), res))
         return _report(rep, real_out, ceil_out, samples_out, seed)
 
-    def run_prediction_with_plan(self, plan: SamplePlan, *, want_real=True,
-                                 want_ceil=True) -> PredictionReport:
+    def run_prediction_with_plan(self, plan: SamplePlan, profile: Optional[FlopProfile] = None, *,
+                                 want_real=True, want_ceil=True) -> PredictionReport:
+        """run_prediction_with_plan (predict.hpp:202-216) on `profile` (installed
+        with set_profile; its flop is each row's table size, f* and the views
+        come from it, F is its total_flop).  Without one, the profile of the
+        loaded matrices is computed on the device first (nothing copied back)."""
+        if profile is not None:
+            self.set_profile(profile)
+        else:
+            t, mx = ctypes.c_int64(), ctypes.c_int64()
+            check(lib().spnnz_gpu_compute_flop(self._ctx, None, HOST, ctypes.byref(t), ctypes.byref(mx)))
         m = self.local_rows
         rows = _rows_arg(plan.sample_rows)
         self._after_torch(rows)
@@ -491,7 +500,7 @@ def run_prediction_with_plan(a: CsrMatrix, b: CsrMatrix, profile: FlopProfile, p
     _check_profile(a, b, profile)
     P = default_predictor()
     P.ensure_loaded(a, b)
-    return P.run_prediction_with_plan(plan)
+    return P.run_prediction_with_plan(plan, profile)
 
 
 def run_prediction(a: CsrMatrix, b: CsrMatrix, seed: int, policy: SamplePolicy = SamplePolicy(),

@@ -26,7 +26,7 @@ def golden():
     import json
     import numpy as np
     g = {}
-    for name in ("refkat", "trials", "configs"):
+    for name in ("refkat", "trials", "configs", "with_plan"):
         with open(os.path.join(GOLDEN, f"{name}.json")) as f:
             g[name] = json.load(f)
     g["cfg1"] = dict(np.load(os.path.join(GOLDEN, "cfg1.npz")))

@@ -7,6 +7,9 @@ Outputs (committed):
   trials.json        per-trial totals + digests for the reference's own test
                      loops (test_flop.cpp:56-68, test_symbolic.cpp:63-77,
                      acceptance.cpp:147-169, test_predict.cpp:184-217)
+  with_plan.json     run_prediction_with_plan on hand-built profiles (the
+                     profile as an input: zeroed / inflated rows, another
+                     total, a capacity violation) -- full arrays
   cfg1.npz           config 1 full arrays (flop, exact nnz, plans, ceil views)
   configs.json       configs 2-5: input digests, totals, report scalars and
                      per-row array digests (exact pass skipped for config 5)
@@ -121,6 +124,64 @@ def trials(R: Reference) -> dict:
     return out
 
 
+def with_plan_cases(R: Reference) -> dict:
+    """spnnz::run_prediction_with_plan (predict.hpp:202-216) on HAND-BUILT
+    profiles: the profile is the function's input, so its flop is each row's
+    hash-table size (tsize 0 counts 0, symbolic.hpp:35-36), f* and the views
+    come from it and F is its total_flop.  Edits keep tsize >= the row's true
+    FLOP (a smaller table would never terminate in the reference), except
+    the capacity case, which the reference rejects (symbolic.hpp:37-40)."""
+    rng = gen.SplitMix64(777)
+    cases = []
+    for t in range(12):
+        m = 30 + rng.next_below(120)
+        k = m if t % 3 else 20 + rng.next_below(100)
+        n = 30 + rng.next_below(120)
+        a = gen.random_pattern(m, k, 0.02 + 0.2 * rng.next_double(), rng)
+        b = a if k == m and t % 3 == 1 else gen.random_pattern(k, n, 0.02 + 0.2 * rng.next_double(), rng)
+        ha = R.matrix(a)
+        hb = ha if b is a else R.matrix(b)
+        flop, F, mx, _ = R.compute_flop(ha, hb, a.rows)
+        kind = ["true", "zeroed", "inflated", "total", "capacity", "zeroed+inflated"][t % 6]
+        f = flop.copy()
+        total, cap = F, mx
+        if "inflated" in kind:
+            for i in range(m):
+                f[i] = f[i] * (1 + rng.next_below(3)) + rng.next_below(5)
+            cap = int(f.max())
+            total = int(f.sum())
+        if "zeroed" in kind:  # after inflating: a zeroed row stays 0
+            for i in range(m):
+                if rng.next_below(3) == 0:
+                    f[i] = 0
+        if kind == "total":
+            total = F * 3 + 17
+        if kind == "capacity":
+            cap = mx - 1
+        nsamp = 1 + rng.next_below(2 * m)
+        rows = np.array([rng.next_below(m) for _ in range(nsamp)], np.int32)
+        if kind == "capacity":
+            rows = np.arange(m, dtype=np.int32)  # exhaustive: the max row is drawn
+        p = nsamp / m if kind != "capacity" else 1.0
+        rec = {"kind": kind, "m": m, "k": k, "n": n, "same": b is a,
+               "a": {"rpt": a.rpt.tolist(), "col": a.col.tolist()},
+               "b": None if b is a else {"rpt": b.rpt.tolist(), "col": b.col.tolist()},
+               "flop": f.tolist(), "total": int(total), "max": int(cap),
+               "rows": rows.tolist(), "p": p}
+        try:
+            rep, real, ceil = R.run_with_plan(ha, hb, f, total, cap, rows, p)
+            rec["report"] = {k2: getattr(rep, k2) for k2, _ in rep._fields_}
+            rec["real"] = real.tolist()
+            rec["ceil"] = ceil.tolist()
+        except ValueError as e:
+            rec["error"] = str(e)
+        cases.append(rec)
+        R.free_matrix(ha)
+        if hb != ha:
+            R.free_matrix(hb)
+    return {"seed": 777, "cases": cases}
+
+
 def config_record(R: Reference, cfg: int, exact: bool) -> dict:
     a, b = gen.make_config(cfg)
     info = gen.CONFIGS[cfg]
@@ -169,6 +230,8 @@ def main():
         json.dump(refkat(R), f, indent=1)
     with open(os.path.join(OUT, "trials.json"), "w") as f:
         json.dump(trials(R), f)
+    with open(os.path.join(OUT, "with_plan.json"), "w") as f:
+        json.dump(with_plan_cases(R), f)
     # config 1: full arrays
     rec, a, b, flop = config_record(R, 1, exact=True)
     ha = R.matrix(a)

@@ -100,6 +100,78 @@ def test_flop_tiles_owning_over_65535_rows(P, oracle):
     assert (pr.flop_per_row == f).all() and pr.total_flop == F and pr.max_flop_row == mx
 
 
+def _long_b(k, n, seed, long_rows=(3, 7), long_len=70000):
+    """B with short random rows plus rows of >= 65535 entries (the uint16
+    degree escape)."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, 9, size=k)
+    for r in long_rows:
+        lens[r] = long_len
+    rpt = np.zeros(k + 1, np.int64)
+    np.cumsum(lens, out=rpt[1:])
+    col = np.empty(int(rpt[-1]), np.int32)
+    for r in range(k):
+        if lens[r]:
+            col[rpt[r]:rpt[r + 1]] = np.sort(rng.choice(n, int(lens[r]), replace=False))
+    return spnnz.CsrMatrix(k, n, rpt, col)
+
+
+@pytest.mark.parametrize("k", [81792, 81793])  # largest K whose degree table fits shared memory, and one more
+@pytest.mark.parametrize("smem", ["1", "0"])
+def test_flop_degree_table_threshold(oracle, monkeypatch, k, smem):
+    """The shared-memory degree table (persistent 8-group blocks) on both sides
+    of its size limit, with the global-memory kernel forced as the A/B
+    reference, incl. B rows past the uint16 escape and A rows spanning tiles."""
+    monkeypatch.setenv("SPNNZ_FLOP_SMEM", smem)
+    rng = np.random.default_rng(k)
+    m = 4000
+    rows = [sorted(int(c) for c in rng.choice(k, int(rng.integers(0, 60)), replace=False)) for _ in range(m)]
+    rows[5] = list(range(0, k, 7))  # ~11.7 K entries: several tiles
+    rows[6] = [3, 7, 9]  # the escape rows
+    rows[100:400] = [[] for _ in range(300)]
+    a = csr(m, k, rows)
+    b = _long_b(k, 100000, k)
+    P = Predictor(0)
+    P.load(a, b)
+    pr = P.compute_flop()
+    f, F, mx = oracle.compute_flop(a, b)
+    assert (pr.flop_per_row == f).all() and pr.total_flop == F and pr.max_flop_row == mx
+    P.close()
+
+
+@pytest.mark.parametrize("rows_mode", ["1", "0"])
+@pytest.mark.parametrize("smem", ["1", "0"])
+@pytest.mark.parametrize("shape", ["stencil", "random", "long+empty"])
+def test_flop_row_mode(oracle, monkeypatch, rows_mode, smem, shape):
+    """Row-per-thread tiles (banded A) forced on and off, on a stencil (where
+    load() picks them) and on shapes it would not pick: per-row FLOP, F and
+    max identical to the oracle either way."""
+    monkeypatch.setenv("SPNNZ_FLOP_ROWS", rows_mode)
+    monkeypatch.setenv("SPNNZ_FLOP_SMEM", smem)
+    if shape == "stencil":
+        a = gen.stencil27(40, 30, 20)
+        b = a
+    elif shape == "random":
+        a = gen.uniform_len(60000, 50000, 0, 40, 3)
+        b = gen.uniform_len(50000, 30000, 0, 20, 4)
+    else:
+        rows = [list(range(0, 30000, 3)), []] + [list(range(i % 50)) for i in range(20000)]
+        rows += [[] for _ in range(7000)] + [list(range(5000))] + [[i % 29999, 29999] for i in range(5000)]
+        a = csr(len(rows), 30000, rows)
+        b = gen.uniform_len(30000, 8000, 0, 30, 5)
+    P = Predictor(0)
+    P.load(a, None if b is a else b)
+    pr = P.compute_flop()
+    f, F, mx = oracle.compute_flop(a, b)
+    assert (pr.flop_per_row == f).all() and pr.total_flop == F and pr.max_flop_row == mx
+    # the fused predictor's emit path runs inside the same tile code
+    monkeypatch.setenv("SPNNZ_FUSED_PREDICT", "1")
+    rep = P.run_prediction(9, SamplePolicy(0.05, -1))
+    orep, of, oceil, oreal = oracle.run_prediction(a, b, 9, 0.05, -1)
+    assert np.array_equal(rep.predicted_row_nnz_ceil, oceil) and rep.z2_star == orep.z2_star
+    P.close()
+
+
 # -------------------------------------------------------------- sampler
 def test_sampler_matches_reference(P, golden):
     for rec in golden["refkat"]["plans"]:
@@ -388,6 +460,68 @@ def test_exhaustive_plan_is_exact():
         assert (e.eps1, e.eps_f, e.eps2) == (0.0, 0.0, 0.0)
 
 
+def _golden_csr(rec, key, rows, cols):
+    m = rec[key]
+    return spnnz.CsrMatrix(rows, cols, np.array(m["rpt"], np.int64), np.array(m["col"], np.int32))
+
+
+@pytest.mark.parametrize("api", ["python", "capi-device-rows"])
+def test_with_plan_hand_built_profiles(golden, api):
+    """run_prediction_with_plan on a caller's profile (predict.hpp:202-216):
+    zeroed rows count 0, inflated rows change f* / F / the views but not the
+    counts, another total_flop moves Z2*, a capacity violation is the
+    reference's invalid_argument -- against the reference's own outputs
+    (tests/golden/with_plan.json, oracle/_ref)."""
+    import torch
+    P = Predictor(0)
+    for rec in golden["with_plan"]["cases"]:
+        a = _golden_csr(rec, "a", rec["m"], rec["k"])
+        b = a if rec["same"] else _golden_csr(rec, "b", rec["k"], rec["n"])
+        prof = spnnz.FlopProfile(np.array(rec["flop"], np.int64), rec["total"], rec["max"])
+        rows = np.array(rec["rows"], np.int32)
+        plan = SamplePlan(rows, len(rows), rec["p"], 0)
+        if api == "capi-device-rows":
+            plan = SamplePlan(torch.tensor(rows, device="cuda"), len(rows), rec["p"], 0)
+        P.load(a, None if rec["same"] else b)
+        if "error" in rec:
+            with pytest.raises(ValueError, match="exceeds capacity"):
+                P.run_prediction_with_plan(plan, prof)
+            assert rec["error"].startswith("HashAccumulator: tsize")
+            continue
+        rep = P.run_prediction_with_plan(plan, prof)
+        r = rec["report"]
+        assert rep.total_flop == r["total_flop"] == rec["total"], rec["kind"]
+        assert rep.stats.sampled_flop == r["sampled_flop"], rec["kind"]
+        assert rep.stats.sampled_nnz == r["sampled_nnz"], rec["kind"]
+        assert rep.stats.sampled_cr == r["sampled_cr"]
+        assert rep.z1_star == r["z1_star"] and rep.z2_star == r["z2_star"], rec["kind"]
+        assert rep.predicted_cr == r["predicted_cr"]
+        assert np.array_equal(rep.predicted_row_nnz, np.array(rec["real"])), rec["kind"]
+        assert np.array_equal(rep.predicted_row_nnz_ceil, np.array(rec["ceil"], np.int64)), rec["kind"]
+        # the standalone sampled_symbolic on the same profile agrees
+        P.set_profile(prof)
+        s = P.sampled_symbolic(rows)
+        assert s.total_nnz == r["sampled_nnz"]
+    P.close()
+
+
+def test_with_plan_uses_profile_not_a_flop_pass():
+    """The free function hands the caller's profile through: a profile whose
+    total differs from the matrices' moves Z2* exactly as the reference's
+    expression F*z*/f* says (predict.hpp:120-121)."""
+    rng = gen.SplitMix64(91)
+    a = gen.random_pattern(200, 200, 0.05, rng)
+    prof = spnnz.compute_flop(a, a)
+    plan = spnnz.make_sample_plan(a.rows, 5, SamplePolicy(0.1, -1))
+    base = spnnz.run_prediction_with_plan(a, a, prof, plan)
+    prof2 = spnnz.FlopProfile(prof.flop_per_row.copy(), prof.total_flop * 7 + 3, prof.max_flop_row)
+    rep = spnnz.run_prediction_with_plan(a, a, prof2, plan)
+    assert rep.total_flop == prof2.total_flop
+    f, z = rep.stats.sampled_flop, rep.stats.sampled_nnz
+    assert (f, z) == (base.stats.sampled_flop, base.stats.sampled_nnz)
+    assert rep.z2_star == float(prof2.total_flop) * float(z) / float(f)
+
+
 def test_free_function_composition(oracle):
     """collect_sample_stats / estimators over GPU pieces equal run_prediction."""
     rng = gen.SplitMix64(55)
@@ -674,6 +808,19 @@ def test_cpp_dropin_header():
         subprocess.run(["make", "-C", root, "build/test_dropin"], check=True, capture_output=True)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_cpp_dropin_reference_types():
+    """The reference's own spnnz::CsrMatrix / FlopProfile / SamplePlan into
+    spnnz::gpu::*, every output compared with the unmodified reference function
+    (tests/cpp/test_dropin_ref.cpp; built where /root/reference exists)."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "build", "test_dropin_ref")
+    if not os.path.exists(exe):
+        pytest.skip("build/test_dropin_ref not built (needs the reference headers at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "all checks passed" in r.stdout, r.stdout + r.stderr
 
 
 # ------------------------------------------------------------------ fuzzing
