@@ -63,6 +63,14 @@ def workload_name(cfg, info, cap):
         ("uncapped" if cap < 0 else f"cap {cap}") + f", seed {info['seed']}"
 
 
+def config_dict(cfg, info, cap, a):
+    """The `config` object: the workload only, identical in both arms (how each
+    arm executes it is reported under `execution`)."""
+    from paper_2207_13848_b200.spnnz import SamplePolicy, plan_size
+    n, _ = plan_size(a.rows, SamplePolicy(info["fraction"], cap))
+    return {"workload": workload_name(cfg, info, cap), "nnz_A": a.nnz(), "rows": a.rows, "sample_num": n}
+
+
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
     """SM clock and throttle reasons sampled DURING the timed region: an NVML
@@ -245,8 +253,9 @@ def run_reference_arm(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic", "config": {"workload": workload_name(args.config, info, args.cap),
-                                         "parallelism": f"cpu threads={cores}"},
+        "data": "synthetic (seeded generator, BASELINE.json config shapes)",
+        "config": config_dict(args.config, info, args.cap, a),
+        "execution": {"parallelism": f"reference CPU path, {cores} host threads ({cpu_model()})"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": cpu_model(),
                          "sample": "full workload per step: compute_flop + make_sample_plan + "
                                    "sampled_symbolic + collect_sample_stats + predict_reference + "
@@ -273,13 +282,16 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_traffic():
-    """dram bytes per FLOP-pass launch from the committed ncu capture."""
+def load_traffic(cfg):
+    """dram bytes per FLOP-pass launch (dram__bytes_read.sum + write.sum of the
+    pass's kernels) and the L2 hit rate, from the committed ncu captures of
+    this config's workload (profiles/flop_traffic.json, per config)."""
     p = os.path.join(ROOT, "profiles", "flop_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d
+        d = d.get(str(cfg))
+        return (d.get("dram_bytes_per_launch"), d) if d else (None, None)
     except Exception:
         return None, None
 
@@ -308,6 +320,8 @@ def run_ours(args, rank, world, local):
     P.synchronize()  # the upload has landed: every step below runs on resident inputs
     policy = SamplePolicy(info["fraction"], args.cap)
     m_local = P.local_rows
+    flop_smem = os.environ.get("SPNNZ_FLOP_SMEM", "1") != "0" and \
+        (b.rows if b is not a else a.rows) <= 81792
     nnz_local = int(a.rpt[P.row_hi] - a.rpt[P.row_lo])
     stream = torch.cuda.ExternalStream(P.stream_handle())
     dev_ceil = torch.empty(max(m_local, 1), dtype=torch.int64, device="cuda")
@@ -380,9 +394,12 @@ def run_ours(args, rank, world, local):
     peak, peak_kind = load_peaks()
     fbytes = flop_pass_bytes(m_local, nnz_local, (b.rows if b is not a else a.rows))
     achieved = fbytes / (phase["flop"] * 1e-3) / 1e9 if phase["flop"] > 0 else 0.0
-    traffic, tmeta = load_traffic()
-    if args.config != 5:  # the committed ncu capture is of the config-5 workload
-        traffic = None
+    traffic, tmeta = load_traffic(args.config)
+    if world > 1:  # the captures are single-GPU (whole-matrix) launches
+        traffic, tmeta = None, None
+    # the floor the FLOP pass's access pattern sets on this matrix, measured
+    # here: the same A.col loads and degree gathers without the row logic
+    floor_stream_ms, floor_gather_ms = P.probe_flop_floor(10)
     pbytes = 16 * m_local
     # sampled symbolic: B_samp = sum_s 16 + 20 len(A_row) + 4 flop_row,
     # dominated by the B.col reads; its bound is shared-memory atomics and the
@@ -450,17 +467,27 @@ def run_ours(args, rank, world, local):
                     "overhead_fraction": (ms_max * 1e-3) / t_exact if t_exact > 0 else None}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
+        # rank 0 only (the other ranks wait at the barrier below): one full pass
+        # of the same workload on this host's cores after a warm-up pass for
+        # the small configs (the reference protocol is 1 warm-up + mean of N,
+        # bench.hpp:146-157); config 5 is one ~2.5 s pass
         cstep, kind, cores, cleanup = cpu_reference_pipeline(a, b, info, args.cap)
+        reps = 1 if a.nnz() > 100_000_000 else 3
+        if reps > 1:
+            cstep()
         t0 = time.perf_counter()
-        cstep()
-        tc = time.perf_counter() - t0
+        for _ in range(reps):
+            cstep()
+        tc = (time.perf_counter() - t0) / reps
         cleanup()
         cpu = {"value": a.nnz() / tc, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": cpu_model(),
-               "sample": f"one full pass of the workload ({tc:.1f} s): compute_flop + "
+               "sample": f"full passes of the workload (mean of {reps}, {tc:.3f} s each): compute_flop + "
                          "make_sample_plan + sampled_symbolic + collect_sample_stats + predict_reference + "
                          "predict_proposed + predict_row_structure_ceil (the GPU step's outputs)"}
 
+    if dist:
+        dist.barrier()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -468,13 +495,15 @@ def run_ours(args, rank, world, local):
             "ms_per_step_median_rank0": ms_median,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (seeded generator, BASELINE.json config shapes)",
-            "config": {"workload": workload_name(args.config, info, args.cap),
-                       "nnz_A": a.nnz(), "rows": a.rows, "sample_num": rep.plan.sample_num,
-                       "parallelism": f"A row-sharded x{world} (nnz-balanced), B replicated, "
-                                      "1 NCCL all-reduce per step",
-                       "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps"},
+            "config": config_dict(args.config, info, args.cap, a),
+            "execution": {"parallelism": f"A row-sharded x{world} (nnz-balanced), B replicated, "
+                                         "1 NCCL all-reduce per step",
+                          "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps",
+                          "flop_kernel": "k_flop_smem (degree table in shared memory)" if flop_smem
+                          else "k_flop (degree gathers from L2)"},
             "roofline": {"bound": "hbm",
-                         "kernel": "FLOP pass (k_degree with the tile partition + k_flop + k_flop_fixup)",
+                         "kernel": "FLOP pass (k_degree with the tile partition + k_flop or k_flop_smem "
+                                   "+ k_flop_fixup)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          # L2 hit rate of the pass (the degree gathers dominate its
@@ -485,18 +514,16 @@ def run_ours(args, rank, world, local):
                          "algorithmic_bytes": fbytes, "avg_ms": phase["flop"],
                          "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json)",
                          # the FLOP pass gathers one B-row length per A nonzero; random
-                         # 2-4 B gathers are capped by the L2->SM request rate (measured
-                         # 287 G/s chip-wide for LDG, TMA and both together,
-                         # profiles/r01_microbench.md), not by HBM
+                         # 2-4 B gathers are capped by the L2->SM request rate, not by
+                         # HBM.  Measured IN THIS RUN on this matrix (probe_flop_floor):
+                         # the pass's A.col loads alone and with the degree gathers,
+                         # none of the row logic -- the floor its access pattern sets
                          "gathers_per_s": nnz_local / (phase["flop"] * 1e-3) if phase["flop"] else 0.0,
-                         "gather_peak_per_s": 287.6e9,
-                         "gather_frac": (nnz_local / (phase["flop"] * 1e-3) / 287.6e9)
-                         if phase["flop"] else 0.0,
-                         # the same loads with none of the row logic, on this very
-                         # matrix (tools/microbench/flop_ceiling.cu, r01_microbench.md)
-                         "pattern_ceiling_ms": 1.500 if args.config == 5 and world == 1 else None,
-                         "pattern_ceiling_frac": (1.500 / phase["flop"]) if args.config == 5 and world == 1
-                         and phase["flop"] else None},
+                         "pattern_stream_ms": floor_stream_ms,
+                         "pattern_ceiling_ms": floor_gather_ms,
+                         "gather_peak_per_s": nnz_local / (floor_gather_ms * 1e-3) if floor_gather_ms else None,
+                         "pattern_ceiling_frac": (floor_gather_ms / phase["flop"]) if phase["flop"] else None,
+                         "pattern_source": "measured in-run (spnnz_gpu_probe_flop_floor, 10 launches)"},
             # the other HBM-streaming kernel the north star names (fused into
             # the FLOP pass only under SPNNZ_FUSED_PREDICT=1)
             "roofline_predict": ({"fused": "into the FLOP pass (SPNNZ_FUSED_PREDICT=1)"}

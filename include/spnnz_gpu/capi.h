@@ -203,6 +203,11 @@ int spnnz_error_report(double z1_star, double z2_star, int64_t f_star, int64_t e
  * names: flop, sample, symbolic, allreduce, predict. */
 int spnnz_gpu_set_profiling(spnnz_gpu_ctx* ctx, int enabled);
 int spnnz_gpu_last_timings(spnnz_gpu_ctx* ctx, double* ms_out5, int64_t* launches);
+/* The floor the FLOP pass's access pattern sets on the loaded matrices: the
+ * same A.col loads (and, for gather_ms, the same uint16 degree gathers) with
+ * none of the row logic, averaged over reps launches (ms, CUDA events).
+ * bench.py reports the pass against it (roofline.pattern_ceiling_*). */
+int spnnz_gpu_probe_flop_floor(spnnz_gpu_ctx* ctx, int reps, double* stream_ms, double* gather_ms);
 /* The context's CUDA stream (cudaStream_t), for callers that time on it. */
 void* spnnz_gpu_stream(spnnz_gpu_ctx* ctx);
 /* Ordering of DEVICE-residency inputs: every call that reads one first makes

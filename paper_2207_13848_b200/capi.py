@@ -83,6 +83,7 @@ _SIGS = {
     "spnnz_gpu_last_timings": (c_int, [c_void_p, c_void_p, POINTER(c_int64)]),
     "spnnz_gpu_stream": (c_void_p, [c_void_p]),
     "spnnz_gpu_set_input_stream": (c_int, [c_void_p, c_void_p]),
+    "spnnz_gpu_probe_flop_floor": (c_int, [c_void_p, c_int, POINTER(c_double), POINTER(c_double)]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -192,6 +192,7 @@ struct spnnz_gpu_ctx {
 
     // scratch
     DBuf<int32_t> tile_x;
+    DBuf<unsigned long long> flop_sched;  // k_flop_smem tile tickets (zeroed once, kept zero)
     DBuf<uint16_t> deg;  // uint16 row lengths of B (rebuilt every FLOP pass)
     DBuf<long long> tile_carry, tile_total, tile_max;
     DBuf<long long> totals;
@@ -495,11 +496,17 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
     RC(c->tile_max.ensure(tiles + 1));
     RC(c->deg.ensure(int64_t(c->b_rows) + 8));  // + padding: shared-memory copies read 16-byte words
     FlopScratch s{c->tile_x.p, c->tile_carry.p, c->tile_total.p, c->tile_max.p};
+    if (!c->flop_sched.p) {
+        RC(c->flop_sched.ensure(2));
+        CU(cudaMemsetAsync(c->flop_sched.p, 0, 2 * sizeof(unsigned long long), stream));
+    }
     FlopMode mode;
+    mode.sched = c->flop_sched.p;
     mode.b_rows = c->b_rows;
     mode.rows_mode = c->rows_mode;
     mode.num_sms = c->num_sms;
     if (const char* e = getenv("SPNNZ_FLOP_SMEM")) mode.no_smem = atoi(e) == 0;  // A/B knob
+    if (const char* e = getenv("SPNNZ_FLOP_PREFETCH")) mode.prefetch_ahead = atoi(e);  // A/B knob
     if (c->pending_upload && stream == c->stream) {
         // B.col still landing: degrees and the partition need only B.rpt; the
         // tiles of each chunk run on fstream as soon as the chunk is in; the
@@ -1436,6 +1443,27 @@ int spnnz_error_report(double z1, double z2, int64_t f_star, int64_t exact_nnz, 
 int spnnz_gpu_set_profiling(spnnz_gpu_ctx* c, int enabled) {
     if (!c) return set_err(SPNNZ_EINVAL, "null context");
     c->profiling = enabled != 0;
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_probe_flop_floor(spnnz_gpu_ctx* c, int reps, double* stream_ms, double* gather_ms) {
+    RC(check_ctx(c));
+    if (reps < 1) return set_err(SPNNZ_EINVAL, "probe: reps must be >= 1");
+    RC(c->deg.ensure(int64_t(c->b_rows) + 8));
+    DBuf<long long> out;
+    RC(out.ensure(std::max<int64_t>(c->a.nnz / 16, 1)));
+    CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, c->stream));
+    double* res[2] = {stream_ms, gather_ms};
+    for (int g = 0; g < 2; ++g) {
+        CU(launch_pattern(c->a, c->deg.p, g == 1, out.p, c->stream));  // warm-up
+        CU(cudaEventRecord(c->ev[0], c->stream));
+        for (int i = 0; i < reps; ++i) CU(launch_pattern(c->a, c->deg.p, g == 1, out.p, c->stream));
+        CU(cudaEventRecord(c->ev[1], c->stream));
+        CU(cudaEventSynchronize(c->ev[1]));
+        float ms = 0;
+        CU(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+        if (res[g]) *res[g] = ms / reps;
+    }
     return SPNNZ_OK;
 }
 

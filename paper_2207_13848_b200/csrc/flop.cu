@@ -308,7 +308,7 @@ struct TileArgs {
     long long* __restrict__ tile_lead;
     long long* __restrict__ tile_total;
     long long* __restrict__ tile_max;
-    int rows_mode;  // banded A (host check at load): short-row tiles go row per thread
+    int prefetch_ahead;  // k_flop: L2-prefetch the columns of tile t + this (0: off)
 };
 
 // The exact degree of B row c given its uint16 entry (0xFFFF: look it up).
@@ -341,24 +341,47 @@ __device__ __forceinline__ void tile_totals(TileSmem<BLOCK, V>& sm, const TileAr
     }
 }
 
+// L2 prefetch of a later tile's columns (one bulk-prefetch instruction: the
+// tile is 8 KB, 16-byte aligned except at a shard's ends), so its col loads
+// find them in L2 instead of waiting on HBM.
+__device__ __forceinline__ void prefetch_tile(const TileArgs& g, int64_t t) {
+    const int64_t ts = tile_start(g.base, g.nnz, t), te = tile_start(g.base, g.nnz, t + 1);
+    const uintptr_t p0 = (reinterpret_cast<uintptr_t>(g.acol + ts) + 15) & ~uintptr_t(15);
+    const uintptr_t p1 = reinterpret_cast<uintptr_t>(g.acol + te) & ~uintptr_t(15);
+    if (p1 > p0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0), "r"(static_cast<unsigned>(p1 - p0))
+                     : "memory");
+}
+
 // Row mode, for banded A (27-point stencil: consecutive rows reach
-// consecutive columns): the tile's columns are staged in shared memory and
-// each thread walks whole rows, so a warp's k-th gathers hit ~32 consecutive
-// degrees (one or two L1 lines) instead of ~9 clusters per instruction.
+// consecutive columns): the tile's columns are staged in shared memory
+// (coalesced, conflict-free: thread tid loads entries tid + k BLOCK) and each
+// thread walks whole rows, so a warp's k-th gathers hit ~32 consecutive
+// degrees (one or two L1 lines) instead of ~9 clusters per instruction.  A
+// row's gathers are issued 16 at a time (a stencil row is 27 entries: two
+// rounds of loads in flight).
 template <int BLOCK, int V, bool PRED, class Deg, class Bar>
 __device__ __forceinline__ void flop_tile_rows(TileSmem<BLOCK, V>& sm, const TileArgs& g, int64_t t, int tid,
-                                               int64_t ts, int n, int32_t r0, int32_t r1, const int32_t (&c)[V],
-                                               Deg deg, Bar bar, const Emit& emit) {
-    const int i0 = tid * V;
+                                               int64_t ts, int n, int32_t r0, int32_t r1, Deg deg, Bar bar,
+                                               const Emit& emit) {
+    constexpr int W = 16;
+    const uint64_t first = policy_evict_first();
+    int64_t ra = 0, rb = 0;
+    if (r0 + tid < r1) {
+        ra = __ldg(&g.arpt[r0 + tid]);
+        rb = __ldg(&g.arpt[r0 + tid + 1]);
+    }
+    const int64_t a0 = __ldg(&g.arpt[r0]);
 #pragma unroll
-    for (int k = 0; k < V; ++k)
-        if (i0 + k < n) sm.rowat[i0 + k] = c[k];
+    for (int k = 0; k < V; ++k) {
+        const int i = tid + k * BLOCK;
+        if (i < n) sm.rowat[i] = ld_stream_i32(g.acol + ts + i, first);
+    }
     bar();
     const int64_t te = ts + n;
     long long tsum = 0, tmax = 0;
     // the leading slice (a row owned by an earlier tile): warp 0
     if (tid < 32) {
-        const int64_t a0 = __ldg(&g.arpt[r0]);
         const int lead_n = static_cast<int>((a0 < te ? a0 : te) - ts);
         long long s = 0;
         for (int i = tid; i < lead_n; i += 32) s += exact_deg(deg(sm.rowat[i]), sm.rowat[i], g.brpt);
@@ -369,23 +392,24 @@ __device__ __forceinline__ void flop_tile_rows(TileSmem<BLOCK, V>& sm, const Til
         }
     }
     for (int32_t r = r0 + tid; r < r1; r += BLOCK) {
-        const int64_t a = __ldg(&g.arpt[r]), b = __ldg(&g.arpt[r + 1]);
-        const int e0 = static_cast<int>(a - ts), e1 = static_cast<int>((b < te ? b : te) - ts);
-        long long s = 0;
-        int e = e0;
-        for (; e + 4 <= e1; e += 4) {  // four gathers in flight
-            int32_t d[4], cc[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) cc[k] = sm.rowat[e + k];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) d[k] = deg(cc[k]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) s += exact_deg(d[k], cc[k], g.brpt);
+        if (r != r0 + tid) {
+            ra = __ldg(&g.arpt[r]);
+            rb = __ldg(&g.arpt[r + 1]);
         }
-        for (; e < e1; ++e) s += exact_deg(deg(sm.rowat[e]), sm.rowat[e], g.brpt);
+        const int e0 = static_cast<int>(ra - ts), e1 = static_cast<int>((rb < te ? rb : te) - ts);
+        long long s = 0;
+        for (int e = e0; e < e1; e += W) {
+            int32_t cc[W], d[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) cc[k] = e + k < e1 ? sm.rowat[e + k] : -1;
+#pragma unroll
+            for (int k = 0; k < W; ++k) d[k] = cc[k] >= 0 ? deg(cc[k]) : 0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) s += cc[k] >= 0 ? exact_deg(d[k], cc[k], g.brpt) : 0;
+        }
         tsum += s;
         g.flop[r] = s;  // partial when the row runs past the tile: the fixup adds the rest
-        if (b <= te) {
+        if (rb <= te) {
             tmax = s > tmax ? s : tmax;
             if (PRED) emit(r, s);
         }
@@ -393,8 +417,9 @@ __device__ __forceinline__ void flop_tile_rows(TileSmem<BLOCK, V>& sm, const Til
     tile_totals<BLOCK, V>(sm, g, t, tid, tsum, tmax, bar);
 }
 
-// One tile of kFlopTile entries by BLOCK threads (tid in [0, BLOCK)).
-template <int BLOCK, int V, bool PRED, class Deg, class Bar>
+// One tile of kFlopTile entries by BLOCK threads (tid in [0, BLOCK)); ROWS:
+// the row-mode instantiation (banded A, chosen on the host at load).
+template <int BLOCK, int V, bool PRED, bool ROWS, class Deg, class Bar>
 __device__ __forceinline__ void flop_tile(TileSmem<BLOCK, V>& sm, const TileArgs& g, int64_t t, int tid,
                                           Deg deg, Bar bar, const Emit& emit) {
     constexpr int TILE = BLOCK * V, NW = BLOCK / 32;
@@ -403,8 +428,14 @@ __device__ __forceinline__ void flop_tile(TileSmem<BLOCK, V>& sm, const TileArgs
     const int64_t ts = tile_start(g.base, g.nnz, t), te = tile_start(g.base, g.nnz, t + 1);
     const int n = static_cast<int>(te - ts);
     const int lane = tid & 31, warp = tid >> 5;
+    if (ROWS) {  // row mode: owned rows averaging <= 48 entries in a banded matrix
+        const int32_t q0 = g.tile_row[t], q1 = g.tile_row[t + 1];
+        if (q1 > q0 && n <= 48 * (q1 - q0)) {
+            flop_tile_rows<BLOCK, V, PRED>(sm, g, t, tid, ts, n, q0, q1, deg, bar, emit);
+            return;
+        }
+    }
     for (int k = tid; k < TILE / 32; k += BLOCK) sm.start[k] = 0u;
-    const int32_t r0 = g.tile_row[t], r1 = g.tile_row[t + 1];
 
     // 1. this thread's V consecutive entries: columns (16-byte evict_first
     //    loads when the tile is whole)
@@ -424,11 +455,6 @@ __device__ __forceinline__ void flop_tile(TileSmem<BLOCK, V>& sm, const TileArgs
 #pragma unroll
         for (int k = 0; k < V; ++k) c[k] = i0 + k < n ? ld_stream_i32(g.acol + ts + i0 + k, first) : -1;
     }
-    // row mode: owned rows averaging <= 48 entries in a banded matrix
-    if (g.rows_mode && r1 > r0 && n <= 48 * (r1 - r0)) {
-        flop_tile_rows<BLOCK, V, PRED>(sm, g, t, tid, ts, n, r0, r1, c, deg, bar, emit);
-        return;
-    }
     //    ... then all V degree gathers in flight
     int32_t d[V];
 #pragma unroll
@@ -442,10 +468,11 @@ __device__ __forceinline__ void flop_tile(TileSmem<BLOCK, V>& sm, const TileArgs
     bar();  // the start bitmap is clear
 
     // 2. owned rows [r0, r1): mark where the non-empty ones start; empty ones are 0
+    const int32_t r0 = g.tile_row[t], r1 = g.tile_row[t + 1];
     for (int32_t r = r0 + tid; r < r1; r += BLOCK) {
-        const int64_t a = __ldg(&g.arpt[r]), b = __ldg(&g.arpt[r + 1]);
-        if (b > a) {
-            const int pos = static_cast<int>(a - ts);
+        const int64_t ra = __ldg(&g.arpt[r]), rb = __ldg(&g.arpt[r + 1]);
+        if (rb > ra) {
+            const int pos = static_cast<int>(ra - ts);
             atomicOr(&sm.start[pos >> 5], 1u << (pos & 31));
             sm.rowat[pos] = r;
         } else {
@@ -525,14 +552,17 @@ __device__ __forceinline__ void flop_tile(TileSmem<BLOCK, V>& sm, const TileArgs
 }
 
 // One block per tile, degrees gathered from global memory (L2).
-template <int BLOCK, int V, bool PRED>
-__global__ void __launch_bounds__(BLOCK, (SPNNZ_FLOP_MINB / BLOCK < 32 ? SPNNZ_FLOP_MINB / BLOCK : 32))
+// (row mode holds a row's 16 gathers in flight: 64 registers, 8 blocks per SM)
+template <int BLOCK, int V, bool PRED, bool ROWS>
+__global__ void __launch_bounds__(BLOCK, ROWS ? 8 : (SPNNZ_FLOP_MINB / BLOCK < 32 ? SPNNZ_FLOP_MINB / BLOCK : 32))
 k_flop(TileArgs g, const uint16_t* __restrict__ bdeg, PredOut pred, int64_t t0) {
     __shared__ TileSmem<BLOCK, V> sm;
     Emit emit{};
     if (PRED) emit = make_emit(pred);
-    flop_tile<BLOCK, V, PRED>(sm, g, t0 + blockIdx.x, threadIdx.x, GlobalDeg{bdeg, policy_evict_last()},
-                              BlockBar{}, emit);
+    if (g.prefetch_ahead && threadIdx.x == 0 && blockIdx.x + g.prefetch_ahead < gridDim.x)
+        prefetch_tile(g, t0 + blockIdx.x + g.prefetch_ahead);
+    flop_tile<BLOCK, V, PRED, ROWS>(sm, g, t0 + blockIdx.x, threadIdx.x, GlobalDeg{bdeg, policy_evict_last()},
+                                    BlockBar{}, emit);
 }
 
 // Persistent blocks of G tile groups (G x 128 threads, one block per SM) with
@@ -540,13 +570,23 @@ k_flop(TileArgs g, const uint16_t* __restrict__ bdeg, PredOut pred, int64_t t0) 
 // gather is a shared-memory load (config 4: K = 65536, 128 KB).  Each group
 // runs the tile code on its own tiles with its own named barrier.
 constexpr int kSmemGroups = 8;
-template <int V, bool PRED>
+template <int V, bool PRED, bool ROWS>
 __global__ void __launch_bounds__(kFlopBlock * kSmemGroups, 1)
 k_flop_smem(TileArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut pred, int64_t t0,
-            int64_t t1) {
+            int64_t t1, unsigned long long* __restrict__ sched) {
     extern __shared__ __align__(16) unsigned char s_raw[];
+    __shared__ int64_t s_next[kSmemGroups][2];
     auto* tiles = reinterpret_cast<TileSmem<kFlopBlock, V>*>(s_raw);
     uint16_t* s_deg = reinterpret_cast<uint16_t*>(s_raw + sizeof(TileSmem<kFlopBlock, V>) * kSmemGroups);
+    const int grp = threadIdx.x / kFlopBlock, tid = threadIdx.x % kFlopBlock;
+    // tiles are handed out by a ticket counter (sched[0]): a block that starts
+    // late (other kernels still hold its SM) just takes fewer; the group that
+    // draws the last out-of-range ticket (sched[1] counts them) resets both
+    if (tid == 0) {
+        const int64_t t = t0 + static_cast<int64_t>(atomicAdd(&sched[0], 1ULL));
+        s_next[grp][0] = t;
+        if (t < t1) prefetch_tile(g, t);
+    }
     // the degree table, 16 bytes per thread per step (k_rows padded to 8)
     const int words = (k_rows + 7) >> 3;
     for (int i = threadIdx.x; i < words; i += blockDim.x)
@@ -554,10 +594,24 @@ k_flop_smem(TileArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredO
     __syncthreads();
     Emit emit{};
     if (PRED) emit = make_emit(pred);
-    const int grp = threadIdx.x / kFlopBlock, tid = threadIdx.x % kFlopBlock;
     const GroupBar<kFlopBlock> bar{1 + grp};
-    for (int64_t t = t0 + int64_t(blockIdx.x) * kSmemGroups + grp; t < t1; t += int64_t(gridDim.x) * kSmemGroups)
-        flop_tile<kFlopBlock, V, PRED>(tiles[grp], g, t, tid, SharedDeg{s_deg}, bar, emit);
+    int64_t t = s_next[grp][0];
+    for (int it = 0; t < t1; ++it) {
+        if (tid == 0) {  // the group's next tile, drawn now so its columns are prefetched
+            const int64_t nx = t0 + static_cast<int64_t>(atomicAdd(&sched[0], 1ULL));
+            s_next[grp][(it + 1) & 1] = nx;
+            if (nx < t1) prefetch_tile(g, nx);
+        }
+        flop_tile<kFlopBlock, V, PRED, ROWS>(tiles[grp], g, t, tid, SharedDeg{s_deg}, bar, emit);
+        t = s_next[grp][(it + 1) & 1];  // written before the tile's barriers
+    }
+    if (tid == 0) {
+        const unsigned long long groups = static_cast<unsigned long long>(gridDim.x) * kSmemGroups;
+        if (atomicAdd(&sched[1], 1ULL) == groups - 1) {
+            sched[0] = 0;
+            sched[1] = 0;
+        }
+    }
 }
 
 // Adds each tile's leading slice to the row it continues (one thread per
@@ -793,7 +847,53 @@ __global__ void k_locality(const int64_t* __restrict__ rpt, const int32_t* __res
     }
 }
 
+// Instrumentation: the FLOP pass's loads with none of its row logic (the
+// floor its access pattern sets on this matrix): 16 consecutive A.col entries
+// per thread (the k_flop loads) and, with GATHER, their 16 degree gathers;
+// one int64 written per thread so nothing is dead code.
+template <bool GATHER>
+__global__ void __launch_bounds__(128, 10) k_pattern(const int32_t* __restrict__ col, int64_t base, int64_t nnz,
+                                                   const uint16_t* __restrict__ deg, long long* __restrict__ out) {
+    const uint64_t first = policy_evict_first(), last = policy_evict_last();
+    const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int64_t e0 = ((base + 3) & ~int64_t(3)) + t * 16;
+    if (e0 + 16 > base + nnz) return;
+    const int4* src = reinterpret_cast<const int4*>(col + e0);
+    int32_t c[16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int4 x = load_cols(src + k, first);
+        c[4 * k] = x.x;
+        c[4 * k + 1] = x.y;
+        c[4 * k + 2] = x.z;
+        c[4 * k + 3] = x.w;
+    }
+    long long s = 0;
+    if (GATHER) {
+        int32_t d[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) d[k] = gather_deg(deg + c[k], last);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) s += d[k];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) s += c[k];
+    }
+    out[t] = s;
+}
+
 }  // namespace
+
+cudaError_t launch_pattern(const DevCsr& a, const uint16_t* deg, bool gather, long long* out, cudaStream_t stream) {
+    const int64_t threads = a.nnz / 16;
+    if (threads < 1) return cudaSuccess;
+    const unsigned grid = static_cast<unsigned>((threads + 127) / 128);
+    if (gather)
+        k_pattern<true><<<grid, 128, 0, stream>>>(a.col, a.base, a.nnz, deg, out);
+    else
+        k_pattern<false><<<grid, 128, 0, stream>>>(a.col, a.base, a.nnz, deg, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_locality(const int64_t* rpt, const int32_t* col, int32_t lo, int32_t hi, int n, int* out3,
                             cudaStream_t stream) {
@@ -940,11 +1040,11 @@ static TileArgs tile_args(const DevCsr& a, const int64_t* brpt, const FlopScratc
     g.tile_lead = s.tile_carry;
     g.tile_total = s.tile_total;
     g.tile_max = s.tile_max;
-    g.rows_mode = mode.rows_mode ? 1 : 0;
+    g.prefetch_ahead = mode.prefetch_ahead;
     return g;
 }
 
-template <bool PRED>
+template <bool PRED, bool ROWS>
 static cudaError_t launch_tiles(const TileArgs& g, const uint16_t* bdeg, int64_t t_begin, int64_t t_end,
                                 cudaStream_t stream, const PredOut& pred, const FlopMode& mode) {
     if (flop_smem_fits(mode.b_rows) && !mode.no_smem) {
@@ -953,16 +1053,16 @@ static cudaError_t launch_tiles(const TileArgs& g, const uint16_t* bdeg, int64_t
         int dev = 0;
         cudaGetDevice(&dev);
         if (!(attr_done.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
-            cudaFuncSetAttribute(k_flop_smem<kFlopIpt, PRED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(k_flop_smem<kFlopIpt, PRED, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  227 * 1024);
             attr_done.fetch_or(1ull << (dev & 63), std::memory_order_release);
         }
         int64_t grid = (t_end - t_begin + kSmemGroups - 1) / kSmemGroups;
         if (grid > mode.num_sms) grid = mode.num_sms;
-        k_flop_smem<kFlopIpt, PRED><<<static_cast<unsigned>(grid), kFlopBlock * kSmemGroups, smem, stream>>>(
-            g, bdeg, mode.b_rows, pred, t_begin, t_end);
+        k_flop_smem<kFlopIpt, PRED, ROWS><<<static_cast<unsigned>(grid), kFlopBlock * kSmemGroups, smem, stream>>>(
+            g, bdeg, mode.b_rows, pred, t_begin, t_end, mode.sched);
     } else {
-        k_flop<kFlopBlock, kFlopIpt, PRED><<<static_cast<unsigned>(t_end - t_begin), kFlopBlock, 0, stream>>>(
+        k_flop<kFlopBlock, kFlopIpt, PRED, ROWS><<<static_cast<unsigned>(t_end - t_begin), kFlopBlock, 0, stream>>>(
             g, bdeg, pred, t_begin);
     }
     return cudaGetLastError();
@@ -973,8 +1073,11 @@ cudaError_t launch_flop_tiles(const DevCsr& a, const uint16_t* bdeg, const int64
                               cudaStream_t stream, const PredOut& pred, const FlopMode& mode) {
     if (t_end <= t_begin) return cudaSuccess;
     const TileArgs g = tile_args(a, brpt, s, flop, mode);
-    return pred.on() ? launch_tiles<true>(g, bdeg, t_begin, t_end, stream, pred, mode)
-                     : launch_tiles<false>(g, bdeg, t_begin, t_end, stream, pred, mode);
+    if (mode.rows_mode)
+        return pred.on() ? launch_tiles<true, true>(g, bdeg, t_begin, t_end, stream, pred, mode)
+                         : launch_tiles<false, true>(g, bdeg, t_begin, t_end, stream, pred, mode);
+    return pred.on() ? launch_tiles<true, false>(g, bdeg, t_begin, t_end, stream, pred, mode)
+                     : launch_tiles<false, false>(g, bdeg, t_begin, t_end, stream, pred, mode);
 }
 
 cudaError_t launch_flop_fixup(const DevCsr& a, const FlopScratch& s, int64_t* flop, long long* totals,

@@ -87,6 +87,8 @@ struct FlopMode {
     int32_t b_rows = 0;
     bool rows_mode = false;
     bool no_smem = false;  // A/B knob: keep the degree table in global memory
+    int prefetch_ahead = 0;  // k_flop: L2-prefetch the columns this many tiles ahead (0: off)
+    unsigned long long* sched = nullptr;  // k_flop_smem's tile tickets: 2 zeroed words, left zeroed
     int num_sms = 148;
 };
 bool flop_smem_fits(int32_t k_rows);
@@ -95,6 +97,9 @@ bool flop_smem_fits(int32_t k_rows);
 cudaError_t launch_locality(const int64_t* rpt, const int32_t* col, int32_t lo, int32_t hi, int n, int* out3,
                             cudaStream_t stream);
 constexpr int kLocalitySamples = 4096;
+// Instrumentation: the FLOP pass's A.col stream (and, with gather, its degree
+// gathers) without the row logic; out needs nnz / 16 entries.
+cudaError_t launch_pattern(const DevCsr& a, const uint16_t* deg, bool gather, long long* out, cudaStream_t stream);
 // rows_mode when most sampled consecutive rows advance like a stencil's
 inline bool banded_rows(int pairs, int advancing, int short_rows) {
     return pairs >= 64 && advancing * 4 >= pairs * 3 && short_rows * 20 >= pairs * 19;

@@ -347,6 +347,13 @@ class Predictor:
         check(lib().spnnz_gpu_last_timings(self._ctx, ms, ctypes.byref(n)))
         return dict(zip(("flop", "sample", "symbolic", "allreduce", "predict"), list(ms))), n.value
 
+    def probe_flop_floor(self, reps: int = 10):
+        """(stream_ms, gather_ms): the FLOP pass's A.col stream alone, and with
+        its degree gathers, without the row logic (instrumentation)."""
+        a, b = ctypes.c_double(), ctypes.c_double()
+        check(lib().spnnz_gpu_probe_flop_floor(self._ctx, reps, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
     def synchronize(self):
         check(lib().spnnz_gpu_synchronize(self._ctx))
 
