@@ -321,7 +321,7 @@ def run_ours(args, rank, world, local):
     policy = SamplePolicy(info["fraction"], args.cap)
     m_local = P.local_rows
     flop_smem = os.environ.get("SPNNZ_FLOP_SMEM", "1") != "0" and \
-        (b.rows if b is not a else a.rows) <= 81792
+        (b.rows if b is not a else a.rows) <= 81280  # flop.cu flop_smem_fits
     nnz_local = int(a.rpt[P.row_hi] - a.rpt[P.row_lo])
     stream = torch.cuda.ExternalStream(P.stream_handle())
     dev_ceil = torch.empty(max(m_local, 1), dtype=torch.int64, device="cuda")
@@ -350,6 +350,8 @@ def run_ours(args, rank, world, local):
     input_bytes = a.rpt.nbytes + a.col.nbytes + (0 if b is a else b.rpt.nbytes + b.col.nbytes)
     flush = None if input_bytes > 2 * l2_bytes else torch.empty(256 << 20, dtype=torch.uint8,
                                                                  device="cuda")
+    # per-phase device times (CUDA events recorded inside the call, also in
+    # its replayed CUDA graph) -- on for the timed steps
     P.set_profiling(True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]

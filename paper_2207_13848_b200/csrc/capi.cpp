@@ -188,6 +188,49 @@ struct spnnz_gpu_ctx {
     // uses its FlopProfile argument (tsize, f*, F, the per-row views)
     bool profile_own = false;
     DBuf<int64_t> flop_true;  // true FLOP of every local row under a caller profile (exact pass)
+    uint64_t epoch = 0;          // bumped by every load (matrices changed)
+    uint64_t profile_gen = 0;    // bumped whenever the resident profile changes
+
+    // Heavy-row sizes (count, entries, products, boundary cells) a sampled
+    // pass needs on the host to size its buffers.  Known in advance -- no
+    // mid-call wait for the binning -- when no row can be heavy (the resident
+    // own profile's max <= kBin5Max) or the same draw ran before on the same
+    // matrices (cached below); checked against the device's counts after the
+    // call, rerun eagerly on a mismatch.
+    struct HeavySizes {
+        int64_t count = 0, ents = 0, products = 0, cells = 0;
+        bool operator==(const HeavySizes& o) const {
+            return count == o.count && ents == o.ents && products == o.products && cells == o.cells;
+        }
+    };
+    bool hc_valid = false;
+    uint64_t hc_epoch = 0, hc_seed = 0;
+    int64_t hc_n = 0;
+    HeavySizes hc;
+    HeavySizes observed;  // filled by run_symbolic from the device counts (valid after the call's sync)
+    bool observed_set = false;
+
+    // CUDA graph of a whole sync-free predictor call, replayed while its key
+    // (matrices, profile, draw, outputs) is unchanged
+    struct GraphKey {
+        int kind = -1;  // 0 run_prediction, 1 on the resident profile
+        uint64_t epoch = 0, profile_gen = 0, seed = 0;
+        int64_t n = 0;
+        const void *rows = nullptr, *ceil = nullptr, *real = nullptr;
+        bool fused = false, profiling = false;
+        bool operator==(const GraphKey& o) const {
+            return kind == o.kind && epoch == o.epoch && profile_gen == o.profile_gen && seed == o.seed &&
+                   n == o.n && rows == o.rows && ceil == o.ceil && real == o.real && fused == o.fused &&
+                   profiling == o.profiling;
+        }
+    };
+    cudaGraphExec_t gexec = nullptr;
+    GraphKey gkey;
+    GraphKey last_eager;  // a key is captured on its second use (buffers sized by the first)
+    int64_t g_launches = 0;
+    HeavySizes g_known;
+    long long* h_init = nullptr;  // pinned: initial totals of a profile-mode call (read by its graph)
+    bool capturing = false;
     int64_t profile_total = 0, profile_max = 0;
 
     // scratch
@@ -385,7 +428,7 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
                  int slot, bool sampled_flop, int64_t* launches, const int64_t* item_flop = nullptr,
                  const DevCsr* a_view = nullptr, const int64_t* window = nullptr,
                  cudaStream_t bin_stream = nullptr, const int64_t* tsize = nullptr,
-                 long long tsize_cap = 0) {
+                 long long tsize_cap = 0, const spnnz_gpu_ctx::HeavySizes* known = nullptr) {
     const bool early = bin_stream != nullptr;
     cudaStream_t bs = early ? bin_stream : c->stream;
     SymScratch s;
@@ -425,7 +468,11 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     CU(launch_sym_tiers(g, s, c->num_sms, c->side));
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaEventRecord(c->join[i], c->side[i]));
     *launches += 6;
-    if (early) {
+    c->observed_set = true;  // the counts land in h_counts / h_meta by the call's end
+    if (known && !tsize) {
+        // sizes known in advance: no wait for the binning
+        if (early) CU(cudaStreamWaitEvent(c->stream, c->fork, 0));  // heavy batches: after the bin
+    } else if (early) {
         CU(cudaEventSynchronize(c->ev_bin));             // bin + the two small copies only
         CU(cudaStreamWaitEvent(c->stream, c->fork, 0));  // heavy batches: after the bin
     } else {
@@ -436,7 +483,8 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
         return set_err(SPNNZ_EINVAL, "HashAccumulator: tsize %lld exceeds capacity %lld",
                        static_cast<long long>(c->h_meta[kMetaCapacity]), tsize_cap);
     }
-    const int64_t heavy = c->h_counts[kHeavyBin];
+    const bool iv_path = interval_path(c);
+    const int64_t heavy = known && !tsize ? known->count : c->h_counts[kHeavyBin];
     if (heavy > 0) {
         // One batch when the heavy rows fit the batch budgets (always for
         // sampled passes); exact passes over every row split the heavy list
@@ -446,11 +494,12 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
         if (const char* env = getenv("SPNNZ_HEAVY_BATCH_PRODUCTS"))  // test knob
             if (atoll(env) > 0) kBudget = atoll(env);
         const int64_t kCellBudget = kBudget;
-        const bool iv = interval_path(c);
+        const bool iv = iv_path;
         struct Batch {
             int64_t first, count, ents, products, cells;
         };
         std::vector<Batch> batches{{0, heavy, c->h_meta[1], c->h_meta[2], iv ? c->h_meta[5] : 0}};
+        if (known && !tsize) batches[0] = Batch{0, heavy, known->ents, known->products, known->cells};
         if (batches[0].products > kBudget || batches[0].cells > kCellBudget) {
             RC(c->heavy_flops.ensure(3 * heavy));
             CU(launch_heavy_flops(g, s, heavy, c->heavy_flops.p, c->stream));
@@ -506,6 +555,8 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
     mode.rows_mode = c->rows_mode;
     mode.num_sms = c->num_sms;
     if (const char* e = getenv("SPNNZ_FLOP_SMEM")) mode.no_smem = atoi(e) == 0;  // A/B knob
+    // row mode: L2-prefetch the columns one wave (8 blocks x SMs) ahead
+    mode.prefetch_ahead = c->rows_mode ? 8 * c->num_sms : 0;
     if (const char* e = getenv("SPNNZ_FLOP_PREFETCH")) mode.prefetch_ahead = atoi(e);  // A/B knob
     if (c->pending_upload && stream == c->stream) {
         // B.col still landing: degrees and the partition need only B.rpt; the
@@ -535,6 +586,19 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
         RC(settle_upload(c));
         CU(launch_flop_fixup(a, s, out->p, c->totals.p, stream, pred));
         *launches += a.rows ? nk + 1 + c->n_chunks : 0;
+        return SPNNZ_OK;
+    }
+    // row blocks (one warp per 32 rows, no partition / fixup) when B is small
+    // enough for their shared degree table (config 4: 75.6 vs 78.8 us for the
+    // tile groups; with the degree array in L2 the tiles win: config 3 140 vs
+    // 150 us)
+    bool rb = !mode.no_smem && flop_rb_smem_fits(c->b_rows);
+    if (const char* e = getenv("SPNNZ_FLOP_RB")) rb = atoi(e) > 0;  // A/B knob
+    if (rb) {
+        int64_t nk = 0;
+        CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, stream, nullptr, nullptr, &nk));
+        CU(launch_flop_rows(a, c->deg.p, c->b_rpt.p, out->p, c->totals.p, stream, pred, mode));
+        *launches += a.rows ? nk + 1 : 0;
         return SPNNZ_OK;
     }
     int64_t nk = 0;
@@ -592,7 +656,10 @@ void fill_report(spnnz_report* r, const long long* t, int64_t n, double p, uint6
 }
 
 void ev_record(spnnz_gpu_ctx* c, int i) {
-    if (c->profiling) cudaEventRecord(c->ev[i], c->stream);
+    // (inside a graph capture the timing events become external event-record
+    // nodes, so a replayed graph still reports its phases)
+    if (c->profiling)
+        cudaEventRecordWithFlags(c->ev[i], c->stream, c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
 }
 
 // last_ms: [0] FLOP pass (fused: + predict) [1] sampler (+ sampled-row FLOP)
@@ -679,7 +746,7 @@ int sample_share(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool need_f
 // per-row division and scattered 8-byte stores land in the gather-bound FLOP
 // kernel: 2.12 ms vs 1.85 + 0.07 ms), so it is not the default.
 int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint64_t seed,
-             int64_t* d_ceil, double* d_real) {
+             int64_t* d_ceil, double* d_real, const spnnz_gpu_ctx::HeavySizes* known = nullptr) {
     int64_t launches = 0;
     const char* fenv = getenv("SPNNZ_FUSED_PREDICT");
     c->fused = fenv && atoi(fenv) > 0;
@@ -694,11 +761,13 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
         const bool beside = !c->pending_upload;
         cudaStream_t ss = beside ? c->side[0] : c->stream;
         if (beside) {
+            // the FLOP pass is queued first (the GPU starts it while the host
+            // queues the side-stream work), the side stream forks before it
             CU(cudaEventRecord(c->fork, c->stream));
             CU(cudaStreamWaitEvent(ss, c->fork, 0));
-        } else {
-            RC(flop_pass(c, &launches));
         }
+        RC(flop_pass(c, &launches));
+        if (beside) CU(cudaEventRecord(c->ev_flop, c->stream));
         if (draw) {
             CU(launch_sample(seed, c->a_rows, n, c->samples.p, ss));
             ++launches;
@@ -706,14 +775,11 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
         // beside the FLOP pass the sampled rows' FLOP is derived directly, so
         // the binning need not wait for the pass either (early run_symbolic)
         RC(sample_share(c, d_rows, n, beside, &sh, &launches, ss));
-        if (beside) {
-            RC(flop_pass(c, &launches));
-            CU(cudaEventRecord(c->ev_flop, c->stream));
-        }
         ev_record(c, 1);
         ev_record(c, 2);
         RC(run_symbolic(c, sh.rows, sh.n, nullptr, kZStar, true, &launches, sh.item_flop,
-                        sh.use_full ? &sh.full : nullptr, sh.window, beside ? ss : nullptr));
+                        sh.use_full ? &sh.full : nullptr, sh.window, beside ? ss : nullptr, nullptr, 0,
+                        known));
         ev_record(c, 3);
         RC(allreduce_totals(c));
         ev_record(c, 4);
@@ -734,7 +800,7 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
         RC(sample_share(c, d_rows, n, true, &sh, &launches));
         ev_record(c, 1);
         RC(run_symbolic(c, sh.rows, sh.n, nullptr, kZStar, true, &launches, sh.item_flop,
-                        sh.use_full ? &sh.full : nullptr, sh.window));
+                        sh.use_full ? &sh.full : nullptr, sh.window, nullptr, nullptr, 0, known));
         ev_record(c, 2);
         RC(allreduce_totals(c, kFStar, 2, false));  // f*, z*: CR is known everywhere
         ev_record(c, 3);
@@ -772,14 +838,15 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
 // F = profile.total_flop, one all-reduce of {f*, z*}, the per-row views of
 // the profile's flop.
 int pipeline_profile(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, int64_t* d_ceil,
-                     double* d_real) {
+                     double* d_real, const spnnz_gpu_ctx::HeavySizes* known = nullptr) {
     int64_t launches = 0;
     RC(settle_upload(c));
-    c->h_totals[kF] = c->profile_total;
-    c->h_totals[kMax] = c->profile_max;
-    for (int i = 0; i < kTotals; ++i)
-        if (i != kF && i != kMax) c->h_totals[i] = 0;
-    CU(cudaMemcpyAsync(c->totals.p, c->h_totals, sizeof(long long) * kTotals, cudaMemcpyHostToDevice,
+    // (a graph of this call re-reads h_init: it holds this profile's values
+    // until the profile changes, which also drops the graph)
+    for (int i = 0; i < kTotals; ++i) c->h_init[i] = 0;
+    c->h_init[kF] = c->profile_total;
+    c->h_init[kMax] = c->profile_max;
+    CU(cudaMemcpyAsync(c->totals.p, c->h_init, sizeof(long long) * kTotals, cudaMemcpyHostToDevice,
                        c->stream));
     const int64_t* item_flop = nullptr;
     if (!c->profile_own && n > 0) {
@@ -795,7 +862,7 @@ int pipeline_profile(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, int64_t
     ev_record(c, 1);
     ev_record(c, 2);
     RC(run_symbolic(c, d_rows, n, nullptr, kZStar, true, &launches, item_flop, nullptr, nullptr,
-                    nullptr, c->profile_own ? nullptr : c->flop.p, c->profile_max));
+                    nullptr, c->profile_own ? nullptr : c->flop.p, c->profile_max, known));
     ev_record(c, 3);
     RC(allreduce_totals(c, kFStar, 2, false));  // f*, z*; F and max are the profile's
     ev_record(c, 4);
@@ -861,6 +928,7 @@ int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_totals, sizeof(long long) * kTotals);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_counts, sizeof(int32_t) * 16);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_meta, sizeof(long long) * kHeavyMeta);
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_init, sizeof(long long) * kTotals);
     for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
     for (int i = 0; i < spnnz_gpu_ctx::kSide && e == cudaSuccess; ++i)
         e = cudaStreamCreateWithPriority(&c->side[i], cudaStreamNonBlocking, prio_side);
@@ -914,6 +982,8 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     if (c->h_totals) cudaFreeHost(c->h_totals);
     if (c->h_counts) cudaFreeHost(c->h_counts);
     if (c->h_meta) cudaFreeHost(c->h_meta);
+    if (c->h_init) cudaFreeHost(c->h_init);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) {
@@ -989,6 +1059,9 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
     c->loaded = false;
     c->profile_valid = false;
     c->profile_own = false;
+    ++c->epoch;
+    ++c->profile_gen;
+    c->hc_valid = false;
     c->same_b = same;
     c->a_rows = a->rows;
     c->a_cols = a->cols;
@@ -1142,6 +1215,7 @@ int spnnz_gpu_compute_flop(spnnz_gpu_ctx* c, int64_t* flop_out, int residency, i
     RC(read_totals(c));
     c->profile_valid = true;
     c->profile_own = true;
+    ++c->profile_gen;
     c->profile_total = c->h_totals[kF];
     c->profile_max = c->h_totals[kMax];
     if (total) *total = c->profile_total;
@@ -1171,6 +1245,7 @@ int spnnz_gpu_set_profile(spnnz_gpu_ctx* c, const int64_t* flop_in, int64_t rows
                            c->stream));
     c->profile_valid = true;
     c->profile_own = false;
+    ++c->profile_gen;
     c->profile_total = total;
     c->profile_max = max;
     return SPNNZ_OK;
@@ -1339,9 +1414,22 @@ int spnnz_gpu_predict_row_structure_ceil(spnnz_gpu_ctx* c, double cr, int64_t* o
 }
 
 namespace {
+// Heavy sizes the device reported for the call that just completed.
+spnnz_gpu_ctx::HeavySizes observed_sizes(const spnnz_gpu_ctx* c) {
+    spnnz_gpu_ctx::HeavySizes o;
+    if (!c->observed_set) return o;
+    o.count = c->h_counts[kHeavyBin];
+    if (o.count > 0) {
+        o.ents = c->h_meta[1];
+        o.products = c->h_meta[2];
+        o.cells = interval_path(c) ? c->h_meta[5] : 0;
+    }
+    return o;
+}
+
 int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, bool draw,
                uint64_t seed, spnnz_report* rep, int64_t* row_ceil, double* row_real,
-               int residency, bool with_profile = false) {
+               int residency, bool with_profile = false, bool redo = false) {
     const int m = local_rows(c);
     int64_t* d_ceil = row_ceil;
     double* d_real = row_real;
@@ -1355,10 +1443,79 @@ int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, boo
             d_real = c->outf.p;
         }
     }
-    if (with_profile)
-        RC(pipeline_profile(c, d_rows, n, m ? d_ceil : nullptr, m ? d_real : nullptr));
-    else
-        RC(pipeline(c, d_rows, n, draw, seed, m ? d_ceil : nullptr, m ? d_real : nullptr));
+    if (!m) d_ceil = nullptr, d_real = nullptr;
+    const char* fenv = getenv("SPNNZ_FUSED_PREDICT");
+    const bool fused = !with_profile && fenv && atoi(fenv) > 0;
+    // heavy sizes known in advance?  (a) no row can be heavy: the resident
+    // profile is this context's own for the loaded matrices and its max fits
+    // bin 5 (for run_prediction the pass recomputes the same profile);
+    // (b) the same draw ran before on the same matrices
+    using HS = spnnz_gpu_ctx::HeavySizes;
+    const HS zero{};
+    const HS* known = nullptr;
+    if (redo) {
+    } else if (c->profile_valid && c->profile_own && c->profile_max <= kBin5Max) known = &zero;
+    else if (draw && c->hc_valid && c->hc_epoch == c->epoch && c->hc_seed == seed && c->hc_n == n) known = &c->hc;
+    if (known && (known->products > (int64_t(1) << 28) || known->cells > (int64_t(1) << 28))) known = nullptr;
+    if (const char* e = getenv("SPNNZ_HEAVY_BATCH_PRODUCTS"))  // test knob: batch planning needs the sync
+        if (atoll(e) > 0) known = nullptr;
+    const HS known_v = known ? *known : HS{};
+
+    // a whole sync-free call runs as one CUDA graph, captured on first use
+    // and replayed while its key holds (no NCCL in graphs, no profiling events)
+    spnnz_gpu_ctx::GraphKey key;
+    key.kind = with_profile ? 1 : 0;
+    key.epoch = c->epoch;
+    key.profile_gen = with_profile ? c->profile_gen : 0;
+    key.seed = draw ? seed : 0;
+    key.n = n;
+    key.rows = draw ? nullptr : d_rows;
+    key.ceil = d_ceil;
+    key.real = d_real;
+    key.fused = fused;
+    key.profiling = c->profiling;
+    const char* genv = getenv("SPNNZ_GRAPH");
+    const bool graphable = known && !c->pending_upload && !c->comm && !(genv && atoi(genv) == 0);
+    c->observed_set = false;
+    if (graphable && c->gexec && c->gkey == key && c->g_known == known_v) {
+        CU(cudaGraphLaunch(c->gexec, c->stream));
+        c->last_launches = c->g_launches;
+        c->observed_set = n > 0;
+        if (!with_profile) {
+            c->profile_valid = true;
+            c->profile_own = true;
+        }
+    } else if (graphable && c->last_eager == key) {
+        if (c->gexec) {
+            cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+        }
+        cudaGraph_t graph = nullptr;
+        CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+        c->capturing = true;
+        int rc = with_profile ? pipeline_profile(c, d_rows, n, d_ceil, d_real, &known_v)
+                              : pipeline(c, d_rows, n, draw, seed, d_ceil, d_real, &known_v);
+        c->capturing = false;
+        const cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
+        if (rc != SPNNZ_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        CU(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&c->gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        CU(ie);
+        c->gkey = key;
+        c->g_known = known_v;
+        c->g_launches = c->last_launches;
+        CU(cudaGraphLaunch(c->gexec, c->stream));
+    } else {
+        if (with_profile)
+            RC(pipeline_profile(c, d_rows, n, d_ceil, d_real, known));
+        else
+            RC(pipeline(c, d_rows, n, draw, seed, d_ceil, d_real, known));
+        c->last_eager = key;
+    }
     if (residency == SPNNZ_HOST && m) {
         if (row_ceil)
             CU(cudaMemcpyAsync(row_ceil, d_ceil, 8 * size_t(m), cudaMemcpyDeviceToHost, c->stream));
@@ -1366,9 +1523,33 @@ int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, boo
             CU(cudaMemcpyAsync(row_real, d_real, 8 * size_t(m), cudaMemcpyDeviceToHost, c->stream));
     }
     RC(read_totals(c));
+    const HS seen = observed_sizes(c);
+    if (known && !(seen == known_v)) {
+        // the advance sizes were wrong (not expected: the same draw on the same
+        // matrices bins the same rows): drop them and redo the call eagerly
+        c->hc_valid = false;
+        if (c->gexec) {
+            cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+        }
+        c->last_eager = spnnz_gpu_ctx::GraphKey();
+        if (const char* e = getenv("SPNNZ_STRICT_SIZES"))
+            if (atoi(e) > 0) return set_err(SPNNZ_ECUDA, "heavy-row sizes known in advance were wrong");
+        return run_common(c, d_rows, n, p, draw, seed, rep, row_ceil, row_real, residency, with_profile, true);
+    }
+    if (draw && !known) {
+        c->hc_valid = true;
+        c->hc_epoch = c->epoch;
+        c->hc_seed = seed;
+        c->hc_n = n;
+        c->hc = seen;
+    }
     ev_collect(c);
-    c->profile_total = c->h_totals[kF];
-    c->profile_max = c->h_totals[kMax];
+    if (!with_profile) {
+        c->profile_total = c->h_totals[kF];
+        c->profile_max = c->h_totals[kMax];
+        ++c->profile_gen;
+    }
     if (rep) fill_report(rep, c->h_totals, n, p, seed);
     return SPNNZ_OK;
 }

@@ -372,10 +372,28 @@ __device__ __forceinline__ void flop_tile_rows(TileSmem<BLOCK, V>& sm, const Til
         rb = __ldg(&g.arpt[r0 + tid + 1]);
     }
     const int64_t a0 = __ldg(&g.arpt[r0]);
+    if (n == V * BLOCK && (reinterpret_cast<uintptr_t>(g.acol + ts) & 15) == 0) {
+        // whole aligned tile: asynchronous 16-byte copies straight into shared
+        // memory (chunk tid + k BLOCK: consecutive lanes, consecutive chunks)
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(sm.rowat));
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-        const int i = tid + k * BLOCK;
-        if (i < n) sm.rowat[i] = ld_stream_i32(g.acol + ts + i, first);
+        for (int k = 0; k < V / 4; ++k) {
+            const int j = tid + k * BLOCK;
+            asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst + 16 * j),
+                         "l"(g.acol + ts + 4 * j), "l"(first)
+                         : "memory");
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    } else {
+        int32_t c[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const int i = tid + k * BLOCK;
+            c[k] = i < n ? ld_stream_i32(g.acol + ts + i, first) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k)
+            if (tid + k * BLOCK < n) sm.rowat[tid + k * BLOCK] = c[k];
     }
     bar();
     const int64_t te = ts + n;
@@ -575,18 +593,15 @@ __global__ void __launch_bounds__(kFlopBlock * kSmemGroups, 1)
 k_flop_smem(TileArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut pred, int64_t t0,
             int64_t t1, unsigned long long* __restrict__ sched) {
     extern __shared__ __align__(16) unsigned char s_raw[];
-    __shared__ int64_t s_next[kSmemGroups][2];
     auto* tiles = reinterpret_cast<TileSmem<kFlopBlock, V>*>(s_raw);
     uint16_t* s_deg = reinterpret_cast<uint16_t*>(s_raw + sizeof(TileSmem<kFlopBlock, V>) * kSmemGroups);
     const int grp = threadIdx.x / kFlopBlock, tid = threadIdx.x % kFlopBlock;
-    // tiles are handed out by a ticket counter (sched[0]): a block that starts
-    // late (other kernels still hold its SM) just takes fewer; the group that
-    // draws the last out-of-range ticket (sched[1] counts them) resets both
-    if (tid == 0) {
-        const int64_t t = t0 + static_cast<int64_t>(atomicAdd(&sched[0], 1ULL));
-        s_next[grp][0] = t;
-        if (t < t1) prefetch_tile(g, t);
-    }
+    // group g of block b takes tiles b G + g, + G gridDim, ... (static: a
+    // same-address ticket counter serialises in L2); its next tile's columns
+    // are L2-prefetched while it works on the current one
+    const int64_t stride = int64_t(gridDim.x) * kSmemGroups;
+    int64_t t = t0 + int64_t(blockIdx.x) * kSmemGroups + grp;
+    if (tid == 0 && t < t1) prefetch_tile(g, t);
     // the degree table, 16 bytes per thread per step (k_rows padded to 8)
     const int words = (k_rows + 7) >> 3;
     for (int i = threadIdx.x; i < words; i += blockDim.x)
@@ -595,23 +610,157 @@ k_flop_smem(TileArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredO
     Emit emit{};
     if (PRED) emit = make_emit(pred);
     const GroupBar<kFlopBlock> bar{1 + grp};
-    int64_t t = s_next[grp][0];
-    for (int it = 0; t < t1; ++it) {
-        if (tid == 0) {  // the group's next tile, drawn now so its columns are prefetched
-            const int64_t nx = t0 + static_cast<int64_t>(atomicAdd(&sched[0], 1ULL));
-            s_next[grp][(it + 1) & 1] = nx;
-            if (nx < t1) prefetch_tile(g, nx);
-        }
+    for (; t < t1; t += stride) {
+        if (tid == 0 && t + stride < t1) prefetch_tile(g, t + stride);
         flop_tile<kFlopBlock, V, PRED, ROWS>(tiles[grp], g, t, tid, SharedDeg{s_deg}, bar, emit);
-        t = s_next[grp][(it + 1) & 1];  // written before the tile's barriers
     }
-    if (tid == 0) {
-        const unsigned long long groups = static_cast<unsigned long long>(gridDim.x) * kSmemGroups;
-        if (atomicAdd(&sched[1], 1ULL) == groups - 1) {
-            sched[0] = 0;
-            sched[1] = 0;
+    (void)sched;
+}
+
+// ------------------------------------------------------------------
+// Row blocks (A with short rows: config 4's A, a stencil): one warp per 32
+// consecutive rows.  Their entries (contiguous in A.col) are copied into the
+// warp's shared staging area with coalesced loads, then each lane sums ITS
+// row from the staging -- so a warp's k-th gathers follow 32 consecutive rows
+// (consecutive columns in a banded A) -- and writes it (32 consecutive int64
+// per warp).  Rows end inside their block: no tile partition, no fixup; F and
+// max go out with one pair of atomics per block.  A block whose entries
+// exceed the staging area falls back to one row at a time (lane-strided).
+// The degree table is in shared memory when B's rows fit (SMEM), else the
+// L2-resident uint16 array.
+constexpr int kRbRows = 32;
+template <bool SMEM>
+struct RbShape {
+    // SMEM: one 1024-thread block per SM beside the degree table; else
+    // 256-thread blocks, several per SM
+    static constexpr int kThreads = SMEM ? 1024 : 256;
+    static constexpr int kWarps = kThreads / 32;
+    static constexpr int kStage = SMEM ? 640 : 1536;  // entries per warp
+};
+
+struct RbArgs {
+    const int64_t* __restrict__ arpt;  // m + 1 absolute offsets
+    const int32_t* __restrict__ acol;
+    const int64_t* __restrict__ brpt;
+    int32_t m;
+    int64_t* __restrict__ flop;
+    long long* __restrict__ totals;
+};
+
+template <bool SMEM, bool PRED>
+__global__ void __launch_bounds__(RbShape<SMEM>::kThreads, 1)
+k_flop_rb(RbArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut pred,
+          unsigned long long* __restrict__ sched) {
+    using Sh = RbShape<SMEM>;
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    int32_t* stage_all = reinterpret_cast<int32_t*>(s_raw);
+    const uint16_t* s_deg = reinterpret_cast<const uint16_t*>(s_raw + size_t(Sh::kWarps) * Sh::kStage * 4);
+    __shared__ long long s_sum[Sh::kWarps], s_max[Sh::kWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t* stage = stage_all + warp * Sh::kStage;
+    const uint64_t first = policy_evict_first(), last = policy_evict_last();
+    if (SMEM) {
+        uint16_t* d = const_cast<uint16_t*>(s_deg);
+        const int words = (k_rows + 7) >> 3;
+        for (int i = threadIdx.x; i < words; i += blockDim.x)
+            reinterpret_cast<int4*>(d)[i] = __ldg(reinterpret_cast<const int4*>(bdeg) + i);
+        __syncthreads();
+    }
+    Emit emit{};
+    if (PRED) emit = make_emit(pred);
+    const auto deg = [&](int32_t c) -> int32_t {
+        const int32_t v = SMEM ? s_deg[c] : gather_deg(bdeg + c, last);
+        return v == 0xFFFF ? static_cast<int32_t>(__ldg(&g.brpt[c + 1]) - __ldg(&g.brpt[c])) : v;
+    };
+    const int64_t units = (int64_t(g.m) + kRbRows - 1) / kRbRows;
+    long long wsum = 0, wmax = 0;
+    // SMEM: units handed out by a ticket counter (a block that starts late
+    // takes fewer); else one unit per warp of the grid
+    // every warp of the grid takes units warp, warp + W, ... (static: a
+    // same-address ticket counter serialises in L2, ~one atomic per 15 ns)
+    for (int64_t u = int64_t(blockIdx.x) * Sh::kWarps + warp; u < units; u += int64_t(gridDim.x) * Sh::kWarps) {
+        const int32_t r0 = static_cast<int32_t>(u * kRbRows);
+        const int32_t r = r0 + lane;
+        const int32_t rl = r0 + kRbRows < g.m ? r0 + kRbRows : g.m;  // rows [r0, rl)
+        const int64_t rs = r < g.m ? __ldg(&g.arpt[r]) : 0;
+        const int64_t re = r < g.m ? __ldg(&g.arpt[r + 1]) : 0;
+        // rows [j, jend) whose entries fit the staging area go together; a
+        // row longer than the area goes alone, lane-strided
+        int32_t j = r0;
+        while (j < rl) {
+            const int64_t Ej = __shfl_sync(0xffffffffu, rs, j - r0);
+            const unsigned fit = __ballot_sync(0xffffffffu, r >= j && r < rl && re - Ej <= Sh::kStage);
+            if (fit == 0u) {  // row j alone
+                const int64_t b = __shfl_sync(0xffffffffu, re, j - r0);
+                long long sum = 0;
+                for (int64_t e = Ej + lane; e < b; e += 32 * 4) {
+                    int32_t c[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) c[k] = e + 32 * k < b ? ld_stream_i32(g.acol + e + 32 * k, first) : -1;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) sum += c[k] >= 0 ? deg(c[k]) : 0;
+                }
+                sum = warp_sum_ll(sum);
+                if (lane == 0) {
+                    g.flop[j] = sum;
+                    if (PRED) emit(j, sum);
+                    wsum += sum;
+                    wmax = sum > wmax ? sum : wmax;
+                }
+                ++j;
+                continue;
+            }
+            const int32_t jend = r0 + 32 - __clz(fit);  // rows [j, jend): a run of lanes
+            const int64_t ne = __shfl_sync(0xffffffffu, re, jend - 1 - r0) - Ej;
+            // stage their columns: 16 loads in flight per lane per round
+            for (int64_t e = lane; e < ne; e += 32 * 16) {
+                int32_t c[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    c[k] = e + 32 * k < ne ? ld_stream_i32(g.acol + Ej + e + 32 * k, first) : 0;
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    if (e + 32 * k < ne) stage[e + 32 * k] = c[k];
+            }
+            __syncwarp();
+            if (r >= j && r < jend) {
+                long long sum = 0;
+                const int i0 = static_cast<int>(rs - Ej), i1 = static_cast<int>(re - Ej);
+                for (int i = i0; i < i1; i += 8) {
+                    int32_t cc[8], d[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) cc[k] = i + k < i1 ? stage[i + k] : -1;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) d[k] = cc[k] >= 0 ? deg(cc[k]) : 0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) sum += d[k];
+                }
+                g.flop[r] = sum;
+                if (PRED) emit(r, sum);
+                wsum += sum;
+                wmax = sum > wmax ? sum : wmax;
+            }
+            __syncwarp();  // the staging is reused next
+            j = jend;
         }
     }
+    wsum = warp_sum_ll(wsum);
+    wmax = warp_max_ll(wmax);
+    if (lane == 0) {
+        s_sum[warp] = wsum;
+        s_max[warp] = wmax;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        long long a = lane < Sh::kWarps ? s_sum[lane] : 0, b = lane < Sh::kWarps ? s_max[lane] : 0;
+        a = warp_sum_ll(a);
+        b = warp_max_ll(b);
+        if (lane == 0) {
+            if (a) atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[kF]), static_cast<unsigned long long>(a));
+            atomicMax(reinterpret_cast<unsigned long long*>(&g.totals[kMax]), static_cast<unsigned long long>(b));
+        }
+    }
+    (void)sched;
 }
 
 // Adds each tile's leading slice to the row it continues (one thread per
@@ -1021,11 +1170,17 @@ cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStr
 }
 #endif
 
+// dynamic shared memory of k_flop_smem; its static part (the ticket slots)
+// is kept under kSmemStatic, and the total under the 227 KB per-block limit
+constexpr size_t kSmemStatic = 1024;
 static size_t flop_smem_bytes(int32_t k_rows) {
     return sizeof(TileSmem<kFlopBlock, kFlopIpt>) * kSmemGroups + ((size_t(k_rows) * 2 + 15) & ~size_t(15));
 }
 
-bool flop_smem_fits(int32_t k_rows) { return k_rows > 0 && flop_smem_bytes(k_rows) <= 227 * 1024; }
+// K <= 81280 rows (tests/test_gpu_parity.py and bench.py name this limit)
+bool flop_smem_fits(int32_t k_rows) {
+    return k_rows > 0 && flop_smem_bytes(k_rows) + kSmemStatic <= 227 * 1024;
+}
 
 static TileArgs tile_args(const DevCsr& a, const int64_t* brpt, const FlopScratch& s, int64_t* flop,
                           const FlopMode& mode) {
@@ -1054,7 +1209,7 @@ static cudaError_t launch_tiles(const TileArgs& g, const uint16_t* bdeg, int64_t
         cudaGetDevice(&dev);
         if (!(attr_done.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
             cudaFuncSetAttribute(k_flop_smem<kFlopIpt, PRED, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 227 * 1024);
+                                 static_cast<int>(227 * 1024 - kSmemStatic));
             attr_done.fetch_or(1ull << (dev & 63), std::memory_order_release);
         }
         int64_t grid = (t_end - t_begin + kSmemGroups - 1) / kSmemGroups;
@@ -1078,6 +1233,52 @@ cudaError_t launch_flop_tiles(const DevCsr& a, const uint16_t* bdeg, const int64
                          : launch_tiles<false, true>(g, bdeg, t_begin, t_end, stream, pred, mode);
     return pred.on() ? launch_tiles<true, false>(g, bdeg, t_begin, t_end, stream, pred, mode)
                      : launch_tiles<false, false>(g, bdeg, t_begin, t_end, stream, pred, mode);
+}
+
+template <bool SMEM, bool PRED>
+static cudaError_t launch_rb(const RbArgs& g, const uint16_t* bdeg, int32_t k_rows, const PredOut& pred,
+                             const FlopMode& mode, cudaStream_t stream) {
+    using Sh = RbShape<SMEM>;
+    const size_t smem = size_t(Sh::kWarps) * Sh::kStage * 4 + (SMEM ? ((size_t(k_rows) * 2 + 15) & ~size_t(15)) : 0);
+    static std::atomic<unsigned long long> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_done.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
+        cudaFuncSetAttribute(k_flop_rb<SMEM, PRED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(227 * 1024 - kSmemStatic));
+        attr_done.fetch_or(1ull << (dev & 63), std::memory_order_release);
+    }
+    const int64_t units = (int64_t(g.m) + kRbRows - 1) / kRbRows;
+    int64_t grid = (units + Sh::kWarps - 1) / Sh::kWarps;
+    if (SMEM && grid > mode.num_sms) grid = mode.num_sms;
+    if (grid < 1) grid = 1;
+    k_flop_rb<SMEM, PRED><<<static_cast<unsigned>(grid), Sh::kThreads, smem, stream>>>(g, bdeg, k_rows, pred,
+                                                                                       mode.sched);
+    return cudaGetLastError();
+}
+
+bool flop_rb_smem_fits(int32_t k_rows) {
+    using Sh = RbShape<true>;
+    return k_rows > 0 && size_t(Sh::kWarps) * Sh::kStage * 4 + ((size_t(k_rows) * 2 + 15) & ~size_t(15)) +
+                             kSmemStatic <= 227 * 1024;
+}
+
+cudaError_t launch_flop_rows(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt, int64_t* flop,
+                             long long* totals, cudaStream_t stream, const PredOut& pred, const FlopMode& mode) {
+    if (a.rows == 0) return cudaSuccess;
+    RbArgs g;
+    g.arpt = a.rpt;
+    g.acol = a.col;
+    g.brpt = brpt;
+    g.m = a.rows;
+    g.flop = flop;
+    g.totals = totals;
+    const bool smem = !mode.no_smem && flop_rb_smem_fits(mode.b_rows);
+    if (smem)
+        return pred.on() ? launch_rb<true, true>(g, bdeg, mode.b_rows, pred, mode, stream)
+                         : launch_rb<true, false>(g, bdeg, mode.b_rows, pred, mode, stream);
+    return pred.on() ? launch_rb<false, true>(g, bdeg, mode.b_rows, pred, mode, stream)
+                     : launch_rb<false, false>(g, bdeg, mode.b_rows, pred, mode, stream);
 }
 
 cudaError_t launch_flop_fixup(const DevCsr& a, const FlopScratch& s, int64_t* flop, long long* totals,

@@ -92,6 +92,13 @@ struct FlopMode {
     int num_sms = 148;
 };
 bool flop_smem_fits(int32_t k_rows);
+// Row-block FLOP pass (A with short rows): one warp per 32 rows over
+// shared-staged columns, degree table in shared memory when B's rows fit
+// (flop_rb_smem_fits); writes flop and adds F / max into totals directly (no
+// partition, no fixup).  mode.sched: the smem kernel's tickets.
+bool flop_rb_smem_fits(int32_t k_rows);
+cudaError_t launch_flop_rows(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt, int64_t* flop,
+                             long long* totals, cudaStream_t stream, const PredOut& pred, const FlopMode& mode);
 // Sampled banded-A check (n pairs of consecutive rows in [lo, hi)), rpt/col
 // device arrays with absolute offsets: out3 = {pairs, advancing, short}.
 cudaError_t launch_locality(const int64_t* rpt, const int32_t* col, int32_t lo, int32_t hi, int n, int* out3,

@@ -116,12 +116,21 @@ def _long_b(k, n, seed, long_rows=(3, 7), long_len=70000):
     return spnnz.CsrMatrix(k, n, rpt, col)
 
 
-@pytest.mark.parametrize("k", [81792, 81793])  # largest K whose degree table fits shared memory, and one more
-@pytest.mark.parametrize("smem", ["1", "0"])
-def test_flop_degree_table_threshold(oracle, monkeypatch, k, smem):
-    """The shared-memory degree table (persistent 8-group blocks) on both sides
-    of its size limit, with the global-memory kernel forced as the A/B
-    reference, incl. B rows past the uint16 escape and A rows spanning tiles."""
+# the FLOP-pass kernels: (row blocks?, shared degree table?)
+FLOP_KERNELS = {"tiles-smem": ("0", "1"), "tiles-global": ("0", "0"), "rb-smem": ("1", "1"),
+                "rb-global": ("1", "0")}
+
+
+# largest K whose degree table fits beside the row-block staging (74752) and
+# beside the tile groups (81280), and one more of each
+@pytest.mark.parametrize("k", [74752, 74753, 81280, 81281])
+@pytest.mark.parametrize("kernel", list(FLOP_KERNELS))
+def test_flop_degree_table_threshold(oracle, monkeypatch, k, kernel):
+    """The shared-memory degree tables (persistent row-block and tile-group
+    blocks) on both sides of their size limits, and the global-memory kernels,
+    incl. B rows past the uint16 escape and A rows spanning tiles / blocks."""
+    rb, smem = FLOP_KERNELS[kernel]
+    monkeypatch.setenv("SPNNZ_FLOP_RB", rb)
     monkeypatch.setenv("SPNNZ_FLOP_SMEM", smem)
     rng = np.random.default_rng(k)
     m = 4000
@@ -140,13 +149,17 @@ def test_flop_degree_table_threshold(oracle, monkeypatch, k, smem):
 
 
 @pytest.mark.parametrize("rows_mode", ["1", "0"])
-@pytest.mark.parametrize("smem", ["1", "0"])
+@pytest.mark.parametrize("kernel", list(FLOP_KERNELS))
 @pytest.mark.parametrize("shape", ["stencil", "random", "long+empty"])
-def test_flop_row_mode(oracle, monkeypatch, rows_mode, smem, shape):
-    """Row-per-thread tiles (banded A) forced on and off, on a stencil (where
-    load() picks them) and on shapes it would not pick: per-row FLOP, F and
-    max identical to the oracle either way."""
+def test_flop_row_mode(oracle, monkeypatch, rows_mode, kernel, shape):
+    """Every FLOP-pass kernel (tiles / row blocks, shared / global degree
+    table) with row-per-thread tiles (banded A) forced on and off, on a
+    stencil (where load() picks them) and on shapes it would not pick
+    (a 10 K-entry row, empty runs, rows longer than a row block's staging):
+    per-row FLOP, F and max identical to the oracle, plain and fused."""
+    rb, smem = FLOP_KERNELS[kernel]
     monkeypatch.setenv("SPNNZ_FLOP_ROWS", rows_mode)
+    monkeypatch.setenv("SPNNZ_FLOP_RB", rb)
     monkeypatch.setenv("SPNNZ_FLOP_SMEM", smem)
     if shape == "stencil":
         a = gen.stencil27(40, 30, 20)
@@ -639,8 +652,21 @@ def test_config_vs_reference_digests(P, golden, cfg):
         s = P.sampled_symbolic(rep.plan.sample_rows)
         assert s.total_nnz == m["z_star"] and digest(s.nnz_per_row) == m["per_sample"]
     if "Z" in rec:
+        # config 5: pinned to the reference's own exact_symbolic (row slices,
+        # tests/golden/make_cfg5_exact.py); per-2^20-row digests localise a miss
         ex = P.exact_symbolic()
+        if "exact_nnz_blocks" in rec:
+            blk = 1 << 20
+            got = [digest(ex.nnz_per_row[i:i + blk]) for i in range(0, a.rows, blk)]
+            bad = [i for i, (x, y) in enumerate(zip(got, rec["exact_nnz_blocks"])) if x != y]
+            assert not bad, f"exact per-row NNZ differs in row blocks {bad}"
         assert ex.total_nnz == rec["Z"] and digest(ex.nnz_per_row) == rec["exact_nnz"]
+        for label in rec["modes"]:
+            if "errors" in rec["modes"][label]:
+                r = rec["modes"][label]["report"]
+                e = spnnz.error_report(r["z1_star"], r["z2_star"], r["sampled_flop"], ex.total_nnz,
+                                       prof.total_flop, r["p"])
+                assert [e.eps1, e.eps_f, e.eps2, e.identity_residual] == rec["modes"][label]["errors"]
         if cfg == 3:
             assert ex.total_nnz == 634 ** 3 and prof.total_flop == 1142 ** 3
 
@@ -778,6 +804,52 @@ def test_repeat_runs_deterministic(P):
     r2 = P.run_prediction(4, SamplePolicy(0.005, UNCAPPED))
     assert r1.stats.sampled_nnz == r2.stats.sampled_nnz and r1.z2_star == r2.z2_star
     assert (r1.predicted_row_nnz_ceil == r2.predicted_row_nnz_ceil).all()
+
+
+def _rep_tuple(r):
+    return (r.total_flop, r.stats.sampled_flop, r.stats.sampled_nnz, r.predicted_cr, r.z1_star, r.z2_star)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_repeat_calls_graph_replay_and_cached_heavy_sizes(golden, cfg, monkeypatch):
+    """Repeated calls take the sync-free path: heavy-row sizes known in advance
+    (no row can be heavy, or the same draw ran before: config 2 has heavy
+    rows), captured into a CUDA graph on the second use and replayed after --
+    every call's outputs equal the eager path's and the reference's; changing
+    the seed, the outputs or the profile drops / re-keys the graph."""
+    import torch
+    monkeypatch.setenv("SPNNZ_STRICT_SIZES", "1")  # a wrong advance size is an error here
+    rec = golden["configs"][str(cfg)] if str(cfg) in golden["configs"] else None
+    info = gen.CONFIGS[cfg]
+    a, b = gen.make_config(cfg)
+    P = Predictor(0)
+    P.load(a, None if b is a else b)
+    pol = SamplePolicy(info["fraction"], UNCAPPED)
+    m = P.local_rows
+    out = torch.empty(m, dtype=torch.int64, device="cuda")
+    reps, ceils = [], []
+    for i in range(5):  # eager (sync), eager (known sizes), capture, replay, replay
+        r = P.run_prediction(info["seed"], pol, ceil_out=out, residency=spnnz.DEVICE,
+                             want_real=False, want_samples=False)
+        reps.append(_rep_tuple(r))
+        ceils.append(out.cpu().numpy().copy())
+        out.fill_(-7)
+    assert all(x == reps[0] for x in reps)
+    assert all(np.array_equal(x, ceils[0]) for x in ceils)
+    if rec:
+        ref = rec["modes"]["uncapped"]
+        assert reps[0][2] == ref["z_star"] and digest(ceils[0]) == ref["ceil"]
+    # another seed: a new key (its own eager run first)
+    r2 = P.run_prediction(info["seed"] + 1, pol, ceil_out=out, residency=1, want_real=False, want_samples=False)
+    monkeypatch.setenv("SPNNZ_GRAPH", "0")
+    r2e = P.run_prediction(info["seed"] + 1, pol, ceil_out=out, residency=1, want_real=False, want_samples=False)
+    assert _rep_tuple(r2) == _rep_tuple(r2e)
+    monkeypatch.delenv("SPNNZ_GRAPH")
+    # the profile path (run_prediction_with_plan on the resident profile), repeated
+    plan = P.make_sample_plan(a.rows, 3, pol)
+    w = [_rep_tuple(P.run_prediction_with_plan(plan)) for _ in range(4)]
+    assert all(x == w[0] for x in w)
+    P.close()
 
 
 def test_device_residency_matches_host(P):
