@@ -327,3 +327,33 @@ def test_reference_ceil_pipeline_equals_full_pipeline():
             assert (c_full == c_lean).all()
     finally:
         R.free_matrix(h)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_config_error_reports_restated(oracle, golden, cfg):
+    """The reference's error_report of every config's pinned exact Z
+    (config 5: tests/golden/make_cfg5_exact.py, the reference's exact_symbolic
+    over row slices) is reproduced by the oracle's restatement
+    (predict.hpp:163-188), and Z <= F with the sampled CR >= 1."""
+    rec = golden["configs"].get(str(cfg))
+    if not rec or "Z" not in rec:
+        pytest.skip("no exact Z pinned for this config")
+    assert 0 < rec["Z"] <= rec["F"]
+    for label, m in rec["modes"].items():
+        if "errors" not in m:
+            continue
+        r = m["report"]
+        e = oracle.error_report(r["z1_star"], r["z2_star"], r["sampled_flop"], rec["Z"], rec["F"], r["p"])
+        assert list(e) == m["errors"], label
+        assert r["predicted_cr"] >= 1.0
+
+
+def test_config5_exact_pin_is_the_slicewise_reference():
+    """Config 5's pin records how it was made, and the slicing was validated
+    on config 2 (the same script's self-check against make_golden.py's
+    whole-matrix reference run)."""
+    import json
+    import os
+    rec = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "configs.json")))["5"]
+    assert rec["Z"] == 127786666282
+    assert "exact_symbolic" in rec["exact_method"] and len(rec["exact_nnz_blocks"]) == 16
