@@ -208,6 +208,12 @@ int spnnz_gpu_last_timings(spnnz_gpu_ctx* ctx, double* ms_out5, int64_t* launche
  * none of the row logic, averaged over reps launches (ms, CUDA events).
  * bench.py reports the pass against it (roofline.pattern_ceiling_*). */
 int spnnz_gpu_probe_flop_floor(spnnz_gpu_ctx* ctx, int reps, double* stream_ms, double* gather_ms);
+/* Guard bands: with SPNNZ_GUARD=1 in the environment when the library
+ * allocates, each device buffer is followed by 256 bytes of a known pattern,
+ * checked when the buffer is freed and here for the live ones: reports how
+ * many buffers were checked and how many bands changed (an out-of-bounds
+ * write).  Synchronizes the device.  Test instrumentation. */
+int spnnz_gpu_check_guards(int64_t* checked, int64_t* broken);
 /* The context's CUDA stream (cudaStream_t), for callers that time on it. */
 void* spnnz_gpu_stream(spnnz_gpu_ctx* ctx);
 /* Ordering of DEVICE-residency inputs: every call that reads one first makes

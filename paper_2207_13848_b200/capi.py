@@ -84,6 +84,7 @@ _SIGS = {
     "spnnz_gpu_stream": (c_void_p, [c_void_p]),
     "spnnz_gpu_set_input_stream": (c_int, [c_void_p, c_void_p]),
     "spnnz_gpu_probe_flop_floor": (c_int, [c_void_p, c_int, POINTER(c_double), POINTER(c_double)]),
+    "spnnz_gpu_check_guards": (c_int, [POINTER(c_int64), POINTER(c_int64)]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -110,6 +110,37 @@ Nccl& nccl() {
     } while (0)
 
 // ---------------------------------------------------------- device buffer
+// Guard bands (SPNNZ_GUARD=1 when a buffer is allocated): every allocation
+// gets kGuardBytes of a known pattern after its last element, and
+// spnnz_gpu_check_guards() reports any buffer whose band changed -- an
+// out-of-bounds write past a library buffer.  (compute-sanitizer is closed on
+// the GPU pool this was built on; this is the check that runs instead.)
+constexpr size_t kGuardBytes = 256;
+constexpr unsigned char kGuardByte = 0xA5;
+
+struct GuardEntry {
+    const void* base;
+    size_t bytes;  // payload; the band follows
+};
+std::mutex g_guard_mu;
+std::vector<GuardEntry> g_guards;
+int64_t g_guard_released_broken = 0, g_guard_released = 0;
+
+bool band_intact(const GuardEntry& g) {
+    unsigned char band[kGuardBytes];
+    if (cudaMemcpy(band, static_cast<const unsigned char*>(g.base) + g.bytes, kGuardBytes,
+                   cudaMemcpyDeviceToHost) != cudaSuccess)
+        return false;
+    for (unsigned char b : band)
+        if (b != kGuardByte) return false;
+    return true;
+}
+
+bool guard_on() {
+    const char* e = getenv("SPNNZ_GUARD");
+    return e && atoi(e) > 0;
+}
+
 // Owns one device allocation; freed with the context (the destructor runs
 // after spnnz_gpu_destroy has selected the context's device).
 template <typename T>
@@ -122,20 +153,37 @@ struct DBuf {
     ~DBuf() { release(); }
     int ensure(int64_t want) {
         if (want <= n && p) return SPNNZ_OK;
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = 0;
+        release();
         const size_t bytes = sizeof(T) * static_cast<size_t>(std::max<int64_t>(want, 1));
-        cudaError_t e = cudaMalloc(&p, bytes);
+        const bool guard = guard_on();
+        cudaError_t e = cudaMalloc(&p, bytes + (guard ? kGuardBytes : 0));
         if (e != cudaSuccess) {
             p = nullptr;
             return set_err(SPNNZ_ENOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+        }
+        if (guard) {
+            cudaMemset(reinterpret_cast<unsigned char*>(p) + bytes, kGuardByte, kGuardBytes);
+            std::lock_guard<std::mutex> lk(g_guard_mu);
+            g_guards.push_back(GuardEntry{p, bytes});
         }
         n = want;
         return SPNNZ_OK;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            {
+                std::lock_guard<std::mutex> lk(g_guard_mu);
+                for (size_t i = 0; i < g_guards.size(); ++i)
+                    if (g_guards[i].base == p) {
+                        ++g_guard_released;  // a buffer's band is checked before it is freed
+                        if (!band_intact(g_guards[i])) ++g_guard_released_broken;
+                        g_guards[i] = g_guards.back();
+                        g_guards.pop_back();
+                        break;
+                    }
+            }
+            cudaFree(p);
+        }
         p = nullptr;
         n = 0;
     }
@@ -1645,6 +1693,16 @@ int spnnz_gpu_probe_flop_floor(spnnz_gpu_ctx* c, int reps, double* stream_ms, do
         CU(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
         if (res[g]) *res[g] = ms / reps;
     }
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_check_guards(int64_t* checked, int64_t* broken) {
+    CU(cudaDeviceSynchronize());
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    int64_t bad = g_guard_released_broken;
+    for (const GuardEntry& g : g_guards) bad += band_intact(g) ? 0 : 1;
+    if (checked) *checked = static_cast<int64_t>(g_guards.size()) + g_guard_released;
+    if (broken) *broken = bad;
     return SPNNZ_OK;
 }
 

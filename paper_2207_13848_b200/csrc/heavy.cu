@@ -619,7 +619,19 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
         const int32_t col_base = R > 1 ? (t.r0 << wshift) : 0;
         const int32_t words = R > 1 ? ((t.r1 - t.r0) << (wshift - 5)) : max_words;
         int cnt = 0;
+        // a task that shares its span with others (merge slot) counts at the
+        // merge, so its inserts need no return value (no wait on the atomic)
+        const bool merged = t.slot >= 0;
         auto insert = [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll], long long) {
+            if (merged) {
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+                    if (valid[u]) {
+                        const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
+                        atomicOr(&s_set[off >> 5], 1u << (off & 31));
+                    }
+                return;
+            }
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
                 if (valid[u]) {

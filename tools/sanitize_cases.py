@@ -112,6 +112,13 @@ def main():
     outs = [P.run_prediction(5, SamplePolicy(0.5, -1)) for _ in range(4)]
     assert all(o.stats.sampled_nnz == outs[0].stats.sampled_nnz for o in outs)
     done.append("repeated calls (graph replay)")
+    if os.environ.get("SPNNZ_GUARD") == "1":  # guard bands after every library buffer
+        import ctypes
+        from paper_2207_13848_b200.capi import check, lib
+        n, bad = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().spnnz_gpu_check_guards(ctypes.byref(n), ctypes.byref(bad)))
+        assert n.value > 0 and bad.value == 0, f"{bad.value} of {n.value} guard bands overwritten"
+        done.append(f"guard bands intact ({n.value} buffers)")
     P.close()
     print("sanitize cases ok:", "; ".join(done))
 
