@@ -882,6 +882,21 @@ def test_cpp_dropin_header():
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+def test_guard_bands_sanitize_cases():
+    """compute-sanitizer is closed on the GPU pool, so out-of-bounds writes are
+    caught with guard bands instead: every library buffer is followed by 256
+    bytes of a known pattern (SPNNZ_GUARD=1), and tools/sanitize_cases.py --
+    every kernel family on small inputs, each result checked against the CPU
+    oracle -- must leave every band intact."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SPNNZ_GUARD="1")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_cases.py")], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "guard bands intact" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_cpp_dropin_reference_types():
     """The reference's own spnnz::CsrMatrix / FlopProfile / SamplePlan into
     spnnz::gpu::*, every output compared with the unmodified reference function
