@@ -287,6 +287,7 @@ struct spnnz_gpu_ctx {
     DBuf<uint16_t> deg;  // uint16 row lengths of B (rebuilt every FLOP pass)
     DBuf<long long> tile_carry, tile_total, tile_max;
     DBuf<long long> totals;
+    DBuf<long long> totals_table;  // world x kTotals: the all-reduce's all-gather table
     long long* h_totals = nullptr;  // pinned mirror
     int32_t* h_counts = nullptr;    // pinned mirror of bin counts
     DBuf<int32_t> counts;
@@ -656,18 +657,17 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
     return SPNNZ_OK;
 }
 
-// Sum-all-reduce of totals[first, first + count) (default: F, f*, z*, Z), and
-// with_max the max of totals[kMax], across ranks.
+// Sum of totals[first, first + count) (default: F, f*, z*, Z) and, with_max,
+// the max of totals[kMax] across ranks -- ONE NCCL all-reduce: a SUM over a
+// world x kTotals table in which each rank fills its own row (an all-gather
+// of 8 x world int64), then the sums and the max are taken on the device.
 int allreduce_totals(spnnz_gpu_ctx* c, int first = 0, int count = 4, bool with_max = true) {
     if (!c->comm) return SPNNZ_OK;
-    Nccl& n = nccl();
-    NC(n.GroupStart());
-    NC(n.AllReduce(c->totals.p + first, c->totals.p + first, count, ncclInt64, ncclSum, c->comm,
-                   c->stream));
-    if (with_max)
-        NC(n.AllReduce(c->totals.p + kMax, c->totals.p + kMax, 1, ncclInt64, ncclMax, c->comm,
-                       c->stream));
-    NC(n.GroupEnd());
+    RC(c->totals_table.ensure(int64_t(c->world) * kTotals));
+    CU(launch_totals_spread(c->totals.p, c->totals_table.p, c->rank, c->world, c->stream));
+    NC(nccl().AllReduce(c->totals_table.p, c->totals_table.p, size_t(c->world) * kTotals, ncclInt64, ncclSum,
+                        c->comm, c->stream));
+    CU(launch_totals_finish(c->totals.p, c->totals_table.p, c->world, first, count, with_max, c->stream));
     return SPNNZ_OK;
 }
 

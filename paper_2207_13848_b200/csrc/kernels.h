@@ -267,6 +267,15 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
 cudaError_t launch_heavy_flops(const SymArgs& args, const SymScratch& s, int64_t count,
                                int64_t* out, cudaStream_t stream);
 
+// The single all-reduce of the totals (sums and the max): spread this rank's
+// totals into row `rank` of a world x kTotals table (zero elsewhere), SUM
+// all-reduce the table, finish: totals[first..first+count) = column sums,
+// totals[kMax] = column max (with_max).
+cudaError_t launch_totals_spread(const long long* totals, long long* table, int rank, int world,
+                                 cudaStream_t stream);
+cudaError_t launch_totals_finish(long long* totals, const long long* table, int world, int first, int count,
+                                 bool with_max, cudaStream_t stream);
+
 // -------------------------------------------------------------- predict
 // ceil view min(flop, ceil(flop / cr)) and/or real view flop / cr.  If
 // totals != nullptr the CR is derived on the device from totals[kFStar],

@@ -86,7 +86,44 @@ k_predict(const int64_t* __restrict__ flop, int64_t m, const long long* __restri
     }
 }
 
+// One NCCL all-reduce for sums AND the max: every rank writes its slots
+// [first, first + count) (and kMax) into its own row of a world x kTotals
+// table that is zero elsewhere; a SUM all-reduce of the table gathers every
+// rank's values, and k_totals_finish reduces the rows (sum, or max for kMax).
+__global__ void k_totals_spread(const long long* __restrict__ totals, long long* __restrict__ table, int rank,
+                                int world) {
+    for (int i = threadIdx.x; i < world * kTotals; i += blockDim.x)
+        table[i] = i / kTotals == rank ? totals[i % kTotals] : 0;
+}
+
+__global__ void k_totals_finish(long long* __restrict__ totals, const long long* __restrict__ table, int world,
+                                int first, int count, int with_max) {
+    const int i = threadIdx.x;
+    if (i >= kTotals) return;
+    const bool sum = i >= first && i < first + count;
+    const bool mx = with_max && i == kMax;
+    if (!sum && !mx) return;
+    long long v = sum ? 0 : table[i];
+    for (int r = 0; r < world; ++r) {
+        const long long x = table[r * kTotals + i];
+        v = sum ? v + x : (x > v ? x : v);
+    }
+    totals[i] = v;
+}
+
 }  // namespace
+
+cudaError_t launch_totals_spread(const long long* totals, long long* table, int rank, int world,
+                                 cudaStream_t stream) {
+    k_totals_spread<<<1, 256, 0, stream>>>(totals, table, rank, world);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_totals_finish(long long* totals, const long long* table, int world, int first, int count,
+                                 bool with_max, cudaStream_t stream) {
+    k_totals_finish<<<1, 32, 0, stream>>>(totals, table, world, first, count, with_max ? 1 : 0);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* rows,
                           cudaStream_t stream) {

@@ -52,11 +52,14 @@ def _worker(rank, world, port, cfg, results):
         own = rows[(rows >= lo) & (rows < hi)] - lo                 # keeps its own draws
         fs = O.sampled_flop(flop, own) if len(own) else 0
         zs = O.sampled_symbolic(mine, b, flop, mx, own)[1] if len(own) else 0
-        t = torch.tensor([F, fs, zs], dtype=torch.int64)
-        m = torch.tensor([mx], dtype=torch.int64)
-        dist.all_reduce(t)                                          # the single exchange
-        dist.all_reduce(m, op=dist.ReduceOp.MAX)
-        F, fs, zs = (int(x) for x in t)
+        # the single exchange, as capi.cpp allreduce_totals does it: each rank
+        # fills its own row of a world x 8 table (slots F, f*, z*, Z, max),
+        # one SUM all-reduce gathers the rows, sums and the max are local
+        table = torch.zeros(world, 8, dtype=torch.int64)
+        table[rank, :5] = torch.tensor([F, fs, zs, 0, mx])
+        dist.all_reduce(table)
+        F, fs, zs = (int(x) for x in table[:, :3].sum(0))
+        m = table[:, 4].max()
         pp = spnnz.predict_proposed(spnnz.SampleStats(fs, zs), F)
         z1 = spnnz.predict_reference(spnnz.SampleStats(fs, zs), spnnz.SamplePlan(p=p))
         ceil = O.predict_row_structure_ceil(flop, pp.predicted_cr)
