@@ -86,7 +86,8 @@ def main():
             rd = sum(num(d, "dram__bytes_read.sum") for d in ks)
             wr = sum(num(d, "dram__bytes_write.sum") for d in ks)
             allt[cfg] = {"kernels": [d["Kernel Name"].split("(")[0] for d in ks],
-                         "source": os.path.relpath(rep, ROOT), "round": args.round,
+                         "source": f"profiles/{args.round}_{os.path.splitext(os.path.basename(rep))[0]}.md",
+                         "round": args.round,
                          "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                          "duration_ms": sum(dur_ms(d) for d in ks),
                          "l2_hit_rate_pct": float(main_k.get("lts__t_sector_hit_rate.pct", "nan").replace(",", "")),
