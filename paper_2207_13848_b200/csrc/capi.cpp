@@ -638,10 +638,9 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
         return SPNNZ_OK;
     }
     // row blocks (one warp per 32 rows, no partition / fixup) when B is small
-    // enough for their shared degree table (config 4: 75.6 vs 78.8 us for the
-    // tile groups; with the degree array in L2 the tiles win: config 3 140 vs
-    // 150 us)
-    bool rb = !mode.no_smem && flop_rb_smem_fits(c->b_rows);
+    // enough for their shared degree table (config 4: 65.5 us, the tile groups
+    // 78.8) or A is banded (config 3: 121 us, row-mode tiles 135)
+    bool rb = (!mode.no_smem && flop_rb_smem_fits(c->b_rows)) || c->rows_mode;
     if (const char* e = getenv("SPNNZ_FLOP_RB")) rb = atoi(e) > 0;  // A/B knob
     if (rb) {
         int64_t nk = 0;

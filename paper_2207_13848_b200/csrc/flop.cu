@@ -635,7 +635,9 @@ struct RbShape {
     // 256-thread blocks, several per SM
     static constexpr int kThreads = SMEM ? 1024 : 256;
     static constexpr int kWarps = kThreads / 32;
-    static constexpr int kStage = SMEM ? 640 : 1536;  // entries per warp
+    // entries staged per warp: SMEM 32 x 640 x 4 B = 80 KB beside the table;
+    // else 8 x 1400 x 4 B = 44.8 KB per block, five blocks per SM (48 registers)
+    static constexpr int kStage = SMEM ? 640 : 1400;
 };
 
 struct RbArgs {
@@ -678,12 +680,26 @@ k_flop_rb(RbArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut p
     // takes fewer); else one unit per warp of the grid
     // every warp of the grid takes units warp, warp + W, ... (static: a
     // same-address ticket counter serialises in L2, ~one atomic per 15 ns)
-    for (int64_t u = int64_t(blockIdx.x) * Sh::kWarps + warp; u < units; u += int64_t(gridDim.x) * Sh::kWarps) {
+    const int64_t ustride = int64_t(gridDim.x) * Sh::kWarps;
+    int64_t u = int64_t(blockIdx.x) * Sh::kWarps + warp;
+    // the row bounds of the warp's next unit are loaded one unit ahead
+    int64_t rs_n = 0, re_n = 0;
+    if (u < units && u * kRbRows + lane < g.m) {
+        rs_n = __ldg(&g.arpt[u * kRbRows + lane]);
+        re_n = __ldg(&g.arpt[u * kRbRows + lane + 1]);
+    }
+    for (; u < units; u += ustride) {
         const int32_t r0 = static_cast<int32_t>(u * kRbRows);
         const int32_t r = r0 + lane;
         const int32_t rl = r0 + kRbRows < g.m ? r0 + kRbRows : g.m;  // rows [r0, rl)
-        const int64_t rs = r < g.m ? __ldg(&g.arpt[r]) : 0;
-        const int64_t re = r < g.m ? __ldg(&g.arpt[r + 1]) : 0;
+        const int64_t rs = rs_n, re = re_n;
+        {
+            const int64_t un = u + ustride, rn = un * kRbRows + lane;
+            if (un < units && rn < g.m) {
+                rs_n = __ldg(&g.arpt[rn]);
+                re_n = __ldg(&g.arpt[rn + 1]);
+            }
+        }
         // rows [j, jend) whose entries fit the staging area go together; a
         // row longer than the area goes alone, lane-strided
         int32_t j = r0;
@@ -712,15 +728,16 @@ k_flop_rb(RbArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut p
             }
             const int32_t jend = r0 + 32 - __clz(fit);  // rows [j, jend): a run of lanes
             const int64_t ne = __shfl_sync(0xffffffffu, re, jend - 1 - r0) - Ej;
-            // stage their columns: 16 loads in flight per lane per round
-            for (int64_t e = lane; e < ne; e += 32 * 16) {
-                int32_t c[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k)
-                    c[k] = e + 32 * k < ne ? ld_stream_i32(g.acol + Ej + e + 32 * k, first) : 0;
-#pragma unroll
-                for (int k = 0; k < 16; ++k)
-                    if (e + 32 * k < ne) stage[e + 32 * k] = c[k];
+            // stage their columns with asynchronous copies (every copy of the
+            // run in flight at once, no registers), coalesced across the warp
+            {
+                const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+                for (int64_t e = lane; e < ne; e += 32)
+                    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(
+                                     dst + 4 * static_cast<uint32_t>(e)),
+                                 "l"(g.acol + Ej + e), "l"(first)
+                                 : "memory");
+                asm volatile("cp.async.wait_all;" ::: "memory");
             }
             __syncwarp();
             if (r >= j && r < jend) {
