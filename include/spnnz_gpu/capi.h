@@ -187,6 +187,15 @@ int spnnz_gpu_run_prediction_with_plan(spnnz_gpu_ctx* ctx, const int32_t* rows, 
                                        int rows_residency, spnnz_report* report, int64_t* row_ceil,
                                        double* row_real, int out_residency);
 
+/* The predict step of the reference's harness (bench.hpp:187-195, the task
+ * its t_predict times): make_sample_plan + sampled_symbolic +
+ * collect_sample_stats + predict_reference + predict_proposed on the
+ * RESIDENT profile, in one call (the plan is drawn on the device; no per-row
+ * view).  report as run_prediction's; sample_rows (host, n entries) nullable.
+ * ESTATE without a profile. */
+int spnnz_gpu_predict_sampled(spnnz_gpu_ctx* ctx, uint64_t seed, double fraction, int64_t cap,
+                              spnnz_report* report, int32_t* sample_rows);
+
 /* ------------------------------------------- scalar estimators (host) */
 /* Same IEEE-double expressions as predict.hpp:86-89, :94-99, :109-123, :163-188. */
 double spnnz_sampled_cr(int64_t sampled_flop, int64_t sampled_nnz);

@@ -337,24 +337,21 @@ inline CaseResult run_case(Session& s, const TestCase& tc, std::uint64_t case_se
     SamplePlan plan;
     SampleStats st;
     double z1 = 0, z2 = 0;
+    // the reference's predict task (make_sample_plan + sampled_symbolic +
+    // collect_sample_stats + predict_reference + predict_proposed,
+    // bench.hpp:187-195) is one device call on the resident profile
     auto predict = [&] {
-        int64_t n = 0;
-        double p = 0;
-        detail::check(spnnz_gpu_make_sample_plan(s.ctx(), tc.a.rows, case_seed, cfg.policy.fraction,
-                                                 cfg.policy.cap, nullptr, SPNNZ_HOST, &n, &p));
-        plan.sample_rows.resize(static_cast<std::size_t>(n));
-        detail::check(spnnz_gpu_make_sample_plan(s.ctx(), tc.a.rows, case_seed, cfg.policy.fraction,
-                                                 cfg.policy.cap, plan.sample_rows.data(), SPNNZ_HOST,
-                                                 &plan.sample_num, &plan.p));
+        spnnz_report rep{};
+        detail::check(spnnz_gpu_predict_sampled(s.ctx(), case_seed, cfg.policy.fraction, cfg.policy.cap, &rep,
+                                                nullptr));
+        plan.sample_num = rep.sample_num;
+        plan.p = rep.p;
         plan.seed = case_seed;
-        const RowNnzResult smp = s.sampled_symbolic(plan.sample_rows);
-        detail::check(spnnz_gpu_sampled_flop(s.ctx(), plan.sample_rows.data(),
-                                             static_cast<int64_t>(plan.sample_rows.size()), SPNNZ_HOST,
-                                             &st.sampled_flop));
-        st.sampled_nnz = smp.total_nnz;
-        st.sampled_cr = spnnz_sampled_cr(st.sampled_flop, st.sampled_nnz);
-        z1 = predict_reference(st, plan);
-        z2 = predict_proposed(st, prof.total_flop).z2_star;
+        st.sampled_flop = rep.sampled_flop;
+        st.sampled_nnz = rep.sampled_nnz;
+        st.sampled_cr = rep.sampled_cr;
+        z1 = rep.z1_star;
+        z2 = rep.z2_star;
     };
     if (cfg.collect_timings) {
         r.t_flop = detail::wall_mean(flop, cfg.warmup, reps);

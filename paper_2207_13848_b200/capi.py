@@ -83,6 +83,7 @@ _SIGS = {
     "spnnz_gpu_last_timings": (c_int, [c_void_p, c_void_p, POINTER(c_int64)]),
     "spnnz_gpu_stream": (c_void_p, [c_void_p]),
     "spnnz_gpu_set_input_stream": (c_int, [c_void_p, c_void_p]),
+    "spnnz_gpu_predict_sampled": (c_int, [c_void_p, c_uint64, c_double, c_int64, POINTER(Report), c_void_p]),
     "spnnz_gpu_probe_flop_floor": (c_int, [c_void_p, c_int, POINTER(c_double), POINTER(c_double)]),
     "spnnz_gpu_check_guards": (c_int, [POINTER(c_int64), POINTER(c_int64)]),
 }

@@ -885,9 +885,14 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
 // F = profile.total_flop, one all-reduce of {f*, z*}, the per-row views of
 // the profile's flop.
 int pipeline_profile(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, int64_t* d_ceil,
-                     double* d_real, const spnnz_gpu_ctx::HeavySizes* known = nullptr) {
+                     double* d_real, const spnnz_gpu_ctx::HeavySizes* known = nullptr, bool draw = false,
+                     uint64_t seed = 0) {
     int64_t launches = 0;
     RC(settle_upload(c));
+    if (draw) {  // the plan drawn on the device into d_rows (= c->samples)
+        CU(launch_sample(seed, c->a_rows, n, c->samples.p, c->stream));
+        ++launches;
+    }
     // (a graph of this call re-reads h_init: it holds this profile's values
     // until the profile changes, which also drops the graph)
     for (int i = 0; i < kTotals; ++i) c->h_init[i] = 0;
@@ -1540,7 +1545,7 @@ int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, boo
         cudaGraph_t graph = nullptr;
         CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
         c->capturing = true;
-        int rc = with_profile ? pipeline_profile(c, d_rows, n, d_ceil, d_real, &known_v)
+        int rc = with_profile ? pipeline_profile(c, d_rows, n, d_ceil, d_real, &known_v, draw, seed)
                               : pipeline(c, d_rows, n, draw, seed, d_ceil, d_real, &known_v);
         c->capturing = false;
         const cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
@@ -1558,7 +1563,7 @@ int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, boo
         CU(cudaGraphLaunch(c->gexec, c->stream));
     } else {
         if (with_profile)
-            RC(pipeline_profile(c, d_rows, n, d_ceil, d_real, known));
+            RC(pipeline_profile(c, d_rows, n, d_ceil, d_real, known, draw, seed));
         else
             RC(pipeline(c, d_rows, n, draw, seed, d_ceil, d_real, known));
         c->last_eager = key;
@@ -1616,6 +1621,20 @@ int spnnz_gpu_run_prediction(spnnz_gpu_ctx* c, uint64_t seed, double fraction, i
         CU(cudaMemcpy(sample_rows, c->samples.p, 4 * size_t(n),
                       residency == SPNNZ_DEVICE ? cudaMemcpyDeviceToDevice
                                                 : cudaMemcpyDeviceToHost));
+    return SPNNZ_OK;
+}
+
+int spnnz_gpu_predict_sampled(spnnz_gpu_ctx* c, uint64_t seed, double fraction, int64_t cap,
+                              spnnz_report* rep, int32_t* sample_rows) {
+    RC(check_ctx(c));
+    if (c->a_cols != c->b_rows) return set_err(SPNNZ_EINVAL, "symbolic: A.cols != B.rows");
+    if (!c->profile_valid) return set_err(SPNNZ_ESTATE, "predict_sampled: no resident profile");
+    int64_t n = 0;
+    double p = 0;
+    RC(sample_count(c->a_rows, fraction, cap, &n, &p));
+    RC(c->samples.ensure(n));
+    RC(run_common(c, c->samples.p, n, p, true, seed, rep, nullptr, nullptr, SPNNZ_HOST, true));
+    if (sample_rows) CU(cudaMemcpy(sample_rows, c->samples.p, 4 * size_t(n), cudaMemcpyDeviceToHost));
     return SPNNZ_OK;
 }
 

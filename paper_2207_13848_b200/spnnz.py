@@ -337,6 +337,18 @@ class Predictor:
         r.plan.sample_num = len(rows)
         return r
 
+    def predict_sampled(self, seed: int, policy: SamplePolicy = SamplePolicy()) -> PredictionReport:
+        """make_sample_plan + sampled_symbolic + collect_sample_stats +
+        predict_reference + predict_proposed on the resident profile, one
+        device call (the reference harness's predict task, bench.hpp:187-195);
+        no per-row view."""
+        n, _ = plan_size(self.a_rows, policy)
+        rows = np.empty(n, np.int32)
+        rep = Report()
+        check(lib().spnnz_gpu_predict_sampled(self._ctx, seed, policy.fraction, policy.cap, ctypes.byref(rep),
+                                              rows.ctypes.data))
+        return _report(rep, None, None, rows, seed)
+
     # -- instrumentation
     def set_profiling(self, on: bool):
         check(lib().spnnz_gpu_set_profiling(self._ctx, int(on)))

@@ -518,6 +518,28 @@ def test_with_plan_hand_built_profiles(golden, api):
     P.close()
 
 
+def test_predict_sampled_equals_reference_task(golden):
+    """spnnz_gpu_predict_sampled (the harness's predict task in one call) gives
+    run_prediction's scalars for the same seed and policy (the reference's
+    run_prediction = compute_flop + make_sample_plan + run_prediction_with_plan),
+    on every repeat (cached sizes, graph replay)."""
+    for cfg in (1, 4):
+        info = gen.CONFIGS[cfg]
+        a, b = gen.make_config(cfg)
+        P = Predictor(0)
+        P.load(a, None if b is a else b)
+        pol = SamplePolicy(info["fraction"], UNCAPPED)
+        full = P.run_prediction(info["seed"], pol)
+        for _ in range(4):
+            r = P.predict_sampled(info["seed"], pol)
+            assert (r.stats.sampled_flop, r.stats.sampled_nnz, r.z1_star, r.z2_star, r.predicted_cr) == \
+                (full.stats.sampled_flop, full.stats.sampled_nnz, full.z1_star, full.z2_star, full.predicted_cr)
+            assert np.array_equal(r.plan.sample_rows, full.plan.sample_rows)
+        ref = golden["configs"][str(cfg)]["modes"]["uncapped"]["report"]
+        assert r.z2_star == ref["z2_star"] and r.stats.sampled_nnz == ref["sampled_nnz"]
+        P.close()
+
+
 def test_with_plan_uses_profile_not_a_flop_pass():
     """The free function hands the caller's profile through: a profile whose
     total differs from the matrices' moves Z2* exactly as the reference's

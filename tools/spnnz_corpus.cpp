@@ -6,6 +6,10 @@
 //   build/spnnz_corpus [--list FILE] [--csv OUT] [--json OUT] [--seed N]
 //                      [--reps N] [--warmup N] [--fraction F] [--cap N]
 //                      [--no-timings] [--device D]
+//   build/spnnz_corpus --overhead      the reference's overhead criterion
+//       (proj/tests/acceptance.cpp:264-294): three synthetic matrices, each
+//       with itself, case seed 97, 5 timed runs after 1 warm-up; mean
+//       (t_flop + t_predict) / t_exact against its 10 % gate
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -17,6 +21,7 @@ int main(int argc, char** argv) {
     using namespace spnnz::gpu;
     RunConfig cfg;
     std::string list, csv, json;
+    bool overhead = false;
     for (int i = 1; i < argc; ++i) {
         const std::string a = argv[i];
         auto next = [&]() -> std::string {
@@ -36,12 +41,37 @@ int main(int argc, char** argv) {
         else if (a == "--cap") cfg.policy.cap = std::stoll(next());
         else if (a == "--device") cfg.device = std::stoi(next());
         else if (a == "--no-timings") cfg.collect_timings = false;
+        else if (a == "--overhead") overhead = true;
         else {
             std::fprintf(stderr, "unknown argument %s\n", a.c_str());
             return 2;
         }
     }
     try {
+        if (overhead) {
+            // the three specs of acceptance.cpp:266-270, each matrix with itself
+            const char* specs[] = {"synth:uniform:150000x150000:nnz=8:seed=71",
+                                   "synth:banded:120000x120000:nnz=10:bw=60:seed=72",
+                                   "synth:uniform:200000x200000:nnz=6:seed=73"};
+            RunConfig oc = cfg;
+            oc.repetitions = 5;
+            oc.warmup = 1;
+            Session s(cfg.device);
+            double sum = 0.0;
+            for (const char* spec : specs) {
+                const NamedMatrix m = resolve_matrix_source(spec);
+                const TestCase tc = build_case(m.name, m.matrix, m.name, m.matrix);
+                const CaseResult r = run_case(s, tc, 97, oc);
+                const double f = (r.t_flop + r.t_predict) / r.t_exact;
+                std::printf("  M %d: t_flop %.6fs t_predict %.6fs t_exact %.6fs -> %.2f%%\n", tc.a.rows, r.t_flop,
+                            r.t_predict, r.t_exact, f * 100.0);
+                sum += f;
+            }
+            const double mean = sum / 3.0;
+            std::printf("%s overhead: mean (t_flop + t_predict)/t_exact = %.2f%% (gate 10%%)\n",
+                        mean <= 0.10 ? "PASS" : "FAIL", mean * 100.0);
+            return 0;
+        }
         std::vector<NamedMatrix> ms;
         if (list.empty()) {
             ms = default_corpus();
