@@ -95,9 +95,11 @@ int spnnz_gpu_synchronize(spnnz_gpu_ctx* ctx);
 int spnnz_gpu_host_alloc(size_t bytes, void** out);
 int spnnz_gpu_host_free(void* p);
 
-/* Host-only: nnz-balanced contiguous row shards, bounds[0..world] with
+/* Host-only: work-balanced contiguous row shards, bounds[0..world] with
  * bounds[0] = 0 and bounds[world] = rows; shard r = [bounds[r], bounds[r+1]).
- * bounds[r] = first row i with rpt[i] >= r*nnz/world (binary search). */
+ * Work of rows [0, i) = (rpt[i] - rpt[0]) + i (an entry and a row cost about
+ * the same in the FLOP and predict passes); bounds[r] = first row i whose
+ * work reaches r*(nnz + rows)/world (binary search). */
 int spnnz_gpu_partition_rows(const int64_t* rpt, int32_t rows, int world, int32_t* bounds);
 
 /* Upload A (this rank's shard) and B (replicated).  b == NULL or b == a means

@@ -274,7 +274,6 @@ struct spnnz_gpu_ctx {
     };
     cudaGraphExec_t gexec = nullptr;
     GraphKey gkey;
-    GraphKey last_eager;  // a key is captured on its second use (buffers sized by the first)
     int64_t g_launches = 0;
     HeavySizes g_known;
     long long* h_init = nullptr;  // pinned: initial totals of a profile-mode call (read by its graph)
@@ -1085,12 +1084,20 @@ int spnnz_gpu_host_free(void* p) {
 int spnnz_gpu_partition_rows(const int64_t* rpt, int32_t rows, int world, int32_t* bounds) {
     if (!rpt || !bounds || world < 1 || rows < 0)
         return set_err(SPNNZ_EINVAL, "partition_rows: bad arguments");
-    const int64_t nnz = rpt[rows] - rpt[0];
+    // balanced on nnz + rows: a row costs about what an entry does (its flop
+    // written, its offsets read, its prediction written vs one column read and
+    // one degree gather), and R-MAT's empty tail rows would otherwise pile
+    // onto the last rank (5.1 M of 16.8 M rows at N = 8 by nnz alone)
+    const int64_t work = rpt[rows] - rpt[0] + rows;
     bounds[0] = 0;
     for (int r = 1; r < world; ++r) {
-        const int64_t target = rpt[0] + nnz * r / world;
-        const int64_t* it = std::lower_bound(rpt, rpt + rows + 1, target);
-        int32_t b = static_cast<int32_t>(it - rpt);
+        const int64_t target = work / world * r + work % world * r / world;
+        int64_t lo = 0, hi = rows;  // first i with (rpt[i] - rpt[0]) + i >= target
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (rpt[mid] - rpt[0] + mid < target) lo = mid + 1; else hi = mid;
+        }
+        int32_t b = static_cast<int32_t>(lo);
         b = std::max(b, bounds[r - 1]);
         bounds[r] = std::min(b, rows);
     }
@@ -1537,36 +1544,63 @@ int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, boo
             c->profile_valid = true;
             c->profile_own = true;
         }
-    } else if (graphable && c->last_eager == key) {
-        if (c->gexec) {
-            cudaGraphExecDestroy(c->gexec);
-            c->gexec = nullptr;
-        }
-        cudaGraph_t graph = nullptr;
-        CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
-        c->capturing = true;
-        int rc = with_profile ? pipeline_profile(c, d_rows, n, d_ceil, d_real, &known_v, draw, seed)
-                              : pipeline(c, d_rows, n, draw, seed, d_ceil, d_real, &known_v);
-        c->capturing = false;
-        const cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
-        if (rc != SPNNZ_OK) {
-            if (graph) cudaGraphDestroy(graph);
-            return rc;
-        }
-        CU(ce);
-        const cudaError_t ie = cudaGraphInstantiate(&c->gexec, graph, 0);
-        cudaGraphDestroy(graph);
-        CU(ie);
-        c->gkey = key;
-        c->g_known = known_v;
-        c->g_launches = c->last_launches;
-        CU(cudaGraphLaunch(c->gexec, c->stream));
     } else {
-        if (with_profile)
-            RC(pipeline_profile(c, d_rows, n, d_ceil, d_real, known, draw, seed));
-        else
-            RC(pipeline(c, d_rows, n, draw, seed, d_ceil, d_real, known));
-        c->last_eager = key;
+        bool ran = false;
+        if (graphable) {
+            // capture on first use (buffers a first call must size are
+            // allocated during the relaxed-mode capture) and launch; a capture
+            // that fails for any reason falls back to the eager call below.
+            // The executable graph is updated in place when the topology
+            // allows (a new key with the same kernels), else re-instantiated.
+            cudaGraph_t graph = nullptr;
+            cudaError_t be = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed);
+            int rc = SPNNZ_ECUDA;
+            cudaError_t ce = be;
+            if (be == cudaSuccess) {
+                c->capturing = true;
+                rc = with_profile ? pipeline_profile(c, d_rows, n, d_ceil, d_real, &known_v, draw, seed)
+                                  : pipeline(c, d_rows, n, draw, seed, d_ceil, d_real, &known_v);
+                c->capturing = false;
+                ce = cudaStreamEndCapture(c->stream, &graph);
+            }
+            if (rc == SPNNZ_OK && ce == cudaSuccess && graph) {
+                cudaError_t ie = cudaErrorUnknown;
+                if (c->gexec) {
+                    cudaGraphExecUpdateResultInfo info;
+                    ie = cudaGraphExecUpdate(c->gexec, graph, &info);
+                    if (ie != cudaSuccess) {
+                        cudaGetLastError();
+                        cudaGraphExecDestroy(c->gexec);
+                        c->gexec = nullptr;
+                    }
+                }
+                if (!c->gexec) ie = cudaGraphInstantiate(&c->gexec, graph, 0);
+                cudaGraphDestroy(graph);
+                if (ie == cudaSuccess) {
+                    c->gkey = key;
+                    c->g_known = known_v;
+                    c->g_launches = c->last_launches;
+                    CU(cudaGraphLaunch(c->gexec, c->stream));
+                    ran = true;
+                } else {
+                    cudaGetLastError();
+                    c->gexec = nullptr;
+                }
+            } else {
+                if (graph) cudaGraphDestroy(graph);
+                cudaGetLastError();
+                if (c->gexec) {
+                    cudaGraphExecDestroy(c->gexec);
+                    c->gexec = nullptr;
+                }
+            }
+        }
+        if (!ran) {
+            if (with_profile)
+                RC(pipeline_profile(c, d_rows, n, d_ceil, d_real, known, draw, seed));
+            else
+                RC(pipeline(c, d_rows, n, draw, seed, d_ceil, d_real, known));
+        }
     }
     if (residency == SPNNZ_HOST && m) {
         if (row_ceil)
@@ -1584,7 +1618,6 @@ int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, boo
             cudaGraphExecDestroy(c->gexec);
             c->gexec = nullptr;
         }
-        c->last_eager = spnnz_gpu_ctx::GraphKey();
         if (const char* e = getenv("SPNNZ_STRICT_SIZES"))
             if (atoi(e) > 0) return set_err(SPNNZ_ECUDA, "heavy-row sizes known in advance were wrong");
         return run_common(c, d_rows, n, p, draw, seed, rep, row_ceil, row_real, residency, with_profile, true);

@@ -62,15 +62,16 @@ def partition(rpt, world):
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
-def test_partition_rows_is_nnz_balanced(world):
+def test_partition_rows_is_work_balanced(world):
     a = gen.rmat(14, 16 << 14, 0.57, 0.19, 0.19, 9)
     b = partition(a.rpt, world)
     assert b[0] == 0 and b[-1] == a.rows and (np.diff(b) >= 0).all()
-    nnz = a.nnz()
+    work = a.nnz() + a.rows
+    w = a.rpt + np.arange(a.rows + 1)  # work of rows [0, i): entries + rows
     for r in range(1, world):
-        # first row whose start offset reaches r*nnz/world
-        t = nnz * r // world
-        assert a.rpt[b[r]] >= t and (b[r] == 0 or a.rpt[b[r] - 1] < t)
+        # first row whose work reaches r*(nnz + rows)/world
+        t = work // world * r + work % world * r // world
+        assert w[b[r]] >= t and (b[r] == 0 or w[b[r] - 1] < t)
 
 
 def test_partition_edge_cases():

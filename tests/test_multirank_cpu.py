@@ -94,9 +94,9 @@ def test_two_rank_prediction_equals_single(cap):
     assert all(parts[i][1] == parts[i + 1][0] for i in range(len(parts) - 1))
     assert (np.concatenate([p[2] for p in parts]) == ceil).all()
     assert (np.concatenate([p[3] for p in parts]) == flop).all()
-    # the shards are nnz-balanced (within one row's worth)
-    nnz = [int(a.rpt[p[1]] - a.rpt[p[0]]) for p in parts]
-    assert abs(nnz[0] - nnz[1]) <= int(np.diff(a.rpt).max()) + 1
+    # the shards are balanced on nnz + rows (within one row's worth)
+    work = [int(a.rpt[p[1]] - a.rpt[p[0]]) + (p[1] - p[0]) for p in parts]
+    assert abs(work[0] - work[1]) <= int(np.diff(a.rpt).max()) + 2
 
 
 def flop_window(item_flop, rank, world):
