@@ -331,9 +331,14 @@ inline CaseResult run_case(Session& s, const TestCase& tc, std::uint64_t case_se
     s.load(tc.a, tc.b);
     const int reps = std::max(cfg.repetitions, 1);
     FlopProfile prof;
-    auto flop = [&] { prof = s.compute_flop(); };
+    // the profile and the exact per-row counts stay on the device (the report
+    // needs only their totals), so the timings are the device work plus one
+    // synchronizing call each -- no host copies of per-row arrays
+    auto flop = [&] {
+        detail::check(spnnz_gpu_compute_flop(s.ctx(), nullptr, SPNNZ_HOST, &prof.total_flop, &prof.max_flop_row));
+    };
     RowNnzResult exact;
-    auto ex = [&] { exact = s.exact_symbolic(); };
+    auto ex = [&] { detail::check(spnnz_gpu_exact_symbolic(s.ctx(), nullptr, SPNNZ_HOST, &exact.total_nnz)); };
     SamplePlan plan;
     SampleStats st;
     double z1 = 0, z2 = 0;

@@ -219,6 +219,7 @@ struct spnnz_gpu_ctx {
     bool b_intervals = false;  // interval heavy path requested (SPNNZ_HEAVY_INTERVALS=1)
     bool b_sorted = false;     // ... and B's rows checked non-decreasing at load
     bool rows_mode = false;    // banded A: the FLOP pass's row-per-thread tiles (checked at load)
+    bool tiers_beside = false; // the symbolic tiers run beside the FLOP pass (A/B knob SPNNZ_TIERS_BESIDE)
     int32_t a_rows = 0, a_cols = 0, b_rows = 0, b_cols = 0;
     int32_t row_lo = 0, row_hi = 0;
     int64_t b_nnz = 0;
@@ -509,9 +510,12 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     CU(cudaMemcpyAsync(c->h_counts, c->counts.p, sizeof(int32_t) * 16, cudaMemcpyDeviceToHost, bs));
     CU(cudaMemcpyAsync(c->h_meta, c->heavy_meta.p, sizeof(long long) * kHeavyMeta, cudaMemcpyDeviceToHost, bs));
     if (early) CU(cudaEventRecord(c->ev_bin, bs));
+    // the tiers wait for the FLOP pass (co-resident at config 5 both slow
+    // down: the tiers' shared tables shrink the L1 the gathers use) unless
+    // c->tiers_beside (small problems, where the FLOP pass is latency-bound)
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) {
         CU(cudaStreamWaitEvent(c->side[i], c->fork, 0));
-        if (early) CU(cudaStreamWaitEvent(c->side[i], c->ev_flop, 0));
+        if (early && !c->tiers_beside) CU(cudaStreamWaitEvent(c->side[i], c->ev_flop, 0));
     }
     CU(launch_sym_tiers(g, s, c->num_sms, c->side));
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaEventRecord(c->join[i], c->side[i]));
@@ -1225,6 +1229,8 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
             }
         }
         c->rows_mode = banded_rows(st[0], st[1], st[2]);
+        c->tiers_beside = false;
+        if (const char* e = getenv("SPNNZ_TIERS_BESIDE")) c->tiers_beside = atoi(e) > 0;  // A/B knob
         if (const char* e = getenv("SPNNZ_FLOP_ROWS")) c->rows_mode = atoi(e) > 0;  // A/B knob
     }
     // The interval heavy path (opt-in, SPNNZ_HEAVY_INTERVALS=1) needs B's rows

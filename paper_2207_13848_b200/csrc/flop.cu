@@ -459,6 +459,19 @@ __device__ __forceinline__ void flop_tile(TileSmem<BLOCK, V>& sm, const TileArgs
     //    loads when the tile is whole)
     const int i0 = tid * V;
     int32_t c[V];
+#if SPNNZ_FLOP_COLLOAD == 3
+    // 32-byte loads (sm_100 LDG.256): a thread's load is one whole sector, so
+    // the columns need no L1 merging and skip L1 (left to the degree lines)
+    if (n == TILE && (reinterpret_cast<uintptr_t>(g.acol + ts) & 31) == 0) {
+        const int32_t* src = g.acol + ts + i0;
+#pragma unroll
+        for (int k = 0; k < V / 8; ++k)
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                         : "=r"(c[8 * k]), "=r"(c[8 * k + 1]), "=r"(c[8 * k + 2]), "=r"(c[8 * k + 3]),
+                           "=r"(c[8 * k + 4]), "=r"(c[8 * k + 5]), "=r"(c[8 * k + 6]), "=r"(c[8 * k + 7])
+                         : "l"(src + 8 * k), "l"(first));
+    } else
+#endif
     if (n == TILE && (reinterpret_cast<uintptr_t>(g.acol + ts) & 15) == 0) {
         const int4* src = reinterpret_cast<const int4*>(g.acol + ts + i0);
 #pragma unroll
