@@ -607,6 +607,9 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
     mode.rows_mode = c->rows_mode;
     mode.num_sms = c->num_sms;
     if (const char* e = getenv("SPNNZ_FLOP_SMEM")) mode.no_smem = atoi(e) == 0;  // A/B knob
+    // degree tables of >= 8 M rows (16 MB) are gathered without L1 allocation
+    mode.gather_nol1 = !c->rows_mode && c->b_rows >= (int32_t(1) << 23);
+    if (const char* e = getenv("SPNNZ_FLOP_NOL1")) mode.gather_nol1 = atoi(e) > 0;  // A/B knob
     // row mode: L2-prefetch the columns one wave (8 blocks x SMs) ahead
     mode.prefetch_ahead = c->rows_mode ? 8 * c->num_sms : 0;
     if (const char* e = getenv("SPNNZ_FLOP_PREFETCH")) mode.prefetch_ahead = atoi(e);  // A/B knob

@@ -196,7 +196,7 @@ __device__ __forceinline__ uint16_t gather_deg(const uint16_t* p, uint64_t last)
 }
 
 #ifndef SPNNZ_FLOP_COLLOAD
-#define SPNNZ_FLOP_COLLOAD 1
+#define SPNNZ_FLOP_COLLOAD 3
 #endif
 // A.col loads: a thread's four 16-byte loads cover 64 contiguous bytes, 64 B
 // apart across lanes, so two loads share each 32-byte sector.  Allocating in
@@ -268,7 +268,16 @@ __device__ __forceinline__ Emit make_emit(const PredOut& p) {
 struct GlobalDeg {
     const uint16_t* deg;
     uint64_t last;
-    __device__ __forceinline__ int32_t operator()(int32_t c) const { return gather_deg(deg + c, last); }
+    bool nol1;  // a table far larger than L1 (config 5: 32 MB): gathers skip L1 allocation
+    __device__ __forceinline__ int32_t operator()(int32_t c) const {
+        if (nol1) {
+            unsigned short v;
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
+                         : "=h"(v) : "l"(deg + c), "l"(last));
+            return v;
+        }
+        return gather_deg(deg + c, last);
+    }
 };
 struct SharedDeg {
     const uint16_t* deg;  // shared window
@@ -309,6 +318,7 @@ struct TileArgs {
     long long* __restrict__ tile_total;
     long long* __restrict__ tile_max;
     int prefetch_ahead;  // k_flop: L2-prefetch the columns of tile t + this (0: off)
+    bool gather_nol1;    // degree gathers without L1 allocation (FlopMode::gather_nol1)
 };
 
 // The exact degree of B row c given its uint16 entry (0xFFFF: look it up).
@@ -592,8 +602,8 @@ k_flop(TileArgs g, const uint16_t* __restrict__ bdeg, PredOut pred, int64_t t0) 
     if (PRED) emit = make_emit(pred);
     if (g.prefetch_ahead && threadIdx.x == 0 && blockIdx.x + g.prefetch_ahead < gridDim.x)
         prefetch_tile(g, t0 + blockIdx.x + g.prefetch_ahead);
-    flop_tile<BLOCK, V, PRED, ROWS>(sm, g, t0 + blockIdx.x, threadIdx.x, GlobalDeg{bdeg, policy_evict_last()},
-                                    BlockBar{}, emit);
+    flop_tile<BLOCK, V, PRED, ROWS>(sm, g, t0 + blockIdx.x, threadIdx.x,
+                                    GlobalDeg{bdeg, policy_evict_last(), g.gather_nol1}, BlockBar{}, emit);
 }
 
 // Persistent blocks of G tile groups (G x 128 threads, one block per SM) with
@@ -1226,6 +1236,7 @@ static TileArgs tile_args(const DevCsr& a, const int64_t* brpt, const FlopScratc
     g.tile_total = s.tile_total;
     g.tile_max = s.tile_max;
     g.prefetch_ahead = mode.prefetch_ahead;
+    g.gather_nol1 = mode.gather_nol1;
     return g;
 }
 

@@ -54,6 +54,13 @@ constexpr int kTaskSpanShift = SPNNZ_SPAN_SHIFT;  // R > 1: task spans of <= 2^1
 constexpr int kPrivRanges = 256;          // per-warp histograms up to this R
 constexpr int kMaxRanges = 4096;          // B.cols < 2^31 with W = 2^19
 constexpr int64_t kTaskProducts = 131072;
+// A/B knob: bitmap inserts that read the word first and skip the atomic when
+// the bit is already set (a duplicate product).  Measured slower (config 2
+// symbolic 299 vs 282 us, where 57 % of the products are duplicates), so off.
+#ifndef SPNNZ_BITMAP_TEST
+#define SPNNZ_BITMAP_TEST 0
+#endif
+constexpr bool kTestFirst = SPNNZ_BITMAP_TEST != 0;
 constexpr int64_t kSmallTaskProducts = 2048;  // ranges this small go to k_heavy_run_small
 
 struct HeavyTask {
@@ -628,7 +635,8 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
                 for (int u = 0; u < kUnroll; ++u)
                     if (valid[u]) {
                         const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
-                        atomicOr(&s_set[off >> 5], 1u << (off & 31));
+                        const uint32_t bit = 1u << (off & 31);
+                        if (!kTestFirst || !(s_set[off >> 5] & bit)) atomicOr(&s_set[off >> 5], bit);
                     }
                 return;
             }
@@ -637,7 +645,7 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
                 if (valid[u]) {
                     const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
                     const uint32_t bit = 1u << (off & 31);
-                    cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
+                    if (!kTestFirst || !(s_set[off >> 5] & bit)) cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
                 }
         };
         // the span's keys: 16-byte vectors over the aligned body, two vectors
@@ -761,7 +769,7 @@ __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, Sym
                 if (valid[u]) {
                     const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
                     const uint32_t bit = 1u << (off & 31);
-                    cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
+                    if (!kTestFirst || !(s_set[off >> 5] & bit)) cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
                 }
         };
         for (long long u0 = t.a; u0 < t.b; u0 += kRunBlock) {

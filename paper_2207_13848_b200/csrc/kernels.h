@@ -88,6 +88,10 @@ struct FlopMode {
     bool rows_mode = false;
     bool no_smem = false;  // A/B knob: keep the degree table in global memory
     int prefetch_ahead = 0;  // k_flop: L2-prefetch the columns this many tiles ahead (0: off)
+    // k_flop: degree gathers skip L1 allocation -- for degree tables far
+    // larger than L1 with no locality to keep (config 5: -1.8 %; config 2's
+    // 2 MB table gains from L1 hits: +80 % without them)
+    bool gather_nol1 = false;
     unsigned long long* sched = nullptr;  // k_flop_smem's tile tickets: 2 zeroed words, left zeroed
     int num_sms = 148;
 };
