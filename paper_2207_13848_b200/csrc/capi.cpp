@@ -583,6 +583,13 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     return SPNNZ_OK;
 }
 
+// Degree tables of >= 8 M rows (16 MB) are gathered without L1 allocation.
+bool flop_gather_nol1(const spnnz_gpu_ctx* c) {
+    bool v = !c->rows_mode && c->b_rows >= (int32_t(1) << 23);
+    if (const char* e = getenv("SPNNZ_FLOP_NOL1")) v = atoi(e) > 0;  // A/B knob
+    return v;
+}
+
 // FLOP pass of the local rows into `out` (default: the resident profile).
 int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr,
               const PredOut& pred = PredOut(), DBuf<int64_t>* out = nullptr) {
@@ -607,9 +614,7 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
     mode.rows_mode = c->rows_mode;
     mode.num_sms = c->num_sms;
     if (const char* e = getenv("SPNNZ_FLOP_SMEM")) mode.no_smem = atoi(e) == 0;  // A/B knob
-    // degree tables of >= 8 M rows (16 MB) are gathered without L1 allocation
-    mode.gather_nol1 = !c->rows_mode && c->b_rows >= (int32_t(1) << 23);
-    if (const char* e = getenv("SPNNZ_FLOP_NOL1")) mode.gather_nol1 = atoi(e) > 0;  // A/B knob
+    mode.gather_nol1 = flop_gather_nol1(c);
     // row mode: L2-prefetch the columns one wave (8 blocks x SMs) ahead
     mode.prefetch_ahead = c->rows_mode ? 8 * c->num_sms : 0;
     if (const char* e = getenv("SPNNZ_FLOP_PREFETCH")) mode.prefetch_ahead = atoi(e);  // A/B knob
@@ -1744,9 +1749,11 @@ int spnnz_gpu_probe_flop_floor(spnnz_gpu_ctx* c, int reps, double* stream_ms, do
     CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, c->stream));
     double* res[2] = {stream_ms, gather_ms};
     for (int g = 0; g < 2; ++g) {
-        CU(launch_pattern(c->a, c->deg.p, g == 1, out.p, c->stream));  // warm-up
+        // the loads of the tile kernel the FLOP pass would pick for this matrix
+        const bool nol1 = flop_gather_nol1(c);
+        CU(launch_pattern(c->a, c->deg.p, g == 1, nol1, out.p, c->stream));  // warm-up
         CU(cudaEventRecord(c->ev[0], c->stream));
-        for (int i = 0; i < reps; ++i) CU(launch_pattern(c->a, c->deg.p, g == 1, out.p, c->stream));
+        for (int i = 0; i < reps; ++i) CU(launch_pattern(c->a, c->deg.p, g == 1, nol1, out.p, c->stream));
         CU(cudaEventRecord(c->ev[1], c->stream));
         CU(cudaEventSynchronize(c->ev[1]));
         float ms = 0;

@@ -265,12 +265,15 @@ __device__ __forceinline__ Emit make_emit(const PredOut& p) {
 // Degree sources: the uint16 degree array in global memory (L2-resident,
 // gathered under evict_last) or a copy of it in shared memory (B with few
 // rows: config 4's 65536 rows are a 128 KB table).  0xFFFF escapes to B.rpt.
+// NOL1: a table far larger than L1 (config 5: 32 MB): gathers skip L1
+// allocation (a compile-time choice: a runtime branch around the 16 gathers
+// cost 5 % at config 5)
+template <bool NOL1 = false>
 struct GlobalDeg {
     const uint16_t* deg;
     uint64_t last;
-    bool nol1;  // a table far larger than L1 (config 5: 32 MB): gathers skip L1 allocation
     __device__ __forceinline__ int32_t operator()(int32_t c) const {
-        if (nol1) {
+        if (NOL1) {
             unsigned short v;
             asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
                          : "=h"(v) : "l"(deg + c), "l"(last));
@@ -318,7 +321,6 @@ struct TileArgs {
     long long* __restrict__ tile_total;
     long long* __restrict__ tile_max;
     int prefetch_ahead;  // k_flop: L2-prefetch the columns of tile t + this (0: off)
-    bool gather_nol1;    // degree gathers without L1 allocation (FlopMode::gather_nol1)
 };
 
 // The exact degree of B row c given its uint16 entry (0xFFFF: look it up).
@@ -594,7 +596,7 @@ __device__ __forceinline__ void flop_tile(TileSmem<BLOCK, V>& sm, const TileArgs
 
 // One block per tile, degrees gathered from global memory (L2).
 // (row mode holds a row's 16 gathers in flight: 64 registers, 8 blocks per SM)
-template <int BLOCK, int V, bool PRED, bool ROWS>
+template <int BLOCK, int V, bool PRED, bool ROWS, bool NOL1>
 __global__ void __launch_bounds__(BLOCK, ROWS ? 8 : (SPNNZ_FLOP_MINB / BLOCK < 32 ? SPNNZ_FLOP_MINB / BLOCK : 32))
 k_flop(TileArgs g, const uint16_t* __restrict__ bdeg, PredOut pred, int64_t t0) {
     __shared__ TileSmem<BLOCK, V> sm;
@@ -602,8 +604,8 @@ k_flop(TileArgs g, const uint16_t* __restrict__ bdeg, PredOut pred, int64_t t0) 
     if (PRED) emit = make_emit(pred);
     if (g.prefetch_ahead && threadIdx.x == 0 && blockIdx.x + g.prefetch_ahead < gridDim.x)
         prefetch_tile(g, t0 + blockIdx.x + g.prefetch_ahead);
-    flop_tile<BLOCK, V, PRED, ROWS>(sm, g, t0 + blockIdx.x, threadIdx.x,
-                                    GlobalDeg{bdeg, policy_evict_last(), g.gather_nol1}, BlockBar{}, emit);
+    flop_tile<BLOCK, V, PRED, ROWS>(sm, g, t0 + blockIdx.x, threadIdx.x, GlobalDeg<NOL1>{bdeg, policy_evict_last()},
+                                    BlockBar{}, emit);
 }
 
 // Persistent blocks of G tile groups (G x 128 threads, one block per SM) with
@@ -1040,28 +1042,27 @@ __global__ void k_locality(const int64_t* __restrict__ rpt, const int32_t* __res
 // floor its access pattern sets on this matrix): 16 consecutive A.col entries
 // per thread (the k_flop loads) and, with GATHER, their 16 degree gathers;
 // one int64 written per thread so nothing is dead code.
-template <bool GATHER>
+template <bool GATHER, bool NOL1>
 __global__ void __launch_bounds__(128, 10) k_pattern(const int32_t* __restrict__ col, int64_t base, int64_t nnz,
                                                    const uint16_t* __restrict__ deg, long long* __restrict__ out) {
     const uint64_t first = policy_evict_first(), last = policy_evict_last();
     const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    const int64_t e0 = ((base + 3) & ~int64_t(3)) + t * 16;
+    const int64_t e0 = ((base + 7) & ~int64_t(7)) + t * 16;
     if (e0 + 16 > base + nnz) return;
-    const int4* src = reinterpret_cast<const int4*>(col + e0);
     int32_t c[16];
+    // the tile kernel's loads: two 32-byte L1-bypassing loads per thread
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int4 x = load_cols(src + k, first);
-        c[4 * k] = x.x;
-        c[4 * k + 1] = x.y;
-        c[4 * k + 2] = x.z;
-        c[4 * k + 3] = x.w;
-    }
+    for (int k = 0; k < 2; ++k)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                     : "=r"(c[8 * k]), "=r"(c[8 * k + 1]), "=r"(c[8 * k + 2]), "=r"(c[8 * k + 3]),
+                       "=r"(c[8 * k + 4]), "=r"(c[8 * k + 5]), "=r"(c[8 * k + 6]), "=r"(c[8 * k + 7])
+                     : "l"(col + e0 + 8 * k), "l"(first));
     long long s = 0;
     if (GATHER) {
+        const GlobalDeg<NOL1> dg{deg, last};
         int32_t d[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) d[k] = gather_deg(deg + c[k], last);
+        for (int k = 0; k < 16; ++k) d[k] = dg(c[k]);
 #pragma unroll
         for (int k = 0; k < 16; ++k) s += d[k];
     } else {
@@ -1073,14 +1074,17 @@ __global__ void __launch_bounds__(128, 10) k_pattern(const int32_t* __restrict__
 
 }  // namespace
 
-cudaError_t launch_pattern(const DevCsr& a, const uint16_t* deg, bool gather, long long* out, cudaStream_t stream) {
+cudaError_t launch_pattern(const DevCsr& a, const uint16_t* deg, bool gather, bool nol1, long long* out,
+                           cudaStream_t stream) {
     const int64_t threads = a.nnz / 16;
     if (threads < 1) return cudaSuccess;
     const unsigned grid = static_cast<unsigned>((threads + 127) / 128);
-    if (gather)
-        k_pattern<true><<<grid, 128, 0, stream>>>(a.col, a.base, a.nnz, deg, out);
+    if (gather && nol1)
+        k_pattern<true, true><<<grid, 128, 0, stream>>>(a.col, a.base, a.nnz, deg, out);
+    else if (gather)
+        k_pattern<true, false><<<grid, 128, 0, stream>>>(a.col, a.base, a.nnz, deg, out);
     else
-        k_pattern<false><<<grid, 128, 0, stream>>>(a.col, a.base, a.nnz, deg, out);
+        k_pattern<false, false><<<grid, 128, 0, stream>>>(a.col, a.base, a.nnz, deg, out);
     return cudaGetLastError();
 }
 
@@ -1236,11 +1240,10 @@ static TileArgs tile_args(const DevCsr& a, const int64_t* brpt, const FlopScratc
     g.tile_total = s.tile_total;
     g.tile_max = s.tile_max;
     g.prefetch_ahead = mode.prefetch_ahead;
-    g.gather_nol1 = mode.gather_nol1;
     return g;
 }
 
-template <bool PRED, bool ROWS>
+template <bool PRED, bool ROWS, bool NOL1 = false>
 static cudaError_t launch_tiles(const TileArgs& g, const uint16_t* bdeg, int64_t t_begin, int64_t t_end,
                                 cudaStream_t stream, const PredOut& pred, const FlopMode& mode) {
     if (flop_smem_fits(mode.b_rows) && !mode.no_smem) {
@@ -1258,7 +1261,7 @@ static cudaError_t launch_tiles(const TileArgs& g, const uint16_t* bdeg, int64_t
         k_flop_smem<kFlopIpt, PRED, ROWS><<<static_cast<unsigned>(grid), kFlopBlock * kSmemGroups, smem, stream>>>(
             g, bdeg, mode.b_rows, pred, t_begin, t_end, mode.sched);
     } else {
-        k_flop<kFlopBlock, kFlopIpt, PRED, ROWS><<<static_cast<unsigned>(t_end - t_begin), kFlopBlock, 0, stream>>>(
+        k_flop<kFlopBlock, kFlopIpt, PRED, ROWS, NOL1><<<static_cast<unsigned>(t_end - t_begin), kFlopBlock, 0, stream>>>(
             g, bdeg, pred, t_begin);
     }
     return cudaGetLastError();
@@ -1272,6 +1275,9 @@ cudaError_t launch_flop_tiles(const DevCsr& a, const uint16_t* bdeg, const int64
     if (mode.rows_mode)
         return pred.on() ? launch_tiles<true, true>(g, bdeg, t_begin, t_end, stream, pred, mode)
                          : launch_tiles<false, true>(g, bdeg, t_begin, t_end, stream, pred, mode);
+    if (mode.gather_nol1)
+        return pred.on() ? launch_tiles<true, false, true>(g, bdeg, t_begin, t_end, stream, pred, mode)
+                         : launch_tiles<false, false, true>(g, bdeg, t_begin, t_end, stream, pred, mode);
     return pred.on() ? launch_tiles<true, false>(g, bdeg, t_begin, t_end, stream, pred, mode)
                      : launch_tiles<false, false>(g, bdeg, t_begin, t_end, stream, pred, mode);
 }

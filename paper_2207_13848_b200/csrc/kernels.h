@@ -110,7 +110,8 @@ cudaError_t launch_locality(const int64_t* rpt, const int32_t* col, int32_t lo, 
 constexpr int kLocalitySamples = 4096;
 // Instrumentation: the FLOP pass's A.col stream (and, with gather, its degree
 // gathers) without the row logic; out needs nnz / 16 entries.
-cudaError_t launch_pattern(const DevCsr& a, const uint16_t* deg, bool gather, long long* out, cudaStream_t stream);
+cudaError_t launch_pattern(const DevCsr& a, const uint16_t* deg, bool gather, bool nol1, long long* out,
+                           cudaStream_t stream);
 // rows_mode when most sampled consecutive rows advance like a stencil's
 inline bool banded_rows(int pairs, int advancing, int short_rows) {
     return pairs >= 64 && advancing * 4 >= pairs * 3 && short_rows * 20 >= pairs * 19;
