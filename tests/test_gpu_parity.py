@@ -892,6 +892,39 @@ def test_device_residency_matches_host(P):
     assert rep2.z2_star == host.z2_star and (rep2.predicted_row_nnz_ceil == host.predicted_row_nnz_ceil).all()
 
 
+def test_device_inputs_produced_on_a_side_stream():
+    """Device inputs an asynchronous kernel writes on a torch side stream are
+    read after it (spnnz_gpu_set_input_stream, set from torch's current
+    stream): sample rows, a profile and the matrices themselves, each written
+    by a queued kernel right before the call."""
+    import torch
+    a, b = gen.make_config(4)
+    P = Predictor(0)
+    P.load(a, b)
+    prof = P.compute_flop()
+    rows_h = P.make_sample_plan(a.rows, 4, SamplePolicy(0.005, UNCAPPED)).sample_rows
+    ref = P.sampled_symbolic(rows_h)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(20_000_000)  # keep the side stream busy
+        rows_d = torch.from_numpy(rows_h.astype(np.int64)).cuda(non_blocking=True).to(torch.int32)
+        got = P.sampled_symbolic(rows_d)
+        assert got.total_nnz == ref.total_nnz
+        assert np.array_equal(got.nnz_per_row.cpu().numpy(), ref.nnz_per_row)
+        torch.cuda._sleep(20_000_000)
+        flop_d = torch.from_numpy(prof.flop_per_row).cuda(non_blocking=True)
+        P.set_profile(spnnz.FlopProfile(flop_d, prof.total_flop, prof.max_flop_row))
+        assert P.sampled_flop(rows_h) == int(prof.flop_per_row[rows_h.astype(np.int64)].sum())
+        torch.cuda._sleep(20_000_000)
+        ta = type("M", (), dict(rows=a.rows, cols=a.cols, rpt=torch.from_numpy(a.rpt).cuda(non_blocking=True),
+                                col=torch.from_numpy(a.col).cuda(non_blocking=True)))()
+        tb = type("M", (), dict(rows=b.rows, cols=b.cols, rpt=torch.from_numpy(b.rpt).cuda(non_blocking=True),
+                                col=torch.from_numpy(b.col).cuda(non_blocking=True)))()
+        P.load(ta, tb)
+        assert P.compute_flop().total_flop == prof.total_flop
+    P.close()
+
+
 def test_cpp_dropin_header():
     """include/spnnz_gpu/spnnz_gpu.hpp: the reference's known answers through
     the C++ mirror (tests/cpp/test_dropin.cpp)."""
