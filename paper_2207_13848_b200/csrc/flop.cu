@@ -654,6 +654,12 @@ k_flop_smem(TileArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredO
 // The degree table is in shared memory when B's rows fit (SMEM), else the
 // L2-resident uint16 array.
 constexpr int kRbRows = 32;
+#ifndef SPNNZ_RB_STAGE
+#define SPNNZ_RB_STAGE 1100
+#endif
+#ifndef SPNNZ_RB_MINB
+#define SPNNZ_RB_MINB 6
+#endif
 template <bool SMEM>
 struct RbShape {
     // SMEM: one 1024-thread block per SM beside the degree table; else
@@ -661,8 +667,9 @@ struct RbShape {
     static constexpr int kThreads = SMEM ? 1024 : 256;
     static constexpr int kWarps = kThreads / 32;
     // entries staged per warp: SMEM 32 x 640 x 4 B = 80 KB beside the table;
-    // else 8 x 1400 x 4 B = 44.8 KB per block, five blocks per SM (48 registers)
-    static constexpr int kStage = SMEM ? 640 : 1400;
+    // else 8 x 1100 x 4 B = 35.2 KB per block, six blocks (48 warps) per SM
+    static constexpr int kStage = SMEM ? 640 : SPNNZ_RB_STAGE;
+    static constexpr int kMinBlocks = SMEM ? 1 : SPNNZ_RB_MINB;
 };
 
 struct RbArgs {
@@ -675,7 +682,7 @@ struct RbArgs {
 };
 
 template <bool SMEM, bool PRED>
-__global__ void __launch_bounds__(RbShape<SMEM>::kThreads, 1)
+__global__ void __launch_bounds__(RbShape<SMEM>::kThreads, RbShape<SMEM>::kMinBlocks)
 k_flop_rb(RbArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut pred,
           unsigned long long* __restrict__ sched) {
     using Sh = RbShape<SMEM>;
