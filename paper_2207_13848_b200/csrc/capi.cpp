@@ -615,6 +615,7 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
     mode.num_sms = c->num_sms;
     if (const char* e = getenv("SPNNZ_FLOP_SMEM")) mode.no_smem = atoi(e) == 0;  // A/B knob
     mode.gather_nol1 = flop_gather_nol1(c);
+    if (const char* e = getenv("SPNNZ_RB_PERSIST")) mode.rb_persistent = atoi(e) > 0;  // A/B knob
     // row mode: L2-prefetch the columns one wave (8 blocks x SMs) ahead
     mode.prefetch_ahead = c->rows_mode ? 8 * c->num_sms : 0;
     if (const char* e = getenv("SPNNZ_FLOP_PREFETCH")) mode.prefetch_ahead = atoi(e);  // A/B knob

@@ -688,10 +688,10 @@ k_flop_rb(RbArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut p
     using Sh = RbShape<SMEM>;
     extern __shared__ __align__(16) unsigned char s_raw[];
     int32_t* stage_all = reinterpret_cast<int32_t*>(s_raw);
-    const uint16_t* s_deg = reinterpret_cast<const uint16_t*>(s_raw + size_t(Sh::kWarps) * Sh::kStage * 4);
+    const uint16_t* s_deg = reinterpret_cast<const uint16_t*>(s_raw + size_t(Sh::kWarps) * (Sh::kStage + 4) * 4);
     __shared__ long long s_sum[Sh::kWarps], s_max[Sh::kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int32_t* stage = stage_all + warp * Sh::kStage;
+    int32_t* stage = stage_all + warp * (Sh::kStage + 4);  // (+ 4: the alignment shift)
     const uint64_t first = policy_evict_first(), last = policy_evict_last();
     if (SMEM) {
         uint16_t* d = const_cast<uint16_t*>(s_deg);
@@ -761,20 +761,36 @@ k_flop_rb(RbArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut p
             const int32_t jend = r0 + 32 - __clz(fit);  // rows [j, jend): a run of lanes
             const int64_t ne = __shfl_sync(0xffffffffu, re, jend - 1 - r0) - Ej;
             // stage their columns with asynchronous copies (every copy of the
-            // run in flight at once, no registers), coalesced across the warp
+            // run in flight at once, no registers), coalesced across the warp:
+            // 16-byte L1-bypassing copies over the aligned body (entry e goes
+            // to stage[sh + e - Ej], sh making the body's destinations 16-byte
+            // aligned), 4-byte copies for the ragged head and tail
+            int sh;
             {
                 const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
-                for (int64_t e = lane; e < ne; e += 32)
+                const int head0 = static_cast<int>(((16 - (reinterpret_cast<uintptr_t>(g.acol + Ej) & 15)) & 15) >> 2);
+                const int h = head0 < ne ? head0 : static_cast<int>(ne);
+                sh = (4 - h) & 3;
+                const int nb = static_cast<int>((ne - h) >> 2);
+                const int tail = static_cast<int>(ne - h - 4 * nb);
+                if (lane < h + tail) {  // head and tail entries
+                    const int e = lane < h ? lane : h + 4 * nb + (lane - h);
                     asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(
-                                     dst + 4 * static_cast<uint32_t>(e)),
+                                     dst + 4u * static_cast<uint32_t>(sh + e)),
                                  "l"(g.acol + Ej + e), "l"(first)
+                                 : "memory");
+                }
+                for (int cch = lane; cch < nb; cch += 32)
+                    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
+                                     dst + 4u * static_cast<uint32_t>(sh + h + 4 * cch)),
+                                 "l"(g.acol + Ej + h + 4 * cch), "l"(first)
                                  : "memory");
                 asm volatile("cp.async.wait_all;" ::: "memory");
             }
             __syncwarp();
             if (r >= j && r < jend) {
                 long long sum = 0;
-                const int i0 = static_cast<int>(rs - Ej), i1 = static_cast<int>(re - Ej);
+                const int i0 = sh + static_cast<int>(rs - Ej), i1 = sh + static_cast<int>(re - Ej);
                 for (int i = i0; i < i1; i += 8) {
                     int32_t cc[8], d[8];
 #pragma unroll
@@ -1293,7 +1309,7 @@ template <bool SMEM, bool PRED>
 static cudaError_t launch_rb(const RbArgs& g, const uint16_t* bdeg, int32_t k_rows, const PredOut& pred,
                              const FlopMode& mode, cudaStream_t stream) {
     using Sh = RbShape<SMEM>;
-    const size_t smem = size_t(Sh::kWarps) * Sh::kStage * 4 + (SMEM ? ((size_t(k_rows) * 2 + 15) & ~size_t(15)) : 0);
+    const size_t smem = size_t(Sh::kWarps) * (Sh::kStage + 4) * 4 + (SMEM ? ((size_t(k_rows) * 2 + 15) & ~size_t(15)) : 0);
     static std::atomic<unsigned long long> attr_done{0};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1303,8 +1319,11 @@ static cudaError_t launch_rb(const RbArgs& g, const uint16_t* bdeg, int32_t k_ro
         attr_done.fetch_or(1ull << (dev & 63), std::memory_order_release);
     }
     const int64_t units = (int64_t(g.m) + kRbRows - 1) / kRbRows;
+    // persistent: one wave of blocks, every warp striding over the units (the
+    // next unit's row bounds are loaded while the current one is summed)
     int64_t grid = (units + Sh::kWarps - 1) / Sh::kWarps;
-    if (SMEM && grid > mode.num_sms) grid = mode.num_sms;
+    const int64_t wave = int64_t(mode.num_sms) * Sh::kMinBlocks;
+    if (grid > wave && (SMEM || mode.rb_persistent)) grid = wave;
     if (grid < 1) grid = 1;
     k_flop_rb<SMEM, PRED><<<static_cast<unsigned>(grid), Sh::kThreads, smem, stream>>>(g, bdeg, k_rows, pred,
                                                                                        mode.sched);
@@ -1313,7 +1332,7 @@ static cudaError_t launch_rb(const RbArgs& g, const uint16_t* bdeg, int32_t k_ro
 
 bool flop_rb_smem_fits(int32_t k_rows) {
     using Sh = RbShape<true>;
-    return k_rows > 0 && size_t(Sh::kWarps) * Sh::kStage * 4 + ((size_t(k_rows) * 2 + 15) & ~size_t(15)) +
+    return k_rows > 0 && size_t(Sh::kWarps) * (Sh::kStage + 4) * 4 + ((size_t(k_rows) * 2 + 15) & ~size_t(15)) +
                              kSmemStatic <= 227 * 1024;
 }
 

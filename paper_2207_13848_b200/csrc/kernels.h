@@ -93,6 +93,7 @@ struct FlopMode {
     // 2 MB table gains from L1 hits: +80 % without them)
     bool gather_nol1 = false;
     unsigned long long* sched = nullptr;  // k_flop_smem's tile tickets: 2 zeroed words, left zeroed
+    bool rb_persistent = true;  // k_flop_rb with L2 degrees: one wave of persistent blocks (A/B knob)
     int num_sms = 148;
 };
 bool flop_smem_fits(int32_t k_rows);

@@ -121,9 +121,9 @@ FLOP_KERNELS = {"tiles-smem": ("0", "1"), "tiles-global": ("0", "0"), "rb-smem":
                 "rb-global": ("1", "0")}
 
 
-# largest K whose degree table fits beside the row-block staging (74752) and
+# largest K whose degree table fits beside the row-block staging (74496) and
 # beside the tile groups (81280), and one more of each
-@pytest.mark.parametrize("k", [74752, 74753, 81280, 81281])
+@pytest.mark.parametrize("k", [74496, 74497, 81280, 81281])
 @pytest.mark.parametrize("kernel", list(FLOP_KERNELS))
 def test_flop_degree_table_threshold(oracle, monkeypatch, k, kernel):
     """The shared-memory degree tables (persistent row-block and tile-group
