@@ -285,6 +285,7 @@ struct spnnz_gpu_ctx {
     DBuf<int32_t> tile_x;
     DBuf<unsigned long long> flop_sched;  // k_flop_smem tile tickets (zeroed once, kept zero)
     DBuf<uint16_t> deg;  // uint16 row lengths of B (rebuilt every FLOP pass)
+    DBuf<unsigned> deg_escapes;  // 1 when some B row has >= 65535 entries (row-block kernels)
     DBuf<long long> tile_carry, tile_total, tile_max;
     DBuf<long long> totals;
     DBuf<long long> totals_table;  // world x kTotals: the all-reduce's all-gather table
@@ -656,8 +657,10 @@ int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr
     if (const char* e = getenv("SPNNZ_FLOP_RB")) rb = atoi(e) > 0;  // A/B knob
     if (rb) {
         int64_t nk = 0;
-        CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, stream, nullptr, nullptr, &nk));
-        CU(launch_flop_rows(a, c->deg.p, c->b_rpt.p, out->p, c->totals.p, stream, pred, mode));
+        RC(c->deg_escapes.ensure(1));
+        CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, stream, nullptr, nullptr, &nk,
+                         c->deg_escapes.p));
+        CU(launch_flop_rows(a, c->deg.p, c->b_rpt.p, out->p, c->totals.p, stream, pred, mode, c->deg_escapes.p));
         *launches += a.rows ? nk + 1 : 0;
         return SPNNZ_OK;
     }

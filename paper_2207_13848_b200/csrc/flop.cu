@@ -96,7 +96,8 @@ __device__ __forceinline__ void degree_row(const TileMarks& mk, uint16_t* deg, i
 // one 8-byte load, all issued before any store, then one 8-byte store of the
 // four degrees (the marking branch would otherwise serialise the loads).
 __global__ void k_degree(const int64_t* __restrict__ brpt, int64_t k_rows,
-                         uint16_t* __restrict__ deg, TileMarks mk) {
+                         uint16_t* __restrict__ deg, TileMarks mk, unsigned* __restrict__ escapes) {
+    bool esc = false;  // a B row of >= 65535 entries (its degree escapes to B.rpt)
     const uint64_t first = policy_evict_first(), last = policy_evict_last();
     if (mk.tile_row && blockIdx.x == 0 && threadIdx.x == 0) mk.ends();
     const int64_t groups = k_rows >> 2;
@@ -117,6 +118,7 @@ __global__ void k_degree(const int64_t* __restrict__ brpt, int64_t k_rows,
         for (int j = 0; j < 4; ++j) {
             const long long d = r[j + 1] - r[j];
             packed |= static_cast<uint64_t>(d < 0xFFFF ? d : 0xFFFF) << (16 * j);
+            esc |= d >= 0xFFFF;
         }
         asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(deg + k), "l"(packed), "l"(last));
         if (mk.tile_row) {
@@ -138,7 +140,12 @@ __global__ void k_degree(const int64_t* __restrict__ brpt, int64_t k_rows,
     }
     // the k_rows % 4 tail
     const int64_t t = (groups << 2) + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (t < k_rows) degree_row(mk, deg, t, __ldg(&brpt[t]), __ldg(&brpt[t + 1]));
+    if (t < k_rows) {
+        const long long lo = __ldg(&brpt[t]), hi = __ldg(&brpt[t + 1]);
+        degree_row(mk, deg, t, lo, hi);
+        esc |= hi - lo >= 0xFFFF;
+    }
+    if (escapes && __any_sync(0xffffffffu, esc) && (threadIdx.x & 31) == 0) atomicOr(escapes, 1u);
 }
 
 __global__ void k_tile_rows(const int64_t* __restrict__ arpt, TileMarks mk) {
@@ -679,6 +686,7 @@ struct RbArgs {
     int32_t m;
     int64_t* __restrict__ flop;
     long long* __restrict__ totals;
+    const unsigned* escapes;  // k_degree's flag: some B row has >= 65535 entries (nullable: assume so)
 };
 
 template <bool SMEM, bool PRED>
@@ -707,6 +715,7 @@ k_flop_rb(RbArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut p
         return v == 0xFFFF ? static_cast<int32_t>(__ldg(&g.brpt[c + 1]) - __ldg(&g.brpt[c])) : v;
     };
     const int64_t units = (int64_t(g.m) + kRbRows - 1) / kRbRows;
+    const bool esc = g.escapes == nullptr || *g.escapes != 0u;  // uniform
     long long wsum = 0, wmax = 0;
     // SMEM: units handed out by a ticket counter (a block that starts late
     // takes fewer); else one unit per warp of the grid
@@ -791,14 +800,34 @@ k_flop_rb(RbArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut p
             if (r >= j && r < jend) {
                 long long sum = 0;
                 const int i0 = sh + static_cast<int>(rs - Ej), i1 = sh + static_cast<int>(re - Ej);
-                for (int i = i0; i < i1; i += 8) {
-                    int32_t cc[8], d[8];
+                if (!esc) {
+                    // no escapes: a row of <= kStage entries sums in 32 bits
+                    // (< 2^11 x 2^16) and every degree is the table's
+                    int acc = 0;
+                    if (SMEM) {
+#pragma unroll 4
+                        for (int i = i0; i < i1; ++i) acc += s_deg[stage[i]];
+                    } else {
+                        for (int i = i0; i < i1; i += 8) {
+                            int32_t d[8];
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) cc[k] = i + k < i1 ? stage[i + k] : -1;
+                            for (int k = 0; k < 8; ++k)
+                                d[k] = i + k < i1 ? static_cast<int32_t>(gather_deg(bdeg + stage[i + k], last)) : 0;
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) d[k] = cc[k] >= 0 ? deg(cc[k]) : 0;
+                            for (int k = 0; k < 8; ++k) acc += d[k];
+                        }
+                    }
+                    sum = acc;
+                } else {
+                    for (int i = i0; i < i1; i += 8) {
+                        int32_t cc[8], d[8];
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) sum += d[k];
+                        for (int k = 0; k < 8; ++k) cc[k] = i + k < i1 ? stage[i + k] : -1;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) d[k] = cc[k] >= 0 ? deg(cc[k]) : 0;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) sum += d[k];
+                    }
                 }
                 g.flop[r] = sum;
                 if (PRED) emit(r, sum);
@@ -1207,7 +1236,8 @@ static unsigned stream_grid(int64_t n, int num_sms) {
 }
 
 cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, uint16_t* deg, int num_sms,
-                          cudaStream_t stream, const DevCsr* a, const FlopScratch* s, int64_t* launches) {
+                          cudaStream_t stream, const DevCsr* a, const FlopScratch* s, int64_t* launches,
+                          unsigned* escapes) {
     // A's partition rides along when A.rpt is a view into B.rpt
     const bool fuse = a && s && a->rows > 0 && a->rpt >= brpt && a->rpt + a->rows <= brpt + k_rows;
     if (k_rows == 0 && !(a && s)) return cudaSuccess;
@@ -1220,7 +1250,8 @@ cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, uint16_t* deg, in
     if (k_rows == 0) return cudaSuccess;
     const TileMarks mk = fuse ? tile_marks(*a, *s, a->rpt - brpt) : TileMarks();
     if (reinterpret_cast<uintptr_t>(brpt) & 15) return cudaErrorMisalignedAddress;  // cudaMalloc'd
-    k_degree<<<stream_grid((k_rows + 3) / 4, num_sms), 256, 0, stream>>>(brpt, k_rows, deg, mk);
+    if (escapes) cudaMemsetAsync(escapes, 0, sizeof(unsigned), stream);
+    k_degree<<<stream_grid((k_rows + 3) / 4, num_sms), 256, 0, stream>>>(brpt, k_rows, deg, mk, escapes);
     if (launches) ++*launches;
     return cudaGetLastError();
 }
@@ -1337,7 +1368,8 @@ bool flop_rb_smem_fits(int32_t k_rows) {
 }
 
 cudaError_t launch_flop_rows(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt, int64_t* flop,
-                             long long* totals, cudaStream_t stream, const PredOut& pred, const FlopMode& mode) {
+                             long long* totals, cudaStream_t stream, const PredOut& pred, const FlopMode& mode,
+                             const unsigned* escapes) {
     if (a.rows == 0) return cudaSuccess;
     RbArgs g;
     g.arpt = a.rpt;
@@ -1346,6 +1378,7 @@ cudaError_t launch_flop_rows(const DevCsr& a, const uint16_t* bdeg, const int64_
     g.m = a.rows;
     g.flop = flop;
     g.totals = totals;
+    g.escapes = escapes;
     const bool smem = !mode.no_smem && flop_rb_smem_fits(mode.b_rows);
     if (smem)
         return pred.on() ? launch_rb<true, true>(g, bdeg, mode.b_rows, pred, mode, stream)

@@ -62,9 +62,10 @@ struct FlopScratch {
 // B.rpt for the exact length.  Gathered under an L2 evict_last policy.
 // Degree array of B and, when a and s are given, A's tile partition (fused
 // into the same pass when A.rpt is a view of B.rpt); *launches counts kernels.
+// escapes (nullable): set to 1 when some B row has >= 65535 entries.
 cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, uint16_t* deg, int num_sms,
                           cudaStream_t stream, const DevCsr* a = nullptr, const FlopScratch* s = nullptr,
-                          int64_t* launches = nullptr);
+                          int64_t* launches = nullptr, unsigned* escapes = nullptr);
 // Fused predict: with ceil/real set, the FLOP pass also writes
 // min(flop, ceil(flop / cr)) (and flop / cr) for every row as its flop becomes
 // final, cr derived on the device from totals[kFStar], totals[kZStar].
@@ -103,7 +104,8 @@ bool flop_smem_fits(int32_t k_rows);
 // partition, no fixup).  mode.sched: the smem kernel's tickets.
 bool flop_rb_smem_fits(int32_t k_rows);
 cudaError_t launch_flop_rows(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt, int64_t* flop,
-                             long long* totals, cudaStream_t stream, const PredOut& pred, const FlopMode& mode);
+                             long long* totals, cudaStream_t stream, const PredOut& pred, const FlopMode& mode,
+                             const unsigned* escapes);
 // Sampled banded-A check (n pairs of consecutive rows in [lo, hi)), rpt/col
 // device arrays with absolute offsets: out3 = {pairs, advancing, short}.
 cudaError_t launch_locality(const int64_t* rpt, const int32_t* col, int32_t lo, int32_t hi, int n, int* out3,

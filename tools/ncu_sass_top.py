@@ -28,10 +28,18 @@ def main():
     tot = sum(int(d["Warp Stall Sampling (All Samples)"] or 0) for _, d in rows) or 1
     rows.sort(key=lambda kd: -int(kd[1]["Warp Stall Sampling (All Samples)"] or 0))
     print(f"total samples {tot}")
+    stalls = [c for c in (hdr or []) if c.startswith("stall_") and "Not Issued" not in c]
+    agg = {c: 0 for c in stalls}
+    for _, d in rows:
+        for c in stalls:
+            agg[c] += int(d.get(c) or 0)
+    print("stall reasons:", ", ".join(f"{c[6:]} {100*v/tot:.0f}%" for c, v in
+                                      sorted(agg.items(), key=lambda kv: -kv[1]) if v))
     for k, d in rows[:top]:
         s = int(d["Warp Stall Sampling (All Samples)"] or 0)
-        print(f"{100*s/tot:5.1f}%  wf {d.get('L1 Wavefronts Shared','')}/{d.get('L1 Wavefronts Shared Ideal','')}"
-              f"  l2sec {d.get('L2 Theoretical Sectors Global','')}  {d['Source'].strip()[:70]}")
+        why = max(stalls, key=lambda c: int(d.get(c) or 0)) if stalls else ""
+        print(f"{100*s/tot:5.1f}%  {why[6:]:12s} wf {d.get('L1 Wavefronts Shared','')}/{d.get('L1 Wavefronts Shared Ideal','')}"
+              f"  {d['Address'][-5:]}  {d['Source'].strip()[:70]}")
 
 
 if __name__ == "__main__":
