@@ -320,8 +320,6 @@ def run_ours(args, rank, world, local):
     P.synchronize()  # the upload has landed: every step below runs on resident inputs
     policy = SamplePolicy(info["fraction"], args.cap)
     m_local = P.local_rows
-    flop_smem = os.environ.get("SPNNZ_FLOP_SMEM", "1") != "0" and \
-        (b.rows if b is not a else a.rows) <= 81280  # flop.cu flop_smem_fits
     nnz_local = int(a.rpt[P.row_hi] - a.rpt[P.row_lo])
     stream = torch.cuda.ExternalStream(P.stream_handle())
     dev_ceil = torch.empty(max(m_local, 1), dtype=torch.int64, device="cuda")
@@ -508,11 +506,9 @@ def run_ours(args, rank, world, local):
             "execution": {"parallelism": f"A row-sharded x{world} (nnz-balanced), B replicated, "
                                          "1 NCCL all-reduce per step",
                           "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps",
-                          "flop_kernel": "k_flop_smem (degree table in shared memory)" if flop_smem
-                          else "k_flop (degree gathers from L2)"},
+                          "flop_kernel": P.last_flop_kernel()},
             "roofline": {"bound": "hbm",
-                         "kernel": "FLOP pass (k_degree with the tile partition + k_flop or k_flop_smem "
-                                   "+ k_flop_fixup)",
+                         "kernel": "FLOP pass (k_degree + " + P.last_flop_kernel() + " [+ k_flop_fixup for tiles])",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          # L2 hit rate of the pass (the degree gathers dominate its

@@ -214,6 +214,9 @@ int spnnz_error_report(double z1_star, double z2_star, int64_t f_star, int64_t e
  * names: flop, sample, symbolic, allreduce, predict. */
 int spnnz_gpu_set_profiling(spnnz_gpu_ctx* ctx, int enabled);
 int spnnz_gpu_last_timings(spnnz_gpu_ctx* ctx, double* ms_out5, int64_t* launches);
+/* Name of the kernel the last FLOP pass ran (the pass picks one per matrix;
+ * "" before the first pass). */
+const char* spnnz_gpu_last_flop_kernel(spnnz_gpu_ctx* ctx);
 /* The floor the FLOP pass's access pattern sets on the loaded matrices: the
  * same A.col loads (and, for gather_ms, the same uint16 degree gathers) with
  * none of the row logic, averaged over reps launches (ms, CUDA events).

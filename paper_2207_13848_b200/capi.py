@@ -81,6 +81,7 @@ _SIGS = {
                                    c_void_p]),
     "spnnz_gpu_set_profiling": (c_int, [c_void_p, c_int]),
     "spnnz_gpu_last_timings": (c_int, [c_void_p, c_void_p, POINTER(c_int64)]),
+    "spnnz_gpu_last_flop_kernel": (ctypes.c_char_p, [c_void_p]),
     "spnnz_gpu_stream": (c_void_p, [c_void_p]),
     "spnnz_gpu_set_input_stream": (c_int, [c_void_p, c_void_p]),
     "spnnz_gpu_predict_sampled": (c_int, [c_void_p, c_uint64, c_double, c_int64, POINTER(Report), c_void_p]),

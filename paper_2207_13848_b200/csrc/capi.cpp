@@ -322,6 +322,7 @@ struct spnnz_gpu_ctx {
     int ev_order = 0;
     cudaEvent_t ev[6] = {};
     double last_ms[5] = {};
+    const char* flop_kernel = "";  // the last FLOP pass's kernel (instrumentation)
     int64_t last_launches = 0;
 };
 
@@ -592,8 +593,17 @@ bool flop_gather_nol1(const spnnz_gpu_ctx* c) {
 }
 
 // FLOP pass of the local rows into `out` (default: the resident profile).
+int flop_pass_impl(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream, const PredOut& pred,
+                   DBuf<int64_t>* out);
 int flop_pass(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream = nullptr,
               const PredOut& pred = PredOut(), DBuf<int64_t>* out = nullptr) {
+    const int rc = flop_pass_impl(c, launches, stream, pred, out);
+    c->flop_kernel = last_flop_kernel();
+    return rc;
+}
+
+int flop_pass_impl(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream, const PredOut& pred,
+                   DBuf<int64_t>* out) {
     if (!stream) stream = c->stream;
     if (!out) out = &c->flop;
     const DevCsr& a = c->a;
@@ -1167,7 +1177,7 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
     }
     c->b_nnz = b_nnz;
     RC(c->b_rpt.ensure(int64_t(bv->rows) + 1));
-    RC(c->b_col.ensure(std::max<int64_t>(b_nnz, 1)));
+    RC(c->b_col.ensure(std::max<int64_t>(b_nnz, 1) + kColPad));
     const bool chunked = residency == SPNNZ_HOST && same && b_nnz >= (int64_t(1) << 24);
     c->n_chunks = 0;
     if (!chunked) {
@@ -1206,7 +1216,7 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
         v.col = c->b_col.p;
     } else {
         RC(c->a_rpt.ensure(int64_t(v.rows) + 1));
-        RC(c->a_col.ensure(std::max<int64_t>(v.nnz, 1)));
+        RC(c->a_col.ensure(std::max<int64_t>(v.nnz, 1) + kColPad));
         CU(cudaMemcpyAsync(c->a_rpt.p, a->rpt + c->row_lo, 8 * (size_t(v.rows) + 1), kind,
                            c->stream));
         if (v.nnz)
@@ -1776,6 +1786,8 @@ int spnnz_gpu_check_guards(int64_t* checked, int64_t* broken) {
     if (broken) *broken = bad;
     return SPNNZ_OK;
 }
+
+const char* spnnz_gpu_last_flop_kernel(spnnz_gpu_ctx* c) { return c && c->flop_kernel ? c->flop_kernel : ""; }
 
 int spnnz_gpu_last_timings(spnnz_gpu_ctx* c, double* ms5, int64_t* launches) {
     if (!c) return set_err(SPNNZ_EINVAL, "null context");

@@ -36,6 +36,7 @@
 // (the 2K-byte degree array's write and re-reads are extra traffic).
 // Integer-only: bit-exact.
 #include <atomic>
+#include <type_traits>
 
 #include <cub/block/block_scan.cuh>
 
@@ -857,6 +858,364 @@ k_flop_rb(RbArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut p
     (void)sched;
 }
 
+// ------------------------------------------------------------------
+// Row streams (B's degree table in shared memory): each warp owns a
+// contiguous range of rows [R0, R1) and streams their entries [E0, E1) as
+// 128-entry chunks -- lane l loads entries c + 4l .. c + 4l + 3 with one
+// aligned 16-byte load, kRsAhead chunks ahead of the one being summed, so
+// A.col is read once, coalesced, with ~2 KB in flight per warp.  Per chunk:
+// the four degrees (shared-memory gathers, masked outside [E0, E1)), and a
+// warp inclusive scan of the lane sums, which gives P(x) = sum of the degrees
+// over [E0, x) at every entry of the chunk.  The rows are taken 32 at a time
+// (lane l owns row rb + l); an owner whose row ends inside the chunk reads
+// P(end) from the lane holding the row's last entry (three shuffles: that
+// lane's inclusive sum and its last three degrees packed), and a row's FLOP
+// is P(end) - P(end of the previous row).  The shared pipe sees ~4 gathers
+// and ~10 shuffles per 128 entries, where the staged row-per-lane walk
+// (k_flop_rb) spent two bank-conflicted loads per entry and ran each warp
+// as long as its longest row (config 4: 6.35 M shared wavefronts, 78 % of
+// the L1 pipe).  ESC: some B row has >= 65535 entries -- degrees escape to
+// B.rpt and the sums run in 64 bits (k_degree's flag picks the variant).
+constexpr int kRsThreads = 1024;
+#ifndef SPNNZ_RS_AHEAD
+#define SPNNZ_RS_AHEAD 3
+#endif
+constexpr int kRsAhead = SPNNZ_RS_AHEAD;  // chunks in flight per warp (4: spills at 64 registers)
+#ifndef SPNNZ_RS_AHEAD8
+#define SPNNZ_RS_AHEAD8 2
+#endif
+constexpr int kRsAhead8 = SPNNZ_RS_AHEAD8;  // 256-entry chunks in flight per warp (fast path)
+constexpr int kRsScratch = kRsThreads / 32 * 256 * 4;  // the fast path's per-warp query scratch (bytes)
+struct RsArgs {
+    const int64_t* __restrict__ arpt;  // m + 1 absolute offsets
+    const int32_t* __restrict__ acol;  // indexed with absolute offsets
+    const int64_t* __restrict__ brpt;
+    int64_t lo, hi;  // absolute entry range backed by acol's allocation
+    int32_t m;
+    int32_t warps;  // warps sharing the rows (a contiguous range each)
+    int64_t* __restrict__ flop;
+    long long* __restrict__ totals;
+    const unsigned* escapes;  // k_degree's flag (nullable: assume escapes)
+};
+
+template <bool PRED, bool ESC>
+__device__ __forceinline__ void rs_warp(const RsArgs& g, const uint16_t* s_deg, int32_t R0, int32_t R1,
+                                        const Emit& emit, long long& wsum, long long& wmax) {
+    using S = typename std::conditional<ESC, long long, int>::type;
+    const int lane = threadIdx.x & 31;
+    const uint64_t first = policy_evict_first();
+    const int64_t E0 = __ldg(&g.arpt[R0]);
+    // positions are 32-bit offsets from a0, the 16-byte aligned address at or
+    // below E0 (chunk starts stay aligned; the launcher keeps A's entries
+    // under 2^31 - 2^16)
+    const int64_t a0 = E0 - static_cast<int64_t>((reinterpret_cast<uintptr_t>(g.acol + E0) & 15) >> 2);
+    const int32_t* col0 = g.acol + a0;
+    const int e0 = static_cast<int>(E0 - a0), e1 = static_cast<int>(__ldg(&g.arpt[R1]) - a0);
+    const int lo = static_cast<int>(g.lo - a0 > -(1 << 30) ? g.lo - a0 : -(1 << 30));
+    const int hi = static_cast<int>(g.hi - a0);
+    // chunk loads: unguarded when the whole chunk lies inside the allocation
+    const auto load = [&](int c) -> int4 {
+        const int p = c + 4 * lane;
+        if (c >= lo && c + 128 <= hi) return ld_stream_v4(reinterpret_cast<const int4*>(col0 + p), first);
+        int4 v = make_int4(0, 0, 0, 0);
+        if (c >= e1) return v;
+        if (p >= lo && p < hi) v.x = ld_stream_i32(col0 + p, first);
+        if (p + 1 >= lo && p + 1 < hi) v.y = ld_stream_i32(col0 + p + 1, first);
+        if (p + 2 >= lo && p + 2 < hi) v.z = ld_stream_i32(col0 + p + 2, first);
+        if (p + 3 >= lo && p + 3 < hi) v.w = ld_stream_i32(col0 + p + 3, first);
+        return v;
+    };
+    const auto deg = [&](int32_t c) -> S {
+        const S v = s_deg[c];
+        if (ESC && v == 0xFFFF) return static_cast<S>(__ldg(&g.brpt[c + 1]) - __ldg(&g.brpt[c]));
+        return v;
+    };
+    // the current 32 rows [rb, rb + 32): lane's row end, resolved flag, P(end);
+    // the next 32 rows' ends are loaded one group ahead (kept raw: converted
+    // when used, so the load's latency stays hidden)
+    int32_t rb = R0;
+    bool valid = rb + lane < R1;
+    int re = valid ? static_cast<int>(__ldg(&g.arpt[rb + lane + 1]) - a0) : e1;
+    int64_t re_next = rb + 32 + lane < R1 ? __ldg(&g.arpt[rb + 32 + lane + 1]) : a0 + e1;
+    bool res = !valid || re <= 0;  // (re <= 0 only for empty rows at E0 == a0: P = 0)
+    long long pend = 0;
+    long long carry = 0;  // P(end of the row before rb)
+    long long base = 0;   // P(c)
+    bool done = R0 >= R1;
+    // the 32 rows are all resolved: write them, move to the next 32 (whose
+    // rows ending at or before c -- empty rows at the stream's start -- have
+    // P(end) = base)
+    const auto advance = [&](int c) {
+        long long prev = __shfl_up_sync(0xffffffffu, pend, 1);
+        if (lane == 0) prev = carry;
+        if (valid) {
+            const long long sum = pend - prev;
+            g.flop[rb + lane] = sum;
+            if (PRED) emit(rb + lane, sum);
+            wsum += sum;
+            wmax = sum > wmax ? sum : wmax;
+        }
+        carry = __shfl_sync(0xffffffffu, pend, 31);
+        rb += 32;
+        done = rb >= R1;
+        valid = rb + lane < R1;
+        re = valid ? static_cast<int>(re_next - a0) : e1;
+        re_next = rb + 32 + lane < R1 ? __ldg(&g.arpt[rb + 32 + lane + 1]) : a0 + e1;
+        res = !valid || re <= c;
+        pend = base;
+    };
+    int4 buf[kRsAhead];
+#pragma unroll
+    for (int k = 0; k < kRsAhead; ++k) buf[k] = load(128 * k);
+    for (int c0 = 0; c0 < e1; c0 += 128 * kRsAhead) {
+#pragma unroll
+        for (int k = 0; k < kRsAhead; ++k) {
+            const int c = c0 + 128 * k;
+            const int4 v = buf[k];
+            buf[k] = load(c + 128 * kRsAhead);
+            if (c >= e1 || done) continue;  // warp-uniform
+            S d0, d1, d2, d3;
+            if (c >= e0 && c + 128 <= e1) {  // interior chunk (warp-uniform): no masking
+                d0 = deg(v.x);
+                d1 = deg(v.y);
+                d2 = deg(v.z);
+                d3 = deg(v.w);
+            } else {
+                const int p = c + 4 * lane;
+                d0 = p >= e0 && p < e1 ? deg(v.x) : 0;
+                d1 = p + 1 >= e0 && p + 1 < e1 ? deg(v.y) : 0;
+                d2 = p + 2 >= e0 && p + 2 < e1 ? deg(v.z) : 0;
+                d3 = p + 3 >= e0 && p + 3 < e1 ? deg(v.w) : 0;
+            }
+            S incl = d0 + d1 + d2 + d3;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const S t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const S total = __shfl_sync(0xffffffffu, incl, 31);
+            for (;;) {
+                // rows ending in (c, c + 128]: P(end) from the lane holding
+                // the row's last entry (index q of the chunk)
+                const bool q = !res && re <= c + 128;
+                const int qi = q ? re - c - 1 : 4 * lane + 3;
+                const int src = qi >> 2, j = qi & 3;
+                S x;
+                if (!ESC) {
+                    const S top = __shfl_sync(0xffffffffu, incl, src);
+                    const unsigned pk = __shfl_sync(0xffffffffu, static_cast<unsigned>(d3) |
+                                                                     (static_cast<unsigned>(d2) << 16), src);
+                    const S e1v = __shfl_sync(0xffffffffu, d1, src);
+                    x = top - (j < 3 ? static_cast<S>(pk & 0xFFFFu) : 0) - (j < 2 ? static_cast<S>(pk >> 16) : 0) -
+                        (j < 1 ? e1v : 0);
+                } else {
+                    const S top = __shfl_sync(0xffffffffu, incl, src);
+                    const S e3 = __shfl_sync(0xffffffffu, d3, src);
+                    const S e2 = __shfl_sync(0xffffffffu, d2, src);
+                    const S e1v = __shfl_sync(0xffffffffu, d1, src);
+                    x = top - (j < 3 ? e3 : 0) - (j < 2 ? e2 : 0) - (j < 1 ? e1v : 0);
+                }
+                if (q) {
+                    pend = base + x;
+                    res = true;
+                }
+                if (!__all_sync(0xffffffffu, res)) break;
+                advance(c);
+                if (done) break;
+            }
+            base += total;
+        }
+    }
+    // no entries left: the remaining rows are empty and end at E1
+    while (!done) {
+        if (!res) pend = base;
+        advance(e1);
+    }
+}
+
+// The fast path (no escapes): 256-entry chunks, lane l holding entries
+// c + 8l .. c + 8l + 7 from one 32-byte load, so the scan, the row queries
+// and the loop cost half as much per entry.  Each lane publishes the prefix
+// P(c + i + 1) - P(c) of its eight entries to the warp's 1 KB of shared
+// scratch (two 16-byte stores, lane-contiguous: 4 wavefronts each) and an
+// owner whose row ends at entry q of the chunk reads scratch slot q.  A.col
+// buffers carry kColPad entries of tail padding, so a chunk is always loaded
+// whole (entries outside [E0, E1) are masked before their gather).
+constexpr int kRsChunk = 256;
+__device__ __forceinline__ int rs_slot(int q) { return ((q & 4) << 5) + ((q >> 3) << 2) + (q & 3); }
+
+template <bool PRED, class Bar>
+__device__ __forceinline__ void rs_warp_fast(const RsArgs& g, const uint16_t* s_deg, int* xs, int32_t R0,
+                                             int32_t R1, const Emit& emit, long long& wsum, long long& wmax,
+                                             const Bar& table_ready) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t first = policy_evict_first();
+    const int64_t E0 = __ldg(&g.arpt[R0]);
+    // 32-bit offsets from a0, the 32-byte aligned address at or below E0
+    const int64_t a0 = E0 - static_cast<int64_t>((reinterpret_cast<uintptr_t>(g.acol + E0) & 31) >> 2);
+    const int32_t* col0 = g.acol + a0 + 8 * lane;
+    const int e0 = static_cast<int>(E0 - a0), e1 = static_cast<int>(__ldg(&g.arpt[R1]) - a0);
+    struct V8 {
+        int v[8];
+    };
+    const auto load = [&](int c) -> V8 {
+        V8 r;
+        if (c < e1) {
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                         : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+                           "=r"(r.v[6]), "=r"(r.v[7])
+                         : "l"(col0 + c), "l"(first));
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) r.v[k] = 0;
+        }
+        return r;
+    };
+    // row ends, one group of 32 ahead: loaded unconditionally (index clamped
+    // to R1, the value replaced at use) so no select waits on a load in
+    // flight
+    const auto end_at = [&](int32_t r) -> int64_t { return __ldg(&g.arpt[(r < R1 ? r : R1 - 1) + 1]); };
+    int32_t rb = R0;
+    bool valid = rb + lane < R1;
+    const int64_t re_raw = end_at(rb + lane);
+    int64_t re_next = end_at(rb + 32 + lane);
+    V8 buf[kRsAhead8];
+#pragma unroll
+    for (int k = 0; k < kRsAhead8; ++k) buf[k] = load(kRsChunk * k);
+    table_ready();  // the block's degree table has landed (the loads above overlap its copy)
+    int re = valid ? static_cast<int>(re_raw - a0) : e1;
+    bool res = !valid || re <= 0;
+    long long pend = 0, carry = 0, base = 0;
+    bool done = R0 >= R1;
+    const auto advance = [&](int c) {
+        long long prev = __shfl_up_sync(0xffffffffu, pend, 1);
+        if (lane == 0) prev = carry;
+        if (valid) {
+            const long long sum = pend - prev;
+            g.flop[rb + lane] = sum;
+            if (PRED) emit(rb + lane, sum);
+            wsum += sum;
+            wmax = sum > wmax ? sum : wmax;
+        }
+        carry = __shfl_sync(0xffffffffu, pend, 31);
+        rb += 32;
+        done = rb >= R1;
+        valid = rb + lane < R1;
+        re = valid ? static_cast<int>(re_next - a0) : e1;
+        re_next = end_at(rb + 32 + lane);
+        res = !valid || re <= c;
+        pend = base;
+    };
+    for (int c0 = 0; c0 < e1; c0 += kRsChunk * kRsAhead8) {
+#pragma unroll
+        for (int k = 0; k < kRsAhead8; ++k) {
+            const int c = c0 + kRsChunk * k;
+            const V8 v = buf[k];
+            buf[k] = load(c + kRsChunk * kRsAhead8);
+            if (c >= e1 || done) continue;  // warp-uniform
+            int x[8];
+            if (c >= e0 && c + kRsChunk <= e1) {  // interior chunk: no masking
+#pragma unroll
+                for (int i = 0; i < 8; ++i) x[i] = s_deg[v.v[i]];
+            } else {
+                const int p = c + 8 * lane;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) x[i] = p + i >= e0 && p + i < e1 ? s_deg[v.v[i]] : 0;
+            }
+#pragma unroll
+            for (int i = 1; i < 8; ++i) x[i] += x[i - 1];
+            int incl = x[7];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            const int excl = incl - x[7];
+            reinterpret_cast<int4*>(xs)[lane] = make_int4(excl + x[0], excl + x[1], excl + x[2], excl + x[3]);
+            reinterpret_cast<int4*>(xs)[32 + lane] = make_int4(excl + x[4], excl + x[5], excl + x[6], excl + x[7]);
+            __syncwarp();
+            for (;;) {
+                // rows ending in (c, c + 256]: P(end) = base + prefix through
+                // the row's last entry
+                if (!res && re <= c + kRsChunk) {
+                    pend = base + xs[rs_slot(re - c - 1)];
+                    res = true;
+                }
+                if (!__all_sync(0xffffffffu, res)) break;
+                advance(c);
+                if (done) break;
+            }
+            __syncwarp();  // the scratch is rewritten by the next chunk
+            base += total;
+        }
+    }
+    while (!done) {
+        if (!res) pend = base;
+        advance(e1);
+    }
+}
+
+// the escape variant (64-bit sums, B rows of >= 65535 entries: rare)
+template <bool PRED>
+__device__ __forceinline__ void rs_warp_esc(const RsArgs& g, const uint16_t* s_deg, int32_t R0, int32_t R1,
+                                         const Emit& emit, long long& wsum, long long& wmax) {
+    rs_warp<PRED, true>(g, s_deg, R0, R1, emit, wsum, wmax);
+}
+
+template <bool PRED>
+__global__ void __launch_bounds__(kRsThreads, 1)
+k_flop_rs(RsArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut pred) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    __shared__ long long s_sum[kRsThreads / 32], s_max[kRsThreads / 32];
+    int* s_xs = reinterpret_cast<int*>(s_raw);  // kRsScratch bytes, then the table
+    uint16_t* s_deg = reinterpret_cast<uint16_t*>(s_raw + kRsScratch);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    {
+        // the degree table: asynchronous 16-byte copies, waited for after
+        // each warp has queued its first loads
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(s_deg));
+        const int words = (k_rows + 7) >> 3;
+        for (int i = threadIdx.x; i < words; i += blockDim.x)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * i),
+                         "l"(reinterpret_cast<const int4*>(bdeg) + i)
+                         : "memory");
+    }
+    const auto table_ready = [] {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+    };
+    Emit emit{};
+    if (PRED) emit = make_emit(pred);
+    long long wsum = 0, wmax = 0;
+    const int w = blockIdx.x * (kRsThreads / 32) + warp;
+    const int32_t R0 = static_cast<int32_t>(int64_t(g.m) * w / g.warps);
+    const int32_t R1 = static_cast<int32_t>(int64_t(g.m) * (w + 1) / g.warps);
+    const bool esc = g.escapes == nullptr || *g.escapes != 0u;  // uniform
+    if (w < g.warps && !esc) {
+        rs_warp_fast<PRED>(g, s_deg, s_xs + warp * 256, R0, R1, emit, wsum, wmax, table_ready);
+    } else {
+        table_ready();
+        if (w < g.warps) rs_warp_esc<PRED>(g, s_deg, R0, R1, emit, wsum, wmax);
+    }
+    wsum = warp_sum_ll(wsum);
+    wmax = warp_max_ll(wmax);
+    if (lane == 0) {
+        s_sum[warp] = wsum;
+        s_max[warp] = wmax;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        long long a = s_sum[lane], b = s_max[lane];
+        a = warp_sum_ll(a);
+        b = warp_max_ll(b);
+        if (lane == 0) {
+            if (a) atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[kF]), static_cast<unsigned long long>(a));
+            atomicMax(reinterpret_cast<unsigned long long*>(&g.totals[kMax]), static_cast<unsigned long long>(b));
+        }
+    }
+}
+
 // Adds each tile's leading slice to the row it continues (one thread per
 // first continuing tile of a row, summing the run of tiles that continue the
 // same row) and reduces F and max over all tiles.
@@ -1268,6 +1627,10 @@ cudaError_t launch_flop_partition(const DevCsr& a, const FlopScratch& s, cudaStr
 }
 #endif
 
+// the FLOP kernel the calling thread launched last (instrumentation)
+static thread_local const char* g_last_kernel = "";
+const char* last_flop_kernel() { return g_last_kernel; }
+
 // dynamic shared memory of k_flop_smem; its static part (the ticket slots)
 // is kept under kSmemStatic, and the total under the 227 KB per-block limit
 constexpr size_t kSmemStatic = 1024;
@@ -1312,9 +1675,11 @@ static cudaError_t launch_tiles(const TileArgs& g, const uint16_t* bdeg, int64_t
         }
         int64_t grid = (t_end - t_begin + kSmemGroups - 1) / kSmemGroups;
         if (grid > mode.num_sms) grid = mode.num_sms;
+        g_last_kernel = "k_flop_smem (tile groups, degree table in shared memory)";
         k_flop_smem<kFlopIpt, PRED, ROWS><<<static_cast<unsigned>(grid), kFlopBlock * kSmemGroups, smem, stream>>>(
             g, bdeg, mode.b_rows, pred, t_begin, t_end, mode.sched);
     } else {
+        g_last_kernel = ROWS ? "k_flop (row-mode tiles, degree gathers from L2)" : "k_flop (tiles, degree gathers from L2)";
         k_flop<kFlopBlock, kFlopIpt, PRED, ROWS, NOL1><<<static_cast<unsigned>(t_end - t_begin), kFlopBlock, 0, stream>>>(
             g, bdeg, pred, t_begin);
     }
@@ -1356,15 +1721,55 @@ static cudaError_t launch_rb(const RbArgs& g, const uint16_t* bdeg, int32_t k_ro
     const int64_t wave = int64_t(mode.num_sms) * Sh::kMinBlocks;
     if (grid > wave && (SMEM || mode.rb_persistent)) grid = wave;
     if (grid < 1) grid = 1;
+    g_last_kernel = SMEM ? "k_flop_rb (staged row blocks, degree table in shared memory)"
+                         : "k_flop_rb (row blocks, degree gathers from L2)";
     k_flop_rb<SMEM, PRED><<<static_cast<unsigned>(grid), Sh::kThreads, smem, stream>>>(g, bdeg, k_rows, pred,
                                                                                        mode.sched);
     return cudaGetLastError();
 }
 
-bool flop_rb_smem_fits(int32_t k_rows) {
+// the staged row-block kernel's table limit (K <= 74496: the A/B reference)
+static bool flop_rb_staged_fits(int32_t k_rows) {
     using Sh = RbShape<true>;
     return k_rows > 0 && size_t(Sh::kWarps) * (Sh::kStage + 4) * 4 + ((size_t(k_rows) * 2 + 15) & ~size_t(15)) +
                              kSmemStatic <= 227 * 1024;
+}
+
+static size_t flop_rs_smem_bytes(int32_t k_rows) { return kRsScratch + ((size_t(k_rows) * 2 + 15) & ~size_t(15)); }
+
+// row streams: the query scratch and the table (K <= 99328)
+bool flop_rb_smem_fits(int32_t k_rows) {
+    return k_rows > 0 && flop_rs_smem_bytes(k_rows) + kSmemStatic <= 227 * 1024;
+}
+
+static bool flop_rs_on() {
+    const char* e = getenv("SPNNZ_FLOP_RS");  // A/B knob: 0 = the staged row blocks
+    return !(e && atoi(e) == 0);
+}
+
+template <bool PRED>
+static cudaError_t launch_rs(const RsArgs& g0, const uint16_t* bdeg, int32_t k_rows, const PredOut& pred,
+                             const FlopMode& mode, cudaStream_t stream) {
+    static std::atomic<unsigned long long> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_done.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
+        cudaFuncSetAttribute(k_flop_rs<PRED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(227 * 1024 - kSmemStatic));
+        attr_done.fetch_or(1ull << (dev & 63), std::memory_order_release);
+    }
+    RsArgs g = g0;
+    // one 1024-thread block per SM; at least 32 rows per warp
+    constexpr int kWarps = kRsThreads / 32;
+    int64_t warps = (int64_t(g.m) + 31) / 32;
+    const int64_t cap = int64_t(mode.num_sms) * kWarps;
+    if (warps > cap) warps = cap;
+    if (warps < 1) warps = 1;
+    g.warps = static_cast<int32_t>(warps);
+    const unsigned grid = static_cast<unsigned>((warps + kWarps - 1) / kWarps);
+    g_last_kernel = "k_flop_rs (row streams, degree table in shared memory)";
+    k_flop_rs<PRED><<<grid, kRsThreads, flop_rs_smem_bytes(k_rows), stream>>>(g, bdeg, k_rows, pred);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_flop_rows(const DevCsr& a, const uint16_t* bdeg, const int64_t* brpt, int64_t* flop,
@@ -1380,7 +1785,23 @@ cudaError_t launch_flop_rows(const DevCsr& a, const uint16_t* bdeg, const int64_
     g.totals = totals;
     g.escapes = escapes;
     const bool smem = !mode.no_smem && flop_rb_smem_fits(mode.b_rows);
-    if (smem)
+    // (row streams keep 32-bit offsets within a warp's entries)
+    const bool rs_ok = a.nnz < (int64_t(1) << 31) - (int64_t(1) << 16);
+    if (smem && rs_ok && (flop_rs_on() || !flop_rb_staged_fits(mode.b_rows))) {
+        RsArgs r;
+        r.arpt = a.rpt;
+        r.acol = a.col;
+        r.brpt = brpt;
+        r.lo = a.base;
+        r.hi = a.base + a.nnz;
+        r.m = a.rows;
+        r.flop = flop;
+        r.totals = totals;
+        r.escapes = escapes;
+        return pred.on() ? launch_rs<true>(r, bdeg, mode.b_rows, pred, mode, stream)
+                         : launch_rs<false>(r, bdeg, mode.b_rows, pred, mode, stream);
+    }
+    if (smem && flop_rb_staged_fits(mode.b_rows))
         return pred.on() ? launch_rb<true, true>(g, bdeg, mode.b_rows, pred, mode, stream)
                          : launch_rb<true, false>(g, bdeg, mode.b_rows, pred, mode, stream);
     return pred.on() ? launch_rb<false, true>(g, bdeg, mode.b_rows, pred, mode, stream)

@@ -98,6 +98,11 @@ struct FlopMode {
     int num_sms = 148;
 };
 bool flop_smem_fits(int32_t k_rows);
+// Tail padding (entries) of the device A.col / B.col buffers: the row-stream
+// FLOP kernel loads whole 256-entry chunks past a shard's last entry.
+constexpr int64_t kColPad = 512;
+// the FLOP kernel this host thread launched last (instrumentation)
+const char* last_flop_kernel();
 // Row-block FLOP pass (A with short rows): one warp per 32 rows over
 // shared-staged columns, degree table in shared memory when B's rows fit
 // (flop_rb_smem_fits); writes flop and adds F / max into totals directly (no

@@ -359,6 +359,10 @@ class Predictor:
         check(lib().spnnz_gpu_last_timings(self._ctx, ms, ctypes.byref(n)))
         return dict(zip(("flop", "sample", "symbolic", "allreduce", "predict"), list(ms))), n.value
 
+    def last_flop_kernel(self) -> str:
+        """The kernel the last FLOP pass ran (instrumentation)."""
+        return (lib().spnnz_gpu_last_flop_kernel(self._ctx) or b"").decode()
+
     def probe_flop_floor(self, reps: int = 10):
         """(stream_ms, gather_ms): the FLOP pass's A.col stream alone, and with
         its degree gathers, without the row logic (instrumentation)."""

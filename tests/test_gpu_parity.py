@@ -116,22 +116,29 @@ def _long_b(k, n, seed, long_rows=(3, 7), long_len=70000):
     return spnnz.CsrMatrix(k, n, rpt, col)
 
 
-# the FLOP-pass kernels: (row blocks?, shared degree table?)
-FLOP_KERNELS = {"tiles-smem": ("0", "1"), "tiles-global": ("0", "0"), "rb-smem": ("1", "1"),
-                "rb-global": ("1", "0")}
+# the FLOP-pass kernels: (row blocks?, shared degree table?, row streams?)
+FLOP_KERNELS = {"tiles-smem": ("0", "1", "1"), "tiles-global": ("0", "0", "1"), "rs-smem": ("1", "1", "1"),
+                "rb-smem": ("1", "1", "0"), "rb-global": ("1", "0", "1")}
 
 
-# largest K whose degree table fits beside the row-block staging (74496) and
-# beside the tile groups (81280), and one more of each
-@pytest.mark.parametrize("k", [74496, 74497, 81280, 81281])
-@pytest.mark.parametrize("kernel", list(FLOP_KERNELS))
-def test_flop_degree_table_threshold(oracle, monkeypatch, k, kernel):
-    """The shared-memory degree tables (persistent row-block and tile-group
-    blocks) on both sides of their size limits, and the global-memory kernels,
-    incl. B rows past the uint16 escape and A rows spanning tiles / blocks."""
-    rb, smem = FLOP_KERNELS[kernel]
+def _flop_kernel_env(monkeypatch, kernel):
+    rb, smem, rs = FLOP_KERNELS[kernel]
     monkeypatch.setenv("SPNNZ_FLOP_RB", rb)
     monkeypatch.setenv("SPNNZ_FLOP_SMEM", smem)
+    monkeypatch.setenv("SPNNZ_FLOP_RS", rs)
+
+
+# largest K whose degree table fits beside the row-block staging (74496),
+# beside the tile groups (81280) and beside the row streams' scratch (99328), and one
+# more of each
+@pytest.mark.parametrize("k", [74496, 74497, 81280, 81281, 99328, 99329])
+@pytest.mark.parametrize("kernel", list(FLOP_KERNELS))
+def test_flop_degree_table_threshold(oracle, monkeypatch, k, kernel):
+    """The shared-memory degree tables (row streams, persistent row-block and
+    tile-group blocks) on both sides of their size limits, and the
+    global-memory kernels, incl. B rows past the uint16 escape and A rows
+    spanning tiles / blocks / a warp's whole row range."""
+    _flop_kernel_env(monkeypatch, kernel)
     rng = np.random.default_rng(k)
     m = 4000
     rows = [sorted(int(c) for c in rng.choice(k, int(rng.integers(0, 60)), replace=False)) for _ in range(m)]
@@ -157,10 +164,8 @@ def test_flop_row_mode(oracle, monkeypatch, rows_mode, kernel, shape):
     stencil (where load() picks them) and on shapes it would not pick
     (a 10 K-entry row, empty runs, rows longer than a row block's staging):
     per-row FLOP, F and max identical to the oracle, plain and fused."""
-    rb, smem = FLOP_KERNELS[kernel]
     monkeypatch.setenv("SPNNZ_FLOP_ROWS", rows_mode)
-    monkeypatch.setenv("SPNNZ_FLOP_RB", rb)
-    monkeypatch.setenv("SPNNZ_FLOP_SMEM", smem)
+    _flop_kernel_env(monkeypatch, kernel)
     if shape == "stencil":
         a = gen.stencil27(40, 30, 20)
         b = a
@@ -771,6 +776,25 @@ def test_detached_shards_combine_to_single_gpu(oracle):
         assert (ceil == ref.predicted_row_nnz_ceil).all()
         for q in shards:
             q.close()
+
+
+@pytest.mark.parametrize("escapes", [False, True])
+def test_detached_rect_shards_row_streams(oracle, escapes):
+    """A != B row shards whose entries start at unaligned offsets (the row
+    streams' 16-byte chunk alignment and the shard allocation's bounds), B's
+    degree table in shared memory, with and without uint16 escapes: the
+    shards' per-row FLOP concatenates to the oracle's."""
+    a = gen.uniform_len(50001, 3000, 0, 33, 11)
+    b = _long_b(3000, 100000, 12) if escapes else gen.uniform_len(3000, 70000, 0, 25, 12)
+    f = oracle.compute_flop(a, b)[0]
+    for world in (3, 7):
+        parts = []
+        for r in range(world):
+            q = Predictor(0, r, world)
+            q.load(a, b)
+            parts.append(q.compute_flop().flop_per_row)
+            q.close()
+        assert (np.concatenate(parts) == f).all()
 
 
 def test_detached_pipeline_shards_sum_to_single_gpu():
