@@ -16,6 +16,8 @@
 // the whole pipeline runs without a host round trip.  Streaming: 16-byte
 // loads of the profile, 16-byte evict-first stores.  8 B read + 8 B written
 // per row (+8 B for the real view).
+#include <atomic>
+
 #include "device_common.cuh"
 #include "kernels.h"
 
@@ -32,15 +34,37 @@ __global__ void k_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* __
     rows[r] = rid;
 }
 
+#ifndef SPNNZ_PRED_MINB
+#define SPNNZ_PRED_MINB 6  // 40 registers: 1536 resident threads per SM
+#endif
 #ifndef SPNNZ_PRED_U
 #define SPNNZ_PRED_U 4
 #endif
 
+// The IEEE quotient out of line: the reciprocal path below certifies almost
+// every row, and keeping __ddiv_rn's slow path out of the kernel body keeps
+// its register count (hence resident threads) low.
+__device__ __noinline__ double div_slow(double a, double b) { return __ddiv_rn(a, b); }
+
+// ceil_view (device_common.cuh) with the division through FastDiv: q is the
+// correctly rounded f / cr either way.
+__device__ __forceinline__ long long ceil_view_fast(long long f, const FastDiv& div, double* q_out) {
+    if (f == 0) {
+        *q_out = 0.0;
+        return 0;
+    }
+    double q;
+    if (!div.fast(static_cast<double>(f), &q)) q = div_slow(static_cast<double>(f), div.b);
+    *q_out = q;
+    return ceil_of(f, q);
+}
+
 template <bool CEIL, bool REAL>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, SPNNZ_PRED_MINB)
 k_predict(const int64_t* __restrict__ flop, int64_t m, const long long* __restrict__ totals,
           double cr_in, int64_t* __restrict__ ceil_out, double* __restrict__ real_out) {
-    const double cr = totals ? predicted_cr(totals[kFStar], totals[kZStar]) : cr_in;
+    FastDiv div;
+    div.init(totals ? predicted_cr(totals[kFStar], totals[kZStar]) : cr_in);
 
     const int64_t pairs = m >> 1;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -63,8 +87,8 @@ k_predict(const int64_t* __restrict__ flop, int64_t m, const long long* __restri
                 const int64_t i = i0 + u * stride;
                 if (i < pairs) {
                     double q0, q1;
-                    const long long c0 = ceil_view(f[u].x, cr, &q0);
-                    const long long c1 = ceil_view(f[u].y, cr, &q1);
+                    const long long c0 = ceil_view_fast(f[u].x, div, &q0);
+                    const long long c1 = ceil_view_fast(f[u].y, div, &q1);
                     if (CEIL) st_stream_ll2(reinterpret_cast<longlong2*>(ceil_out) + i, make_longlong2(c0, c1));
                     if (REAL) st_stream_d2(reinterpret_cast<double2*>(real_out) + i, make_double2(q0, q1));
                 }
@@ -72,14 +96,14 @@ k_predict(const int64_t* __restrict__ flop, int64_t m, const long long* __restri
         }
         if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
             double q;
-            const long long c = ceil_view(flop[m - 1], cr, &q);
+            const long long c = ceil_view_fast(flop[m - 1], div, &q);
             if (CEIL) ceil_out[m - 1] = c;
             if (REAL) real_out[m - 1] = q;
         }
     } else {
         for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += stride) {
             double q;
-            const long long c = ceil_view(flop[i], cr, &q);
+            const long long c = ceil_view_fast(flop[i], div, &q);
             if (CEIL) ceil_out[i] = c;
             if (REAL) real_out[i] = q;
         }
@@ -145,7 +169,23 @@ cudaError_t launch_predict(const int64_t* flop, int64_t m, const long long* tota
 #ifndef SPNNZ_PRED_GRID
 #define SPNNZ_PRED_GRID 32
 #endif
-    const int64_t cap = int64_t(num_sms) * SPNNZ_PRED_GRID;
+    // at most one wave of resident blocks (a second, partial wave of a small
+    // view doubled its time: 71 registers held 3 blocks per SM)
+    static std::atomic<int> resident[3] = {0, 0, 0};
+    const int kind = ceil_out && real_out ? 0 : ceil_out ? 1 : 2;
+    int per_sm = resident[kind].load(std::memory_order_relaxed);
+    if (per_sm == 0) {
+        if (kind == 0)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_predict<true, true>, 256, 0);
+        else if (kind == 1)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_predict<true, false>, 256, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_predict<false, true>, 256, 0);
+        if (per_sm < 1) per_sm = 1;
+        resident[kind].store(per_sm, std::memory_order_relaxed);
+    }
+    int64_t cap = int64_t(num_sms) * per_sm;
+    if (cap > int64_t(num_sms) * SPNNZ_PRED_GRID) cap = int64_t(num_sms) * SPNNZ_PRED_GRID;
     if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
     const unsigned g = static_cast<unsigned>(grid);
