@@ -61,6 +61,11 @@ constexpr int64_t kTaskProducts = 131072;
 #define SPNNZ_BITMAP_TEST 0
 #endif
 constexpr bool kTestFirst = SPNNZ_BITMAP_TEST != 0;
+// A/B knob: the unit sort's range ranks from runs of equal ranges in lane
+// order (0), __match_any_sync (1) or one ballot per range bit (2)
+#ifndef SPNNZ_SORT_MATCH
+#define SPNNZ_SORT_MATCH 1
+#endif
 constexpr int64_t kSmallTaskProducts = 2048;  // ranges this small go to k_heavy_run_small
 
 struct HeavyTask {
@@ -417,75 +422,111 @@ __global__ void __launch_bounds__(kHB) k_heavy_place(SymArgs g, SymScratch sc, i
 }
 
 // ---- 3u. (1 < R <= kPrivRanges) sort each unit in place instead of count +
-// place: the unit's products are counting-sorted by range in shared memory
-// and written back to the unit's own window of the product buffer, with its
-// R + 1 range starts in heavy_utab; the per-(item, range) totals go to
-// heavy_rc for the planner.  A task then reads range r as one slice per unit.
+// place: the unit's products are counting-sorted by range and written back to
+// the unit's own window of the product buffer, with its R + 1 range starts in
+// heavy_utab; the per-(item, range) totals go to heavy_rc for the planner.  A
+// task then reads range r as one slice per unit.
+// A warp's 32 keys are consecutive products -- runs of one sorted B row -- so
+// they fall in a few ranges: lanes of one range combine (warp_range_rank:
+// one ballot per range bit) and their lowest lane takes the block's cursor
+// for all of them, where per-lane atomics on the same counter serialised
+// (63 M of the kernel's 88 M shared wavefronts were bank conflicts at config
+// 5).  The rank within the range is kept beside the key; after the scan of
+// the range totals each key is written straight to its final position.
+__device__ __forceinline__ int warp_range_rank(int* counters, int bucket, bool valid, int nbits) {
+    const int lane = threadIdx.x & 31;
+#if SPNNZ_SORT_MATCH == 1
+    unsigned peers = __match_any_sync(kFull, valid ? bucket : -1);
+    if (!valid) peers = 0u;
+    const int leader = peers ? __ffs(peers) - 1 : lane;
+    int base = 0;
+    if (valid && lane == leader) base = atomicAdd(&counters[bucket], __popc(peers));
+    base = __shfl_sync(kFull, base, leader);
+    return base + __popc(peers & ((1u << lane) - 1));
+#elif SPNNZ_SORT_MATCH == 2
+    unsigned peers = __ballot_sync(kFull, valid);
+    for (int b = 0; b < nbits; ++b) {
+        const bool bit = (bucket >> b) & 1;
+        const unsigned bal = __ballot_sync(kFull, bit);
+        peers &= bit ? bal : ~bal;
+    }
+    const int leader = peers ? __ffs(peers) - 1 : lane;
+    int base = 0;
+    if (valid && lane == leader) base = atomicAdd(&counters[bucket], __popc(peers));
+    base = __shfl_sync(kFull, base, leader);
+    return base + __popc(peers & ((1u << lane) - 1));
+#else
+    // runs of equal ranges in lane order (the keys are sorted within a B
+    // row): each run's first lane takes the cursor for the run
+    (void)nbits;
+    const int prev = __shfl_up_sync(kFull, bucket, 1);
+    const unsigned vmask = __ballot_sync(kFull, valid);
+    const unsigned heads = __ballot_sync(kFull, valid && (lane == 0 || prev != bucket)) | ~vmask;
+    const unsigned le = 0xffffffffu >> (31 - lane);       // lanes <= lane
+    const int head = 31 - __clz(heads & le);               // this lane's run head
+    const unsigned after = heads & ~le;                    // heads (or invalid lanes) above the lane
+    const int next = after ? __ffs(after) - 1 : 32;
+    int base = 0;
+    if (valid && head == lane) base = atomicAdd(&counters[bucket], next - lane);
+    base = __shfl_sync(kFull, base, head);
+    return base + lane - head;
+#endif
+}
+
 __global__ void __launch_bounds__(kHB, 6) k_heavy_sort_units(SymArgs g, SymScratch sc, int64_t first,
                                                           int64_t count, int R, int wshift) {
     __shared__ int s_off[kHB + 1];
     __shared__ int64_t s_b0[kHB];
-    // dynamic: keys_in[U] | keys_out[U] | hist[kHW][R] | offs[R + 1]
+    // dynamic: keys[U] | ranks[U] | hist[R] (kHW * R reserved) | offs[R + 1]
     extern __shared__ int4 s_dyn_sort[];
     int32_t* s_in = reinterpret_cast<int32_t*>(s_dyn_sort);
-    int32_t* s_out = s_in + kHeavyUnitProducts;
-    int* s_hist = s_out + kHeavyUnitProducts;  // [w * R + r]
+    int32_t* s_rank = s_in + kHeavyUnitProducts;
+    int* s_hist = s_rank + kHeavyUnitProducts;
     int* s_offs = s_hist + kHW * R;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31;
+    const int nbits = 32 - __clz(R - 1);
     const long long units = sc.heavy_meta[0];
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit un = find_unit_block(sc, count, u);
-        for (int k = threadIdx.x; k < kHW * R; k += kHB) s_hist[k] = 0;
+        for (int k = threadIdx.x; k < R; k += kHB) s_hist[k] = 0;
+        // (item_products starts with a barrier: the counters are zero before
+        // the first rank is taken)
         item_products<kHB>(g, sc, first, un.item, un.p0, un.p1, s_off, s_b0,
                            [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll],
                                long long q) {
 #pragma unroll
-                               for (int k = 0; k < kUnroll; ++k)
-                                   if (valid[k]) s_in[q + 32 * k] = keys[k];
+                               for (int k = 0; k < kUnroll; ++k) {
+                                   const int rk = warp_range_rank(s_hist, keys[k] >> wshift, valid[k], nbits);
+                                   if (valid[k]) {
+                                       s_in[q + 32 * k] = keys[k];
+                                       s_rank[q + 32 * k] = rk;
+                                   }
+                               }
                            }, un.e0);
         const int n = static_cast<int>(un.p1 - un.p0);
-        for (int i = threadIdx.x; i < n; i += kHB) atomicAdd(&s_hist[w * R + (s_in[i] >> wshift)], 1);
-        __syncthreads();
-        // per range: warp offsets inside the range, the range total
+        // range totals -> the planner's per-(item, range) counts
         long long* rc = sc.heavy_rc + un.item * R;
-        for (int r = threadIdx.x; r < R; r += kHB) {
-            int tot = 0;
-#pragma unroll
-            for (int v = 0; v < kHW; ++v) {
-                const int c = s_hist[v * R + r];
-                s_hist[v * R + r] = tot;
-                tot += c;
-            }
-            s_offs[r] = tot;
-            if (tot)
-                atomicAdd(reinterpret_cast<unsigned long long*>(&rc[r]), static_cast<unsigned long long>(tot));
-        }
-        __syncthreads();
+        for (int r = threadIdx.x; r < R; r += kHB)
+            if (s_hist[r]) atomicAdd(reinterpret_cast<unsigned long long*>(&rc[r]), static_cast<unsigned long long>(s_hist[r]));
         if (threadIdx.x < 32) {  // exclusive scan of the R totals by warp 0
             const int per = (R + 31) / 32;
             const int r0 = lane * per, r1 = r0 + per < R ? r0 + per : R;
             int sum = 0;
-            for (int r = r0; r < r1; ++r) sum += s_offs[r];
+            for (int r = r0; r < r1; ++r) sum += s_hist[r];
             const int incl = warp_incl_scan(sum);
             int run = incl - sum;
             for (int r = r0; r < r1; ++r) {
-                const int c = s_offs[r];
                 s_offs[r] = run;
-                run += c;
+                run += s_hist[r];
             }
             if (lane == 31) s_offs[R] = incl;
         }
         __syncthreads();
-        // warp cursors become absolute positions in the sorted unit
-        for (int k = threadIdx.x; k < kHW * R; k += kHB) s_hist[k] += s_offs[k % R];
-        __syncthreads();
-        for (int i = threadIdx.x; i < n; i += kHB) {  // same thread <-> key mapping as the histogram
-            const int key = s_in[i];
-            s_out[atomicAdd(&s_hist[w * R + (key >> wshift)], 1)] = key;
-        }
-        __syncthreads();
         int32_t* dst = sc.heavy_pbuf + sc.heavy_foff[un.item] + un.p0;
-        for (int i = threadIdx.x; i < n; i += kHB) dst[i] = s_out[i];
+        for (int i = threadIdx.x; i < n; i += kHB) {
+            const int key = s_in[i];
+            dst[s_offs[key >> wshift] + s_rank[i]] = key;
+        }
         int32_t* tab = sc.heavy_utab + u * (R + 1);
         for (int r = threadIdx.x; r <= R; r += kHB) tab[r] = s_offs[r];
     }
