@@ -197,6 +197,9 @@ struct spnnz_gpu_ctx {
     // host-residency loads of C = A*A upload B.col in chunks on a copy stream
     // so the next FLOP pass can start on the tiles whose entries have landed
     cudaStream_t cstream = nullptr, fstream = nullptr;
+    cudaStream_t hstream = nullptr;   // heavy batches beside the FLOP pass (heavy_beside)
+    cudaEvent_t ev_hdone = nullptr;
+    int heavy_beside = -1;            // A/B knob SPNNZ_HEAVY_BESIDE (-1: the policy in run_symbolic)
     static constexpr int kChunks = 8;
     cudaEvent_t ev_rpt = nullptr, ev_chunk[kChunks] = {}, ev_fdone = nullptr;
     int64_t chunk_tile_end[kChunks] = {};
@@ -219,7 +222,7 @@ struct spnnz_gpu_ctx {
     bool b_intervals = false;  // interval heavy path requested (SPNNZ_HEAVY_INTERVALS=1)
     bool b_sorted = false;     // ... and B's rows checked non-decreasing at load
     bool rows_mode = false;    // banded A: the FLOP pass's row-per-thread tiles (checked at load)
-    bool tiers_beside = false; // the symbolic tiers run beside the FLOP pass (A/B knob SPNNZ_TIERS_BESIDE)
+    int tiers_beside = -1;     // the symbolic tiers run beside the FLOP pass (A/B knob SPNNZ_TIERS_BESIDE; -1: policy)
     int32_t a_rows = 0, a_cols = 0, b_rows = 0, b_cols = 0;
     int32_t row_lo = 0, row_hi = 0;
     int64_t b_nnz = 0;
@@ -512,12 +515,27 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     CU(cudaMemcpyAsync(c->h_counts, c->counts.p, sizeof(int32_t) * 16, cudaMemcpyDeviceToHost, bs));
     CU(cudaMemcpyAsync(c->h_meta, c->heavy_meta.p, sizeof(long long) * kHeavyMeta, cudaMemcpyDeviceToHost, bs));
     if (early) CU(cudaEventRecord(c->ev_bin, bs));
-    // the tiers wait for the FLOP pass (co-resident at config 5 both slow
-    // down: the tiers' shared tables shrink the L1 the gathers use) unless
-    // c->tiers_beside (small problems, where the FLOP pass is latency-bound)
+    // Early mode (the FLOP pass queued before): which symbolic work runs
+    // beside the pass.  When the heavy rows are the long pole (their products
+    // above ~0.43 x the pass's A entries: the heavy chain runs at ~100 G
+    // products/s, the pass at ~240 G entries/s) the heavy batches start right
+    // after the binning and the tiers wait for the pass (config 2: step 430 ->
+    // 404 us); otherwise the tiers start beside the pass and the heavy chain
+    // follows it (config 5: 2819 -> 2793 us; heavy beside there: 2885).  The
+    // heavy products come from the sizes known in advance (repeated draws),
+    // else from the previous call on the same matrices.
+    bool heavy_long = false;
+    {
+        int64_t hp = -1;
+        if (known && !tsize) hp = known->products;
+        else if (c->hc_valid && c->hc_epoch == c->epoch) hp = c->hc.products;
+        heavy_long = hp >= 0 && hp * 7 > int64_t(3) * std::max<int64_t>(c->a.nnz, 1);
+    }
+    const bool tiers_beside = c->tiers_beside >= 0 ? c->tiers_beside > 0 : !heavy_long;
+    const bool heavy_beside_pol = c->heavy_beside >= 0 ? c->heavy_beside > 0 : heavy_long;
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) {
         CU(cudaStreamWaitEvent(c->side[i], c->fork, 0));
-        if (early && !c->tiers_beside) CU(cudaStreamWaitEvent(c->side[i], c->ev_flop, 0));
+        if (early && !tiers_beside) CU(cudaStreamWaitEvent(c->side[i], c->ev_flop, 0));
     }
     CU(launch_sym_tiers(g, s, c->num_sms, c->side));
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaEventRecord(c->join[i], c->side[i]));
@@ -575,10 +593,19 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
             }
             batches.push_back(b);
         }
+        // beside: the heavy batches start on their own stream right after the
+        // binning (early mode), concurrently with the FLOP pass
+        const bool hb = early && heavy_beside_pol;
+        cudaStream_t hs = hb ? c->hstream : c->stream;
+        if (hb) CU(cudaStreamWaitEvent(hs, c->fork, 0));
         for (const Batch& b : batches) {
             RC(heavy_buffers(c, b.count, b.ents, b.products, b.cells, &s));
-            CU(launch_sym_heavy(g, s, iv, b.first, b.count, c->num_sms, c->stream, launches,
+            CU(launch_sym_heavy(g, s, iv, b.first, b.count, c->num_sms, hs, launches,
                                 c->pending_upload ? nullptr : c->fstream, c->ev_bin, c->ev_flop));
+        }
+        if (hb) {
+            CU(cudaEventRecord(c->ev_hdone, hs));
+            CU(cudaStreamWaitEvent(c->stream, c->ev_hdone, 0));
         }
     }
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaStreamWaitEvent(c->stream, c->join[i], 0));
@@ -1011,6 +1038,8 @@ int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz
         e = cudaStreamCreateWithPriority(&c->side[i], cudaStreamNonBlocking, prio_side);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->fstream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->hstream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_hdone, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_rpt, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fdone, cudaEventDisableTiming);
     for (int i = 0; i < spnnz_gpu_ctx::kChunks && e == cudaSuccess; ++i)
@@ -1053,6 +1082,7 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->cstream) cudaStreamSynchronize(c->cstream);
     if (c->fstream) cudaStreamSynchronize(c->fstream);
+    if (c->hstream) cudaStreamSynchronize(c->hstream);
     if (c->comm) nccl().CommDestroy(c->comm);
     // device buffers: the DBuf members free themselves in `delete c` below
     // (the device is already selected)
@@ -1077,6 +1107,8 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     if (c->ev_fdone) cudaEventDestroy(c->ev_fdone);
     if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->fstream) cudaStreamDestroy(c->fstream);
+    if (c->hstream) cudaStreamDestroy(c->hstream);
+    if (c->ev_hdone) cudaEventDestroy(c->ev_hdone);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return SPNNZ_OK;
@@ -1251,8 +1283,10 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
             }
         }
         c->rows_mode = banded_rows(st[0], st[1], st[2]);
-        c->tiers_beside = false;
+        c->tiers_beside = -1;
         if (const char* e = getenv("SPNNZ_TIERS_BESIDE")) c->tiers_beside = atoi(e) > 0;  // A/B knob
+        c->heavy_beside = -1;
+        if (const char* e = getenv("SPNNZ_HEAVY_BESIDE")) c->heavy_beside = atoi(e) > 0;  // A/B knob
         if (const char* e = getenv("SPNNZ_FLOP_ROWS")) c->rows_mode = atoi(e) > 0;  // A/B knob
     }
     // The interval heavy path (opt-in, SPNNZ_HEAVY_INTERVALS=1) needs B's rows
