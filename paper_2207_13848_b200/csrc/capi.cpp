@@ -199,6 +199,7 @@ struct spnnz_gpu_ctx {
     cudaStream_t cstream = nullptr, fstream = nullptr;
     cudaStream_t hstream = nullptr;   // heavy batches beside the FLOP pass (heavy_beside)
     cudaEvent_t ev_hdone = nullptr;
+    cudaEvent_t ev_gate = nullptr;    // the FLOP pass's end, for heavy runs gated behind it
     int heavy_beside = -1;            // A/B knob SPNNZ_HEAVY_BESIDE (-1: the policy in run_symbolic)
     static constexpr int kChunks = 8;
     cudaEvent_t ev_rpt = nullptr, ev_chunk[kChunks] = {}, ev_fdone = nullptr;
@@ -601,7 +602,8 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
         for (const Batch& b : batches) {
             RC(heavy_buffers(c, b.count, b.ents, b.products, b.cells, &s));
             CU(launch_sym_heavy(g, s, iv, b.first, b.count, c->num_sms, hs, launches,
-                                c->pending_upload ? nullptr : c->fstream, c->ev_bin, c->ev_flop));
+                                c->pending_upload ? nullptr : c->fstream, c->ev_bin, c->ev_flop,
+                                hb && c->heavy_beside == 2 ? c->ev_gate : nullptr));
         }
         if (hb) {
             CU(cudaEventRecord(c->ev_hdone, hs));
@@ -866,7 +868,10 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
             CU(cudaStreamWaitEvent(ss, c->fork, 0));
         }
         RC(flop_pass(c, &launches));
-        if (beside) CU(cudaEventRecord(c->ev_flop, c->stream));
+        if (beside) {
+            CU(cudaEventRecord(c->ev_flop, c->stream));
+            CU(cudaEventRecord(c->ev_gate, c->stream));
+        }
         if (draw) {
             CU(launch_sample(seed, c->a_rows, n, c->samples.p, ss));
             ++launches;
@@ -1040,6 +1045,7 @@ int spnnz_gpu_create(int device, int rank, int world, const void* nccl_id, spnnz
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->fstream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->hstream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_hdone, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_gate, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_rpt, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fdone, cudaEventDisableTiming);
     for (int i = 0; i < spnnz_gpu_ctx::kChunks && e == cudaSuccess; ++i)
@@ -1109,6 +1115,7 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     if (c->fstream) cudaStreamDestroy(c->fstream);
     if (c->hstream) cudaStreamDestroy(c->hstream);
     if (c->ev_hdone) cudaEventDestroy(c->ev_hdone);
+    if (c->ev_gate) cudaEventDestroy(c->ev_gate);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return SPNNZ_OK;
@@ -1286,7 +1293,7 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
         c->tiers_beside = -1;
         if (const char* e = getenv("SPNNZ_TIERS_BESIDE")) c->tiers_beside = atoi(e) > 0;  // A/B knob
         c->heavy_beside = -1;
-        if (const char* e = getenv("SPNNZ_HEAVY_BESIDE")) c->heavy_beside = atoi(e) > 0;  // A/B knob
+        if (const char* e = getenv("SPNNZ_HEAVY_BESIDE")) c->heavy_beside = atoi(e);  // A/B knob (2: sort beside, runs after the pass)
         if (const char* e = getenv("SPNNZ_FLOP_ROWS")) c->rows_mode = atoi(e) > 0;  // A/B knob
     }
     // The interval heavy path (opt-in, SPNNZ_HEAVY_INTERVALS=1) needs B's rows

@@ -1257,7 +1257,7 @@ cudaError_t launch_heavy_flops(const SymArgs& args, const SymScratch& s, int64_t
 
 cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sorted, int64_t first,
                              int64_t count, int num_sms, cudaStream_t stream, int64_t* launches,
-                             cudaStream_t aux, cudaEvent_t ev_a, cudaEvent_t ev_b) {
+                             cudaStream_t aux, cudaEvent_t ev_a, cudaEvent_t ev_b, cudaEvent_t run_gate) {
     if (count == 0) return cudaSuccess;
     int64_t n = 0;  // kernels launched (memsets not counted)
     static std::atomic<unsigned long long> attr_done{0};  // one bit per device; the sets are idempotent
@@ -1299,6 +1299,7 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
         if (geo.unit_sorted) {
             k_heavy_sort_units<<<sms * 6, kHB, sort_smem(R), stream>>>(args, s, first, count, R, geo.wshift);
             k_heavy_plan_units<<<items, kPrivRanges, 0, stream>>>(s, count, R, s.heavy_task_cap);
+            if (run_gate) cudaStreamWaitEvent(stream, run_gate, 0);  // the runs after the gate (FLOP pass)
             // the bitmap tasks and the small hash tasks are independent: on
             // two streams (aux given) each fills the other's tail
             if (aux) {

@@ -273,7 +273,8 @@ cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_s
 // joined through the events ev_a, ev_b.
 cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sorted, int64_t first,
                              int64_t count, int num_sms, cudaStream_t stream, int64_t* launches = nullptr,
-                             cudaStream_t aux = nullptr, cudaEvent_t ev_a = nullptr, cudaEvent_t ev_b = nullptr);
+                             cudaStream_t aux = nullptr, cudaEvent_t ev_a = nullptr, cudaEvent_t ev_b = nullptr,
+                             cudaEvent_t run_gate = nullptr);
 // Per heavy item in list order: out[i] = FLOP, out[count + i] = A-row length,
 // out[2 count + i] = boundary-table cells (batch planning when the heavy rows'
 // products exceed one batch's buffers).
