@@ -66,7 +66,11 @@ constexpr bool kTestFirst = SPNNZ_BITMAP_TEST != 0;
 #ifndef SPNNZ_SORT_MATCH
 #define SPNNZ_SORT_MATCH 1
 #endif
-constexpr int64_t kSmallTaskProducts = 2048;  // ranges this small go to k_heavy_run_small
+constexpr int64_t kSmallTaskProducts = 2048;
+#ifndef SPNNZ_RUN_U
+#define SPNNZ_RUN_U 8
+#endif
+constexpr int kRunU = SPNNZ_RUN_U;  // keys in flight per lane, R == 1 tasks (products straight from B)  // ranges this small go to k_heavy_run_small
 
 struct HeavyTask {
     int32_t item;    // index in the batch
@@ -240,7 +244,7 @@ __device__ __forceinline__ Unit find_unit_block(const SymScratch& sc, int64_t co
 // relative to p0 (clamped to [0, p1 - p0], B-row starts shifted to match) so
 // the per-product cursor works in 32-bit.  fn(keys, valid, q) with keys[u]
 // = product p0 + q + 32 u.  e0: the entry holding product p0, or -1.
-template <int BLOCK, typename Fn>
+template <int BLOCK, int U = kUnroll, typename Fn>
 __device__ __forceinline__ void item_products(const SymArgs& g, const SymScratch& sc,
                                               int64_t first, int64_t item, long long p0,
                                               long long p1, int* s_off, int64_t* s_b0, Fn&& fn,
@@ -274,7 +278,7 @@ __device__ __forceinline__ void item_products(const SymArgs& g, const SymScratch
             if (i < n) s_b0[i] = eb[e + i] + (cl - rel);
         }
         __syncthreads();
-        chunk_products<BLOCK / 32>(s_off, s_b0, n, s_off[0], s_off[n], g.bcol, fn);
+        chunk_products<BLOCK / 32, U>(s_off, s_b0, n, s_off[0], s_off[n], g.bcol, fn);
         const bool done = s_off[n] >= span || e + n >= L;
         if (done) break;
         e += n;
@@ -637,6 +641,31 @@ __global__ void k_heavy_tasks_r1(SymScratch sc, int64_t count, int64_t task_cap)
     }
 }
 
+// ORs a task's shared bitmap into its merge slot and counts the bits it set
+// first.  The returning global atomics are issued kMergeBatch at a time
+// before any result is used: one after another each waited a full L2 round
+// trip (a 32 K-word slot = 32 dependent atomics per thread of a 1024-thread
+// block, ~30 us per task at config 2, where the largest rows split into ~30
+// tasks).
+constexpr int kMergeBatch = 8;
+template <int BLOCK>
+__device__ __forceinline__ int merge_words(const uint32_t* s_set, uint32_t* gbm, int32_t words) {
+    int cnt = 0;
+    for (int k0 = threadIdx.x; k0 < words; k0 += BLOCK * kMergeBatch) {
+        uint32_t w[kMergeBatch], old[kMergeBatch];
+#pragma unroll
+        for (int b = 0; b < kMergeBatch; ++b) {
+            const int k = k0 + b * BLOCK;
+            w[b] = k < words ? s_set[k] : 0u;
+        }
+#pragma unroll
+        for (int b = 0; b < kMergeBatch; ++b) old[b] = w[b] ? atomicOr(&gbm[k0 + b * BLOCK], w[b]) : ~0u;
+#pragma unroll
+        for (int b = 0; b < kMergeBatch; ++b) cnt += __popc(w[b] & ~old[b]);
+    }
+    return cnt;
+}
+
 // ---- 5. run the tasks: one block per task, a shared bitmap over the span,
 // kept all-zero between tasks.
 // MODE: kRunItem (R == 1) products straight from the B rows; kRunBuckets the
@@ -670,10 +699,11 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
         // a task that shares its span with others (merge slot) counts at the
         // merge, so its inserts need no return value (no wait on the atomic)
         const bool merged = t.slot >= 0;
-        auto insert = [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll], long long) {
+        auto insert = [&](const auto& keys, const auto& valid, long long) {
+            constexpr int UU = static_cast<int>(sizeof(valid) / sizeof(valid[0]));
             if (merged) {
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u)
+                for (int u = 0; u < UU; ++u)
                     if (valid[u]) {
                         const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
                         const uint32_t bit = 1u << (off & 31);
@@ -682,7 +712,7 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
                 return;
             }
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u)
+            for (int u = 0; u < UU; ++u)
                 if (valid[u]) {
                     const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
                     const uint32_t bit = 1u << (off & 31);
@@ -720,17 +750,14 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
         if constexpr (MODE == kRunBuckets) {
             contiguous(insert);
         } else {
-            item_products<kRunBlock>(g, sc, first, t.item, t.a, t.b, s_off, s_b0, insert);
+            item_products<kRunBlock, kRunU>(g, sc, first, t.item, t.a, t.b, s_off, s_b0, insert);
         }
         __syncthreads();  // every insert is done
         if (t.slot >= 0) {
             // span shared by several tasks: the bits this task adds first
             cnt = 0;
             uint32_t* gbm = sc.pool + int64_t(t.slot) * slot_words;
-            for (int k = threadIdx.x; k < words; k += kRunBlock) {
-                const uint32_t w = s_set[k];
-                if (w) cnt += __popc(w & ~atomicOr(&gbm[k], w));
-            }
+            cnt = merge_words<kRunBlock>(s_set, gbm, words);
             __syncthreads();  // the merge scan has read the bitmap
         }
         cnt = static_cast<int>(warp_sum_ll(cnt));
@@ -840,10 +867,7 @@ __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, Sym
             // span shared by several tasks: the bits this task adds first
             cnt = 0;
             uint32_t* gbm = sc.pool + int64_t(t.slot) * slot_words;
-            for (int k = threadIdx.x; k < words; k += kRunBlock) {
-                const uint32_t w = s_set[k];
-                if (w) cnt += __popc(w & ~atomicOr(&gbm[k], w));
-            }
+            cnt = merge_words<kRunBlock>(s_set, gbm, words);
             __syncthreads();  // the merge scan has read the bitmap
         }
         cnt = static_cast<int>(warp_sum_ll(cnt));
