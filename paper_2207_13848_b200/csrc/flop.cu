@@ -666,8 +666,12 @@ constexpr int kRbRows = 32;
 #define SPNNZ_RB_STAGE 1100
 #endif
 #ifndef SPNNZ_RB_MINB
-#define SPNNZ_RB_MINB 6
+#define SPNNZ_RB_MINB 3
 #endif
+#ifndef SPNNZ_RB_GV
+#define SPNNZ_RB_GV 32
+#endif
+constexpr int kRbGv = SPNNZ_RB_GV;  // L2 degree gathers in flight per lane (row blocks)
 template <bool SMEM>
 struct RbShape {
     // SMEM: one 1024-thread block per SM beside the degree table; else
@@ -675,7 +679,9 @@ struct RbShape {
     static constexpr int kThreads = SMEM ? 1024 : 256;
     static constexpr int kWarps = kThreads / 32;
     // entries staged per warp: SMEM 32 x 640 x 4 B = 80 KB beside the table;
-    // else 8 x 1100 x 4 B = 35.2 KB per block, six blocks (48 warps) per SM
+    // else 8 x 1100 x 4 B = 35.2 KB per block, three blocks (24 warps) per SM
+    // whose lanes keep 32 degree gathers in flight (a stencil row's 27 in one
+    // round; config 3: 82.7 -> 68 us, against 48 warps with 8 in flight)
     static constexpr int kStage = SMEM ? 640 : SPNNZ_RB_STAGE;
     static constexpr int kMinBlocks = SMEM ? 1 : SPNNZ_RB_MINB;
 };
@@ -809,13 +815,13 @@ k_flop_rb(RbArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut p
 #pragma unroll 4
                         for (int i = i0; i < i1; ++i) acc += s_deg[stage[i]];
                     } else {
-                        for (int i = i0; i < i1; i += 8) {
-                            int32_t d[8];
+                        for (int i = i0; i < i1; i += kRbGv) {
+                            int32_t d[kRbGv];
 #pragma unroll
-                            for (int k = 0; k < 8; ++k)
+                            for (int k = 0; k < kRbGv; ++k)
                                 d[k] = i + k < i1 ? static_cast<int32_t>(gather_deg(bdeg + stage[i + k], last)) : 0;
 #pragma unroll
-                            for (int k = 0; k < 8; ++k) acc += d[k];
+                            for (int k = 0; k < kRbGv; ++k) acc += d[k];
                         }
                     }
                     sum = acc;
