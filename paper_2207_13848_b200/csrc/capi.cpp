@@ -279,8 +279,17 @@ struct spnnz_gpu_ctx {
     };
     cudaGraphExec_t gexec = nullptr;
     GraphKey gkey;
+    // compute_flop's own graph: keyed by the matrices, the output and its
+    // residency (the pass has no data-dependent host decision)
+    cudaGraphExec_t fgexec = nullptr;
+    uint64_t fg_epoch = 0;
+    const void* fg_out = nullptr;
+    int fg_res = -1;
+    int64_t fg_launches = 0;
     int64_t g_launches = 0;
     HeavySizes g_known;
+    bool used_small = false;  // the last pipeline took the fused small path (run_small)
+    bool g_small = false;     // ... and so does the captured graph
     long long* h_init = nullptr;  // pinned: initial totals of a profile-mode call (read by its graph)
     bool capturing = false;
     int64_t profile_total = 0, profile_max = 0;
@@ -832,6 +841,41 @@ int sample_share(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool need_f
     return SPNNZ_OK;
 }
 
+// Small problems: the whole sampled symbolic pass as one kernel
+// (launch_sym_small) when no row can leave bin 2 -- the resident profile is
+// this context's own for the loaded matrices (a repeated call: the same
+// matrices give the same max) and its max FLOP is at most kBin2Max -- on one
+// rank.  A/B knob SPNNZ_SYM_SMALL=0.
+bool small_path(const spnnz_gpu_ctx* c) {
+    const char* e = getenv("SPNNZ_SYM_SMALL");
+    if (e && atoi(e) == 0) return false;
+    return c->world == 1 && c->profile_valid && c->profile_own && c->profile_max <= kBin2Max;
+}
+
+int run_small(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint64_t seed, cudaStream_t stream,
+              int64_t* launches) {
+    SymArgs g;
+    g.a = c->a;
+    g.brpt = c->b_rpt.p;
+    g.bcol = c->b_col.p;
+    g.bcols = c->b_cols;
+    g.row_lo = c->row_lo;
+    g.flop = c->flop.p;
+    g.rows = d_rows;
+    g.n_items = n;
+    g.out = nullptr;
+    g.totals = c->totals.p;
+    g.total_slot = kZStar;
+    g.sampled_flop = true;
+    CU(launch_sym_small(g, seed, c->a_rows, draw, c->samples.p, c->num_sms, stream));
+    ++*launches;
+    // no heavy rows by construction: the call's observed heavy sizes are zero
+    c->h_counts[kHeavyBin] = 0;
+    c->observed_set = true;
+    c->used_small = true;
+    return SPNNZ_OK;
+}
+
 // Pipeline body shared by run_prediction and run_prediction_with_plan:
 // FLOP pass -> sampler -> sampled symbolic -> one all-reduce -> predict pass.
 // Default schedule (inputs resident): the sampler, the sampled rows' FLOP
@@ -867,11 +911,22 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
             CU(cudaEventRecord(c->fork, c->stream));
             CU(cudaStreamWaitEvent(ss, c->fork, 0));
         }
+        const bool small = small_path(c);
         RC(flop_pass(c, &launches));
         if (beside) {
             CU(cudaEventRecord(c->ev_flop, c->stream));
             CU(cudaEventRecord(c->ev_gate, c->stream));
         }
+        if (small) {
+            // draw + FLOP + count in one kernel, beside the FLOP pass
+            RC(run_small(c, d_rows, n, draw, seed, ss, &launches));
+            if (beside) {
+                CU(cudaEventRecord(c->join[0], ss));
+                CU(cudaStreamWaitEvent(c->stream, c->join[0], 0));
+            }
+            ev_record(c, 1);
+            ev_record(c, 2);
+        } else {
         if (draw) {
             CU(launch_sample(seed, c->a_rows, n, c->samples.p, ss));
             ++launches;
@@ -884,6 +939,7 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
         RC(run_symbolic(c, sh.rows, sh.n, nullptr, kZStar, true, &launches, sh.item_flop,
                         sh.use_full ? &sh.full : nullptr, sh.window, beside ? ss : nullptr, nullptr, 0,
                         known));
+        }
         ev_record(c, 3);
         RC(allreduce_totals(c));
         ev_record(c, 4);
@@ -946,7 +1002,8 @@ int pipeline_profile(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, int64_t
                      uint64_t seed = 0) {
     int64_t launches = 0;
     RC(settle_upload(c));
-    if (draw) {  // the plan drawn on the device into d_rows (= c->samples)
+    const bool small = small_path(c);
+    if (draw && !small) {  // the plan drawn on the device into d_rows (= c->samples)
         CU(launch_sample(seed, c->a_rows, n, c->samples.p, c->stream));
         ++launches;
     }
@@ -970,8 +1027,11 @@ int pipeline_profile(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, int64_t
     ev_record(c, 0);
     ev_record(c, 1);
     ev_record(c, 2);
-    RC(run_symbolic(c, d_rows, n, nullptr, kZStar, true, &launches, item_flop, nullptr, nullptr,
-                    nullptr, c->profile_own ? nullptr : c->flop.p, c->profile_max, known));
+    if (small)
+        RC(run_small(c, d_rows, n, draw, seed, c->stream, &launches));
+    else
+        RC(run_symbolic(c, d_rows, n, nullptr, kZStar, true, &launches, item_flop, nullptr, nullptr,
+                        nullptr, c->profile_own ? nullptr : c->flop.p, c->profile_max, known));
     ev_record(c, 3);
     RC(allreduce_totals(c, kFStar, 2, false));  // f*, z*; F and max are the profile's
     ev_record(c, 4);
@@ -1097,6 +1157,7 @@ int spnnz_gpu_destroy(spnnz_gpu_ctx* c) {
     if (c->h_meta) cudaFreeHost(c->h_meta);
     if (c->h_init) cudaFreeHost(c->h_init);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->fgexec) cudaGraphExecDestroy(c->fgexec);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) {
@@ -1330,15 +1391,71 @@ int spnnz_gpu_compute_flop(spnnz_gpu_ctx* c, int64_t* flop_out, int residency, i
     RC(check_ctx(c));
     RC(dims_ok(c, "compute_flop"));
     int64_t launches = 0;
-    CU(cudaMemsetAsync(c->totals.p, 0, sizeof(long long) * kTotals, c->stream));
-    RC(flop_pass(c, &launches));
-    RC(allreduce_totals(c));
     const int m = local_rows(c);
-    if (flop_out && m) {
-        CU(cudaMemcpyAsync(flop_out, c->flop.p, 8 * size_t(m),
-                           residency == SPNNZ_DEVICE ? cudaMemcpyDeviceToDevice
-                                                     : cudaMemcpyDeviceToHost,
-                           c->stream));
+    const auto body = [&]() -> int {
+        CU(cudaMemsetAsync(c->totals.p, 0, sizeof(long long) * kTotals, c->stream));
+        RC(flop_pass(c, &launches));
+        RC(allreduce_totals(c));
+        if (flop_out && m) {
+            CU(cudaMemcpyAsync(flop_out, c->flop.p, 8 * size_t(m),
+                               residency == SPNNZ_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                               c->stream));
+        }
+        return SPNNZ_OK;
+    };
+    // a repeated pass on the same matrices and output replays one CUDA graph
+    // (host-side launch cost of the memset, the kernels and the copy, ~35 ->
+    // ~20 us per call on small matrices); no NCCL inside graphs
+    const char* genv = getenv("SPNNZ_GRAPH");
+    const bool graphable = !c->pending_upload && !c->comm && !(genv && atoi(genv) == 0);
+    if (graphable && c->fgexec && c->fg_epoch == c->epoch && c->fg_out == flop_out && c->fg_res == residency) {
+        CU(cudaGraphLaunch(c->fgexec, c->stream));
+        launches = c->fg_launches;
+    } else if (graphable && c->fg_epoch == c->epoch && c->fg_res == -2) {
+        // second pass on these matrices: capture it
+        cudaGraph_t graph = nullptr;
+        bool ran = false;
+        if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed) == cudaSuccess) {
+            c->capturing = true;
+            const int rc = body();
+            c->capturing = false;
+            const cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
+            if (rc == SPNNZ_OK && ce == cudaSuccess && graph) {
+                // the previous matrices' executable graph is updated in place
+                // when the topology allows (a new shape, same kernels), else
+                // re-instantiated
+                cudaError_t ie = cudaErrorUnknown;
+                if (c->fgexec) {
+                    cudaGraphExecUpdateResultInfo info;
+                    ie = cudaGraphExecUpdate(c->fgexec, graph, &info);
+                    if (ie != cudaSuccess) {
+                        cudaGetLastError();
+                        cudaGraphExecDestroy(c->fgexec);
+                        c->fgexec = nullptr;
+                    }
+                }
+                if (!c->fgexec) ie = cudaGraphInstantiate(&c->fgexec, graph, 0);
+                if (ie == cudaSuccess) {
+                    c->fg_out = flop_out;
+                    c->fg_res = residency;
+                    c->fg_launches = launches;
+                    CU(cudaGraphLaunch(c->fgexec, c->stream));
+                    ran = true;
+                } else {
+                    c->fgexec = nullptr;
+                }
+            }
+            if (graph) cudaGraphDestroy(graph);
+        }
+        cudaGetLastError();
+        if (!ran) {
+            launches = 0;
+            RC(body());
+        }
+    } else {
+        RC(body());
+        c->fg_epoch = c->epoch;
+        c->fg_res = -2;  // seen once: the next call on these matrices is captured
     }
     RC(read_totals(c));
     c->profile_valid = true;
@@ -1605,7 +1722,9 @@ int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, boo
     const char* genv = getenv("SPNNZ_GRAPH");
     const bool graphable = known && !c->pending_upload && !c->comm && !(genv && atoi(genv) == 0);
     c->observed_set = false;
+    c->used_small = false;
     if (graphable && c->gexec && c->gkey == key && c->g_known == known_v) {
+        if (c->g_small) c->h_counts[kHeavyBin] = 0;  // (no copy of the bin counts in that graph)
         CU(cudaGraphLaunch(c->gexec, c->stream));
         c->last_launches = c->g_launches;
         c->observed_set = n > 0;
@@ -1648,6 +1767,7 @@ int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, boo
                 if (ie == cudaSuccess) {
                     c->gkey = key;
                     c->g_known = known_v;
+                    c->g_small = c->used_small;
                     c->g_launches = c->last_launches;
                     CU(cudaGraphLaunch(c->gexec, c->stream));
                     ran = true;

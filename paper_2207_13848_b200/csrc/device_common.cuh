@@ -17,6 +17,15 @@ __device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t r) {
     return z ^ (z >> 31);
 }
 
+// Row of draw r of make_sample_plan (predict.hpp:48-54): u = (z >> 11) 2^-53
+// exact, M u one IEEE multiply, truncation toward zero, the rid >= M guard.
+__device__ __forceinline__ int32_t draw_row(uint64_t seed, uint64_t r, int32_t num_rows) {
+    const uint64_t z = splitmix_at(seed, r);
+    const double u = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
+    const int32_t rid = __double2int_rz(__dmul_rn(static_cast<double>(num_rows), u));
+    return rid >= num_rows ? num_rows - 1 : rid;
+}
+
 // 32-bit mixer for hash-table slots (any injective-enough mix works: the
 // distinct count does not depend on the hash, symbolic.hpp:13-16 and
 // proj/tests/test_symbolic.cpp:94-109).

@@ -27,11 +27,7 @@ namespace {
 __global__ void k_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* __restrict__ rows) {
     const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (r >= n) return;
-    const uint64_t z = splitmix_at(seed, static_cast<uint64_t>(r));
-    const double u = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
-    int32_t rid = __double2int_rz(__dmul_rn(static_cast<double>(num_rows), u));
-    if (rid >= num_rows) rid = num_rows - 1;
-    rows[r] = rid;
+    rows[r] = draw_row(seed, static_cast<uint64_t>(r), num_rows);
 }
 
 #ifndef SPNNZ_PRED_MINB

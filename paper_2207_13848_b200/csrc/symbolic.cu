@@ -187,6 +187,76 @@ __global__ void __launch_bounds__(BLOCK) k_sym_warp_hash(SymArgs g, SymScratch s
                   static_cast<unsigned long long>(acc));
 }
 
+// ------------------------------------ small problems: one fused kernel
+// Every row's FLOP is at most kBin2Max (the context's own resident profile
+// says so): no binning pass, no tier streams -- one warp per item draws its
+// row (make_sample_plan's draw, as k_sample), walks its products into a
+// 1024-slot shared hash (bin 2's tier), and adds the row's FLOP (f*, summed
+// from the same walk) and its distinct count (z*).  A sampled call becomes
+// one kernel instead of sample + bin + five tiers on four streams.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_sym_small(SymArgs g, uint64_t seed, int32_t num_rows, int draw,
+                                                     int32_t* __restrict__ rows_out) {
+    constexpr int kSlots = 1024;
+    constexpr int W = BLOCK / 32;
+    __shared__ __align__(16) int s_table[W][kSlots];
+    __shared__ int s_off[W][33];
+    __shared__ int64_t s_b0[W][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    int* table = s_table[wib];
+    int* off = s_off[wib];
+    int64_t* b0s = s_b0[wib];
+    long long acc = 0, facc = 0;
+    for (int64_t i = blockIdx.x * int64_t(W) + wib; i < g.n_items; i += int64_t(gridDim.x) * W) {
+        int32_t rid;
+        if (draw) {
+            rid = draw_row(seed, static_cast<uint64_t>(i), num_rows);
+            if (lane == 0) rows_out[i] = rid;
+        } else {
+            rid = g.rows[i];
+        }
+        const int32_t r = rid - g.row_lo;
+        const int64_t a0 = g.a.rpt[r], a1 = g.a.rpt[r + 1];
+        hash_clear(table, kSlots, lane, 32);
+        int cnt = 0;
+        long long f = 0;
+        for (int64_t e0 = a0; e0 < a1; e0 += 32) {
+            const int64_t e = e0 + lane;
+            int d = 0;
+            int64_t b0 = 0;
+            if (e < a1) {
+                const int c = __ldg(&g.a.col[e]);
+                b0 = __ldg(&g.brpt[c]);
+                d = static_cast<int>(__ldg(&g.brpt[c + 1]) - b0);
+            }
+            f += d;
+            const int incl = warp_incl_scan(d);
+            const int nent = static_cast<int>(a1 - e0 < 32 ? a1 - e0 : 32);
+            off[lane] = incl - d;
+            b0s[lane] = b0;
+            if (lane == nent - 1) off[nent] = incl;
+            __syncwarp();
+            chunk_products<1>(off, b0s, nent, 0, off[nent], g.bcol, HashSink{table, kSlots, &cnt});
+            __syncwarp();
+        }
+        cnt = static_cast<int>(warp_sum_ll(cnt));
+        f = warp_sum_ll(f);
+        if (lane == 0) {
+            if (g.out) g.out[i] = cnt;
+            acc += cnt;
+            facc += f;
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if (acc)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[g.total_slot]),
+                      static_cast<unsigned long long>(acc));
+        if (g.sampled_flop && facc)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[kFStar]), static_cast<unsigned long long>(facc));
+    }
+}
+
 // ------------------------------ bins 3-5: block + shared-memory hash
 template <int BLOCK, int SLOTS, int BIN, int UNROLL>
 __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch sc) {
@@ -271,6 +341,16 @@ void set_smem_attr() {
 }
 
 }  // namespace
+
+cudaError_t launch_sym_small(const SymArgs& args, uint64_t seed, int32_t num_rows, bool draw, int32_t* rows_out,
+                             int num_sms, cudaStream_t stream) {
+    if (args.n_items == 0) return cudaSuccess;
+    constexpr int B = 256;
+    int64_t grid = (args.n_items + B / 32 - 1) / (B / 32);
+    if (grid > int64_t(num_sms) * 8) grid = int64_t(num_sms) * 8;
+    k_sym_small<B><<<static_cast<unsigned>(grid), B, 0, stream>>>(args, seed, num_rows, draw ? 1 : 0, rows_out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_sym_bin(const SymArgs& args, const SymScratch& s, cudaStream_t stream) {
     if (args.n_items == 0) return cudaSuccess;

@@ -856,6 +856,36 @@ def _rep_tuple(r):
     return (r.total_flop, r.stats.sampled_flop, r.stats.sampled_nnz, r.predicted_cr, r.z1_star, r.z2_star)
 
 
+@pytest.mark.parametrize("small", ["1", "0"])
+def test_small_fused_path_vs_oracle(oracle, small, monkeypatch):
+    """The fused small-problem kernel (every row's FLOP <= 512, the context's
+    own profile: taken from the second call on, then captured into a graph and
+    replayed) against the tiered path and the oracle: z*, f*, the drawn rows,
+    the ceil view; an exact pass between two replays (which rewrites the host
+    mirror of the bin counts) must not trip the advance-size check."""
+    monkeypatch.setenv("SPNNZ_SYM_SMALL", small)
+    monkeypatch.setenv("SPNNZ_STRICT_SIZES", "1")
+    a = gen.uniform_len(30000, 30000, 0, 13, 5)
+    orep, of, oceil, _ = oracle.run_prediction(a, a, 7, 0.05, -1)
+    assert of.max() <= 512
+    P = Predictor(0)
+    P.load(a)
+    for k in range(4):
+        rep = P.run_prediction(7, SamplePolicy(0.05, UNCAPPED))
+        assert rep.stats.sampled_nnz == orep.sampled_nnz and rep.stats.sampled_flop == orep.sampled_flop, k
+        assert rep.z2_star == orep.z2_star and rep.total_flop == orep.total_flop
+        assert np.array_equal(rep.predicted_row_nnz_ceil, oceil)
+        plan = oracle.make_sample_plan(a.rows, 7, 0.05, -1)
+        assert np.array_equal(rep.plan.sample_rows, plan[0] if isinstance(plan, tuple) else plan)
+        if k == 2:
+            P.exact_symbolic()
+    for k in range(3):
+        ps = P.predict_sampled(11, SamplePolicy(0.05, UNCAPPED))
+        o2 = oracle.run_prediction(a, a, 11, 0.05, -1, want_rows=False)[0]
+        assert ps.stats.sampled_nnz == o2.sampled_nnz and ps.z2_star == o2.z2_star
+    P.close()
+
+
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4])
 def test_repeat_calls_graph_replay_and_cached_heavy_sizes(golden, cfg, monkeypatch):
     """Repeated calls take the sync-free path: heavy-row sizes known in advance

@@ -1,0 +1,11 @@
+mkdir -p gpurun_out; rm -f gpurun_out/ab_*.log
+for rep in 1 2; do bash tools/ab.sh 2 ipt8 b256 mb2k g1; for f in gpurun_out/ab_2_*.log; do cp $f ${f%.log}_r$rep.txt; done; done
+bash tools/ab.sh 5 ipt8 b256 mb2k g1
+for f in gpurun_out/ab_2_*_r*.txt gpurun_out/ab_5_*.log; do python - "$f" <<'PY'
+import json,sys
+try:
+  d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
+  print(sys.argv[1], round(d['ms_per_step']*1000,1), {k:round(v*1000,1) for k,v in d['phases_ms'].items()}, round(d['roofline']['frac'],3))
+except Exception as e: print(sys.argv[1], 'fail', e)
+PY
+done
