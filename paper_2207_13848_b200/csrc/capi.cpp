@@ -288,6 +288,8 @@ struct spnnz_gpu_ctx {
     int64_t fg_launches = 0;
     int64_t g_launches = 0;
     HeavySizes g_known;
+    bool dbg_t = false;              // SPNNZ_DEBUG_TIMELINE: per-stream end times to stderr
+    cudaEvent_t dbg_ev[8] = {};       // [0] start [1] FLOP end [2..5] tier streams [6] heavy end [7] join
     bool used_small = false;  // the last pipeline took the fused small path (run_small)
     bool g_small = false;     // ... and so does the captured graph
     long long* h_init = nullptr;  // pinned: initial totals of a profile-mode call (read by its graph)
@@ -549,6 +551,7 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     }
     CU(launch_sym_tiers(g, s, c->num_sms, c->side));
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaEventRecord(c->join[i], c->side[i]));
+    if (c->dbg_t) for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaEventRecord(c->dbg_ev[2 + i], c->side[i]));
     *launches += 6;
     c->observed_set = true;  // the counts land in h_counts / h_meta by the call's end
     if (known && !tsize) {
@@ -618,6 +621,7 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
             CU(cudaEventRecord(c->ev_hdone, hs));
             CU(cudaStreamWaitEvent(c->stream, c->ev_hdone, 0));
         }
+        if (c->dbg_t) CU(cudaEventRecord(c->dbg_ev[6], hs));
     }
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaStreamWaitEvent(c->stream, c->join[i], 0));
     return SPNNZ_OK;
@@ -912,7 +916,14 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
             CU(cudaStreamWaitEvent(ss, c->fork, 0));
         }
         const bool small = small_path(c);
+        c->dbg_t = !c->capturing && getenv("SPNNZ_DEBUG_TIMELINE") != nullptr;
+        if (c->dbg_t) {
+            for (auto& e : c->dbg_ev)
+                if (!e) cudaEventCreate(&e);
+            CU(cudaEventRecord(c->dbg_ev[0], c->stream));
+        }
         RC(flop_pass(c, &launches));
+        if (c->dbg_t) CU(cudaEventRecord(c->dbg_ev[1], c->stream));
         if (beside) {
             CU(cudaEventRecord(c->ev_flop, c->stream));
             CU(cudaEventRecord(c->ev_gate, c->stream));
@@ -939,6 +950,16 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
         RC(run_symbolic(c, sh.rows, sh.n, nullptr, kZStar, true, &launches, sh.item_flop,
                         sh.use_full ? &sh.full : nullptr, sh.window, beside ? ss : nullptr, nullptr, 0,
                         known));
+        }
+        if (c->dbg_t) {
+            CU(cudaEventRecord(c->dbg_ev[7], c->stream));
+            CU(cudaEventSynchronize(c->dbg_ev[7]));
+            float t[8] = {};
+            for (int i = 1; i < 8; ++i) cudaEventElapsedTime(&t[i], c->dbg_ev[0], c->dbg_ev[i]);
+            fprintf(stderr, "timeline us: flop %.1f tiers %.1f %.1f %.1f %.1f heavy %.1f join %.1f\n", 1e3 * t[1],
+                    1e3 * t[2], 1e3 * t[3], 1e3 * t[4], 1e3 * t[5], 1e3 * t[6], 1e3 * t[7]);
+            heavy_debug_print(c->dbg_ev[0]);
+            c->dbg_t = false;
         }
         ev_record(c, 3);
         RC(allreduce_totals(c));

@@ -34,6 +34,8 @@
 // Every count is a set cardinality: exact and independent of bucketing, task
 // boundaries and scheduling.
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 
 #include "symbolic_common.cuh"
 
@@ -70,7 +72,11 @@ constexpr int64_t kSmallTaskProducts = 2048;
 #ifndef SPNNZ_RUN_U
 #define SPNNZ_RUN_U 8
 #endif
-constexpr int kRunU = SPNNZ_RUN_U;  // keys in flight per lane, R == 1 tasks (products straight from B)  // ranges this small go to k_heavy_run_small
+constexpr int kRunU = SPNNZ_RUN_U;
+#ifndef SPNNZ_SORT_U
+#define SPNNZ_SORT_U 4
+#endif
+constexpr int kSortU = SPNNZ_SORT_U;  // keys in flight per lane in the unit sort  // keys in flight per lane, R == 1 tasks (products straight from B)  // ranges this small go to k_heavy_run_small
 
 struct HeavyTask {
     int32_t item;    // index in the batch
@@ -495,11 +501,11 @@ __global__ void __launch_bounds__(kHB, 6) k_heavy_sort_units(SymArgs g, SymScrat
         for (int k = threadIdx.x; k < R; k += kHB) s_hist[k] = 0;
         // (item_products starts with a barrier: the counters are zero before
         // the first rank is taken)
-        item_products<kHB>(g, sc, first, un.item, un.p0, un.p1, s_off, s_b0,
-                           [&](const int (&keys)[kUnroll], const bool (&valid)[kUnroll],
+        item_products<kHB, kSortU>(g, sc, first, un.item, un.p0, un.p1, s_off, s_b0,
+                           [&](const int (&keys)[kSortU], const bool (&valid)[kSortU],
                                long long q) {
 #pragma unroll
-                               for (int k = 0; k < kUnroll; ++k) {
+                               for (int k = 0; k < kSortU; ++k) {
                                    const int rk = warp_range_rank(s_hist, keys[k] >> wshift, valid[k], nbits);
                                    if (valid[k]) {
                                        s_in[q + 32 * k] = keys[k];
@@ -1279,6 +1285,26 @@ cudaError_t launch_heavy_flops(const SymArgs& args, const SymScratch& s, int64_t
     return cudaGetLastError();
 }
 
+// debug timeline (SPNNZ_DEBUG_TIMELINE): events after each heavy kernel
+static cudaEvent_t g_hev[12] = {};
+static const char* g_hname[12] = {};
+static int g_hn = 0;
+static bool g_hdbg = false;
+static void hmark(const char* name, cudaStream_t st) {
+    if (!g_hdbg || g_hn >= 12) return;
+    if (!g_hev[g_hn]) cudaEventCreate(&g_hev[g_hn]);
+    g_hname[g_hn] = name;
+    cudaEventRecord(g_hev[g_hn++], st);
+}
+void heavy_debug_print(cudaEvent_t start) {
+    for (int i = 0; i < g_hn; ++i) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, start, g_hev[i]);
+        fprintf(stderr, "  heavy %s end %.1f us\n", g_hname[i], 1e3 * t);
+    }
+    g_hn = 0;
+}
+
 cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sorted, int64_t first,
                              int64_t count, int num_sms, cudaStream_t stream, int64_t* launches,
                              cudaStream_t aux, cudaEvent_t ev_a, cudaEvent_t ev_b, cudaEvent_t run_gate) {
@@ -1307,8 +1333,12 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
     const int R = geo.ranges;
     const unsigned sms = static_cast<unsigned>(num_sms);
     const unsigned items = static_cast<unsigned>(count);
+    g_hdbg = getenv("SPNNZ_DEBUG_TIMELINE") != nullptr;
+    g_hn = 0;
     k_heavy_prep<<<1, kPrepBlock, 0, stream>>>(args, s, first, count);
+    hmark("prep", stream);
     k_heavy_entries<<<items, kEntB, 0, stream>>>(args, s, first);
+    hmark("entries", stream);
     n += 2;
     if (sorted) {
         cudaMemsetAsync(s.heavy_bnd, 0, sizeof(int32_t) * s.heavy_bnd_cap, stream);
@@ -1322,7 +1352,9 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
         cudaMemsetAsync(s.heavy_rc, 0, sizeof(long long) * count * R, stream);
         if (geo.unit_sorted) {
             k_heavy_sort_units<<<sms * 6, kHB, sort_smem(R), stream>>>(args, s, first, count, R, geo.wshift);
+            hmark("sort", stream);
             k_heavy_plan_units<<<items, kPrivRanges, 0, stream>>>(s, count, R, s.heavy_task_cap);
+            hmark("plan", stream);
             if (run_gate) cudaStreamWaitEvent(stream, run_gate, 0);  // the runs after the gate (FLOP pass)
             // the bitmap tasks and the small hash tasks are independent: on
             // two streams (aux given) each fills the other's tail
@@ -1332,8 +1364,10 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
             }
             k_heavy_run_units<512><<<sms * SPNNZ_RUN_GRID, 512, (1 << kTaskSpanShift) / 8, stream>>>(
                 args, s, first, R, geo.wshift, geo.wwords);
+            hmark("run_units", stream);
             k_heavy_run_small<<<sms * 3, kSG * kSGroups, kSGroups * kSSlots * 4, aux ? aux : stream>>>(
                 args, s, first, R);
+            hmark("run_small", aux ? aux : stream);
             if (aux) {
                 cudaEventRecord(ev_b, aux);
                 cudaStreamWaitEvent(stream, ev_b, 0);

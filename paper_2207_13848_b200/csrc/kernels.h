@@ -280,6 +280,7 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
                              int64_t count, int num_sms, cudaStream_t stream, int64_t* launches = nullptr,
                              cudaStream_t aux = nullptr, cudaEvent_t ev_a = nullptr, cudaEvent_t ev_b = nullptr,
                              cudaEvent_t run_gate = nullptr);
+void heavy_debug_print(cudaEvent_t start);  // SPNNZ_DEBUG_TIMELINE
 // Per heavy item in list order: out[i] = FLOP, out[count + i] = A-row length,
 // out[2 count + i] = boundary-table cells (batch planning when the heavy rows'
 // products exceed one batch's buffers).
