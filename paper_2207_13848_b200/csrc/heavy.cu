@@ -43,7 +43,10 @@ namespace spnnz_gpu {
 namespace {
 using namespace sym;
 
-constexpr int kHB = 256;                  // block of the unit passes
+#ifndef SPNNZ_HB
+#define SPNNZ_HB 256
+#endif
+constexpr int kHB = SPNNZ_HB;             // block of the unit passes
 constexpr int kHW = kHB / 32;             // warps per unit block
 constexpr int kSpanShift = 20;            // R == 1: one span of <= 2^20 columns (128 KB)
 #ifndef SPNNZ_SPAN_SHIFT
@@ -92,7 +95,10 @@ __device__ __forceinline__ const int32_t* heavy_list(const SymScratch& sc, int64
 
 // ---- 0a. batch bookkeeping: per item its units, entries, products,
 // interval tasks and boundary-table cells, as exclusive prefixes (1 block)
-constexpr int kPrepBlock = 1024;
+#ifndef SPNNZ_PREP_BLOCK
+#define SPNNZ_PREP_BLOCK 1024
+#endif
+constexpr int kPrepBlock = SPNNZ_PREP_BLOCK;
 
 __global__ void __launch_bounds__(kPrepBlock) k_heavy_prep(SymArgs g, SymScratch sc, int64_t first,
                                                            int64_t count) {
@@ -151,7 +157,10 @@ __global__ void __launch_bounds__(kPrepBlock) k_heavy_prep(SymArgs g, SymScratch
 // row of up to kEntB * kEntV entries costs one dependent load chain (the
 // walk of 256 entries per step made the longest heavy row the critical path:
 // ~30 us whatever the number of heavy rows).
-constexpr int kEntB = 512, kEntV = 4;
+#ifndef SPNNZ_ENT_BLOCK
+#define SPNNZ_ENT_BLOCK 512
+#endif
+constexpr int kEntB = SPNNZ_ENT_BLOCK, kEntV = 4;
 __global__ void __launch_bounds__(kEntB) k_heavy_entries(SymArgs g, SymScratch sc, int64_t first) {
     using Scan = cub::BlockScan<long long, kEntB>;
     __shared__ typename Scan::TempStorage tmp;
@@ -483,7 +492,7 @@ __device__ __forceinline__ int warp_range_rank(int* counters, int bucket, bool v
 #endif
 }
 
-__global__ void __launch_bounds__(kHB, 6) k_heavy_sort_units(SymArgs g, SymScratch sc, int64_t first,
+__global__ void __launch_bounds__(kHB, 1536 / kHB) k_heavy_sort_units(SymArgs g, SymScratch sc, int64_t first,
                                                           int64_t count, int R, int wshift) {
     __shared__ int s_off[kHB + 1];
     __shared__ int64_t s_b0[kHB];
@@ -1351,7 +1360,7 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
     if (R > 1) {
         cudaMemsetAsync(s.heavy_rc, 0, sizeof(long long) * count * R, stream);
         if (geo.unit_sorted) {
-            k_heavy_sort_units<<<sms * 6, kHB, sort_smem(R), stream>>>(args, s, first, count, R, geo.wshift);
+            k_heavy_sort_units<<<sms * (1536 / kHB), kHB, sort_smem(R), stream>>>(args, s, first, count, R, geo.wshift);
             hmark("sort", stream);
             k_heavy_plan_units<<<items, kPrivRanges, 0, stream>>>(s, count, R, s.heavy_task_cap);
             hmark("plan", stream);
