@@ -490,6 +490,17 @@ int heavy_buffers(spnnz_gpu_ctx* c, int64_t count, int64_t ents, int64_t product
 // the host learns the heavy count without waiting for it; the tiers wait for
 // the FLOP pass and the heavy batches queue behind it on c->stream -- no
 // host round trip between the FLOP pass and the symbolic work.
+// The heavy rows are the long pole of the call when their products exceed
+// ~0.43x the FLOP pass's A entries (the heavy chain runs at ~100 G products/s,
+// the pass at ~240 G entries/s); the products come from the sizes known in
+// advance, else from the previous call on the same matrices.
+bool heavy_long_pole(const spnnz_gpu_ctx* c, const spnnz_gpu_ctx::HeavySizes* known) {
+    int64_t hp = -1;
+    if (known) hp = known->products;
+    else if (c->hc_valid && c->hc_epoch == c->epoch) hp = c->hc.products;
+    return hp >= 0 && hp * 7 > int64_t(3) * std::max<int64_t>(c->a.nnz, 1);
+}
+
 int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64_t* d_out,
                  int slot, bool sampled_flop, int64_t* launches, const int64_t* item_flop = nullptr,
                  const DevCsr* a_view = nullptr, const int64_t* window = nullptr,
@@ -536,13 +547,7 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     // follows it (config 5: 2819 -> 2793 us; heavy beside there: 2885).  The
     // heavy products come from the sizes known in advance (repeated draws),
     // else from the previous call on the same matrices.
-    bool heavy_long = false;
-    {
-        int64_t hp = -1;
-        if (known && !tsize) hp = known->products;
-        else if (c->hc_valid && c->hc_epoch == c->epoch) hp = c->hc.products;
-        heavy_long = hp >= 0 && hp * 7 > int64_t(3) * std::max<int64_t>(c->a.nnz, 1);
-    }
+    const bool heavy_long = heavy_long_pole(c, tsize ? nullptr : known);
     const bool tiers_beside = c->tiers_beside >= 0 ? c->tiers_beside > 0 : !heavy_long;
     const bool heavy_beside_pol = c->heavy_beside >= 0 ? c->heavy_beside > 0 : heavy_long;
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) {
@@ -942,9 +947,21 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
             CU(launch_sample(seed, c->a_rows, n, c->samples.p, ss));
             ++launches;
         }
-        // beside the FLOP pass the sampled rows' FLOP is derived directly, so
-        // the binning need not wait for the pass either (early run_symbolic)
-        RC(sample_share(c, d_rows, n, beside, &sh, &launches, ss));
+        // The sampled rows' FLOP: on one rank the binning reads the resident
+        // profile after the pass (the pass's grid leaves no room beside it
+        // anyway: deriving it directly only added three
+        // kernels after the pass); multi-GPU splits the list by FLOP, which
+        // sample_share derives directly from A and B.rpt
+        // ... except when the heavy rows are the long pole (run_symbolic's
+        // policy): their chain then starts beside the pass (config 2: 435 ->
+        // 402 us with the direct FLOP; configs 3 / 4: 148 -> 144, 139 -> 130 us
+        // from the profile)
+        const char* ie = getenv("SPNNZ_ITEM_FLOP");  // A/B knob: 1 / 0 = always / never directly on one rank
+        bool direct = c->world > 1 || heavy_long_pole(c, known);
+        if (ie) direct = c->world > 1 || atoi(ie) > 0;
+        direct = direct && beside;
+        RC(sample_share(c, d_rows, n, direct, &sh, &launches, ss));
+        if (beside && !sh.item_flop) CU(cudaStreamWaitEvent(ss, c->ev_flop, 0));
         ev_record(c, 1);
         ev_record(c, 2);
         RC(run_symbolic(c, sh.rows, sh.n, nullptr, kZStar, true, &launches, sh.item_flop,

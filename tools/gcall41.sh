@@ -1,0 +1,17 @@
+mkdir -p gpurun_out; rm -f gpurun_out/rep_*.log
+for rep in 1 2; do for c in 5 2 3 4; do
+  for v in base; do
+    case $v in base) E="";; if1) E="SPNNZ_ITEM_FLOP=1";; esac
+    env $E python bench.py --config $c --no-e2e --no-cpu-baseline --no-accuracy > gpurun_out/rep_${c}_${v}_$rep.log 2>&1
+  done
+done; done
+python - <<'PY'
+import json,glob,collections
+r=collections.defaultdict(list)
+for f in glob.glob('gpurun_out/rep_*.log'):
+    _,c,v,k=f[:-4].split('/')[-1].split('_')
+    try: r[(c,v)].append(json.loads(open(f).read().strip().splitlines()[-1])['ms_per_step']*1000)
+    except Exception as e: print(f,e)
+for k in sorted(r): print(k, [round(x,1) for x in sorted(r[k])])
+PY
+python tools/timeline.py 5 3 2>&1 | grep -E "timeline|heavy " | tail -7
