@@ -858,7 +858,7 @@ int sample_share(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool need_f
 bool small_path(const spnnz_gpu_ctx* c) {
     const char* e = getenv("SPNNZ_SYM_SMALL");
     if (e && atoi(e) == 0) return false;
-    return c->world == 1 && c->profile_valid && c->profile_own && c->profile_max <= kBin2Max;
+    return c->world == 1 && c->profile_valid && c->profile_own && c->profile_max <= kBin3Max;
 }
 
 int run_small(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint64_t seed, cudaStream_t stream,
@@ -876,8 +876,19 @@ int run_small(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uin
     g.totals = c->totals.p;
     g.total_slot = kZStar;
     g.sampled_flop = true;
-    CU(launch_sym_small(g, seed, c->a_rows, draw, c->samples.p, c->num_sms, stream));
-    ++*launches;
+    // items above bin 2 (a block each) on a side stream beside the warps'
+    const bool two = c->profile_max > kBin2Max;
+    cudaStream_t sb = two ? c->side[1] : nullptr;
+    if (two) {
+        CU(cudaEventRecord(c->fork, stream));
+        CU(cudaStreamWaitEvent(sb, c->fork, 0));
+    }
+    CU(launch_sym_small(g, seed, c->a_rows, draw, c->samples.p, c->num_sms, stream, sb));
+    *launches += two ? 2 : 1;
+    if (two) {
+        CU(cudaEventRecord(c->join[1], sb));
+        CU(cudaStreamWaitEvent(stream, c->join[1], 0));
+    }
     // no heavy rows by construction: the call's observed heavy sizes are zero
     c->h_counts[kHeavyBin] = 0;
     c->observed_set = true;
@@ -934,7 +945,10 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
             CU(cudaEventRecord(c->ev_gate, c->stream));
         }
         if (small) {
-            // draw + FLOP + count in one kernel, beside the FLOP pass
+            // draw + FLOP + count in one kernel beside the FLOP pass; with
+            // rows above bin 2, two kernels after the pass (they read this
+            // call's profile to pick each item's kernel)
+            if (beside && c->profile_max > kBin2Max) CU(cudaStreamWaitEvent(ss, c->ev_flop, 0));
             RC(run_small(c, d_rows, n, draw, seed, ss, &launches));
             if (beside) {
                 CU(cudaEventRecord(c->join[0], ss));

@@ -259,11 +259,13 @@ struct SymArgs {
 };
 constexpr int kMetaCapacity = 9;  // heavy_meta slot: largest tsize above the profile's capacity
 
-// Small problems (every row's FLOP <= kBin2Max, one rank, the context's own
-// profile): draw (draw: rows_out[i] = make_sample_plan's row i), FLOP and
-// distinct count of every item in one kernel; adds z* (and f*) to totals.
+// Small problems (every row's FLOP <= kBin3Max, one rank, the context's own
+// profile in args.flop): draw (draw: rows_out[i] = make_sample_plan's row i),
+// FLOP and distinct count of every item -- items of FLOP <= kBin2Max one warp
+// each on `stream`, the rest (stream_b non-null: the profile's max is above
+// bin 2) one block each on stream_b; adds z* (and f*) to totals.
 cudaError_t launch_sym_small(const SymArgs& args, uint64_t seed, int32_t num_rows, bool draw, int32_t* rows_out,
-                             int num_sms, cudaStream_t stream);
+                             int num_sms, cudaStream_t stream, cudaStream_t stream_b = nullptr);
 // Classifies items into bins (writes out[] = 0 for empty / foreign rows).
 cudaError_t launch_sym_bin(const SymArgs& args, const SymScratch& s, cudaStream_t stream);
 // Runs the smem tiers (bins 1-5) over the binned lists; grids are persistent

@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_warp_hash(SymArgs g, SymScratch s
 // one kernel instead of sample + bin + five tiers on four streams.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_sym_small(SymArgs g, uint64_t seed, int32_t num_rows, int draw,
-                                                     int32_t* __restrict__ rows_out) {
+                                                     int32_t* __restrict__ rows_out, int split) {
     constexpr int kSlots = 1024;
     constexpr int W = BLOCK / 32;
     __shared__ __align__(16) int s_table[W][kSlots];
@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_small(SymArgs g, uint64_t seed, i
             rid = g.rows[i];
         }
         const int32_t r = rid - g.row_lo;
+        if (split && g.flop[r] > kBin2Max) continue;  // k_sym_small_block's (the resident own profile)
         const int64_t a0 = g.a.rpt[r], a1 = g.a.rpt[r + 1];
         hash_clear(table, kSlots, lane, 32);
         int cnt = 0;
@@ -249,6 +250,62 @@ __global__ void __launch_bounds__(BLOCK) k_sym_small(SymArgs g, uint64_t seed, i
         __syncwarp();
     }
     if (lane == 0) {
+        if (acc)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[g.total_slot]),
+                      static_cast<unsigned long long>(acc));
+        if (g.sampled_flop && facc)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[kFStar]), static_cast<unsigned long long>(facc));
+    }
+}
+
+// The same for the items of kBin2Max < FLOP <= kBin3Max (launched beside
+// k_sym_small when the profile's max is above bin 2): one block per item,
+// bin 3's 4096-slot table, the item's row drawn again (the same draw).
+template <int BLOCK, int SLOTS>
+__global__ void __launch_bounds__(BLOCK) k_sym_small_block(SymArgs g, uint64_t seed, int32_t num_rows, int draw) {
+    __shared__ __align__(16) int table[SLOTS];
+    using Scan = cub::BlockScan<int, BLOCK>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int s_off[BLOCK + 1];
+    __shared__ int64_t s_b0[BLOCK];
+    __shared__ long long s_red[BLOCK / 32];
+    long long acc = 0, facc = 0;
+    for (int64_t i = blockIdx.x; i < g.n_items; i += gridDim.x) {
+        const int32_t rid = draw ? draw_row(seed, static_cast<uint64_t>(i), num_rows) : g.rows[i];
+        const int32_t r = rid - g.row_lo;
+        const int64_t f = g.flop[r];
+        if (f <= kBin2Max) continue;  // k_sym_small's (uniform per block)
+        const int64_t a0 = g.a.rpt[r], a1 = g.a.rpt[r + 1];
+        hash_clear(table, SLOTS, threadIdx.x, BLOCK);
+        int cnt = 0;
+        for (int64_t c0 = a0; c0 < a1; c0 += BLOCK) {
+            const int64_t e = c0 + threadIdx.x;
+            int d = 0;
+            int64_t b0 = 0;
+            if (e < a1) {
+                const int c = __ldg(&g.a.col[e]);
+                b0 = __ldg(&g.brpt[c]);
+                d = static_cast<int>(__ldg(&g.brpt[c + 1]) - b0);
+            }
+            int excl, total;
+            Scan(scan_tmp).ExclusiveSum(d, excl, total);
+            const int nent = static_cast<int>(a1 - c0 < BLOCK ? a1 - c0 : BLOCK);
+            s_off[threadIdx.x] = excl;
+            s_b0[threadIdx.x] = b0;
+            if (threadIdx.x == 0) s_off[nent] = total;
+            __syncthreads();  // also orders the table fill before the inserts
+            chunk_products<BLOCK / 32>(s_off, s_b0, nent, 0, total, g.bcol, HashSink{table, SLOTS, &cnt});
+            __syncthreads();
+        }
+        const long long tot = block_sum_ll<BLOCK>(cnt, s_red);
+        if (threadIdx.x == 0) {
+            if (g.out) g.out[i] = tot;
+            acc += tot;
+            facc += f;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
         if (acc)
             atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[g.total_slot]),
                       static_cast<unsigned long long>(acc));
@@ -343,12 +400,18 @@ void set_smem_attr() {
 }  // namespace
 
 cudaError_t launch_sym_small(const SymArgs& args, uint64_t seed, int32_t num_rows, bool draw, int32_t* rows_out,
-                             int num_sms, cudaStream_t stream) {
+                             int num_sms, cudaStream_t stream, cudaStream_t stream_b) {
     if (args.n_items == 0) return cudaSuccess;
     constexpr int B = 256;
     int64_t grid = (args.n_items + B / 32 - 1) / (B / 32);
     if (grid > int64_t(num_sms) * 8) grid = int64_t(num_sms) * 8;
-    k_sym_small<B><<<static_cast<unsigned>(grid), B, 0, stream>>>(args, seed, num_rows, draw ? 1 : 0, rows_out);
+    k_sym_small<B><<<static_cast<unsigned>(grid), B, 0, stream>>>(args, seed, num_rows, draw ? 1 : 0, rows_out,
+                                                                    stream_b ? 1 : 0);
+    if (stream_b) {
+        int64_t gb = args.n_items < int64_t(num_sms) * 8 ? args.n_items : int64_t(num_sms) * 8;
+        k_sym_small_block<256, 4096><<<static_cast<unsigned>(gb), 256, 0, stream_b>>>(args, seed, num_rows,
+                                                                                     draw ? 1 : 0);
+    }
     return cudaGetLastError();
 }
 
