@@ -950,12 +950,14 @@ int pipeline(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, bool draw, uint
             // call's profile to pick each item's kernel)
             if (beside && c->profile_max > kBin2Max) CU(cudaStreamWaitEvent(ss, c->ev_flop, 0));
             RC(run_small(c, d_rows, n, draw, seed, ss, &launches));
+            // phases: the FLOP pass ends at ev 1; ev 2 -> 3 is the symbolic
+            // kernels' remainder after it (the join)
+            ev_record(c, 1);
+            ev_record(c, 2);
             if (beside) {
                 CU(cudaEventRecord(c->join[0], ss));
                 CU(cudaStreamWaitEvent(c->stream, c->join[0], 0));
             }
-            ev_record(c, 1);
-            ev_record(c, 2);
         } else {
         if (draw) {
             CU(launch_sample(seed, c->a_rows, n, c->samples.p, ss));
