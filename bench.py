@@ -386,6 +386,7 @@ def run_ours(args, rank, world, local):
         for k in phase:
             phase[k] += t[k]
     P.set_profiling(False)
+    flop_kernel = P.last_flop_kernel()  # the timed steps' FLOP kernel (the e2e path's chunked upload uses tiles)
     step_ms = [s.elapsed_time(e) for s, e in ev]
     ms = float(sum(step_ms)) / args.steps
     ms_median = float(np.median(step_ms))  # SURVEY §8d asks for the median of >= 10 runs
@@ -506,9 +507,9 @@ def run_ours(args, rank, world, local):
             "execution": {"parallelism": f"A row-sharded x{world} (nnz-balanced), B replicated, "
                                          "1 NCCL all-reduce per step",
                           "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps",
-                          "flop_kernel": P.last_flop_kernel()},
+                          "flop_kernel": flop_kernel},
             "roofline": {"bound": "hbm",
-                         "kernel": "FLOP pass (k_degree + " + P.last_flop_kernel() + " [+ k_flop_fixup for tiles])",
+                         "kernel": "FLOP pass (k_degree + " + flop_kernel + " [+ k_flop_fixup for tiles])",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          # L2 hit rate of the pass (the degree gathers dominate its
