@@ -5,6 +5,23 @@
 
 namespace spnnz_gpu {
 
+// Device-side bounds checks (a build with -DSPNNZ_DEBUG_BOUNDS=1; the GPU
+// pool has compute-sanitizer closed): a violated index traps the kernel, so
+// the call fails loudly instead of reading or writing past a table.
+#ifndef SPNNZ_DEBUG_BOUNDS
+#define SPNNZ_DEBUG_BOUNDS 0
+#endif
+#if SPNNZ_DEBUG_BOUNDS
+#define SPNNZ_ASSERT(cond) \
+    do {                  \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define SPNNZ_ASSERT(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 constexpr int kWarp = 32;
 
 // SplitMix64 output number r (0-based) of a generator seeded with `seed`:

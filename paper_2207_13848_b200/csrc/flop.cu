@@ -718,6 +718,7 @@ k_flop_rb(RbArgs g, const uint16_t* __restrict__ bdeg, int32_t k_rows, PredOut p
     Emit emit{};
     if (PRED) emit = make_emit(pred);
     const auto deg = [&](int32_t c) -> int32_t {
+        SPNNZ_ASSERT(c >= 0 && c < k_rows);
         const int32_t v = SMEM ? s_deg[c] : gather_deg(bdeg + c, last);
         return v == 0xFFFF ? static_cast<int32_t>(__ldg(&g.brpt[c + 1]) - __ldg(&g.brpt[c])) : v;
     };
@@ -902,6 +903,7 @@ struct RsArgs {
     int64_t* __restrict__ flop;
     long long* __restrict__ totals;
     const unsigned* escapes;  // k_degree's flag (nullable: assume escapes)
+    int32_t k_rows;           // B's rows (the degree table's length; bounds checks)
 };
 
 template <bool PRED, bool ESC>
@@ -932,6 +934,7 @@ __device__ __forceinline__ void rs_warp(const RsArgs& g, const uint16_t* s_deg, 
         return v;
     };
     const auto deg = [&](int32_t c) -> S {
+        SPNNZ_ASSERT(c >= 0 && c < g.k_rows);
         const S v = s_deg[c];
         if (ESC && v == 0xFFFF) return static_cast<S>(__ldg(&g.brpt[c + 1]) - __ldg(&g.brpt[c]));
         return v;
@@ -1122,11 +1125,18 @@ __device__ __forceinline__ void rs_warp_fast(const RsArgs& g, const uint16_t* s_
             int x[8];
             if (c >= e0 && c + kRsChunk <= e1) {  // interior chunk: no masking
 #pragma unroll
-                for (int i = 0; i < 8; ++i) x[i] = s_deg[v.v[i]];
+                for (int i = 0; i < 8; ++i) {
+                    SPNNZ_ASSERT(v.v[i] >= 0 && v.v[i] < g.k_rows);
+                    x[i] = s_deg[v.v[i]];
+                }
             } else {
                 const int p = c + 8 * lane;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) x[i] = p + i >= e0 && p + i < e1 ? s_deg[v.v[i]] : 0;
+                for (int i = 0; i < 8; ++i) {
+                    const bool in = p + i >= e0 && p + i < e1;
+                    SPNNZ_ASSERT(!in || (v.v[i] >= 0 && v.v[i] < g.k_rows));
+                    x[i] = in ? s_deg[v.v[i]] : 0;
+                }
             }
 #pragma unroll
             for (int i = 1; i < 8; ++i) x[i] += x[i - 1];
@@ -1145,6 +1155,7 @@ __device__ __forceinline__ void rs_warp_fast(const RsArgs& g, const uint16_t* s_
                 // rows ending in (c, c + 256]: P(end) = base + prefix through
                 // the row's last entry
                 if (!res && re <= c + kRsChunk) {
+                    SPNNZ_ASSERT(re - c - 1 >= 0 && re - c - 1 < kRsChunk);
                     pend = base + xs[rs_slot(re - c - 1)];
                     res = true;
                 }
@@ -1804,6 +1815,7 @@ cudaError_t launch_flop_rows(const DevCsr& a, const uint16_t* bdeg, const int64_
         r.flop = flop;
         r.totals = totals;
         r.escapes = escapes;
+        r.k_rows = mode.b_rows;
         return pred.on() ? launch_rs<true>(r, bdeg, mode.b_rows, pred, mode, stream)
                          : launch_rs<false>(r, bdeg, mode.b_rows, pred, mode, stream);
     }

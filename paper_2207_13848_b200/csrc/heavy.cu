@@ -721,6 +721,7 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
                 for (int u = 0; u < UU; ++u)
                     if (valid[u]) {
                         const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
+                    SPNNZ_ASSERT((off >> 5) < static_cast<uint32_t>(words));
                         const uint32_t bit = 1u << (off & 31);
                         if (!kTestFirst || !(s_set[off >> 5] & bit)) atomicOr(&s_set[off >> 5], bit);
                     }
@@ -730,6 +731,7 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
             for (int u = 0; u < UU; ++u)
                 if (valid[u]) {
                     const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
+                    SPNNZ_ASSERT((off >> 5) < static_cast<uint32_t>(words));
                     const uint32_t bit = 1u << (off & 31);
                     if (!kTestFirst || !(s_set[off >> 5] & bit)) cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
                 }
@@ -851,6 +853,7 @@ __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, Sym
             for (int u = 0; u < kUnroll; ++u)
                 if (valid[u]) {
                     const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
+                    SPNNZ_ASSERT((off >> 5) < static_cast<uint32_t>(words));
                     const uint32_t bit = 1u << (off & 31);
                     if (!kTestFirst || !(s_set[off >> 5] & bit)) cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
                 }
@@ -1211,6 +1214,7 @@ __global__ void __launch_bounds__(kIvBlock, 2) k_heavy_intervals(SymArgs g, SymS
                                                   for (int v = 0; v < kUnroll; ++v)
                                                       if (valid[v]) {
                                                           const uint32_t off = static_cast<uint32_t>(keys[v] - c0);
+                                                          SPNNZ_ASSERT((off >> 5) < static_cast<uint32_t>(kIvSmem / 4));
                                                           const uint32_t bit = 1u << (off & 31);
                                                           cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
                                                       }

@@ -27,7 +27,13 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 // multiply-high range reduction so any table size works.
 __device__ __forceinline__ int hash_insert(int* table, uint32_t size, int key) {
     uint32_t h = __umulhi(mix32(static_cast<uint32_t>(key)), size);
+#if SPNNZ_DEBUG_BOUNDS
+    uint32_t probes = 0;
+#endif
     for (;;) {
+#if SPNNZ_DEBUG_BOUNDS
+        SPNNZ_ASSERT(++probes <= size);  // a full table would never terminate
+#endif
         const int cur = table[h];
         if (cur == key) return 0;
         if (cur == kEmpty) {
@@ -102,6 +108,7 @@ __device__ __forceinline__ void chunk_products(const OffT* off, const int64_t* b
                 if (nxt <= q) {
                     do {
                         ++e;
+                        SPNNZ_ASSERT(e < n);
                         nxt = off[e + 1];
                     } while (nxt <= q);
                     kb = static_cast<long long>(b0[e]) - static_cast<long long>(off[e]);
@@ -141,7 +148,13 @@ __device__ __forceinline__ void hash_clear(int* table, int size, int t, int nt) 
 // probe of the loop.
 __device__ __forceinline__ int hash_insert_shared(uint32_t table_s, uint32_t size, int key) {
     uint32_t h = __umulhi(mix32(static_cast<uint32_t>(key)), size);
+#if SPNNZ_DEBUG_BOUNDS
+    uint32_t probes = 0;
+#endif
     for (;;) {
+#if SPNNZ_DEBUG_BOUNDS
+        SPNNZ_ASSERT(++probes <= size);  // a full table would never terminate
+#endif
         const uint32_t addr = table_s + 4u * h;
         int cur;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(cur) : "r"(addr) : "memory");
