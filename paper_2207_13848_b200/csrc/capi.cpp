@@ -311,7 +311,7 @@ struct spnnz_gpu_ctx {
     int64_t list_cap = 0;
     DBuf<int64_t> heavy_unit_off, heavy_eoff, heavy_foff, heavy_epre, heavy_eb0, heavy_flops;
     DBuf<long long> heavy_rc, heavy_cur;
-    DBuf<int32_t> heavy_pbuf, heavy_utab;
+    DBuf<int32_t> heavy_pbuf, heavy_utab, heavy_slot_item;
     DBuf<int64_t> heavy_boff;                  // interval path (sorted B)
     DBuf<int32_t> heavy_bnd, heavy_unit_item, heavy_unit_e0;
     DBuf<int4> heavy_tasks;  // HeavyTask = 32 bytes = 2 x int4
@@ -416,7 +416,6 @@ int sym_scratch(spnnz_gpu_ctx* c, int64_t items, SymScratch* s) {
     s->heavy_eb0 = c->heavy_eb0.p;
     s->heavy_meta = c->heavy_meta.p;
     s->pool = c->pool.p;
-
     return SPNNZ_OK;
 }
 
@@ -479,6 +478,8 @@ int heavy_buffers(spnnz_gpu_ctx* c, int64_t count, int64_t ents, int64_t product
     s->heavy_tasks = c->heavy_tasks.p;
     s->heavy_task_cap = tasks;
     s->pool = c->pool.p;
+    RC(c->heavy_slot_item.ensure(std::max<int64_t>(slots, 1)));
+    s->heavy_slot_item = c->heavy_slot_item.p;
 
     return SPNNZ_OK;
 }

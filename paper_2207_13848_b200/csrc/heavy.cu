@@ -584,6 +584,7 @@ __global__ void __launch_bounds__(kPrivRanges) k_heavy_plan_units(SymScratch sc,
         const int32_t slot = parts > 1 ? static_cast<int32_t>(atomicAdd(
                                              reinterpret_cast<unsigned long long*>(&sc.heavy_meta[4]), 1ULL))
                                        : -1;
+        if (slot >= 0) sc.heavy_slot_item[slot] = static_cast<int32_t>(i);
         HeavyTask* out = reinterpret_cast<HeavyTask*>(sc.heavy_tasks) + s_base + excl;
         for (int q = 0; q < parts; ++q)
             out[q] = HeavyTask{static_cast<int32_t>(i), slot, r, r + 1, nu * q / parts, nu * (q + 1) / parts};
@@ -625,6 +626,7 @@ __global__ void __launch_bounds__(128) k_heavy_plan(SymScratch sc, int64_t count
             const int32_t slot = parts > 1 ? static_cast<int32_t>(atomicAdd(
                                                  reinterpret_cast<unsigned long long*>(&sc.heavy_meta[4]), 1ULL))
                                            : -1;
+            if (slot >= 0) sc.heavy_slot_item[slot] = static_cast<int32_t>(i);
             HeavyTask* out = tasks + s_base + excl;
             for (int q = 0; q < parts; ++q) {
                 const long long p = a + q * kTaskProducts;
@@ -649,6 +651,7 @@ __global__ void k_heavy_tasks_r1(SymScratch sc, int64_t count, int64_t task_cap)
     const int32_t slot = parts > 1 ? static_cast<int32_t>(atomicAdd(
                                          reinterpret_cast<unsigned long long*>(&sc.heavy_meta[4]), 1ULL))
                                    : -1;
+    if (slot >= 0) sc.heavy_slot_item[slot] = static_cast<int32_t>(i);
     HeavyTask* out = reinterpret_cast<HeavyTask*>(sc.heavy_tasks) + base;
     for (long long q = 0; q < parts; ++q) {
         const long long a = q * kTaskProducts;
@@ -656,29 +659,47 @@ __global__ void k_heavy_tasks_r1(SymScratch sc, int64_t count, int64_t task_cap)
     }
 }
 
-// ORs a task's shared bitmap into its merge slot and counts the bits it set
-// first.  The returning global atomics are issued kMergeBatch at a time
-// before any result is used: one after another each waited a full L2 round
-// trip (a 32 K-word slot = 32 dependent atomics per thread of a 1024-thread
-// block, ~30 us per task at config 2, where the largest rows split into ~30
-// tasks).
-constexpr int kMergeBatch = 8;
+// ORs a task's shared bitmap into its merge slot: non-returning reductions
+// (red.global.or, ~1.6x the returning atomics' rate in L2, and no thread
+// waits for a result); the slot's bits are counted once, after every task
+// that shares it has merged (k_heavy_slot_count).  (Counting each task's
+// first-set bits needed the returning atomic per word: at config 2 the largest
+// rows split into ~30 tasks, 32 K words each.)
 template <int BLOCK>
-__device__ __forceinline__ int merge_words(const uint32_t* s_set, uint32_t* gbm, int32_t words) {
-    int cnt = 0;
-    for (int k0 = threadIdx.x; k0 < words; k0 += BLOCK * kMergeBatch) {
-        uint32_t w[kMergeBatch], old[kMergeBatch];
-#pragma unroll
-        for (int b = 0; b < kMergeBatch; ++b) {
-            const int k = k0 + b * BLOCK;
-            w[b] = k < words ? s_set[k] : 0u;
-        }
-#pragma unroll
-        for (int b = 0; b < kMergeBatch; ++b) old[b] = w[b] ? atomicOr(&gbm[k0 + b * BLOCK], w[b]) : ~0u;
-#pragma unroll
-        for (int b = 0; b < kMergeBatch; ++b) cnt += __popc(w[b] & ~old[b]);
+__device__ __forceinline__ void merge_words(const uint32_t* s_set, uint32_t* gbm, int32_t words) {
+    for (int k = threadIdx.x; k < words; k += BLOCK) {
+        const uint32_t w = s_set[k];
+        if (w) asm volatile("red.global.or.b32 [%0], %1;" ::"l"(gbm + k), "r"(w) : "memory");
     }
-    return cnt;
+}
+
+// One block per used merge slot: the distinct columns its tasks found
+// together, added to the slot's item and to the total.
+constexpr int kSlotBlock = 256;
+__global__ void __launch_bounds__(kSlotBlock) k_heavy_slot_count(SymArgs g, SymScratch sc, int64_t first,
+                                                                 int64_t slot_words) {
+    __shared__ long long s_red[kSlotBlock / 32];
+    const long long used = sc.heavy_meta[4];
+    const int32_t* list = heavy_list(sc, first);
+    for (long long sl = blockIdx.x; sl < used; sl += gridDim.x) {
+        const uint4* w4 = reinterpret_cast<const uint4*>(sc.pool + sl * slot_words);
+        long long c = 0;
+        for (int64_t k = threadIdx.x; k < slot_words / 4; k += kSlotBlock) {
+            const uint4 v = w4[k];
+            c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+        }
+        for (int64_t k = (slot_words & ~int64_t(3)) + threadIdx.x; k < slot_words; k += kSlotBlock)
+            c += __popc(sc.pool[sl * slot_words + k]);
+        const long long tot = block_sum_ll<kSlotBlock>(c, s_red);
+        if (threadIdx.x == 0 && tot) {
+            if (g.out)
+                atomicAdd(reinterpret_cast<unsigned long long*>(&g.out[list[sc.heavy_slot_item[sl]]]),
+                          static_cast<unsigned long long>(tot));
+            atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[g.total_slot]),
+                      static_cast<unsigned long long>(tot));
+        }
+        __syncthreads();
+    }
 }
 
 // ---- 5. run the tasks: one block per task, a shared bitmap over the span,
@@ -774,7 +795,8 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
             // span shared by several tasks: the bits this task adds first
             cnt = 0;
             uint32_t* gbm = sc.pool + int64_t(t.slot) * slot_words;
-            cnt = merge_words<kRunBlock>(s_set, gbm, words);
+            merge_words<kRunBlock>(s_set, gbm, words);
+            cnt = 0;  // the slot's bits are counted once all its tasks are in (k_heavy_slot_count)
             __syncthreads();  // the merge scan has read the bitmap
         }
         cnt = static_cast<int>(warp_sum_ll(cnt));
@@ -885,7 +907,8 @@ __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, Sym
             // span shared by several tasks: the bits this task adds first
             cnt = 0;
             uint32_t* gbm = sc.pool + int64_t(t.slot) * slot_words;
-            cnt = merge_words<kRunBlock>(s_set, gbm, words);
+            merge_words<kRunBlock>(s_set, gbm, words);
+            cnt = 0;  // the slot's bits are counted once all its tasks are in (k_heavy_slot_count)
             __syncthreads();  // the merge scan has read the bitmap
         }
         cnt = static_cast<int>(warp_sum_ll(cnt));
@@ -1403,8 +1426,9 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
             args, s, first, R, geo.wshift, geo.wwords);
         n += 2;
     }
+    k_heavy_slot_count<<<sms * 4, kSlotBlock, 0, stream>>>(args, s, first, int64_t(geo.wwords));
     k_heavy_clean<<<sms * 4, 256, 0, stream>>>(s, int64_t(geo.wwords));
-    if (launches) *launches += n + 1;
+    if (launches) *launches += n + 2;
     return cudaGetLastError();
 }
 

@@ -207,6 +207,7 @@ struct SymScratch {
     void* heavy_tasks = nullptr;         // HeavyTask[heavy_task_cap]
     int64_t heavy_task_cap = 0;
     uint32_t* pool = nullptr;            // merge bitmaps (W bits each), zero between calls
+    int32_t* heavy_slot_item = nullptr;  // per merge slot: the batch item it belongs to
     long long* heavy_meta = nullptr;     // kHeavyMeta slots: [0] units [1] sum(len+1)
                                          // [2] sum(flop) of heavy rows [3] tasks [4] merge
                                          // slots used [5] sum((P-1) len) [6] sum(P) of heavy
