@@ -58,7 +58,10 @@ constexpr int kSpanShift = 20;            // R == 1: one span of <= 2^20 columns
 constexpr int kTaskSpanShift = SPNNZ_SPAN_SHIFT;  // R > 1: task spans of <= 2^19 columns (64 KB)
 constexpr int kPrivRanges = 256;          // per-warp histograms up to this R
 constexpr int kMaxRanges = 4096;          // B.cols < 2^31 with W = 2^19
-constexpr int64_t kTaskProducts = 131072;
+#ifndef SPNNZ_TASK_PRODUCTS
+#define SPNNZ_TASK_PRODUCTS 131072
+#endif
+constexpr int64_t kTaskProducts = SPNNZ_TASK_PRODUCTS;
 // A/B knob: bitmap inserts that read the word first and skip the atomic when
 // the bit is already set (a duplicate product).  Measured slower (config 2
 // symbolic 299 vs 282 us, where 57 % of the products are duplicates), so off.
@@ -673,23 +676,47 @@ __device__ __forceinline__ void merge_words(const uint32_t* s_set, uint32_t* gbm
     }
 }
 
-// One block per used merge slot: the distinct columns its tasks found
-// together, added to the slot's item and to the total.
+// The used merge slots, cut into parts of kSlotPart words, one part per
+// block at a time: the distinct columns its tasks found together (a partial
+// count per part, added to the slot's item and to the total), the words
+// zeroed on the way (the pool stays all-zero between calls).
 constexpr int kSlotBlock = 256;
+constexpr int64_t kSlotPart = 4096;  // words per part: 4 uint4 per thread
 __global__ void __launch_bounds__(kSlotBlock) k_heavy_slot_count(SymArgs g, SymScratch sc, int64_t first,
                                                                  int64_t slot_words) {
     __shared__ long long s_red[kSlotBlock / 32];
     const long long used = sc.heavy_meta[4];
     const int32_t* list = heavy_list(sc, first);
-    for (long long sl = blockIdx.x; sl < used; sl += gridDim.x) {
-        const uint4* w4 = reinterpret_cast<const uint4*>(sc.pool + sl * slot_words);
+    const int64_t parts = (slot_words + kSlotPart - 1) / kSlotPart;
+    for (long long it = blockIdx.x; it < used * parts; it += gridDim.x) {
+        const long long sl = it / parts;
+        const int64_t w0 = (it % parts) * kSlotPart;
+        const int64_t w1 = w0 + kSlotPart < slot_words ? w0 + kSlotPart : slot_words;
+        uint32_t* w = sc.pool + sl * slot_words;
         long long c = 0;
-        for (int64_t k = threadIdx.x; k < slot_words / 4; k += kSlotBlock) {
-            const uint4 v = w4[k];
-            c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+        if (((w1 - w0) & 3) == 0 && (w0 & 3) == 0) {
+            uint4* v4 = reinterpret_cast<uint4*>(w + w0);
+            const int n4 = static_cast<int>((w1 - w0) >> 2);
+            uint4 v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int q = threadIdx.x + k * kSlotBlock;
+                v[k] = q < n4 ? v4[q] : make_uint4(0u, 0u, 0u, 0u);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int q = threadIdx.x + k * kSlotBlock;
+                if (q < n4) {
+                    c += __popc(v[k].x) + __popc(v[k].y) + __popc(v[k].z) + __popc(v[k].w);
+                    v4[q] = make_uint4(0u, 0u, 0u, 0u);
+                }
+            }
+        } else {
+            for (int64_t k = w0 + threadIdx.x; k < w1; k += kSlotBlock) {
+                c += __popc(w[k]);
+                w[k] = 0u;
+            }
         }
-        for (int64_t k = (slot_words & ~int64_t(3)) + threadIdx.x; k < slot_words; k += kSlotBlock)
-            c += __popc(sc.pool[sl * slot_words + k]);
         const long long tot = block_sum_ll<kSlotBlock>(c, s_red);
         if (threadIdx.x == 0 && tot) {
             if (g.out)
@@ -1271,14 +1298,6 @@ __global__ void k_heavy_flops(SymArgs g, SymScratch sc, int64_t count, int64_t* 
     out[2 * count + i] = (interval_geometry(g.bcols).count - 1) * L;
 }
 
-// ---- 6. return the used merge bitmaps to zero
-__global__ void k_heavy_clean(SymScratch sc, int64_t slot_words) {
-    const long long used = sc.heavy_meta[4] * slot_words;
-    for (long long i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < used;
-         i += int64_t(gridDim.x) * blockDim.x)
-        sc.pool[i] = 0u;
-}
-
 int sort_smem(int R) { return int(2 * kHeavyUnitProducts * 4 + ((kHW + 1) * R + 1) * 4); }
 
 int place_smem() { return int(kMaxRanges * 8 + 2 * kHeavyUnitProducts * 4 + kMaxRanges * 4 + (kMaxRanges + 1) * 4); }
@@ -1427,8 +1446,7 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
         n += 2;
     }
     k_heavy_slot_count<<<sms * 4, kSlotBlock, 0, stream>>>(args, s, first, int64_t(geo.wwords));
-    k_heavy_clean<<<sms * 4, 256, 0, stream>>>(s, int64_t(geo.wwords));
-    if (launches) *launches += n + 2;
+    if (launches) *launches += n + 1;
     return cudaGetLastError();
 }
 
