@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kPrepBlock) k_heavy_prep(SymArgs g, SymScratch
         sc.heavy_meta[4] = 0;  // merge slots
         sc.heavy_meta[7] = 0;  // interval-task cursor
         sc.heavy_meta[8] = 0;  // small tasks
+        sc.heavy_meta[10] = 0;  // k_heavy_run's task ticket
     }
 }
 
@@ -751,10 +752,18 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
                                     : static_cast<int32_t>((int64_t(g.bcols) + 31) / 32);
     for (int k = threadIdx.x; k < max_words; k += kRunBlock) s_set[k] = 0u;
     long long acc = 0;
-    for (long long ti = blockIdx.x; ti < ntask; ti += gridDim.x) {
+    // tasks by ticket (a few hundred atomics): a block that starts late --
+    // its SM still busy with a tier kernel -- takes fewer instead of holding
+    // a fixed share back
+    __shared__ long long s_ti;
+    for (;;) {
         __syncthreads();  // previous task's clear is complete
-        if (threadIdx.x == 0) s_task = tasks[ti];
+        if (threadIdx.x == 0) {
+            s_ti = static_cast<long long>(atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[10]), 1ULL));
+            if (s_ti < ntask) s_task = tasks[s_ti];
+        }
         __syncthreads();
+        if (s_ti >= ntask) break;
         const HeavyTask t = s_task;
         const int32_t col_base = R > 1 ? (t.r0 << wshift) : 0;
         const int32_t words = R > 1 ? ((t.r1 - t.r0) << (wshift - 5)) : max_words;
@@ -881,17 +890,27 @@ __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, Sym
         }
     };
     long long acc = 0;
-    long long ti = blockIdx.x;
+    // tasks by ticket (as k_heavy_run); the next ticket and its descriptor
+    // are taken while the current task runs
+    __shared__ long long s_tk;
+    const auto ticket = [&]() -> long long {
+        __syncthreads();
+        if (threadIdx.x == 0)
+            s_tk = static_cast<long long>(atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[10]), 1ULL));
+        __syncthreads();
+        return s_tk;
+    };
+    long long ti = ticket();
     HeavyTask tn{};
     int nlo = 0, nhi = 0;
     if (ti < ntask) {
         tn = tasks[ti];
         fetch(tn, nlo, nhi);
     }
-    for (; ti < ntask; ti += gridDim.x) {
+    while (ti < ntask) {
         const HeavyTask t = tn;
         int lo = nlo, hi = nhi;
-        const long long tj = ti + gridDim.x;
+        const long long tj = ticket();
         if (tj < ntask) tn = tasks[tj];  // in flight during this task
         const int32_t col_base = t.r0 << wshift;
         const int32_t words = (t.r1 - t.r0) << (wshift - 5);
@@ -947,6 +966,7 @@ __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, Sym
         }
         uint4* s4 = reinterpret_cast<uint4*>(s_set);
         for (int k = threadIdx.x; k < (words >> 2); k += kRunBlock) s4[k] = make_uint4(0u, 0u, 0u, 0u);
+        ti = tj;
     }
     if (lane == 0 && acc)
         atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[g.total_slot]),
