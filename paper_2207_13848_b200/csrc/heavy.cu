@@ -152,7 +152,8 @@ __global__ void __launch_bounds__(kPrepBlock) k_heavy_prep(SymArgs g, SymScratch
         sc.heavy_meta[4] = 0;  // merge slots
         sc.heavy_meta[7] = 0;  // interval-task cursor
         sc.heavy_meta[8] = 0;  // small tasks
-        sc.heavy_meta[10] = 0;  // k_heavy_run's task ticket
+        sc.heavy_meta[10] = 0;  // the bitmap runs' task ticket
+        sc.heavy_meta[11] = 0;  // k_heavy_run_small's task ticket
     }
 }
 
@@ -978,6 +979,7 @@ __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, Sym
 // 4096-slot shared hash and its own named barrier, so an SM keeps twelve
 // small tasks in flight instead of three bitmap tasks.
 constexpr int kSG = 128, kSGroups = 4, kSSlots = 4096;
+constexpr int kSmallGrab = 2;  // small tasks per ticket
 
 __device__ __forceinline__ void group_sync(int grp) {
     asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(kSG) : "memory");
@@ -995,7 +997,22 @@ __global__ void __launch_bounds__(kSG * kSGroups, 3) k_heavy_run_small(SymArgs g
     const long long ntask = sc.heavy_meta[8];
     const int32_t* list = heavy_list(sc, first);
     long long acc = 0;
-    for (long long ti = blockIdx.x * int64_t(kSGroups) + grp; ti < ntask; ti += int64_t(gridDim.x) * kSGroups) {
+    // tasks by ticket, kSmallGrab per atomic (thousands of small tasks: one
+    // counter, a few thousand atomics)
+    __shared__ long long s_tk[kSGroups];
+    long long tk = 0, tk_end = 0;
+    for (;;) {
+        if (tk == tk_end) {
+            group_sync(grp);
+            if (gt == 0)
+                s_tk[grp] = static_cast<long long>(
+                    atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[11]), static_cast<unsigned long long>(kSmallGrab)));
+            group_sync(grp);
+            tk = s_tk[grp];
+            tk_end = tk + kSmallGrab;
+        }
+        if (tk >= ntask) break;
+        const long long ti = tk++;
         const HeavyTask t = *(tasks - ti);
         hash_clear(table, kSSlots, gt, kSG);
         const long long ubase = sc.heavy_unit_off[t.item];
