@@ -439,9 +439,15 @@ cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_s
     const unsigned sms = static_cast<unsigned>(num_sms);
     k_sym_tiny<256><<<sms * 4, 256, 0, streams[0]>>>(args, s);
     k_sym_warp_hash<256><<<sms * 4, 256, 0, streams[0]>>>(args, s);
-    k_sym_block_hash<kT3Block, kT3Slots, 3, SPNNZ_T3_UNROLL><<<sms * 8, kT3Block, kT3Slots * 4, streams[1]>>>(args, s);
-    k_sym_block_hash<kT4Block, kT4Slots, 4, SPNNZ_T4_UNROLL><<<sms * SPNNZ_T4_BLOCKS_PER_SM, kT4Block, kT4Slots * 4, streams[2]>>>(args, s);
-    k_sym_block_hash<kT5Block, kT5Slots, 5, SPNNZ_T5_UNROLL><<<sms, kT5Block, kT5Slots * 4, streams[3]>>>(args, s);
+    // grid multiple (A/B knob SPNNZ_TIER_WAVES): more, shorter blocks over
+    // the same rows free SMs between rows (for higher-priority work)
+    static const int waves = [] {
+        const char* e = getenv("SPNNZ_TIER_WAVES");
+        return e && atoi(e) > 0 ? atoi(e) : 1;
+    }();
+    k_sym_block_hash<kT3Block, kT3Slots, 3, SPNNZ_T3_UNROLL><<<sms * 8 * waves, kT3Block, kT3Slots * 4, streams[1]>>>(args, s);
+    k_sym_block_hash<kT4Block, kT4Slots, 4, SPNNZ_T4_UNROLL><<<sms * SPNNZ_T4_BLOCKS_PER_SM * waves, kT4Block, kT4Slots * 4, streams[2]>>>(args, s);
+    k_sym_block_hash<kT5Block, kT5Slots, 5, SPNNZ_T5_UNROLL><<<sms * waves, kT5Block, kT5Slots * 4, streams[3]>>>(args, s);
     return cudaGetLastError();
 }
 
