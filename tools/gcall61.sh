@@ -1,0 +1,17 @@
+mkdir -p gpurun_out; rm -f gpurun_out/rep_*.log
+for rep in 1 2; do for c in 5 2; do
+  for v in base p1 w4 p1w4 p1w8; do
+    case $v in base) E="";; p1) E="SPNNZ_STREAM_PRIO=1";; w4) E="SPNNZ_TIER_WAVES=4";; p1w4) E="SPNNZ_STREAM_PRIO=1 SPNNZ_TIER_WAVES=4";; p1w8) E="SPNNZ_STREAM_PRIO=1 SPNNZ_TIER_WAVES=8";; esac
+    env $E python bench.py --config $c --no-e2e --no-cpu-baseline --no-accuracy > gpurun_out/rep_${c}_${v}_$rep.log 2>&1
+  done
+done; done
+python - <<'PY'
+import json,glob,collections
+r=collections.defaultdict(list)
+for f in glob.glob('gpurun_out/rep_*.log'):
+    _,c,v,k=f[:-4].split('/')[-1].split('_')
+    try: r[(c,v)].append(round(json.loads(open(f).read().strip().splitlines()[-1])['ms_per_step']*1000,1))
+    except Exception as e: print(f,e)
+for k in sorted(r): print(k, sorted(r[k]))
+PY
+SPNNZ_STREAM_PRIO=1 SPNNZ_TIER_WAVES=4 python tools/timeline.py 5 3 2>&1 | grep -E "timeline|heavy " | tail -7
