@@ -576,12 +576,46 @@ __global__ void __launch_bounds__(kPrivRanges) k_heavy_plan_units(SymScratch sc,
     if (threadIdx.x == 0)
         s_base = static_cast<long long>(atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[3]),
                                                   static_cast<unsigned long long>(total)));
+    __shared__ long long s_cnt[kPrivRanges];
+    __shared__ int s_g0[kPrivRanges], s_g1[kPrivRanges];
+    s_cnt[r] = cnt;
     __syncthreads();
-    if (small) {  // small ranges: a list of their own, filled from the end of the array
-        const long long k = static_cast<long long>(
-            atomicAdd(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[8]), 1ULL));
-        reinterpret_cast<HeavyTask*>(sc.heavy_tasks)[task_cap - 1 - k] =
-            HeavyTask{static_cast<int32_t>(i), -1, r, r + 1, 0, nu};
+    if (threadIdx.x == 0) {
+        // small ranges: a list of their own, filled from the end of the array;
+        // consecutive small (and empty) ranges share one task up to
+        // kSmallTaskProducts products (fewer tasks each reading every unit's
+        // table; the 4096-slot hash holds any 2048 products at load <= 1/2)
+        int ng = 0;
+        const auto emit_small = [&](int r0, int r1) {
+            s_g0[ng] = r0;
+            s_g1[ng++] = r1;
+        };
+        int g0 = 0;
+        long long gsum = 0;
+        for (int q = 0; q < R; ++q) {
+            const long long c = s_cnt[q];
+            if (c > kSmallTaskProducts) {  // a bitmap task: closes the group
+                if (gsum > 0) emit_small(g0, q);
+                g0 = q + 1;
+                gsum = 0;
+                continue;
+            }
+            if (gsum > 0 && gsum + c > kSmallTaskProducts) {
+                emit_small(g0, q);
+                g0 = q;
+                gsum = 0;
+            }
+            gsum += c;
+        }
+        if (gsum > 0) emit_small(g0, R);
+        // one reservation per item for its groups
+        const long long k0 = ng ? static_cast<long long>(atomicAdd(
+                                      reinterpret_cast<unsigned long long*>(&sc.heavy_meta[8]),
+                                      static_cast<unsigned long long>(ng)))
+                                : 0;
+        for (int q = 0; q < ng; ++q)
+            reinterpret_cast<HeavyTask*>(sc.heavy_tasks)[task_cap - 1 - (k0 + q)] =
+                HeavyTask{static_cast<int32_t>(i), -1, s_g0[q], s_g1[q], 0, nu};
     }
     __syncthreads();
     if (s_base + total + sc.heavy_meta[8] > task_cap) __trap();  // host sizes task_cap to heavy_task_bound()
