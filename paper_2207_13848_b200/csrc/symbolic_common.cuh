@@ -146,8 +146,20 @@ __device__ __forceinline__ void hash_clear(int* table, int size, int t, int nt) 
 // hash_insert on a 32-bit shared-window address: the generic-pointer form
 // re-derives the shared window (S2R SR_CgaCtaId + 64-bit arithmetic) on every
 // probe of the loop.
+#ifndef SPNNZ_HASH_FIB
+#define SPNNZ_HASH_FIB 1
+#endif
+// slot hash: one Fibonacci multiply (default; config 5 step -13 us) or mix32 (A/B knob)
+__device__ __forceinline__ uint32_t slot_hash(int key) {
+#if SPNNZ_HASH_FIB
+    return static_cast<uint32_t>(key) * 0x9E3779B1u;
+#else
+    return mix32(static_cast<uint32_t>(key));
+#endif
+}
+
 __device__ __forceinline__ int hash_insert_shared(uint32_t table_s, uint32_t size, int key) {
-    uint32_t h = __umulhi(mix32(static_cast<uint32_t>(key)), size);
+    uint32_t h = __umulhi(slot_hash(key), size);
 #if SPNNZ_DEBUG_BOUNDS
     uint32_t probes = 0;
 #endif
