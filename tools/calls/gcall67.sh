@@ -1,6 +1,6 @@
 mkdir -p gpurun_out; rm -f gpurun_out/ab_*.log gpurun_out/ab_*_r*.txt
-SPNNZ_GPU_LIB=build/var_cas/libspnnz_gpu.so timeout 900 python -m pytest tests -m gpu -x -q -k "bin or config_vs or small or trials" > gpurun_out/t67.log 2>&1; echo "cas tests rc=$?"; tail -1 gpurun_out/t67.log
-for rep in 1 2; do for c in 5 2; do bash tools/ab.sh $c cas; for f in gpurun_out/ab_${c}_*.log; do cp $f ${f%.log}_r$rep.txt; done; done; done
+timeout 900 python -m pytest tests -m gpu -x -q -k "heavy or bin or config_vs or batching" > gpurun_out/t67.log 2>&1; echo "nopc tests rc=$?"; tail -1 gpurun_out/t67.log
+for rep in 1 2; do for c in 5 2; do bash tools/ab.sh $c nopc; for f in gpurun_out/ab_${c}_*.log; do cp $f ${f%.log}_r$rep.txt; done; done; done
 for f in gpurun_out/ab_*_r*.txt; do python - "$f" <<'PY'
 import json,sys
 try:
