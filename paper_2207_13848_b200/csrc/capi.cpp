@@ -301,6 +301,7 @@ struct spnnz_gpu_ctx {
     DBuf<unsigned long long> flop_sched;  // k_flop_smem tile tickets (zeroed once, kept zero)
     DBuf<uint16_t> deg;  // uint16 row lengths of B (rebuilt every FLOP pass)
     DBuf<unsigned> deg_escapes;  // 1 when some B row has >= 65535 entries (row-block kernels)
+    uint64_t esc_epoch = ~0ull;   // the load whose B deg_escapes was last zeroed for
     DBuf<long long> tile_carry, tile_total, tile_max;
     DBuf<long long> totals;
     DBuf<long long> totals_table;  // world x kTotals: the all-reduce's all-gather table
@@ -716,6 +717,10 @@ int flop_pass_impl(spnnz_gpu_ctx* c, int64_t* launches, cudaStream_t stream, con
     if (rb) {
         int64_t nk = 0;
         RC(c->deg_escapes.ensure(1));
+        if (c->esc_epoch != c->epoch) {  // k_degree only ever raises the flag for the same B
+            CU(cudaMemsetAsync(c->deg_escapes.p, 0, sizeof(unsigned), stream));
+            c->esc_epoch = c->epoch;
+        }
         CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, stream, nullptr, nullptr, &nk,
                          c->deg_escapes.p));
         CU(launch_flop_rows(a, c->deg.p, c->b_rpt.p, out->p, c->totals.p, stream, pred, mode, c->deg_escapes.p));
@@ -1827,10 +1832,14 @@ int run_common(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n, double p, boo
                     CU(cudaGraphLaunch(c->gexec, c->stream));
                     ran = true;
                 } else {
+                    if (getenv("SPNNZ_DEBUG_GRAPH"))
+                        fprintf(stderr, "spnnz_gpu: graph instantiate failed: %s\n", cudaGetErrorString(ie));
                     cudaGetLastError();
                     c->gexec = nullptr;
                 }
             } else {
+                if (getenv("SPNNZ_DEBUG_GRAPH"))
+                    fprintf(stderr, "spnnz_gpu: graph capture failed: rc %d, %s\n", rc, cudaGetErrorString(ce));
                 if (graph) cudaGraphDestroy(graph);
                 cudaGetLastError();
                 if (c->gexec) {

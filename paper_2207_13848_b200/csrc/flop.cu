@@ -1626,7 +1626,8 @@ cudaError_t launch_degree(const int64_t* brpt, int64_t k_rows, uint16_t* deg, in
     if (k_rows == 0) return cudaSuccess;
     const TileMarks mk = fuse ? tile_marks(*a, *s, a->rpt - brpt) : TileMarks();
     if (reinterpret_cast<uintptr_t>(brpt) & 15) return cudaErrorMisalignedAddress;  // cudaMalloc'd
-    if (escapes) cudaMemsetAsync(escapes, 0, sizeof(unsigned), stream);
+    // (escapes: zeroed by the caller once per loaded B -- the flag only ever
+    // goes 0 -> 1 for the same B, so no per-call reset is needed)
     k_degree<<<stream_grid((k_rows + 3) / 4, num_sms), 256, 0, stream>>>(brpt, k_rows, deg, mk, escapes);
     if (launches) ++*launches;
     return cudaGetLastError();
