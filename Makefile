@@ -40,7 +40,7 @@ $(BUILD)/test_dropin: tests/cpp/test_dropin.cpp include/spnnz_gpu/spnnz_gpu.hpp 
 # C++ drop-in with the reference's own types (test infrastructure: built only
 # where the reference headers exist, like oracle/_ref; run on a GPU box)
 REF_INC ?= /root/reference/proj/include
-dropin_ref:
+dropin_ref: $(OUT)/libspnnz_gpu.so
 	@if [ -d "$(REF_INC)/spnnz" ]; then \
 	  $(MAKE) --no-print-directory $(BUILD)/test_dropin_ref; \
 	else echo "reference headers absent: skipping build/test_dropin_ref"; fi
