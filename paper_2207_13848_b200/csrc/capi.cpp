@@ -1984,15 +1984,21 @@ int spnnz_gpu_probe_flop_floor(spnnz_gpu_ctx* c, int reps, double* stream_ms, do
     if (reps < 1) return set_err(SPNNZ_EINVAL, "probe: reps must be >= 1");
     RC(c->deg.ensure(int64_t(c->b_rows) + 8));
     DBuf<long long> out;
-    RC(out.ensure(std::max<int64_t>(c->a.nnz / 16, 1)));
+    RC(out.ensure(std::max<int64_t>(std::max<int64_t>(c->a.nnz / 16, int64_t(c->num_sms) * 1024), 1)));
     CU(launch_degree(c->b_rpt.p, c->b_rows, c->deg.p, c->num_sms, c->stream));
     double* res[2] = {stream_ms, gather_ms};
+    // the loads of the kernel the FLOP pass picks for this matrix: the row
+    // streams' shape with its shared-memory table, else the tile kernel's
+    const bool table = pattern_table_applies(c->a, c->b_rows, c->rows_mode);
+    const bool nol1 = flop_gather_nol1(c);
+    const auto probe = [&](bool gather) {
+        return table ? launch_pattern_table(c->a, c->deg.p, c->b_rows, c->num_sms, gather, out.p, c->stream)
+                     : launch_pattern(c->a, c->deg.p, gather, nol1, out.p, c->stream);
+    };
     for (int g = 0; g < 2; ++g) {
-        // the loads of the tile kernel the FLOP pass would pick for this matrix
-        const bool nol1 = flop_gather_nol1(c);
-        CU(launch_pattern(c->a, c->deg.p, g == 1, nol1, out.p, c->stream));  // warm-up
+        CU(probe(g == 1));  // warm-up
         CU(cudaEventRecord(c->ev[0], c->stream));
-        for (int i = 0; i < reps; ++i) CU(launch_pattern(c->a, c->deg.p, g == 1, nol1, out.p, c->stream));
+        for (int i = 0; i < reps; ++i) CU(probe(g == 1));
         CU(cudaEventRecord(c->ev[1], c->stream));
         CU(cudaEventSynchronize(c->ev[1]));
         float ms = 0;

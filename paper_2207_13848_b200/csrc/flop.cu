@@ -1500,6 +1500,76 @@ __global__ void __launch_bounds__(128, 10) k_pattern(const int32_t* __restrict__
     out[t] = s;
 }
 
+// The same instrumentation for the row-stream pass (k_flop_rs): one
+// 1024-thread block per SM copies the uint16 degree table into shared memory,
+// each warp streams a contiguous slice of A.col as 256-entry chunks (one
+// 32-byte load per lane, kRsAhead8 chunks in flight) and, with GATHER, gathers
+// the eight degrees of each from the shared table.  No row logic (no scan, no
+// scratch, no A.rpt, no flop written): the floor the loads and the shared
+// gathers set for that kernel's shape.
+template <bool GATHER>
+__global__ void __launch_bounds__(kRsThreads, 1)
+k_pattern_table(const int32_t* __restrict__ col, int64_t base, int64_t nnz, const uint16_t* __restrict__ bdeg,
+                int32_t k_rows, long long* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    uint16_t* s_deg = reinterpret_cast<uint16_t*>(s_raw + kRsScratch);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (GATHER) {
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(s_deg));
+        const int words = (k_rows + 7) >> 3;
+        for (int i = threadIdx.x; i < words; i += blockDim.x)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * i),
+                         "l"(reinterpret_cast<const int4*>(bdeg) + i)
+                         : "memory");
+    }
+    const uint64_t first = policy_evict_first();
+    const int64_t warps = int64_t(gridDim.x) * (kRsThreads / 32);
+    const int64_t w = blockIdx.x * int64_t(kRsThreads / 32) + warp;
+    // whole 256-entry chunks, 32-byte aligned, split evenly over the warps
+    const int64_t a0 = (base + 7) & ~int64_t(7);
+    const int64_t chunks = (base + nnz - a0) / kRsChunk;
+    const int64_t c_lo = chunks * w / warps, c_hi = chunks * (w + 1) / warps;
+    const int32_t* p = col + a0 + c_lo * kRsChunk + 8 * lane;
+    const int n = static_cast<int>(c_hi - c_lo);
+    struct V8 {
+        int v[8];
+    };
+    const auto load = [&](int c) -> V8 {
+        V8 r;
+        if (c < n) {
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                         : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+                           "=r"(r.v[6]), "=r"(r.v[7])
+                         : "l"(p + int64_t(c) * kRsChunk), "l"(first));
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) r.v[k] = 0;
+        }
+        return r;
+    };
+    V8 buf[kRsAhead8];
+#pragma unroll
+    for (int k = 0; k < kRsAhead8; ++k) buf[k] = load(k);
+    if (GATHER) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+    }
+    long long s = 0;
+    for (int c0 = 0; c0 < n; c0 += kRsAhead8) {
+#pragma unroll
+        for (int k = 0; k < kRsAhead8; ++k) {
+            const V8 v = buf[k];
+            buf[k] = load(c0 + k + kRsAhead8);
+            if (c0 + k >= n) continue;
+            int x = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x += GATHER ? static_cast<int>(s_deg[v.v[i]]) : v.v[i];
+            s += x;
+        }
+    }
+    out[blockIdx.x * int64_t(kRsThreads) + threadIdx.x] = s;
+}
+
 }  // namespace
 
 cudaError_t launch_pattern(const DevCsr& a, const uint16_t* deg, bool gather, bool nol1, long long* out,
@@ -1866,6 +1936,29 @@ cudaError_t launch_check_rows(const int32_t* rows, int64_t n, int32_t num_rows, 
                               cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
     k_check_rows<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(rows, n, num_rows, bad);
+    return cudaGetLastError();
+}
+
+bool pattern_table_applies(const DevCsr& a, int32_t k_rows, bool rows_mode) {
+    return !rows_mode && flop_rb_smem_fits(k_rows) && flop_rs_on() &&
+           a.nnz < (int64_t(1) << 31) - (int64_t(1) << 16) && a.nnz >= kRsChunk;
+}
+
+cudaError_t launch_pattern_table(const DevCsr& a, const uint16_t* deg, int32_t k_rows, int num_sms, bool gather,
+                                 long long* out, cudaStream_t stream) {
+    static std::atomic<unsigned long long> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_done.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
+        cudaFuncSetAttribute(k_pattern_table<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(227 * 1024 - kSmemStatic));
+        attr_done.fetch_or(1ull << (dev & 63), std::memory_order_release);
+    }
+    if (gather)
+        k_pattern_table<true><<<num_sms, kRsThreads, flop_rs_smem_bytes(k_rows), stream>>>(a.col, a.base, a.nnz,
+                                                                                           deg, k_rows, out);
+    else
+        k_pattern_table<false><<<num_sms, kRsThreads, 0, stream>>>(a.col, a.base, a.nnz, deg, k_rows, out);
     return cudaGetLastError();
 }
 

@@ -120,6 +120,11 @@ constexpr int kLocalitySamples = 4096;
 // gathers) without the row logic; out needs nnz / 16 entries.
 cudaError_t launch_pattern(const DevCsr& a, const uint16_t* deg, bool gather, bool nol1, long long* out,
                            cudaStream_t stream);
+// The same for the row-stream pass (degree table in shared memory): the
+// shape of k_flop_rs (one 1024-thread block per SM); out needs num_sms * 1024.
+bool pattern_table_applies(const DevCsr& a, int32_t k_rows, bool rows_mode);
+cudaError_t launch_pattern_table(const DevCsr& a, const uint16_t* deg, int32_t k_rows, int num_sms, bool gather,
+                                 long long* out, cudaStream_t stream);
 // rows_mode when most sampled consecutive rows advance like a stencil's
 inline bool banded_rows(int pairs, int advancing, int short_rows) {
     return pairs >= 64 && advancing * 4 >= pairs * 3 && short_rows * 20 >= pairs * 19;
