@@ -315,6 +315,11 @@ __global__ void __launch_bounds__(BLOCK) k_sym_small_block(SymArgs g, uint64_t s
 }
 
 // ------------------------------ bins 3-5: block + shared-memory hash
+#ifndef SPNNZ_TIER_TICKETS
+#define SPNNZ_TIER_TICKETS 1
+#endif
+constexpr int kTicketBase = 8;  // counts[kTicketBase + bin]: the bin's row tickets (bins 3-5)
+static_assert(kTicketBase + 5 < 16 && kTicketBase > kNoBin - 1, "ticket counters live in the spare bin counters");
 template <int BLOCK, int SLOTS, int BIN, int UNROLL>
 __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch sc) {
     extern __shared__ int4 s_dyn[];
@@ -327,7 +332,24 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
     const int32_t* list = sc.lists + int64_t(BIN) * sc.capacity;
     const int n = sc.counts[BIN];
     long long acc = 0;
+#if SPNNZ_TIER_TICKETS
+    // rows by ticket (counts[kTicketBase + BIN], zeroed with the bin counts):
+    // a bin's rows differ 3x in FLOP and a block sees only ~9-15 of them, so
+    // static striding left the slowest block ~20-40 % over the mean.  Thread
+    // 0 takes the next ticket while the current row runs (the L2 round trip
+    // stays off the row's critical path).
+    __shared__ int s_ticket;
+    int next = 0;
+    if (threadIdx.x == 0) next = atomicAdd(&sc.counts[kTicketBase + BIN], 1);
+    for (;;) {
+        if (threadIdx.x == 0) s_ticket = next;
+        __syncthreads();
+        const int i = s_ticket;
+        if (i >= n) break;
+        if (threadIdx.x == 0) next = atomicAdd(&sc.counts[kTicketBase + BIN], 1);
+#else
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
+#endif
         const ItemRow it = item_row(g, list[i]);
         hash_clear(table, SLOTS, threadIdx.x, BLOCK);
         int cnt = 0;

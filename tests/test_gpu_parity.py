@@ -1099,3 +1099,24 @@ def test_detached_shards_more_ranks_than_heavy_samples(oracle):
         zs += rep.stats.sampled_nnz
         q.close()
     assert (fs, zs) == (ref.stats.sampled_flop, ref.stats.sampled_nnz)
+
+
+def test_pattern_floor_probe_both_shapes(P):
+    # instrumentation (bench.py's roofline.pattern_*): the L2-gather probe for
+    # the tile kernels and the shared-table probe for the row streams; neither
+    # may disturb the FLOP pass that follows
+    a = gen.uniform_len(1 << 14, 1 << 12, 4, 32, 11)   # K = 4096: row streams
+    b = gen.geometric(1 << 12, 1 << 14, 12.0, 12)
+    P.load(a, b)
+    before = P.compute_flop().flop_per_row.copy()
+    assert "row streams" in P.last_flop_kernel()
+    s_ms, g_ms = P.probe_flop_floor(3)
+    assert s_ms > 0 and g_ms > 0
+    assert np.array_equal(P.compute_flop().flop_per_row, before)
+    r = gen.rmat(17, 1 << 21, 0.57, 0.19, 0.19, 3)     # K = 131072: tiles, L2 gathers
+    P.load(r, r)
+    before = P.compute_flop().flop_per_row.copy()
+    assert "row streams" not in P.last_flop_kernel()
+    s_ms, g_ms = P.probe_flop_floor(3)
+    assert s_ms > 0 and g_ms > 0
+    assert np.array_equal(P.compute_flop().flop_per_row, before)
