@@ -223,6 +223,8 @@ struct spnnz_gpu_ctx {
     bool b_intervals = false;  // interval heavy path requested (SPNNZ_HEAVY_INTERVALS=1)
     bool b_sorted = false;     // ... and B's rows checked non-decreasing at load
     bool rows_mode = false;    // banded A: the FLOP pass's row-per-thread tiles (checked at load)
+    int64_t mp_part = kMpPart;       // its products per pass (test knob SPNNZ_MP_PART, read at load)
+    int64_t mp_max = kMpMaxDefault;  // multipass tier limit (knob SPNNZ_MP_MAX read at load; 0 = heavy path instead)
     int tiers_beside = -1;     // the symbolic tiers run beside the FLOP pass (A/B knob SPNNZ_TIERS_BESIDE; -1: policy)
     int32_t a_rows = 0, a_cols = 0, b_rows = 0, b_cols = 0;
     int32_t row_lo = 0, row_hi = 0;
@@ -529,6 +531,8 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     g.window = window;
     g.tsize = tsize;
     g.tsize_cap = tsize_cap;
+    g.mp_max = c->mp_max;
+    g.mp_part = c->mp_part;
     CU(cudaMemsetAsync(c->counts.p, 0, sizeof(int32_t) * 16, bs));
     CU(cudaMemsetAsync(c->heavy_meta.p, 0, sizeof(long long) * kHeavyMeta, bs));
     if (n_items == 0) return SPNNZ_OK;
@@ -559,7 +563,7 @@ int run_symbolic(spnnz_gpu_ctx* c, const int32_t* d_rows, int64_t n_items, int64
     CU(launch_sym_tiers(g, s, c->num_sms, c->side));
     for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaEventRecord(c->join[i], c->side[i]));
     if (c->dbg_t) for (int i = 0; i < spnnz_gpu_ctx::kSide; ++i) CU(cudaEventRecord(c->dbg_ev[2 + i], c->side[i]));
-    *launches += 6;
+    *launches += g.mp_max > kBin5Max ? 7 : 6;
     c->observed_set = true;  // the counts land in h_counts / h_meta by the call's end
     if (known && !tsize) {
         // sizes known in advance: no wait for the binning
@@ -1413,6 +1417,10 @@ int spnnz_gpu_load(spnnz_gpu_ctx* c, const spnnz_csr_view* a, const spnnz_csr_vi
         c->rows_mode = banded_rows(st[0], st[1], st[2]);
         c->tiers_beside = -1;
         if (const char* e = getenv("SPNNZ_TIERS_BESIDE")) c->tiers_beside = atoi(e) > 0;  // A/B knob
+        c->mp_max = kMpMaxDefault;
+        if (const char* e = getenv("SPNNZ_MP_MAX")) c->mp_max = atoll(e);  // A/B knob
+        c->mp_part = kMpPart;
+        if (const char* e = getenv("SPNNZ_MP_PART")) c->mp_part = std::max<long long>(1, atoll(e));  // test knob
         c->heavy_beside = -1;
         if (const char* e = getenv("SPNNZ_HEAVY_BESIDE")) c->heavy_beside = atoi(e);  // A/B knob (2: sort beside, runs after the pass)
         if (const char* e = getenv("SPNNZ_FLOP_ROWS")) c->rows_mode = atoi(e) > 0;  // A/B knob

@@ -152,7 +152,7 @@ cudaError_t launch_sample(uint64_t seed, int32_t num_rows, int64_t n, int32_t* r
 // Items are either an explicit list of GLOBAL row ids (sampled mode) or all
 // local rows (exact mode, rows == nullptr).  Items whose row is outside the
 // shard [row_lo, row_lo + a.rows) get 0.  Rows are binned by FLOP:
-constexpr int kNumBins = 7;
+constexpr int kNumBins = 8;
 constexpr int64_t kBin1Max = 32;     // warp, __match_any_sync dedup
 constexpr int64_t kBin2Max = 512;    // warp, 1024-slot smem hash per warp
 #ifndef SPNNZ_BIN3_MAX
@@ -168,8 +168,27 @@ constexpr int64_t kBin3Max = SPNNZ_BIN3_MAX;  // 256-thread block, 4096-slot sme
 constexpr int64_t kBin4Max = SPNNZ_BIN4_MAX;  // 512-thread block, 16384-slot smem hash
 constexpr int64_t kBin5Max = SPNNZ_BIN5_MAX;  // 1024-thread block, 49152-slot smem hash
 constexpr int kHeavyBin = 6;         // heavier: units of kHeavyUnitProducts
-constexpr int kForeignBin = 7;       // row owned by another rank
-constexpr int kNoBin = 8;            // padding lane
+// kBin5Max < FLOP <= SymArgs::mp_max: bin 5's block and table, the row's
+// products walked in P = ceil(FLOP / kMpPart) passes, pass k inserting the
+// keys whose mixed hash falls in part k (k_sym_multipass, symbolic.cu)
+constexpr int kMpBin = 7;
+constexpr int kForeignBin = 8;       // row owned by another rank
+constexpr int kNoBin = 9;            // padding lane
+#ifndef SPNNZ_MP_PART
+#define SPNNZ_MP_PART 20000
+#endif
+constexpr int64_t kMpPart = SPNNZ_MP_PART;  // products per pass (mean): table load ~0.4
+// Off by default (0: those rows take the heavy path): measured 3x slower at
+// config 5 (SPNNZ_MP_MAX=98304: k_sym_multipass 922 us for 45 M products) --
+// a filtered-out product saves no warp instructions while any lane of its
+// warp matches, so a pass costs as much as bin 5's single pass.  Opt-in
+// through the runtime knob SPNNZ_MP_MAX (read at load), kept under test.
+#ifndef SPNNZ_MP_MAX
+#define SPNNZ_MP_MAX 0
+#endif
+constexpr int64_t kMpMaxDefault = SPNNZ_MP_MAX;
+// row tickets of the block tiers live in the spare bin counters (16 in all)
+SPNNZ_HD constexpr int ticket_slot(int bin) { return bin == kMpBin ? 13 : 7 + bin; }
 //        products, many blocks per row over a global bitmap of B.cols bits.
 constexpr int64_t kHeavyUnitProducts = 4096;
 // Sorted B (the interval path, heavy.cu): B's columns are cut into
@@ -262,6 +281,8 @@ struct SymArgs {
     // overrun a tier's table.  nullptr: the profile is this context's own.
     const int64_t* tsize = nullptr;
     long long tsize_cap = 0;
+    int64_t mp_max = 0;  // rows of kBin5Max < FLOP <= mp_max take the multipass tier (0: none)
+    int64_t mp_part = kMpPart;  // its products per pass (test knob SPNNZ_MP_PART: a large value forces redos)
 };
 constexpr int kMetaCapacity = 9;  // heavy_meta slot: largest tsize above the profile's capacity
 

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_bin(SymArgs g, SymScratch sc) {
                     atomicMax(reinterpret_cast<unsigned long long*>(&sc.heavy_meta[kMetaCapacity]),
                               static_cast<unsigned long long>(ts));
                 bin = (f == 0 || ts == 0) ? 0 : f <= kBin1Max ? 1 : f <= kBin2Max ? 2 : f <= kBin3Max ? 3
-                                 : f <= kBin4Max ? 4 : f <= kBin5Max ? 5 : kHeavyBin;
+                                 : f <= kBin4Max ? 4 : f <= kBin5Max ? 5 : f <= g.mp_max ? kMpBin : kHeavyBin;
                 if (bin == kHeavyBin) {
                     hl = g.a.rpt[r + 1] - g.a.rpt[r] + 1;
                     hf = f;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_bin(SymArgs g, SymScratch sc) {
         }
         // warp-aggregated append to the bin lists
         const unsigned peers = __match_any_sync(kFull, bin);
-        if (bin >= 1 && bin <= kHeavyBin) {
+        if ((bin >= 1 && bin <= kHeavyBin) || bin == kMpBin) {
             const int leader = __ffs(peers) - 1;
             int pos = 0;
             if (lane == leader) pos = atomicAdd(&sc.counts[bin], __popc(peers));
@@ -318,8 +318,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_small_block(SymArgs g, uint64_t s
 #ifndef SPNNZ_TIER_TICKETS
 #define SPNNZ_TIER_TICKETS 1
 #endif
-constexpr int kTicketBase = 8;  // counts[kTicketBase + bin]: the bin's row tickets (bins 3-5)
-static_assert(kTicketBase + 5 < 16 && kTicketBase > kNoBin - 1, "ticket counters live in the spare bin counters");
+static_assert(ticket_slot(3) > kNoBin && ticket_slot(kMpBin) < 16, "ticket counters live in the spare bin counters");
 template <int BLOCK, int SLOTS, int BIN, int UNROLL>
 __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch sc) {
     extern __shared__ int4 s_dyn[];
@@ -333,20 +332,20 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
     const int n = sc.counts[BIN];
     long long acc = 0;
 #if SPNNZ_TIER_TICKETS
-    // rows by ticket (counts[kTicketBase + BIN], zeroed with the bin counts):
+    // rows by ticket (counts[ticket_slot(BIN)], zeroed with the bin counts):
     // a bin's rows differ 3x in FLOP and a block sees only ~9-15 of them, so
     // static striding left the slowest block ~20-40 % over the mean.  Thread
     // 0 takes the next ticket while the current row runs (the L2 round trip
     // stays off the row's critical path).
     __shared__ int s_ticket;
     int next = 0;
-    if (threadIdx.x == 0) next = atomicAdd(&sc.counts[kTicketBase + BIN], 1);
+    if (threadIdx.x == 0) next = atomicAdd(&sc.counts[ticket_slot(BIN)], 1);
     for (;;) {
         if (threadIdx.x == 0) s_ticket = next;
         __syncthreads();
         const int i = s_ticket;
         if (i >= n) break;
-        if (threadIdx.x == 0) next = atomicAdd(&sc.counts[kTicketBase + BIN], 1);
+        if (threadIdx.x == 0) next = atomicAdd(&sc.counts[ticket_slot(BIN)], 1);
 #else
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
 #endif
@@ -385,6 +384,149 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
                   static_cast<unsigned long long>(acc));
 }
 
+// ------------------------- multipass tier: kBin5Max < FLOP <= mp_max
+// Bin 5's shape (one 1024-thread block per SM, a 49152-slot shared hash) for
+// rows too big for one table: the row's products are walked P = ceil(FLOP /
+// kMpPart) times and pass k inserts only the keys whose mixed hash lands in
+// part k (mix32 is a bijection of the key, independent of the slot hash), so
+// each pass sees ~FLOP / P products and the passes' distinct counts add up to
+// the row's.  OPT-IN (SPNNZ_MP_MAX, default 0): the idea was that a filtered-
+// out product costs only its coalesced load and one multiply, against the
+// heavy path's counting sort + bitmap task (~190 thread instructions per
+// product) -- but in SIMT a skipped key saves nothing while any lane of its
+// warp inserts, so every pass costs bin 5's full ~3 warp instructions per
+// product: measured 922 us for config 5's 45 M products of 24576 < FLOP <=
+// 98304 (the heavy path: ~380 us for the same rows).  Kept under test as a
+// recorded experiment.  Exactness does not depend on the hash: a pass whose table fills
+// (probe sequence above kMpProbeCap -- keys crafted against mix32, or far
+// more products in one part than the mean) raises a flag, and the row is
+// redone with twice the passes; parts are hash ranges of a bijection, so
+// that ends.  Rows of at most BLOCK entries (nearly all: FLOP <= 98304 at
+// ~340 products per entry) stage their entry offsets once for all passes.
+constexpr int kMpProbeCap = 2048;
+__device__ __forceinline__ int hash_insert_shared_capped(uint32_t table_s, uint32_t size, int key) {
+    uint32_t h = __umulhi(slot_hash(key), size);
+    for (int probes = 0; probes < kMpProbeCap; ++probes) {
+        const uint32_t addr = table_s + 4u * h;
+        int cur;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(cur) : "r"(addr) : "memory");
+        if (cur == key) return 0;
+        if (cur == kEmpty) {
+            int prev;
+            asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;"
+                         : "=r"(prev) : "r"(addr), "r"(kEmpty), "r"(key) : "memory");
+            if (prev == kEmpty) return 1;
+            if (prev == key) return 0;
+        }
+        h = (h + 1 == size) ? 0 : h + 1;
+    }
+    return -1;
+}
+
+template <int U>
+struct PartSinkU {
+    uint32_t table_s, size, part, parts;
+    int* cnt;
+    volatile int* ovf;
+    __device__ __forceinline__ void operator()(const int (&keys)[U], const bool (&valid)[U], long long) const {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!valid[u] || __umulhi(mix32(static_cast<uint32_t>(keys[u])), parts) != part) continue;
+            if (*ovf) continue;  // the pass is lost already: the row is redone
+            const int r = hash_insert_shared_capped(table_s, size, keys[u]);
+            if (r < 0) *ovf = 1; else *cnt += r;
+        }
+    }
+};
+
+template <int BLOCK, int SLOTS, int UNROLL>
+__global__ void __launch_bounds__(BLOCK, 1) k_sym_multipass(SymArgs g, SymScratch sc) {
+    extern __shared__ int4 s_dyn[];
+    int* table = reinterpret_cast<int*>(s_dyn);
+    using Scan = cub::BlockScan<int, BLOCK>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int s_off[BLOCK + 1];
+    __shared__ int64_t s_b0[BLOCK];
+    __shared__ long long s_red[BLOCK / 32];
+    __shared__ int s_ticket, s_ovf;
+    const int32_t* list = sc.lists + int64_t(kMpBin) * sc.capacity;
+    const int n = sc.counts[kMpBin];
+    const uint32_t table_s = static_cast<uint32_t>(__cvta_generic_to_shared(table));
+    long long acc = 0;
+    int next = 0;
+    if (threadIdx.x == 0) next = atomicAdd(&sc.counts[ticket_slot(kMpBin)], 1);
+    for (;;) {
+        if (threadIdx.x == 0) s_ticket = next;
+        __syncthreads();
+        const int i = s_ticket;
+        if (i >= n) break;
+        if (threadIdx.x == 0) next = atomicAdd(&sc.counts[ticket_slot(kMpBin)], 1);
+        const int32_t s = list[i];
+        const ItemRow it = item_row(g, s);
+        const int32_t rid = g.rows ? g.rows[s] : g.row_lo + s;
+        const int64_t f = g.item_flop ? g.item_flop[s] : g.flop[rid - g.row_lo];
+        uint32_t parts = static_cast<uint32_t>((f + g.mp_part - 1) / g.mp_part);
+        if (parts < 1) parts = 1;
+        const bool single = it.a1 - it.a0 <= BLOCK;  // one chunk of entries: staged once
+        long long tot = 0;
+        for (;;) {
+            int cnt = 0;
+            if (threadIdx.x == 0) s_ovf = 0;
+            int nent = 0, total = 0;
+            // entries [c0, c0 + BLOCK) -> s_off / s_b0 (every thread calls it)
+#define SPNNZ_MP_STAGE(c0)                                                          \
+    do {                                                                            \
+        const int64_t e_ = (c0) + threadIdx.x;                                      \
+        int d_ = 0;                                                                 \
+        int64_t b0_ = 0;                                                            \
+        if (e_ < it.a1) {                                                           \
+            const int c_ = __ldg(&g.a.col[e_]);                                     \
+            b0_ = __ldg(&g.brpt[c_]);                                               \
+            d_ = static_cast<int>(__ldg(&g.brpt[c_ + 1]) - b0_);                    \
+        }                                                                           \
+        int excl_;                                                                  \
+        Scan(scan_tmp).ExclusiveSum(d_, excl_, total);                              \
+        nent = static_cast<int>(it.a1 - (c0) < BLOCK ? it.a1 - (c0) : BLOCK);       \
+        s_off[threadIdx.x] = excl_;                                                 \
+        s_b0[threadIdx.x] = b0_;                                                    \
+        if (threadIdx.x == 0) s_off[nent] = total;                                  \
+    } while (0)
+            if (single) SPNNZ_MP_STAGE(it.a0);
+            for (uint32_t part = 0; part < parts; ++part) {
+                hash_clear(table, SLOTS, threadIdx.x, BLOCK);
+                const PartSinkU<UNROLL> sink{table_s, static_cast<uint32_t>(SLOTS), part, parts, &cnt, &s_ovf};
+                if (single) {
+                    __syncthreads();  // the staged entries and the cleared table (and s_ovf = 0)
+                    chunk_products<BLOCK / 32, UNROLL>(s_off, s_b0, nent, 0, total, g.bcol, sink);
+                    __syncthreads();  // inserts done before the next pass clears
+                } else {
+                    for (int64_t c0 = it.a0; c0 < it.a1; c0 += BLOCK) {
+                        SPNNZ_MP_STAGE(c0);
+                        __syncthreads();
+                        chunk_products<BLOCK / 32, UNROLL>(s_off, s_b0, nent, 0, total, g.bcol, sink);
+                        __syncthreads();
+                    }
+                }
+#undef SPNNZ_MP_STAGE
+                if (s_ovf) break;  // uniform: read after the barrier that ends the pass
+            }
+            __syncthreads();
+            const bool ovf = s_ovf != 0;
+            tot = block_sum_ll<BLOCK>(cnt, s_red);
+            __syncthreads();  // s_ovf and s_red are reused by a redo / the next row
+            if (!ovf) break;
+            parts *= 2;
+        }
+        if (threadIdx.x == 0) {
+            if (g.out) g.out[it.s] = tot;
+            acc += tot;
+        }
+    }
+    if (threadIdx.x == 0 && acc)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&g.totals[g.total_slot]),
+                  static_cast<unsigned long long>(acc));
+}
+
 #ifndef SPNNZ_T4_SLOTS
 #define SPNNZ_T4_SLOTS 16384
 #endif
@@ -411,6 +553,9 @@ static_assert(kBin1Max <= 32, "bin 1 stages a row's products in one warp's 32 sl
 #endif
 #ifndef SPNNZ_T5_UNROLL
 #define SPNNZ_T5_UNROLL 4
+#endif
+#ifndef SPNNZ_MP_UNROLL
+#define SPNNZ_MP_UNROLL 8
 #endif
 
 template <int BLOCK, int SLOTS, int BIN, int UNROLL>
@@ -456,6 +601,8 @@ cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_s
         set_smem_attr<kT3Block, kT3Slots, 3, SPNNZ_T3_UNROLL>();
         set_smem_attr<kT4Block, kT4Slots, 4, SPNNZ_T4_UNROLL>();
         set_smem_attr<kT5Block, kT5Slots, 5, SPNNZ_T5_UNROLL>();
+        cudaFuncSetAttribute(k_sym_multipass<kT5Block, kT5Slots, SPNNZ_MP_UNROLL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kT5Slots * 4);
         attr_done.fetch_or(1ull << (dev & 63), std::memory_order_release);
     }
     const unsigned sms = static_cast<unsigned>(num_sms);
@@ -470,6 +617,10 @@ cudaError_t launch_sym_tiers(const SymArgs& args, const SymScratch& s, int num_s
     k_sym_block_hash<kT3Block, kT3Slots, 3, SPNNZ_T3_UNROLL><<<sms * 8 * waves, kT3Block, kT3Slots * 4, streams[1]>>>(args, s);
     k_sym_block_hash<kT4Block, kT4Slots, 4, SPNNZ_T4_UNROLL><<<sms * SPNNZ_T4_BLOCKS_PER_SM * waves, kT4Block, kT4Slots * 4, streams[2]>>>(args, s);
     k_sym_block_hash<kT5Block, kT5Slots, 5, SPNNZ_T5_UNROLL><<<sms * waves, kT5Block, kT5Slots * 4, streams[3]>>>(args, s);
+    // the multipass rows (bin 5's footprint: one block per SM) before bin 5 would
+    // hold the biggest rows back; after it they share its stream
+    if (args.mp_max > kBin5Max)
+        k_sym_multipass<kT5Block, kT5Slots, SPNNZ_MP_UNROLL><<<sms, kT5Block, kT5Slots * 4, streams[3]>>>(args, s);
     return cudaGetLastError();
 }
 

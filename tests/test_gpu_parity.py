@@ -279,12 +279,16 @@ def tier_matrix(n_rows, n_cols, lens, b_lens, seed):
 
 # heavy-row algorithms (heavy.cu): the default sort-agnostic bucket paths and
 # the opt-in sorted-B interval path
-HEAVY_PATHS = ["default", "intervals"]
+# "multipass": the opt-in multipass hash tier (SPNNZ_MP_MAX) takes the rows
+# up to 98304 products, the default heavy path the heavier ones
+HEAVY_PATHS = ["default", "intervals", "multipass"]
 
 
 def heavy_path(monkeypatch, path):
     if path == "intervals":
         monkeypatch.setenv("SPNNZ_HEAVY_INTERVALS", "1")
+    if path == "multipass":
+        monkeypatch.setenv("SPNNZ_MP_MAX", "98304")
 
 
 @pytest.mark.parametrize("path", HEAVY_PATHS)
@@ -1062,6 +1066,11 @@ def test_fuzz_pipeline_vs_oracle(oracle, case, monkeypatch):
         monkeypatch.setenv("SPNNZ_FUSED_PREDICT", "1")
     if case % 4 == 3:
         monkeypatch.setenv("SPNNZ_HEAVY_BATCH_PRODUCTS", "50000")
+    if case % 3 == 0:
+        monkeypatch.setenv("SPNNZ_MP_MAX", "98304")    # the opt-in multipass tier below the heavy path
+    elif case % 3 == 1:
+        monkeypatch.setenv("SPNNZ_MP_MAX", "98304")
+        monkeypatch.setenv("SPNNZ_MP_PART", "150000")  # ... with too few passes: redos
     q = Predictor(0)
     q.load(a, b)
     prof = q.compute_flop()
@@ -1120,3 +1129,44 @@ def test_pattern_floor_probe_both_shapes(P):
     s_ms, g_ms = P.probe_flop_floor(3)
     assert s_ms > 0 and g_ms > 0
     assert np.array_equal(P.compute_flop().flop_per_row, before)
+
+
+@pytest.mark.parametrize("part", [None, 7000, 1000000])
+def test_multipass_tier_vs_oracle(oracle, part, monkeypatch):
+    """Rows of 24576 < FLOP <= 98304 on the opt-in multipass hash tier: nearly all
+    distinct, duplicate-heavy, one with more entries than the block (staged
+    per pass), and rows just inside / outside the tier's limits; with the
+    default part size, many small passes, and a part size that puts the whole
+    row in one pass (the table fills: the row is redone with 2x, 4x passes)."""
+    monkeypatch.setenv("SPNNZ_MP_MAX", "98304")  # the tier is opt-in
+    if part is not None:
+        monkeypatch.setenv("SPNNZ_MP_PART", str(part))
+    rng = np.random.default_rng(23)
+    nb, ncols = 6000, 1 << 22
+    b_lens = list(rng.integers(20, 60, nb - 1200)) + [1] * 1200
+    b_rows = [np.sort(rng.choice(ncols, size=int(L), replace=False)).tolist() for L in b_lens[:nb - 1200]]
+    b_rows += [[int(rng.integers(0, 50))] for _ in range(1200)]  # one-entry rows over 50 columns: duplicates
+    b = csr(nb, ncols, b_rows)
+    long_ids = np.arange(nb - 1200)
+    a_rows = [np.sort(rng.choice(long_ids, size=L, replace=False)).tolist() for L in (700, 1000, 1500, 2300, 620, 2700)]
+    # duplicate-heavy: 1100 long rows' products + 1200 products over 50 columns
+    a_rows.append(np.sort(np.concatenate([rng.choice(long_ids, size=700, replace=False),
+                                          np.arange(nb - 1200, nb)])).tolist())
+    a_rows.append([3, 4])
+    a = csr(len(a_rows), nb, a_rows)
+    q = Predictor(0)
+    q.load(a, b)
+    prof = q.compute_flop()
+    f, F, mx = oracle.compute_flop(a, b)
+    assert (prof.flop_per_row == f).all()
+    assert ((f > 24576) & (f <= 98304)).sum() >= 5 and (f > 98304).any()
+    assert max(len(r) for r in a_rows) > 1024  # an entry list longer than the block
+    ex = q.exact_symbolic()
+    nnz, Z = oracle.exact_symbolic(a, b, f, mx)
+    assert (ex.nnz_per_row == nnz).all() and ex.total_nnz == Z
+    rows = np.arange(a.rows, dtype=np.int32)[::-1].copy()
+    s2 = q.sampled_symbolic(rows)
+    assert (s2.nnz_per_row == nnz[rows]).all() and s2.total_nnz == Z
+    ex2 = q.exact_symbolic()  # tickets and bin counters reset per call
+    assert (ex2.nnz_per_row == nnz).all()
+    q.close()
