@@ -457,14 +457,21 @@ __global__ void __launch_bounds__(kHB) k_heavy_place(SymArgs g, SymScratch sc, i
 // (63 M of the kernel's 88 M shared wavefronts were bank conflicts at config
 // 5).  The rank within the range is kept beside the key; after the scan of
 // the range totals each key is written straight to its final position.
-__device__ __forceinline__ int warp_range_rank(int* counters, int bucket, bool valid, int nbits) {
+// counters_s: the 32-bit shared-window address of the range counters (the
+// generic-pointer atomicAdd re-derived the window for every key)
+__device__ __forceinline__ int shared_add(uint32_t addr, int v) {
+    int old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ int warp_range_rank(uint32_t counters_s, int bucket, bool valid, int nbits) {
     const int lane = threadIdx.x & 31;
 #if SPNNZ_SORT_MATCH == 1
     unsigned peers = __match_any_sync(kFull, valid ? bucket : -1);
     if (!valid) peers = 0u;
     const int leader = peers ? __ffs(peers) - 1 : lane;
     int base = 0;
-    if (valid && lane == leader) base = atomicAdd(&counters[bucket], __popc(peers));
+    if (valid && lane == leader) base = shared_add(counters_s + 4u * bucket, __popc(peers));
     base = __shfl_sync(kFull, base, leader);
     return base + __popc(peers & ((1u << lane) - 1));
 #elif SPNNZ_SORT_MATCH == 2
@@ -476,7 +483,7 @@ __device__ __forceinline__ int warp_range_rank(int* counters, int bucket, bool v
     }
     const int leader = peers ? __ffs(peers) - 1 : lane;
     int base = 0;
-    if (valid && lane == leader) base = atomicAdd(&counters[bucket], __popc(peers));
+    if (valid && lane == leader) base = shared_add(counters_s + 4u * bucket, __popc(peers));
     base = __shfl_sync(kFull, base, leader);
     return base + __popc(peers & ((1u << lane) - 1));
 #else
@@ -491,7 +498,7 @@ __device__ __forceinline__ int warp_range_rank(int* counters, int bucket, bool v
     const unsigned after = heads & ~le;                    // heads (or invalid lanes) above the lane
     const int next = after ? __ffs(after) - 1 : 32;
     int base = 0;
-    if (valid && head == lane) base = atomicAdd(&counters[bucket], next - lane);
+    if (valid && head == lane) base = shared_add(counters_s + 4u * bucket, next - lane);
     base = __shfl_sync(kFull, base, head);
     return base + lane - head;
 #endif
@@ -509,6 +516,12 @@ __global__ void __launch_bounds__(kHB, 1536 / kHB) k_heavy_sort_units(SymArgs g,
     int* s_offs = s_hist + kHW * R;
     const int lane = threadIdx.x & 31;
     const int nbits = 32 - __clz(R - 1);
+    // shared-window addresses held in registers (opaque to the compiler, which
+    // otherwise re-derives the window -- S2UR SR_CgaCtaId + three uniform
+    // instructions -- at every store and atomic of the rank loop)
+    uint32_t in_s = static_cast<uint32_t>(__cvta_generic_to_shared(s_in));
+    uint32_t hist_s = static_cast<uint32_t>(__cvta_generic_to_shared(s_hist));
+    asm volatile("" : "+r"(in_s), "+r"(hist_s));
     const long long units = sc.heavy_meta[0];
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit un = find_unit_block(sc, count, u);
@@ -519,11 +532,12 @@ __global__ void __launch_bounds__(kHB, 1536 / kHB) k_heavy_sort_units(SymArgs g,
                            [&](const int (&keys)[kSortU], const bool (&valid)[kSortU],
                                long long q) {
 #pragma unroll
+                               const uint32_t at = in_s + 4u * static_cast<uint32_t>(q);
                                for (int k = 0; k < kSortU; ++k) {
-                                   const int rk = warp_range_rank(s_hist, keys[k] >> wshift, valid[k], nbits);
-                                   if (valid[k]) {
-                                       s_in[q + 32 * k] = keys[k];
-                                       s_rank[q + 32 * k] = rk;
+                                   const int rk = warp_range_rank(hist_s, keys[k] >> wshift, valid[k], nbits);
+                                   if (valid[k]) {  // s_in[q + 32 k] = key, s_rank[q + 32 k] = rank
+                                       asm volatile("st.shared.b32 [%0], %1;" ::"r"(at + 128u * k), "r"(keys[k]) : "memory");
+                                       asm volatile("st.shared.b32 [%0], %1;" ::"r"(at + 128u * k + static_cast<uint32_t>(4 * kHeavyUnitProducts)), "r"(rk) : "memory");
                                    }
                                }
                            }, un.e0);

@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
     __shared__ long long s_red[BLOCK / 32];
     const int32_t* list = sc.lists + int64_t(BIN) * sc.capacity;
     const int n = sc.counts[BIN];
+    const uint32_t table_s = shared_window_reg(table);
     long long acc = 0;
 #if SPNNZ_TIER_TICKETS
     // rows by ticket (counts[ticket_slot(BIN)], zeroed with the bin counts):
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(BLOCK) k_sym_block_hash(SymArgs g, SymScratch 
             if (threadIdx.x == 0) s_off[nent] = total;
             __syncthreads();  // also orders the table fill before the inserts
             chunk_products<BLOCK / 32, UNROLL>(s_off, s_b0, nent, 0, total, g.bcol,
-                                               HashSinkU<UNROLL>{table, SLOTS, &cnt});
+                                               HashSinkU<UNROLL>{table, SLOTS, &cnt, table_s});
             __syncthreads();
         }
         const long long tot = block_sum_ll<BLOCK>(cnt, s_red);

@@ -182,15 +182,27 @@ __device__ __forceinline__ int hash_insert_shared(uint32_t table_s, uint32_t siz
     }
 }
 
+// A shared-memory pointer's 32-bit window address, opaque to the compiler so
+// it stays in a register: left to itself the compiler re-derives the window
+// (S2R SR_CgaCtaId + three more instructions) at every access in a loop.
+__device__ __forceinline__ uint32_t shared_window_reg(const void* p) {
+    uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    asm volatile("" : "+r"(a));
+    return a;
+}
+
 // fn adaptor: insert each valid key into a shared-memory hash table.
 template <int U = kUnroll>
 struct HashSinkU {
     int* table;
     uint32_t size;
     int* cnt;
+    // the table's shared-window address when the kernel holds it in a register
+    // (shared_window_reg): derived from `table` per key otherwise
+    uint32_t table_s = 0;
     __device__ __forceinline__ void operator()(const int (&keys)[U], const bool (&valid)[U], long long) const {
 #if SPNNZ_HASH_PTX
-        const uint32_t ts = static_cast<uint32_t>(__cvta_generic_to_shared(table));
+        const uint32_t ts = table_s ? table_s : static_cast<uint32_t>(__cvta_generic_to_shared(table));
 #endif
 #pragma unroll
         for (int u = 0; u < U; ++u)
