@@ -69,39 +69,64 @@ __device__ __forceinline__ ItemRow item_row(const SymArgs& g, int32_t s) {
 // dependent chain per product.
 constexpr int kUnroll = 4;
 
-template <int WARPS, int U = kUnroll, typename OffT, typename Fn>
-__device__ __forceinline__ void chunk_products(const OffT* off, const int64_t* b0, int n, OffT q0,
-                                               OffT q1, const int32_t* __restrict__ bcol, Fn&& fn) {
+// A shared-memory pointer's 32-bit window address, opaque to the compiler so
+// it stays in a register: left to itself the compiler re-derives the window
+// (S2R SR_CgaCtaId + three more instructions) at every access in a loop.
+__device__ __forceinline__ uint32_t shared_window_reg(const void* p) {
+    uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    asm volatile("" : "+r"(a));
+    return a;
+}
+__device__ __forceinline__ int lds_i32(uint32_t addr) {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ long long lds_i64(uint32_t addr) {
+    long long v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
+}
+
+// off / b0 are SHARED-memory arrays (every caller stages them there): they are
+// read through register-held window addresses, and the lane's current entry
+// is kept as a pointer to its product 0 in bcol, so a key costs one 32 x 32 +
+// 64 multiply-add for its address instead of a 64-bit add, a shift and the
+// window derivation.
+template <int WARPS, int U = kUnroll, typename Fn>
+__device__ __forceinline__ void chunk_products(const int* off, const int64_t* b0, int n, int q0,
+                                               int q1, const int32_t* __restrict__ bcol, Fn&& fn) {
     const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) % WARPS;
-    const OffT span = q1 - q0;
+    const int span = q1 - q0;
     if (span <= 0 || n <= 0) return;
-    OffT per = (span + WARPS - 1) / WARPS;
-    per = (per + 31) & ~OffT(31);
-    const OffT ws = q0 + w * per;
-    const OffT we = ws + per < q1 ? ws + per : q1;
+    const uint32_t off_s = shared_window_reg(off), b0_s = shared_window_reg(b0);
+    int per = (span + WARPS - 1) / WARPS;
+    per = (per + 31) & ~31;
+    const int ws = q0 + w * per;
+    const int we = ws + per < q1 ? ws + per : q1;
     // warp-uniform loop (fn may use warp collectives); lanes past the end of
     // the warp's slice run with valid = false
     int e = 0;
     if (ws + lane < we) {
-        const OffT p = ws + lane;
+        const int p = ws + lane;
         int lo = 0, hi = n - 1;  // largest e with off[e] <= p
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if (off[mid] <= p) lo = mid; else hi = mid - 1;
+            if (lds_i32(off_s + 4u * mid) <= p) lo = mid; else hi = mid - 1;
         }
         e = lo;
     }
     // the lane's current entry lives in registers: its end offset and the
-    // B.col index of product 0 (key of product q = bcol[kb + q])
-    OffT nxt = off[e + 1];
-    long long kb = static_cast<long long>(b0[e]) - static_cast<long long>(off[e]);
-    for (OffT base = ws; base < we; base += 32 * U) {
-        const OffT p = base + lane;
+    // address of its product 0 in bcol (key of product q = bp[q])
+    int nxt = lds_i32(off_s + 4u * (e + 1));
+    const int32_t* bp = bcol + (lds_i64(b0_s + 8u * e) - static_cast<long long>(lds_i32(off_s + 4u * e)));
+    for (int base = ws; base < we; base += 32 * U) {
+        const int p = base + lane;
         int keys[U];
         bool valid[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const OffT q = p + 32 * u;
+            const int q = p + 32 * u;
             valid[u] = q < we;
             keys[u] = 0;
             if (valid[u]) {
@@ -109,11 +134,11 @@ __device__ __forceinline__ void chunk_products(const OffT* off, const int64_t* b
                     do {
                         ++e;
                         SPNNZ_ASSERT(e < n);
-                        nxt = off[e + 1];
+                        nxt = lds_i32(off_s + 4u * (e + 1));
                     } while (nxt <= q);
-                    kb = static_cast<long long>(b0[e]) - static_cast<long long>(off[e]);
+                    bp = bcol + (lds_i64(b0_s + 8u * e) - static_cast<long long>(lds_i32(off_s + 4u * e)));
                 }
-                keys[u] = __ldg(&bcol[kb + q]);
+                keys[u] = __ldg(bp + q);
             }
         }
         fn(keys, valid, static_cast<long long>(p));  // keys[u] is product p + 32 u
@@ -180,15 +205,6 @@ __device__ __forceinline__ int hash_insert_shared(uint32_t table_s, uint32_t siz
         }
         h = (h + 1 == size) ? 0 : h + 1;
     }
-}
-
-// A shared-memory pointer's 32-bit window address, opaque to the compiler so
-// it stays in a register: left to itself the compiler re-derives the window
-// (S2R SR_CgaCtaId + three more instructions) at every access in a loop.
-__device__ __forceinline__ uint32_t shared_window_reg(const void* p) {
-    uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
-    asm volatile("" : "+r"(a));
-    return a;
 }
 
 // fn adaptor: insert each valid key into a shared-memory hash table.
