@@ -92,6 +92,23 @@ struct HeavyTask {
 };
 static_assert(sizeof(HeavyTask) == 32, "task layout");
 
+// Shared bitmap inserts on a register-held window address (shared_window_reg):
+// bit `off` of the bitmap at set_s.  The generic-pointer atomicOr re-derived
+// the shared window -- and the task's column base -- for every key.
+__device__ __forceinline__ void bit_set(uint32_t set_s, uint32_t off) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(set_s + ((off >> 3) & ~3u)), "r"(1u << (off & 31)) : "memory");
+}
+__device__ __forceinline__ int bit_set_new(uint32_t set_s, uint32_t off) {  // 1 if the bit was clear
+    uint32_t old;
+    asm volatile("atom.shared.or.b32 %0, [%1], %2;"
+                 : "=r"(old) : "r"(set_s + ((off >> 3) & ~3u)), "r"(1u << (off & 31)) : "memory");
+    return static_cast<int>(~(old >> (off & 31)) & 1u);
+}
+__device__ __forceinline__ int32_t opaque_reg(int32_t v) {
+    asm volatile("" : "+r"(v));
+    return v;
+}
+
 __device__ __forceinline__ const int32_t* heavy_list(const SymScratch& sc, int64_t first) {
     return sc.lists + int64_t(kHeavyBin) * sc.capacity + first;
 }
@@ -800,6 +817,7 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
     const int32_t max_words = R > 1 ? (1 << (kTaskSpanShift - 5))
                                     : static_cast<int32_t>((int64_t(g.bcols) + 31) / 32);
     for (int k = threadIdx.x; k < max_words; k += kRunBlock) s_set[k] = 0u;
+    const uint32_t set_s = shared_window_reg(s_set);
     long long acc = 0;
     // tasks by ticket (a few hundred atomics): a block that starts late --
     // its SM still busy with a tier kernel -- takes fewer instead of holding
@@ -814,7 +832,7 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
         __syncthreads();
         if (s_ti >= ntask) break;
         const HeavyTask t = s_task;
-        const int32_t col_base = R > 1 ? (t.r0 << wshift) : 0;
+        const int32_t col_base = opaque_reg(R > 1 ? (t.r0 << wshift) : 0);
         const int32_t words = R > 1 ? ((t.r1 - t.r0) << (wshift - 5)) : max_words;
         int cnt = 0;
         // a task that shares its span with others (merge slot) counts at the
@@ -828,8 +846,7 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
                     if (valid[u]) {
                         const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
                     SPNNZ_ASSERT((off >> 5) < static_cast<uint32_t>(words));
-                        const uint32_t bit = 1u << (off & 31);
-                        if (!kTestFirst || !(s_set[off >> 5] & bit)) atomicOr(&s_set[off >> 5], bit);
+                        if (!kTestFirst || !(s_set[off >> 5] & (1u << (off & 31)))) bit_set(set_s, off);
                     }
                 return;
             }
@@ -838,8 +855,7 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
                 if (valid[u]) {
                     const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
                     SPNNZ_ASSERT((off >> 5) < static_cast<uint32_t>(words));
-                    const uint32_t bit = 1u << (off & 31);
-                    if (!kTestFirst || !(s_set[off >> 5] & bit)) cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
+                    if (!kTestFirst || !(s_set[off >> 5] & (1u << (off & 31)))) cnt += bit_set_new(set_s, off);
                 }
         };
         // the span's keys: 16-byte vectors over the aligned body, two vectors
@@ -929,6 +945,7 @@ __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, Sym
     const int lane = threadIdx.x & 31;
     constexpr int32_t kWords = 1 << (kTaskSpanShift - 5);
     for (int k = threadIdx.x; k < kWords; k += kRunBlock) s_set[k] = 0u;
+    const uint32_t set_s = shared_window_reg(s_set);
     // unit-table entries of task t for this thread's unit (first round only)
     auto fetch = [&](const HeavyTask& t, int& lo, int& hi) {
         lo = hi = 0;
@@ -961,7 +978,7 @@ __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, Sym
         int lo = nlo, hi = nhi;
         const long long tj = ticket();
         if (tj < ntask) tn = tasks[tj];  // in flight during this task
-        const int32_t col_base = t.r0 << wshift;
+        const int32_t col_base = opaque_reg(t.r0 << wshift);
         const int32_t words = (t.r1 - t.r0) << (wshift - 5);
         const long long pbase = sc.heavy_foff[t.item];
         int cnt = 0;
@@ -971,8 +988,7 @@ __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, Sym
                 if (valid[u]) {
                     const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
                     SPNNZ_ASSERT((off >> 5) < static_cast<uint32_t>(words));
-                    const uint32_t bit = 1u << (off & 31);
-                    if (!kTestFirst || !(s_set[off >> 5] & bit)) cnt += (atomicOr(&s_set[off >> 5], bit) & bit) ? 0 : 1;
+                    if (!kTestFirst || !(s_set[off >> 5] & (1u << (off & 31)))) cnt += bit_set_new(set_s, off);
                 }
         };
         for (long long u0 = t.a; u0 < t.b; u0 += kRunBlock) {
@@ -1038,6 +1054,7 @@ __global__ void __launch_bounds__(kSG * kSGroups, 3) k_heavy_run_small(SymArgs g
     extern __shared__ int4 s_dyn_rs[];
     const int grp = threadIdx.x / kSG, gt = threadIdx.x % kSG, gw = gt >> 5, lane = threadIdx.x & 31;
     int* table = reinterpret_cast<int*>(s_dyn_rs) + grp * kSSlots;
+    const uint32_t table_s = shared_window_reg(table);
     __shared__ int s_off[kSGroups][kSG + 1];
     __shared__ int64_t s_b0[kSGroups][kSG];
     __shared__ int s_wt[kSGroups][kSG / 32];
@@ -1095,7 +1112,7 @@ __global__ void __launch_bounds__(kSG * kSGroups, 3) k_heavy_run_small(SymArgs g
             if (gt == 0) s_off[grp][n] = tot;
             group_sync(grp);  // also orders the table clear before the inserts
             chunk_products<kSG / 32>(s_off[grp], s_b0[grp], n, 0, tot, sc.heavy_pbuf,
-                                     HashSink{table, kSSlots, &cnt});
+                                     HashSink{table, kSSlots, &cnt, table_s});
         }
         cnt = static_cast<int>(warp_sum_ll(cnt));
         if (lane == 0 && cnt) {
