@@ -68,6 +68,9 @@ __device__ __forceinline__ ItemRow item_row(const SymArgs& g, int32_t s) {
 // memory operations fn issues per key -- overlap instead of forming one
 // dependent chain per product.
 constexpr int kUnroll = 4;
+#ifndef SPNNZ_CHUNK_FAST
+#define SPNNZ_CHUNK_FAST 1
+#endif
 
 // A shared-memory pointer's 32-bit window address, opaque to the compiler so
 // it stays in a register: left to itself the compiler re-derives the window
@@ -120,7 +123,33 @@ __device__ __forceinline__ void chunk_products(const int* off, const int64_t* b0
     // address of its product 0 in bcol (key of product q = bp[q])
     int nxt = lds_i32(off_s + 4u * (e + 1));
     const int32_t* bp = bcol + (lds_i64(b0_s + 8u * e) - static_cast<long long>(lds_i32(off_s + 4u * e)));
-    for (int base = ws; base < we; base += 32 * U) {
+    const auto advance = [&](int q) {  // the lane's entry for product q >= nxt
+        do {
+            ++e;
+            SPNNZ_ASSERT(e < n);
+            nxt = lds_i32(off_s + 4u * (e + 1));
+        } while (nxt <= q);
+        bp = bcol + (lds_i64(b0_s + 8u * e) - static_cast<long long>(lds_i32(off_s + 4u * e)));
+    };
+    int base = ws;
+#if SPNNZ_CHUNK_FAST
+    // whole iterations (every lane's U products inside the slice): no range
+    // checks, and fn sees constant-true valid flags (its per-key tests fold)
+    for (; base + 32 * U <= we; base += 32 * U) {
+        const int p = base + lane;
+        int keys[U];
+        bool valid[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q = p + 32 * u;
+            valid[u] = true;
+            if (nxt <= q) advance(q);
+            keys[u] = __ldg(bp + q);
+        }
+        fn(keys, valid, static_cast<long long>(p));
+    }
+#endif
+    for (; base < we; base += 32 * U) {
         const int p = base + lane;
         int keys[U];
         bool valid[U];
@@ -130,14 +159,7 @@ __device__ __forceinline__ void chunk_products(const int* off, const int64_t* b0
             valid[u] = q < we;
             keys[u] = 0;
             if (valid[u]) {
-                if (nxt <= q) {
-                    do {
-                        ++e;
-                        SPNNZ_ASSERT(e < n);
-                        nxt = lds_i32(off_s + 4u * (e + 1));
-                    } while (nxt <= q);
-                    bp = bcol + (lds_i64(b0_s + 8u * e) - static_cast<long long>(lds_i32(off_s + 4u * e)));
-                }
+                if (nxt <= q) advance(q);
                 keys[u] = __ldg(bp + q);
             }
         }
