@@ -553,7 +553,7 @@ static_assert(kBin1Max <= 32, "bin 1 stages a row's products in one warp's 32 sl
 #define SPNNZ_T4_UNROLL 8
 #endif
 #ifndef SPNNZ_T5_UNROLL
-#define SPNNZ_T5_UNROLL 4
+#define SPNNZ_T5_UNROLL 8
 #endif
 #ifndef SPNNZ_MP_UNROLL
 #define SPNNZ_MP_UNROLL 8
