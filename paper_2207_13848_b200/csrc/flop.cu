@@ -1768,6 +1768,23 @@ static cudaError_t launch_tiles(const TileArgs& g, const uint16_t* bdeg, int64_t
             g, bdeg, mode.b_rows, pred, t_begin, t_end, mode.sched);
     } else {
         g_last_kernel = ROWS ? "k_flop (row-mode tiles, degree gathers from L2)" : "k_flop (tiles, degree gathers from L2)";
+        // A/B knob: the shared-memory carve-out (percent of the SM's 228 KB;
+        // the rest is L1 for the degree gathers): fewer resident tile blocks,
+        // more L1.  Unset: the driver sizes it for the most resident blocks.
+        static const int carve = [] {
+            const char* e = getenv("SPNNZ_FLOP_CARVEOUT");
+            return e ? atoi(e) : -1;
+        }();
+        if (carve >= 0) {
+            static std::atomic<unsigned long long> carve_done{0};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (!(carve_done.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
+                cudaFuncSetAttribute(k_flop<kFlopBlock, kFlopIpt, PRED, ROWS, NOL1>,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+                carve_done.fetch_or(1ull << (dev & 63), std::memory_order_release);
+            }
+        }
         k_flop<kFlopBlock, kFlopIpt, PRED, ROWS, NOL1><<<static_cast<unsigned>(t_end - t_begin), kFlopBlock, 0, stream>>>(
             g, bdeg, pred, t_begin);
     }
