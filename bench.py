@@ -377,6 +377,8 @@ def run_ours(args, rank, world, local):
     # per-phase device times: CUDA events recorded inside the call (also inside
     # its replayed CUDA graph), the same number of steps after the timed ones
     P.set_profiling(True)
+    for _ in range(2):  # untimed: the profiled call is captured into its own graph on first use
+        step()
     for i in range(args.steps):
         if flush is not None:
             flush.zero_()
