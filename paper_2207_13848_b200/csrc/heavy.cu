@@ -80,7 +80,7 @@ constexpr int64_t kSmallTaskProducts = 2048;
 #endif
 constexpr int kRunU = SPNNZ_RUN_U;
 #ifndef SPNNZ_SORT_U
-#define SPNNZ_SORT_U 4
+#define SPNNZ_SORT_U 8
 #endif
 constexpr int kSortU = SPNNZ_SORT_U;  // keys in flight per lane in the unit sort  // keys in flight per lane, R == 1 tasks (products straight from B)  // ranges this small go to k_heavy_run_small
 

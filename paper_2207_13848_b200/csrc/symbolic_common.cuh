@@ -67,7 +67,10 @@ __device__ __forceinline__ ItemRow item_row(const SymArgs& g, int32_t s) {
 // so the loads -- and whatever
 // memory operations fn issues per key -- overlap instead of forming one
 // dependent chain per product.
-constexpr int kUnroll = 4;
+#ifndef SPNNZ_UNROLL
+#define SPNNZ_UNROLL 4
+#endif
+constexpr int kUnroll = SPNNZ_UNROLL;  // A/B: 8 -> config 5 step see DESIGN
 #ifndef SPNNZ_CHUNK_FAST
 #define SPNNZ_CHUNK_FAST 1
 #endif
