@@ -74,7 +74,10 @@ constexpr bool kTestFirst = SPNNZ_BITMAP_TEST != 0;
 #ifndef SPNNZ_SORT_MATCH
 #define SPNNZ_SORT_MATCH 1
 #endif
-constexpr int64_t kSmallTaskProducts = 2048;
+#ifndef SPNNZ_SMALL_TASK
+#define SPNNZ_SMALL_TASK 2048
+#endif
+constexpr int64_t kSmallTaskProducts = SPNNZ_SMALL_TASK;  // (A/B: 1024 / 512, see DESIGN)
 #ifndef SPNNZ_RUN_U
 #define SPNNZ_RUN_U 8
 #endif
