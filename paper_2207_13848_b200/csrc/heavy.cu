@@ -1045,7 +1045,14 @@ __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, Sym
 // 512-thread block is four independent 128-thread groups, each with a
 // 4096-slot shared hash and its own named barrier, so an SM keeps twelve
 // small tasks in flight instead of three bitmap tasks.
-constexpr int kSG = 128, kSGroups = 4, kSSlots = 4096;
+#ifndef SPNNZ_SMALL_GROUPS
+#define SPNNZ_SMALL_GROUPS 4
+#endif
+#ifndef SPNNZ_SMALL_SLOTS
+#define SPNNZ_SMALL_SLOTS 4096
+#endif
+constexpr int kSG = 128, kSGroups = SPNNZ_SMALL_GROUPS, kSSlots = SPNNZ_SMALL_SLOTS;
+static_assert(kSSlots >= 2 * kSmallTaskProducts, "small-range table load <= 1/2");
 constexpr int kSmallGrab = 2;  // small tasks per ticket
 
 __device__ __forceinline__ void group_sync(int grp) {
