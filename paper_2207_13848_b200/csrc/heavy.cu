@@ -107,6 +107,28 @@ __device__ __forceinline__ int bit_set_new(uint32_t set_s, uint32_t off) {  // 1
                  : "=r"(old) : "r"(set_s + ((off >> 3) & ~3u)), "r"(1u << (off & 31)) : "memory");
     return static_cast<int>(~(old >> (off & 31)) & 1u);
 }
+// Swizzled bit positions for the one-span bitmaps (R == 1, spans of >= 2^10
+// bits): a warp's 32 keys are consecutive products of sorted B rows -- close
+// columns -- and in the plain layout they pile onto a few words of a few
+// banks (config 2: 13.9 M of the run kernel's 17.8 M shared wavefronts were
+// bank conflicts).  Column offset o = low5 | mid5 << 5 | high << 10 goes to
+// word low5 | high << 5 (its bank is the column's low five bits), bit mid5: a
+// bijection of the span, so counts and merge slots are unchanged.
+template <bool SWZ>
+__device__ __forceinline__ void bit_set_l(uint32_t set_s, uint32_t off) {
+    if (!SWZ) return bit_set(set_s, off);
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(set_s + (((off & 31u) | ((off >> 10) << 5)) << 2)),
+                 "r"(1u << ((off >> 5) & 31u)) : "memory");
+}
+template <bool SWZ>
+__device__ __forceinline__ int bit_set_new_l(uint32_t set_s, uint32_t off) {
+    if (!SWZ) return bit_set_new(set_s, off);
+    uint32_t old;
+    asm volatile("atom.shared.or.b32 %0, [%1], %2;"
+                 : "=r"(old) : "r"(set_s + (((off & 31u) | ((off >> 10) << 5)) << 2)), "r"(1u << ((off >> 5) & 31u))
+                 : "memory");
+    return static_cast<int>(~(old >> ((off >> 5) & 31u)) & 1u);
+}
 __device__ __forceinline__ int32_t opaque_reg(int32_t v) {
     asm volatile("" : "+r"(v));
     return v;
@@ -805,9 +827,10 @@ __global__ void __launch_bounds__(kSlotBlock) k_heavy_slot_count(SymArgs g, SymS
 // task's contiguous bucket span (unit-sorted buckets: k_heavy_run_units).
 constexpr int kRunItem = 0, kRunBuckets = 1;
 
-template <int kRunBlock, int MODE>
+template <int kRunBlock, int MODE, bool SWZ = false>
 __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch sc, int64_t first,
                                                          int R, int wshift, int32_t slot_words) {
+    static_assert(!SWZ || MODE == kRunItem, "swizzled bitmaps: the one-span (R == 1) tasks");
     extern __shared__ int4 s_dyn[];
     uint32_t* s_set = reinterpret_cast<uint32_t*>(s_dyn);
     __shared__ int s_off[kRunBlock + 1];
@@ -818,6 +841,7 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
     const int32_t* list = heavy_list(sc, first);
     const int lane = threadIdx.x & 31;
     const int32_t max_words = R > 1 ? (1 << (kTaskSpanShift - 5))
+                              : SWZ ? slot_words  // every word of the 2^wshift-bit span
                                     : static_cast<int32_t>((int64_t(g.bcols) + 31) / 32);
     for (int k = threadIdx.x; k < max_words; k += kRunBlock) s_set[k] = 0u;
     const uint32_t set_s = shared_window_reg(s_set);
@@ -849,7 +873,7 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
                     if (valid[u]) {
                         const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
                     SPNNZ_ASSERT((off >> 5) < static_cast<uint32_t>(words));
-                        if (!kTestFirst || !(s_set[off >> 5] & (1u << (off & 31)))) bit_set(set_s, off);
+                        if (SWZ || !kTestFirst || !(s_set[off >> 5] & (1u << (off & 31)))) bit_set_l<SWZ>(set_s, off);
                     }
                 return;
             }
@@ -858,7 +882,7 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
                 if (valid[u]) {
                     const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
                     SPNNZ_ASSERT((off >> 5) < static_cast<uint32_t>(words));
-                    if (!kTestFirst || !(s_set[off >> 5] & (1u << (off & 31)))) cnt += bit_set_new(set_s, off);
+                    if (SWZ || !kTestFirst || !(s_set[off >> 5] & (1u << (off & 31)))) cnt += bit_set_new_l<SWZ>(set_s, off);
                 }
         };
         // the span's keys: 16-byte vectors over the aligned body, two vectors
@@ -1483,6 +1507,8 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
     if (!(attr_done.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
         cudaFuncSetAttribute(k_heavy_run<1024, kRunItem>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (1 << kSpanShift) / 8);
+        cudaFuncSetAttribute(k_heavy_run<1024, kRunItem, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (1 << kSpanShift) / 8);
         cudaFuncSetAttribute(k_heavy_run<512, kRunBuckets>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (1 << kTaskSpanShift) / 8);
         cudaFuncSetAttribute(k_heavy_run_units<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1553,8 +1579,18 @@ cudaError_t launch_sym_heavy(const SymArgs& args, const SymScratch& s, bool sort
     } else {
         k_heavy_tasks_r1<<<static_cast<unsigned>((count + 127) / 128), 128, 0, stream>>>(
             s, count, s.heavy_task_cap);
-        k_heavy_run<1024, kRunItem><<<sms, 1024, (1 << kSpanShift) / 8, stream>>>(
-            args, s, first, R, geo.wshift, geo.wwords);
+        // swizzled bitmap layout (bank = the column's low five bits) for spans
+        // of >= 2^10 bits; A/B knob SPNNZ_BITMAP_SWZ=0
+        static const bool swz_on = [] {
+            const char* e = getenv("SPNNZ_BITMAP_SWZ");
+            return !(e && atoi(e) == 0);
+        }();
+        if (swz_on && geo.wshift >= 10)
+            k_heavy_run<1024, kRunItem, true><<<sms, 1024, (1 << kSpanShift) / 8, stream>>>(
+                args, s, first, R, geo.wshift, geo.wwords);
+        else
+            k_heavy_run<1024, kRunItem><<<sms, 1024, (1 << kSpanShift) / 8, stream>>>(
+                args, s, first, R, geo.wshift, geo.wwords);
         n += 2;
     }
     k_heavy_slot_count<<<sms * 4, kSlotBlock, 0, stream>>>(args, s, first, int64_t(geo.wwords));
