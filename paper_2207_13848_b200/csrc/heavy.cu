@@ -957,6 +957,10 @@ __global__ void __launch_bounds__(kRunBlock) k_heavy_run(SymArgs g, SymScratch s
 // entries of the block's next task are already in flight, so a task costs
 // one global round trip less.  Tasks with more than kRunBlock units stage
 // their slices in rounds (no prefetch).
+#ifndef SPNNZ_UNITS_SWZ
+#define SPNNZ_UNITS_SWZ 0
+#endif
+constexpr bool kUnitsSwz = SPNNZ_UNITS_SWZ != 0;  // A/B: the swizzled layout for the unit-sorted bitmap tasks
 template <int kRunBlock>
 __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, SymScratch sc, int64_t first,
                                                                int R, int wshift, int32_t slot_words) {
@@ -1015,7 +1019,7 @@ __global__ void __launch_bounds__(kRunBlock, 3) k_heavy_run_units(SymArgs g, Sym
                 if (valid[u]) {
                     const uint32_t off = static_cast<uint32_t>(keys[u] - col_base);
                     SPNNZ_ASSERT((off >> 5) < static_cast<uint32_t>(words));
-                    if (!kTestFirst || !(s_set[off >> 5] & (1u << (off & 31)))) cnt += bit_set_new(set_s, off);
+                    if (kUnitsSwz || !kTestFirst || !(s_set[off >> 5] & (1u << (off & 31)))) cnt += bit_set_new_l<kUnitsSwz>(set_s, off);
                 }
         };
         for (long long u0 = t.a; u0 < t.b; u0 += kRunBlock) {
